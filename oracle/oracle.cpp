@@ -1,0 +1,683 @@
+/*
+ * oracle/oracle.cpp -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation (C++17, IEEE double)
+ * of the HELIOS++ virtual-laser-scanning hot path (arXiv 2101.09154):
+ * subray fan-out -> nearest hit (brute force over every triangle) ->
+ * transmissive-voxel segments -> radiometry -> full-waveform sum -> peaks.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_2101_09154_b200/) never does, and this file shares no code, header,
+ * table or constant generator with it.
+ *
+ * Citations: "P:n" = PAPER.md line n (section / equation named in prose);
+ * "R<k>" = the reading with that id in DESIGN.md section 3 (the ambiguity
+ * register).  Every function follows the paper's order and notation; where
+ * the paper defines a result plainly (a nearest hit, a sum, a local maximum)
+ * the function is that definition written out (minimum over ALL triangles,
+ * direct sums, a predicate applied to every bin).
+ *
+ * Parity pins: every exported function is pinned by a -m "not gpu" test in
+ * tests/test_oracle_*.py against closed forms, printed values, brute force or
+ * an independent library (curand's host Philox generator); see DESIGN.md s.4.
+ */
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <vector>
+
+namespace {
+
+const double kPi = 3.14159265358979323846;
+const double kC = 299792458.0;  // speed of light, m/s (Sec. 3.4)
+const double kInf = std::numeric_limits<double>::infinity();
+const double kNaN = std::numeric_limits<double>::quiet_NaN();
+
+struct V3 {
+  double x, y, z;
+};
+V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+V3 scale(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+V3 cross(V3 a, V3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+double norm(V3 a) { return std::sqrt(dot(a, a)); }
+
+}  // namespace
+
+extern "C" {
+
+/* ------------------------------------------------------------------------
+ * Subray pattern (Fig. 6 caption P:204; readings R1, R2, R4).
+ * ring i = 1..q carries floor(2*pi*i) subrays; a central subray is
+ * always added.  R1: counts reachable by that rule select it; the hexagonal
+ * counts 1 + 3q(q+1) select n_i = 6i.  Returns q (>= 0), or -1 if the count
+ * is reachable by neither rule.  *rule = 0 paper rule, 1 hexagonal.
+ * ---------------------------------------------------------------------- */
+int oracle_resolve_subrays(uint32_t count, int* rule) {
+  for (int q = 0; q <= 64; ++q) {
+    uint64_t n = 1;
+    for (int i = 1; i <= q; ++i) n += (uint64_t)std::floor(2.0 * kPi * i);
+    if (n == count) {
+      if (rule) *rule = 0;
+      return q;
+    }
+  }
+  for (int q = 0; q <= 64; ++q) {
+    uint64_t n = 1 + 3ull * q * (q + 1);
+    if (n == count) {
+      if (rule) *rule = 1;
+      return q;
+    }
+  }
+  return -1;
+}
+
+/* Ring size n_i under the given rule (P:199 / R1). */
+static int ring_size(int rule, int i) {
+  if (rule == 0) return (int)std::floor(2.0 * kPi * i);
+  return 6 * i;
+}
+
+/* Per-subray ring index i(s), slot j(s), ring size n_i and angles
+ * theta_i = (i/q) * beta (R2), phi = 2*pi*j/n_i (R4).  Order: centre, then
+ * rings outward, slots by j (R4).  Returns 0, or -1 on a bad count. */
+int oracle_subray_pattern(uint32_t count, double beta, int* ring, int* slot,
+                          int* ring_n, double* theta, double* phi) {
+  int rule = 0;
+  int q = oracle_resolve_subrays(count, &rule);
+  if (q < 0) return -1;
+  uint32_t s = 0;
+  ring[s] = 0;
+  slot[s] = 0;
+  ring_n[s] = 1;
+  theta[s] = 0.0;
+  phi[s] = 0.0;
+  ++s;
+  for (int i = 1; i <= q; ++i) {
+    int n = ring_size(rule, i);
+    for (int j = 0; j < n; ++j) {
+      ring[s] = i;
+      slot[s] = j;
+      ring_n[s] = n;
+      theta[s] = ((double)i / (double)q) * beta;
+      phi[s] = 2.0 * kPi * (double)j / (double)n;
+      ++s;
+    }
+  }
+  return 0;
+}
+
+/* Subray direction ("sampled in a regular pattern around the central
+ * ray"; R4 frame): d = pulse direction normalised; a = z unless |d_z| > 0.9,
+ * then x; u = normalize(a x d); v = d x u;
+ * d_s = cos(theta) d + sin(theta) (cos(phi) u + sin(phi) v). */
+void oracle_subray_direction(const double d_in[3], double theta, double phi,
+                             double out[3]) {
+  V3 d = {d_in[0], d_in[1], d_in[2]};
+  d = scale(d, 1.0 / norm(d));
+  V3 a = std::fabs(d.z) > 0.9 ? V3{1.0, 0.0, 0.0} : V3{0.0, 0.0, 1.0};
+  V3 u = cross(a, d);
+  u = scale(u, 1.0 / norm(u));
+  V3 v = cross(d, u);
+  V3 ring = add(scale(u, std::cos(phi)), scale(v, std::sin(phi)));
+  V3 ds = add(scale(d, std::cos(theta)), scale(ring, std::sin(theta)));
+  out[0] = ds.x;
+  out[1] = ds.y;
+  out[2] = ds.z;
+}
+
+/* ------------------------------------------------------------------------
+ * Eq. 1: I = I0 exp(-2 r^2 / w^2).
+ * Eq. 2: w = w0 sqrt(omega0^2 + omega^2), omega = lambda R/(pi w0^2),
+ *                omega0 = lambda R0/(pi w0^2).  lambda given in nm.
+ * ---------------------------------------------------------------------- */
+double oracle_eq1_intensity(double I0, double r, double w) {
+  return I0 * std::exp(-2.0 * r * r / (w * w));
+}
+
+double oracle_eq2_beam_width(double w0, double lambda_nm, double R, double R0) {
+  double lambda = lambda_nm * 1e-9;
+  double omega = lambda * R / (kPi * w0 * w0);
+  double omega0 = lambda * R0 / (kPi * w0 * w0);
+  return w0 * std::sqrt(omega0 * omega0 + omega * omega);
+}
+
+/* Subray base intensity I_s at hit range R (R5): r = R sin(theta_i); w from
+ * Eq. 2 when w0 > 0, else the far-field specialisation w = R tan(beta). */
+double oracle_subray_intensity(double I0, double theta, double beta, double R,
+                               double w0, double lambda_nm, double R0) {
+  double r = R * std::sin(theta);
+  double w = (w0 > 0.0) ? oracle_eq2_beam_width(w0, lambda_nm, R, R0)
+                        : R * std::tan(beta);
+  if (r == 0.0) return I0;  // beam centre (Eq. 1 with r = 0)
+  return oracle_eq1_intensity(I0, r, w);
+}
+
+/* Eq. 3: P(t) = I (t/tau)^2 exp(-t/tau), tau = pulse length / 1.75
+ * (P:208). */
+double oracle_eq3_pulse(double I, double t, double tau) {
+  double x = t / tau;
+  return I * x * x * std::exp(-x);
+}
+
+/* Eq. 7: I = lambda sigma P alpha^2 / (4 pi d^4 beta^2) (R14, R16). */
+double oracle_eq7_intensity(double lambda_eff, double sigma, double P,
+                            double alpha, double d, double beta) {
+  return lambda_eff * sigma * P * alpha * alpha /
+         (4.0 * kPi * d * d * d * d * beta * beta);
+}
+
+/* ------------------------------------------------------------------------
+ * Ray-triangle intersection (triangles have only t0; R21: t > 0,
+ * two-sided).  Moller-Trumbore in double on the fp32 vertices promoted to
+ * double.  Inclusive edges; |det| <= 1e-12 |e1||e2| is a miss (parallel ray
+ * or degenerate triangle).  Returns t, or -1 on a miss; *cos_inc receives
+ * |n . d| / |d| (incidence folded to [0, pi/2]).
+ * ---------------------------------------------------------------------- */
+double oracle_ray_triangle(const double o_in[3], const double d_in[3],
+                           const float* tri9, double* cos_inc) {
+  V3 o = {o_in[0], o_in[1], o_in[2]};
+  V3 d = {d_in[0], d_in[1], d_in[2]};
+  V3 v0 = {tri9[0], tri9[1], tri9[2]};
+  V3 v1 = {tri9[3], tri9[4], tri9[5]};
+  V3 v2 = {tri9[6], tri9[7], tri9[8]};
+  V3 e1 = sub(v1, v0);
+  V3 e2 = sub(v2, v0);
+  V3 p = cross(d, e2);
+  double det = dot(e1, p);
+  if (std::fabs(det) <= 1e-12 * norm(e1) * norm(e2)) return -1.0;
+  double inv = 1.0 / det;
+  V3 s = sub(o, v0);
+  double u = dot(s, p) * inv;
+  if (u < 0.0 || u > 1.0) return -1.0;
+  V3 q = cross(s, e1);
+  double v = dot(d, q) * inv;
+  if (v < 0.0 || u + v > 1.0) return -1.0;
+  double t = dot(e2, q) * inv;
+  if (!(t > 0.0)) return -1.0;
+  if (cos_inc) {
+    V3 n = cross(e1, e2);
+    *cos_inc = std::fabs(dot(n, d)) / (norm(n) * norm(d));
+  }
+  return t;
+}
+
+/* Nearest hit by brute force over EVERY triangle ("minimum distance
+ * intersection"; R22 ties -> lower id).  Returns the id or -1 (miss).
+ * *t_out, *cos_out, *n_cand (#triangles with t <= t_min + 1e-6 m) and *gap
+ * (t_second - t_min over distinct triangles, +inf if none). */
+int64_t oracle_nearest_triangle(const double o[3], const double d[3],
+                                const float* tris, uint32_t n_tris,
+                                double* t_out, double* cos_out,
+                                int32_t* n_cand, double* gap) {
+  double best = kInf, best_cos = 0.0;
+  int64_t best_id = -1;
+  std::vector<double> hits;  // t of every triangle the ray hits
+  for (uint32_t i = 0; i < n_tris; ++i) {
+    double c = 0.0;
+    double t = oracle_ray_triangle(o, d, tris + 9ull * i, &c);
+    if (t < 0.0) continue;
+    hits.push_back(t);
+    if (t < best) {  // strict: the lower id wins an exact tie (R22)
+      best = t;
+      best_id = i;
+      best_cos = c;
+    }
+  }
+  int32_t cand = 0;
+  double second = kInf;
+  bool skipped_best = false;
+  for (double t : hits) {
+    if (t <= best + 1e-6) ++cand;
+    if (t == best && !skipped_best) {
+      skipped_best = true;
+      continue;
+    }
+    second = std::min(second, t);
+  }
+  if (t_out) *t_out = best_id >= 0 ? best : kInf;
+  if (cos_out) *cos_out = best_cos;
+  if (n_cand) *n_cand = cand;
+  if (gap) *gap = second - best;
+  return best_id;
+}
+
+/* ------------------------------------------------------------------------
+ * Philox4x32-10 (Salmon et al., SC'11), written from its published
+ * definition (DESIGN.md s.3 R18/R19): rounds (c0..c3) ->
+ * (hi(M1 c2) ^ c1 ^ k0, lo(M1 c2), hi(M0 c0) ^ c3 ^ k1, lo(M0 c0)),
+ * key bump k0 += 0x9E3779B9, k1 += 0xBB67AE85 between rounds, 10 rounds.
+ * ---------------------------------------------------------------------- */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2],
+                          uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0;
+    c1 = n1;
+    c2 = n2;
+    c3 = n3;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+/* Uniform draw R in [0,1) for a transmission decision (R18,
+ * R19): key = (seed_lo, seed_hi), ctr = (pulse_lo, pulse_hi, subray, voxel),
+ * u = (x0 >> 8) * 2^-24. */
+double oracle_transmission_u(uint64_t seed, uint64_t pulse, uint32_t subray,
+                             uint32_t voxel) {
+  uint32_t ctr[4] = {(uint32_t)pulse, (uint32_t)(pulse >> 32), subray, voxel};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t x[4];
+  oracle_philox4x32_10(ctr, key, x);
+  return (double)(x[0] >> 8) * (1.0 / 16777216.0);
+}
+
+/* G(|d_z|) for sigma = PAD * G (R15): LUT over |d_z| in [0,1] at uniform
+ * knots, linear interpolation; no LUT -> spherical LAD, G = 0.5. */
+double oracle_g_function(const float* lut, uint32_t n_lut, double abs_dz) {
+  if (!lut || n_lut == 0) return 0.5;
+  double x = abs_dz * (double)(n_lut - 1);
+  int64_t k = (int64_t)std::floor(x);
+  if (k < 0) k = 0;
+  if (k > (int64_t)n_lut - 2) k = (int64_t)n_lut - 2;
+  double f = x - (double)k;
+  return (double)lut[k] * (1.0 - f) + (double)lut[k + 1] * f;
+}
+
+/* ------------------------------------------------------------------------
+ * Voxel segments along a ray (P:366 re-entrant rays with eps -> 0, R20).
+ * Independent of any incremental DDA: clip the ray to the grid box and to
+ * (0, t_max]; enumerate EVERY x-, y- and z-plane crossing parameter inside
+ * that interval directly, sort them, and assign each sub-interval to the
+ * voxel containing its midpoint; merge runs of the same voxel and drop
+ * zero-length pieces.  Writes up to max_seg (t_a, t_b, voxel id) triples in
+ * ray order and returns the count (or -(count) if truncated).
+ * ---------------------------------------------------------------------- */
+int64_t oracle_voxel_segments(const double o_in[3], const double d_in[3],
+                              const uint32_t n[3], const double origin[3],
+                              double vs, double t_max, double* ta, double* tb,
+                              uint32_t* vid, int64_t max_seg) {
+  double o[3] = {o_in[0], o_in[1], o_in[2]};
+  double d[3] = {d_in[0], d_in[1], d_in[2]};
+  // Slab clip against the grid box.
+  double t_in = 0.0, t_out = t_max;
+  for (int a = 0; a < 3; ++a) {
+    double lo = origin[a];
+    double hi = origin[a] + (double)n[a] * vs;
+    if (d[a] == 0.0) {
+      if (o[a] < lo || o[a] > hi) return 0;
+      continue;
+    }
+    double t0 = (lo - o[a]) / d[a];
+    double t1 = (hi - o[a]) / d[a];
+    if (t0 > t1) std::swap(t0, t1);
+    t_in = std::max(t_in, t0);
+    t_out = std::min(t_out, t1);
+  }
+  if (!(t_in < t_out)) return 0;
+  // Every plane crossing strictly inside (t_in, t_out).
+  std::vector<double> ts;
+  ts.push_back(t_in);
+  for (int a = 0; a < 3; ++a) {
+    if (d[a] == 0.0) continue;
+    for (uint32_t k = 0; k <= n[a]; ++k) {
+      double plane = origin[a] + (double)k * vs;
+      double t = (plane - o[a]) / d[a];
+      if (t > t_in && t < t_out) ts.push_back(t);
+    }
+  }
+  ts.push_back(t_out);
+  std::sort(ts.begin(), ts.end());
+  int64_t cnt = 0;
+  bool trunc = false;
+  for (size_t i = 0; i + 1 < ts.size(); ++i) {
+    double a = ts[i], b = ts[i + 1];
+    if (!(b > a)) continue;  // zero-length piece
+    double m = 0.5 * (a + b);
+    int64_t idx[3];
+    for (int ax = 0; ax < 3; ++ax) {
+      double c = (o[ax] + m * d[ax] - origin[ax]) / vs;
+      int64_t k = (int64_t)std::floor(c);
+      if (k < 0) k = 0;
+      if (k >= (int64_t)n[ax]) k = (int64_t)n[ax] - 1;
+      idx[ax] = k;
+    }
+    uint32_t id = (uint32_t)(idx[0] + (int64_t)n[0] * (idx[1] + (int64_t)n[1] * idx[2]));
+    if (cnt > 0 && vid[cnt - 1] == id && tb[cnt - 1] == a) {
+      tb[cnt - 1] = b;  // same voxel continues
+      continue;
+    }
+    if (cnt >= max_seg) {
+      trunc = true;
+      break;
+    }
+    ta[cnt] = a;
+    tb[cnt] = b;
+    vid[cnt] = id;
+    ++cnt;
+  }
+  return trunc ? -cnt : cnt;
+}
+
+/* ------------------------------------------------------------------------
+ * Simulation parameters (mirrors DESIGN.md s.2; plain doubles).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  double divergence_rad;        // beta (R3)
+  double pulse_length_ns;       // tau = pulse_length / 1.75
+  double bin_width_ns;          // Delta
+  double max_fullwave_range_ns; // window
+  double detection_threshold;   // thr (R11)
+  double peak_power_w;          // I0 (Eq. 1)
+  double efficiency;            // lambda of Eq. 7
+  double receiver_diameter_m;   // alpha of Eq. 7 (R14)
+  double wavelength_nm;         // lambda of Eq. 2
+  double beam_waist_m;          // w0 of Eq. 2 (0 -> far field, R5)
+  double focus_range_m;         // R0 of Eq. 2
+  uint64_t seed;                // Philox key (R19)
+  uint32_t subray_count;        // (R1)
+  uint32_t max_returns;         // (R11)
+} oracle_params;
+
+typedef struct {
+  const float* tris;     // [n_tris][9]
+  const float* refl;     // [n_tris] or NULL -> 0.5
+  uint32_t n_tris;
+  const float* pad;      // [nz][ny][nx] or NULL
+  uint32_t n[3];         // nx, ny, nz
+  double origin[3];
+  double voxel_size;
+  const float* g_lut;
+  uint32_t n_lut;
+} oracle_scene;
+
+typedef struct {
+  // per pulse
+  int32_t* n_returns;    // [n]
+  int64_t* k0;           // [n]
+  double* waveform;      // [n][n_bins] or NULL
+  double* ret_range;     // [n][max_returns]
+  double* ret_time;
+  double* ret_intensity;
+  uint32_t* ret_prim;
+  int32_t* ret_number;
+  double* peak_margin;   // [n] min relative margin of every peak decision
+  double* attr_margin;   // [n] min relative gap between the top two contributions
+  // per subray, [n][N]
+  double* sub_range;     // NaN on miss
+  double* sub_amp;
+  uint32_t* sub_prim;    // UINT32_MAX on miss
+  int64_t* sub_k;        // -1 on miss
+  int32_t* sub_ncand;
+  double* sub_gap;
+  double* sub_kmargin;   // |2R/(c Delta) - round(.)|
+  double* sub_umargin;   // min |u - exp(-sigma L)| over this subray's decisions
+} oracle_outputs;
+
+uint32_t oracle_waveform_bins(double window_ns, double bin_ns) {
+  if (!(bin_ns > 0.0) || !(window_ns >= bin_ns)) return 0;
+  return (uint32_t)std::ceil(window_ns / bin_ns);  // R9
+}
+
+/* One pulse: steps O1..O8 of DESIGN.md s.3 (the paper's order). */
+static void simulate_pulse(const oracle_scene* sc, const oracle_params* pr,
+                           const float* origin, const float* direction,
+                           double time_s, uint64_t pulse_id, int64_t i,
+                           const double* theta,
+                           const double* phi, const oracle_outputs* out) {
+  const uint32_t N = pr->subray_count;
+  const double beta = pr->divergence_rad;
+  const double delta = pr->bin_width_ns;
+  const double tau = pr->pulse_length_ns / 1.75;
+  const uint32_t n_bins = oracle_waveform_bins(pr->max_fullwave_range_ns, delta);
+  const int64_t Lp = (int64_t)std::ceil(20.0 * tau / delta);           // R9
+  const uint32_t maxr = pr->max_returns;
+  const double K = pr->efficiency * pr->receiver_diameter_m *
+                   pr->receiver_diameter_m / (4.0 * kPi * beta * beta);  // Eq. 7
+
+  double o[3] = {origin[0], origin[1], origin[2]};
+  double d[3] = {direction[0], direction[1], direction[2]};
+  double dn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+
+  // Per-subray results.
+  std::vector<double> R(N, kNaN), A(N, 0.0);
+  std::vector<uint32_t> prim(N, 0xFFFFFFFFu);
+  std::vector<int64_t> ks(N, -1);
+  std::vector<int32_t> ncand(N, 0);
+  std::vector<double> gapv(N, kInf), kmarg(N, kInf), umarg(N, kInf);
+
+  if (dn > 0.0) {
+    for (uint32_t s = 0; s < N; ++s) {
+      // O1: subray direction.
+      double ds[3];
+      oracle_subray_direction(d, theta[s], phi[s], ds);
+      // O2: nearest triangle, brute force.
+      double t_tri = kInf, cos_inc = 0.0, gap = kInf;
+      int32_t nc = 0;
+      int64_t tid = oracle_nearest_triangle(o, ds, sc->tris, sc->n_tris, &t_tri,
+                                            &cos_inc, &nc, &gap);
+      // O3: transmissive voxels before the triangle.
+      bool vox_hit = false;
+      double t_vox = 0.0, sigma_vox = 0.0;
+      uint32_t vox_id = 0;
+      double um = kInf;
+      if (sc->pad) {
+        double tmax = tid >= 0 ? t_tri : kInf;
+        int64_t cap = (int64_t)sc->n[0] + sc->n[1] + sc->n[2] + 2;
+        std::vector<double> ta(cap), tb(cap);
+        std::vector<uint32_t> vid(cap);
+        int64_t ns = oracle_voxel_segments(o, ds, sc->n, sc->origin, sc->voxel_size,
+                                           tmax, ta.data(), tb.data(), vid.data(), cap);
+        if (ns < 0) ns = -ns;
+        double G = oracle_g_function(sc->g_lut, sc->n_lut, std::fabs(ds[2]));
+        for (int64_t k = 0; k < ns; ++k) {
+          double PAD = sc->pad[vid[k]];
+          if (!(PAD > 0.0)) continue;  // sigma = 0 lets the ray continue
+          double sigma = PAD * G;        // Eq. 4 via the G-LUT (R15)
+          double L = tb[k] - ta[k];
+          double u = oracle_transmission_u(pr->seed, pulse_id, s, vid[k]);
+          double pass_p = std::exp(-sigma * L);
+          um = std::min(um, std::fabs(u - pass_p));
+          if (u < pass_p) continue;      // s = -ln(u)/sigma > L: transmit (R17)
+          vox_hit = true;                 // Eq. 6: echo at distance s into the voxel
+          t_vox = ta[k] + (-std::log(u)) / sigma;
+          sigma_vox = sigma;
+          vox_id = vid[k];
+          break;
+        }
+      }
+      // O4/O5: event, range, radiometry.
+      double Rs = kNaN, sig_eff = 0.0;
+      uint32_t pid = 0xFFFFFFFFu;
+      if (vox_hit) {
+        Rs = t_vox;
+        sig_eff = sigma_vox;                            // R16
+        pid = sc->n_tris + vox_id;
+      } else if (tid >= 0) {
+        Rs = t_tri;
+        double rho = sc->refl ? (double)sc->refl[tid] : 0.5;
+        sig_eff = rho * cos_inc;                        // R14 (Lambertian)
+        pid = (uint32_t)tid;
+      }
+      if (pid != 0xFFFFFFFFu) {
+        double Is = oracle_subray_intensity(pr->peak_power_w, theta[s], beta, Rs,
+                                            pr->beam_waist_m, pr->wavelength_nm,
+                                            pr->focus_range_m);      // Eq. 1, 2
+        A[s] = K * sig_eff * Is / (Rs * Rs * Rs * Rs);                 // Eq. 7
+        R[s] = Rs;
+        prim[s] = pid;
+        double x = 2.0 * Rs / kC / (delta * 1e-9);  // two-way time in bins (R8, R9)
+        ks[s] = (int64_t)std::floor(x);
+        kmarg[s] = std::fabs(x - std::nearbyint(x));
+        ncand[s] = vox_hit ? 1 : nc;
+        gapv[s] = vox_hit ? kInf : gap;
+      }
+      umarg[s] = um;
+    }
+  }
+
+  // O6: full waveform (Eq. 3).
+  int64_t k0 = -1;
+  for (uint32_t s = 0; s < N; ++s)
+    if (ks[s] >= 0 && (k0 < 0 || ks[s] < k0)) k0 = ks[s];
+  std::vector<double> W(n_bins, 0.0);
+  if (k0 >= 0) {
+    for (uint32_t s = 0; s < N; ++s) {
+      if (ks[s] < 0) continue;
+      int64_t off = ks[s] - k0;
+      if (off >= (int64_t)n_bins) continue;  // beyond maxFullwaveRange: discarded
+      for (int64_t j = 0; j < Lp; ++j) {
+        int64_t k = off + j;
+        if (k >= (int64_t)n_bins) break;
+        double t = ((double)j + 0.5) * delta;  // bin-centre sampling (R9)
+        W[k] += oracle_eq3_pulse(A[s], t, tau);
+      }
+    }
+  }
+  // j* = argmax of the binned outgoing pulse (R12).
+  int64_t jstar = 0;
+  {
+    double best = -1.0;
+    for (int64_t j = 0; j < Lp; ++j) {
+      double p = oracle_eq3_pulse(1.0, ((double)j + 0.5) * delta, tau);
+      if (p > best) {
+        best = p;
+        jstar = j;
+      }
+    }
+  }
+
+  // O7: local-maximum peaks (R11-R13).
+  double M = 0.0;
+  for (uint32_t k = 0; k < n_bins; ++k) M = std::max(M, W[k]);
+  double thr = pr->detection_threshold * M;
+  int32_t nret = 0;
+  double pmarg = kInf, amarg = kInf;
+  for (int64_t k = 1; k + 1 < (int64_t)n_bins; ++k) {
+    // decision margins of the comparisons that involve a non-zero bin
+    double a = W[k], l = W[k - 1], r = W[k + 1];
+    if (std::max(a, l) > 0.0) pmarg = std::min(pmarg, std::fabs(a - l) / std::max(a, l));
+    if (std::max(a, r) > 0.0) pmarg = std::min(pmarg, std::fabs(a - r) / std::max(a, r));
+    if (a > 0.0 && M > 0.0) pmarg = std::min(pmarg, std::fabs(a - thr) / M);
+    bool peak = a > l && a > r && a >= thr;
+    if (!peak) continue;
+    if ((uint32_t)nret >= maxr) continue;  // keep the earliest max_returns
+    // Attribution (R13): subray with the largest contribution to bin k.
+    double c1 = -1.0, c2 = -1.0;
+    uint32_t who = 0xFFFFFFFFu;
+    for (uint32_t s = 0; s < N; ++s) {
+      if (ks[s] < 0) continue;
+      int64_t off = ks[s] - k0;
+      if (off >= (int64_t)n_bins) continue;
+      int64_t j = k - off;
+      if (j < 0 || j >= Lp) continue;
+      double c = oracle_eq3_pulse(A[s], ((double)j + 0.5) * delta, tau);
+      if (c > c1) {
+        c2 = c1;
+        c1 = c;
+        who = prim[s];
+      } else if (c > c2) {
+        c2 = c;
+      }
+    }
+    if (c1 > 0.0 && c2 >= 0.0) amarg = std::min(amarg, (c1 - c2) / c1);
+    int64_t slot = i * (int64_t)maxr + nret;
+    out->ret_range[slot] =
+        0.5 * kC * ((double)(k0 + k - jstar) + 0.5) * delta * 1e-9;  // R12
+    out->ret_time[slot] = time_s;
+    out->ret_intensity[slot] = a;
+    out->ret_prim[slot] = who;
+    out->ret_number[slot] = nret + 1;
+    ++nret;
+  }
+
+  // O8: emit.
+  out->n_returns[i] = nret;
+  out->k0[i] = k0;
+  if (out->waveform)
+    for (uint32_t k = 0; k < n_bins; ++k) out->waveform[i * (int64_t)n_bins + k] = W[k];
+  out->peak_margin[i] = pmarg;
+  out->attr_margin[i] = amarg;
+  for (uint32_t s = 0; s < N; ++s) {
+    int64_t x = i * (int64_t)N + s;
+    out->sub_range[x] = R[s];
+    out->sub_amp[x] = A[s];
+    out->sub_prim[x] = prim[s];
+    out->sub_k[x] = ks[s];
+    out->sub_ncand[x] = ncand[s];
+    out->sub_gap[x] = gapv[s];
+    out->sub_kmargin[x] = kmarg[s];
+    out->sub_umargin[x] = umarg[s];
+  }
+}
+
+/* Simulate the listed pulses (a seeded subset or all of them).  pulse_ids
+ * are the GLOBAL pulse indices (Philox counter).  Parallel over pulses
+ * with a plain thread pool (P:289's pulse-level multithreading); nothing is
+ * shared or reduced across threads, so the result is thread-count
+ * independent.  Returns 0, or -1 on invalid parameters. */
+int oracle_simulate(const oracle_scene* sc, const oracle_params* pr,
+                    const float* origins, const float* directions,
+                    const double* times, const uint64_t* pulse_ids,
+                    int64_t n_pulses, int n_threads, const oracle_outputs* out) {
+  const uint32_t N = pr->subray_count;
+  std::vector<int> ring(N), slot(N), ring_n(N);
+  std::vector<double> theta(N), phi(N);
+  if (oracle_subray_pattern(N, pr->divergence_rad, ring.data(), slot.data(),
+                            ring_n.data(), theta.data(), phi.data()) != 0)
+    return -1;
+  if (oracle_waveform_bins(pr->max_fullwave_range_ns, pr->bin_width_ns) == 0) return -1;
+  if (pr->max_returns < 1) return -1;
+  for (int64_t i = 0; i < n_pulses; ++i) {
+    out->n_returns[i] = 0;
+    for (uint32_t r = 0; r < pr->max_returns; ++r) {
+      int64_t x = i * pr->max_returns + r;
+      out->ret_range[x] = 0.0;
+      out->ret_time[x] = 0.0;
+      out->ret_intensity[x] = 0.0;
+      out->ret_prim[x] = 0;
+      out->ret_number[x] = 0;
+    }
+  }
+  if (n_threads < 1) n_threads = 1;
+  std::atomic<int64_t> next(0);
+  auto worker = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n_pulses) break;
+      simulate_pulse(sc, pr, origins + 3 * i, directions + 3 * i, times ? times[i] : 0.0,
+                     pulse_ids[i], i, theta.data(), phi.data(), out);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < n_threads; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  return 0;
+}
+
+}  // extern "C"

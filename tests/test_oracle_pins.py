@@ -1,0 +1,490 @@
+"""Pins of the fp64 oracle against things other than itself (-m "not gpu").
+
+Each test names the passage / closed form / independent routine it pins
+(DESIGN.md s.4 lists them).  Expected values come from the paper's printed
+numbers, closed forms of plane geometry, scipy quadrature / root finding,
+brute-force sampling, or curand's host Philox generator -- never from the
+oracle itself and never from the CUDA path.
+"""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+from scipy import integrate, optimize
+
+import oracle
+from workloads import Scene, ScannerParams, window_ns_for_range
+
+C = 299792458.0
+
+
+# ------------------------------------------------------------------ subrays
+def test_subray_counts_printed_in_paper():
+    # Fig. 6 caption: quality 5 -> 93 subrays, quality 9 -> 279.
+    assert oracle.resolve_subrays(93) == (5, 0)
+    assert oracle.resolve_subrays(279) == (9, 0)
+
+
+def test_subray_count_formula_and_hex_rule():
+    # N(q) = 1 + sum_{i<=q} floor(2 pi i); R1 hexagonal 1 + 3q(q+1).
+    paper = [1, 7, 19, 37, 62, 93, 130, 173, 223, 279]
+    for q, n in enumerate(paper):
+        assert oracle.resolve_subrays(n)[0] == q
+    for q, n in [(4, 61), (5, 91), (6, 127), (7, 169), (8, 217), (9, 271)]:
+        assert oracle.resolve_subrays(n) == (q, 1)
+    assert oracle.resolve_subrays(20)[0] == -1
+    with pytest.raises(ValueError):
+        oracle.subray_pattern(20, 1e-3)
+
+
+def test_subray_geometry_invariants():
+    # angle(d_s, d) = theta_i = (i/q) beta (R2); ring azimuth spacing 2 pi / n_i
+    # exactly; |d_s| = 1; slot 0 along u = normalize(a x d) (R4).
+    beta = 0.3e-3
+    rng = np.random.default_rng(1)
+    for count in (19, 37, 91, 93):
+        ring, slot, rn, th, ph = oracle.subray_pattern(count, beta)
+        q = ring.max()
+        assert np.allclose(th, ring / q * beta, rtol=0, atol=1e-18)
+        for _ in range(5):
+            d = rng.normal(size=3)
+            d /= np.linalg.norm(d)
+            a = np.array([1.0, 0, 0]) if abs(d[2]) > 0.9 else np.array([0, 0, 1.0])
+            u = np.cross(a, d)
+            u /= np.linalg.norm(u)
+            dirs = np.array([oracle.subray_direction(d, th[s], ph[s]) for s in range(count)])
+            assert np.allclose(np.linalg.norm(dirs, axis=1), 1.0, atol=1e-14)
+            ang = np.arccos(np.clip(dirs @ d, -1, 1))
+            # arccos near 1 is ill-conditioned; use the perpendicular norm instead
+            perp = dirs - np.outer(dirs @ d, d)
+            assert np.allclose(np.linalg.norm(perp, axis=1), np.sin(th), rtol=1e-9, atol=1e-15)
+            assert np.allclose(ang[0], 0.0, atol=1e-7)
+            for i in range(1, q + 1):
+                sel = np.where(ring == i)[0]
+                p = perp[sel] / np.linalg.norm(perp[sel], axis=1, keepdims=True)
+                # slot 0 along u
+                assert np.allclose(p[0], u, atol=1e-8)
+                # consecutive slots separated by 2 pi / n_i
+                cosang = np.sum(p * np.roll(p, -1, axis=0), axis=1)
+                assert np.allclose(cosang, math.cos(2 * math.pi / len(sel)), atol=1e-9)
+
+
+# ------------------------------------------------------------------ Eq. 1-3, 7
+def test_eq1_closed_forms():
+    assert oracle.eq1_intensity(2.0, 0.0, 0.7) == 2.0
+    assert oracle.eq1_intensity(1.0, 0.7, 0.7) == pytest.approx(math.exp(-2), rel=1e-15)
+    assert oracle.eq1_intensity(1.0, 1.4, 0.7) == pytest.approx(math.exp(-8), rel=1e-15)
+    assert oracle.eq1_intensity(1.0, 0.7, 0.7) == pytest.approx(0.13534, abs=1e-5)
+
+
+def test_eq2_closed_forms():
+    w0, lam, R0 = 0.01, 1550.0, 1000.0
+    om0 = lam * 1e-9 * R0 / (math.pi * w0 * w0)
+    assert oracle.eq2_beam_width(w0, lam, 0.0, R0) == pytest.approx(w0 * om0, rel=1e-14)
+    assert oracle.eq2_beam_width(w0, lam, R0, R0) == pytest.approx(math.sqrt(2) * w0 * om0,
+                                                                   rel=1e-14)
+    # R0 = 0 -> w = lambda R / (pi w0)
+    assert oracle.eq2_beam_width(w0, lam, 500.0, 0.0) == pytest.approx(
+        lam * 1e-9 * 500.0 / (math.pi * w0), rel=1e-14)
+
+
+def test_far_field_subray_weights():
+    # R5: far field -> weights exp(-2 sin^2 th / tan^2 beta) ~ exp(-2 (i/q)^2);
+    # q = 3: 1, 0.800737, 0.411112, 0.135335.
+    beta = 0.3e-3
+    ring, _, _, th, _ = oracle.subray_pattern(37, beta)
+    expect = {0: 1.0, 1: 0.800737, 2: 0.411112, 3: 0.135335}
+    for s in range(37):
+        w = oracle.subray_intensity(1.0, th[s], beta, 123.0)
+        assert w == pytest.approx(expect[int(ring[s])], abs=2e-6)
+
+
+def test_eq3_pulse_shape():
+    tau = 4.0 / 1.75
+    assert tau == pytest.approx(2.285714, abs=1e-6)
+    # peak at t = 2 tau with value 4 e^-2 I
+    res = optimize.minimize_scalar(lambda t: -oracle.eq3_pulse(1.0, t, tau),
+                                   bounds=(0.1, 20), method="bounded",
+                                   options={"xatol": 1e-10})
+    assert res.x == pytest.approx(2 * tau, rel=1e-6)
+    assert oracle.eq3_pulse(3.0, 2 * tau, tau) == pytest.approx(3 * 4 * math.exp(-2), rel=1e-15)
+    # integral = 2 tau I (Gamma(3))
+    val, _ = integrate.quad(lambda t: oracle.eq3_pulse(1.5, t, tau), 0, np.inf)
+    assert val == pytest.approx(2 * tau * 1.5, rel=1e-9)
+    # FWHM = 3.394681 tau (half-maximum roots of x^2 e^-x = 2 e^-2)
+    half = 2 * math.exp(-2)
+    a = optimize.brentq(lambda t: oracle.eq3_pulse(1.0, t, tau) - half, 1e-6, 2 * tau)
+    b = optimize.brentq(lambda t: oracle.eq3_pulse(1.0, t, tau) - half, 2 * tau, 30 * tau)
+    assert (b - a) / tau == pytest.approx(3.394681, abs=2e-6)
+    # SPEC S:300 worked example: 3.5 ns pulse -> tau = 2 ns, peak at 4 ns
+    assert 3.5 / 1.75 == 2.0
+
+
+def test_eq7_example_and_d4_law():
+    # lambda 0.9, sigma 0.1, P 1, alpha^2 4e-4, beta^2 9e-8, d 100 -> 3.183099e-7
+    v = oracle.eq7_intensity(0.9, 0.1, 1.0, 0.02, 100.0, 3e-4)
+    assert v == pytest.approx(0.9 * 0.1 * 4e-4 / (4 * math.pi * 1e8 * 9e-8), rel=1e-12)
+    assert v == pytest.approx(3.183099e-7, rel=1e-6)
+    assert v / oracle.eq7_intensity(0.9, 0.1, 1.0, 0.02, 200.0, 3e-4) == pytest.approx(16.0,
+                                                                                        rel=1e-12)
+    assert oracle.eq7_intensity(0.9, 0.0, 1.0, 0.02, 100.0, 3e-4) == 0.0
+
+
+# ------------------------------------------------------------------ intersection
+def test_ray_triangle_worked_examples():
+    tri = np.array([[-1, -1, 0], [1, -1, 0], [0, 1, 0]], np.float32)
+    t, c = oracle.ray_triangle([0, 0, 1], [0, 0, -1], tri)
+    assert t == 1.0 and c == 1.0
+    assert oracle.ray_triangle([0, 0, 1], [1, 0, 0], tri)[0] < 0  # parallel
+    assert oracle.ray_triangle([0, 0, -1], [0, 0, -1], tri)[0] < 0  # behind origin
+    assert oracle.ray_triangle([5, 0, 1], [0, 0, -1], tri)[0] < 0  # outside
+
+
+def test_ray_triangle_constructed_hits_and_misses():
+    # Rays aimed at a known barycentric point P: t = |P - O|, cos = |n.d|.
+    # Rays aimed just outside an edge miss.
+    rng = np.random.default_rng(2)
+    for _ in range(2000):
+        tri = rng.uniform(-10, 10, (3, 3)).astype(np.float32)
+        v = tri.astype(np.float64)
+        n = np.cross(v[1] - v[0], v[2] - v[0])
+        if np.linalg.norm(n) < 1e-2:
+            continue
+        b = rng.dirichlet([1, 1, 1])
+        b = 0.05 + 0.85 * b  # well inside
+        b /= b.sum()
+        P = b @ v
+        O = rng.uniform(-30, 30, 3)
+        d = (P - O) / np.linalg.norm(P - O)
+        if abs(np.dot(n / np.linalg.norm(n), d)) < 1e-3:
+            continue
+        t, c = oracle.ray_triangle(O, d, tri)
+        assert t == pytest.approx(np.linalg.norm(P - O), rel=1e-9)
+        assert c == pytest.approx(abs(np.dot(n, d)) / np.linalg.norm(n), rel=1e-9)
+        # outside: push P beyond edge v1-v2 (barycentric of v0 negative)
+        Q = v[1] * 0.55 + v[2] * 0.55 - v[0] * 0.10
+        dq = (Q - O) / np.linalg.norm(Q - O)
+        assert oracle.ray_triangle(O, dq, tri)[0] < 0
+
+
+def test_nearest_of_two_planes():
+    # S:85 worked example: planes z=1, z=2, nadir ray from z=5 -> t0 = 3.
+    big = 10.0
+    tris = []
+    for z in (1.0, 2.0):
+        tris += [[[-big, -big, z], [big, -big, z], [big, big, z]],
+                 [[-big, -big, z], [big, big, z], [-big, big, z]]]
+    tris = np.array(tris, np.float32)
+    i, t, c, nc, gap = oracle.nearest_triangle([0.3, 0.1, 5], [0, 0, -1], tris)
+    assert t == 3.0 and i in (2, 3) and gap == pytest.approx(1.0)
+    # ray on the shared diagonal: both triangles tie -> candidate set 2, lower id
+    i, t, c, nc, gap = oracle.nearest_triangle([0.5, 0.5, 5], [0, 0, -1], tris)
+    assert t == 3.0 and i == 2 and nc == 2
+
+
+def test_nearest_is_min_over_all_triangles():
+    # Brute force definition: the reported hit is the minimum over every
+    # triangle's own intersection (each of which is pinned above).
+    rng = np.random.default_rng(3)
+    tris = rng.uniform(-5, 5, (300, 3, 3)).astype(np.float32)
+    for _ in range(200):
+        o = rng.uniform(-8, 8, 3)
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        ts = np.array([oracle.ray_triangle(o, d, tri)[0] for tri in tris])
+        ts[ts < 0] = np.inf
+        i, t, _, _, _ = oracle.nearest_triangle(o, d, tris)
+        if np.isinf(ts.min()):
+            assert i == -1
+        else:
+            assert i == int(np.argmin(ts)) and t == ts.min()
+
+
+# ------------------------------------------------------------------ Philox / RNG
+def _curand_host_philox(seed: int, offset_words: int, n: int) -> np.ndarray:
+    lib = ctypes.CDLL("libcurand.so.10") if _has("libcurand.so.10") else ctypes.CDLL(
+        "/usr/local/cuda/lib64/libcurand.so.10")
+    gen = ctypes.c_void_p()
+    assert lib.curandCreateGeneratorHost(ctypes.byref(gen), 161) == 0
+    assert lib.curandSetPseudoRandomGeneratorSeed(gen, ctypes.c_ulonglong(seed)) == 0
+    assert lib.curandSetGeneratorOffset(gen, ctypes.c_ulonglong(offset_words)) == 0
+    out = np.zeros(n, np.uint32)
+    assert lib.curandGenerate(gen, out.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(n)) == 0
+    lib.curandDestroyGenerator(gen)
+    return out
+
+
+def _has(name):
+    try:
+        ctypes.CDLL(name)
+        return True
+    except OSError:
+        return False
+
+
+def test_philox_matches_curand_host_generator():
+    # curand's host PHILOX4_32_10 generator (an independent implementation of
+    # Salmon et al. SC'11) lays its stream out as 65536 "threads": block b of
+    # the output is philox4x32_10(ctr = (b // 65536, 0, b % 65536, 0),
+    # key = (seed_lo, seed_hi)).  This pins the round function, the key
+    # schedule and counter words c0, c2 (c1, c3: tests/test_gpu_philox.py).
+    rng = np.random.default_rng(4)
+    for seed in (0, 1, 0x123456789ABCDEF0, int(rng.integers(0, 2**63))):
+        out = _curand_host_philox(seed, 0, 4 * 3 * 65536).reshape(-1, 4)
+        blocks = np.concatenate([np.arange(8), rng.integers(0, out.shape[0], 40)])
+        for b in blocks:
+            b = int(b)
+            got = oracle.philox4x32_10([b // 65536, 0, b % 65536, 0],
+                                       [seed & 0xFFFFFFFF, seed >> 32])
+            assert np.array_equal(out[b], got), (seed, b)
+
+
+def test_transmission_u_is_exact_24bit_uniform():
+    # R18: u = (x0 >> 8) 2^-24 in [0,1), exactly representable; roughly uniform.
+    us = np.array([oracle.transmission_u(7, p, s, v) for p in range(50) for s in range(19)
+                   for v in (0, 3, 99)])
+    assert us.min() >= 0 and us.max() < 1
+    assert np.all(us * 2**24 == np.floor(us * 2**24))
+    assert abs(us.mean() - 0.5) < 0.03
+    # word 0 of the counter-based draw
+    x = oracle.philox4x32_10([5, 0, 3, 99], [7, 0])
+    assert oracle.transmission_u(7, 5, 3, 99) == (int(x[0]) >> 8) / 2**24
+
+
+def test_g_function():
+    # R15: no LUT -> spherical LAD, G = 0.5; LUT linear interpolation is exact
+    # on a linear table.
+    assert oracle.g_function(None, 0.3) == 0.5
+    lut = np.linspace(0.2, 0.8, 11).astype(np.float32)
+    for x in (0.0, 0.05, 0.5, 0.93, 1.0):
+        assert oracle.g_function(lut, x) == pytest.approx(0.2 + 0.6 * x, abs=1e-7)
+
+
+# ------------------------------------------------------------------ voxels
+def test_voxel_segments_against_dense_sampling():
+    # Independent check: points sampled densely along the ray fall in the
+    # voxel of the segment that contains them; segments tile [t_in, t_out].
+    rng = np.random.default_rng(5)
+    n = np.array([5, 4, 3])
+    origin = np.array([-1.3, 0.4, 2.0])
+    vs = 0.7
+    hi = origin + n * vs
+    for _ in range(300):
+        o = rng.uniform(origin - 2, hi + 2)
+        target = rng.uniform(origin, hi)
+        d = (target - o) / np.linalg.norm(target - o)
+        tmax = rng.choice([np.inf, rng.uniform(0.5, 6.0)])
+        ta, tb, vid = oracle.voxel_segments(o, d, n, origin, vs, tmax)
+        if len(ta) == 0:
+            continue
+        assert np.all(tb > ta)
+        assert np.all(ta[1:] == tb[:-1])
+        assert np.all(vid[1:] != vid[:-1])
+        ts = np.linspace(ta[0], tb[-1], 4001)[1:-1]
+        k = np.searchsorted(tb, ts)
+        pts = o + ts[:, None] * d
+        c = np.floor((pts - origin) / vs).astype(int)
+        near = np.abs((pts - origin) / vs - np.rint((pts - origin) / vs)).min(axis=1) < 1e-7
+        ok = ~near & np.all((c >= 0) & (c < n), axis=1)
+        ids = c[:, 0] + n[0] * (c[:, 1] + n[1] * c[:, 2])
+        assert np.array_equal(ids[ok], vid[k[ok]])
+        # the entry and exit are the ray's slab interval with the box, clipped
+        tl = (origin - o) / d
+        th = (hi - o) / d
+        t_in = max(0.0, np.minimum(tl, th).max())
+        t_out = min(tmax, np.maximum(tl, th).min())
+        assert ta[0] == pytest.approx(t_in, abs=1e-12)
+        assert tb[-1] == pytest.approx(t_out, abs=1e-12)
+
+
+# ------------------------------------------------------------------ simulate
+def _plane_scene(half=1000.0, z=0.0, refl=0.5):
+    tri = np.array([[[-half, -half, z], [half, -half, z], [half, half, z]],
+                    [[-half, -half, z], [half, half, z], [-half, half, z]]], np.float32)
+    return Scene(tri, np.full(2, refl, np.float32))
+
+
+def _run(scene, params, o, d, ids=None, threads=4):
+    o = np.asarray(o, np.float32).reshape(-1, 3)
+    d = np.asarray(d, np.float32).reshape(-1, 3)
+    n = o.shape[0]
+    ids = np.arange(n, dtype=np.uint64) if ids is None else ids
+    return oracle.simulate(scene, params, o, d, np.arange(n) * 1e-5, ids, n_threads=threads)
+
+
+def test_plane_range_and_lambertian_radiometry():
+    # Plane at z=0, scanner at height h: R_s = h / |d_s,z|; A_s = K rho
+    # |d_s,z| I_s / R_s^4 (Eq. 7 with sigma = rho cos, R14), I_s = far-field
+    # weight (R5); k_s = floor(2 R / (c Delta)).
+    p = ScannerParams(divergence_rad=0.3e-3, subray_count=19)
+    h = 10.0
+    ring, _, _, th, _ = oracle.subray_pattern(19, p.divergence_rad)
+    for zen_deg in (180.0, 170.0, 150.0, 120.0):
+        z = math.radians(zen_deg)
+        d = np.array([math.sin(z), 0.0, math.cos(z)], np.float32)
+        r = _run(_plane_scene(), p, [0, 0, h], d)
+        dd = d.astype(np.float64) / np.linalg.norm(d.astype(np.float64))
+        dirs = np.array([oracle.subray_direction(dd, th[s], _) for s, _ in
+                         zip(range(19), oracle.subray_pattern(19, p.divergence_rad)[4])])
+        R = h / np.abs(dirs[:, 2])
+        assert np.allclose(r.sub_range[0], R, rtol=1e-12)
+        K = 1.0 / (4 * math.pi * p.divergence_rad ** 2)
+        I = np.exp(-2 * np.sin(th) ** 2 / math.tan(p.divergence_rad) ** 2)
+        A = K * 0.5 * np.abs(dirs[:, 2]) * I / R ** 4
+        assert np.allclose(r.sub_amp[0], A, rtol=1e-12)
+        assert np.array_equal(r.sub_k[0], np.floor(2 * R / (C * 1e-9)).astype(np.int64))
+        # C1 zenith 170 deg: 10.1543 m
+        if zen_deg == 170.0:
+            assert R[0] == pytest.approx(10.1543, abs=1e-4)
+
+
+def test_range_time_conversion():
+    # 149.896229 m <-> 1000 ns two-way (c = 299 792 458 m/s).
+    assert 2 * 149.896229 / C * 1e9 == pytest.approx(1000.0, abs=1e-6)
+    p = ScannerParams(subray_count=1, bin_width_ns=1.0,
+                      max_fullwave_range_ns=window_ns_for_range(400))
+    R_true = 149.896229 + 0.5 * 0.149896229  # centre of bin 1000
+    r = _run(_plane_scene(z=0.0), p, [0, 0, R_true], [0, 0, -1])
+    assert r.sub_k[0, 0] == 1000 and r.k0[0] == 1000
+
+
+def test_single_peak_isolated_plane():
+    # All subrays in one bin (nadir onto a plane): exactly one return at
+    # R = (c/2)(k_s + 1/2) Delta within c Delta / 4 of the truth (R12).
+    p = ScannerParams(subray_count=19)
+    for h in (10.0, 37.3, 150.0):
+        r = _run(_plane_scene(), p, [0, 0, h], [0, 0, -1])
+        assert r.n_returns[0] == 1
+        assert abs(r.ret_range[0, 0] - h) <= C * 1e-9 / 4
+        assert r.ret_prim[0, 0] in (0, 1)
+        assert r.ret_number[0, 0] == 1
+
+
+def test_waveform_energy_matches_integral():
+    # Sum_k W[k] Delta / tau -> (Sum_s A_s) * int_0^inf x^2 e^-x dx = 2 Sum_s A_s
+    # (midpoint rule error: 1.3e-4 at Delta = 1 ns, 7e-8 at 0.25 ns).
+    for delta, tol in ((1.0, 3e-4), (0.25, 1e-6)):
+        p = ScannerParams(subray_count=37, bin_width_ns=delta)
+        tau = p.pulse_length_ns / 1.75
+        r = _run(_plane_scene(), p, [0, 0, 50.0], [0.3, 0.1, -1.0])
+        total = r.waveform[0].sum() * delta / tau
+        assert total == pytest.approx(2 * r.sub_amp[0].sum(), rel=tol)
+
+
+def _two_plane_scene(gap=10.0, refl_b=0.5):
+    # plane A (ids 0,1): z = 0, x in [-100, 0]; plane B (ids 2,3): z = -gap
+    a = [[[-100, -100, 0], [0, -100, 0], [0, 100, 0]],
+         [[-100, -100, 0], [0, 100, 0], [-100, 100, 0]]]
+    b = [[[-100, -100, -gap], [100, -100, -gap], [100, 100, -gap]],
+         [[-100, -100, -gap], [100, 100, -gap], [-100, 100, -gap]]]
+    return Scene(np.array(a + b, np.float32),
+                 np.array([0.5, 0.5, refl_b, refl_b], np.float32))
+
+
+def test_two_echoes_numbered_in_time_order():
+    p = ScannerParams(subray_count=19)
+    r = _run(_two_plane_scene(10.0), p, [0, 0, 20.0], [0, 0, -1])
+    assert r.n_returns[0] == 2
+    assert list(r.ret_number[0, :2]) == [1, 2]
+    assert abs(r.ret_range[0, 0] - 20.0) <= C * 1e-9 / 4 + 1e-3
+    assert abs(r.ret_range[0, 1] - 30.0) <= C * 1e-9 / 4 + 1e-3
+    assert r.ret_prim[0, 0] in (0, 1) and r.ret_prim[0, 1] in (2, 3)
+    # cap: max_returns = 1 keeps the earliest
+    p1 = ScannerParams(subray_count=19, max_returns=1)
+    r1 = _run(_two_plane_scene(10.0), p1, [0, 0, 20.0], [0, 0, -1])
+    assert r1.n_returns[0] == 1 and r1.ret_range[0, 0] == r.ret_range[0, 0]
+
+
+def test_threshold_and_window_discard():
+    p = ScannerParams(subray_count=19, detection_threshold=0.05)
+    # second echo 100x weaker than the first -> below 5 % of the max
+    r = _run(_two_plane_scene(10.0, refl_b=0.005), p, [0, 0, 20.0], [0, 0, -1])
+    assert r.n_returns[0] == 1
+    # second surface 300 m further: beyond the 200 m window -> discarded
+    r = _run(_two_plane_scene(300.0), p, [0, 0, 20.0], [0, 0, -1])
+    assert r.n_returns[0] == 1
+    sel = r.sub_prim[0] >= 2
+    assert sel.any()
+    n_bins = r.waveform.shape[1]
+    assert np.all(r.sub_k[0][sel] - r.k0[0] >= n_bins)
+    # the waveform holds only plane A's energy
+    tau = p.pulse_length_ns / 1.75
+    total = r.waveform[0].sum() * 1.0 / tau
+    assert total == pytest.approx(2 * r.sub_amp[0][~sel].sum(), rel=3e-4)
+
+
+def test_miss_gives_empty_pulse():
+    p = ScannerParams(subray_count=19)
+    r = _run(_plane_scene(), p, [0, 0, 10.0], [0, 0, 1.0])
+    assert r.k0[0] == -1 and r.n_returns[0] == 0 and not r.waveform[0].any()
+    assert np.all(np.isnan(r.sub_range[0])) and np.all(r.sub_prim[0] == 0xFFFFFFFF)
+
+
+def test_beer_lambert_single_voxel():
+    # Eq. 6 + P:392 (R17): P(pass) = exp(-sigma L); depth of a return ~
+    # exponential(sigma) truncated to [0, L].
+    for sigma_L in (0.25, 1.0, 3.0):
+        L = 100.0
+        sigma = sigma_L / L
+        pad = np.full((1, 1, 1), 2 * sigma, np.float32)  # G = 0.5 (spherical)
+        scene = Scene(np.zeros((0, 3, 3), np.float32), None, pad, (-50.0, -50.0, 0.0), L)
+        p = ScannerParams(subray_count=19, seed=11)
+        n = 3000
+        r = _run(scene, p, np.tile([0, 0, 200.0], (n, 1)), np.tile([0, 0, -1.0], (n, 1)))
+        hit = r.sub_prim != 0xFFFFFFFF
+        N = hit.size
+        pe = math.exp(-float(np.float32(2 * sigma)) * 0.5 * L)
+        assert abs((~hit).mean() - pe) <= 3 * math.sqrt(pe * (1 - pe) / N)
+        depth = (r.sub_range[hit] - 100.0)  # entry at t = 100 (cos theta ~ 1)
+        assert depth.min() >= -1e-3 and depth.max() <= L + 1e-3
+        s = float(np.float32(2 * sigma)) * 0.5
+        mean = 1 / s - L * math.exp(-s * L) / (1 - math.exp(-s * L))
+        var_bound = (L * L / 12 + 1 / s ** 2)
+        assert abs(depth.mean() - mean) <= 4 * math.sqrt(var_bound / depth.size)
+        assert np.all(r.sub_prim[hit] == 0)  # n_tris (0) + voxel id 0
+
+
+def test_beer_lambert_slab_of_voxels():
+    # 10 stacked voxels of PAD p: P(pass through all) = exp(-sigma sum L).
+    L = 10.0
+    sigma = 0.1 / L
+    pad = np.full((10, 1, 1), 2 * sigma, np.float32)
+    scene = Scene(np.zeros((0, 3, 3), np.float32), None, pad, (-5.0, -5.0, 0.0), L)
+    p = ScannerParams(subray_count=19, seed=3)
+    n = 4000
+    r = _run(scene, p, np.tile([0, 0, 200.0], (n, 1)), np.tile([0, 0, -1.0], (n, 1)))
+    hit = r.sub_prim != 0xFFFFFFFF
+    s = float(np.float32(2 * sigma)) * 0.5
+    pe = math.exp(-s * 100.0)
+    assert abs((~hit).mean() - pe) <= 3 * math.sqrt(pe * (1 - pe) / hit.size)
+    # voxel ids are reported as n_tris + id and are in [0, 10)
+    assert np.all(r.sub_prim[hit] < 10)
+
+
+def test_triangle_inside_voxel_clips_the_chord():
+    # R20: a triangle inside a voxel clips the chord; a very dense voxel
+    # returns before the surface, an empty one lets the ray reach it.
+    tri = _plane_scene(half=50.0, z=5.0).tri_xyz
+    for pad_v, expect_vox in ((0.0, False), (1e4, True)):
+        pad = np.full((1, 1, 1), pad_v, np.float32)
+        scene = Scene(tri, np.full(2, 0.5, np.float32), pad, (-5.0, -5.0, 0.0), 10.0)
+        r = _run(scene, ScannerParams(subray_count=7), [0, 0, 20.0], [0, 0, -1.0])
+        if expect_vox:
+            assert np.all(r.sub_prim[0] == 2)  # n_tris (2) + voxel 0
+            assert np.all(r.sub_range[0] < 15.0) and np.all(r.sub_range[0] >= 10.0)
+        else:
+            assert np.all(r.sub_prim[0] < 2)
+            assert np.allclose(r.sub_range[0], 15.0, rtol=1e-6)
+
+
+def test_thread_count_invariance_and_repeatability():
+    # the oracle's result does not depend on the thread count.
+    from workloads import make_workload
+    w = make_workload("C3", scale=0.02)
+    o, d, t = w.pulses(0, 60)
+    ids = np.arange(60, dtype=np.uint64)
+    a = oracle.simulate(w.scene, w.params, o, d, t, ids, n_threads=1)
+    b = oracle.simulate(w.scene, w.params, o, d, t, ids, n_threads=7)
+    for f in ("n_returns", "k0", "waveform", "ret_range", "sub_range", "sub_prim"):
+        assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), f
