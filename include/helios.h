@@ -1,0 +1,221 @@
+/*
+ * helios.h -- C ABI of libhelios.so, the B200 (sm_100a) hot path of
+ * HELIOS++-style virtual laser scanning (Winiwarter et al., arXiv 2101.09154).
+ *
+ * Citations: "P:n" = line n of the paper text, with the section /
+ * equation named; "R<k>" = reading k of DESIGN.md s.3 (where the paper is
+ * silent, ambiguous or garbled).
+ *
+ * The problem, as the paper states it:
+ *   - a scene is a set of primitives S = {P1..Pn} (Sec. 5.1): here
+ *     triangles (meshes and DTM rasters) and one grid of
+ *     transmissive voxels carrying plant area density;
+ *   - every emitted pulse is fanned out into subrays on concentric rings
+ *     (Fig. 6), each cast independently to its first hit
+ *     (P:197);
+ *   - each hit's power follows the Gaussian beam profile (Eq. 1; Eq. 2,
+ *     P:193) and the radar equation (Eq. 7);
+ *   - the subray returns are binned into the pulse's full waveform with the
+ *     pulse shape of Eq. 3 and a local-maximum filter
+ *     turns it into discrete returns, linked to the waveform by the
+ *     pulse index ("fullwaveIndex").
+ *
+ * Conventions for every call:
+ *   - d_* = CUDA device pointer (cudaMalloc / torch CUDA tensor), h_* = host.
+ *     Pointers named "p_*" may be either: the library asks the driver
+ *     (cudaPointerGetAttributes) and stages host memory through device
+ *     scratch itself (host <-> device copies are then part of the call).
+ *   - Every call returns helios_status.  No C++ exception or abort crosses
+ *     the ABI.  On failure helios_last_error() names the offending field.
+ *   - Calls never read or write host memory asynchronously after returning.
+ */
+#ifndef HELIOS_H_
+#define HELIOS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* helios_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  HELIOS_OK = 0,
+  HELIOS_ERR_INVALID_ARGUMENT = 1, /* bad pointer / value; see helios_last_error()      */
+  HELIOS_ERR_OUT_OF_MEMORY = 2,    /* device allocation failed                          */
+  HELIOS_ERR_CUDA = 3,             /* any other CUDA runtime error                      */
+  HELIOS_ERR_NOT_BUILT = 4,        /* helios_simulate before helios_build_accel         */
+  HELIOS_ERR_EMPTY_SCENE = 5       /* n_tris == 0 and no voxel grid                     */
+} helios_status;
+
+/* Thread-local, NUL-terminated description of the last failure on this
+ * thread ("" after a success).  Valid until the next helios_* call on the
+ * same thread. */
+const char* helios_last_error(void);
+
+/* Library version string, e.g. "helios-b200 0.1 sm_100a". */
+const char* helios_version(void);
+
+/* ------------------------------------------------------------------------
+ * Scene (Sec. 5.1; P:272 mixed-model scenes).
+ * ---------------------------------------------------------------------- */
+typedef struct helios_scene_s* helios_scene; /* opaque, library-owned */
+
+typedef struct {
+  /* Triangles.  [n_tris][3 vertices][xyz] fp32, row-major.
+   * Primitive id = row index.  May be NULL iff n_tris == 0.                */
+  const float* p_tri_xyz;
+  /* [n_tris] Lambertian reflectance rho in [0,1] ("dependent on the
+   * material", R14).  NULL -> 0.5 for every triangle.                      */
+  const float* p_tri_reflectance;
+  uint32_t n_tris;
+  /* Transmissive voxel grid.  [nz][ny][nx] fp32
+   * plant area density (m^2/m^3) >= 0; NULL -> no grid.  Voxel id
+   * = ix + nx*(iy + ny*iz); reported as prim id n_tris + voxel id.          */
+  const float* p_voxel_pad;
+  uint32_t nx, ny, nz;
+  double grid_origin[3]; /* min corner (m)   */
+  double voxel_size;     /* edge (m), > 0    */
+  /* G(|d_z|) for sigma = PAD * G (Eq. 4 / Table 2, R15): n_lut values at
+   * |d_z| = k/(n_lut-1), linear interpolation.  NULL / 0 -> spherical LAD,
+   * G = 0.5.  n_lut == 1 is invalid; n_lut <= 4096.                         */
+  const float* h_g_lut;
+  uint32_t n_lut;
+} helios_scene_desc;
+
+/* Copy the scene into library-owned device memory (the caller may free its
+ * arrays on return; the stream is synchronised).
+ * Errors: INVALID_ARGUMENT (NULL desc/out, NULL triangles with n_tris > 0,
+ * non-finite vertex, reflectance outside [0,1], PAD < 0 or non-finite,
+ * voxel_size <= 0, n_tris + nx*ny*nz >= 2^32 - 1, n_lut == 1 or > 4096,
+ * n_tris >= 2^28); EMPTY_SCENE (no triangles and no grid);
+ * OUT_OF_MEMORY; CUDA. */
+helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream stream,
+                                  helios_scene* out);
+
+/* Build the acceleration structure on the device (replaces the paper's
+ * kd-tree, by an LBVH): 30-bit Morton codes of triangle centroids,
+ * radix sort, Karras hierarchy, bottom-up AABB refit, 64-B child-pair nodes,
+ * triangles permuted to leaf order.  Idempotent.  Synchronises the stream.
+ * Errors: INVALID_ARGUMENT (NULL scene), OUT_OF_MEMORY, CUDA. */
+helios_status helios_build_accel(helios_scene scene, helios_stream stream);
+
+/* Free everything the scene owns.  NULL is a no-op.  Must not race with a
+ * helios_simulate on the same scene. */
+helios_status helios_scene_destroy(helios_scene scene);
+
+/* Statistics of a built scene (for logs and the roofline accounting). */
+typedef struct {
+  uint32_t n_tris, n_nodes, max_depth, leaf_max;
+  uint64_t node_bytes, tri_bytes, grid_bytes;
+  double build_ms; /* device time of the last helios_build_accel */
+} helios_scene_info;
+helios_status helios_scene_get_info(helios_scene scene, helios_scene_info* out);
+
+/* ------------------------------------------------------------------------
+ * Scanner / beam / detector parameters.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  double divergence_rad;  /* beta: 1/e^2 HALF-angle of the beam (R3), in (0, 0.1)   */
+  uint32_t subray_count;  /* paper rule 1 + sum floor(2 pi i):
+                             {1,7,19,37,62,93,130,173,223,279}; or hexagonal
+                             1 + 3q(q+1) (R1): {61,91,127,169,217,271}          */
+  double pulse_length_ns; /* tau = pulse_length_ns / 1.75, > 0            */
+  double bin_width_ns;    /* Delta, binWidth_ns, > 0               */
+  double max_fullwave_range_ns; /* maxFullwaveRange_ns, >= bin width;
+                                   n_bins = ceil(window / Delta) (R9)            */
+  float detection_threshold;    /* fraction of the pulse's waveform max (R11), (0,1] */
+  uint32_t max_returns;         /* 1..255; earliest returns kept (R11)           */
+  double peak_power_w;          /* I0 of Eq. 1 (> 0)                             */
+  double efficiency;            /* lambda of Eq. 7 (atmosphere x efficiency), >= 0 */
+  double receiver_diameter_m;   /* alpha of Eq. 7 (R14), >= 0                    */
+  double wavelength_nm;         /* lambda of Eq. 2, > 0 when beam_waist_m > 0    */
+  double beam_waist_m;          /* w0 of Eq. 2; 0 -> far field w = R tan(beta) (R5) */
+  double focus_range_m;         /* R0 of Eq. 2, >= 0                             */
+  uint64_t seed;                /* Philox-4x32-10 key for transmission draws (R19) */
+} helios_scanner_params;
+
+/* Number of waveform bins, ceil(max_fullwave_range_ns / bin_width_ns);
+ * 0 if the parameters are invalid. */
+uint32_t helios_waveform_bins(const helios_scanner_params* params);
+
+/* Kernel length L_p = ceil(20 tau / Delta) of the binned outgoing pulse (R9). */
+uint32_t helios_pulse_taps(const helios_scanner_params* params);
+
+/* ------------------------------------------------------------------------
+ * Pulses and outputs.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const float* p_origin;    /* [n_pulses][3] fp32 (m)                               */
+  const float* p_direction; /* [n_pulses][3] fp32, non-zero; normalised in fp64 (R24) */
+  const double* p_time_s;   /* [n_pulses] GPS time, copied into returns; may be NULL */
+  uint64_t n_pulses;
+  uint64_t pulse_index_base; /* global id of element 0: Philox counter and output
+                                pulse id ("fullwaveIndex").  Splitting a run
+                                into batches with matching bases is bitwise
+                                identical to one call.                           */
+} helios_pulses;
+
+/* One discrete return (P:215, P:276 LAS point format 1 fields). 32 bytes. */
+typedef struct {
+  double range_m;        /* (c/2)(k0 + k - j* + 1/2) Delta (R12)                */
+  double gps_time_s;     /* the pulse's time                                    */
+  float intensity;       /* waveform value at the peak bin                      */
+  uint32_t prim_id;      /* generating primitive (R13): triangle row, or
+                            n_tris + voxel id                                   */
+  uint8_t return_number; /* 1-based, time order                                 */
+  uint8_t n_returns;     /* returns of this pulse                               */
+  uint8_t pad[6];
+} helios_return;
+
+/* One subray's event (debug / parity export). 16 bytes.
+ * Miss: range NaN, amplitude 0, prim UINT32_MAX. */
+typedef struct {
+  double range_m;  /* ray parameter of the event (m)  */
+  float amplitude; /* A_s = K sigma_eff I_s / R^4 (Eq. 1, 7) */
+  uint32_t prim_id;
+} helios_subray_hit;
+
+typedef struct {
+  uint8_t* p_n_returns;        /* [n_pulses]                                        */
+  helios_return* p_returns;    /* [n_pulses][max_returns]; unused slots zeroed     */
+  int64_t* p_wf_first_bin;     /* [n_pulses] absolute bin k0 of waveform[0]; -1 = no hit */
+  float* p_waveform;           /* [n_pulses][n_bins] or NULL (binning still runs) */
+  helios_subray_hit* p_subray_hits; /* [n_pulses][subray_count] or NULL              */
+} helios_outputs;
+
+/* Optional per-call accounting.  Inputs: collect_counters.  Everything else
+ * is written by helios_simulate. */
+typedef struct {
+  uint32_t collect_counters; /* in: 1 -> run the instrumented traversal variant
+                                (node / triangle / voxel-step counters; slower:
+                                for roofline byte accounting only)               */
+  uint32_t kernel_launches;  /* out: kernels launched by this call               */
+  uint64_t pulses, subrays;
+  uint64_t subray_hits, voxel_returns, returns;     /* only with collect_counters */
+  uint64_t nodes_visited, tris_tested, voxel_steps; /* only with collect_counters */
+  double trace_ms;    /* out: summed device time of the trace launches (K6), CUDA events */
+  double waveform_ms; /* out: summed device time of the waveform launches (K7)          */
+} helios_stats;
+
+/* Simulate n_pulses pulses (the hot path: subray fan-out, nearest hit against
+ * triangles and transmissive voxels, radiometry, full waveform, peaks).
+ * Enqueues on `stream` and synchronises it before returning (blocking).
+ * Pointers in pulses/outputs may be device or host memory (see top).
+ * stats may be NULL; when non-NULL the per-kernel device times are measured
+ * with CUDA events on `stream`, and with stats->collect_counters = 1 the
+ * traversal counters are collected by an instrumented kernel variant.
+ * Errors: INVALID_ARGUMENT (NULL args, parameter out of range, a zero-length
+ * pulse direction -- detected on the device; that pulse's outputs are then
+ * those of a pulse with no hit), NOT_BUILT, OUT_OF_MEMORY, CUDA.
+ * n_pulses == 0 is OK and writes nothing. */
+helios_status helios_simulate(helios_scene scene, const helios_scanner_params* params,
+                              const helios_pulses* pulses, const helios_outputs* outputs,
+                              helios_stream stream, helios_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELIOS_H_ */

@@ -1,0 +1,590 @@
+// api.cu -- the C ABI of libhelios.so (include/helios.h) and its host runtime:
+// argument validation, scene ownership, the beam-pattern tables, scratch
+// management (stream-ordered cudaMallocAsync), host<->device staging, pulse
+// chunking so the K6->K7 subray records stay L2-resident, and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace helios;
+
+struct helios_scene_s {
+  uint32_t n_tris = 0;
+  float* d_xyz = nullptr;   // original order (build input)
+  float* d_refl = nullptr;
+  float* d_pad = nullptr;
+  uint32_t nx = 0, ny = 0, nz = 0;
+  double origin[3] = {0, 0, 0};
+  double vs = 0;
+  float* d_lut = nullptr;
+  uint32_t n_lut = 0;
+  bool built = false;
+  BuildResult bvh{};
+  int device = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+helios_status fail(helios_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+helios_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation)
+    return fail(HELIOS_ERR_OUT_OF_MEMORY, "%s: out of device memory", what);
+  return fail(HELIOS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define TRY_CUDA(expr, what)                        \
+  do {                                              \
+    cudaError_t e_ = (expr);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+bool device_accessible(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// ---- subray pattern (P:199 / R1): paper rule floor(2 pi i), or hexagonal 6i
+struct Pattern {
+  int q = -1;
+  bool hex = false;
+};
+Pattern resolve_pattern(uint32_t count) {
+  Pattern pt;
+  uint64_t total = 1;
+  for (int q = 0; q <= 64 && total <= count; ++q) {
+    if (q > 0) total += (uint64_t)std::floor(2.0 * kPi * (double)q);
+    if (total == count) {
+      pt.q = q;
+      return pt;
+    }
+  }
+  for (int q = 0; q <= 64; ++q) {
+    if (1ull + 3ull * (uint64_t)q * (uint64_t)(q + 1) == count) {
+      pt.q = q;
+      pt.hex = true;
+      return pt;
+    }
+  }
+  return pt;
+}
+
+std::vector<SubrayConst> subray_table(uint32_t count, double beta, Pattern pt) {
+  std::vector<SubrayConst> t;
+  t.reserve(count);
+  const double tb = std::tan(beta);
+  auto push = [&](double theta, double phi) {
+    SubrayConst c{};
+    const double st = std::sin(theta);
+    c.cos_t = std::cos(theta);
+    c.a = st * std::cos(phi);
+    c.b = st * std::sin(phi);
+    c.sin_t = st;
+    c.w_far = theta == 0.0 ? 1.0 : std::exp(-2.0 * st * st / (tb * tb));
+    t.push_back(c);
+  };
+  push(0.0, 0.0);  // central subray
+  for (int i = 1; i <= pt.q; ++i) {
+    const int n = pt.hex ? 6 * i : (int)std::floor(2.0 * kPi * (double)i);
+    const double theta = (double)i / (double)pt.q * beta;  // R2
+    for (int j = 0; j < n; ++j) push(theta, 2.0 * kPi * (double)j / (double)n);  // R4
+  }
+  return t;
+}
+
+struct Derived {
+  uint32_t n_bins = 0, taps = 0, jstar = 0;
+  std::vector<double> kernel;
+  Pattern pt;
+};
+
+helios_status validate_params(const helios_scanner_params* p, Derived* d) {
+  if (!p) return fail(HELIOS_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (!(p->divergence_rad > 0.0 && p->divergence_rad < 0.1))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "divergence_rad must be in (0, 0.1)");
+  d->pt = resolve_pattern(p->subray_count);
+  if (d->pt.q < 0 || p->subray_count > (uint32_t)kMaxSubrays)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                "subray_count %u is neither 1+sum floor(2 pi i) nor 1+3q(q+1)", p->subray_count);
+  if (!(p->pulse_length_ns > 0.0) || !std::isfinite(p->pulse_length_ns))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulse_length_ns must be > 0");
+  if (!(p->bin_width_ns > 0.0) || !std::isfinite(p->bin_width_ns))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "bin_width_ns must be > 0");
+  if (!(p->max_fullwave_range_ns >= p->bin_width_ns) || !std::isfinite(p->max_fullwave_range_ns))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "max_fullwave_range_ns must be >= bin_width_ns");
+  if (!(p->detection_threshold > 0.0f && p->detection_threshold <= 1.0f))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "detection_threshold must be in (0, 1]");
+  if (p->max_returns < 1 || p->max_returns > 255)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "max_returns must be in [1, 255]");
+  if (!(p->peak_power_w > 0.0) || !std::isfinite(p->peak_power_w))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "peak_power_w must be > 0");
+  if (!(p->efficiency >= 0.0) || !(p->receiver_diameter_m >= 0.0) ||
+      !std::isfinite(p->efficiency) || !std::isfinite(p->receiver_diameter_m))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "efficiency / receiver_diameter_m must be >= 0");
+  if (!(p->beam_waist_m >= 0.0) || !(p->focus_range_m >= 0.0))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "beam_waist_m / focus_range_m must be >= 0");
+  if (p->beam_waist_m > 0.0 && !(p->wavelength_nm > 0.0))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "wavelength_nm must be > 0 with Eq. 2 (beam_waist_m > 0)");
+  const double nb = std::ceil(p->max_fullwave_range_ns / p->bin_width_ns);  // R9
+  const double tau = p->pulse_length_ns / 1.75;
+  const double taps = std::ceil(20.0 * tau / p->bin_width_ns);               // R9
+  if (nb > 1e6) return fail(HELIOS_ERR_INVALID_ARGUMENT, "too many waveform bins (%g)", nb);
+  if (taps > kMaxTaps || taps < 1)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulse kernel of %g taps out of range", taps);
+  d->n_bins = (uint32_t)nb;
+  d->taps = (uint32_t)taps;
+  if (waveform_warps(d->n_bins, p->subray_count, d->taps) == 0)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                "n_bins %u does not fit the per-pulse shared-memory waveform", d->n_bins);
+  d->kernel.resize(d->taps);
+  double best = -1.0;
+  for (uint32_t j = 0; j < d->taps; ++j) {
+    const double x = ((double)j + 0.5) * p->bin_width_ns / tau;  // bin centre (R9)
+    d->kernel[j] = x * x * std::exp(-x);                             // Eq. 3 shape
+    if (d->kernel[j] > best) {
+      best = d->kernel[j];
+      d->jstar = j;
+    }
+  }
+  return HELIOS_OK;
+}
+
+// ---- validation kernel for scene arrays (finite vertices, rho in [0,1], PAD >= 0)
+__global__ void k_check_scene(const float* __restrict__ xyz, uint64_t n_xyz,
+                              const float* __restrict__ refl, uint64_t n_refl,
+                              const float* __restrict__ pad, uint64_t n_pad,
+                              unsigned* __restrict__ bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_xyz; i += stride)
+    if (!isfinite(xyz[i])) atomicOr(bad, 1u);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_refl; i += stride) {
+    const float r = refl[i];
+    if (!(r >= 0.0f && r <= 1.0f)) atomicOr(bad, 2u);
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+    const float v = pad[i];
+    if (!(v >= 0.0f) || !isfinite(v)) atomicOr(bad, 4u);
+  }
+}
+
+template <class T>
+cudaError_t copy_in(T** dst, const T* src, size_t count, cudaStream_t s) {
+  cudaError_t e = cudaMallocAsync((void**)dst, sizeof(T) * (count ? count : 1), s);
+  if (e != cudaSuccess) return e;
+  if (count) e = cudaMemcpyAsync(*dst, src, sizeof(T) * count, cudaMemcpyDefault, s);
+  return e;
+}
+
+void free_scene(helios_scene sc, cudaStream_t s) {
+  cudaFreeAsync(sc->d_xyz, s);
+  cudaFreeAsync(sc->d_refl, s);
+  cudaFreeAsync(sc->d_pad, s);
+  cudaFreeAsync(sc->d_lut, s);
+  cudaFreeAsync(sc->bvh.tris, s);
+  cudaFreeAsync(sc->bvh.nodes, s);
+  cudaStreamSynchronize(s);
+}
+
+// one argument array: device-accessible as given, or staged through scratch
+struct Staged {
+  void* dev = nullptr;
+  bool owned = false;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* helios_last_error(void) { return g_err.c_str(); }
+
+const char* helios_version(void) { return "helios-b200 0.1 sm_100a"; }
+
+helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream stream,
+                                  helios_scene* out) {
+  g_err.clear();
+  if (!desc || !out) return fail(HELIOS_ERR_INVALID_ARGUMENT, "desc/out is NULL");
+  *out = nullptr;
+  const cudaStream_t s = (cudaStream_t)stream;
+  if (desc->n_tris > 0 && !desc->p_tri_xyz)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_tri_xyz is NULL with n_tris = %u", desc->n_tris);
+  if (desc->n_tris >= (1u << 28))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "n_tris >= 2^28 is not supported");
+  const bool grid = desc->p_voxel_pad != nullptr;
+  uint64_t nvox = 0;
+  if (grid) {
+    if (desc->nx == 0 || desc->ny == 0 || desc->nz == 0)
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "voxel grid dims must be > 0");
+    if (!(desc->voxel_size > 0.0) || !std::isfinite(desc->voxel_size))
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "voxel_size must be > 0");
+    for (int a = 0; a < 3; ++a)
+      if (!std::isfinite(desc->grid_origin[a]))
+        return fail(HELIOS_ERR_INVALID_ARGUMENT, "grid_origin must be finite");
+    nvox = (uint64_t)desc->nx * desc->ny * desc->nz;
+    if ((uint64_t)desc->n_tris + nvox >= 0xFFFFFFFFull)
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "n_tris + nx*ny*nz must be < 2^32 - 1");
+  }
+  if (desc->n_tris == 0 && !grid)
+    return fail(HELIOS_ERR_EMPTY_SCENE, "scene has no triangles and no voxel grid");
+  if (desc->n_lut == 1 || desc->n_lut > (uint32_t)kMaxLut)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "n_lut must be 0 or in [2, %d]", kMaxLut);
+  if (desc->n_lut > 0 && !desc->h_g_lut)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "h_g_lut is NULL with n_lut > 0");
+  for (uint32_t k = 0; k < desc->n_lut; ++k)
+    if (!(desc->h_g_lut[k] >= 0.0f) || !std::isfinite(desc->h_g_lut[k]))
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "h_g_lut[%u] must be finite and >= 0", k);
+
+  helios_scene sc = new (std::nothrow) helios_scene_s();
+  if (!sc) return fail(HELIOS_ERR_OUT_OF_MEMORY, "host allocation failed");
+  cudaGetDevice(&sc->device);
+  sc->n_tris = desc->n_tris;
+  cudaError_t e = cudaSuccess;
+  unsigned* d_bad = nullptr;
+  unsigned bad = 0;
+  do {
+    if (desc->n_tris) {
+      if ((e = copy_in(&sc->d_xyz, desc->p_tri_xyz, 9ull * desc->n_tris, s)) != cudaSuccess) break;
+      if (desc->p_tri_reflectance &&
+          (e = copy_in(&sc->d_refl, desc->p_tri_reflectance, desc->n_tris, s)) != cudaSuccess)
+        break;
+    }
+    if (grid) {
+      sc->nx = desc->nx;
+      sc->ny = desc->ny;
+      sc->nz = desc->nz;
+      for (int a = 0; a < 3; ++a) sc->origin[a] = desc->grid_origin[a];
+      sc->vs = desc->voxel_size;
+      if ((e = copy_in(&sc->d_pad, desc->p_voxel_pad, nvox, s)) != cudaSuccess) break;
+    }
+    if (desc->n_lut) {
+      sc->n_lut = desc->n_lut;
+      if ((e = copy_in(&sc->d_lut, desc->h_g_lut, desc->n_lut, s)) != cudaSuccess) break;
+    }
+    if ((e = cudaMallocAsync((void**)&d_bad, sizeof(unsigned), s)) != cudaSuccess) break;
+    if ((e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned), s)) != cudaSuccess) break;
+    k_check_scene<<<148 * 4, 256, 0, s>>>(sc->d_xyz, 9ull * sc->n_tris, sc->d_refl,
+                                         sc->d_refl ? sc->n_tris : 0, sc->d_pad,
+                                         grid ? nvox : 0, d_bad);
+    if ((e = cudaGetLastError()) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(&bad, d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+      break;
+    e = cudaStreamSynchronize(s);
+  } while (0);
+  cudaFreeAsync(d_bad, s);
+  if (e != cudaSuccess) {
+    free_scene(sc, s);
+    delete sc;
+    return cuda_fail(e, "helios_scene_create");
+  }
+  if (bad) {
+    free_scene(sc, s);
+    delete sc;
+    if (bad & 1u) return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_tri_xyz has a non-finite vertex");
+    if (bad & 2u) return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_tri_reflectance outside [0, 1]");
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_voxel_pad has a negative or non-finite value");
+  }
+  *out = sc;
+  return HELIOS_OK;
+}
+
+helios_status helios_build_accel(helios_scene sc, helios_stream stream) {
+  g_err.clear();
+  if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (sc->built) return HELIOS_OK;
+  const cudaStream_t s = (cudaStream_t)stream;
+  char err[256] = {0};
+  cudaError_t e = build_lbvh(sc->d_xyz, sc->d_refl, sc->n_tris, s, &sc->bvh, err, sizeof(err));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation)
+      return fail(HELIOS_ERR_OUT_OF_MEMORY, "helios_build_accel: %s", err);
+    return fail(HELIOS_ERR_CUDA, "helios_build_accel: %s", err);
+  }
+  sc->built = true;
+  return HELIOS_OK;
+}
+
+helios_status helios_scene_destroy(helios_scene sc) {
+  g_err.clear();
+  if (!sc) return HELIOS_OK;
+  free_scene(sc, nullptr);
+  delete sc;
+  return HELIOS_OK;
+}
+
+helios_status helios_scene_get_info(helios_scene sc, helios_scene_info* out) {
+  g_err.clear();
+  if (!sc || !out) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene/out is NULL");
+  out->n_tris = sc->n_tris;
+  out->n_nodes = sc->bvh.n_nodes;
+  out->max_depth = sc->bvh.max_depth;
+  out->leaf_max = kLeafMax;
+  out->node_bytes = (uint64_t)sc->bvh.n_nodes * sizeof(Node);
+  out->tri_bytes = (uint64_t)sc->n_tris * sizeof(TriRecord);
+  out->grid_bytes = (uint64_t)sc->nx * sc->ny * sc->nz * sizeof(float);
+  out->build_ms = sc->bvh.ms;
+  return HELIOS_OK;
+}
+
+uint32_t helios_waveform_bins(const helios_scanner_params* params) {
+  Derived d;
+  std::string keep = g_err;
+  const uint32_t r = validate_params(params, &d) == HELIOS_OK ? d.n_bins : 0;
+  g_err = keep;
+  return r;
+}
+
+uint32_t helios_pulse_taps(const helios_scanner_params* params) {
+  Derived d;
+  std::string keep = g_err;
+  const uint32_t r = validate_params(params, &d) == HELIOS_OK ? d.taps : 0;
+  g_err = keep;
+  return r;
+}
+
+helios_status helios_simulate(helios_scene sc, const helios_scanner_params* params,
+                              const helios_pulses* pulses, const helios_outputs* outputs,
+                              helios_stream stream, helios_stats* stats) {
+  g_err.clear();
+  if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (!pulses || !outputs) return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs is NULL");
+  Derived d;
+  helios_status st = validate_params(params, &d);
+  if (st != HELIOS_OK) return st;
+  if (!sc->built) return fail(HELIOS_ERR_NOT_BUILT, "helios_build_accel has not been called");
+  const bool counters = stats && stats->collect_counters;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->collect_counters = counters ? 1u : 0u;
+  }
+  const uint64_t n = pulses->n_pulses;
+  if (n == 0) return HELIOS_OK;
+  if (!pulses->p_origin || !pulses->p_direction)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_origin/p_direction is NULL");
+  if (!outputs->p_n_returns || !outputs->p_returns || !outputs->p_wf_first_bin)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                "p_n_returns/p_returns/p_wf_first_bin must not be NULL");
+  const uint32_t N = params->subray_count;
+  const uint32_t R = params->max_returns;
+  const cudaStream_t s = (cudaStream_t)stream;
+
+  // ---- host tables
+  const std::vector<SubrayConst> tab = subray_table(N, params->divergence_rad, d.pt);
+  const double beta = params->divergence_rad;
+  const double K = params->efficiency * params->receiver_diameter_m * params->receiver_diameter_m /
+                   (4.0 * kPi * beta * beta);  // Eq. 7 (R14)
+
+  // ---- scratch + staging
+  std::vector<void*> scratch;
+  auto alloc = [&](void** p, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
+    if (e == cudaSuccess) scratch.push_back(*p);
+    return e;
+  };
+  auto cleanup = [&]() {
+    for (void* p : scratch) cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+  };
+  struct Arr {
+    const void* user;
+    size_t bytes;
+    bool in;  // host->device before, else device->host after
+    void* dev;
+    bool staged;
+  };
+  Arr arrs[] = {
+      {pulses->p_origin, 12 * n, true, nullptr, false},
+      {pulses->p_direction, 12 * n, true, nullptr, false},
+      {pulses->p_time_s, 8 * n, true, nullptr, false},
+      {outputs->p_n_returns, n, false, nullptr, false},
+      {outputs->p_returns, sizeof(helios_return) * R * n, false, nullptr, false},
+      {outputs->p_wf_first_bin, 8 * n, false, nullptr, false},
+      {outputs->p_waveform, 4ull * d.n_bins * n, false, nullptr, false},
+      {outputs->p_subray_hits, sizeof(helios_subray_hit) * N * n, false, nullptr, false},
+  };
+  cudaError_t e = cudaSuccess;
+  for (Arr& a : arrs) {
+    if (!a.user) continue;
+    if (device_accessible(a.user)) {
+      a.dev = const_cast<void*>(a.user);
+      continue;
+    }
+    a.staged = true;
+    if ((e = alloc(&a.dev, a.bytes)) != cudaSuccess) break;
+    if (a.in && (e = cudaMemcpyAsync(a.dev, a.user, a.bytes, cudaMemcpyHostToDevice, s)) !=
+                    cudaSuccess)
+      break;
+  }
+  SubrayConst* d_tab = nullptr;
+  double* d_ker = nullptr;
+  unsigned* d_err = nullptr;
+  unsigned long long* d_cnt = nullptr;
+  helios_subray_hit* d_rec = nullptr;
+  // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
+  const uint64_t chunk = std::max<uint64_t>(1024, (48ull << 20) / (16ull * N));
+  const bool own_rec = arrs[7].dev == nullptr;
+  if (e == cudaSuccess) e = alloc((void**)&d_tab, sizeof(SubrayConst) * N);
+  if (e == cudaSuccess) e = alloc((void**)&d_ker, sizeof(double) * d.taps);
+  if (e == cudaSuccess) e = alloc((void**)&d_err, sizeof(unsigned));
+  if (e == cudaSuccess) e = alloc((void**)&d_cnt, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess && own_rec)
+    e = alloc((void**)&d_rec, sizeof(helios_subray_hit) * N * std::min(n, chunk));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_tab, tab.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_ker, d.kernel.data(), sizeof(double) * d.taps, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, sizeof(unsigned), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, s);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "helios_simulate (setup)");
+  }
+
+  TraceArgs ta{};
+  ta.tris = sc->bvh.tris;
+  ta.nodes = sc->bvh.nodes;
+  ta.root = sc->bvh.root;
+  ta.n_tris = sc->n_tris;
+  ta.pad = sc->d_pad;
+  ta.nx = sc->nx;
+  ta.ny = sc->ny;
+  ta.nz = sc->nz;
+  ta.gx0 = sc->origin[0];
+  ta.gy0 = sc->origin[1];
+  ta.gz0 = sc->origin[2];
+  ta.vs = sc->vs;
+  ta.g_lut = sc->d_lut;
+  ta.n_lut = sc->n_lut;
+  ta.sub = d_tab;
+  ta.N = N;
+  ta.seed = params->seed;
+  ta.K = K;
+  ta.I0 = params->peak_power_w;
+  ta.eq2 = params->beam_waist_m > 0.0 ? 1 : 0;
+  ta.w0 = params->beam_waist_m;
+  ta.lambda_m = params->wavelength_nm * 1e-9;
+  ta.R0 = params->focus_range_m;
+  ta.err_flag = d_err;
+  ta.counters = d_cnt;
+
+  WaveArgs wa{};
+  wa.N = N;
+  wa.n_bins = d.n_bins;
+  wa.taps = d.taps;
+  wa.jstar = d.jstar;
+  wa.kernel = d_ker;
+  wa.delta_ns = params->bin_width_ns;
+  wa.thr = params->detection_threshold;
+  wa.max_returns = R;
+  wa.counters = counters ? d_cnt + 4 : nullptr;
+
+  const float* org = (const float*)arrs[0].dev;
+  const float* dir = (const float*)arrs[1].dev;
+  const double* tim = (const double*)arrs[2].dev;
+  uint8_t* nret = (uint8_t*)arrs[3].dev;
+  helios_return* rets = (helios_return*)arrs[4].dev;
+  int64_t* k0 = (int64_t*)arrs[5].dev;
+  float* wf = (float*)arrs[6].dev;
+  helios_subray_hit* hits = (helios_subray_hit*)arrs[7].dev;
+
+  // per-kernel device time (CUDA events on the launching stream)
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    if (!stats) return;
+    cudaEvent_t x;
+    if (cudaEventCreate(&x) == cudaSuccess) {
+      cudaEventRecord(x, s);
+      ev.push_back(x);
+    }
+  };
+  uint32_t launches = 0;
+  for (uint64_t b = 0; b < n && e == cudaSuccess; b += chunk) {
+    const uint64_t m = std::min(chunk, n - b);
+    ta.origin = org + 3 * b;
+    ta.direction = dir + 3 * b;
+    ta.n_pulses = m;
+    ta.pulse_base = pulses->pulse_index_base + b;
+    ta.out = own_rec ? d_rec : hits + b * N;
+    mark();
+    e = launch_trace(ta, counters, s);
+    if (e != cudaSuccess) break;
+    mark();
+    wa.rec = ta.out;
+    wa.n_pulses = m;
+    wa.time_s = tim ? tim + b : nullptr;
+    wa.n_returns = nret + b;
+    wa.returns = rets + b * R;
+    wa.first_bin = k0 + b;
+    wa.waveform = wf ? wf + b * (uint64_t)d.n_bins : nullptr;
+    e = launch_waveform(wa, s);
+    mark();
+    launches += 2;
+  }
+  unsigned herr = 0;
+  unsigned long long hcnt[8] = {0};
+  if (e == cudaSuccess) {
+    for (Arr& a : arrs)
+      if (a.staged && !a.in && a.dev) {
+        e = cudaMemcpyAsync(const_cast<void*>(a.user), a.dev, a.bytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) break;
+      }
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && counters)
+    e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  double t_trace = 0.0, t_wave = 0.0;
+  for (size_t i = 0; i + 2 < ev.size(); i += 3) {
+    float a = 0.f, b2 = 0.f;
+    if (cudaEventElapsedTime(&a, ev[i], ev[i + 1]) == cudaSuccess &&
+        cudaEventElapsedTime(&b2, ev[i + 1], ev[i + 2]) == cudaSuccess) {
+      t_trace += a;
+      t_wave += b2;
+    }
+  }
+  for (cudaEvent_t x : ev) cudaEventDestroy(x);
+  cudaGetLastError();
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "helios_simulate");
+  if (stats) {
+    stats->pulses = n;
+    stats->subrays = n * N;
+    stats->kernel_launches = launches;
+    stats->trace_ms = t_trace;
+    stats->waveform_ms = t_wave;
+    stats->nodes_visited = hcnt[0];
+    stats->tris_tested = hcnt[1];
+    stats->voxel_steps = hcnt[2];
+    stats->voxel_returns = hcnt[3];
+    stats->subray_hits = hcnt[4];
+    stats->returns = hcnt[5];
+  }
+  if (herr) return fail(HELIOS_ERR_INVALID_ARGUMENT, "a pulse direction has zero length");
+  return HELIOS_OK;
+}
+
+}  // extern "C"

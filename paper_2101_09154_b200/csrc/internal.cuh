@@ -1,0 +1,121 @@
+// internal.cuh -- shared declarations of libhelios (not part of the ABI).
+//
+// Layout in HBM (DESIGN.md s.6):
+//   triangles  : TriRecord[n_tris] in LBVH leaf order, 48 B = 3 x float4
+//                { v0.xyz, bits(original id) } { v1.xyz, reflectance } { v2.xyz, 0 }
+//   nodes      : Node[n_tris - 1] child-pair nodes, 64 B = 4 x float4
+//                { c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y }
+//                { c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y }
+//                { c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z }
+//                { bits(ref0), bits(ref1), 0, 0 }
+//                ref >= 0: internal node index; ref < 0: leaf, see leaf_ref().
+//   voxel grid : PAD float[nz][ny][nx] (x fastest).
+//   subray rec : helios_subray_hit[n_pulses][N] (16 B), K6 -> K7.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/helios.h"
+
+namespace helios {
+
+constexpr int kMaxSubrays = 512;      // >= largest supported count (279)
+constexpr int kStackSize = 64;        // LBVH depth bound (checked at build)
+constexpr int kLeafMax = 4;           // triangles per collapsed leaf
+constexpr int kMaxLut = 4096;
+constexpr int kMaxTaps = 8192;        // L_p bound (validated)
+constexpr double kC = 299792458.0;    // m/s
+constexpr double kPi = 3.14159265358979323846;
+
+struct __align__(16) TriRecord {
+  float4 a, b, c;
+};
+struct __align__(16) Node {
+  float4 xy0, xy1, z01, ref;
+};
+
+// leaf reference: bit 31 set, bits [3,31) = first triangle, bits [0,3) = count-1
+__host__ __device__ inline int32_t leaf_ref(uint32_t first, uint32_t count) {
+  return (int32_t)(0x80000000u | (first << 3) | (count - 1u));
+}
+__host__ __device__ inline bool ref_is_leaf(int32_t r) { return r < 0; }
+__host__ __device__ inline uint32_t leaf_first(int32_t r) {
+  return ((uint32_t)r & 0x7FFFFFFFu) >> 3;
+}
+__host__ __device__ inline uint32_t leaf_count(int32_t r) { return ((uint32_t)r & 7u) + 1u; }
+constexpr int32_t kEmptyRef = 0x7FFFFFFF;  // never-hit child (box is inverted)
+
+// Per-subray constants of the beam pattern (R2, R4, R5), fp64.
+struct SubrayConst {
+  double cos_t;     // cos(theta_i)
+  double a;         // sin(theta_i) cos(phi)
+  double b;         // sin(theta_i) sin(phi)
+  double sin_t;     // sin(theta_i)  (r = R sin theta_i)
+  double w_far;     // far-field weight exp(-2 sin^2 theta / tan^2 beta) (R5)
+  double pad_[3];
+};
+
+// Everything a trace launch needs, passed by value (kernel parameter space).
+struct TraceArgs {
+  const TriRecord* tris;
+  const Node* nodes;
+  int32_t root;          // root node ref (internal index or leaf ref)
+  uint32_t n_tris;
+  const float* pad;      // voxel grid or nullptr
+  uint32_t nx, ny, nz;
+  double gx0, gy0, gz0, vs;
+  const float* g_lut;
+  uint32_t n_lut;
+  const SubrayConst* sub;
+  uint32_t N;            // subrays per pulse
+  const float* origin;   // [n][3]
+  const float* direction;
+  uint64_t n_pulses;
+  uint64_t pulse_base;
+  uint64_t seed;
+  double K;              // lambda alpha^2 / (4 pi beta^2)    (Eq. 7)
+  double I0;
+  int eq2;               // 1: Eq. 2 beam width; 0: far field
+  double w0, lambda_m, R0;
+  helios_subray_hit* out;  // [n][N]
+  unsigned int* err_flag;  // set on zero-length direction
+  unsigned long long* counters;  // instrumented variant: [nodes, tris, voxel steps, voxel returns]
+};
+
+struct WaveArgs {
+  const helios_subray_hit* rec;  // [n][N]
+  uint32_t N;
+  uint64_t n_pulses;
+  uint32_t n_bins;
+  uint32_t taps;                 // L_p
+  uint32_t jstar;                // argmax of the binned pulse (R12)
+  const double* kernel;          // p[j], j < taps
+  double delta_ns;               // bin width Delta
+  float thr;
+  uint32_t max_returns;
+  const double* time_s;          // may be nullptr
+  uint8_t* n_returns;
+  helios_return* returns;
+  int64_t* first_bin;
+  float* waveform;               // may be nullptr
+  unsigned long long* counters;  // [subray hits, returns] or nullptr
+};
+
+// launchers (trace.cu / waveform.cu)
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s);
+cudaError_t launch_waveform(const WaveArgs& a, cudaStream_t s);
+int waveform_warps(uint32_t n_bins, uint32_t N, uint32_t taps);
+
+// LBVH build (lbvh.cu)
+struct BuildResult {
+  TriRecord* tris;   // device, leaf order
+  Node* nodes;       // device
+  uint32_t n_nodes;
+  int32_t root;
+  uint32_t max_depth;
+  float ms;
+};
+cudaError_t build_lbvh(const float* d_tri_xyz, const float* d_refl, uint32_t n,
+                       cudaStream_t s, BuildResult* out, char* err, size_t err_len);
+
+}  // namespace helios

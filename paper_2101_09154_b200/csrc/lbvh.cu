@@ -1,0 +1,367 @@
+// lbvh.cu -- on-device LBVH build (helios_build_accel).
+//
+// Replaces the paper's CPU kd-tree (Sec. 5.1: recursive search,
+// x/y/z split cycling by depth) with a linear BVH built entirely on the GPU:
+//   K1 centroid bounds (block reduce + ordered-int atomics)
+//   K1 30-bit Morton codes (10 bits per axis over the centroid AABB)
+//   K2 radix sort of (code, index)   [CUB onesweep, library sort]
+//   K3 Karras hierarchy: N-1 internal nodes, delta = clz(code_i ^ code_j),
+//      index tie-break (32 + clz(i ^ j)) for duplicate codes
+//   K4 bottom-up AABB refit (second-arriving child computes the parent)
+//   K5 layout: 64-B child-pair nodes, subtrees of <= kLeafMax triangles
+//      collapsed into leaves, triangles permuted to leaf order (48 B).
+// fp32 min/max of fp32 vertices is exact, so every box contains its
+// triangles exactly; traversal adds the conservative slack (trace.cu).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdio>
+
+#include "internal.cuh"
+
+namespace helios {
+namespace {
+
+__device__ __forceinline__ unsigned f2ord(float f) {
+  unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+__global__ void k_centroid_bounds(const float* __restrict__ xyz, uint32_t n,
+                                  unsigned* __restrict__ bounds /* [6] ordered */) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float* t = xyz + 9ull * i;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float c = (t[a] + t[3 + a] + t[6 + a]) * (1.0f / 3.0f);
+      lo[a] = fminf(lo[a], c);
+      hi[a] = fmaxf(hi[a], c);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(bounds + a, f2ord(lo[a]));
+      atomicMax(bounds + 3 + a, f2ord(hi[a]));
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t expand10(uint32_t v) {
+  v = (v * 0x00010001u) & 0xFF0000FFu;
+  v = (v * 0x00000101u) & 0x0F00F00Fu;
+  v = (v * 0x00000011u) & 0xC30C30C3u;
+  v = (v * 0x00000005u) & 0x49249249u;
+  return v;
+}
+
+__global__ void k_morton(const float* __restrict__ xyz, uint32_t n,
+                         const unsigned* __restrict__ bounds, uint32_t* __restrict__ codes,
+                         uint32_t* __restrict__ idx) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* t = xyz + 9ull * i;
+  uint32_t q[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float lo = ord2f(bounds[a]), hi = ord2f(bounds[3 + a]);
+    float c = (t[a] + t[3 + a] + t[6 + a]) * (1.0f / 3.0f);
+    float ext = hi - lo;
+    float f = ext > 0.0f ? (c - lo) / ext : 0.0f;
+    int k = (int)(f * 1024.0f);
+    q[a] = (uint32_t)min(max(k, 0), 1023);
+  }
+  codes[i] = (expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]);
+  idx[i] = i;
+}
+
+__device__ __forceinline__ int delta(const uint32_t* __restrict__ codes, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  uint32_t a = codes[i], b = codes[j];
+  if (a == b) return 32 + __clz((unsigned)(i ^ j));
+  return __clz(a ^ b);
+}
+
+// Karras 2012 hierarchy: internal node i covers [first, last]; split gamma.
+// child encoding: >= 0 internal node, < 0 sorted leaf ~k.
+__global__ void k_karras(const uint32_t* __restrict__ codes, int n, int* __restrict__ child,
+                         int* __restrict__ parent_int, int* __restrict__ parent_leaf,
+                         int* __restrict__ range) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int d = (delta(codes, n, i, i + 1) - delta(codes, n, i, i - 1)) >= 0 ? 1 : -1;
+  int dmin = delta(codes, n, i, i - d);
+  int lmax = 2;
+  while (delta(codes, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (delta(codes, n, i, i + (l + t) * d) > dmin) l += t;
+  int j = i + l * d;
+  int dnode = delta(codes, n, i, j);
+  int s = 0;
+  int t = l;
+  do {
+    t = (t + 1) >> 1;
+    if (delta(codes, n, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  int gamma = i + s * d + min(d, 0);
+  int first = min(i, j), last = max(i, j);
+  int left = (first == gamma) ? ~gamma : gamma;
+  int right = (last == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+  child[2 * i] = left;
+  child[2 * i + 1] = right;
+  range[2 * i] = first;
+  range[2 * i + 1] = last;
+  if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
+  if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
+  if (i == 0) parent_int[0] = -1;
+}
+
+struct Box {
+  float lo[3], hi[3];
+};
+
+__device__ __forceinline__ Box tri_box(const float* __restrict__ xyz, uint32_t src) {
+  const float* t = xyz + 9ull * src;
+  Box b;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = fminf(fminf(t[a], t[3 + a]), t[6 + a]);
+    b.hi[a] = fmaxf(fmaxf(t[a], t[3 + a]), t[6 + a]);
+  }
+  return b;
+}
+
+__device__ __forceinline__ Box load_box_cg(const float* p) {
+  Box b;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = __ldcg(p + a);
+    b.hi[a] = __ldcg(p + 3 + a);
+  }
+  return b;
+}
+__device__ __forceinline__ void store_box(float* p, const Box& b) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    __stcg(p + a, b.lo[a]);
+    __stcg(p + 3 + a, b.hi[a]);
+  }
+}
+
+__global__ void k_refit(const float* __restrict__ xyz, const uint32_t* __restrict__ sorted_idx,
+                        int n, const int* __restrict__ child, const int* __restrict__ parent_int,
+                        const int* __restrict__ parent_leaf, float* __restrict__ leafbox,
+                        float* __restrict__ nodebox, unsigned* __restrict__ flags) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  Box b = tri_box(xyz, sorted_idx[k]);
+  store_box(leafbox + 6ull * k, b);
+  __threadfence();
+  int p = parent_leaf[k];
+  while (p >= 0) {
+    if (atomicAdd(flags + p, 1u) == 0u) return;  // first arrival: sibling finishes
+    __threadfence();
+    Box u;
+    int c0 = child[2 * p], c1 = child[2 * p + 1];
+    Box b0 = load_box_cg(c0 < 0 ? leafbox + 6ull * (~c0) : nodebox + 6ull * c0);
+    Box b1 = load_box_cg(c1 < 0 ? leafbox + 6ull * (~c1) : nodebox + 6ull * c1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      u.lo[a] = fminf(b0.lo[a], b1.lo[a]);
+      u.hi[a] = fmaxf(b0.hi[a], b1.hi[a]);
+    }
+    store_box(nodebox + 6ull * p, u);
+    __threadfence();
+    p = parent_int[p];
+  }
+}
+
+__device__ __forceinline__ int32_t make_ref(int c, const int* __restrict__ range) {
+  if (c < 0) return leaf_ref((uint32_t)(~c), 1u);
+  int first = range[2 * c], last = range[2 * c + 1];
+  int size = last - first + 1;
+  if (size <= kLeafMax) return leaf_ref((uint32_t)first, (uint32_t)size);
+  return c;
+}
+
+__global__ void k_layout(int n, const int* __restrict__ child, const int* __restrict__ range,
+                         const float* __restrict__ leafbox, const float* __restrict__ nodebox,
+                         Node* __restrict__ nodes) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int c0 = child[2 * i], c1 = child[2 * i + 1];
+  const float* b0 = c0 < 0 ? leafbox + 6ull * (~c0) : nodebox + 6ull * c0;
+  const float* b1 = c1 < 0 ? leafbox + 6ull * (~c1) : nodebox + 6ull * c1;
+  Node nd;
+  nd.xy0 = make_float4(b0[0], b0[3], b0[1], b0[4]);
+  nd.xy1 = make_float4(b1[0], b1[3], b1[1], b1[4]);
+  nd.z01 = make_float4(b0[2], b0[5], b1[2], b1[5]);
+  nd.ref = make_float4(__int_as_float(make_ref(c0, range)), __int_as_float(make_ref(c1, range)),
+                       0.0f, 0.0f);
+  nodes[i] = nd;
+}
+
+// depth (internal nodes on the path from the root) of every non-collapsed node
+__global__ void k_depth(int n, const int* __restrict__ range, const int* __restrict__ parent_int,
+                        unsigned* __restrict__ max_depth) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  if (range[2 * i + 1] - range[2 * i] + 1 <= kLeafMax) return;  // collapsed into a leaf
+  unsigned d = 1;
+  for (int p = parent_int[i]; p >= 0; p = parent_int[p]) ++d;
+  atomicMax(max_depth, d);
+}
+
+__global__ void k_permute(const float* __restrict__ xyz, const float* __restrict__ refl,
+                          const uint32_t* __restrict__ sorted_idx, uint32_t n,
+                          TriRecord* __restrict__ out) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  uint32_t src = sorted_idx[k];
+  const float* t = xyz + 9ull * src;
+  float r = refl ? refl[src] : 0.5f;
+  TriRecord rec;
+  rec.a = make_float4(t[0], t[1], t[2], __uint_as_float(src));
+  rec.b = make_float4(t[3], t[4], t[5], r);
+  rec.c = make_float4(t[6], t[7], t[8], 0.0f);
+  out[k] = rec;
+}
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), s);
+}
+
+}  // namespace
+
+cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStream_t s,
+                       BuildResult* out, char* err, size_t err_len) {
+  out->tris = nullptr;
+  out->nodes = nullptr;
+  out->n_nodes = 0;
+  out->root = kEmptyRef;
+  out->max_depth = 0;
+  out->ms = 0.f;
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  unsigned* bounds = nullptr;
+  uint32_t *codes = nullptr, *idx = nullptr, *codes_s = nullptr, *idx_s = nullptr;
+  int *child = nullptr, *parent_int = nullptr, *parent_leaf = nullptr, *range = nullptr;
+  float *leafbox = nullptr, *nodebox = nullptr;
+  unsigned *flags = nullptr, *dmax = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  const int T = 256;
+  const unsigned nb = (n + T - 1) / T;
+  const unsigned ni = n > 1 ? (n - 1 + T - 1) / T : 1;
+  unsigned init_bounds[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
+  unsigned hdepth = 0;
+
+#define CK(x)                 \
+  do {                        \
+    e = (x);                  \
+    if (e != cudaSuccess) {   \
+      snprintf(err, err_len, "build_lbvh: %s at %s:%d", cudaGetErrorString(e), __FILE__, __LINE__); \
+      goto done;              \
+    }                         \
+  } while (0)
+
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  CK(dalloc(&bounds, 6, s));
+  CK(cudaMemcpyAsync(bounds, init_bounds, sizeof(init_bounds), cudaMemcpyHostToDevice, s));
+  CK(dalloc(&codes, n, s));
+  CK(dalloc(&idx, n, s));
+  CK(dalloc(&codes_s, n, s));
+  CK(dalloc(&idx_s, n, s));
+  CK(dalloc(&out->tris, n, s));
+  k_centroid_bounds<<<min(nb, 148u * 8u), T, 0, s>>>(xyz, n, bounds);
+  CK(cudaGetLastError());
+  k_morton<<<nb, T, 0, s>>>(xyz, n, bounds, codes, idx);
+  CK(cudaGetLastError());
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0,
+                                     30, s));
+  CK(cudaMallocAsync(&temp, temp_bytes ? temp_bytes : 1, s));
+  CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0, 30,
+                                     s));
+  if (n <= (uint32_t)kLeafMax) {
+    out->root = leaf_ref(0, n);
+    out->max_depth = 0;
+  } else {
+    CK(dalloc(&child, 2ull * (n - 1), s));
+    CK(dalloc(&range, 2ull * (n - 1), s));
+    CK(dalloc(&parent_int, n - 1, s));
+    CK(dalloc(&parent_leaf, n, s));
+    CK(dalloc(&leafbox, 6ull * n, s));
+    CK(dalloc(&nodebox, 6ull * (n - 1), s));
+    CK(dalloc(&flags, n - 1, s));
+    CK(dalloc(&dmax, 1, s));
+    CK(cudaMemsetAsync(flags, 0, sizeof(unsigned) * (n - 1), s));
+    CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned), s));
+    CK(dalloc(&out->nodes, n - 1, s));
+    k_karras<<<ni, T, 0, s>>>(codes_s, (int)n, child, parent_int, parent_leaf, range);
+    CK(cudaGetLastError());
+    k_refit<<<nb, T, 0, s>>>(xyz, idx_s, (int)n, child, parent_int, parent_leaf, leafbox, nodebox,
+                             flags);
+    CK(cudaGetLastError());
+    k_layout<<<ni, T, 0, s>>>((int)n, child, range, leafbox, nodebox, out->nodes);
+    CK(cudaGetLastError());
+    k_depth<<<ni, T, 0, s>>>((int)n, range, parent_int, dmax);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&hdepth, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    out->n_nodes = n - 1;
+    out->root = 0;
+  }
+  k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s, n, out->tris);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaEventElapsedTime(&out->ms, e0, e1));
+  if (n > (uint32_t)kLeafMax) out->max_depth = hdepth;
+  if (out->max_depth > (uint32_t)kStackSize) {
+    snprintf(err, err_len, "build_lbvh: tree depth %u exceeds the traversal stack (%d)",
+             out->max_depth, kStackSize);
+    e = cudaErrorInvalidValue;
+  }
+#undef CK
+done:
+  cudaFreeAsync(bounds, s);
+  cudaFreeAsync(codes, s);
+  cudaFreeAsync(idx, s);
+  cudaFreeAsync(codes_s, s);
+  cudaFreeAsync(idx_s, s);
+  cudaFreeAsync(temp, s);
+  cudaFreeAsync(child, s);
+  cudaFreeAsync(range, s);
+  cudaFreeAsync(parent_int, s);
+  cudaFreeAsync(parent_leaf, s);
+  cudaFreeAsync(leafbox, s);
+  cudaFreeAsync(nodebox, s);
+  cudaFreeAsync(flags, s);
+  cudaFreeAsync(dmax, s);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(out->tris, s);
+    cudaFreeAsync(out->nodes, s);
+    out->tris = nullptr;
+    out->nodes = nullptr;
+  }
+  cudaStreamSynchronize(s);
+  return e;
+}
+
+}  // namespace helios

@@ -1,0 +1,334 @@
+// trace.cu -- K6: subray fan-out + nearest hit + transmissive voxels + radiometry.
+//
+// One thread per (pulse, subray), subray fastest, so the lanes of a warp
+// carry the nearly-parallel subrays of one or two pulses and
+// walk the same BVH nodes: coherent float4 node loads served from L1.
+//
+// Precision contract (DESIGN.md s.3 C-0):
+//   * subray directions in fp64 (P:199 pattern, R2/R4 frame);
+//   * BVH boxes tested in fp32 with a conservative relative slack, so the
+//     fp32 ray never culls a box the fp64 ray enters;
+//   * every leaf triangle is decided by fp64 Moller-Trumbore on the fp32
+//     vertices (the exact definition the oracle uses), nearest by fp64 t,
+//     exact ties -> lower primitive id (R22);
+//   * the voxel march (3D-DDA) computes each plane crossing directly in fp64
+//     (no accumulated increments), chord lengths, exp(-sigma L), -ln(u)/sigma
+//     in fp64 (R17-R20);
+//   * range, Eq. 1/2 intensity and Eq. 7 amplitude in fp64 (R5, R14, R16).
+#include <math.h>
+
+#include "internal.cuh"
+#include "philox.cuh"
+
+namespace helios {
+namespace {
+
+constexpr float kBoxSlack = 1e-6f;  // >> 4 * 2^-24 relative error of an fp32 slab value
+
+struct D3 {
+  double x, y, z;
+};
+__device__ __forceinline__ D3 d3(double x, double y, double z) { return {x, y, z}; }
+__device__ __forceinline__ D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ D3 cross(D3 a, D3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+__device__ __forceinline__ float safe_inv(float d) {
+  // a zero component would give (b - o) * inf = NaN on a box face through the
+  // origin; 1e-30 keeps the slab finite and the test conservative
+  return 1.0f / (fabsf(d) < 1e-30f ? copysignf(1e-30f, d) : d);
+}
+
+// Slab test of one child box; returns the entry distance (or +inf on a miss).
+__device__ __forceinline__ float box_enter(float lox, float hix, float loy, float hiy, float loz,
+                                           float hiz, float ox, float oy, float oz, float ix,
+                                           float iy, float iz, float tbest) {
+  const float tx0 = (lox - ox) * ix, tx1 = (hix - ox) * ix;
+  const float ty0 = (loy - oy) * iy, ty1 = (hiy - oy) * iy;
+  const float tz0 = (loz - oz) * iz, tz1 = (hiz - oz) * iz;
+  const float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+  const float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tbest));
+  return (tmin * (1.0f - kBoxSlack) <= tmax * (1.0f + kBoxSlack)) ? tmin : INFINITY;
+}
+
+// fp64 Moller-Trumbore (the oracle's definition, R21): t or -1.
+__device__ __forceinline__ double mt64(const D3& o, const D3& d, const TriRecord& tr) {
+  const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
+  const D3 e1 = sub(d3(tr.b.x, tr.b.y, tr.b.z), v0);
+  const D3 e2 = sub(d3(tr.c.x, tr.c.y, tr.c.z), v0);
+  const D3 p = cross(d, e2);
+  const double det = dot(e1, p);
+  // |det| <= 1e-12 |e1||e2|, squared to avoid two square roots
+  if (det * det <= 1e-24 * dot(e1, e1) * dot(e2, e2)) return -1.0;
+  const double inv = 1.0 / det;
+  const D3 s = sub(o, v0);
+  const double u = dot(s, p) * inv;
+  if (u < 0.0 || u > 1.0) return -1.0;
+  const D3 q = cross(s, e1);
+  const double v = dot(d, q) * inv;
+  if (v < 0.0 || u + v > 1.0) return -1.0;
+  const double t = dot(e2, q) * inv;
+  return t > 0.0 ? t : -1.0;
+}
+
+__device__ __forceinline__ TriRecord load_tri(const TriRecord* __restrict__ t, uint32_t k) {
+  TriRecord r;
+  r.a = __ldg(&t[k].a);
+  r.b = __ldg(&t[k].b);
+  r.c = __ldg(&t[k].c);
+  return r;
+}
+
+__device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, double o, double d) {
+  // crossing of plane org + k vs, computed directly (same arithmetic as the
+  // oracle's plane enumeration; intrinsics forbid FMA contraction)
+  return (__dadd_rn(org, __dmul_rn((double)k, vs)) - o) / d;
+}
+
+template <bool INSTR>
+__global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
+  const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t total = a.n_pulses * (uint64_t)a.N;
+  if (gid >= total) return;
+  const uint64_t p = gid / a.N;
+  const uint32_t s = (uint32_t)(gid - p * a.N);
+  unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0;
+
+  helios_subray_hit rec;
+  rec.range_m = __longlong_as_double(0x7FF8000000000000ll);  // NaN
+  rec.amplitude = 0.0f;
+  rec.prim_id = 0xFFFFFFFFu;
+
+  // ---- A2: subray fan-out (R2, R4), fp64
+  const float ox = __ldg(a.origin + 3 * p), oy = __ldg(a.origin + 3 * p + 1),
+              oz = __ldg(a.origin + 3 * p + 2);
+  double dx = __ldg(a.direction + 3 * p), dy = __ldg(a.direction + 3 * p + 1),
+         dz = __ldg(a.direction + 3 * p + 2);
+  const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+  if (!(dn > 0.0) || !isfinite(dn)) {
+    if (s == 0) atomicOr(a.err_flag, 1u);
+    a.out[gid] = rec;
+    return;
+  }
+  {
+    const double r = 1.0 / dn;
+    dx *= r;
+    dy *= r;
+    dz *= r;
+  }
+  double ux, uy, uz;
+  if (fabs(dz) > 0.9) {  // a = x: u = x cross d
+    ux = 0.0;
+    uy = -dz;
+    uz = dy;
+  } else {  // a = z: u = z cross d
+    ux = -dy;
+    uy = dx;
+    uz = 0.0;
+  }
+  {
+    const double r = 1.0 / sqrt(ux * ux + uy * uy + uz * uz);
+    ux *= r;
+    uy *= r;
+    uz *= r;
+  }
+  const double vx = dy * uz - dz * uy, vy = dz * ux - dx * uz, vz = dx * uy - dy * ux;
+  const SubrayConst sc = a.sub[s];
+  const D3 D = d3(sc.cos_t * dx + sc.a * ux + sc.b * vx, sc.cos_t * dy + sc.a * uy + sc.b * vy,
+                  sc.cos_t * dz + sc.a * uz + sc.b * vz);
+  const D3 O = d3(ox, oy, oz);
+
+  // ---- A3: nearest triangle (LBVH; fp32 boxes, fp64 decisions)
+  double t_best = INFINITY;
+  uint32_t best_id = 0xFFFFFFFFu, best_k = 0;
+  if (a.n_tris > 0) {
+    const float ix = safe_inv((float)D.x), iy = safe_inv((float)D.y), iz = safe_inv((float)D.z);
+    int32_t stack[kStackSize];
+    int sp = 0;
+    int32_t ref = a.root;
+    for (;;) {
+      if (ref_is_leaf(ref)) {
+        const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
+        for (uint32_t k = first; k < first + cnt; ++k) {
+          const TriRecord tr = load_tri(a.tris, k);
+          if (INSTR) ++c_tris;
+          const double t = mt64(O, D, tr);
+          if (t > 0.0) {
+            const uint32_t id = __float_as_uint(tr.a.w);
+            if (t < t_best || (t == t_best && id < best_id)) {
+              t_best = t;
+              best_id = id;
+              best_k = k;
+            }
+          }
+        }
+        if (sp == 0) break;
+        ref = stack[--sp];
+        continue;
+      }
+      const Node* nd = a.nodes + ref;
+      const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
+                   rf = __ldg(&nd->ref);
+      if (INSTR) ++c_nodes;
+      const float tb = (float)t_best;
+      const float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, ox, oy, oz, ix, iy, iz, tb);
+      const float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, ox, oy, oz, ix, iy, iz, tb);
+      const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
+      const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
+      if (h0 && h1) {
+        const bool near0 = t0 <= t1;
+        ref = near0 ? r0 : r1;
+        stack[sp++] = near0 ? r1 : r0;
+      } else if (h0) {
+        ref = r0;
+      } else if (h1) {
+        ref = r1;
+      } else {
+        if (sp == 0) break;
+        ref = stack[--sp];
+      }
+    }
+  }
+
+  // ---- A4: transmissive voxels before the triangle hit
+  bool vox_hit = false;
+  double t_vox = 0.0, sigma_vox = 0.0;
+  uint32_t vox_id = 0;
+  if (a.pad != nullptr) {
+    const double org[3] = {a.gx0, a.gy0, a.gz0};
+    const uint32_t nn[3] = {a.nx, a.ny, a.nz};
+    const double o3[3] = {O.x, O.y, O.z}, d3v[3] = {D.x, D.y, D.z};
+    double t_in = 0.0, t_out = (best_id != 0xFFFFFFFFu) ? t_best : INFINITY;
+    bool inside = true;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const double lo = org[ax], hi = org[ax] + (double)nn[ax] * a.vs;
+      if (d3v[ax] == 0.0) {
+        if (o3[ax] < lo || o3[ax] > hi) inside = false;
+        continue;
+      }
+      double ta = (lo - o3[ax]) / d3v[ax], tb = (hi - o3[ax]) / d3v[ax];
+      if (ta > tb) {
+        const double tmp = ta;
+        ta = tb;
+        tb = tmp;
+      }
+      t_in = fmax(t_in, ta);
+      t_out = fmin(t_out, tb);
+    }
+    if (inside && t_in < t_out) {
+      // G(|d_z|) (R15)
+      double G = 0.5;
+      if (a.g_lut != nullptr) {
+        const double x = fabs(D.z) * (double)(a.n_lut - 1);
+        int64_t k = (int64_t)floor(x);
+        k = k < 0 ? 0 : (k > (int64_t)a.n_lut - 2 ? (int64_t)a.n_lut - 2 : k);
+        const double f = x - (double)k;
+        G = (double)__ldg(a.g_lut + k) * (1.0 - f) + (double)__ldg(a.g_lut + k + 1) * f;
+      }
+      int idx[3];
+      double tn[3];
+      int stp[3];
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const double c = (o3[ax] + t_in * d3v[ax] - org[ax]) / a.vs;
+        int k = (int)floor(c);
+        k = k < 0 ? 0 : (k >= (int)nn[ax] ? (int)nn[ax] - 1 : k);
+        idx[ax] = k;
+        stp[ax] = d3v[ax] > 0.0 ? 1 : (d3v[ax] < 0.0 ? -1 : 0);
+        tn[ax] = stp[ax] > 0   ? plane_t(org[ax], (uint32_t)(k + 1), a.vs, o3[ax], d3v[ax])
+                 : stp[ax] < 0 ? plane_t(org[ax], (uint32_t)k, a.vs, o3[ax], d3v[ax])
+                               : INFINITY;
+      }
+      double t_cur = t_in;
+      for (;;) {
+        const int ax = (tn[0] <= tn[1] && tn[0] <= tn[2]) ? 0 : (tn[1] <= tn[2] ? 1 : 2);
+        const double t_exit = tn[ax];
+        const double t_end = fmin(t_exit, t_out);
+        const double L = t_end - t_cur;
+        if (INSTR) ++c_vox;
+        if (L > 0.0) {
+          const uint32_t id = (uint32_t)idx[0] + a.nx * ((uint32_t)idx[1] + a.ny * (uint32_t)idx[2]);
+          const float pad = __ldg(a.pad + id);
+          if (pad > 0.0f) {
+            const double sigma = (double)pad * G;  // Eq. 4 via the G LUT
+            const double u = transmission_u(a.seed, a.pulse_base + p, s, id);
+            if (!(u < exp(-sigma * L))) {  // s = -ln(u)/sigma <= L: echo (R17)
+              vox_hit = true;
+              t_vox = t_cur + (-log(u)) / sigma;  // Eq. 6
+              sigma_vox = sigma;
+              vox_id = id;
+              if (INSTR) ++c_voxret;
+              break;
+            }
+          }
+        }
+        if (t_exit >= t_out) break;
+        idx[ax] += stp[ax];
+        if (idx[ax] < 0 || idx[ax] >= (int)nn[ax]) break;
+        tn[ax] = plane_t(org[ax], (uint32_t)(stp[ax] > 0 ? idx[ax] + 1 : idx[ax]), a.vs, o3[ax],
+                         d3v[ax]);
+        t_cur = t_exit;
+      }
+    }
+  }
+
+  // ---- A5: range + radiometry (Eq. 1, 2, 7; R5, R14, R16)
+  double R = 0.0, sig_eff = 0.0;
+  uint32_t pid = 0xFFFFFFFFu;
+  if (vox_hit) {
+    R = t_vox;
+    sig_eff = sigma_vox;
+    pid = a.n_tris + vox_id;
+  } else if (best_id != 0xFFFFFFFFu) {
+    const TriRecord tr = load_tri(a.tris, best_k);
+    const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
+    const D3 n = cross(sub(d3(tr.b.x, tr.b.y, tr.b.z), v0), sub(d3(tr.c.x, tr.c.y, tr.c.z), v0));
+    const double cos_inc = fabs(dot(n, D)) / (sqrt(dot(n, n)) * sqrt(dot(D, D)));
+    R = t_best;
+    sig_eff = (double)tr.b.w * cos_inc;
+    pid = best_id;
+  }
+  if (pid != 0xFFFFFFFFu) {
+    double I;
+    if (a.eq2) {
+      const double r = R * sc.sin_t;
+      const double om = a.lambda_m * R / (kPi * a.w0 * a.w0);
+      const double om0 = a.lambda_m * a.R0 / (kPi * a.w0 * a.w0);
+      const double w = a.w0 * sqrt(om0 * om0 + om * om);
+      I = (r == 0.0) ? a.I0 : a.I0 * exp(-2.0 * r * r / (w * w));
+    } else {
+      I = a.I0 * sc.w_far;
+    }
+    rec.range_m = R;
+    rec.amplitude = (float)(a.K * sig_eff * I / (R * R * R * R));
+    rec.prim_id = pid;
+  }
+  a.out[gid] = rec;
+
+  if (INSTR) {
+    atomicAdd(a.counters + 0, c_nodes);
+    atomicAdd(a.counters + 1, c_tris);
+    atomicAdd(a.counters + 2, c_vox);
+    atomicAdd(a.counters + 3, c_voxret);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) {
+  const uint64_t total = a.n_pulses * (uint64_t)a.N;
+  if (total == 0) return cudaSuccess;
+  const unsigned T = 128;
+  const uint64_t blocks = (total + T - 1) / T;
+  if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  if (instrumented)
+    k_trace<true><<<(unsigned)blocks, T, 0, s>>>(a);
+  else
+    k_trace<false><<<(unsigned)blocks, T, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace helios

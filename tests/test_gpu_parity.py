@@ -1,0 +1,79 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element
+by element on the same seeded inputs (DESIGN.md s.4, rules C-4)."""
+import numpy as np
+import pytest
+
+from parity import compare, gpu_invariants
+from gpu_util import gpu_run, oracle_run, take, workload
+
+pytestmark = pytest.mark.gpu
+
+
+def _parity(w, start, count, sample=None, params=None, seed=0):
+    g = gpu_run(w, start, count, params=params)
+    p = params or w.params
+    errs = gpu_invariants(g, p.max_returns, p.detection_threshold)
+    assert not errs, errs
+    if sample is None:
+        idx = np.arange(count)
+    else:
+        rng = np.random.default_rng(seed)
+        idx = np.unique(np.concatenate([np.arange(min(count, 64)),
+                                        rng.choice(count, min(sample, count), replace=False),
+                                        [count - 1]]))
+    o = oracle_run(w, start + idx, params=params)
+    rep = compare(take(g, idx), o, w.scene.n_tris, p.bin_width_ns)
+    print(rep.summary())
+    assert rep.ok(), rep.summary()
+    hits = (o.sub_prim != 0xFFFFFFFF).mean()
+    return rep, hits
+
+
+def test_c1_tiny_tls_plane_all_pulses():
+    w = workload("C1")
+    rep, hits = _parity(w, 0, w.n_pulses)
+    assert 0.5 < hits < 1.0  # zenith 100 deg rays reach past the square: some misses
+    assert sum(rep.exempt_pulses.values()) <= 0.01 * rep.pulses
+
+
+def test_c2_als_dtm_reduced():
+    w = workload("C2", 0.125)  # 64^2 DTM, 7938 triangles
+    rep, hits = _parity(w, 1000, 3001)
+    assert hits > 0.99
+
+
+def test_c3_tls_forest_reduced():
+    w = workload("C3", 0.03)
+    rep, hits = _parity(w, 2000, 2500)
+    assert hits > 0.3
+
+
+def test_c4_voxel_canopy_reduced():
+    w = workload("C4", 0.1)
+    rep, hits = _parity(w, 0, 20000, sample=4000)
+    assert rep.subrays > 0
+
+
+def test_c5_city_terrain_reduced_hex91_and_paper93():
+    w = workload("C5", 0.03)
+    _parity(w, 500, 1500)
+    from dataclasses import replace
+    p93 = replace(w.params, subray_count=93)
+    _parity(w, 500, 700, params=p93)
+
+
+def test_eq2_beam_width_and_g_lut():
+    # Eq. 2 (beam waist > 0) and a non-trivial G LUT on the voxel canopy
+    from dataclasses import replace
+    w = workload("C4", 0.1)
+    w2 = replace(w, scene=replace(w.scene, g_lut=np.linspace(0.3, 0.8, 17).astype(np.float32)))
+    p = replace(w.params, beam_waist_m=0.01, wavelength_nm=1550.0, focus_range_m=50.0,
+                subray_count=37, detection_threshold=0.02)
+    _parity(w2, 1000, 3000, params=p)
+
+
+def test_many_subrays_and_max_returns_cap():
+    from dataclasses import replace
+    w = workload("C3", 0.03)
+    p = replace(w.params, subray_count=279, max_returns=2, detection_threshold=0.01)
+    _parity(w, 3000, 400, params=p)
