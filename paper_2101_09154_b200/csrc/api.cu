@@ -101,9 +101,9 @@ std::vector<SubrayConst> subray_table(uint32_t count, double beta, Pattern pt) {
     SubrayConst c{};
     const double st = std::sin(theta);
     c.cos_t = std::cos(theta);
-    c.a = st * std::cos(phi);
-    c.b = st * std::sin(phi);
     c.sin_t = st;
+    c.cos_p = std::cos(phi);
+    c.sin_p = std::sin(phi);
     c.w_far = theta == 0.0 ? 1.0 : std::exp(-2.0 * st * st / (tb * tb));
     t.push_back(c);
   };
@@ -157,9 +157,9 @@ helios_status validate_params(const helios_scanner_params* p, Derived* d) {
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulse kernel of %g taps out of range", taps);
   d->n_bins = (uint32_t)nb;
   d->taps = (uint32_t)taps;
-  if (waveform_warps(d->n_bins, p->subray_count, d->taps) == 0)
+  if (!waveform_fits(d->n_bins, p->subray_count, d->taps))
     return fail(HELIOS_ERR_INVALID_ARGUMENT,
-                "n_bins %u does not fit the per-pulse shared-memory waveform", d->n_bins);
+                "pulse kernel / subray tables do not fit shared memory");
   d->kernel.resize(d->taps);
   double best = -1.0;
   for (uint32_t j = 0; j < d->taps; ++j) {
@@ -351,19 +351,15 @@ helios_status helios_scene_get_info(helios_scene sc, helios_scene_info* out) {
 }
 
 uint32_t helios_waveform_bins(const helios_scanner_params* params) {
+  g_err.clear();
   Derived d;
-  std::string keep = g_err;
-  const uint32_t r = validate_params(params, &d) == HELIOS_OK ? d.n_bins : 0;
-  g_err = keep;
-  return r;
+  return validate_params(params, &d) == HELIOS_OK ? d.n_bins : 0;
 }
 
 uint32_t helios_pulse_taps(const helios_scanner_params* params) {
+  g_err.clear();
   Derived d;
-  std::string keep = g_err;
-  const uint32_t r = validate_params(params, &d) == HELIOS_OK ? d.taps : 0;
-  g_err = keep;
-  return r;
+  return validate_params(params, &d) == HELIOS_OK ? d.taps : 0;
 }
 
 helios_status helios_simulate(helios_scene sc, const helios_scanner_params* params,
@@ -444,6 +440,12 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   unsigned* d_err = nullptr;
   unsigned long long* d_cnt = nullptr;
   helios_subray_hit* d_rec = nullptr;
+  double* d_wscratch = nullptr;
+  const WavePlan plan = plan_waveform(d.n_bins, N, d.taps);
+  if (plan.warps == 0) {
+    cleanup();
+    return fail(HELIOS_ERR_CUDA, "helios_simulate: waveform kernel cannot be configured");
+  }
   // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
   const uint64_t chunk = std::max<uint64_t>(1024, (48ull << 20) / (16ull * N));
   const bool own_rec = arrs[7].dev == nullptr;
@@ -453,6 +455,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   if (e == cudaSuccess) e = alloc((void**)&d_cnt, sizeof(unsigned long long) * 8);
   if (e == cudaSuccess && own_rec)
     e = alloc((void**)&d_rec, sizeof(helios_subray_hit) * N * std::min(n, chunk));
+  if (e == cudaSuccess) e = alloc((void**)&d_wscratch, plan.scratch_bytes);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_tab, tab.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
@@ -540,7 +543,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     wa.returns = rets + b * R;
     wa.first_bin = k0 + b;
     wa.waveform = wf ? wf + b * (uint64_t)d.n_bins : nullptr;
-    e = launch_waveform(wa, s);
+    e = launch_waveform(wa, plan, d_wscratch, s);
     mark();
     launches += 2;
   }

@@ -48,9 +48,9 @@ constexpr int32_t kEmptyRef = 0x7FFFFFFF;  // never-hit child (box is inverted)
 // Per-subray constants of the beam pattern (R2, R4, R5), fp64.
 struct SubrayConst {
   double cos_t;     // cos(theta_i)
-  double a;         // sin(theta_i) cos(phi)
-  double b;         // sin(theta_i) sin(phi)
-  double sin_t;     // sin(theta_i)  (r = R sin theta_i)
+  double sin_t;     // sin(theta_i)  (also r = R sin theta_i)
+  double cos_p;     // cos(phi)
+  double sin_p;     // sin(phi)
   double w_far;     // far-field weight exp(-2 sin^2 theta / tan^2 beta) (R5)
   double pad_[3];
 };
@@ -103,8 +103,17 @@ struct WaveArgs {
 
 // launchers (trace.cu / waveform.cu)
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s);
-cudaError_t launch_waveform(const WaveArgs& a, cudaStream_t s);
-int waveform_warps(uint32_t n_bins, uint32_t N, uint32_t taps);
+
+struct WavePlan {
+  int warps;            // warps per block (0 = does not fit)
+  size_t smem;          // dynamic shared memory per block
+  uint32_t grid;        // persistent grid (SMs x occupancy)
+  size_t scratch_bytes; // per-warp global rows for wide pulses
+};
+WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);
+bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps);
+cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scratch,
+                            cudaStream_t s);
 
 // LBVH build (lbvh.cu)
 struct BuildResult {

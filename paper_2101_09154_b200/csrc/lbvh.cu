@@ -201,8 +201,18 @@ __global__ void k_layout(int n, const int* __restrict__ child, const int* __rest
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
   int c0 = child[2 * i], c1 = child[2 * i + 1];
-  const float* b0 = c0 < 0 ? leafbox + 6ull * (~c0) : nodebox + 6ull * c0;
-  const float* b1 = c1 < 0 ? leafbox + 6ull * (~c1) : nodebox + 6ull * c1;
+  const float* q0 = c0 < 0 ? leafbox + 6ull * (~c0) : nodebox + 6ull * c0;
+  const float* q1 = c1 < 0 ? leafbox + 6ull * (~c1) : nodebox + 6ull * c1;
+  // boxes padded outward (directed rounding): a ray lying exactly on a face of
+  // a flat or axis-aligned box (zero direction component) is never culled
+  float b0[6], b1[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b0[a] = __fsub_rd(q0[a], fmaf(fabsf(q0[a]), 1e-6f, 1e-30f));
+    b0[3 + a] = __fadd_ru(q0[3 + a], fmaf(fabsf(q0[3 + a]), 1e-6f, 1e-30f));
+    b1[a] = __fsub_rd(q1[a], fmaf(fabsf(q1[a]), 1e-6f, 1e-30f));
+    b1[3 + a] = __fadd_ru(q1[3 + a], fmaf(fabsf(q1[3 + a]), 1e-6f, 1e-30f));
+  }
   Node nd;
   nd.xy0 = make_float4(b0[0], b0[3], b0[1], b0[4]);
   nd.xy1 = make_float4(b1[0], b1[3], b1[1], b1[4]);

@@ -25,15 +25,28 @@ namespace {
 
 constexpr float kBoxSlack = 1e-6f;  // >> 4 * 2^-24 relative error of an fp32 slab value
 
+// fp64 helpers with explicit round-to-nearest intrinsics: no FMA contraction,
+// so every expression below evaluates exactly like the oracle's (same
+// operation tree, IEEE double, -ffp-contract=off): decisions at shared edges
+// and voxel faces are then bit-identical on both sides (P1 in DESIGN.md).
 struct D3 {
   double x, y, z;
 };
 __device__ __forceinline__ D3 d3(double x, double y, double z) { return {x, y, z}; }
-__device__ __forceinline__ D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-__device__ __forceinline__ double dot(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ D3 cross(D3 a, D3 b) {
-  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dif(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ D3 sub(D3 a, D3 b) { return {dif(a.x, b.x), dif(a.y, b.y), dif(a.z, b.z)}; }
+__device__ __forceinline__ D3 scale(D3 a, double s) { return {mul(a.x, s), mul(a.y, s), mul(a.z, s)}; }
+__device__ __forceinline__ D3 vadd(D3 a, D3 b) { return {add(a.x, b.x), add(a.y, b.y), add(a.z, b.z)}; }
+__device__ __forceinline__ double dot(D3 a, D3 b) {
+  return add(add(mul(a.x, b.x), mul(a.y, b.y)), mul(a.z, b.z));
 }
+__device__ __forceinline__ D3 cross(D3 a, D3 b) {
+  return {dif(mul(a.y, b.z), mul(a.z, b.y)), dif(mul(a.z, b.x), mul(a.x, b.z)),
+          dif(mul(a.x, b.y), mul(a.y, b.x))};
+}
+__device__ __forceinline__ double norm(D3 a) { return __dsqrt_rn(dot(a, a)); }
 
 __device__ __forceinline__ float safe_inv(float d) {
   // a zero component would give (b - o) * inf = NaN on a box face through the
@@ -53,23 +66,25 @@ __device__ __forceinline__ float box_enter(float lox, float hix, float loy, floa
   return (tmin * (1.0f - kBoxSlack) <= tmax * (1.0f + kBoxSlack)) ? tmin : INFINITY;
 }
 
-// fp64 Moller-Trumbore (the oracle's definition, R21): t or -1.
+// fp64 Moller-Trumbore (the oracle's definition and operation order, R21):
+// t or -1.  The degeneracy cut |det| <= 1e-12 |e1||e2| is evaluated squared
+// (no square roots); it differs from the oracle's form only for rays within
+// ~1e-16 relative of the cut (parallel to the plane).
 __device__ __forceinline__ double mt64(const D3& o, const D3& d, const TriRecord& tr) {
   const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
   const D3 e1 = sub(d3(tr.b.x, tr.b.y, tr.b.z), v0);
   const D3 e2 = sub(d3(tr.c.x, tr.c.y, tr.c.z), v0);
   const D3 p = cross(d, e2);
   const double det = dot(e1, p);
-  // |det| <= 1e-12 |e1||e2|, squared to avoid two square roots
-  if (det * det <= 1e-24 * dot(e1, e1) * dot(e2, e2)) return -1.0;
-  const double inv = 1.0 / det;
+  if (mul(det, det) <= mul(mul(1e-24, dot(e1, e1)), dot(e2, e2))) return -1.0;
+  const double inv = __drcp_rn(det);
   const D3 s = sub(o, v0);
-  const double u = dot(s, p) * inv;
+  const double u = mul(dot(s, p), inv);
   if (u < 0.0 || u > 1.0) return -1.0;
   const D3 q = cross(s, e1);
-  const double v = dot(d, q) * inv;
-  if (v < 0.0 || u + v > 1.0) return -1.0;
-  const double t = dot(e2, q) * inv;
+  const double v = mul(dot(d, q), inv);
+  if (v < 0.0 || add(u, v) > 1.0) return -1.0;
+  const double t = mul(dot(e2, q), inv);
   return t > 0.0 ? t : -1.0;
 }
 
@@ -84,7 +99,7 @@ __device__ __forceinline__ TriRecord load_tri(const TriRecord* __restrict__ t, u
 __device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, double o, double d) {
   // crossing of plane org + k vs, computed directly (same arithmetic as the
   // oracle's plane enumeration; intrinsics forbid FMA contraction)
-  return (__dadd_rn(org, __dmul_rn((double)k, vs)) - o) / d;
+  return __ddiv_rn(__dsub_rn(__dadd_rn(org, __dmul_rn((double)k, vs)), o), d);
 }
 
 template <bool INSTR>
@@ -104,40 +119,24 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
   // ---- A2: subray fan-out (R2, R4), fp64
   const float ox = __ldg(a.origin + 3 * p), oy = __ldg(a.origin + 3 * p + 1),
               oz = __ldg(a.origin + 3 * p + 2);
-  double dx = __ldg(a.direction + 3 * p), dy = __ldg(a.direction + 3 * p + 1),
-         dz = __ldg(a.direction + 3 * p + 2);
-  const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+  D3 Dp = d3(__ldg(a.direction + 3 * p), __ldg(a.direction + 3 * p + 1),
+             __ldg(a.direction + 3 * p + 2));
+  const double dn = norm(Dp);
   if (!(dn > 0.0) || !isfinite(dn)) {
     if (s == 0) atomicOr(a.err_flag, 1u);
     a.out[gid] = rec;
     return;
   }
-  {
-    const double r = 1.0 / dn;
-    dx *= r;
-    dy *= r;
-    dz *= r;
-  }
-  double ux, uy, uz;
-  if (fabs(dz) > 0.9) {  // a = x: u = x cross d
-    ux = 0.0;
-    uy = -dz;
-    uz = dy;
-  } else {  // a = z: u = z cross d
-    ux = -dy;
-    uy = dx;
-    uz = 0.0;
-  }
-  {
-    const double r = 1.0 / sqrt(ux * ux + uy * uy + uz * uz);
-    ux *= r;
-    uy *= r;
-    uz *= r;
-  }
-  const double vx = dy * uz - dz * uy, vy = dz * ux - dx * uz, vz = dx * uy - dy * ux;
+  Dp = scale(Dp, __drcp_rn(dn));
+  // frame (R4): a = x if |d_z| > 0.9 else z; u = normalize(a x d); v = d x u
+  const D3 ax = fabs(Dp.z) > 0.9 ? d3(1.0, 0.0, 0.0) : d3(0.0, 0.0, 1.0);
+  D3 U = cross(ax, Dp);
+  U = scale(U, __drcp_rn(norm(U)));
+  const D3 V = cross(Dp, U);
   const SubrayConst sc = a.sub[s];
-  const D3 D = d3(sc.cos_t * dx + sc.a * ux + sc.b * vx, sc.cos_t * dy + sc.a * uy + sc.b * vy,
-                  sc.cos_t * dz + sc.a * uz + sc.b * vz);
+  // d_s = cos(theta) d + sin(theta) (cos(phi) u + sin(phi) v)
+  const D3 ring = vadd(scale(U, sc.cos_p), scale(V, sc.sin_p));
+  const D3 D = vadd(scale(Dp, sc.cos_t), scale(ring, sc.sin_t));
   const D3 O = d3(ox, oy, oz);
 
   // ---- A3: nearest triangle (LBVH; fp32 boxes, fp64 decisions)
@@ -204,12 +203,12 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
     bool inside = true;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      const double lo = org[ax], hi = org[ax] + (double)nn[ax] * a.vs;
+      const double lo = org[ax], hi = add(org[ax], mul((double)nn[ax], a.vs));
       if (d3v[ax] == 0.0) {
         if (o3[ax] < lo || o3[ax] > hi) inside = false;
         continue;
       }
-      double ta = (lo - o3[ax]) / d3v[ax], tb = (hi - o3[ax]) / d3v[ax];
+      double ta = __ddiv_rn(dif(lo, o3[ax]), d3v[ax]), tb = __ddiv_rn(dif(hi, o3[ax]), d3v[ax]);
       if (ta > tb) {
         const double tmp = ta;
         ta = tb;
@@ -286,7 +285,7 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
     const TriRecord tr = load_tri(a.tris, best_k);
     const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
     const D3 n = cross(sub(d3(tr.b.x, tr.b.y, tr.b.z), v0), sub(d3(tr.c.x, tr.c.y, tr.c.z), v0));
-    const double cos_inc = fabs(dot(n, D)) / (sqrt(dot(n, n)) * sqrt(dot(D, D)));
+    const double cos_inc = __ddiv_rn(fabs(dot(n, D)), mul(norm(n), norm(D)));
     R = t_best;
     sig_eff = (double)tr.b.w * cos_inc;
     pid = best_id;

@@ -1,20 +1,27 @@
 // waveform.cu -- K7: full-waveform binning + local-maximum peaks -> returns.
 //
 // One warp per pulse (grid-stride).  The pulse's subray records (16 B each,
-// written by K6) are read once; the waveform is accumulated in shared memory
-// in fp64 ("the recorded power for each bin is taken as the sum of the
-// subray's waveforms, shifted according to the different ranges"), strictly
-// in subray order -- no atomics, so the sum is deterministic and its
-// decisions (max, local maxima, threshold) are taken in the same precision as
-// the oracle's.  The dense row is stored as fp32.
+// written by K6) are read once.  P:215: "the recorded power for each bin is
+// taken as the sum of the subray's waveforms, shifted according to the
+// different ranges of the subrays":
 //
-//   k_s  = floor(2 R_s / c / Delta)                  (R8, R9; same fp64 ops as the oracle)
+//   k_s  = floor(2 R_s / c / Delta)                  (R8, R9; the oracle's fp64 operations)
 //   k0   = min_s k_s                                  (window anchor, R9)
 //   W[k] = sum_s A_s p[k - (k_s - k0)],  p[j] = f((j + 1/2) Delta / tau),
 //          f(x) = x^2 e^-x  (Eq. 3),  j < L_p = ceil(20 tau / Delta)
 //   peak at k in [1, n_bins-2]: W[k] > W[k-1], W[k] > W[k+1], W[k] >= thr max W
 //   (P:215 local-maximum filter; R11), earliest max_returns kept,
 //   range (c/2)(k0 + k - j* + 1/2) Delta (R12), prim = argmax_s contribution (R13).
+//
+// Evaluation (deterministic, fp64, no atomics): the subrays of a pulse fall
+// into few distinct bin offsets o_s = k_s - k0 (coherent footprint), so the
+// amplitudes are first summed per offset group (each group in subray order),
+// then each lane computes its bins W[k] = sum_o A_o p[k - o] directly.  Pulses
+// whose offsets spread over >= kAggCap bins use the per-subray accumulation.
+// The waveform window lives in a small per-warp shared-memory buffer; a pulse
+// whose support exceeds it (rare: a footprint spanning > kWCap - L_p bins)
+// uses a per-warp global scratch row.  Rows are stored as fp32 with 16-byte
+// vector stores (zeros outside the support).
 #include <math.h>
 
 #include "internal.cuh"
@@ -23,6 +30,8 @@ namespace helios {
 namespace {
 
 constexpr int kMaxWarps = 8;
+constexpr int kWCap = 512;    // fp64 bins per warp in shared memory
+constexpr int kAggCap = 64;   // offset groups handled by the grouped path
 constexpr size_t kSmemCap = 200 * 1024;
 
 __device__ __forceinline__ long long warp_min_ll(long long v) {
@@ -44,17 +53,33 @@ __device__ __forceinline__ double warp_max_d(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a) {
+struct Layout {
+  size_t ker_d, per_warp_d, w_off, agg_off, off_off, amp_off;
+};
+__host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
+  Layout L;
+  L.ker_d = (taps + 1) & ~1u;
+  L.w_off = 0;
+  L.agg_off = kWCap;
+  L.off_off = kWCap + kAggCap;                 // int[N] packed 2 per double
+  L.amp_off = L.off_off + (N + 1) / 2;         // float[N]
+  L.per_warp_d = L.amp_off + (N + 1) / 2;
+  return L;
+}
+
+__global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a,
+                                                             double* __restrict__ gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t N = a.N, nb = a.n_bins, taps = a.taps;
-  // smem: kernel[taps] | per warp: W[nb] (double), off[N] (int), amp[N] (float)
+  const Layout L = layout_for(N, taps);
   double* ker = reinterpret_cast<double*>(smem_raw);
-  const size_t ker_d = (taps + 1) & ~1u;
-  const size_t per_warp_d = nb + ((N + 1) / 2) + ((N + 1) / 2);
-  double* W = ker + ker_d + warp * per_warp_d;
-  int* off = reinterpret_cast<int*>(W + nb);
-  float* amp = reinterpret_cast<float*>(W + nb + (N + 1) / 2);
+  double* base = ker + L.ker_d + (size_t)warp * L.per_warp_d;
+  double* Ws = base + L.w_off;
+  double* agg = base + L.agg_off;
+  int* off = reinterpret_cast<int*>(base + L.off_off);
+  float* amp = reinterpret_cast<float*>(base + L.amp_off);
+  double* Wg = gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
 
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
   __syncthreads();
@@ -62,7 +87,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a) {
   for (uint64_t p = (uint64_t)blockIdx.x * nw + warp; p < a.n_pulses;
        p += (uint64_t)gridDim.x * nw) {
     const helios_subray_hit* rec = a.rec + p * N;
-    // pass 1: bins k_s (fp64, the oracle's operation order) and k0
+    // pass 1: absolute bins k_s (fp64, the oracle's operation order) and k0
     long long kmin = LLONG_MAX;
     for (uint32_t s = lane; s < N; s += 32) {
       const helios_subray_hit r = rec[s];
@@ -71,121 +96,132 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a) {
         k = (long long)floor(2.0 * r.range_m / kC / (a.delta_ns * 1e-9));
         kmin = k < kmin ? k : kmin;
       }
-      off[s] = (int)(k < 0 ? -1 : k);  // absolute bin for now (fits: R < 3e8 m)
+      off[s] = (int)k;  // absolute bin for now (R < 3e8 m fits an int)
       amp[s] = r.amplitude;
     }
     __syncwarp();
     const long long k0 = warp_min_ll(kmin);
-    uint8_t nret = 0;
     helios_return* slots = a.returns + p * a.max_returns;
     float* row = a.waveform ? a.waveform + p * (uint64_t)nb : nullptr;
-    if (k0 == LLONG_MAX) {  // no hit (R23): empty row, no returns
-      if (lane == 0) {
-        a.first_bin[p] = -1;
-        a.n_returns[p] = 0;
+    uint32_t S = 0;
+    double* W = Ws;
+    uint8_t nret = 0;
+    if (k0 != LLONG_MAX) {
+      // offsets within the window; beyond maxFullwaveRange -> discarded
+      int maxoff = 0;
+      for (uint32_t s = lane; s < N; s += 32) {
+        int o = off[s];
+        if (o >= 0) {
+          o = (int)((long long)o - k0);
+          if (o >= (int)nb) o = -2;
+          else maxoff = max(maxoff, o);
+          off[s] = o;
+        }
       }
-      for (uint32_t q = lane; q < a.max_returns * 4u; q += 32)
-        reinterpret_cast<double*>(slots)[q] = 0.0;
-      if (row)
-        for (uint32_t k = lane; k < nb; k += 32) row[k] = 0.0f;
-      continue;
-    }
-    // offsets relative to the window; support length S
-    int maxoff = 0;
-    for (uint32_t s = lane; s < N; s += 32) {
-      int o = off[s];
-      if (o >= 0) {
-        o = (int)((long long)o - k0);
-        if (o >= (int)nb) o = -2;  // beyond maxFullwaveRange: discarded
-        else maxoff = max(maxoff, o);
-        off[s] = o;
-      }
-    }
-    maxoff = warp_max_i(maxoff);
-    const uint32_t S = min(nb, (uint32_t)maxoff + taps);
-    for (uint32_t k = lane; k < S; k += 32) W[k] = 0.0;
-    __syncwarp();
-    // accumulate in subray order (deterministic)
-    for (uint32_t s = 0; s < N; ++s) {
-      const int o = off[s];
-      if (o < 0) continue;
-      const double A = (double)amp[s];
-      for (uint32_t j = lane; j < taps; j += 32) {
-        const uint32_t k = (uint32_t)o + j;
-        if (k < S) W[k] += A * ker[j];
-      }
+      maxoff = warp_max_i(maxoff);
+      S = min(nb, (uint32_t)maxoff + taps);
+      W = (S <= (uint32_t)kWCap) ? Ws : Wg;
       __syncwarp();
-    }
-    // maximum
-    double M = 0.0;
-    for (uint32_t k = lane; k < S; k += 32) M = fmax(M, W[k]);
-    M = warp_max_d(M);
-    const double thr = (double)a.thr * M;
-    // local maxima in time order (ballot over 32 consecutive bins)
-    for (uint32_t base = 0; base < S && nret < a.max_returns; base += 32) {
-      const uint32_t k = base + lane;
-      bool pk = false;
-      if (k >= 1 && k + 1 < nb && k < S) {
-        const double w = W[k], wl = W[k - 1], wr = (k + 1 < S) ? W[k + 1] : 0.0;
-        pk = w > wl && w > wr && w >= thr;
-      }
-      unsigned m = __ballot_sync(0xffffffffu, pk);
-      while (m && nret < a.max_returns) {
-        const uint32_t kk = base + (__ffs(m) - 1);
-        m &= m - 1;
-        // attribution (R13): largest contribution A_s p[kk - o_s], ties -> lowest s
-        double bc = -1.0;
-        uint32_t bs = 0xFFFFFFFFu;
-        for (uint32_t s = lane; s < N; s += 32) {
+      if (maxoff < kAggCap) {
+        // amplitude per offset group, each group summed in subray order
+        for (int o = lane; o <= maxoff; o += 32) {
+          double acc = 0.0;
+          for (uint32_t s = 0; s < N; ++s)
+            if (off[s] == o) acc += (double)amp[s];
+          agg[o] = acc;
+        }
+        __syncwarp();
+        for (uint32_t k = lane; k < S; k += 32) {
+          const int olo = max(0, (int)k - (int)taps + 1), ohi = min(maxoff, (int)k);
+          double w = 0.0;
+          for (int o = olo; o <= ohi; ++o) w += agg[o] * ker[k - o];
+          W[k] = w;
+        }
+      } else {
+        // wide footprint: per-subray accumulation in subray order
+        for (uint32_t k = lane; k < S; k += 32) W[k] = 0.0;
+        __syncwarp();
+        for (uint32_t s = 0; s < N; ++s) {
           const int o = off[s];
           if (o < 0) continue;
-          const int j = (int)kk - o;
-          if (j < 0 || j >= (int)taps) continue;
-          const double c = (double)amp[s] * ker[j];
-          if (c > bc) {
-            bc = c;
-            bs = s;
+          const double A = (double)amp[s];
+          for (uint32_t j = lane; j < taps; j += 32) {
+            const uint32_t k = (uint32_t)o + j;
+            if (k < S) W[k] += A * ker[j];
           }
+          __syncwarp();
         }
+      }
+      __syncwarp();
+      // maximum
+      double M = 0.0;
+      for (uint32_t k = lane; k < S; k += 32) M = fmax(M, W[k]);
+      M = warp_max_d(M);
+      const double thr = (double)a.thr * M;
+      // local maxima in time order (ballot over 32 consecutive bins)
+      for (uint32_t b0 = 0; b0 < S && nret < a.max_returns; b0 += 32) {
+        const uint32_t k = b0 + lane;
+        bool pk = false;
+        if (k >= 1 && k + 1 < nb && k < S) {
+          const double w = W[k], wl = W[k - 1], wr = (k + 1 < S) ? W[k + 1] : 0.0;
+          pk = w > wl && w > wr && w >= thr;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, pk);
+        while (m && nret < a.max_returns) {
+          const uint32_t kk = b0 + (__ffs(m) - 1);
+          m &= m - 1;
+          // attribution (R13): largest contribution A_s p[kk - o_s], ties -> lowest s
+          double bc = -1.0;
+          uint32_t bs = 0xFFFFFFFFu;
+          for (uint32_t s = lane; s < N; s += 32) {
+            const int o = off[s];
+            if (o < 0) continue;
+            const int j = (int)kk - o;
+            if (j < 0 || j >= (int)taps) continue;
+            const double c = (double)amp[s] * ker[j];
+            if (c > bc) {
+              bc = c;
+              bs = s;
+            }
+          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double c2 = __shfl_xor_sync(0xffffffffu, bc, o);
-          const uint32_t s2 = __shfl_xor_sync(0xffffffffu, bs, o);
-          if (c2 > bc || (c2 == bc && s2 < bs)) {
-            bc = c2;
-            bs = s2;
+          for (int o = 16; o > 0; o >>= 1) {
+            const double c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+            const uint32_t s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            if (c2 > bc || (c2 == bc && s2 < bs)) {
+              bc = c2;
+              bs = s2;
+            }
           }
+          if (lane == 0) {
+            helios_return r;
+            r.range_m = 0.5 * kC * ((double)(k0 + (long long)kk - (long long)a.jstar) + 0.5) *
+                        a.delta_ns * 1e-9;
+            r.gps_time_s = a.time_s ? a.time_s[p] : 0.0;
+            r.intensity = (float)W[kk];
+            r.prim_id = rec[bs].prim_id;
+            r.return_number = (uint8_t)(nret + 1);
+            r.n_returns = 0;  // patched below once the count is known
+            for (int q = 0; q < 6; ++q) r.pad[q] = 0;
+            slots[nret] = r;
+          }
+          ++nret;
         }
-        if (lane == 0) {
-          helios_return r;
-          r.range_m = 0.5 * kC * ((double)(k0 + (long long)kk - (long long)a.jstar) + 0.5) *
-                      a.delta_ns * 1e-9;
-          r.gps_time_s = a.time_s ? a.time_s[p] : 0.0;
-          r.intensity = (float)W[kk];
-          r.prim_id = rec[bs].prim_id;
-          r.return_number = (uint8_t)(nret + 1);
-          r.n_returns = 0;  // patched below once the count is known
-          for (int q = 0; q < 6; ++q) r.pad[q] = 0;
-          slots[nret] = r;
-        }
-        ++nret;
       }
     }
     __syncwarp();
-    // patch n_returns into the slots, zero the unused ones
+    // return slots: patch the count, zero the unused ones
     for (uint32_t r = lane; r < a.max_returns; r += 32) {
       if (r < nret) {
         slots[r].n_returns = nret;
       } else {
-        double* q = reinterpret_cast<double*>(slots + r);
-        q[0] = 0.0;
-        q[1] = 0.0;
-        q[2] = 0.0;
-        q[3] = 0.0;
+        double2* q = reinterpret_cast<double2*>(slots + r);
+        q[0] = make_double2(0.0, 0.0);
+        q[1] = make_double2(0.0, 0.0);
       }
     }
     if (lane == 0) {
-      a.first_bin[p] = k0;
+      a.first_bin[p] = (k0 == LLONG_MAX) ? -1 : k0;
       a.n_returns[p] = nret;
       if (a.counters) atomicAdd(a.counters + 1, (unsigned long long)nret);
     }
@@ -196,44 +232,81 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a) {
       for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
       if (lane == 0) atomicAdd(a.counters + 0, (unsigned long long)h);
     }
-    if (row)
-      for (uint32_t k = lane; k < nb; k += 32) row[k] = k < S ? (float)W[k] : 0.0f;
+    if (row) {
+      // dense fp32 row: scalar head/tail, 16-byte stores for the aligned body
+      const uint32_t mis = (uint32_t)(((uintptr_t)row >> 2) & 3u);
+      const uint32_t head = min(nb, (4u - mis) & 3u);
+      if (lane < head) row[lane] = lane < S ? (float)W[lane] : 0.0f;
+      const uint32_t nvec = (nb - head) >> 2;
+      float4* body = reinterpret_cast<float4*>(row + head);
+      for (uint32_t q = lane; q < nvec; q += 32) {
+        const uint32_t k = head + 4 * q;
+        float4 v;
+        if (k >= S) {
+          v = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          v.x = (float)W[k];
+          v.y = k + 1 < S ? (float)W[k + 1] : 0.0f;
+          v.z = k + 2 < S ? (float)W[k + 2] : 0.0f;
+          v.w = k + 3 < S ? (float)W[k + 3] : 0.0f;
+        }
+        body[q] = v;
+      }
+      const uint32_t t0 = head + 4 * nvec;
+      if (t0 + lane < nb) row[t0 + lane] = t0 + lane < S ? (float)W[t0 + lane] : 0.0f;
+    }
     __syncwarp();
   }
 }
 
+size_t smem_for(uint32_t N, uint32_t taps, int warps) {
+  const Layout L = layout_for(N, taps);
+  return 8 * (L.ker_d + (size_t)warps * L.per_warp_d);
+}
+
 }  // namespace
 
-static size_t smem_for(uint32_t n_bins, uint32_t N, uint32_t taps, int warps) {
-  const size_t ker_d = (taps + 1) & ~1u;
-  const size_t per_warp_d = n_bins + ((N + 1) / 2) + ((N + 1) / 2);
-  return 8 * (ker_d + (size_t)warps * per_warp_d);
-}
-
-// warps per block that fit the shared-memory budget (0 = does not fit)
-int waveform_warps(uint32_t n_bins, uint32_t N, uint32_t taps) {
+WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
+  WavePlan pl{};
+  int warps = 0;
   for (int w = kMaxWarps; w >= 1; --w)
-    if (smem_for(n_bins, N, taps, w) <= kSmemCap) return w;
-  return 0;
-}
-
-cudaError_t launch_waveform(const WaveArgs& a, cudaStream_t s) {
-  if (a.n_pulses == 0) return cudaSuccess;
-  const int warps = waveform_warps(a.n_bins, a.N, a.taps);
-  if (warps == 0) return cudaErrorInvalidValue;
-  const size_t smem = smem_for(a.n_bins, a.N, a.taps, warps);
-  cudaError_t e = cudaFuncSetAttribute(k_waveform, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+    if (smem_for(N, taps, w) <= kSmemCap) {
+      warps = w;
+      break;
+    }
+  if (warps == 0) return pl;
+  pl.warps = warps;
+  pl.smem = smem_for(N, taps, warps);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform, warps * 32, smem);
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  uint64_t want = (a.n_pulses + warps - 1) / warps;
-  uint64_t grid = (uint64_t)sms * per_sm;
+  if (cudaFuncSetAttribute(k_waveform, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)pl.smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform, warps * 32, pl.smem) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    pl.warps = 0;
+    return pl;
+  }
+  pl.grid = (uint32_t)(sms * per_sm);
+  pl.scratch_bytes = sizeof(double) * (size_t)pl.grid * warps * n_bins;
+  return pl;
+}
+
+bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps) {
+  (void)n_bins;
+  return smem_for(N, taps, 1) <= kSmemCap;
+}
+
+cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scratch,
+                            cudaStream_t s) {
+  if (a.n_pulses == 0) return cudaSuccess;
+  if (pl.warps == 0) return cudaErrorInvalidValue;
+  uint64_t want = (a.n_pulses + pl.warps - 1) / pl.warps;
+  uint64_t grid = pl.grid;
   if (want < grid) grid = want;
-  k_waveform<<<(unsigned)grid, warps * 32, smem, s>>>(a);
+  k_waveform<<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
   return cudaGetLastError();
 }
 

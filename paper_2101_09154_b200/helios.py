@@ -286,7 +286,7 @@ def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=Fals
     hp = params if isinstance(params, helios_scanner_params) else make_params(params)
     nb = helios_waveform_bins(hp)
     if nb == 0:
-        raise HeliosError(HELIOS_ERR_INVALID_ARGUMENT, "invalid waveform parameters")
+        raise HeliosError(HELIOS_ERR_INVALID_ARGUMENT, helios_last_error())
     kw = dict(device=device)
     if device == "cpu" and pin_memory:
         kw["pin_memory"] = True
@@ -308,6 +308,9 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     (Outputs, helios_stats | None).  stats=True: per-kernel device times;
     counters=True: also the instrumented traversal counters."""
     hp = params if isinstance(params, helios_scanner_params) else make_params(params)
+    host = lambda x, dt: np.ascontiguousarray(x, dt) if isinstance(x, np.ndarray) else x
+    origin, direction = host(origin, np.float32), host(direction, np.float32)
+    time_s = host(time_s, np.float64)
     n = int(origin.shape[0])
     if outputs is None:
         dev = "cuda" if (not isinstance(origin, np.ndarray) and origin.is_cuda) else "cpu"

@@ -225,6 +225,15 @@ def boxes(rng: np.random.Generator, n: int, h: np.ndarray, lo: float, hi: float)
             np.repeat(refl, 10).astype(np.float32), np.stack([cx, cy, radius], 1))
 
 
+def _scaled_flight(alt: float, fov_deg: float, width: float, scale: float):
+    """Full size: (alt, fov) as stated.  Reduced parity scenes: fly lower and
+    narrow the swath so it stays on the smaller scene (most subrays hit)."""
+    if scale >= 1.0:
+        return alt, fov_deg
+    a = max(alt * scale, 120.0)
+    return a, min(fov_deg, float(np.degrees(np.arctan(0.42 * width / a))))
+
+
 def _dir_sawtooth(theta: np.ndarray) -> np.ndarray:
     """Across-track (x) deflection, nadir-looking: (sin th, 0, -cos th)."""
     return np.stack([np.sin(theta), np.zeros_like(theta), -np.cos(theta)], -1)
@@ -260,12 +269,14 @@ def _c2(scale: float, seed: int):
     dur = (n - 1) / 60.0
     prf = n_pulses / dur
     xc = (n - 1) / 2.0
+    # reduced scenes keep the swath on the (smaller) DTM
+    alt, fov = _scaled_flight(500.0, 30.0, n, scale)
 
     def fn(idx):
         t = idx.astype(np.float64) / prf
-        th = np.radians(-30.0 + 60.0 * np.mod(100.0 * t, 1.0))
+        th = np.radians(-fov + 2 * fov * np.mod(100.0 * t, 1.0))
         d = _dir_sawtooth(th)
-        o = np.stack([np.full_like(t, xc), 60.0 * t, np.full_like(t, 500.0)], -1)
+        o = np.stack([np.full_like(t, xc), 60.0 * t, np.full_like(t, alt)], -1)
         return o.astype(np.float32), d.astype(np.float32), t
 
     return scene, params, n_pulses, fn
@@ -342,10 +353,11 @@ def _c4(scale: float, seed: int):
     speed = 5.0
     dur = 2 * half / speed
     prf = n_pulses / dur
+    fov = 45.0 if scale >= 1.0 else min(45.0, float(np.degrees(np.arctan(0.42 * 2 * half / 60.0))))
 
     def fn(idx):
         t = idx.astype(np.float64) / prf
-        th = np.radians(-45.0 + 90.0 * np.mod(50.0 * t, 1.0))
+        th = np.radians(-fov + 2 * fov * np.mod(50.0 * t, 1.0))
         d = _dir_sawtooth(th)
         o = np.stack([np.zeros_like(t), -half + speed * t, np.full_like(t, 80.0)], -1)
         return o.astype(np.float32), d.astype(np.float32), t
@@ -390,16 +402,17 @@ def _c5(scale: float, seed: int):
     line_dur = (n - 1) / 60.0
     prf = per_line / line_dur
     xs = (600.0 * (n / 2048.0), 1448.0 * (n / 2048.0))
+    alt, fov = _scaled_flight(1000.0, 35.0, 0.8 * n, scale)
 
     def fn(idx):
         line = idx // per_line
         m = idx % per_line
         tl = m.astype(np.float64) / prf
         t = line * line_dur + tl
-        th = np.radians(-35.0 + 70.0 * np.mod(200.0 * t, 1.0))
+        th = np.radians(-fov + 2 * fov * np.mod(200.0 * t, 1.0))
         d = _dir_sawtooth(th)
         x = np.where(line == 0, xs[0], xs[1])
-        o = np.stack([x, 60.0 * tl, np.full_like(tl, 1000.0)], -1)
+        o = np.stack([x, 60.0 * tl, np.full_like(tl, alt)], -1)
         return o.astype(np.float32), d.astype(np.float32), t
 
     return scene, params, n_pulses, fn
