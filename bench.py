@@ -263,12 +263,13 @@ def run_ours(args):
     value = subrays / (ms_max / 1e3) / 1e6
 
     # ---- algorithmic bytes (instrumented, untimed re-run of the same batches)
-    nodes = tris = vox = 0
+    nodes = tris = vox = f64 = 0
     for i in range(args.warmup, steps_total):
         st = step(i, counters=True)
         nodes += st.nodes_visited
         tris += st.tris_tested
         vox += st.voxel_steps
+        f64 += st.fp64_tests
     sub_rank = B * N * args.steps
     b_ray = 64 * nodes + 48 * tris + 4 * vox
     b_trace = b_ray + 24 * B * args.steps + 16 * sub_rank  # + pulse inputs + records
@@ -331,8 +332,10 @@ def run_ours(args):
                          "bytes_per_launch": b_trace / max(1, launches // 2),
                          "avg_launch_ms": trace_ms / max(1, launches // 2),
                          "share_of_step": trace_ms / ms if ms > 0 else None,
+                         "waveform_share_of_step": wave_ms / ms if ms > 0 else None,
                          "nodes_per_ray": nodes / sub_rank, "tris_per_ray": tris / sub_rank,
                          "voxel_steps_per_ray": vox / sub_rank,
+                         "fp64_tests_per_ray": f64 / sub_rank,
                          "step_R1": r1},
             "gpu_launches": launches,
             "clocks": clk,

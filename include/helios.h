@@ -196,6 +196,7 @@ typedef struct {
   uint64_t pulses, subrays;
   uint64_t subray_hits, voxel_returns, returns;     /* only with collect_counters */
   uint64_t nodes_visited, tris_tested, voxel_steps; /* only with collect_counters */
+  uint64_t fp64_tests; /* triangles the fp32 prefilter could not reject (collect_counters) */
   double trace_ms;    /* out: summed device time of the trace launches (K6), CUDA events */
   double waveform_ms; /* out: summed device time of the waveform launches (K7)          */
 } helios_stats;

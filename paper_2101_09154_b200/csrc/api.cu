@@ -9,6 +9,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <limits>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -29,6 +31,57 @@ struct helios_scene_s {
   bool built = false;
   BuildResult bvh{};
   int device = 0;
+
+  // Scratch cache: one device buffer per stream, grown on demand, reused by
+  // later calls on the same stream, freed by helios_scene_destroy.
+  struct Slot {
+    cudaStream_t stream;
+    char* ptr;
+    size_t bytes;
+    bool busy;
+  };
+  std::mutex mu;
+  std::vector<Slot> slots;
+
+  cudaError_t acquire(cudaStream_t s, size_t bytes, char** out) {
+    std::lock_guard<std::mutex> g(mu);
+    for (Slot& sl : slots) {
+      if (sl.stream != s || sl.busy) continue;
+      if (sl.bytes < bytes) {
+        cudaFreeAsync(sl.ptr, s);
+        sl.ptr = nullptr;
+        sl.bytes = 0;
+        cudaError_t e = cudaMallocAsync((void**)&sl.ptr, bytes, s);
+        if (e != cudaSuccess) return e;
+        sl.bytes = bytes;
+      }
+      sl.busy = true;
+      *out = sl.ptr;
+      return cudaSuccess;
+    }
+    Slot sl{s, nullptr, bytes, true};
+    cudaError_t e = cudaMallocAsync((void**)&sl.ptr, bytes ? bytes : 256, s);
+    if (e != cudaSuccess) return e;
+    slots.push_back(sl);
+    *out = sl.ptr;
+    return cudaSuccess;
+  }
+  void release(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    for (Slot& sl : slots)
+      if (sl.stream == s && sl.busy) {
+        sl.busy = false;
+        return;
+      }
+  }
+  void free_slots() {
+    std::lock_guard<std::mutex> g(mu);
+    for (Slot& sl : slots) {
+      cudaStreamSynchronize(sl.stream);
+      cudaFree(sl.ptr);
+    }
+    slots.clear();
+  }
 };
 
 namespace {
@@ -200,6 +253,7 @@ cudaError_t copy_in(T** dst, const T* src, size_t count, cudaStream_t s) {
 }
 
 void free_scene(helios_scene sc, cudaStream_t s) {
+  sc->free_slots();
   cudaFreeAsync(sc->d_xyz, s);
   cudaFreeAsync(sc->d_refl, s);
   cudaFreeAsync(sc->d_pad, s);
@@ -260,6 +314,15 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
   helios_scene sc = new (std::nothrow) helios_scene_s();
   if (!sc) return fail(HELIOS_ERR_OUT_OF_MEMORY, "host allocation failed");
   cudaGetDevice(&sc->device);
+  {
+    // keep stream-ordered allocations mapped across synchronisations
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, sc->device) == cudaSuccess) {
+      uint64_t keep = std::numeric_limits<uint64_t>::max();
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   sc->n_tris = desc->n_tris;
   cudaError_t e = cudaSuccess;
   unsigned* d_bad = nullptr;
@@ -394,17 +457,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const double K = params->efficiency * params->receiver_diameter_m * params->receiver_diameter_m /
                    (4.0 * kPi * beta * beta);  // Eq. 7 (R14)
 
-  // ---- scratch + staging
-  std::vector<void*> scratch;
-  auto alloc = [&](void** p, size_t bytes) -> cudaError_t {
-    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, s);
-    if (e == cudaSuccess) scratch.push_back(*p);
-    return e;
-  };
-  auto cleanup = [&]() {
-    for (void* p : scratch) cudaFreeAsync(p, s);
-    cudaStreamSynchronize(s);
-  };
+  // ---- scratch (one cached buffer per (scene, stream)) + host staging
   struct Arr {
     const void* user;
     size_t bytes;
@@ -422,40 +475,55 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
       {outputs->p_waveform, 4ull * d.n_bins * n, false, nullptr, false},
       {outputs->p_subray_hits, sizeof(helios_subray_hit) * N * n, false, nullptr, false},
   };
-  cudaError_t e = cudaSuccess;
-  for (Arr& a : arrs) {
+  const WavePlan plan = plan_waveform(d.n_bins, N, d.taps);
+  if (plan.warps == 0)
+    return fail(HELIOS_ERR_CUDA, "helios_simulate: waveform kernel cannot be configured");
+  // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
+  const uint64_t chunk = std::max<uint64_t>(1024, (48ull << 20) / (16ull * N));
+  const bool own_rec = outputs->p_subray_hits == nullptr;
+  size_t total = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t at = total;
+    total += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  const size_t o_tab = carve(sizeof(SubrayConst) * N);
+  const size_t o_ker = carve(sizeof(double) * d.taps);
+  const size_t o_err = carve(sizeof(unsigned));
+  const size_t o_cnt = carve(sizeof(unsigned long long) * 8);
+  const size_t o_rec = carve(own_rec ? sizeof(helios_subray_hit) * N * std::min(n, chunk) : 0);
+  const size_t o_ws = carve(plan.scratch_bytes);
+  size_t o_arr[8];
+  for (int i = 0; i < 8; ++i) {
+    Arr& a = arrs[i];
+    o_arr[i] = 0;
     if (!a.user) continue;
     if (device_accessible(a.user)) {
       a.dev = const_cast<void*>(a.user);
       continue;
     }
     a.staged = true;
-    if ((e = alloc(&a.dev, a.bytes)) != cudaSuccess) break;
-    if (a.in && (e = cudaMemcpyAsync(a.dev, a.user, a.bytes, cudaMemcpyHostToDevice, s)) !=
-                    cudaSuccess)
-      break;
+    o_arr[i] = carve(a.bytes);
   }
-  SubrayConst* d_tab = nullptr;
-  double* d_ker = nullptr;
-  unsigned* d_err = nullptr;
-  unsigned long long* d_cnt = nullptr;
-  helios_subray_hit* d_rec = nullptr;
-  double* d_wscratch = nullptr;
-  const WavePlan plan = plan_waveform(d.n_bins, N, d.taps);
-  if (plan.warps == 0) {
-    cleanup();
-    return fail(HELIOS_ERR_CUDA, "helios_simulate: waveform kernel cannot be configured");
+  char* buf = nullptr;
+  cudaError_t e = sc->acquire(s, total, &buf);
+  if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
+    sc->release(s);
+  };
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i) {
+    Arr& a = arrs[i];
+    if (!a.staged) continue;
+    a.dev = buf + o_arr[i];
+    if (a.in) e = cudaMemcpyAsync(a.dev, a.user, a.bytes, cudaMemcpyHostToDevice, s);
   }
-  // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
-  const uint64_t chunk = std::max<uint64_t>(1024, (48ull << 20) / (16ull * N));
-  const bool own_rec = arrs[7].dev == nullptr;
-  if (e == cudaSuccess) e = alloc((void**)&d_tab, sizeof(SubrayConst) * N);
-  if (e == cudaSuccess) e = alloc((void**)&d_ker, sizeof(double) * d.taps);
-  if (e == cudaSuccess) e = alloc((void**)&d_err, sizeof(unsigned));
-  if (e == cudaSuccess) e = alloc((void**)&d_cnt, sizeof(unsigned long long) * 8);
-  if (e == cudaSuccess && own_rec)
-    e = alloc((void**)&d_rec, sizeof(helios_subray_hit) * N * std::min(n, chunk));
-  if (e == cudaSuccess) e = alloc((void**)&d_wscratch, plan.scratch_bytes);
+  SubrayConst* d_tab = reinterpret_cast<SubrayConst*>(buf + o_tab);
+  double* d_ker = reinterpret_cast<double*>(buf + o_ker);
+  unsigned* d_err = reinterpret_cast<unsigned*>(buf + o_err);
+  unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(buf + o_cnt);
+  helios_subray_hit* d_rec = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec) : nullptr;
+  double* d_wscratch = reinterpret_cast<double*>(buf + o_ws);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_tab, tab.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
@@ -583,6 +651,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     stats->tris_tested = hcnt[1];
     stats->voxel_steps = hcnt[2];
     stats->voxel_returns = hcnt[3];
+    stats->fp64_tests = hcnt[6];
     stats->subray_hits = hcnt[4];
     stats->returns = hcnt[5];
   }

@@ -88,6 +88,51 @@ __device__ __forceinline__ double mt64(const D3& o, const D3& d, const TriRecord
   return t > 0.0 ? t : -1.0;
 }
 
+// fp32 prefilter.  Returns true only when the triangle is DEFINITELY not a
+// candidate (a miss of the fp64 test, or a hit farther than t_hi); otherwise
+// the fp64 test above decides.  Forward-error argument: e1, e2, s are
+// differences of fp32 inputs (relative error <= u = 2^-24 per component), the
+// fp32 direction differs from the fp64 one by <= u relative per component, and
+// each triple product (det, u*det, v*det, t*det) is a 5-operation sum of
+// products, so |computed - exact| <= 8u * sum|terms| <= 8u * |a|_1 |b|_1 |c|_1.
+// The margins below use 32u (4x slack) plus the rounding of the comparisons.
+struct F3 {
+  float x, y, z;
+};
+__device__ __forceinline__ F3 fsub(F3 a, F3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ float fdot(F3 a, F3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ F3 fcross(F3 a, F3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ float l1(F3 a) { return fabsf(a.x) + fabsf(a.y) + fabsf(a.z); }
+
+__device__ __forceinline__ bool mt32_definite_miss(const F3& o, const F3& d, float dl1,
+                                                   const TriRecord& tr, float t_hi) {
+  constexpr float kU = 32.0f * 5.9604645e-8f;
+  const F3 v0 = {tr.a.x, tr.a.y, tr.a.z};
+  const F3 e1 = fsub({tr.b.x, tr.b.y, tr.b.z}, v0);
+  const F3 e2 = fsub({tr.c.x, tr.c.y, tr.c.z}, v0);
+  const F3 sv = fsub(o, v0);
+  const float A = l1(e1), B = l1(e2), S = l1(sv);
+  const F3 p = fcross(d, e2);
+  const float det = fdot(e1, p);
+  const float err_det = kU * A * dl1 * B;
+  const float adet = fabsf(det);
+  if (!(adet > err_det)) return false;  // sign of det uncertain (or NaN): decide in fp64
+  const float sg = det > 0.0f ? 1.0f : -1.0f;
+  const float nu = fdot(sv, p) * sg;
+  const F3 q = fcross(sv, e1);
+  const float nv = fdot(d, q) * sg;
+  const float nt = fdot(e2, q) * sg;
+  const float err_u = kU * S * dl1 * B, err_v = kU * S * A * dl1, err_t = kU * B * S * A;
+  if (nu < -err_u || nv < -err_v || nt < -err_t) return true;  // u < 0, v < 0, t < 0
+  if (nu - adet > err_u + err_det) return true;                 // u > 1
+  if ((nu + nv) - adet > (err_u + err_v + err_det) * 1.0001f) return true;  // u + v > 1
+  // t = nt / adet > t_hi (cannot be the nearest hit)
+  if (t_hi < 3.0e38f && nt - t_hi * adet > (err_t + t_hi * err_det) * 1.0001f + 1e-30f) return true;
+  return false;
+}
+
 __device__ __forceinline__ TriRecord load_tri(const TriRecord* __restrict__ t, uint32_t k) {
   TriRecord r;
   r.a = __ldg(&t[k].a);
@@ -109,7 +154,7 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
   if (gid >= total) return;
   const uint64_t p = gid / a.N;
   const uint32_t s = (uint32_t)(gid - p * a.N);
-  unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0;
+  unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;
 
   helios_subray_hit rec;
   rec.range_m = __longlong_as_double(0x7FF8000000000000ll);  // NaN
@@ -144,15 +189,21 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
   uint32_t best_id = 0xFFFFFFFFu, best_k = 0;
   if (a.n_tris > 0) {
     const float ix = safe_inv((float)D.x), iy = safe_inv((float)D.y), iz = safe_inv((float)D.z);
+    const F3 O32 = {ox, oy, oz};
+    const F3 D32 = {(float)D.x, (float)D.y, (float)D.z};
+    const float dl1 = l1(D32);
     int32_t stack[kStackSize];
     int sp = 0;
     int32_t ref = a.root;
     for (;;) {
       if (ref_is_leaf(ref)) {
         const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
+        const float t_hi = __double2float_ru(t_best);
         for (uint32_t k = first; k < first + cnt; ++k) {
           const TriRecord tr = load_tri(a.tris, k);
           if (INSTR) ++c_tris;
+          if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
+          if (INSTR) ++c_f64;
           const double t = mt64(O, D, tr);
           if (t > 0.0) {
             const uint32_t id = __float_as_uint(tr.a.w);
@@ -312,6 +363,7 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
     atomicAdd(a.counters + 1, c_tris);
     atomicAdd(a.counters + 2, c_vox);
     atomicAdd(a.counters + 3, c_voxret);
+    atomicAdd(a.counters + 6, c_f64);
   }
 }
 
