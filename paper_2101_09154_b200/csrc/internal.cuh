@@ -22,6 +22,7 @@ namespace helios {
 constexpr int kMaxSubrays = 512;      // >= largest supported count (279)
 constexpr int kStackSize = 64;        // LBVH depth bound (checked at build)
 constexpr int kLeafMax = 4;           // triangles per collapsed leaf
+constexpr int kMortonBits = 21;       // per axis (63-bit codes)
 constexpr int kMaxLut = 4096;
 constexpr int kMaxTaps = 8192;        // L_p bound (validated)
 constexpr double kC = 299792458.0;    // m/s

@@ -3,10 +3,11 @@
 // Replaces the paper's CPU kd-tree (Sec. 5.1: recursive search,
 // x/y/z split cycling by depth) with a linear BVH built entirely on the GPU:
 //   K1 centroid bounds (block reduce + ordered-int atomics)
-//   K1 30-bit Morton codes (10 bits per axis over the centroid AABB)
+//   K1 Morton codes of the centroids: 3 x kMortonBits bits over an isotropic
+//      grid (kMortonBits = 21 -> 63-bit codes; DESIGN.md s.8 says why not 30)
 //   K2 radix sort of (code, index)   [CUB onesweep, library sort]
 //   K3 Karras hierarchy: N-1 internal nodes, delta = clz(code_i ^ code_j),
-//      index tie-break (32 + clz(i ^ j)) for duplicate codes
+//      index tie-break (64 + clz(i ^ j)) for duplicate codes
 //   K4 bottom-up AABB refit (second-arriving child computes the parent)
 //   K5 layout: 64-B child-pair nodes, subtrees of <= kLeafMax triangles
 //      collapsed into leaves, triangles permuted to leaf order (48 B).
@@ -15,6 +16,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -57,44 +59,58 @@ __global__ void k_centroid_bounds(const float* __restrict__ xyz, uint32_t n,
   }
 }
 
-__device__ __forceinline__ uint32_t expand10(uint32_t v) {
-  v = (v * 0x00010001u) & 0xFF0000FFu;
-  v = (v * 0x00000101u) & 0x0F00F00Fu;
-  v = (v * 0x00000011u) & 0xC30C30C3u;
-  v = (v * 0x00000005u) & 0x49249249u;
+// spread the low 21 bits of v to every third bit of a 63-bit word
+__device__ __forceinline__ uint64_t expand21(uint64_t v) {
+  v &= 0x1FFFFFull;
+  v = (v | (v << 32)) & 0x1F00000000FFFFull;
+  v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+  v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+  v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
   return v;
 }
 
+// Morton code of the centroid over an ISOTROPIC grid: every axis uses the
+// largest extent of the centroid AABB, so on flat scenes (2 km x 2 km x
+// 0.2 km) the top levels split x/y first instead of slicing the whole scene
+// into thin z slabs that every nadir ray crosses.  kMortonBits per axis.
 __global__ void k_morton(const float* __restrict__ xyz, uint32_t n,
-                         const unsigned* __restrict__ bounds, uint32_t* __restrict__ codes,
-                         uint32_t* __restrict__ idx) {
+                         const unsigned* __restrict__ bounds, uint64_t* __restrict__ codes,
+                         uint32_t* __restrict__ idx, int bits, int isotropic) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float* t = xyz + 9ull * i;
-  uint32_t q[3];
+  float lo[3], ex[3], ext = 0.0f;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    float lo = ord2f(bounds[a]), hi = ord2f(bounds[3 + a]);
-    float c = (t[a] + t[3 + a] + t[6 + a]) * (1.0f / 3.0f);
-    float ext = hi - lo;
-    float f = ext > 0.0f ? (c - lo) / ext : 0.0f;
-    int k = (int)(f * 1024.0f);
-    q[a] = (uint32_t)min(max(k, 0), 1023);
+    lo[a] = ord2f(bounds[a]);
+    ex[a] = ord2f(bounds[3 + a]) - lo[a];
+    ext = fmaxf(ext, ex[a]);
   }
-  codes[i] = (expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]);
+  const double cells = (double)(1u << bits);
+  uint64_t q[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double c = ((double)t[a] + (double)t[3 + a] + (double)t[6 + a]) / 3.0;
+    const float e = isotropic ? ext : ex[a];
+    const double f = e > 0.0f ? (c - (double)lo[a]) / (double)e : 0.0;
+    long long k = (long long)(f * cells);
+    q[a] = (uint64_t)min(max(k, 0ll), (long long)(cells - 1));
+  }
+  codes[i] = (expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]);
   idx[i] = i;
 }
 
-__device__ __forceinline__ int delta(const uint32_t* __restrict__ codes, int n, int i, int j) {
+__device__ __forceinline__ int delta(const uint64_t* __restrict__ codes, int n, int i, int j) {
   if (j < 0 || j >= n) return -1;
-  uint32_t a = codes[i], b = codes[j];
-  if (a == b) return 32 + __clz((unsigned)(i ^ j));
-  return __clz(a ^ b);
+  const uint64_t a = codes[i], b = codes[j];
+  if (a == b) return 64 + __clz((unsigned)(i ^ j));
+  return __clzll((long long)(a ^ b));
 }
 
 // Karras 2012 hierarchy: internal node i covers [first, last]; split gamma.
 // child encoding: >= 0 internal node, < 0 sorted leaf ~k.
-__global__ void k_karras(const uint32_t* __restrict__ codes, int n, int* __restrict__ child,
+__global__ void k_karras(const uint64_t* __restrict__ codes, int n, int* __restrict__ child,
                          int* __restrict__ parent_int, int* __restrict__ parent_leaf,
                          int* __restrict__ range) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -267,7 +283,8 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   cudaError_t e = cudaSuccess;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   unsigned* bounds = nullptr;
-  uint32_t *codes = nullptr, *idx = nullptr, *codes_s = nullptr, *idx_s = nullptr;
+  uint64_t *codes = nullptr, *codes_s = nullptr;
+  uint32_t *idx = nullptr, *idx_s = nullptr;
   int *child = nullptr, *parent_int = nullptr, *parent_leaf = nullptr, *range = nullptr;
   float *leafbox = nullptr, *nodebox = nullptr;
   unsigned *flags = nullptr, *dmax = nullptr;
@@ -278,6 +295,12 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   const unsigned ni = n > 1 ? (n - 1 + T - 1) / T : 1;
   unsigned init_bounds[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
   unsigned hdepth = 0;
+  // tuning knobs for measurements (DESIGN.md s.8): HELIOS_MORTON_BITS (1..21),
+  // HELIOS_MORTON_ANISO=1 (per-axis normalisation)
+  int bits = kMortonBits, isotropic = 1;
+  if (const char* v = getenv("HELIOS_MORTON_BITS")) bits = atoi(v);
+  if (bits < 1 || bits > 21) bits = kMortonBits;
+  if (const char* v = getenv("HELIOS_MORTON_ANISO")) isotropic = atoi(v) ? 0 : 1;
 
 #define CK(x)                 \
   do {                        \
@@ -300,13 +323,13 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   CK(dalloc(&out->tris, n, s));
   k_centroid_bounds<<<min(nb, 148u * 8u), T, 0, s>>>(xyz, n, bounds);
   CK(cudaGetLastError());
-  k_morton<<<nb, T, 0, s>>>(xyz, n, bounds, codes, idx);
+  k_morton<<<nb, T, 0, s>>>(xyz, n, bounds, codes, idx, bits, isotropic);
   CK(cudaGetLastError());
   CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0,
-                                     30, s));
+                                     3 * bits, s));
   CK(cudaMallocAsync(&temp, temp_bytes ? temp_bytes : 1, s));
-  CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0, 30,
-                                     s));
+  CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0,
+                                     3 * bits, s));
   if (n <= (uint32_t)kLeafMax) {
     out->root = leaf_ref(0, n);
     out->max_depth = 0;
