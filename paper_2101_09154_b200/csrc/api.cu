@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -593,6 +594,10 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     }
   };
   uint32_t launches = 0;
+  // traversal mode: warp-cooperative packets (default) or per-ray threads;
+  // HELIOS_TRAVERSAL=ray selects the latter (A/B measurements)
+  bool packet = true;
+  if (const char* v = getenv("HELIOS_TRAVERSAL")) packet = strcmp(v, "ray") != 0;
   for (uint64_t b = 0; b < n && e == cudaSuccess; b += chunk) {
     const uint64_t m = std::min(chunk, n - b);
     ta.origin = org + 3 * b;
@@ -601,7 +606,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     ta.pulse_base = pulses->pulse_index_base + b;
     ta.out = own_rec ? d_rec : hits + b * N;
     mark();
-    e = launch_trace(ta, counters, s);
+    e = launch_trace(ta, counters, packet, s);
     if (e != cudaSuccess) break;
     mark();
     wa.rec = ta.out;

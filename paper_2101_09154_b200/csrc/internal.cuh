@@ -103,7 +103,7 @@ struct WaveArgs {
 };
 
 // launchers (trace.cu / waveform.cu)
-cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s);
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, bool packet, cudaStream_t s);
 
 struct WavePlan {
   int warps;            // warps per block (0 = does not fit)

@@ -55,6 +55,13 @@ __device__ __forceinline__ float safe_inv(float d) {
 }
 
 // Slab test of one child box; returns the entry distance (or +inf on a miss).
+// t = (b - o) * inv per slab has a purely RELATIVE error <= 4u (u = 2^-24:
+// difference, reciprocal, product, and the fp32 rounding of the fp64
+// direction), whatever the direction (zero components are replaced by
+// +-1e-30, so no NaN); the interval is widened by the relative slack
+// kBoxSlack >> 4u: the fp32 test never culls a box the fp64 ray enters.
+// (An fma(b, inv, -o*inv) form saves 6 instructions but carries an absolute
+// error ~u |o * inv|, unbounded for axis-parallel rays -- not used.)
 __device__ __forceinline__ float box_enter(float lox, float hix, float loy, float hiy, float loz,
                                            float hiz, float ox, float oy, float oz, float ix,
                                            float iy, float iz, float tbest) {
@@ -63,7 +70,8 @@ __device__ __forceinline__ float box_enter(float lox, float hix, float loy, floa
   const float tz0 = (loz - oz) * iz, tz1 = (hiz - oz) * iz;
   const float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
   const float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tbest));
-  return (tmin * (1.0f - kBoxSlack) <= tmax * (1.0f + kBoxSlack)) ? tmin : INFINITY;
+  constexpr float kWiden = (1.0f + kBoxSlack) / (1.0f - kBoxSlack);
+  return (tmin <= tmax * kWiden) ? tmin : INFINITY;
 }
 
 // fp64 Moller-Trumbore (the oracle's definition and operation order, R21):
@@ -147,13 +155,178 @@ __device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, dou
   return __ddiv_rn(__dsub_rn(__dadd_rn(org, __dmul_rn((double)k, vs)), o), d);
 }
 
+// Per-ray traversal (one thread walks its own subray; "while-while", stack in
+// local memory).  Returns through t_best / best_id / best_k.
 template <bool INSTR>
+__device__ __forceinline__ void traverse_ray(const TraceArgs& a, const D3& O, const D3& D,
+                                             const F3& O32, const F3& D32, float dl1, float ix,
+                                             float iy, float iz, double& t_best,
+                                             uint32_t& best_id, uint32_t& best_k,
+                                             unsigned long long& c_nodes,
+                                             unsigned long long& c_tris,
+                                             unsigned long long& c_f64) {
+  int32_t stack[kStackSize];
+  int sp = 0;
+  int32_t ref = a.root;
+  for (;;) {
+    if (ref_is_leaf(ref)) {
+      const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
+      const float t_hi = __double2float_ru(t_best);
+      for (uint32_t k = first; k < first + cnt; ++k) {
+        const TriRecord tr = load_tri(a.tris, k);
+        if (INSTR) ++c_tris;
+        if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
+        if (INSTR) ++c_f64;
+        const double t = mt64(O, D, tr);
+        if (t > 0.0) {
+          const uint32_t id = __float_as_uint(tr.a.w);
+          if (t < t_best || (t == t_best && id < best_id)) {
+            t_best = t;
+            best_id = id;
+            best_k = k;
+          }
+        }
+      }
+      if (sp == 0) break;
+      ref = stack[--sp];
+      continue;
+    }
+    const Node* nd = a.nodes + ref;
+    const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
+                 rf = __ldg(&nd->ref);
+    if (INSTR) ++c_nodes;
+    const float tb = (float)t_best;
+    const float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix,
+                               iy, iz, tb);
+    const float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix,
+                               iy, iz, tb);
+    const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
+    const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
+    if (h0 && h1) {
+      const bool near0 = t0 <= t1;
+      ref = near0 ? r0 : r1;
+      stack[sp++] = near0 ? r1 : r0;
+    } else if (h0) {
+      ref = r0;
+    } else if (h1) {
+      ref = r1;
+    } else {
+      if (sp == 0) break;
+      ref = stack[--sp];
+    }
+  }
+}
+
+// Warp-cooperative masked packet traversal.  The 32 lanes of a warp hold
+// consecutive (pulse, subray) rays -- the nearly parallel subrays of one or
+// two pulses (beam divergence <= 0.5 mrad here).  The warp walks ONE
+// path through the tree: at each node every lane whose bit is in the mask
+// tests both child boxes against its own ray and t_best; a child is visited
+// with the mask of the lanes that hit it (ballot), the far child is pushed
+// with its own mask.  Control flow is warp-uniform, the node load is one
+// broadcast per warp, and the stack of (node, mask) pairs is distributed over
+// the lanes' registers (entry i lives in lane i % 32), so no local memory.
+// Every lane visits a superset of the nodes its own per-ray traversal would
+// visit, so the result is identical.
+template <bool INSTR>
+__device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, const D3& O,
+                                                const D3& D, const F3& O32, const F3& D32,
+                                                float dl1, float ix, float iy, float iz,
+                                                double& t_best, uint32_t& best_id,
+                                                uint32_t& best_k, unsigned long long& c_nodes,
+                                                unsigned long long& c_tris,
+                                                unsigned long long& c_f64) {
+  const unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int32_t stA_r = 0, stB_r = 0;
+  unsigned stA_m = 0, stB_m = 0;
+  int sp = 0;
+  int32_t ref = a.root;
+  for (;;) {
+    const bool mine = (m >> lane) & 1u;
+    if (ref_is_leaf(ref)) {
+      if (mine) {
+        const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
+        const float t_hi = __double2float_ru(t_best);
+        for (uint32_t k = first; k < first + cnt; ++k) {
+          const TriRecord tr = load_tri(a.tris, k);
+          if (INSTR) ++c_tris;
+          if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
+          if (INSTR) ++c_f64;
+          const double t = mt64(O, D, tr);
+          if (t > 0.0) {
+            const uint32_t id = __float_as_uint(tr.a.w);
+            if (t < t_best || (t == t_best && id < best_id)) {
+              t_best = t;
+              best_id = id;
+              best_k = k;
+            }
+          }
+        }
+      }
+      if (sp == 0) break;
+      --sp;
+      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+      continue;
+    }
+    const Node* nd = a.nodes + ref;
+    const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
+                 rf = __ldg(&nd->ref);
+    float t0 = INFINITY, t1 = INFINITY;
+    if (mine) {
+      if (INSTR) ++c_nodes;
+      const float tb = (float)t_best;
+      t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy, iz,
+                     tb);
+      t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy, iz,
+                     tb);
+    }
+    const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
+    const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
+    const unsigned m0 = __ballot_sync(kFull, h0), m1 = __ballot_sync(kFull, h1);
+    if (m0 && m1) {
+      const unsigned both = m0 & m1;
+      const unsigned pref1 = __ballot_sync(kFull, h0 && h1 && t1 < t0);
+      const bool near0 = both ? (2 * __popc(pref1) <= __popc(both)) : (__popc(m0) >= __popc(m1));
+      const int32_t far_r = near0 ? r1 : r0;
+      const unsigned far_m = near0 ? m1 : m0;
+      if (lane == (sp & 31)) {
+        if (sp < 32) {
+          stA_r = far_r;
+          stA_m = far_m;
+        } else {
+          stB_r = far_r;
+          stB_m = far_m;
+        }
+      }
+      ++sp;
+      ref = near0 ? r0 : r1;
+      m = near0 ? m0 : m1;
+    } else if (m0) {
+      ref = r0;
+      m = m0;
+    } else if (m1) {
+      ref = r1;
+      m = m1;
+    } else {
+      if (sp == 0) break;
+      --sp;
+      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+    }
+  }
+}
+
+template <bool INSTR, bool PACKET>
 __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t total = a.n_pulses * (uint64_t)a.N;
-  if (gid >= total) return;
-  const uint64_t p = gid / a.N;
-  const uint32_t s = (uint32_t)(gid - p * a.N);
+  const bool in_range = gid < total;
+  if (!PACKET && !in_range) return;
+  const uint64_t g = in_range ? gid : 0;  // out-of-range lanes ride along (packet mode)
+  const uint64_t p = g / a.N;
+  const uint32_t s = (uint32_t)(g - p * a.N);
   unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;
 
   helios_subray_hit rec;
@@ -167,12 +340,18 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
   D3 Dp = d3(__ldg(a.direction + 3 * p), __ldg(a.direction + 3 * p + 1),
              __ldg(a.direction + 3 * p + 2));
   const double dn = norm(Dp);
+  bool valid = in_range;
   if (!(dn > 0.0) || !isfinite(dn)) {
-    if (s == 0) atomicOr(a.err_flag, 1u);
+    if (in_range && s == 0) atomicOr(a.err_flag, 1u);
+    valid = false;
+    Dp = d3(0.0, 0.0, 1.0);  // placeholder; the lane reports a miss
+  } else {
+    Dp = scale(Dp, __drcp_rn(dn));
+  }
+  if (!PACKET && !valid) {
     a.out[gid] = rec;
     return;
   }
-  Dp = scale(Dp, __drcp_rn(dn));
   // frame (R4): a = x if |d_z| > 0.9 else z; u = normalize(a x d); v = d x u
   const D3 ax = fabs(Dp.z) > 0.9 ? d3(1.0, 0.0, 0.0) : d3(0.0, 0.0, 1.0);
   D3 U = cross(ax, Dp);
@@ -192,54 +371,19 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
     const F3 O32 = {ox, oy, oz};
     const F3 D32 = {(float)D.x, (float)D.y, (float)D.z};
     const float dl1 = l1(D32);
-    int32_t stack[kStackSize];
-    int sp = 0;
-    int32_t ref = a.root;
-    for (;;) {
-      if (ref_is_leaf(ref)) {
-        const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
-        const float t_hi = __double2float_ru(t_best);
-        for (uint32_t k = first; k < first + cnt; ++k) {
-          const TriRecord tr = load_tri(a.tris, k);
-          if (INSTR) ++c_tris;
-          if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
-          if (INSTR) ++c_f64;
-          const double t = mt64(O, D, tr);
-          if (t > 0.0) {
-            const uint32_t id = __float_as_uint(tr.a.w);
-            if (t < t_best || (t == t_best && id < best_id)) {
-              t_best = t;
-              best_id = id;
-              best_k = k;
-            }
-          }
-        }
-        if (sp == 0) break;
-        ref = stack[--sp];
-        continue;
-      }
-      const Node* nd = a.nodes + ref;
-      const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
-                   rf = __ldg(&nd->ref);
-      if (INSTR) ++c_nodes;
-      const float tb = (float)t_best;
-      const float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, ox, oy, oz, ix, iy, iz, tb);
-      const float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, ox, oy, oz, ix, iy, iz, tb);
-      const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
-      const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
-      if (h0 && h1) {
-        const bool near0 = t0 <= t1;
-        ref = near0 ? r0 : r1;
-        stack[sp++] = near0 ? r1 : r0;
-      } else if (h0) {
-        ref = r0;
-      } else if (h1) {
-        ref = r1;
-      } else {
-        if (sp == 0) break;
-        ref = stack[--sp];
-      }
+    if (PACKET) {
+      const unsigned m = __ballot_sync(0xffffffffu, valid);
+      if (m)
+        traverse_packet<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
+                               c_nodes, c_tris, c_f64);
+    } else {
+      traverse_ray<INSTR>(a, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k, c_nodes,
+                          c_tris, c_f64);
     }
+  }
+  if (!valid) {
+    if (in_range) a.out[gid] = rec;
+    return;
   }
 
   // ---- A4: transmissive voxels before the triangle hit
@@ -369,16 +513,23 @@ __global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
 
 }  // namespace
 
-cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) {
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, bool packet, cudaStream_t s) {
   const uint64_t total = a.n_pulses * (uint64_t)a.N;
   if (total == 0) return cudaSuccess;
   const unsigned T = 128;
   const uint64_t blocks = (total + T - 1) / T;
   if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-  if (instrumented)
-    k_trace<true><<<(unsigned)blocks, T, 0, s>>>(a);
-  else
-    k_trace<false><<<(unsigned)blocks, T, 0, s>>>(a);
+  if (packet) {
+    if (instrumented)
+      k_trace<true, true><<<(unsigned)blocks, T, 0, s>>>(a);
+    else
+      k_trace<false, true><<<(unsigned)blocks, T, 0, s>>>(a);
+  } else {
+    if (instrumented)
+      k_trace<true, false><<<(unsigned)blocks, T, 0, s>>>(a);
+    else
+      k_trace<false, false><<<(unsigned)blocks, T, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
