@@ -127,26 +127,21 @@ def barrier(world):
 
 # ------------------------------------------------------------------ CPU oracle
 def oracle_sample(w, n_threads: int, budget_s: float, seed: int = 0):
-    """Time the oracle (as it stands) on a bounded sample of the workload's
-    pulses; returns (pulses, seconds, threads)."""
+    """Time the oracle (as it stands) on a bounded random sample of the
+    workload's pulses, sized to ~budget_s of wall time on n_threads host
+    threads (calibrated on a small first sample); returns (pulses, seconds)."""
     import oracle
     rng = np.random.default_rng(seed)
-    # calibrate with one pulse per thread, then scale to the budget
-    ids = np.sort(rng.choice(w.n_pulses, n_threads, replace=False))
-    o, d, t = w.pulses_at(ids)
-    t0 = time.perf_counter()
-    oracle.simulate(w.scene, w.params, o, d, t, ids.astype(np.uint64), n_threads=n_threads)
-    dt = time.perf_counter() - t0
-    total_p, total_t = n_threads, dt
-    if dt < budget_s / 2:
-        k = int(min(2_000_000, max(n_threads, n_threads * (budget_s - dt) / max(dt, 1e-6))))
-        ids = np.sort(rng.choice(w.n_pulses, min(k, w.n_pulses), replace=False))
+    k = 1
+    while True:
+        ids = np.sort(rng.choice(w.n_pulses, k, replace=False))
         o, d, t = w.pulses_at(ids)
         t0 = time.perf_counter()
         oracle.simulate(w.scene, w.params, o, d, t, ids.astype(np.uint64), n_threads=n_threads)
-        total_t = time.perf_counter() - t0
-        total_p = len(ids)
-    return total_p, total_t
+        dt = time.perf_counter() - t0
+        if dt >= 0.4 * budget_s or k >= 2_000_000:
+            return k, dt
+        k = int(min(2_000_000, max(2 * k, k * 0.8 * budget_s / max(dt, 1e-3))))
 
 
 def run_reference(args):
@@ -160,7 +155,8 @@ def run_reference(args):
     N = w.params.subray_count
     threads = os.cpu_count() or 1
     rng = np.random.default_rng(1)
-    per_step = threads  # one pulse per host thread per step (brute force is slow)
+    # each step: a bounded random sample of the workload, ~args.ref_budget s
+    per_step, _ = oracle_sample(w, threads, args.ref_budget, seed=123)
     times = []
     for i in range(args.warmup + args.steps):
         ids = np.sort(rng.choice(w.n_pulses, per_step, replace=False))
@@ -361,6 +357,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=12.0,
+                    help="seconds of oracle work per --impl reference step")
     args = ap.parse_args()
     args.config = args.config.upper()
     if args.impl == "reference":

@@ -443,19 +443,15 @@ uint32_t oracle_waveform_bins(double window_ns, double bin_ns) {
   return (uint32_t)std::ceil(window_ns / bin_ns);  // R9
 }
 
-/* One pulse: steps O1..O8 of DESIGN.md s.3 (the paper's order). */
-static void simulate_pulse(const oracle_scene* sc, const oracle_params* pr,
-                           const float* origin, const float* direction,
-                           double time_s, uint64_t pulse_id, int64_t i,
-                           const double* theta,
-                           const double* phi, const oracle_outputs* out) {
+/* One subray of pulse i: steps O1..O5 of DESIGN.md s.4 (the paper's order).
+ * Writes the per-subray outputs (range, amplitude, prim, bin, margins). */
+static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
+                            const float* origin, const float* direction, uint64_t pulse_id,
+                            int64_t i, uint32_t s, const double* theta, const double* phi,
+                            const oracle_outputs* out) {
   const uint32_t N = pr->subray_count;
   const double beta = pr->divergence_rad;
   const double delta = pr->bin_width_ns;
-  const double tau = pr->pulse_length_ns / 1.75;                        // P:208
-  const uint32_t n_bins = oracle_waveform_bins(pr->max_fullwave_range_ns, delta);
-  const int64_t Lp = (int64_t)std::ceil(20.0 * tau / delta);           // R9
-  const uint32_t maxr = pr->max_returns;
   const double K = pr->efficiency * pr->receiver_diameter_m *
                    pr->receiver_diameter_m / (4.0 * kPi * beta * beta);  // Eq. 7
 
@@ -463,15 +459,12 @@ static void simulate_pulse(const oracle_scene* sc, const oracle_params* pr,
   double d[3] = {direction[0], direction[1], direction[2]};
   double dn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
 
-  // Per-subray results.
-  std::vector<double> R(N, kNaN), A(N, 0.0);
-  std::vector<uint32_t> prim(N, 0xFFFFFFFFu);
-  std::vector<int64_t> ks(N, -1);
-  std::vector<int32_t> ncand(N, 0);
-  std::vector<double> gapv(N, kInf), kmarg(N, kInf), umarg(N, kInf);
-
+  double Rs_out = kNaN, A_out = 0.0, gap_out = kInf, kmarg_out = kInf, umarg_out = kInf;
+  uint32_t prim_out = 0xFFFFFFFFu;
+  int64_t k_out = -1;
+  int32_t ncand_out = 0;
   if (dn > 0.0) {
-    for (uint32_t s = 0; s < N; ++s) {
+    {
       // O1: subray direction.
       double ds[3];
       oracle_subray_direction(d, theta[s], phi[s], ds);
@@ -527,18 +520,41 @@ static void simulate_pulse(const oracle_scene* sc, const oracle_params* pr,
         double Is = oracle_subray_intensity(pr->peak_power_w, theta[s], beta, Rs,
                                             pr->beam_waist_m, pr->wavelength_nm,
                                             pr->focus_range_m);      // Eq. 1, 2
-        A[s] = K * sig_eff * Is / (Rs * Rs * Rs * Rs);                 // Eq. 7
-        R[s] = Rs;
-        prim[s] = pid;
+        A_out = K * sig_eff * Is / (Rs * Rs * Rs * Rs);                // Eq. 7
+        Rs_out = Rs;
+        prim_out = pid;
         double x = 2.0 * Rs / kC / (delta * 1e-9);  // two-way time in bins (R8, R9)
-        ks[s] = (int64_t)std::floor(x);
-        kmarg[s] = std::fabs(x - std::nearbyint(x));
-        ncand[s] = vox_hit ? 1 : nc;
-        gapv[s] = vox_hit ? kInf : gap;
+        k_out = (int64_t)std::floor(x);
+        kmarg_out = std::fabs(x - std::nearbyint(x));
+        ncand_out = vox_hit ? 1 : nc;
+        gap_out = vox_hit ? kInf : gap;
       }
-      umarg[s] = um;
+      umarg_out = um;
     }
   }
+  int64_t x = i * (int64_t)N + s;
+  out->sub_range[x] = Rs_out;
+  out->sub_amp[x] = A_out;
+  out->sub_prim[x] = prim_out;
+  out->sub_k[x] = k_out;
+  out->sub_ncand[x] = ncand_out;
+  out->sub_gap[x] = gap_out;
+  out->sub_kmargin[x] = kmarg_out;
+  out->sub_umargin[x] = umarg_out;
+}
+
+/* Pulse i after all its subrays: steps O6..O8 (waveform, peaks, returns). */
+static void finish_pulse(const oracle_params* pr, double time_s, int64_t i,
+                         const oracle_outputs* out) {
+  const uint32_t N = pr->subray_count;
+  const double delta = pr->bin_width_ns;
+  const double tau = pr->pulse_length_ns / 1.75;                        // P:208
+  const uint32_t n_bins = oracle_waveform_bins(pr->max_fullwave_range_ns, delta);
+  const int64_t Lp = (int64_t)std::ceil(20.0 * tau / delta);           // R9
+  const uint32_t maxr = pr->max_returns;
+  const double* A = out->sub_amp + i * (int64_t)N;
+  const uint32_t* prim = out->sub_prim + i * (int64_t)N;
+  const int64_t* ks = out->sub_k + i * (int64_t)N;
 
   // O6: full waveform (Eq. 3).
   int64_t k0 = -1;
@@ -622,17 +638,6 @@ static void simulate_pulse(const oracle_scene* sc, const oracle_params* pr,
     for (uint32_t k = 0; k < n_bins; ++k) out->waveform[i * (int64_t)n_bins + k] = W[k];
   out->peak_margin[i] = pmarg;
   out->attr_margin[i] = amarg;
-  for (uint32_t s = 0; s < N; ++s) {
-    int64_t x = i * (int64_t)N + s;
-    out->sub_range[x] = R[s];
-    out->sub_amp[x] = A[s];
-    out->sub_prim[x] = prim[s];
-    out->sub_k[x] = ks[s];
-    out->sub_ncand[x] = ncand[s];
-    out->sub_gap[x] = gapv[s];
-    out->sub_kmargin[x] = kmarg[s];
-    out->sub_umargin[x] = umarg[s];
-  }
 }
 
 /* Simulate the listed pulses (a seeded subset or all of them).  pulse_ids
@@ -664,19 +669,30 @@ int oracle_simulate(const oracle_scene* sc, const oracle_params* pr,
     }
   }
   if (n_threads < 1) n_threads = 1;
-  std::atomic<int64_t> next(0);
-  auto worker = [&]() {
-    for (;;) {
-      int64_t i = next.fetch_add(1);
-      if (i >= n_pulses) break;
-      simulate_pulse(sc, pr, origins + 3 * i, directions + 3 * i, times ? times[i] : 0.0,
-                     pulse_ids[i], i, theta.data(), phi.data(), out);
-    }
+  // Phase 1: every (pulse, subray) pair is independent; phase 2:
+  // every pulse's waveform and peaks.  Plain thread pool with an atomic work
+  // counter; nothing is reduced across threads (thread-count independent).
+  auto run_pool = [&](int64_t n_items, auto&& body) {
+    std::atomic<int64_t> next(0);
+    auto worker = [&]() {
+      for (;;) {
+        int64_t k = next.fetch_add(1);
+        if (k >= n_items) break;
+        body(k);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < n_threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
   };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < n_threads; ++t) pool.emplace_back(worker);
-  worker();
-  for (auto& th : pool) th.join();
+  run_pool(n_pulses * (int64_t)N, [&](int64_t k) {
+    const int64_t i = k / N;
+    const uint32_t s = (uint32_t)(k % N);
+    simulate_subray(sc, pr, origins + 3 * i, directions + 3 * i, pulse_ids[i], i, s,
+                    theta.data(), phi.data(), out);
+  });
+  run_pool(n_pulses, [&](int64_t i) { finish_pulse(pr, times ? times[i] : 0.0, i, out); });
   return 0;
 }
 
