@@ -40,31 +40,40 @@ struct helios_scene_s {
     char* ptr;
     size_t bytes;
     bool busy;
+    cudaStream_t copy;  // non-blocking copy stream for host staging (lazy)
   };
   std::mutex mu;
   std::vector<Slot> slots;
 
-  cudaError_t acquire(cudaStream_t s, size_t bytes, char** out) {
+  cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy) {
     std::lock_guard<std::mutex> g(mu);
-    for (Slot& sl : slots) {
-      if (sl.stream != s || sl.busy) continue;
-      if (sl.bytes < bytes) {
-        cudaFreeAsync(sl.ptr, s);
-        sl.ptr = nullptr;
-        sl.bytes = 0;
-        cudaError_t e = cudaMallocAsync((void**)&sl.ptr, bytes, s);
-        if (e != cudaSuccess) return e;
-        sl.bytes = bytes;
+    Slot* use = nullptr;
+    for (Slot& sl : slots)
+      if (sl.stream == s && !sl.busy) {
+        use = &sl;
+        break;
       }
-      sl.busy = true;
-      *out = sl.ptr;
-      return cudaSuccess;
+    if (!use) {
+      slots.push_back(Slot{s, nullptr, 0, false, nullptr});
+      use = &slots.back();
     }
-    Slot sl{s, nullptr, bytes, true};
-    cudaError_t e = cudaMallocAsync((void**)&sl.ptr, bytes ? bytes : 256, s);
-    if (e != cudaSuccess) return e;
-    slots.push_back(sl);
-    *out = sl.ptr;
+    if (use->bytes < bytes) {
+      if (use->ptr) cudaFreeAsync(use->ptr, s);
+      use->ptr = nullptr;
+      use->bytes = 0;
+      cudaError_t e = cudaMallocAsync((void**)&use->ptr, bytes ? bytes : 256, s);
+      if (e != cudaSuccess) return e;
+      use->bytes = bytes;
+    }
+    if (copy) {
+      if (!use->copy) {
+        cudaError_t e = cudaStreamCreateWithFlags(&use->copy, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+      }
+      *copy = use->copy;
+    }
+    use->busy = true;
+    *out = use->ptr;
     return cudaSuccess;
   }
   void release(cudaStream_t s) {
@@ -79,6 +88,10 @@ struct helios_scene_s {
     std::lock_guard<std::mutex> g(mu);
     for (Slot& sl : slots) {
       cudaStreamSynchronize(sl.stream);
+      if (sl.copy) {
+        cudaStreamSynchronize(sl.copy);
+        cudaStreamDestroy(sl.copy);
+      }
       cudaFree(sl.ptr);
     }
     slots.clear();
@@ -457,30 +470,35 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const double beta = params->divergence_rad;
   const double K = params->efficiency * params->receiver_diameter_m * params->receiver_diameter_m /
                    (4.0 * kPi * beta * beta);  // Eq. 7 (R14)
-
-  // ---- scratch (one cached buffer per (scene, stream)) + host staging
-  struct Arr {
-    const void* user;
-    size_t bytes;
-    bool in;  // host->device before, else device->host after
-    void* dev;
-    bool staged;
-  };
-  Arr arrs[] = {
-      {pulses->p_origin, 12 * n, true, nullptr, false},
-      {pulses->p_direction, 12 * n, true, nullptr, false},
-      {pulses->p_time_s, 8 * n, true, nullptr, false},
-      {outputs->p_n_returns, n, false, nullptr, false},
-      {outputs->p_returns, sizeof(helios_return) * R * n, false, nullptr, false},
-      {outputs->p_wf_first_bin, 8 * n, false, nullptr, false},
-      {outputs->p_waveform, 4ull * d.n_bins * n, false, nullptr, false},
-      {outputs->p_subray_hits, sizeof(helios_subray_hit) * N * n, false, nullptr, false},
-  };
   const WavePlan plan = plan_waveform(d.n_bins, N, d.taps);
   if (plan.warps == 0)
     return fail(HELIOS_ERR_CUDA, "helios_simulate: waveform kernel cannot be configured");
+
+  // ---- argument arrays: device-accessible as given, or staged per chunk.
+  // Per-pulse bytes of each array; chunk-local offsets are (b * per_pulse).
+  struct Arr {
+    const void* user;
+    size_t per_pulse;
+    bool in;      // host->device before the chunk's kernels, else device->host after
+    bool staged;  // host memory: two chunk buffers in scratch (double buffering)
+    size_t off[2];
+  };
+  Arr arrs[] = {
+      {pulses->p_origin, 12, true, false, {0, 0}},
+      {pulses->p_direction, 12, true, false, {0, 0}},
+      {pulses->p_time_s, 8, true, false, {0, 0}},
+      {outputs->p_n_returns, 1, false, false, {0, 0}},
+      {outputs->p_returns, sizeof(helios_return) * R, false, false, {0, 0}},
+      {outputs->p_wf_first_bin, 8, false, false, {0, 0}},
+      {outputs->p_waveform, 4ull * d.n_bins, false, false, {0, 0}},
+      {outputs->p_subray_hits, sizeof(helios_subray_hit) * N, false, false, {0, 0}},
+  };
+  bool any_staged = false;
+  for (Arr& a : arrs)
+    if (a.user && !device_accessible(a.user)) a.staged = any_staged = true;
+
   // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
-  const uint64_t chunk = std::max<uint64_t>(1024, (48ull << 20) / (16ull * N));
+  const uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
   const bool own_rec = outputs->p_subray_hits == nullptr;
   size_t total = 0;
   auto carve = [&](size_t bytes) {
@@ -492,41 +510,27 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const size_t o_ker = carve(sizeof(double) * d.taps);
   const size_t o_err = carve(sizeof(unsigned));
   const size_t o_cnt = carve(sizeof(unsigned long long) * 8);
-  const size_t o_rec = carve(own_rec ? sizeof(helios_subray_hit) * N * std::min(n, chunk) : 0);
   const size_t o_ws = carve(plan.scratch_bytes);
-  size_t o_arr[8];
-  for (int i = 0; i < 8; ++i) {
-    Arr& a = arrs[i];
-    o_arr[i] = 0;
-    if (!a.user) continue;
-    if (device_accessible(a.user)) {
-      a.dev = const_cast<void*>(a.user);
-      continue;
-    }
-    a.staged = true;
-    o_arr[i] = carve(a.bytes);
-  }
+  const size_t o_rec = carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0);
+  for (Arr& a : arrs)
+    if (a.staged)
+      for (int k = 0; k < 2; ++k) a.off[k] = carve(a.per_pulse * chunk);
+
   char* buf = nullptr;
-  cudaError_t e = sc->acquire(s, total, &buf);
+  cudaStream_t cs = nullptr;
+  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
+    if (cs) cudaStreamSynchronize(cs);
     sc->release(s);
   };
-  for (int i = 0; i < 8 && e == cudaSuccess; ++i) {
-    Arr& a = arrs[i];
-    if (!a.staged) continue;
-    a.dev = buf + o_arr[i];
-    if (a.in) e = cudaMemcpyAsync(a.dev, a.user, a.bytes, cudaMemcpyHostToDevice, s);
-  }
   SubrayConst* d_tab = reinterpret_cast<SubrayConst*>(buf + o_tab);
   double* d_ker = reinterpret_cast<double*>(buf + o_ker);
   unsigned* d_err = reinterpret_cast<unsigned*>(buf + o_err);
   unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(buf + o_cnt);
-  helios_subray_hit* d_rec = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec) : nullptr;
   double* d_wscratch = reinterpret_cast<double*>(buf + o_ws);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(d_tab, tab.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
+  e = cudaMemcpyAsync(d_tab, tab.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_ker, d.kernel.data(), sizeof(double) * d.taps, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, sizeof(unsigned), s);
@@ -574,15 +578,6 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   wa.max_returns = R;
   wa.counters = counters ? d_cnt + 4 : nullptr;
 
-  const float* org = (const float*)arrs[0].dev;
-  const float* dir = (const float*)arrs[1].dev;
-  const double* tim = (const double*)arrs[2].dev;
-  uint8_t* nret = (uint8_t*)arrs[3].dev;
-  helios_return* rets = (helios_return*)arrs[4].dev;
-  int64_t* k0 = (int64_t*)arrs[5].dev;
-  float* wf = (float*)arrs[6].dev;
-  helios_subray_hit* hits = (helios_subray_hit*)arrs[7].dev;
-
   // per-kernel device time (CUDA events on the launching stream)
   std::vector<cudaEvent_t> ev;
   auto mark = [&]() {
@@ -593,46 +588,97 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
       ev.push_back(x);
     }
   };
-  uint32_t launches = 0;
+  // staging pipeline events (copy stream <-> compute stream)
+  cudaEvent_t in_done[2] = {nullptr, nullptr}, k_done[2] = {nullptr, nullptr},
+              out_done[2] = {nullptr, nullptr};
+  if (any_staged)
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&k_done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
+    }
+  // the copy stream must not start before the setup work on `s`
+  if (any_staged && e == cudaSuccess) {
+    e = cudaEventRecord(k_done[1], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, k_done[1], 0);
+  }
+  auto dev_ptr = [&](const Arr& a, int slot, uint64_t b) -> char* {
+    if (!a.user) return nullptr;
+    if (a.staged) return buf + a.off[slot];
+    return (char*)a.user + a.per_pulse * b;
+  };
+  auto copy_in = [&](uint64_t b, int slot) -> cudaError_t {
+    const uint64_t m = std::min(chunk, n - b);
+    for (const Arr& a : arrs)
+      if (a.staged && a.in) {
+        cudaError_t r = cudaMemcpyAsync(buf + a.off[slot], (const char*)a.user + a.per_pulse * b,
+                                        a.per_pulse * m, cudaMemcpyHostToDevice, cs);
+        if (r != cudaSuccess) return r;
+      }
+    return cudaEventRecord(in_done[slot], cs);
+  };
+
   // traversal mode: warp-cooperative packets (default) or per-ray threads;
   // HELIOS_TRAVERSAL=ray selects the latter (A/B measurements)
   bool packet = true;
   if (const char* v = getenv("HELIOS_TRAVERSAL")) packet = strcmp(v, "ray") != 0;
-  for (uint64_t b = 0; b < n && e == cudaSuccess; b += chunk) {
+  uint32_t launches = 0;
+  const uint64_t n_chunks = (n + chunk - 1) / chunk;
+  if (any_staged && e == cudaSuccess) e = copy_in(0, 0);
+  for (uint64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
+    const uint64_t b = c * chunk;
     const uint64_t m = std::min(chunk, n - b);
-    ta.origin = org + 3 * b;
-    ta.direction = dir + 3 * b;
+    const int slot = (int)(c & 1);
+    if (any_staged) {
+      // inputs of this chunk are on the device; the D2H of chunk c-2 (same
+      // slot) has drained the output buffers we are about to overwrite
+      e = cudaStreamWaitEvent(s, in_done[slot], 0);
+      if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(s, out_done[slot], 0);
+      if (e != cudaSuccess) break;
+    }
+    ta.origin = (const float*)dev_ptr(arrs[0], slot, b);
+    ta.direction = (const float*)dev_ptr(arrs[1], slot, b);
     ta.n_pulses = m;
     ta.pulse_base = pulses->pulse_index_base + b;
-    ta.out = own_rec ? d_rec : hits + b * N;
+    ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec)
+                     : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
     mark();
     e = launch_trace(ta, counters, packet, s);
     if (e != cudaSuccess) break;
     mark();
     wa.rec = ta.out;
     wa.n_pulses = m;
-    wa.time_s = tim ? tim + b : nullptr;
-    wa.n_returns = nret + b;
-    wa.returns = rets + b * R;
-    wa.first_bin = k0 + b;
-    wa.waveform = wf ? wf + b * (uint64_t)d.n_bins : nullptr;
+    wa.time_s = (const double*)dev_ptr(arrs[2], slot, b);
+    wa.n_returns = (uint8_t*)dev_ptr(arrs[3], slot, b);
+    wa.returns = (helios_return*)dev_ptr(arrs[4], slot, b);
+    wa.first_bin = (int64_t*)dev_ptr(arrs[5], slot, b);
+    wa.waveform = (float*)dev_ptr(arrs[6], slot, b);
     e = launch_waveform(wa, plan, d_wscratch, s);
     mark();
     launches += 2;
+    if (e != cudaSuccess || !any_staged) continue;
+    e = cudaEventRecord(k_done[slot], s);
+    // prefetch the next chunk's inputs into the other slot (its previous
+    // user, chunk c-1, has been consumed by the kernels already enqueued)
+    if (e == cudaSuccess && c + 1 < n_chunks) {
+      if (c >= 1) e = cudaStreamWaitEvent(cs, k_done[slot ^ 1], 0);
+      if (e == cudaSuccess) e = copy_in(b + chunk, slot ^ 1);
+    }
+    // drain this chunk's outputs
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, k_done[slot], 0);
+    for (const Arr& a : arrs)
+      if (e == cudaSuccess && a.staged && !a.in)
+        e = cudaMemcpyAsync((char*)a.user + a.per_pulse * b, buf + a.off[slot], a.per_pulse * m,
+                            cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], cs);
   }
   unsigned herr = 0;
   unsigned long long hcnt[8] = {0};
-  if (e == cudaSuccess) {
-    for (Arr& a : arrs)
-      if (a.staged && !a.in && a.dev) {
-        e = cudaMemcpyAsync(const_cast<void*>(a.user), a.dev, a.bytes, cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) break;
-      }
-  }
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && counters)
     e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && cs) e = cudaStreamSynchronize(cs);
   double t_trace = 0.0, t_wave = 0.0;
   for (size_t i = 0; i + 2 < ev.size(); i += 3) {
     float a = 0.f, b2 = 0.f;
@@ -643,6 +689,11 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     }
   }
   for (cudaEvent_t x : ev) cudaEventDestroy(x);
+  for (int k = 0; k < 2; ++k) {
+    if (in_done[k]) cudaEventDestroy(in_done[k]);
+    if (k_done[k]) cudaEventDestroy(k_done[k]);
+    if (out_done[k]) cudaEventDestroy(out_done[k]);
+  }
   cudaGetLastError();
   cleanup();
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate");

@@ -318,8 +318,11 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   }
 }
 
+#ifndef HELIOS_TRACE_MIN_BLOCKS
+#define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
+#endif
 template <bool INSTR, bool PACKET>
-__global__ void __launch_bounds__(128) k_trace(const TraceArgs a) {
+__global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t total = a.n_pulses * (uint64_t)a.N;
   const bool in_range = gid < total;

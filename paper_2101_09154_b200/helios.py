@@ -17,7 +17,7 @@ from dataclasses import dataclass, fields
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhelios.so")
+LIB_PATH = os.environ.get("HELIOS_LIB") or os.path.join(_HERE, "libhelios.so")
 
 HELIOS_OK = 0
 HELIOS_ERR_INVALID_ARGUMENT = 1
@@ -309,7 +309,12 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     (Outputs, helios_stats | None).  stats=True: per-kernel device times;
     counters=True: also the instrumented traversal counters."""
     hp = params if isinstance(params, helios_scanner_params) else make_params(params)
-    host = lambda x, dt: np.ascontiguousarray(x, dt) if isinstance(x, np.ndarray) else x
+    def host(x, dt):
+        if x is None:
+            return None
+        if isinstance(x, np.ndarray):
+            return np.ascontiguousarray(x, dt)
+        return x if x.is_contiguous() else x.contiguous()
     origin, direction = host(origin, np.float32), host(direction, np.float32)
     time_s = host(time_s, np.float64)
     n = int(origin.shape[0])

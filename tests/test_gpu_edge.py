@@ -83,19 +83,30 @@ def test_batch_split_and_repeat_are_bitwise_identical():
         assert np.array_equal(a[k].view(np.uint8), cat.view(np.uint8)), k
 
 
-def test_host_buffers_match_device_buffers():
+@pytest.mark.parametrize("subrays,n", [(37, 3000), (279, 25000)])
+def test_host_buffers_match_device_buffers(subrays, n):
+    # host (pageable numpy / pinned torch) buffers go through the library's
+    # chunked, double-buffered staging pipeline; 279 subrays x 25000 pulses
+    # spans three chunks
+    import torch
     h = _h()
     w = workload("C3", 0.03)
     from gpu_util import scene_for
     sc = scene_for(w)
-    o, d, t = w.pulses(100, 3000)
-    dev_out, _ = h.simulate(sc, w.params, _dev(o), _dev(d), _dev(t), pulse_index_base=100,
+    p = replace(w.params, subray_count=subrays)
+    o, d, t = w.pulses(100, n)
+    dev_out, _ = h.simulate(sc, p, _dev(o), _dev(d), _dev(t), pulse_index_base=100,
                             subray_hits=True)
-    host_out = h.alloc_outputs(3000, h.make_params(w.params), device="cpu", subray_hits=True)
-    h.simulate(sc, w.params, o, d, t, pulse_index_base=100, outputs=host_out)
-    a, b = dev_out.numpy(), host_out.numpy()
-    for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
-        assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+    a = dev_out.numpy()
+    host_out = h.alloc_outputs(n, h.make_params(p), device="cpu", subray_hits=True)
+    h.simulate(sc, p, o, d, t, pulse_index_base=100, outputs=host_out)
+    pin_out = h.alloc_outputs(n, h.make_params(p), device="cpu", subray_hits=True,
+                              pin_memory=True)
+    h.simulate(sc, p, *(torch.from_numpy(x).pin_memory() for x in (o, d, t)),
+               pulse_index_base=100, outputs=pin_out)
+    for b in (host_out.numpy(), pin_out.numpy()):
+        for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
+            assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
 
 
 def test_waveform_output_optional_binning_still_runs():

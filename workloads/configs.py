@@ -72,10 +72,12 @@ class Workload:
         if count is None:
             count = self.n_pulses - start
         idx = np.arange(start, start + count, dtype=np.int64)
-        return self._pulse_fn(idx)
+        return self.pulses_at(idx)
 
     def pulses_at(self, ids: np.ndarray):
-        return self._pulse_fn(np.asarray(ids, np.int64))
+        o, d, t = self._pulse_fn(np.asarray(ids, np.int64))
+        return (np.ascontiguousarray(o, np.float32), np.ascontiguousarray(d, np.float32),
+                np.ascontiguousarray(t, np.float64))
 
 
 def _rng(seed: int, cfg: int, stream: int) -> np.random.Generator:
