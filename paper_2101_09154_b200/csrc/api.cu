@@ -41,11 +41,13 @@ struct helios_scene_s {
     size_t bytes;
     bool busy;
     cudaStream_t copy;  // non-blocking copy stream for host staging (lazy)
+    cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
   };
   std::mutex mu;
   std::vector<Slot> slots;
 
-  cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy) {
+  cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy,
+                      cudaStream_t* wave) {
     std::lock_guard<std::mutex> g(mu);
     Slot* use = nullptr;
     for (Slot& sl : slots)
@@ -54,7 +56,7 @@ struct helios_scene_s {
         break;
       }
     if (!use) {
-      slots.push_back(Slot{s, nullptr, 0, false, nullptr});
+      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
@@ -72,6 +74,11 @@ struct helios_scene_s {
       }
       *copy = use->copy;
     }
+    if (!use->wave) {
+      cudaError_t e = cudaStreamCreateWithFlags(&use->wave, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    *wave = use->wave;
     use->busy = true;
     *out = use->ptr;
     return cudaSuccess;
@@ -91,6 +98,10 @@ struct helios_scene_s {
       if (sl.copy) {
         cudaStreamSynchronize(sl.copy);
         cudaStreamDestroy(sl.copy);
+      }
+      if (sl.wave) {
+        cudaStreamSynchronize(sl.wave);
+        cudaStreamDestroy(sl.wave);
       }
       cudaFree(sl.ptr);
     }
@@ -470,7 +481,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const double beta = params->divergence_rad;
   const double K = params->efficiency * params->receiver_diameter_m * params->receiver_diameter_m /
                    (4.0 * kPi * beta * beta);  // Eq. 7 (R14)
-  const WavePlan plan = plan_waveform(d.n_bins, N, d.taps);
+  WavePlan plan = plan_waveform(d.n_bins, N, d.taps);
   if (plan.warps == 0)
     return fail(HELIOS_ERR_CUDA, "helios_simulate: waveform kernel cannot be configured");
 
@@ -511,17 +522,20 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const size_t o_err = carve(sizeof(unsigned));
   const size_t o_cnt = carve(sizeof(unsigned long long) * 8);
   const size_t o_ws = carve(plan.scratch_bytes);
-  const size_t o_rec = carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0);
+  // two record buffers: K6 of chunk c+1 overlaps K7 of chunk c
+  const size_t o_rec[2] = {carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0),
+                           carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0)};
   for (Arr& a : arrs)
     if (a.staged)
       for (int k = 0; k < 2; ++k) a.off[k] = carve(a.per_pulse * chunk);
 
   char* buf = nullptr;
-  cudaStream_t cs = nullptr;
-  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr);
+  cudaStream_t cs = nullptr, ws = nullptr;
+  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr, &ws);
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
+    cudaStreamSynchronize(ws);
     if (cs) cudaStreamSynchronize(cs);
     sc->release(s);
   };
@@ -578,29 +592,34 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   wa.max_returns = R;
   wa.counters = counters ? d_cnt + 4 : nullptr;
 
-  // per-kernel device time (CUDA events on the launching stream)
-  std::vector<cudaEvent_t> ev;
-  auto mark = [&]() {
+  // per-kernel device time (CUDA events on each kernel's stream)
+  std::vector<cudaEvent_t> ev_t, ev_w;
+  auto mark = [&](std::vector<cudaEvent_t>& v, cudaStream_t st) {
     if (!stats) return;
     cudaEvent_t x;
     if (cudaEventCreate(&x) == cudaSuccess) {
-      cudaEventRecord(x, s);
-      ev.push_back(x);
+      cudaEventRecord(x, st);
+      v.push_back(x);
     }
   };
-  // staging pipeline events (copy stream <-> compute stream)
-  cudaEvent_t in_done[2] = {nullptr, nullptr}, k_done[2] = {nullptr, nullptr},
-              out_done[2] = {nullptr, nullptr};
-  if (any_staged)
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+  // Stream graph per chunk c (slot = c & 1):
+  //   s  : [wait in_done]  [wait w_done(c-2)]  K6(c)  -> t_done
+  //   ws : wait t_done  [wait out_done(c-2)]   K7(c)  -> w_done
+  //   cs : wait w_done(c-1) -> H2D(c+1) -> in_done ; wait w_done(c) -> D2H(c) -> out_done
+  // so K7(c) runs concurrently with K6(c+1) and the copies with both.
+  cudaEvent_t in_done[2] = {}, t_done[2] = {}, w_done[2] = {}, out_done[2] = {};
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess && any_staged) {
       e = cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&k_done[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
     }
+  }
   // the copy stream must not start before the setup work on `s`
   if (any_staged && e == cudaSuccess) {
-    e = cudaEventRecord(k_done[1], s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, k_done[1], 0);
+    e = cudaEventRecord(t_done[1], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, t_done[1], 0);
   }
   auto dev_ptr = [&](const Arr& a, int slot, uint64_t b) -> char* {
     if (!a.user) return nullptr;
@@ -619,9 +638,25 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   };
 
   // traversal mode: warp-cooperative packets (default) or per-ray threads;
-  // HELIOS_TRAVERSAL=ray selects the latter (A/B measurements)
+  // HELIOS_TRAVERSAL=ray selects the latter (A/B measurements).
   bool packet = true;
   if (const char* v = getenv("HELIOS_TRAVERSAL")) packet = strcmp(v, "ray") != 0;
+  // K7 overlaps K6 on its own stream, except on voxel scenes: there K6 is
+  // ALU-bound (fp64 DDA + Philox) and a concurrent K7 costs more than it
+  // hides (measured: profiles/r01_overlap_ab.txt).  HELIOS_SERIAL=0/1 forces.
+  bool serial = sc->d_pad != nullptr;
+  if (const char* v = getenv("HELIOS_SERIAL")) serial = atoi(v) != 0;
+  if (serial) ws = s;
+  if (ws != s) {
+    // optional cap on K7's persistent grid while it shares the SMs with K6
+    // (HELIOS_WAVE_BLOCKS_PER_SM; default: full grid, measured best)
+    int bps = 0;
+    if (const char* v = getenv("HELIOS_WAVE_BLOCKS_PER_SM")) bps = atoi(v);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (bps > 0) plan.grid_cap = (uint32_t)(sms * bps);
+  }
   uint32_t launches = 0;
   const uint64_t n_chunks = (n + chunk - 1) / chunk;
   if (any_staged && e == cudaSuccess) e = copy_in(0, 0);
@@ -629,23 +664,22 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     const uint64_t b = c * chunk;
     const uint64_t m = std::min(chunk, n - b);
     const int slot = (int)(c & 1);
-    if (any_staged) {
-      // inputs of this chunk are on the device; the D2H of chunk c-2 (same
-      // slot) has drained the output buffers we are about to overwrite
-      e = cudaStreamWaitEvent(s, in_done[slot], 0);
-      if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(s, out_done[slot], 0);
-      if (e != cudaSuccess) break;
-    }
+    if (any_staged) e = cudaStreamWaitEvent(s, in_done[slot], 0);
+    if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(s, w_done[slot], 0);
+    if (e != cudaSuccess) break;
     ta.origin = (const float*)dev_ptr(arrs[0], slot, b);
     ta.direction = (const float*)dev_ptr(arrs[1], slot, b);
     ta.n_pulses = m;
     ta.pulse_base = pulses->pulse_index_base + b;
-    ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec)
+    ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec[slot])
                      : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
-    mark();
+    mark(ev_t, s);
     e = launch_trace(ta, counters, packet, s);
+    mark(ev_t, s);
+    if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
+    if (e == cudaSuccess && any_staged && c >= 2) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
     if (e != cudaSuccess) break;
-    mark();
     wa.rec = ta.out;
     wa.n_pulses = m;
     wa.time_s = (const double*)dev_ptr(arrs[2], slot, b);
@@ -653,25 +687,30 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     wa.returns = (helios_return*)dev_ptr(arrs[4], slot, b);
     wa.first_bin = (int64_t*)dev_ptr(arrs[5], slot, b);
     wa.waveform = (float*)dev_ptr(arrs[6], slot, b);
-    e = launch_waveform(wa, plan, d_wscratch, s);
-    mark();
+    mark(ev_w, ws);
+    e = launch_waveform(wa, plan, d_wscratch, ws);
+    mark(ev_w, ws);
+    if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], ws);
     launches += 2;
     if (e != cudaSuccess || !any_staged) continue;
-    e = cudaEventRecord(k_done[slot], s);
-    // prefetch the next chunk's inputs into the other slot (its previous
-    // user, chunk c-1, has been consumed by the kernels already enqueued)
-    if (e == cudaSuccess && c + 1 < n_chunks) {
-      if (c >= 1) e = cudaStreamWaitEvent(cs, k_done[slot ^ 1], 0);
+    // prefetch the next chunk's inputs into the other slot once chunk c-1's
+    // kernels (K6 reads origin/direction, K7 reads time) are done with it
+    if (c + 1 < n_chunks) {
+      if (c >= 1) e = cudaStreamWaitEvent(cs, w_done[slot ^ 1], 0);
       if (e == cudaSuccess) e = copy_in(b + chunk, slot ^ 1);
     }
     // drain this chunk's outputs
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, k_done[slot], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, w_done[slot], 0);
     for (const Arr& a : arrs)
       if (e == cudaSuccess && a.staged && !a.in)
         e = cudaMemcpyAsync((char*)a.user + a.per_pulse * b, buf + a.off[slot], a.per_pulse * m,
                             cudaMemcpyDeviceToHost, cs);
     if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], cs);
   }
+  // join: the caller's stream is ordered after every kernel of this call
+  if (e == cudaSuccess && ws != s && n_chunks > 0)
+    for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
+      e = cudaStreamWaitEvent(s, w_done[k], 0);
   unsigned herr = 0;
   unsigned long long hcnt[8] = {0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
@@ -679,19 +718,22 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && cs) e = cudaStreamSynchronize(cs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ws);
   double t_trace = 0.0, t_wave = 0.0;
-  for (size_t i = 0; i + 2 < ev.size(); i += 3) {
-    float a = 0.f, b2 = 0.f;
-    if (cudaEventElapsedTime(&a, ev[i], ev[i + 1]) == cudaSuccess &&
-        cudaEventElapsedTime(&b2, ev[i + 1], ev[i + 2]) == cudaSuccess) {
-      t_trace += a;
-      t_wave += b2;
-    }
+  for (size_t i = 0; i + 1 < ev_t.size(); i += 2) {
+    float a = 0.f;
+    if (cudaEventElapsedTime(&a, ev_t[i], ev_t[i + 1]) == cudaSuccess) t_trace += a;
   }
-  for (cudaEvent_t x : ev) cudaEventDestroy(x);
+  for (size_t i = 0; i + 1 < ev_w.size(); i += 2) {
+    float a = 0.f;
+    if (cudaEventElapsedTime(&a, ev_w[i], ev_w[i + 1]) == cudaSuccess) t_wave += a;
+  }
+  for (cudaEvent_t x : ev_t) cudaEventDestroy(x);
+  for (cudaEvent_t x : ev_w) cudaEventDestroy(x);
   for (int k = 0; k < 2; ++k) {
     if (in_done[k]) cudaEventDestroy(in_done[k]);
-    if (k_done[k]) cudaEventDestroy(k_done[k]);
+    if (t_done[k]) cudaEventDestroy(t_done[k]);
+    if (w_done[k]) cudaEventDestroy(w_done[k]);
     if (out_done[k]) cudaEventDestroy(out_done[k]);
   }
   cudaGetLastError();

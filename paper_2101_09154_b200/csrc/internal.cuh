@@ -110,6 +110,7 @@ struct WavePlan {
   size_t smem;          // dynamic shared memory per block
   uint32_t grid;        // persistent grid (SMs x occupancy)
   size_t scratch_bytes; // per-warp global rows for wide pulses
+  uint32_t grid_cap;    // 0 = full persistent grid; else max blocks (overlap with K6)
 };
 WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);
 bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps);

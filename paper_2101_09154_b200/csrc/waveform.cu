@@ -305,6 +305,7 @@ cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scrat
   if (pl.warps == 0) return cudaErrorInvalidValue;
   uint64_t want = (a.n_pulses + pl.warps - 1) / pl.warps;
   uint64_t grid = pl.grid;
+  if (pl.grid_cap && pl.grid_cap < grid) grid = pl.grid_cap;
   if (want < grid) grid = want;
   k_waveform<<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
   return cudaGetLastError();
