@@ -155,8 +155,10 @@ def run_reference(args):
     N = w.params.subray_count
     threads = os.cpu_count() or 1
     rng = np.random.default_rng(1)
-    # each step: a bounded random sample of the workload, ~args.ref_budget s
-    per_step, _ = oracle_sample(w, threads, args.ref_budget, seed=123)
+    # each step: a bounded random sample of the workload, sized so that the
+    # whole --warmup + --steps run takes about 2.5 minutes of oracle work
+    budget = max(1.0, min(args.ref_budget, 150.0 / max(1, args.steps + args.warmup)))
+    per_step, _ = oracle_sample(w, threads, budget, seed=123)
     times = []
     for i in range(args.warmup + args.steps):
         ids = np.sort(rng.choice(w.n_pulses, per_step, replace=False))
@@ -272,6 +274,19 @@ def run_ours(args):
     b_pulse = (32 + 8 + 1 + 4 * n_bins + 32 * p.max_returns) * B * args.steps
     peak, peak_src = peaks()
     ach_trace = b_trace / (trace_ms / 1e3) / 1e9
+    n_trace_launches = max(1, launches // 2)
+    traffic, limiter = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f).get(args.config)
+        if tj:
+            kt = tj["k_trace"]
+            traffic = kt["dram_bytes"] / kt["units"] * (sub_rank / n_trace_launches)
+            limiter = {"issue_slots_busy": kt["issue_slots_busy"],
+                       "dram_bytes_per_subray": kt["dram_bytes"] / kt["units"],
+                       "l1_hit": kt["l1_hit"], "source": tj["source"]}
+    except Exception:
+        pass
     r1 = (b_ray + b_pulse) / (ms / 1e3) / 1e9 / peak
 
     # ---- end to end through the C ABI with host buffers (copies inside)
@@ -324,9 +339,10 @@ def run_ours(args):
                        "build_ms": round(info.build_ms, 2), "gen_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "kernel": "k_trace", "achieved": ach_trace,
                          "peak": peak, "unit": "GB/s", "frac": ach_trace / peak,
-                         "traffic": None, "peak_source": peak_src,
-                         "bytes_per_launch": b_trace / max(1, launches // 2),
-                         "avg_launch_ms": trace_ms / max(1, launches // 2),
+                         "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_launch": b_trace / n_trace_launches,
+                         "avg_launch_ms": trace_ms / n_trace_launches,
+                         "ncu_limiter": limiter,
                          "share_of_step": trace_ms / ms if ms > 0 else None,
                          "waveform_share_of_step": wave_ms / ms if ms > 0 else None,
                          "nodes_per_ray": nodes / sub_rank, "tris_per_ray": tris / sub_rank,
