@@ -262,14 +262,16 @@ def run_ours(args):
 
     # ---- algorithmic bytes (instrumented, untimed re-run of the same batches)
     nodes = tris = vox = f64 = 0
+    node_bytes = 64
     for i in range(args.warmup, steps_total):
         st = step(i, counters=True)
+        node_bytes = st.node_bytes or 64
         nodes += st.nodes_visited
         tris += st.tris_tested
         vox += st.voxel_steps
         f64 += st.fp64_tests
     sub_rank = B * N * args.steps
-    b_ray = 64 * nodes + 48 * tris + 4 * vox
+    b_ray = node_bytes * nodes + 48 * tris + 4 * vox
     b_trace = b_ray + 24 * B * args.steps + 16 * sub_rank  # + pulse inputs + records
     b_pulse = (32 + 8 + 1 + 4 * n_bins + 32 * p.max_returns) * B * args.steps
     peak, peak_src = peaks()
@@ -345,7 +347,8 @@ def run_ours(args):
                          "ncu_limiter": limiter,
                          "share_of_step": trace_ms / ms if ms > 0 else None,
                          "waveform_share_of_step": wave_ms / ms if ms > 0 else None,
-                         "nodes_per_ray": nodes / sub_rank, "tris_per_ray": tris / sub_rank,
+                         "nodes_per_ray": nodes / sub_rank, "node_bytes": node_bytes,
+                         "tris_per_ray": tris / sub_rank,
                          "voxel_steps_per_ray": vox / sub_rank,
                          "fp64_tests_per_ray": f64 / sub_rank,
                          "step_R1": r1},

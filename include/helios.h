@@ -193,6 +193,8 @@ typedef struct {
                                 (node / triangle / voxel-step counters; slower:
                                 for roofline byte accounting only)               */
   uint32_t kernel_launches;  /* out: kernels launched by this call               */
+  uint32_t node_bytes;       /* out: bytes per BVH node of the traversal that ran */
+  uint32_t reserved_;
   uint64_t pulses, subrays;
   uint64_t subray_hits, voxel_returns, returns;     /* only with collect_counters */
   uint64_t nodes_visited, tris_tested, voxel_steps; /* only with collect_counters */

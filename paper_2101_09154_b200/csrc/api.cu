@@ -285,6 +285,7 @@ void free_scene(helios_scene sc, cudaStream_t s) {
   cudaFreeAsync(sc->d_lut, s);
   cudaFreeAsync(sc->bvh.tris, s);
   cudaFreeAsync(sc->bvh.nodes, s);
+  cudaFreeAsync(sc->bvh.nodes4, s);
   cudaStreamSynchronize(s);
 }
 
@@ -558,6 +559,8 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   ta.tris = sc->bvh.tris;
   ta.nodes = sc->bvh.nodes;
   ta.root = sc->bvh.root;
+  ta.nodes4 = sc->bvh.nodes4;
+  ta.root4 = sc->bvh.root4;
   ta.n_tris = sc->n_tris;
   ta.pad = sc->d_pad;
   ta.nx = sc->nx;
@@ -639,8 +642,14 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
 
   // traversal mode: warp-cooperative packets (default) or per-ray threads;
   // HELIOS_TRAVERSAL=ray selects the latter (A/B measurements).
-  bool packet = true;
-  if (const char* v = getenv("HELIOS_TRAVERSAL")) packet = strcmp(v, "ray") != 0;
+  // traversal: 1 = packet over the binary tree (default, measured best),
+  // 2 = packet over the 4-wide tree (needs HELIOS_BVH4=1 at build time),
+  // 0 = per-ray threads; HELIOS_TRAVERSAL=packet2|packet4|ray
+  int mode = 1;
+  if (const char* v = getenv("HELIOS_TRAVERSAL")) {
+    if (!strcmp(v, "ray")) mode = 0;
+    else if (!strcmp(v, "packet4") && (sc->bvh.nodes4 || ref_is_leaf(sc->bvh.root))) mode = 2;
+  }
   // K7 overlaps K6 on its own stream, except on voxel scenes: there K6 is
   // ALU-bound (fp64 DDA + Philox) and a concurrent K7 costs more than it
   // hides (measured: profiles/r01_overlap_ab.txt).  HELIOS_SERIAL=0/1 forces.
@@ -674,7 +683,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec[slot])
                      : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
     mark(ev_t, s);
-    e = launch_trace(ta, counters, packet, s);
+    e = launch_trace(ta, counters, mode, s);
     mark(ev_t, s);
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
@@ -743,6 +752,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     stats->pulses = n;
     stats->subrays = n * N;
     stats->kernel_launches = launches;
+    stats->node_bytes = mode == 2 ? (uint32_t)sizeof(Node4) : (uint32_t)sizeof(Node);
     stats->trace_ms = t_trace;
     stats->waveform_ms = t_wave;
     stats->nodes_visited = hcnt[0];

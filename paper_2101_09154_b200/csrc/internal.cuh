@@ -21,7 +21,10 @@ namespace helios {
 
 constexpr int kMaxSubrays = 512;      // >= largest supported count (279)
 constexpr int kStackSize = 64;        // LBVH depth bound (checked at build)
-constexpr int kLeafMax = 4;           // triangles per collapsed leaf
+#ifndef HELIOS_LEAF_MAX
+#define HELIOS_LEAF_MAX 2  // measured best (profiles/r01_leaf_ab.txt)
+#endif
+constexpr int kLeafMax = HELIOS_LEAF_MAX;  // triangles per collapsed leaf (<= 8)
 constexpr int kMortonBits = 21;       // per axis (63-bit codes)
 constexpr int kMaxLut = 4096;
 constexpr int kMaxTaps = 8192;        // L_p bound (validated)
@@ -33,6 +36,11 @@ struct __align__(16) TriRecord {
 };
 struct __align__(16) Node {
   float4 xy0, xy1, z01, ref;
+};
+// 4-wide node (128 B = 8 x float4), SoA over the 4 children; unused slots
+// carry kEmptyRef.  Collapsed on the device from the binary LBVH.
+struct __align__(16) Node4 {
+  float4 lox, hix, loy, hiy, loz, hiz, ref, pad;
 };
 
 // leaf reference: bit 31 set, bits [3,31) = first triangle, bits [0,3) = count-1
@@ -61,6 +69,8 @@ struct TraceArgs {
   const TriRecord* tris;
   const Node* nodes;
   int32_t root;          // root node ref (internal index or leaf ref)
+  const Node4* nodes4;
+  int32_t root4;
   uint32_t n_tris;
   const float* pad;      // voxel grid or nullptr
   uint32_t nx, ny, nz;
@@ -103,7 +113,8 @@ struct WaveArgs {
 };
 
 // launchers (trace.cu / waveform.cu)
-cudaError_t launch_trace(const TraceArgs& a, bool instrumented, bool packet, cudaStream_t s);
+// mode: 0 per-ray binary, 1 packet binary, 2 packet 4-wide
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s);
 
 struct WavePlan {
   int warps;            // warps per block (0 = does not fit)
@@ -125,6 +136,9 @@ struct BuildResult {
   int32_t root;
   uint32_t max_depth;
   float ms;
+  Node4* nodes4;     // device, 4-wide collapse (nullptr if not built)
+  uint32_t n_nodes4;
+  int32_t root4;
 };
 cudaError_t build_lbvh(const float* d_tri_xyz, const float* d_refl, uint32_t n,
                        cudaStream_t s, BuildResult* out, char* err, size_t err_len);

@@ -264,6 +264,96 @@ __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict
   out[k] = rec;
 }
 
+// ---- 4-wide collapse (top-down, one kernel per level) ----------------------
+// Each queue entry (binary node b, wide node w) expands b's children greedily:
+// while fewer than 4, replace the internal child with the largest box surface
+// area by its two children.  Internal children of the result become new wide
+// nodes (queued for the next level).
+__device__ __forceinline__ float box_area(const float* b) {
+  const float dx = b[1] - b[0], dy = b[3] - b[2], dz = b[5] - b[4];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__device__ __forceinline__ void child_of(const Node& nd, int k, int32_t* ref, float* b) {
+  if (k == 0) {
+    b[0] = nd.xy0.x; b[1] = nd.xy0.y; b[2] = nd.xy0.z; b[3] = nd.xy0.w;
+    b[4] = nd.z01.x; b[5] = nd.z01.y;
+    *ref = __float_as_int(nd.ref.x);
+  } else {
+    b[0] = nd.xy1.x; b[1] = nd.xy1.y; b[2] = nd.xy1.z; b[3] = nd.xy1.w;
+    b[4] = nd.z01.z; b[5] = nd.z01.w;
+    *ref = __float_as_int(nd.ref.y);
+  }
+}
+
+__global__ void k_collapse4(const Node* __restrict__ nodes, const int2* __restrict__ qin,
+                            uint32_t n_in, int2* __restrict__ qout, unsigned* __restrict__ n_out,
+                            unsigned* __restrict__ n_wide, Node4* __restrict__ wide) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_in) return;
+  const int2 e = qin[t];
+  int32_t ref[4];
+  float box[4][6];
+  int cnt = 2;
+  {
+    const Node nd = nodes[e.x];
+    child_of(nd, 0, &ref[0], box[0]);
+    child_of(nd, 1, &ref[1], box[1]);
+  }
+  while (cnt < 4) {
+    int pick = -1;
+    float best = -1.0f;
+    for (int i = 0; i < cnt; ++i)
+      if (!ref_is_leaf(ref[i])) {
+        const float a = box_area(box[i]);
+        if (a > best) {
+          best = a;
+          pick = i;
+        }
+      }
+    if (pick < 0) break;
+    const Node nd = nodes[ref[pick]];
+    child_of(nd, 0, &ref[pick], box[pick]);
+    child_of(nd, 1, &ref[cnt], box[cnt]);
+    ++cnt;
+  }
+  float lo[3][4], hi[3][4];
+  int32_t out_ref[4];
+  for (int i = 0; i < 4; ++i) {
+    if (i < cnt) {
+      for (int a = 0; a < 3; ++a) {
+        lo[a][i] = box[i][2 * a];
+        hi[a][i] = box[i][2 * a + 1];
+      }
+      if (ref_is_leaf(ref[i])) {
+        out_ref[i] = ref[i];
+      } else {
+        const unsigned w = atomicAdd(n_wide, 1u);
+        const unsigned q = atomicAdd(n_out, 1u);
+        qout[q] = make_int2(ref[i], (int)w);
+        out_ref[i] = (int32_t)w;
+      }
+    } else {
+      for (int a = 0; a < 3; ++a) {
+        lo[a][i] = 0.0f;
+        hi[a][i] = 0.0f;
+      }
+      out_ref[i] = kEmptyRef;
+    }
+  }
+  Node4 w;
+  w.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+  w.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+  w.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+  w.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+  w.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+  w.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+  w.ref = make_float4(__int_as_float(out_ref[0]), __int_as_float(out_ref[1]),
+                      __int_as_float(out_ref[2]), __int_as_float(out_ref[3]));
+  w.pad = make_float4(0.f, 0.f, 0.f, 0.f);
+  wide[e.y] = w;
+}
+
 template <class T>
 cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
   return cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), s);
@@ -279,6 +369,9 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   out->root = kEmptyRef;
   out->max_depth = 0;
   out->ms = 0.f;
+  out->nodes4 = nullptr;
+  out->n_nodes4 = 0;
+  out->root4 = kEmptyRef;
   if (n == 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -287,7 +380,10 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   uint32_t *idx = nullptr, *idx_s = nullptr;
   int *child = nullptr, *parent_int = nullptr, *parent_leaf = nullptr, *range = nullptr;
   float *leafbox = nullptr, *nodebox = nullptr;
-  unsigned *flags = nullptr, *dmax = nullptr;
+  unsigned *flags = nullptr, *dmax = nullptr, *wcnt = nullptr;
+  int2 *qa = nullptr, *qb = nullptr;
+  Node4* wide_tmp = nullptr;
+  unsigned hw[2] = {0, 0};
   void* temp = nullptr;
   size_t temp_bytes = 0;
   const int T = 256;
@@ -332,6 +428,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
                                      3 * bits, s));
   if (n <= (uint32_t)kLeafMax) {
     out->root = leaf_ref(0, n);
+    out->root4 = out->root;
     out->max_depth = 0;
   } else {
     CK(dalloc(&child, 2ull * (n - 1), s));
@@ -357,6 +454,40 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     CK(cudaMemcpyAsync(&hdepth, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     out->n_nodes = n - 1;
     out->root = 0;
+    // 4-wide collapse, level by level (opt-in: HELIOS_BVH4=1; measured no faster
+    // than packet traversal of the binary tree, profiles/r01_wide_ab.txt)
+    const char* w4 = getenv("HELIOS_BVH4");
+    if (w4 && atoi(w4)) {
+    CK(dalloc(&qa, n - 1, s));
+    CK(dalloc(&qb, n - 1, s));
+    CK(dalloc(&wcnt, 2, s));
+    CK(dalloc(&wide_tmp, n - 1, s));
+    {
+      const int2 root_entry = make_int2(0, 0);
+      const unsigned init[2] = {0u, 1u};  // next-queue size, wide nodes allocated
+      CK(cudaMemcpyAsync(qa, &root_entry, sizeof(int2), cudaMemcpyHostToDevice, s));
+      uint32_t n_in = 1;
+      while (n_in > 0) {
+        CK(cudaMemcpyAsync(wcnt, init, sizeof(unsigned), cudaMemcpyHostToDevice, s));
+        if (hw[1] == 0) CK(cudaMemcpyAsync(wcnt + 1, init + 1, sizeof(unsigned),
+                                           cudaMemcpyHostToDevice, s));
+        k_collapse4<<<(n_in + T - 1) / T, T, 0, s>>>(out->nodes, qa, n_in, qb, wcnt, wcnt + 1,
+                                                    wide_tmp);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hw, wcnt, sizeof(hw), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        n_in = hw[0];
+        int2* tq = qa;
+        qa = qb;
+        qb = tq;
+      }
+    }
+    out->n_nodes4 = hw[1];
+    CK(dalloc(&out->nodes4, out->n_nodes4, s));
+    CK(cudaMemcpyAsync(out->nodes4, wide_tmp, sizeof(Node4) * out->n_nodes4,
+                       cudaMemcpyDeviceToDevice, s));
+    out->root4 = 0;
+    }
   }
   k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s, n, out->tris);
   CK(cudaGetLastError());
@@ -385,13 +516,19 @@ done:
   cudaFreeAsync(nodebox, s);
   cudaFreeAsync(flags, s);
   cudaFreeAsync(dmax, s);
+  cudaFreeAsync(wcnt, s);
+  cudaFreeAsync(qa, s);
+  cudaFreeAsync(qb, s);
+  cudaFreeAsync(wide_tmp, s);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   if (e != cudaSuccess) {
     cudaFreeAsync(out->tris, s);
     cudaFreeAsync(out->nodes, s);
+    cudaFreeAsync(out->nodes4, s);
     out->tris = nullptr;
     out->nodes = nullptr;
+    out->nodes4 = nullptr;
   }
   cudaStreamSynchronize(s);
   return e;

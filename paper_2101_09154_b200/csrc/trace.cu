@@ -24,6 +24,9 @@ namespace helios {
 namespace {
 
 constexpr float kBoxSlack = 1e-6f;  // >> 4 * 2^-24 relative error of an fp32 slab value
+// lazy culling of popped stack entries compares the stored (already widened)
+// entry distance with t_best rounded to fp32, widened again
+constexpr float kCullSlack = 1.0f + 4.0f * kBoxSlack;
 
 // fp64 helpers with explicit round-to-nearest intrinsics: no FMA contraction,
 // so every expression below evaluates exactly like the oracle's (same
@@ -318,10 +321,131 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   }
 }
 
+// 4-wide variant of the packet traversal: each step tests the 4 children of
+// a Node4 (one 128-B broadcast load), visits the hit children nearest-first
+// (ordered by the entry distance of the lowest lane that hits each child) and
+// pushes the others with their lane masks.
+template <bool INSTR>
+__device__ __forceinline__ void traverse_packet4(const TraceArgs& a, unsigned m, const D3& O,
+                                                 const D3& D, const F3& O32, const F3& D32,
+                                                 float dl1, float ix, float iy, float iz,
+                                                 double& t_best, uint32_t& best_id,
+                                                 uint32_t& best_k, unsigned long long& c_nodes,
+                                                 unsigned long long& c_tris,
+                                                 unsigned long long& c_f64) {
+  const unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int32_t stA_r = 0, stB_r = 0;
+  unsigned stA_m = 0, stB_m = 0;
+  int sp = 0;
+  int32_t ref = a.root4;
+  float tstk[kStackSize];  // this lane's entry distance of every pushed child
+  auto push = [&](int32_t r, unsigned mk, float tl) {
+    if (lane == (sp & 31)) {
+      if (sp < 32) {
+        stA_r = r;
+        stA_m = mk;
+      } else {
+        stB_r = r;
+        stB_m = mk;
+      }
+    }
+    tstk[sp] = tl;
+    ++sp;
+  };
+  // pop with lazy culling: lanes whose t_best is already nearer than their
+  // entry distance into the child leave its mask; empty entries are skipped
+  // without loading the node.  Returns false when the stack is exhausted.
+  auto pop = [&]() -> bool {
+    for (;;) {
+      if (sp == 0) return false;
+      --sp;
+      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+      const bool keep = ((m >> lane) & 1u) && !(tstk[sp] > (float)t_best * kCullSlack);
+      m = __ballot_sync(kFull, keep);
+      if (m) return true;
+    }
+  };
+  for (;;) {
+    const bool mine = (m >> lane) & 1u;
+    if (ref_is_leaf(ref)) {
+      if (mine) {
+        const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
+        const float t_hi = __double2float_ru(t_best);
+        for (uint32_t k = first; k < first + cnt; ++k) {
+          const TriRecord tr = load_tri(a.tris, k);
+          if (INSTR) ++c_tris;
+          if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
+          if (INSTR) ++c_f64;
+          const double t = mt64(O, D, tr);
+          if (t > 0.0) {
+            const uint32_t id = __float_as_uint(tr.a.w);
+            if (t < t_best || (t == t_best && id < best_id)) {
+              t_best = t;
+              best_id = id;
+              best_k = k;
+            }
+          }
+        }
+      }
+      if (!pop()) break;
+      continue;
+    }
+    const Node4* nd = a.nodes4 + ref;
+    const float4 lx = __ldg(&nd->lox), hx = __ldg(&nd->hix), ly = __ldg(&nd->loy),
+                 hy = __ldg(&nd->hiy), lz = __ldg(&nd->loz), hz = __ldg(&nd->hiz),
+                 rf = __ldg(&nd->ref);
+    const int32_t r[4] = {__float_as_int(rf.x), __float_as_int(rf.y), __float_as_int(rf.z),
+                          __float_as_int(rf.w)};
+    float t[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+    if (mine) {
+      if (INSTR) ++c_nodes;
+      const float tb = (float)t_best;
+      t[0] = box_enter(lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, O32.x, O32.y, O32.z, ix, iy, iz, tb);
+      t[1] = box_enter(lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, O32.x, O32.y, O32.z, ix, iy, iz, tb);
+      if (r[2] != kEmptyRef)
+        t[2] = box_enter(lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, O32.x, O32.y, O32.z, ix, iy, iz, tb);
+      if (r[3] != kEmptyRef)
+        t[3] = box_enter(lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, O32.x, O32.y, O32.z, ix, iy, iz, tb);
+    }
+    // per child: lane mask and a warp-uniform ordering key
+    unsigned mk[4];
+    float key[4];
+    int32_t rr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mk[i] = __ballot_sync(kFull, t[i] < INFINITY);
+      const float ti = __shfl_sync(kFull, t[i], mk[i] ? (__ffs(mk[i]) - 1) : 0);
+      key[i] = mk[i] ? ti : INFINITY;
+      rr[i] = r[i];
+    }
+    // sort the 4 (key, ref, mask, own t) tuples ascending (5-exchange network)
+#define HELIOS_CSWAP(i, j)                                            \
+    if (key[j] < key[i]) {                                            \
+      const float tk = key[i]; key[i] = key[j]; key[j] = tk;          \
+      const int32_t trf = rr[i]; rr[i] = rr[j]; rr[j] = trf;          \
+      const unsigned tm = mk[i]; mk[i] = mk[j]; mk[j] = tm;           \
+      const float tt = t[i]; t[i] = t[j]; t[j] = tt;                  \
+    }
+    HELIOS_CSWAP(0, 1) HELIOS_CSWAP(2, 3) HELIOS_CSWAP(0, 2) HELIOS_CSWAP(1, 3) HELIOS_CSWAP(1, 2)
+#undef HELIOS_CSWAP
+    if (!mk[0]) {  // nothing hit (keys of misses are +inf, sorted last)
+      if (!pop()) break;
+      continue;
+    }
+    if (mk[3]) push(rr[3], mk[3], t[3]);
+    if (mk[2]) push(rr[2], mk[2], t[2]);
+    if (mk[1]) push(rr[1], mk[1], t[1]);
+    ref = rr[0];
+    m = mk[0];
+  }
+}
+
 #ifndef HELIOS_TRACE_MIN_BLOCKS
 #define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
 #endif
-template <bool INSTR, bool PACKET>
+template <bool INSTR, bool PACKET, bool WIDE>
 __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t total = a.n_pulses * (uint64_t)a.N;
@@ -376,9 +500,14 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
     const float dl1 = l1(D32);
     if (PACKET) {
       const unsigned m = __ballot_sync(0xffffffffu, valid);
-      if (m)
-        traverse_packet<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
-                               c_nodes, c_tris, c_f64);
+      if (m) {
+        if (WIDE)
+          traverse_packet4<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
+                                  c_nodes, c_tris, c_f64);
+        else
+          traverse_packet<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
+                                 c_nodes, c_tris, c_f64);
+      }
     } else {
       traverse_ray<INSTR>(a, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k, c_nodes,
                           c_tris, c_f64);
@@ -516,22 +645,20 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
 
 }  // namespace
 
-cudaError_t launch_trace(const TraceArgs& a, bool instrumented, bool packet, cudaStream_t s) {
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s) {
   const uint64_t total = a.n_pulses * (uint64_t)a.N;
   if (total == 0) return cudaSuccess;
   const unsigned T = 128;
   const uint64_t blocks = (total + T - 1) / T;
   if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-  if (packet) {
-    if (instrumented)
-      k_trace<true, true><<<(unsigned)blocks, T, 0, s>>>(a);
-    else
-      k_trace<false, true><<<(unsigned)blocks, T, 0, s>>>(a);
-  } else {
-    if (instrumented)
-      k_trace<true, false><<<(unsigned)blocks, T, 0, s>>>(a);
-    else
-      k_trace<false, false><<<(unsigned)blocks, T, 0, s>>>(a);
+  const unsigned g = (unsigned)blocks;
+  switch (mode * 2 + (instrumented ? 1 : 0)) {
+    case 0: k_trace<false, false, false><<<g, T, 0, s>>>(a); break;
+    case 1: k_trace<true, false, false><<<g, T, 0, s>>>(a); break;
+    case 2: k_trace<false, true, false><<<g, T, 0, s>>>(a); break;
+    case 3: k_trace<true, true, false><<<g, T, 0, s>>>(a); break;
+    case 4: k_trace<false, true, true><<<g, T, 0, s>>>(a); break;
+    default: k_trace<true, true, true><<<g, T, 0, s>>>(a); break;
   }
   return cudaGetLastError();
 }
