@@ -54,6 +54,7 @@ class OracleParams(ctypes.Structure):
         ("peak_power_w", _d), ("efficiency", _d), ("receiver_diameter_m", _d),
         ("wavelength_nm", _d), ("beam_waist_m", _d), ("focus_range_m", _d),
         ("seed", _u64), ("subray_count", _u32), ("max_returns", _u32),
+        ("fit_echo_width", _u32), ("pad_", _u32),
     ]
 
 
@@ -68,7 +69,7 @@ class OracleScene(ctypes.Structure):
 class OracleOutputs(ctypes.Structure):
     _fields_ = [(n, _vp) for n in (
         "n_returns", "k0", "waveform", "ret_range", "ret_time", "ret_intensity",
-        "ret_prim", "ret_number", "peak_margin", "attr_margin", "sub_range",
+        "ret_prim", "ret_number", "ret_width", "peak_margin", "attr_margin", "sub_range",
         "sub_amp", "sub_prim", "sub_k", "sub_ncand", "sub_gap", "sub_kmargin",
         "sub_umargin")]
 
@@ -102,6 +103,8 @@ def lib():
         L.oracle_g_function.argtypes = [_vp, _u32, _d]
         L.oracle_voxel_segments.restype = _i64
         L.oracle_voxel_segments.argtypes = [_vp, _vp, _vp, _vp, _d, _d, _vp, _vp, _vp, _i64]
+        L.oracle_fit_echo_width.restype = _d
+        L.oracle_fit_echo_width.argtypes = [_vp, _i64, _i64, _d, _d, _vp, _vp]
         L.oracle_waveform_bins.restype = _u32
         L.oracle_waveform_bins.argtypes = [_d, _d]
         L.oracle_simulate.restype = ctypes.c_int
@@ -221,6 +224,16 @@ def voxel_segments(o, d, n, origin, vs, t_max=float("inf")):
     return ta[:k].copy(), tb[:k].copy(), vid[:k].copy()
 
 
+def fit_echo_width(W, k: int, delta_ns: float, pulse_length_ns: float):
+    """(sigma, A, m) of the Gaussian fitted around bin k (R28)."""
+    W = np.ascontiguousarray(W, np.float64)
+    A = ctypes.c_double()
+    m = ctypes.c_double()
+    s = lib().oracle_fit_echo_width(_p(W), W.size, int(k), delta_ns, pulse_length_ns,
+                                    ctypes.byref(A), ctypes.byref(m))
+    return s, A.value, m.value
+
+
 def waveform_bins(window_ns: float, bin_ns: float) -> int:
     return int(lib().oracle_waveform_bins(window_ns, bin_ns))
 
@@ -236,6 +249,7 @@ class OracleResult:
     ret_intensity: np.ndarray
     ret_prim: np.ndarray
     ret_number: np.ndarray
+    ret_width: np.ndarray
     peak_margin: np.ndarray
     attr_margin: np.ndarray
     sub_range: np.ndarray
@@ -281,7 +295,8 @@ def simulate(scene, params, origins, directions, times, pulse_ids,
     sc.n_lut = 0 if lut is None else lut.size
     pr = OracleParams()
     for f, _ in OracleParams._fields_:
-        setattr(pr, f, getattr(params, f))
+        if f != "pad_":
+            setattr(pr, f, getattr(params, f))
     o = np.ascontiguousarray(origins, np.float32).reshape(n, 3)
     d = np.ascontiguousarray(directions, np.float32).reshape(n, 3)
     t = np.ascontiguousarray(times, np.float64).reshape(n)
@@ -291,7 +306,8 @@ def simulate(scene, params, origins, directions, times, pulse_ids,
         waveform=np.zeros((n, nb), np.float64) if want_waveform else None,
         ret_range=np.zeros((n, R)), ret_time=np.zeros((n, R)),
         ret_intensity=np.zeros((n, R)), ret_prim=np.zeros((n, R), np.uint32),
-        ret_number=np.zeros((n, R), np.int32), peak_margin=np.zeros(n),
+        ret_number=np.zeros((n, R), np.int32), ret_width=np.zeros((n, R)),
+        peak_margin=np.zeros(n),
         attr_margin=np.zeros(n), sub_range=np.zeros((n, N)), sub_amp=np.zeros((n, N)),
         sub_prim=np.zeros((n, N), np.uint32), sub_k=np.zeros((n, N), np.int64),
         sub_ncand=np.zeros((n, N), np.int32), sub_gap=np.zeros((n, N)),

@@ -384,6 +384,102 @@ int64_t oracle_voxel_segments(const double o_in[3], const double d_in[3],
 }
 
 /* ------------------------------------------------------------------------
+ * Echo width ("Optionally, a Gaussian may be fitted to the resulting
+ * waveform, to get a measure of echo width (i.e. standard deviation of the
+ * Gaussian)"; "non-linear least squares").  Reading R28:
+ * window = bins k-w..k+w (clipped), w = ceil(3 pulse_length / Delta);
+ * x_i = (i - k) Delta (ns), y_i = W[i];  g(x) = A exp(-(x - m)^2 / (2 s^2));
+ * Levenberg-Marquardt from A = W[k], m = 0, s = pulse_length / (2 sqrt(2 ln 2)),
+ * lambda = 1e-3, step (J^T J + lambda diag(J^T J)) d = J^T r, accept iff the
+ * sum of squares decreases (lambda /= 10) else lambda *= 10; stop when an
+ * accepted step has max_i |d_i| / (|p_i| + 1e-12) < 1e-10, or after 100
+ * iterations (then: no width, NaN), or lambda > 1e16 (converged in place).
+ * Returns |s|, or NaN.
+ * ---------------------------------------------------------------------- */
+static double sse_gauss(const double* x, const double* y, int n, double A, double m, double s) {
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double z = (x[i] - m) / s;
+    double r = y[i] - A * std::exp(-0.5 * z * z);
+    acc += r * r;
+  }
+  return acc;
+}
+
+double oracle_fit_echo_width(const double* W, int64_t n_bins, int64_t k, double delta_ns,
+                             double pulse_length_ns, double* A_out, double* m_out) {
+  const int64_t w = (int64_t)std::ceil(3.0 * pulse_length_ns / delta_ns);
+  const int64_t lo = std::max<int64_t>(0, k - w), hi = std::min<int64_t>(n_bins - 1, k + w);
+  const int n = (int)(hi - lo + 1);
+  std::vector<double> x(n), y(n);
+  for (int i = 0; i < n; ++i) {
+    x[i] = (double)(lo + i - k) * delta_ns;
+    y[i] = W[lo + i];
+  }
+  double A = W[k], m = 0.0, s = pulse_length_ns / (2.0 * std::sqrt(2.0 * std::log(2.0)));
+  double lambda = 1e-3;
+  double cur = sse_gauss(x.data(), y.data(), n, A, m, s);
+  bool converged = false;
+  for (int it = 0; it < 100; ++it) {
+    // normal equations
+    double H[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, g[3] = {0, 0, 0};
+    for (int i = 0; i < n; ++i) {
+      double z = (x[i] - m) / s;
+      double e = std::exp(-0.5 * z * z);
+      double J[3] = {e, A * e * z / s, A * e * z * z / s};  // d/dA, d/dm, d/ds
+      double r = y[i] - A * e;
+      for (int a = 0; a < 3; ++a) {
+        g[a] += J[a] * r;
+        for (int b = 0; b < 3; ++b) H[a][b] += J[a] * J[b];
+      }
+    }
+    double M[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) M[a][b] = H[a][b] + (a == b ? lambda * H[a][a] : 0.0);
+    // solve M d = g (Cramer's rule on the 3x3 system)
+    double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                 M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                 M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+    if (!(std::fabs(det) > 0.0) || !std::isfinite(det)) break;
+    double d[3];
+    for (int c = 0; c < 3; ++c) {
+      double T[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) T[a][b] = (b == c) ? g[a] : M[a][b];
+      d[c] = (T[0][0] * (T[1][1] * T[2][2] - T[1][2] * T[2][1]) -
+              T[0][1] * (T[1][0] * T[2][2] - T[1][2] * T[2][0]) +
+              T[0][2] * (T[1][0] * T[2][1] - T[1][1] * T[2][0])) / det;
+    }
+    double nA = A + d[0], nm = m + d[1], ns = s + d[2];
+    double next = sse_gauss(x.data(), y.data(), n, nA, nm, ns);
+    if (std::isfinite(next) && next < cur) {
+      double rel = std::max({std::fabs(d[0]) / (std::fabs(A) + 1e-12),
+                             std::fabs(d[1]) / (std::fabs(m) + 1e-12),
+                             std::fabs(d[2]) / (std::fabs(s) + 1e-12)});
+      A = nA;
+      m = nm;
+      s = ns;
+      cur = next;
+      lambda /= 10.0;
+      if (rel < 1e-10) {
+        converged = true;
+        break;
+      }
+    } else {
+      lambda *= 10.0;
+      if (lambda > 1e16) {
+        converged = true;  // no further decrease possible: at the minimum
+        break;
+      }
+    }
+  }
+  if (A_out) *A_out = A;
+  if (m_out) *m_out = m;
+  if (!converged || !std::isfinite(s)) return kNaN;
+  return std::fabs(s);
+}
+
+/* ------------------------------------------------------------------------
  * Simulation parameters (mirrors DESIGN.md s.2; plain doubles).
  * ---------------------------------------------------------------------- */
 typedef struct {
@@ -401,6 +497,8 @@ typedef struct {
   uint64_t seed;                // Philox key (R19)
   uint32_t subray_count;        // (R1)
   uint32_t max_returns;         // (R11)
+  uint32_t fit_echo_width;      // optional Gaussian echo-width fit (R28)
+  uint32_t pad_;
 } oracle_params;
 
 typedef struct {
@@ -425,6 +523,7 @@ typedef struct {
   double* ret_intensity;
   uint32_t* ret_prim;
   int32_t* ret_number;
+  double* ret_width;     // [n][max_returns] fitted echo width sigma (ns); NaN = no fit
   double* peak_margin;   // [n] min relative margin of every peak decision
   double* attr_margin;   // [n] min relative gap between the top two contributions
   // per subray, [n][N]
@@ -628,6 +727,10 @@ static void finish_pulse(const oracle_params* pr, double time_s, int64_t i,
     out->ret_intensity[slot] = a;
     out->ret_prim[slot] = who;
     out->ret_number[slot] = nret + 1;
+    out->ret_width[slot] =
+        pr->fit_echo_width
+            ? oracle_fit_echo_width(W.data(), n_bins, k, delta, pr->pulse_length_ns, nullptr, nullptr)
+            : kNaN;
     ++nret;
   }
 
@@ -666,6 +769,7 @@ int oracle_simulate(const oracle_scene* sc, const oracle_params* pr,
       out->ret_intensity[x] = 0.0;
       out->ret_prim[x] = 0;
       out->ret_number[x] = 0;
+      out->ret_width[x] = kNaN;
     }
   }
   if (n_threads < 1) n_threads = 1;

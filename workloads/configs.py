@@ -56,6 +56,7 @@ class ScannerParams:
     beam_waist_m: float = 0.0
     focus_range_m: float = 0.0
     seed: int = 0
+    fit_echo_width: int = 0  # optional Gaussian echo-width fit
 
 
 @dataclass
