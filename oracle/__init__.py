@@ -54,7 +54,7 @@ class OracleParams(ctypes.Structure):
         ("peak_power_w", _d), ("efficiency", _d), ("receiver_diameter_m", _d),
         ("wavelength_nm", _d), ("beam_waist_m", _d), ("focus_range_m", _d),
         ("seed", _u64), ("subray_count", _u32), ("max_returns", _u32),
-        ("fit_echo_width", _u32), ("pad_", _u32),
+        ("fit_echo_width", _u32), ("pad_", _u32), ("range_noise_sd_m", _d),
     ]
 
 
@@ -103,6 +103,8 @@ def lib():
         L.oracle_g_function.argtypes = [_vp, _u32, _d]
         L.oracle_voxel_segments.restype = _i64
         L.oracle_voxel_segments.argtypes = [_vp, _vp, _vp, _vp, _d, _d, _vp, _vp, _vp, _i64]
+        L.oracle_range_noise.restype = _d
+        L.oracle_range_noise.argtypes = [_u64, _u64, _u32]
         L.oracle_fit_echo_width.restype = _d
         L.oracle_fit_echo_width.argtypes = [_vp, _i64, _i64, _d, _d, _vp, _vp]
         L.oracle_waveform_bins.restype = _u32
@@ -224,6 +226,12 @@ def voxel_segments(o, d, n, origin, vs, t_max=float("inf")):
     return ta[:k].copy(), tb[:k].copy(), vid[:k].copy()
 
 
+def range_noise(seed: int, pulse: int, return_number: int) -> float:
+    """Standard-normal ranging error of a return (R29, Box-Muller on
+    Philox stream tag 1)."""
+    return float(lib().oracle_range_noise(seed, pulse, return_number))
+
+
 def fit_echo_width(W, k: int, delta_ns: float, pulse_length_ns: float):
     """(sigma, A, m) of the Gaussian fitted around bin k (R28)."""
     W = np.ascontiguousarray(W, np.float64)
@@ -296,7 +304,7 @@ def simulate(scene, params, origins, directions, times, pulse_ids,
     pr = OracleParams()
     for f, _ in OracleParams._fields_:
         if f != "pad_":
-            setattr(pr, f, getattr(params, f))
+            setattr(pr, f, getattr(params, f, 0))
     o = np.ascontiguousarray(origins, np.float32).reshape(n, 3)
     d = np.ascontiguousarray(directions, np.float32).reshape(n, 3)
     t = np.ascontiguousarray(times, np.float64).reshape(n)

@@ -296,6 +296,23 @@ double oracle_transmission_u(uint64_t seed, uint64_t pulse, uint32_t subray,
   return (double)(x[0] >> 8) * (1.0 / 16777216.0);
 }
 
+/* Ranging error ("A single distance measurement is attributed with a
+ * random ranging error, drawn from a normal distribution"; reading R29):
+ * standard normal z for return number j (1-based) of pulse p by Box-Muller on
+ * Philox-4x32-10 with key = (seed_lo, seed_hi ^ 1) (stream tag 1; tag 0 is
+ * the transmission stream, R19), ctr = (p_lo, p_hi, j, 0):
+ * u1 = ((x0 >> 8) + 1) 2^-24 in (0, 1], u2 = (x1 >> 8) 2^-24,
+ * z = sqrt(-2 ln u1) cos(2 pi u2).  The return's range is R + sigma z. */
+double oracle_range_noise(uint64_t seed, uint64_t pulse, uint32_t return_number) {
+  uint32_t ctr[4] = {(uint32_t)pulse, (uint32_t)(pulse >> 32), return_number, 0u};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32) ^ 1u};
+  uint32_t x[4];
+  oracle_philox4x32_10(ctr, key, x);
+  double u1 = (double)((x[0] >> 8) + 1u) * (1.0 / 16777216.0);
+  double u2 = (double)(x[1] >> 8) * (1.0 / 16777216.0);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * kPi * u2);
+}
+
 /* G(|d_z|) for sigma = PAD * G (R15): LUT over |d_z| in [0,1] at uniform
  * knots, linear interpolation; no LUT -> spherical LAD, G = 0.5. */
 double oracle_g_function(const float* lut, uint32_t n_lut, double abs_dz) {
@@ -499,6 +516,7 @@ typedef struct {
   uint32_t max_returns;         // (R11)
   uint32_t fit_echo_width;      // optional Gaussian echo-width fit (R28)
   uint32_t pad_;
+  double range_noise_sd_m;      // ranging error sigma (R29), 0 -> none
 } oracle_params;
 
 typedef struct {
@@ -643,7 +661,7 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
 }
 
 /* Pulse i after all its subrays: steps O6..O8 (waveform, peaks, returns). */
-static void finish_pulse(const oracle_params* pr, double time_s, int64_t i,
+static void finish_pulse(const oracle_params* pr, double time_s, uint64_t pulse_id, int64_t i,
                          const oracle_outputs* out) {
   const uint32_t N = pr->subray_count;
   const double delta = pr->bin_width_ns;
@@ -723,6 +741,9 @@ static void finish_pulse(const oracle_params* pr, double time_s, int64_t i,
     int64_t slot = i * (int64_t)maxr + nret;
     out->ret_range[slot] =
         0.5 * kC * ((double)(k0 + k - jstar) + 0.5) * delta * 1e-9;  // R12
+    if (pr->range_noise_sd_m > 0.0)  // P:288, R29
+      out->ret_range[slot] += pr->range_noise_sd_m *
+                              oracle_range_noise(pr->seed, pulse_id, (uint32_t)(nret + 1));
     out->ret_time[slot] = time_s;
     out->ret_intensity[slot] = a;
     out->ret_prim[slot] = who;
@@ -796,7 +817,8 @@ int oracle_simulate(const oracle_scene* sc, const oracle_params* pr,
     simulate_subray(sc, pr, origins + 3 * i, directions + 3 * i, pulse_ids[i], i, s,
                     theta.data(), phi.data(), out);
   });
-  run_pool(n_pulses, [&](int64_t i) { finish_pulse(pr, times ? times[i] : 0.0, i, out); });
+  run_pool(n_pulses, [&](int64_t i) { finish_pulse(pr, times ? times[i] : 0.0, pulse_ids[i], i, out);
+  });
   return 0;
 }
 

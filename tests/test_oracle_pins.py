@@ -541,3 +541,51 @@ def test_simulate_reports_echo_width_only_when_asked():
     assert r1.ret_width[0, 0] == sig and 1.0 < sig < 6.0
     # the return's range is still taken from the local maximum, not the fit
     assert r1.ret_range[0, 0] == r0.ret_range[0, 0]
+
+
+# ------------------------------------------------------------------ ranging error (NEXT f4)
+def test_range_noise_is_standard_normal():
+    # "a random ranging error, drawn from a normal distribution" (R29).
+    # Pinned by distribution tests (a dropped factor, a wrong log/cos argument
+    # or a correlated pair of streams fails one of them): KS against the normal
+    # CDF, first four moments, and independence across returns and pulses.
+    from scipy import stats
+    n = 60000
+    z1 = np.array([oracle.range_noise(7, p, 1) for p in range(n)])
+    z2 = np.array([oracle.range_noise(7, p, 2) for p in range(n)])
+    for z in (z1, z2):
+        assert stats.kstest(z, "norm").pvalue > 1e-4
+        assert abs(z.mean()) < 5 / math.sqrt(n)
+        assert abs(z.var() - 1) < 5 * math.sqrt(2 / n)
+        assert abs(stats.skew(z)) < 5 * math.sqrt(6 / n)
+        assert abs(stats.kurtosis(z)) < 5 * math.sqrt(24 / n)
+    assert abs(np.corrcoef(z1, z2)[0, 1]) < 5 / math.sqrt(n)
+    assert abs(np.corrcoef(z1[:-1], z1[1:])[0, 1]) < 5 / math.sqrt(n)
+    # a different seed is a different stream
+    z3 = np.array([oracle.range_noise(8, p, 1) for p in range(2000)])
+    assert not np.array_equal(z3, z1[:2000])
+
+
+def test_range_noise_in_simulate_shifts_only_the_return_range():
+    # sigma = 0 -> noiseless; sigma > 0 -> every return's range moves by
+    # sigma * z(seed, pulse, return number); waveform, counts, prims unchanged.
+    from dataclasses import replace
+    from workloads import make_workload
+    w = make_workload("C2", scale=0.06)
+    o, d, t = w.pulses(100, 300)
+    ids = np.arange(100, 400, dtype=np.uint64)
+    a = oracle.simulate(w.scene, w.params, o, d, t, ids)
+    b = oracle.simulate(w.scene, replace(w.params, range_noise_sd_m=0.0), o, d, t, ids)
+    assert np.array_equal(a.ret_range, b.ret_range)
+    sd = 0.03
+    c = oracle.simulate(w.scene, replace(w.params, range_noise_sd_m=sd, seed=5), o, d, t, ids)
+    for f in ("n_returns", "k0", "waveform", "ret_prim", "ret_intensity"):
+        assert np.array_equal(getattr(a, f), getattr(c, f)), f
+    assert a.n_returns.sum() > 200
+    used = np.arange(a.ret_range.shape[1])[None, :] < a.n_returns[:, None]
+    z = (c.ret_range - a.ret_range)[used] / sd
+    from scipy import stats
+    assert stats.kstest(z, "norm").pvalue > 1e-4
+    i, j = np.nonzero(used)
+    want = np.array([oracle.range_noise(5, int(ids[ii]), int(jj) + 1) for ii, jj in zip(i, j)])
+    assert np.allclose(z, want, rtol=0, atol=1e-9)

@@ -57,6 +57,8 @@ class ScannerParams:
     focus_range_m: float = 0.0
     seed: int = 0
     fit_echo_width: int = 0  # optional Gaussian echo-width fit
+    reserved_: int = 0
+    range_noise_sd_m: float = 0.0  # ranging error sigma, 0 -> none
 
 
 @dataclass
