@@ -135,6 +135,16 @@ typedef struct {
   double beam_waist_m;          /* w0 of Eq. 2; 0 -> far field w = R tan(beta) (R5) */
   double focus_range_m;         /* R0 of Eq. 2, >= 0                             */
   uint64_t seed;                /* Philox-4x32-10 key for transmission draws (R19) */
+  uint32_t fit_echo_width;      /* 0 or 1: fit a Gaussian to every return's echo
+                                   ("Optionally, a Gaussian may be fitted ...
+                                   to get a measure of echo width", P:280 non-linear
+                                   least squares; reading R28: Levenberg-Marquardt
+                                   over bins k +- ceil(3 pulse_length / Delta))      */
+  uint32_t reserved_;           /* must be 0                                         */
+  double range_noise_sd_m;      /* >= 0: sigma of the normal ranging error added to
+                                   every return's range (reading R29:
+                                   Box-Muller on Philox stream tag 1, counter
+                                   (pulse, return number)); 0 -> noiseless       */
 } helios_scanner_params;
 
 /* Number of waveform bins, ceil(max_fullwave_range_ns / bin_width_ns);
@@ -158,7 +168,8 @@ typedef struct {
                                 identical to one call.                           */
 } helios_pulses;
 
-/* One discrete return (P:215, P:276 LAS point format 1 fields). 32 bytes. */
+/* One discrete return (P:215, P:276 LAS point format 1 fields; echo width
+ * P:280). 32 bytes. */
 typedef struct {
   double range_m;        /* (c/2)(k0 + k - j* + 1/2) Delta (R12)                */
   double gps_time_s;     /* the pulse's time                                    */
@@ -167,7 +178,10 @@ typedef struct {
                             n_tris + voxel id                                   */
   uint8_t return_number; /* 1-based, time order                                 */
   uint8_t n_returns;     /* returns of this pulse                               */
-  uint8_t pad[6];
+  uint8_t pad[2];        /* zero                                                */
+  float echo_width_ns;   /* fitted Gaussian sigma (ns) when fit_echo_width = 1
+                            (R28); NaN when not requested or when
+                            the fit did not converge                           */
 } helios_return;
 
 /* One subray's event (debug / parity export). 16 bytes.

@@ -218,6 +218,10 @@ helios_status validate_params(const helios_scanner_params* p, Derived* d) {
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "detection_threshold must be in (0, 1]");
   if (p->max_returns < 1 || p->max_returns > 255)
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "max_returns must be in [1, 255]");
+  if (!(p->range_noise_sd_m >= 0.0) || !std::isfinite(p->range_noise_sd_m))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "range_noise_sd_m must be finite and >= 0");
+  if (p->fit_echo_width > 1 || p->reserved_ != 0)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "fit_echo_width must be 0 or 1, reserved_ 0");
   if (!(p->peak_power_w > 0.0) || !std::isfinite(p->peak_power_w))
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "peak_power_w must be > 0");
   if (!(p->efficiency >= 0.0) || !(p->receiver_diameter_m >= 0.0) ||
@@ -593,7 +597,13 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   wa.delta_ns = params->bin_width_ns;
   wa.thr = params->detection_threshold;
   wa.max_returns = R;
+  // echo-width fit (R28): window half-width and LM start value
+  wa.fit = params->fit_echo_width;
+  wa.fit_half = (int)std::ceil(3.0 * params->pulse_length_ns / params->bin_width_ns);
+  wa.fit_s0 = params->pulse_length_ns / (2.0 * std::sqrt(2.0 * std::log(2.0)));
   wa.counters = counters ? d_cnt + 4 : nullptr;
+  wa.noise_sd = params->range_noise_sd_m;
+  wa.seed = params->seed;
 
   // per-kernel device time (CUDA events on each kernel's stream)
   std::vector<cudaEvent_t> ev_t, ev_w;
@@ -691,6 +701,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     if (e != cudaSuccess) break;
     wa.rec = ta.out;
     wa.n_pulses = m;
+    wa.pulse_base = ta.pulse_base;
     wa.time_s = (const double*)dev_ptr(arrs[2], slot, b);
     wa.n_returns = (uint8_t*)dev_ptr(arrs[3], slot, b);
     wa.returns = (helios_return*)dev_ptr(arrs[4], slot, b);

@@ -110,6 +110,12 @@ struct WaveArgs {
   int64_t* first_bin;
   float* waveform;               // may be nullptr
   unsigned long long* counters;  // [subray hits, returns] or nullptr
+  uint32_t fit;                  // 1: Gaussian echo-width fit per return (R28)
+  int fit_half;                  // window half-width ceil(3 pulse_length / Delta) bins
+  double fit_s0;                 // LM start sigma = pulse_length / (2 sqrt(2 ln 2)) ns
+  double noise_sd;               // ranging error sigma (R29), 0 = none
+  uint64_t seed;                 // Philox key
+  uint64_t pulse_base;           // global id of pulse 0 of this launch
 };
 
 // launchers (trace.cu / waveform.cu)

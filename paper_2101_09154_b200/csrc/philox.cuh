@@ -30,4 +30,16 @@ __device__ __forceinline__ double transmission_u(uint64_t seed, uint64_t pulse, 
   return (double)(x.x >> 8) * (1.0 / 16777216.0);
 }
 
+// Ranging error (R29): standard normal for return number j (1-based)
+// of pulse p.  Key = (seed_lo, seed_hi ^ 1) -- stream tag 1, disjoint from the
+// transmission stream -- counter (p_lo, p_hi, j, 0); Box-Muller on
+// u1 = ((x0 >> 8) + 1) 2^-24 in (0, 1] and u2 = (x1 >> 8) 2^-24.
+__device__ __forceinline__ double range_noise(uint64_t seed, uint64_t pulse, uint32_t j) {
+  const uint4 x = philox4x32_10(make_uint4((uint32_t)pulse, (uint32_t)(pulse >> 32), j, 0u),
+                                make_uint2((uint32_t)seed, (uint32_t)(seed >> 32) ^ 1u));
+  const double u1 = (double)((x.x >> 8) + 1u) * (1.0 / 16777216.0);
+  const double u2 = (double)(x.y >> 8) * (1.0 / 16777216.0);
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
 }  // namespace helios

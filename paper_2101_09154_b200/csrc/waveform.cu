@@ -25,6 +25,7 @@
 #include <math.h>
 
 #include "internal.cuh"
+#include "philox.cuh"
 
 namespace helios {
 namespace {
@@ -51,6 +52,93 @@ __device__ __forceinline__ double warp_max_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+  // xor butterfly: every lane ends with the bitwise-identical sum (fp64 addition
+  // is commutative), so the LM decisions below are warp-uniform.
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Echo width ("Optionally, a Gaussian may be fitted to the resulting
+// waveform, to get a measure of echo width (i.e. standard deviation of the
+// Gaussian)"; non-linear least squares).  Reading R28 (DESIGN.md s.3):
+// bins k-w..k+w clipped to the window, x = (i - k) Delta, y = W[i];
+// g(x) = A exp(-(x-m)^2 / 2s^2); Levenberg-Marquardt from (W[k], 0, s0),
+// lambda 1e-3, (J^T J + lambda diag J^T J) d = J^T r by Cramer's rule, accept iff
+// the sum of squares drops (lambda /= 10) else lambda *= 10; converged when an
+// accepted step has max |d_i| / (|p_i| + 1e-12) < 1e-10 or lambda > 1e16;
+// 100 iterations without convergence -> NaN.  The whole warp runs one fit:
+// lanes own bins, sums are warp-reduced (identical on every lane).
+__device__ double fit_echo_width(const double* __restrict__ W, uint32_t S, uint32_t nb,
+                                 int k, int half, double delta, double s0) {
+  const int lane = threadIdx.x & 31;
+  const int lo = max(0, k - half), hi = min((int)nb - 1, k + half);
+  const int n = hi - lo + 1;
+  auto yv = [&](int i) { return (uint32_t)(lo + i) < S ? W[lo + i] : 0.0; };
+  double A = W[k], m = 0.0, s = s0, lambda = 1e-3;
+  auto sse = [&](double a_, double m_, double s_) {
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double x = (double)(lo + i - k) * delta;
+      const double z = (x - m_) / s_;
+      const double r = yv(i) - a_ * exp(-0.5 * z * z);
+      acc += r * r;
+    }
+    return warp_sum_d(acc);
+  };
+  double cur = sse(A, m, s);
+  bool converged = false;
+  for (int it = 0; it < 100; ++it) {
+    double h00 = 0, h01 = 0, h02 = 0, h11 = 0, h12 = 0, h22 = 0, g0 = 0, g1 = 0, g2 = 0;
+    for (int i = lane; i < n; i += 32) {
+      const double x = (double)(lo + i - k) * delta;
+      const double z = (x - m) / s;
+      const double e = exp(-0.5 * z * z);
+      const double j0 = e, j1 = A * e * z / s, j2 = A * e * z * z / s;
+      const double r = yv(i) - A * e;
+      g0 += j0 * r; g1 += j1 * r; g2 += j2 * r;
+      h00 += j0 * j0; h01 += j0 * j1; h02 += j0 * j2;
+      h11 += j1 * j1; h12 += j1 * j2; h22 += j2 * j2;
+    }
+    h00 = warp_sum_d(h00); h01 = warp_sum_d(h01); h02 = warp_sum_d(h02);
+    h11 = warp_sum_d(h11); h12 = warp_sum_d(h12); h22 = warp_sum_d(h22);
+    g0 = warp_sum_d(g0); g1 = warp_sum_d(g1); g2 = warp_sum_d(g2);
+    const double m00 = h00 + lambda * h00, m11 = h11 + lambda * h11, m22 = h22 + lambda * h22;
+    const double m01 = h01, m02 = h02, m12 = h12;  // symmetric
+    const double c00 = m11 * m22 - m12 * m12, c01 = m01 * m22 - m12 * m02,
+                 c02 = m01 * m12 - m11 * m02;
+    const double det = m00 * c00 - m01 * c01 + m02 * c02;
+    if (!(fabs(det) > 0.0) || !isfinite(det)) break;
+    // Cramer's rule: column c of M replaced by g
+    const double d0 = (g0 * c00 - m01 * (g1 * m22 - m12 * g2) + m02 * (g1 * m12 - m11 * g2)) / det;
+    const double d1 = (m00 * (g1 * m22 - m12 * g2) - g0 * c01 + m02 * (m01 * g2 - g1 * m02)) / det;
+    const double d2 = (m00 * (m11 * g2 - g1 * m12) - m01 * (m01 * g2 - g1 * m02) + g0 * c02) / det;
+    const double nA = A + d0, nm = m + d1, ns = s + d2;
+    const double next = sse(nA, nm, ns);
+    if (isfinite(next) && next < cur) {
+      const double rel = fmax(fmax(fabs(d0) / (fabs(A) + 1e-12), fabs(d1) / (fabs(m) + 1e-12)),
+                              fabs(d2) / (fabs(s) + 1e-12));
+      A = nA;
+      m = nm;
+      s = ns;
+      cur = next;
+      lambda /= 10.0;
+      if (rel < 1e-10) {
+        converged = true;
+        break;
+      }
+    } else {
+      lambda *= 10.0;
+      if (lambda > 1e16) {
+        converged = true;
+        break;
+      }
+    }
+  }
+  return (converged && isfinite(s)) ? fabs(s) : __longlong_as_double(0x7ff8000000000000ll);
 }
 
 struct Layout {
@@ -193,16 +281,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a,
               bs = s2;
             }
           }
+          const double width = a.fit ? fit_echo_width(W, S, nb, (int)kk, a.fit_half, a.delta_ns,
+                                                       a.fit_s0)
+                                     : __longlong_as_double(0x7ff8000000000000ll);
           if (lane == 0) {
             helios_return r;
             r.range_m = 0.5 * kC * ((double)(k0 + (long long)kk - (long long)a.jstar) + 0.5) *
                         a.delta_ns * 1e-9;
+            if (a.noise_sd > 0.0)  // ranging error (R29)
+              r.range_m += a.noise_sd * range_noise(a.seed, a.pulse_base + p, nret + 1u);
             r.gps_time_s = a.time_s ? a.time_s[p] : 0.0;
             r.intensity = (float)W[kk];
             r.prim_id = rec[bs].prim_id;
             r.return_number = (uint8_t)(nret + 1);
             r.n_returns = 0;  // patched below once the count is known
-            for (int q = 0; q < 6; ++q) r.pad[q] = 0;
+            r.pad[0] = r.pad[1] = 0;
+            r.echo_width_ns = (float)width;
             slots[nret] = r;
           }
           ++nret;

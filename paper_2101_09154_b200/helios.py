@@ -53,7 +53,8 @@ class helios_scanner_params(ctypes.Structure):
                 ("bin_width_ns", _d), ("max_fullwave_range_ns", _d),
                 ("detection_threshold", _f), ("max_returns", _u32), ("peak_power_w", _d),
                 ("efficiency", _d), ("receiver_diameter_m", _d), ("wavelength_nm", _d),
-                ("beam_waist_m", _d), ("focus_range_m", _d), ("seed", _u64)]
+                ("beam_waist_m", _d), ("focus_range_m", _d), ("seed", _u64),
+                ("fit_echo_width", _u32), ("reserved_", _u32), ("range_noise_sd_m", _d)]
 
 
 class helios_pulses(ctypes.Structure):
@@ -83,7 +84,7 @@ class helios_scene_info(ctypes.Structure):
 
 RETURN_DTYPE = np.dtype([("range_m", "<f8"), ("gps_time_s", "<f8"), ("intensity", "<f4"),
                          ("prim_id", "<u4"), ("return_number", "u1"), ("n_returns", "u1"),
-                         ("pad", "u1", 6)])
+                         ("pad", "u1", 2), ("echo_width_ns", "<f4")])
 SUBRAY_DTYPE = np.dtype([("range_m", "<f8"), ("amplitude", "<f4"), ("prim_id", "<u4")])
 assert RETURN_DTYPE.itemsize == 32 and SUBRAY_DTYPE.itemsize == 16
 
@@ -193,7 +194,7 @@ def make_params(p) -> helios_scanner_params:
     """helios_scanner_params from any object with the same field names."""
     out = helios_scanner_params()
     for name, _ in helios_scanner_params._fields_:
-        setattr(out, name, getattr(p, name))
+        setattr(out, name, getattr(p, name, 0))
     return out
 
 

@@ -163,6 +163,21 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
             r.fail("return gps time", i)
         if not p_attr_ex[i] and not np.array_equal(gr["prim_id"], orc.ret_prim[i, :m]):
             r.fail("return prim", i, f"{gr['prim_id']} vs {orc.ret_prim[i, :m]}")
+        # echo width (R28): NaN <=> NaN (not requested / not
+        # converged), else the same least-squares optimum within 1e-6 relative
+        # (both fit in fp64 to a 1e-10 relative step; the GPU's fp32 record adds 6e-8)
+        if "echo_width_ns" in gr.dtype.names:
+            gw_ = gr["echo_width_ns"].astype(np.float64)
+            ow_ = orc.ret_width[i, :m]
+            if np.any(np.isnan(gw_) != np.isnan(ow_)):
+                r.fail("echo width NaN pattern", i, f"{gw_} vs {ow_}")
+            else:
+                f = ~np.isnan(ow_)
+                if f.any():
+                    rw = np.abs(gw_[f] - ow_[f]) / np.abs(ow_[f])
+                    r.rel("echo_width", rw.max())
+                    if rw.max() > 1e-6:
+                        r.fail("echo width", i, f"{gw_} vs {ow_}")
     return r
 
 

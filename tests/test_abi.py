@@ -77,3 +77,38 @@ def test_sass_is_sm100a(libpath):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", libpath],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """ctypes / numpy record layouts of the binding == the C compiler's layout
+    of include/helios.h (sizes and every field offset)."""
+    import paper_2101_09154_b200 as h
+    hh = h.helios
+    structs = {"helios_scene_desc": hh.helios_scene_desc,
+               "helios_scanner_params": hh.helios_scanner_params,
+               "helios_pulses": hh.helios_pulses, "helios_outputs": hh.helios_outputs,
+               "helios_stats": hh.helios_stats, "helios_scene_info": hh.helios_scene_info}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "helios.h"', "int main(){"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    for name, dt in (("helios_return", h.RETURN_DTYPE), ("helios_subray_hit", h.SUBRAY_DTYPE)):
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f in dt.names:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", f"-I{ROOT}/include", str(src), "-o", str(exe)])
+    got = dict(l.rsplit(" ", 1) for l in subprocess.check_output([str(exe)], text=True).split("\n")
+               if l)
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
+    for name, dt in (("helios_return", h.RETURN_DTYPE), ("helios_subray_hit", h.SUBRAY_DTYPE)):
+        assert int(got[name]) == dt.itemsize, name
+        for f in dt.names:
+            assert int(got[f"{name}.{f}"]) == dt.fields[f][1], (name, f)

@@ -77,3 +77,31 @@ def test_many_subrays_and_max_returns_cap():
     w = workload("C3", 0.03)
     p = replace(w.params, subray_count=279, max_returns=2, detection_threshold=0.01)
     _parity(w, 3000, 400, params=p)
+
+
+@pytest.mark.parametrize("name,scale,start,count", [("C2", 0.125, 7000, 1500),
+                                                    ("C3", 0.03, 2000, 1200),
+                                                    ("C4", 0.1, 4000, 3000)])
+def test_echo_width_fit(name, scale, start, count):
+    # optional Gaussian echo-width fit per return (NEXT f1; R28):
+    # same least-squares optimum as the oracle's fp64 Levenberg-Marquardt
+    from dataclasses import replace
+    w = workload(name, scale)
+    p = replace(w.params, fit_echo_width=1)
+    rep, _ = _parity(w, start, count, params=p)
+    assert "echo_width" in rep.max_rel  # some finite widths were compared
+
+
+def test_range_noise():
+    # ranging error per return (NEXT f4; R29): same Philox stream and
+    # Box-Muller on both sides; only the return ranges move
+    from dataclasses import replace
+    w = workload("C2", 0.125)
+    p = replace(w.params, range_noise_sd_m=0.05, seed=11)
+    _parity(w, 2000, 2000, params=p)
+    a = gpu_run(w, 2000, 500)
+    b = gpu_run(w, 2000, 500, params=p)
+    used = np.arange(a["returns"].shape[1])[None, :] < a["n_returns"][:, None]
+    dz = (b["returns"]["range_m"] - a["returns"]["range_m"])[used] / 0.05
+    assert used.sum() > 300 and 0.7 < dz.std() < 1.3 and abs(dz.mean()) < 0.2
+    assert np.array_equal(a["waveform"], b["waveform"])
