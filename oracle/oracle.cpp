@@ -411,6 +411,10 @@ int64_t oracle_voxel_segments(const double o_in[3], const double d_in[3],
  * sum of squares decreases (lambda /= 10) else lambda *= 10; stop when an
  * accepted step has max_i |d_i| / (|p_i| + 1e-12) < 1e-10, or after 100
  * iterations (then: no width, NaN), or lambda > 1e16 (converged in place).
+ * A Gaussian is identifiable from the window only if its centre and width
+ * lie inside it: a converged fit with A <= 0, |m| > w Delta or |s| > w Delta
+ * (the least-squares optimum running off to a flat, infinitely wide
+ * Gaussian on non-peaked data) is reported as no width.
  * Returns |s|, or NaN.
  * ---------------------------------------------------------------------- */
 static double sse_gauss(const double* x, const double* y, int n, double A, double m, double s) {
@@ -493,6 +497,8 @@ double oracle_fit_echo_width(const double* W, int64_t n_bins, int64_t k, double 
   if (A_out) *A_out = A;
   if (m_out) *m_out = m;
   if (!converged || !std::isfinite(s)) return kNaN;
+  const double span = (double)w * delta_ns;
+  if (!(A > 0.0) || std::fabs(m) > span || std::fabs(s) > span) return kNaN;
   return std::fabs(s);
 }
 

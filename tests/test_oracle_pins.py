@@ -589,3 +589,19 @@ def test_range_noise_in_simulate_shifts_only_the_return_range():
     i, j = np.nonzero(used)
     want = np.array([oracle.range_noise(5, int(ids[ii]), int(jj) + 1) for ii, jj in zip(i, j)])
     assert np.allclose(z, want, rtol=0, atol=1e-9)
+
+
+def test_echo_width_unidentifiable_window_has_no_width():
+    # R28: a window whose least-squares Gaussian is not inside it (a monotone
+    # ramp, a constant) has no width (NaN) instead of a runaway sigma.
+    delta, plen = 1.0, 4.0
+    x = np.arange(100, dtype=float)
+    for W in (1e-6 * (1 + 0.01 * x), np.full(100, 3e-7), 1e-6 * np.exp(0.02 * x)):
+        sig, _, _ = oracle.fit_echo_width(W, 50, delta, plen)
+        assert math.isnan(sig)
+    # a Gaussian wider than the window (sigma 20 ns > 12 ns half-width) has none
+    W = _gauss((x - 50) * delta, 1e-6, 0.0, 20.0)
+    assert math.isnan(oracle.fit_echo_width(W, 50, delta, plen)[0])
+    # ...while one inside it is still recovered exactly
+    W = _gauss((x - 50) * delta, 1e-6, 0.5, 5.0)
+    assert oracle.fit_echo_width(W, 50, delta, plen)[0] == pytest.approx(5.0, rel=1e-8)
