@@ -404,7 +404,8 @@ int64_t oracle_voxel_segments(const double o_in[3], const double d_in[3],
  * Echo width ("Optionally, a Gaussian may be fitted to the resulting
  * waveform, to get a measure of echo width (i.e. standard deviation of the
  * Gaussian)"; "non-linear least squares").  Reading R28:
- * window = bins k-w..k+w (clipped), w = ceil(3 pulse_length / Delta);
+ * window = the echo: the bins around k over which W decreases strictly away
+ * from the peak, at most w = ceil(3 pulse_length / Delta) on each side;
  * x_i = (i - k) Delta (ns), y_i = W[i];  g(x) = A exp(-(x - m)^2 / (2 s^2));
  * Levenberg-Marquardt from A = W[k], m = 0, s = pulse_length / (2 sqrt(2 ln 2)),
  * lambda = 1e-3, step (J^T J + lambda diag(J^T J)) d = J^T r, accept iff the
@@ -430,7 +431,9 @@ static double sse_gauss(const double* x, const double* y, int n, double A, doubl
 double oracle_fit_echo_width(const double* W, int64_t n_bins, int64_t k, double delta_ns,
                              double pulse_length_ns, double* A_out, double* m_out) {
   const int64_t w = (int64_t)std::ceil(3.0 * pulse_length_ns / delta_ns);
-  const int64_t lo = std::max<int64_t>(0, k - w), hi = std::min<int64_t>(n_bins - 1, k + w);
+  int64_t lo = k, hi = k;  // the echo: W strictly decreasing away from the peak, within k +- w
+  while (lo - 1 >= std::max<int64_t>(0, k - w) && W[lo - 1] < W[lo]) --lo;
+  while (hi + 1 <= std::min<int64_t>(n_bins - 1, k + w) && W[hi + 1] < W[hi]) ++hi;
   const int n = (int)(hi - lo + 1);
   std::vector<double> x(n), y(n);
   for (int i = 0; i < n; ++i) {

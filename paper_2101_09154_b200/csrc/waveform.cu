@@ -65,19 +65,41 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // Echo width ("Optionally, a Gaussian may be fitted to the resulting
 // waveform, to get a measure of echo width (i.e. standard deviation of the
 // Gaussian)"; non-linear least squares).  Reading R28 (DESIGN.md s.3):
-// bins k-w..k+w clipped to the window, x = (i - k) Delta, y = W[i];
+// the echo's bins: W strictly decreasing away from k, at most w = ceil(3
+// pulse_length / Delta) on each side; x = (i - k) Delta, y = W[i];
 // g(x) = A exp(-(x-m)^2 / 2s^2); Levenberg-Marquardt from (W[k], 0, s0),
 // lambda 1e-3, (J^T J + lambda diag J^T J) d = J^T r by Cramer's rule, accept iff
 // the sum of squares drops (lambda /= 10) else lambda *= 10; converged when an
 // accepted step has max |d_i| / (|p_i| + 1e-12) < 1e-10 or lambda > 1e16;
-// 100 iterations without convergence -> NaN.  The whole warp runs one fit:
+// 100 iterations without convergence, A <= 0, |m| > w Delta or |s| > w Delta
+// (not identifiable from the window) -> NaN.  The whole warp runs one fit:
 // lanes own bins, sums are warp-reduced (identical on every lane).
 __device__ double fit_echo_width(const double* __restrict__ W, uint32_t S, uint32_t nb,
                                  int k, int half, double delta, double s0) {
   const int lane = threadIdx.x & 31;
-  const int lo = max(0, k - half), hi = min((int)nb - 1, k + half);
+  auto wv = [&](int i) { return (uint32_t)i < S ? W[i] : 0.0; };  // bins >= S are zero
+  // the echo: bins around k over which W decreases strictly away from the
+  // peak, at most `half` on each side (ballot over 32 bins at a time)
+  int lo = k, hi = k;
+  for (int base = 0;; base += 32) {
+    const int i = k - 1 - base - lane;
+    const unsigned stop = __ballot_sync(0xffffffffu, !(i >= max(0, k - half) && wv(i) < wv(i + 1)));
+    if (stop) {
+      lo = k - base - (__ffs(stop) - 1);
+      break;
+    }
+  }
+  for (int base = 0;; base += 32) {
+    const int i = k + 1 + base + lane;
+    const unsigned stop = __ballot_sync(0xffffffffu,
+                                        !(i <= min((int)nb - 1, k + half) && wv(i) < wv(i - 1)));
+    if (stop) {
+      hi = k + base + (__ffs(stop) - 1);
+      break;
+    }
+  }
   const int n = hi - lo + 1;
-  auto yv = [&](int i) { return (uint32_t)(lo + i) < S ? W[lo + i] : 0.0; };
+  auto yv = [&](int i) { return wv(lo + i); };
   double A = W[k], m = 0.0, s = s0, lambda = 1e-3;
   auto sse = [&](double a_, double m_, double s_) {
     double acc = 0.0;
@@ -138,7 +160,11 @@ __device__ double fit_echo_width(const double* __restrict__ W, uint32_t S, uint3
       }
     }
   }
-  return (converged && isfinite(s)) ? fabs(s) : __longlong_as_double(0x7ff8000000000000ll);
+  // identifiable only with centre and width inside the window (R28)
+  const double span = (double)half * delta;
+  if (!converged || !isfinite(s) || !(A > 0.0) || fabs(m) > span || fabs(s) > span)
+    return __longlong_as_double(0x7ff8000000000000ll);
+  return fabs(s);
 }
 
 struct Layout {

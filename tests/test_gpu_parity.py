@@ -22,7 +22,8 @@ def _parity(w, start, count, sample=None, params=None, seed=0):
                                         rng.choice(count, min(sample, count), replace=False),
                                         [count - 1]]))
     o = oracle_run(w, start + idx, params=params)
-    rep = compare(take(g, idx), o, w.scene.n_tris, p.bin_width_ns)
+    span = np.ceil(3 * p.pulse_length_ns / p.bin_width_ns) * p.bin_width_ns
+    rep = compare(take(g, idx), o, w.scene.n_tris, p.bin_width_ns, fit_span_ns=span)
     print(rep.summary())
     assert rep.ok(), rep.summary()
     hits = (o.sub_prim != 0xFFFFFFFF).mean()

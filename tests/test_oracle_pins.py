@@ -521,7 +521,12 @@ def test_echo_width_matches_minpack_on_eq3_echo():
         k = 100 + int(np.argmax(p))
         sig, Af, mf = oracle.fit_echo_width(W, k, delta, plen)
         w = int(np.ceil(3 * plen / delta))
-        sel = np.arange(max(0, k - w), min(len(W), k + w + 1))
+        lo, hi = k, k  # R28 window: strictly decreasing away from the peak, <= w bins
+        while lo - 1 >= max(0, k - w) and W[lo - 1] < W[lo]:
+            lo -= 1
+        while hi + 1 <= min(len(W) - 1, k + w) and W[hi + 1] < W[hi]:
+            hi += 1
+        sel = np.arange(lo, hi + 1)
         x = (sel - k) * delta
         popt, _ = optimize.curve_fit(_gauss, x, W[sel], p0=[W[k], 0.0, 1.5], xtol=1e-14,
                                      ftol=1e-14, gtol=1e-14, maxfev=20000)
@@ -593,7 +598,9 @@ def test_range_noise_in_simulate_shifts_only_the_return_range():
 
 def test_echo_width_unidentifiable_window_has_no_width():
     # R28: a window whose least-squares Gaussian is not inside it (a monotone
-    # ramp, a constant) has no width (NaN) instead of a runaway sigma.
+    # ramp, a constant) has no width (NaN) instead of a runaway sigma.  The
+    # echo window stops where W stops decreasing away from the peak, so a
+    # neighbouring echo does not enter the fit.
     delta, plen = 1.0, 4.0
     x = np.arange(100, dtype=float)
     for W in (1e-6 * (1 + 0.01 * x), np.full(100, 3e-7), 1e-6 * np.exp(0.02 * x)):
@@ -605,3 +612,9 @@ def test_echo_width_unidentifiable_window_has_no_width():
     # ...while one inside it is still recovered exactly
     W = _gauss((x - 50) * delta, 1e-6, 0.5, 5.0)
     assert oracle.fit_echo_width(W, 50, delta, plen)[0] == pytest.approx(5.0, rel=1e-8)
+    # two echoes 9 ns apart: each one's width is that of its own hump
+    xs = (x - 50) * delta
+    W = _gauss(xs, 1e-6, 0.0, 1.5) + _gauss(xs, 0.5e-6, 9.0, 1.5)
+    s1 = oracle.fit_echo_width(W, 50, delta, plen)[0]
+    s2 = oracle.fit_echo_width(W, 59, delta, plen)[0]
+    assert abs(s1 - 1.5) < 0.05 and abs(s2 - 1.5) < 0.1
