@@ -205,6 +205,9 @@ def run_ours(args):
     t_gen = time.perf_counter()
     w = make_workload(args.config)
     t_gen = time.perf_counter() - t_gen
+    from dataclasses import replace as _replace
+    w.params = _replace(w.params, fit_echo_width=int(args.fit_echo_width),
+                        range_noise_sd_m=args.range_noise)
     p = w.params
     N = p.subray_count
     hp = h.make_params(p)
@@ -291,30 +294,43 @@ def run_ours(args):
         pass
     r1 = (b_ray + b_pulse) / (ms / 1e3) / 1e9 / peak
 
-    # ---- end to end through the C ABI with host buffers (copies inside)
-    e2e = None
+    # ---- end to end through the C ABI with host buffers (copies inside):
+    # every step copies its pulses host->device and the full result back
+    # (returns + the complete waveform, as lossless packed support rows; the
+    # dense-row variant is reported beside it)
+    e2e = e2e_dense = None
     if not args.no_e2e:
-        start, o, d, t = batches[args.warmup]
-        ho, hd, ht = (x.cpu().pin_memory() for x in (o, d, t))
-        hout = h.alloc_outputs(B, hp, device="cpu", waveform=True, pin_memory=True)
-        h.simulate(scene, hp, ho, hd, ht, pulse_index_base=start, outputs=hout)
-        torch.cuda.synchronize()
-        barrier(world)
-        t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
+        def run_e2e(compact):
+            start, o, d, t = batches[args.warmup]
+            ho, hd, ht = (x.cpu().pin_memory() for x in (o, d, t))
+            hout = h.alloc_outputs(B, hp, device="cpu", waveform=not compact, pin_memory=True,
+                                   compact=compact,
+                                   compact_capacity=B * n_bins if compact else None)
             h.simulate(scene, hp, ho, hd, ht, pulse_index_base=start, outputs=hout)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
-        h2d = B * (12 + 12 + 8)
-        d2h = B * (1 + 8 + 32 * p.max_returns + 4 * n_bins)
-        e2e = {"value": B * N * args.steps * world / (ems / 1e3) / 1e6, "unit": "Mrays/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "pulses_per_s": B * args.steps * world / (ems / 1e3)}
-        del hout
+            torch.cuda.synchronize()
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.steps):
+                h.simulate(scene, hp, ho, hd, ht, pulse_index_base=start, outputs=hout)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
+            h2d = B * (12 + 12 + 8)
+            d2h = B * (1 + 8 + 32 * p.max_returns)
+            if compact:
+                d2h += 8 * (B + 1) + 4 * int(hout.wf_offset[-1])
+            else:
+                d2h += 4 * n_bins * B
+            del hout
+            return {"value": B * N * args.steps * world / (ems / 1e3) / 1e6, "unit": "Mrays/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "pulses_per_s": B * args.steps * world / (ems / 1e3),
+                    "waveform_output": "packed support rows (lossless)" if compact
+                    else "dense rows"}
+        e2e = run_e2e(True)
+        e2e_dense = run_e2e(False)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -338,7 +354,9 @@ def run_ours(args):
                        "subrays_per_pulse": N, "n_tris": w.scene.n_tris,
                        "n_bins": n_bins, "l2": "inputs larger than L2 (scene + outputs)",
                        "bvh_nodes": info.n_nodes, "bvh_depth": info.max_depth,
-                       "build_ms": round(info.build_ms, 2), "gen_s": round(t_gen, 1)},
+                       "build_ms": round(info.build_ms, 2), "gen_s": round(t_gen, 1),
+                       "fit_echo_width": int(args.fit_echo_width),
+                       "range_noise_sd_m": args.range_noise},
             "roofline": {"bound": "hbm", "kernel": "k_trace", "achieved": ach_trace,
                          "peak": peak, "unit": "GB/s", "frac": ach_trace / peak,
                          "traffic": traffic, "peak_source": peak_src,
@@ -355,6 +373,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,
+            "e2e_dense_rows": e2e_dense,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -374,6 +393,10 @@ def main():
     ap.add_argument("--config", default=os.environ.get("HELIOS_BENCH_CONFIG", "C5"))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fit-echo-width", action="store_true",
+                    help="optional Gaussian echo-width fit per return (P:280)")
+    ap.add_argument("--range-noise", type=float, default=0.0,
+                    help="ranging error sigma in m (P:288)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=12.0,

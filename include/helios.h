@@ -47,7 +47,9 @@ typedef enum {
   HELIOS_ERR_OUT_OF_MEMORY = 2,    /* device allocation failed                          */
   HELIOS_ERR_CUDA = 3,             /* any other CUDA runtime error                      */
   HELIOS_ERR_NOT_BUILT = 4,        /* helios_simulate before helios_build_accel         */
-  HELIOS_ERR_EMPTY_SCENE = 5       /* n_tris == 0 and no voxel grid                     */
+  HELIOS_ERR_EMPTY_SCENE = 5,      /* n_tris == 0 and no voxel grid                     */
+  HELIOS_ERR_CAPACITY = 6          /* p_wf_compact too small: p_wf_offset[n_pulses] holds
+                                      the floats needed; every other output is complete */
 } helios_status;
 
 /* Thread-local, NUL-terminated description of the last failure on this
@@ -198,6 +200,20 @@ typedef struct {
   int64_t* p_wf_first_bin;     /* [n_pulses] absolute bin k0 of waveform[0]; -1 = no hit */
   float* p_waveform;           /* [n_pulses][n_bins] or NULL (binning still runs) */
   helios_subray_hit* p_subray_hits; /* [n_pulses][subray_count] or NULL              */
+  /* Compact (sparse-support) waveform output, lossless: the bins of row p
+   * that can be non-zero, W[0 .. len_p), packed back to back in pulse order.
+   * len_p = min(n_bins, max_s (k_s - k0) + L_p) over the subrays whose bin
+   * lies in the window (R9), 0 for a pulse without hit; every dense bin at or
+   * beyond len_p is exactly 0.  Row p occupies
+   * p_wf_compact[p_wf_offset[p] .. p_wf_offset[p+1]), p_wf_offset[0] = 0
+   * (offsets relative to this call).  p_wf_offset is required with
+   * p_wf_compact and may be given alone (lengths only).  If
+   * p_wf_offset[n_pulses] > wf_compact_capacity the call returns
+   * HELIOS_ERR_CAPACITY after completing everything else; rows past the
+   * capacity are then not (or not completely) written.                      */
+  float* p_wf_compact;         /* [wf_compact_capacity] or NULL                     */
+  uint64_t* p_wf_offset;       /* [n_pulses + 1] or NULL                            */
+  uint64_t wf_compact_capacity;
 } helios_outputs;
 
 /* Optional per-call accounting.  Inputs: collect_counters.  Everything else

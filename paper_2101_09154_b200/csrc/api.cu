@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "internal.cuh"
 
 using namespace helios;
@@ -42,12 +44,13 @@ struct helios_scene_s {
     bool busy;
     cudaStream_t copy;  // non-blocking copy stream for host staging (lazy)
     cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
+    uint64_t* pinned;   // 4 pinned words: per chunk slot (first, last) row offset (lazy)
   };
   std::mutex mu;
   std::vector<Slot> slots;
 
   cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy,
-                      cudaStream_t* wave) {
+                      cudaStream_t* wave, uint64_t** pinned = nullptr) {
     std::lock_guard<std::mutex> g(mu);
     Slot* use = nullptr;
     for (Slot& sl : slots)
@@ -56,7 +59,7 @@ struct helios_scene_s {
         break;
       }
     if (!use) {
-      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr});
+      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
@@ -79,8 +82,13 @@ struct helios_scene_s {
       if (e != cudaSuccess) return e;
     }
     *wave = use->wave;
+    if (!use->pinned) {
+      cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * sizeof(uint64_t));
+      if (e != cudaSuccess) return e;
+    }
     use->busy = true;
     *out = use->ptr;
+    if (pinned) *pinned = use->pinned;
     return cudaSuccess;
   }
   void release(cudaStream_t s) {
@@ -104,6 +112,7 @@ struct helios_scene_s {
         cudaStreamDestroy(sl.wave);
       }
       cudaFree(sl.ptr);
+      if (sl.pinned) cudaFreeHost(sl.pinned);
     }
     slots.clear();
   }
@@ -477,9 +486,13 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   if (!outputs->p_n_returns || !outputs->p_returns || !outputs->p_wf_first_bin)
     return fail(HELIOS_ERR_INVALID_ARGUMENT,
                 "p_n_returns/p_returns/p_wf_first_bin must not be NULL");
+  if (outputs->p_wf_compact && !outputs->p_wf_offset)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_wf_compact needs p_wf_offset");
   const uint32_t N = params->subray_count;
   const uint32_t R = params->max_returns;
   const cudaStream_t s = (cudaStream_t)stream;
+  const bool want_offs = outputs->p_wf_offset != nullptr;
+  const bool compact_staged = outputs->p_wf_compact && !device_accessible(outputs->p_wf_compact);
 
   // ---- host tables
   const std::vector<SubrayConst> tab = subray_table(N, params->divergence_rad, d.pt);
@@ -509,7 +522,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
       {outputs->p_waveform, 4ull * d.n_bins, false, false, {0, 0}},
       {outputs->p_subray_hits, sizeof(helios_subray_hit) * N, false, false, {0, 0}},
   };
-  bool any_staged = false;
+  bool any_staged = compact_staged;
   for (Arr& a : arrs)
     if (a.user && !device_accessible(a.user)) a.staged = any_staged = true;
 
@@ -533,10 +546,21 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   for (Arr& a : arrs)
     if (a.staged)
       for (int k = 0; k < 2; ++k) a.off[k] = carve(a.per_pulse * chunk);
+  // compact output: per-pulse lengths, call-wide offsets, scan temp, staging
+  size_t scan_bytes = 0;
+  if (want_offs)
+    cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (int)chunk, s);
+  const size_t o_len = carve(want_offs ? sizeof(uint64_t) * chunk : 0);
+  const size_t o_offs = carve(want_offs ? sizeof(uint64_t) * (n + 1) : 0);
+  const size_t o_scan = carve(want_offs ? scan_bytes : 0);
+  const size_t o_cst[2] = {carve(compact_staged ? 4ull * d.n_bins * chunk : 0),
+                           carve(compact_staged ? 4ull * d.n_bins * chunk : 0)};
 
   char* buf = nullptr;
   cudaStream_t cs = nullptr, ws = nullptr;
-  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr, &ws);
+  uint64_t* pin = nullptr;  // [slot][first, last] row offsets of a staged compact chunk
+  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr, &ws, &pin);
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
@@ -554,6 +578,9 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     e = cudaMemcpyAsync(d_ker, d.kernel.data(), sizeof(double) * d.taps, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, sizeof(unsigned), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, s);
+  uint64_t* d_len = reinterpret_cast<uint64_t*>(buf + o_len);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(buf + o_offs);
+  if (e == cudaSuccess && want_offs) e = cudaMemsetAsync(d_offs, 0, sizeof(uint64_t), s);
   if (e != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "helios_simulate (setup)");
@@ -603,6 +630,10 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   wa.fit_s0 = params->pulse_length_ns / (2.0 * std::sqrt(2.0 * std::log(2.0)));
   wa.counters = counters ? d_cnt + 4 : nullptr;
   wa.noise_sd = params->range_noise_sd_m;
+  wa.compact = compact_staged ? nullptr : outputs->p_wf_compact;
+  wa.compact_staged = compact_staged ? 1 : 0;
+  wa.capacity = outputs->p_wf_compact ? outputs->wf_compact_capacity : 0;
+  wa.err_flag = d_err;
   wa.seed = params->seed;
 
   // per-kernel device time (CUDA events on each kernel's stream)
@@ -621,8 +652,13 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   //   cs : wait w_done(c-1) -> H2D(c+1) -> in_done ; wait w_done(c) -> D2H(c) -> out_done
   // so K7(c) runs concurrently with K6(c+1) and the copies with both.
   cudaEvent_t in_done[2] = {}, t_done[2] = {}, w_done[2] = {}, out_done[2] = {};
+  cudaEvent_t off_done[2] = {}, cd_done[2] = {};  // compact: offsets of chunk known / drained
   for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess && compact_staged) {
+      e = cudaEventCreateWithFlags(&off_done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cd_done[k], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess && any_staged) {
       e = cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming);
@@ -648,6 +684,24 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
         if (r != cudaSuccess) return r;
       }
     return cudaEventRecord(in_done[slot], cs);
+  };
+
+  // staged compact rows of chunk c: the host learns the chunk's offset range
+  // from the pinned mirror (written on `s` right after the chunk's scan), then
+  // queues the copy behind K7(c) on the copy stream.  Called one iteration
+  // late, so the GPU never waits for the host.
+  const uint64_t cap = outputs->wf_compact_capacity;
+  auto drain_compact = [&](uint64_t c) -> cudaError_t {
+    const int sl = (int)(c & 1);
+    cudaError_t r = cudaEventSynchronize(off_done[sl]);
+    if (r != cudaSuccess) return r;
+    const uint64_t first = pin[2 * sl], last = std::min(pin[2 * sl + 1], cap);
+    r = cudaStreamWaitEvent(cs, w_done[sl], 0);
+    if (r == cudaSuccess && last > first)
+      r = cudaMemcpyAsync(outputs->p_wf_compact + first, buf + o_cst[sl],
+                          sizeof(float) * (last - first), cudaMemcpyDeviceToHost, cs);
+    if (r == cudaSuccess) r = cudaEventRecord(cd_done[sl], cs);
+    return r;
   };
 
   // traversal mode: warp-cooperative packets (default) or per-ray threads;
@@ -695,9 +749,26 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     mark(ev_t, s);
     e = launch_trace(ta, counters, mode, s);
     mark(ev_t, s);
+    if (e == cudaSuccess && want_offs) {
+      // lengths -> inclusive scan into offs[b+1 ..] -> + offs[b] (previous chunks)
+      e = launch_support(ta.out, N, m, d.n_bins, d.taps, params->bin_width_ns, d_len, s);
+      size_t tb = scan_bytes;
+      if (e == cudaSuccess)
+        e = cub::DeviceScan::InclusiveSum(buf + o_scan, tb, d_len, d_offs + b + 1, (int)m, s);
+      if (e == cudaSuccess) e = launch_add_carry(d_offs + b, m, s);
+      launches += 3;
+      if (e == cudaSuccess && compact_staged) {
+        e = cudaMemcpyAsync(pin + 2 * slot, d_offs + b, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(pin + 2 * slot + 1, d_offs + b + m, sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaEventRecord(off_done[slot], s);
+      }
+    }
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
     if (e == cudaSuccess && any_staged && c >= 2) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
+    if (e == cudaSuccess && compact_staged && c >= 2) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
     if (e != cudaSuccess) break;
     wa.rec = ta.out;
     wa.n_pulses = m;
@@ -707,11 +778,14 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     wa.returns = (helios_return*)dev_ptr(arrs[4], slot, b);
     wa.first_bin = (int64_t*)dev_ptr(arrs[5], slot, b);
     wa.waveform = (float*)dev_ptr(arrs[6], slot, b);
+    wa.offs = want_offs ? d_offs + b : nullptr;
+    if (compact_staged) wa.compact = reinterpret_cast<float*>(buf + o_cst[slot]);
     mark(ev_w, ws);
     e = launch_waveform(wa, plan, d_wscratch, ws);
     mark(ev_w, ws);
     if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], ws);
     launches += 2;
+    if (e == cudaSuccess && compact_staged && c >= 1) e = drain_compact(c - 1);
     if (e != cudaSuccess || !any_staged) continue;
     // prefetch the next chunk's inputs into the other slot once chunk c-1's
     // kernels (K6 reads origin/direction, K7 reads time) are done with it
@@ -727,13 +801,25 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
                             cudaMemcpyDeviceToHost, cs);
     if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], cs);
   }
+  if (e == cudaSuccess && compact_staged && n_chunks > 0) e = drain_compact(n_chunks - 1);
+  // call-wide offsets to the caller (device or host memory)
+  if (e == cudaSuccess && want_offs) {
+    for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess && ws != s; ++k)
+      e = cudaStreamWaitEvent(s, w_done[k], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(outputs->p_wf_offset, d_offs, sizeof(uint64_t) * (n + 1),
+                          cudaMemcpyDefault, s);
+  }
   // join: the caller's stream is ordered after every kernel of this call
   if (e == cudaSuccess && ws != s && n_chunks > 0)
     for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
       e = cudaStreamWaitEvent(s, w_done[k], 0);
   unsigned herr = 0;
   unsigned long long hcnt[8] = {0};
+  uint64_t htotal = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && want_offs)
+    e = cudaMemcpyAsync(&htotal, d_offs + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && counters)
     e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -755,6 +841,8 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     if (t_done[k]) cudaEventDestroy(t_done[k]);
     if (w_done[k]) cudaEventDestroy(w_done[k]);
     if (out_done[k]) cudaEventDestroy(out_done[k]);
+    if (off_done[k]) cudaEventDestroy(off_done[k]);
+    if (cd_done[k]) cudaEventDestroy(cd_done[k]);
   }
   cudaGetLastError();
   cleanup();
@@ -774,7 +862,11 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     stats->subray_hits = hcnt[4];
     stats->returns = hcnt[5];
   }
-  if (herr) return fail(HELIOS_ERR_INVALID_ARGUMENT, "a pulse direction has zero length");
+  if (herr & 4u) return fail(HELIOS_ERR_CUDA, "internal: compact row length mismatch");
+  if (herr & 1u) return fail(HELIOS_ERR_INVALID_ARGUMENT, "a pulse direction has zero length");
+  if (outputs->p_wf_compact && htotal > outputs->wf_compact_capacity)
+    return fail(HELIOS_ERR_CAPACITY, "compact waveform needs %llu floats, capacity %llu",
+                (unsigned long long)htotal, (unsigned long long)outputs->wf_compact_capacity);
   return HELIOS_OK;
 }
 

@@ -113,6 +113,11 @@ struct WaveArgs {
   uint32_t fit;                  // 1: Gaussian echo-width fit per return (R28)
   int fit_half;                  // window half-width ceil(3 pulse_length / Delta) bins
   double fit_s0;                 // LM start sigma = pulse_length / (2 sqrt(2 ln 2)) ns
+  float* compact;                // packed support rows or nullptr
+  const uint64_t* offs;          // [n_pulses + 1] call-relative row offsets (nullptr: none)
+  int compact_staged;            // 1: `compact` is a chunk staging slot based at offs[0]
+  uint64_t capacity;             // floats available in the caller's compact buffer
+  unsigned int* err_flag;        // bit 2: internal length mismatch
   double noise_sd;               // ranging error sigma (R29), 0 = none
   uint64_t seed;                 // Philox key
   uint64_t pulse_base;           // global id of pulse 0 of this launch
@@ -130,6 +135,12 @@ struct WavePlan {
   uint32_t grid_cap;    // 0 = full persistent grid; else max blocks (overlap with K6)
 };
 WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);
+// support length len_p of every pulse's waveform (for the compact output)
+cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_pulses,
+                           uint32_t n_bins, uint32_t taps, double delta_ns, uint64_t* len,
+                           cudaStream_t s);
+// offs[1 + i] += offs[0] for i < m (carry of the previous chunks)
+cudaError_t launch_add_carry(uint64_t* offs, uint64_t m, cudaStream_t s);
 bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps);
 cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scratch,
                             cudaStream_t s);

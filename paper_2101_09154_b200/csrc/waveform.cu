@@ -24,6 +24,8 @@
 // vector stores (zeros outside the support).
 #include <math.h>
 
+#include <algorithm>
+
 #include "internal.cuh"
 #include "philox.cuh"
 
@@ -165,6 +167,51 @@ __device__ double fit_echo_width(const double* __restrict__ W, uint32_t S, uint3
   if (!converged || !isfinite(s) || !(A > 0.0) || fabs(m) > span || fabs(s) > span)
     return __longlong_as_double(0x7ff8000000000000ll);
   return fabs(s);
+}
+
+// Support length of each pulse's waveform (compact output): one warp per
+// pulse, the same k_s / k0 / offset rules as K7's pass 1 (R9).
+__global__ void k_support(const helios_subray_hit* __restrict__ rec, uint32_t N, uint64_t n,
+                          uint32_t nb, uint32_t taps, double delta_ns,
+                          uint64_t* __restrict__ len) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t p = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += warps) {
+    const helios_subray_hit* r = rec + p * N;
+    long long kmin = LLONG_MAX, kmax_all = -1;
+    for (uint32_t s = lane; s < N; s += 32) {
+      const helios_subray_hit h = r[s];
+      if (h.prim_id != 0xFFFFFFFFu) {
+        const long long k = (long long)floor(2.0 * h.range_m / kC / (delta_ns * 1e-9));
+        kmin = k < kmin ? k : kmin;
+      }
+    }
+    const long long k0 = warp_min_ll(kmin);
+    uint64_t L = 0;
+    if (k0 != LLONG_MAX) {
+      for (uint32_t s = lane; s < N; s += 32) {
+        const helios_subray_hit h = r[s];
+        if (h.prim_id != 0xFFFFFFFFu) {
+          const long long o = (long long)floor(2.0 * h.range_m / kC / (delta_ns * 1e-9)) - k0;
+          if (o < (long long)nb && o > kmax_all) kmax_all = o;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const long long v = __shfl_xor_sync(0xffffffffu, kmax_all, o);
+        kmax_all = v > kmax_all ? v : kmax_all;
+      }
+      L = (uint64_t)min((long long)nb, kmax_all + (long long)taps);
+    }
+    if (lane == 0) len[p] = L;
+  }
+}
+
+__global__ void k_add_carry(uint64_t* __restrict__ offs, uint64_t m) {
+  const uint64_t c = offs[0];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    offs[1 + i] += c;
 }
 
 struct Layout {
@@ -352,6 +399,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a,
       for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
       if (lane == 0) atomicAdd(a.counters + 0, (unsigned long long)h);
     }
+    if (a.offs) {
+      // compact row: W[0 .. len) at its packed offset (lossless; bins >= len are 0)
+      const uint64_t o0 = a.offs[p], len = a.offs[p + 1] - o0;
+      if (lane == 0 && len != (uint64_t)S) atomicOr(a.err_flag, 4u);
+      if (a.compact && o0 + len <= a.capacity) {
+        float* dst = a.compact + (a.compact_staged ? o0 - a.offs[0] : o0);
+        for (uint32_t k = lane; k < (uint32_t)len; k += 32) dst[k] = k < S ? (float)W[k] : 0.0f;
+      }
+    }
     if (row) {
       // dense fp32 row: scalar head/tail, 16-byte stores for the aligned body
       const uint32_t mis = (uint32_t)(((uintptr_t)row >> 2) & 3u);
@@ -417,6 +473,22 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
 bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps) {
   (void)n_bins;
   return smem_for(N, taps, 1) <= kSmemCap;
+}
+
+cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_pulses,
+                           uint32_t n_bins, uint32_t taps, double delta_ns, uint64_t* len,
+                           cudaStream_t s) {
+  if (n_pulses == 0) return cudaSuccess;
+  const uint64_t blocks = std::min<uint64_t>((n_pulses + 7) / 8, 148ull * 16);
+  k_support<<<(unsigned)blocks, 256, 0, s>>>(rec, N, n_pulses, n_bins, taps, delta_ns, len);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_carry(uint64_t* offs, uint64_t m, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const uint64_t blocks = std::min<uint64_t>((m + 255) / 256, 148ull * 8);
+  k_add_carry<<<(unsigned)blocks, 256, 0, s>>>(offs, m);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scratch,

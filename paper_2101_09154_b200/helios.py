@@ -25,8 +25,9 @@ HELIOS_ERR_OUT_OF_MEMORY = 2
 HELIOS_ERR_CUDA = 3
 HELIOS_ERR_NOT_BUILT = 4
 HELIOS_ERR_EMPTY_SCENE = 5
+HELIOS_ERR_CAPACITY = 6
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OUT_OF_MEMORY", 3: "CUDA", 4: "NOT_BUILT",
-           5: "EMPTY_SCENE"}
+           5: "EMPTY_SCENE", 6: "CAPACITY"}
 
 EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helios_build_accel",
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
@@ -64,7 +65,8 @@ class helios_pulses(ctypes.Structure):
 
 class helios_outputs(ctypes.Structure):
     _fields_ = [("p_n_returns", _vp), ("p_returns", _vp), ("p_wf_first_bin", _vp),
-                ("p_waveform", _vp), ("p_subray_hits", _vp)]
+                ("p_waveform", _vp), ("p_subray_hits", _vp), ("p_wf_compact", _vp),
+                ("p_wf_offset", _vp), ("wf_compact_capacity", _u64)]
 
 
 class helios_stats(ctypes.Structure):
@@ -266,6 +268,14 @@ class Outputs:
     wf_first_bin: object   # int64 [n]
     waveform: object       # float32 [n, n_bins] or None
     subray_hits: object    # uint8 [n, N, 16] (SUBRAY_DTYPE records) or None
+    wf_compact: object = None  # float32 [capacity] packed support rows, or None
+    wf_offset: object = None   # uint64 [n + 1] row offsets into wf_compact, or None
+
+    def compact_row(self, p: int):
+        """Support row p as a host numpy array: W[0 .. len_p) of the dense row."""
+        host = lambda x: x if isinstance(x, np.ndarray) else x.cpu().numpy()
+        off = host(self.wf_offset)
+        return host(self.wf_compact[int(off[p]):int(off[p + 1])])
 
     def numpy(self) -> dict:
         """Host copies; records decoded to numpy structured arrays."""
@@ -280,11 +290,17 @@ class Outputs:
         h = host(self.subray_hits)
         out["subray_hits"] = None if h is None else np.ascontiguousarray(h).view(
             SUBRAY_DTYPE)[..., 0]
+        out["wf_offset"] = host(self.wf_offset)
+        out["wf_compact"] = host(self.wf_compact)
         return out
 
 
 def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=False,
-                  pin_memory=False) -> Outputs:
+                  pin_memory=False, compact: bool = False,
+                  compact_capacity: int | None = None) -> Outputs:
+    """Caller-owned outputs.  compact=True adds the packed support rows
+    (default capacity n * (L_p + 64) floats; helios_simulate reports
+    HELIOS_ERR_CAPACITY with the exact need if that is too small)."""
     import torch
     hp = params if isinstance(params, helios_scanner_params) else make_params(params)
     nb = helios_waveform_bins(hp)
@@ -300,12 +316,16 @@ def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=Fals
         wf_first_bin=torch.empty(n, dtype=torch.int64, **kw),
         waveform=torch.empty((n, nb), dtype=torch.float32, **kw) if waveform else None,
         subray_hits=torch.empty((n, N, 16), dtype=torch.uint8, **kw) if subray_hits else None,
+        wf_compact=torch.empty(int(compact_capacity if compact_capacity is not None else
+                                   n * (helios_pulse_taps(hp) + 64)), dtype=torch.float32, **kw)
+        if compact else None,
+        wf_offset=torch.empty(n + 1, dtype=torch.int64, **kw) if compact else None,
     )
 
 
 def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_base: int = 0,
              outputs: Outputs | None = None, waveform: bool = True, subray_hits: bool = False,
-             stream=None, stats: bool = False, counters: bool = False):
+             stream=None, stats: bool = False, counters: bool = False, compact: bool = False):
     """Run helios_simulate.  origin/direction: [n,3] float32 (CUDA tensors, or
     host tensors / numpy arrays -- staged by the library).  Returns
     (Outputs, helios_stats | None).  stats=True: per-kernel device times;
@@ -322,7 +342,7 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     n = int(origin.shape[0])
     if outputs is None:
         dev = "cuda" if (not isinstance(origin, np.ndarray) and origin.is_cuda) else "cpu"
-        outputs = alloc_outputs(n, hp, dev, waveform, subray_hits)
+        outputs = alloc_outputs(n, hp, dev, waveform, subray_hits, compact=compact)
     p = helios_pulses()
     p.p_origin = _ptr(origin)
     p.p_direction = _ptr(direction)
@@ -335,8 +355,25 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     o.p_wf_first_bin = _ptr(outputs.wf_first_bin)
     o.p_waveform = _ptr(outputs.waveform)
     o.p_subray_hits = _ptr(outputs.subray_hits)
+    o.p_wf_compact = _ptr(outputs.wf_compact)
+    o.p_wf_offset = _ptr(outputs.wf_offset)
+    o.wf_compact_capacity = 0 if outputs.wf_compact is None else int(outputs.wf_compact.numel()
+                                                                     if hasattr(outputs.wf_compact, "numel") else outputs.wf_compact.size)
     st = helios_stats() if (stats or counters) else None
     if st is not None:
         st.collect_counters = 1 if counters else 0
-    helios_simulate(scene.handle, hp, p, o, stream, st)
+    try:
+        helios_simulate(scene.handle, hp, p, o, stream, st)
+    except HeliosError as err:
+        if err.status != HELIOS_ERR_CAPACITY:
+            raise
+        # grow the packed buffer to the exact need reported in the offsets and rerun
+        import torch
+        need = int(outputs.wf_offset[-1])
+        old = outputs.wf_compact
+        outputs.wf_compact = torch.empty(need, dtype=torch.float32, device=old.device,
+                                         pin_memory=bool(getattr(old, "is_pinned", lambda: False)()))
+        o.p_wf_compact = _ptr(outputs.wf_compact)
+        o.wf_compact_capacity = need
+        helios_simulate(scene.handle, hp, p, o, stream, st)
     return outputs, st
