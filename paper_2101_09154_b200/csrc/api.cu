@@ -782,6 +782,10 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     if (compact_staged) wa.compact = reinterpret_cast<float*>(buf + o_cst[slot]);
     mark(ev_w, ws);
     e = launch_waveform(wa, plan, d_wscratch, ws);
+    if (e == cudaSuccess && wa.noise_sd > 0.0) {
+      e = launch_range_noise(wa, ws);
+      ++launches;
+    }
     mark(ev_w, ws);
     if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], ws);
     launches += 2;

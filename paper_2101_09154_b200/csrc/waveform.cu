@@ -207,6 +207,20 @@ __global__ void k_support(const helios_subray_hit* __restrict__ rec, uint32_t N,
   }
 }
 
+// Ranging error (R29): every used return slot's range += sigma z,
+// z from Philox stream tag 1 at (pulse, return number).  A separate pass so
+// K7 keeps its register budget (fp64 log / cos / sqrt).
+__global__ void k_range_noise(helios_return* __restrict__ ret, const uint8_t* __restrict__ nr,
+                              uint64_t n, uint32_t R, double sd, uint64_t seed,
+                              uint64_t pulse_base) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * R;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = i / R;
+    const uint32_t j = (uint32_t)(i - p * R);
+    if (j < nr[p]) ret[i].range_m += sd * range_noise(seed, pulse_base + p, j + 1u);
+  }
+}
+
 __global__ void k_add_carry(uint64_t* __restrict__ offs, uint64_t m) {
   const uint64_t c = offs[0];
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
@@ -228,7 +242,10 @@ __host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
   return L;
 }
 
-__global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a,
+// FIT: the echo-width fit is compiled into a separate instance so the plain
+// path keeps its register budget (the fp64 LM needs ~2.5x the registers).
+template <bool FIT>
+__global__ void __launch_bounds__(kMaxWarps * 32, FIT ? 1 : 5) k_waveform(const WaveArgs a,
                                                              double* __restrict__ gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -354,15 +371,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32) k_waveform(const WaveArgs a,
               bs = s2;
             }
           }
-          const double width = a.fit ? fit_echo_width(W, S, nb, (int)kk, a.fit_half, a.delta_ns,
-                                                       a.fit_s0)
-                                     : __longlong_as_double(0x7ff8000000000000ll);
+          const double width = FIT ? fit_echo_width(W, S, nb, (int)kk, a.fit_half, a.delta_ns,
+                                                    a.fit_s0)
+                                   : __longlong_as_double(0x7ff8000000000000ll);
           if (lane == 0) {
             helios_return r;
             r.range_m = 0.5 * kC * ((double)(k0 + (long long)kk - (long long)a.jstar) + 0.5) *
                         a.delta_ns * 1e-9;
-            if (a.noise_sd > 0.0)  // ranging error (R29)
-              r.range_m += a.noise_sd * range_noise(a.seed, a.pulse_base + p, nret + 1u);
             r.gps_time_s = a.time_s ? a.time_s[p] : 0.0;
             r.intensity = (float)W[kk];
             r.prim_id = rec[bs].prim_id;
@@ -456,9 +471,9 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaFuncSetAttribute(k_waveform, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_waveform<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)pl.smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform, warps * 32, pl.smem) !=
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform<false>, warps * 32, pl.smem) !=
           cudaSuccess ||
       per_sm < 1) {
     cudaGetLastError();
@@ -484,6 +499,15 @@ cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_
   return cudaGetLastError();
 }
 
+cudaError_t launch_range_noise(const WaveArgs& a, cudaStream_t s) {
+  if (a.n_pulses == 0 || !(a.noise_sd > 0.0)) return cudaSuccess;
+  const uint64_t total = a.n_pulses * a.max_returns;
+  const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148ull * 8);
+  k_range_noise<<<(unsigned)blocks, 256, 0, s>>>(a.returns, a.n_returns, a.n_pulses,
+                                                  a.max_returns, a.noise_sd, a.seed, a.pulse_base);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_add_carry(uint64_t* offs, uint64_t m, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   const uint64_t blocks = std::min<uint64_t>((m + 255) / 256, 148ull * 8);
@@ -499,7 +523,23 @@ cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scrat
   uint64_t grid = pl.grid;
   if (pl.grid_cap && pl.grid_cap < grid) grid = pl.grid_cap;
   if (want < grid) grid = want;
-  k_waveform<<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
+  if (a.fit) {
+    // the fit instance has its own register budget: size its grid on its own
+    int dev = 0, sms = 148, ps = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(k_waveform<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_waveform<true>, pl.warps * 32,
+                                                        pl.smem);
+    if (e != cudaSuccess) return e;
+    if (ps < 1) return cudaErrorInvalidConfiguration;
+    const uint64_t g2 = std::min<uint64_t>(grid, (uint64_t)sms * ps);
+    k_waveform<true><<<(unsigned)g2, pl.warps * 32, pl.smem, s>>>(a, scratch);
+  } else {
+    k_waveform<false><<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
+  }
   return cudaGetLastError();
 }
 
