@@ -554,6 +554,13 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const size_t o_len = carve(want_offs ? sizeof(uint64_t) * chunk : 0);
   const size_t o_offs = carve(want_offs ? sizeof(uint64_t) * (n + 1) : 0);
   const size_t o_scan = carve(want_offs ? scan_bytes : 0);
+  // echo-width jobs of one K7 launch (K7 and k_fit are serial on their stream)
+  const uint32_t fit_stride = 2u * (uint32_t)std::ceil(3.0 * params->pulse_length_ns /
+                                                        params->bin_width_ns) + 1u;
+  const bool fit = params->fit_echo_width != 0;
+  const size_t o_fjob = carve(fit ? sizeof(FitJob) * chunk * R : 0);
+  const size_t o_fy = carve(fit ? sizeof(double) * fit_stride * chunk * R : 0);
+  const size_t o_fcnt = carve(fit ? sizeof(unsigned) : 0);
   const size_t o_cst[2] = {carve(compact_staged ? 4ull * d.n_bins * chunk : 0),
                            carve(compact_staged ? 4ull * d.n_bins * chunk : 0)};
 
@@ -630,6 +637,10 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   wa.fit_s0 = params->pulse_length_ns / (2.0 * std::sqrt(2.0 * std::log(2.0)));
   wa.counters = counters ? d_cnt + 4 : nullptr;
   wa.noise_sd = params->range_noise_sd_m;
+  wa.fit_jobs = reinterpret_cast<FitJob*>(buf + o_fjob);
+  wa.fit_y = reinterpret_cast<double*>(buf + o_fy);
+  wa.fit_stride = fit_stride;
+  wa.fit_count = reinterpret_cast<unsigned*>(buf + o_fcnt);
   wa.compact = compact_staged ? nullptr : outputs->p_wf_compact;
   wa.compact_staged = compact_staged ? 1 : 0;
   wa.capacity = outputs->p_wf_compact ? outputs->wf_compact_capacity : 0;
@@ -781,7 +792,9 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     wa.offs = want_offs ? d_offs + b : nullptr;
     if (compact_staged) wa.compact = reinterpret_cast<float*>(buf + o_cst[slot]);
     mark(ev_w, ws);
-    e = launch_waveform(wa, plan, d_wscratch, ws);
+    if (fit) e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
+    if (e == cudaSuccess) e = launch_waveform(wa, plan, d_wscratch, ws);
+    if (fit) ++launches;
     if (e == cudaSuccess && wa.noise_sd > 0.0) {
       e = launch_range_noise(wa, ws);
       ++launches;

@@ -93,6 +93,14 @@ struct TraceArgs {
   unsigned long long* counters;  // instrumented variant: [nodes, tris, voxel steps, voxel returns]
 };
 
+// One echo-width fit job (R28), appended by K7, solved by k_fit.
+struct FitJob {
+  uint32_t slot;  // return slot index p * max_returns + j within the launch
+  int16_t lo;     // first window bin relative to the peak bin (<= 0)
+  uint16_t n;     // window bins
+  double peak;    // W[k] (LM start amplitude)
+};
+
 struct WaveArgs {
   const helios_subray_hit* rec;  // [n][N]
   uint32_t N;
@@ -111,6 +119,10 @@ struct WaveArgs {
   float* waveform;               // may be nullptr
   unsigned long long* counters;  // [subray hits, returns] or nullptr
   uint32_t fit;                  // 1: Gaussian echo-width fit per return (R28)
+  FitJob* fit_jobs;              // [n_pulses * max_returns] job list (fit only)
+  double* fit_y;                 // [n_pulses * max_returns][fit_stride] window values
+  uint32_t fit_stride;           // 2 fit_half + 1
+  unsigned* fit_count;           // jobs appended (zeroed before each launch)
   int fit_half;                  // window half-width ceil(3 pulse_length / Delta) bins
   double fit_s0;                 // LM start sigma = pulse_length / (2 sqrt(2 ln 2)) ns
   float* compact;                // packed support rows or nullptr

@@ -67,22 +67,27 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // Echo width ("Optionally, a Gaussian may be fitted to the resulting
 // waveform, to get a measure of echo width (i.e. standard deviation of the
 // Gaussian)"; non-linear least squares).  Reading R28 (DESIGN.md s.3):
-// the echo's bins: W strictly decreasing away from k, at most w = ceil(3
-// pulse_length / Delta) on each side; x = (i - k) Delta, y = W[i];
+// the echo's bins -- W strictly decreasing away from the peak k, at most
+// w = ceil(3 pulse_length / Delta) on each side; x = (i - k) Delta, y = W[i];
 // g(x) = A exp(-(x-m)^2 / 2s^2); Levenberg-Marquardt from (W[k], 0, s0),
 // lambda 1e-3, (J^T J + lambda diag J^T J) d = J^T r by Cramer's rule, accept iff
 // the sum of squares drops (lambda /= 10) else lambda *= 10; converged when an
 // accepted step has max |d_i| / (|p_i| + 1e-12) < 1e-10 or lambda > 1e16;
 // 100 iterations without convergence, A <= 0, |m| > w Delta or |s| > w Delta
-// (not identifiable from the window) -> NaN.  The whole warp runs one fit:
-// lanes own bins, sums are warp-reduced (identical on every lane).
-__device__ double fit_echo_width(const double* __restrict__ W, uint32_t S, uint32_t nb,
-                                 int k, int half, double delta, double s0) {
+// (not identifiable from the window) -> NaN.
+//
+// Split in two: K7 finds each return's echo window (warp ballots over the
+// fp64 waveform in shared memory) and appends a job {slot, window} to a
+// per-launch list; k_fit then runs one LM per THREAD, summing the window
+// sequentially in bin order (no warp reductions on the critical path).
+
+// window [k + lo, k + hi] of the echo at k (all lanes; result warp-uniform)
+__device__ __forceinline__ void echo_window(const double* __restrict__ W, uint32_t S, uint32_t nb,
+                                            int k, int half, int& lo, int& hi) {
   const int lane = threadIdx.x & 31;
   auto wv = [&](int i) { return (uint32_t)i < S ? W[i] : 0.0; };  // bins >= S are zero
-  // the echo: bins around k over which W decreases strictly away from the
-  // peak, at most `half` on each side (ballot over 32 bins at a time)
-  int lo = k, hi = k;
+  lo = k;
+  hi = k;
   for (int base = 0;; base += 32) {
     const int i = k - 1 - base - lane;
     const unsigned stop = __ballot_sync(0xffffffffu, !(i >= max(0, k - half) && wv(i) < wv(i + 1)));
@@ -100,73 +105,82 @@ __device__ double fit_echo_width(const double* __restrict__ W, uint32_t S, uint3
       break;
     }
   }
-  const int n = hi - lo + 1;
-  auto yv = [&](int i) { return wv(lo + i); };
-  double A = W[k], m = 0.0, s = s0, lambda = 1e-3;
-  auto sse = [&](double a_, double m_, double s_) {
-    double acc = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      const double x = (double)(lo + i - k) * delta;
-      const double z = (x - m_) / s_;
-      const double r = yv(i) - a_ * exp(-0.5 * z * z);
-      acc += r * r;
-    }
-    return warp_sum_d(acc);
-  };
-  double cur = sse(A, m, s);
-  bool converged = false;
-  for (int it = 0; it < 100; ++it) {
-    double h00 = 0, h01 = 0, h02 = 0, h11 = 0, h12 = 0, h22 = 0, g0 = 0, g1 = 0, g2 = 0;
-    for (int i = lane; i < n; i += 32) {
-      const double x = (double)(lo + i - k) * delta;
-      const double z = (x - m) / s;
-      const double e = exp(-0.5 * z * z);
-      const double j0 = e, j1 = A * e * z / s, j2 = A * e * z * z / s;
-      const double r = yv(i) - A * e;
-      g0 += j0 * r; g1 += j1 * r; g2 += j2 * r;
-      h00 += j0 * j0; h01 += j0 * j1; h02 += j0 * j2;
-      h11 += j1 * j1; h12 += j1 * j2; h22 += j2 * j2;
-    }
-    h00 = warp_sum_d(h00); h01 = warp_sum_d(h01); h02 = warp_sum_d(h02);
-    h11 = warp_sum_d(h11); h12 = warp_sum_d(h12); h22 = warp_sum_d(h22);
-    g0 = warp_sum_d(g0); g1 = warp_sum_d(g1); g2 = warp_sum_d(g2);
-    const double m00 = h00 + lambda * h00, m11 = h11 + lambda * h11, m22 = h22 + lambda * h22;
-    const double m01 = h01, m02 = h02, m12 = h12;  // symmetric
-    const double c00 = m11 * m22 - m12 * m12, c01 = m01 * m22 - m12 * m02,
-                 c02 = m01 * m12 - m11 * m02;
-    const double det = m00 * c00 - m01 * c01 + m02 * c02;
-    if (!(fabs(det) > 0.0) || !isfinite(det)) break;
-    // Cramer's rule: column c of M replaced by g
-    const double d0 = (g0 * c00 - m01 * (g1 * m22 - m12 * g2) + m02 * (g1 * m12 - m11 * g2)) / det;
-    const double d1 = (m00 * (g1 * m22 - m12 * g2) - g0 * c01 + m02 * (m01 * g2 - g1 * m02)) / det;
-    const double d2 = (m00 * (m11 * g2 - g1 * m12) - m01 * (m01 * g2 - g1 * m02) + g0 * c02) / det;
-    const double nA = A + d0, nm = m + d1, ns = s + d2;
-    const double next = sse(nA, nm, ns);
-    if (isfinite(next) && next < cur) {
-      const double rel = fmax(fmax(fabs(d0) / (fabs(A) + 1e-12), fabs(d1) / (fabs(m) + 1e-12)),
-                              fabs(d2) / (fabs(s) + 1e-12));
-      A = nA;
-      m = nm;
-      s = ns;
-      cur = next;
-      lambda /= 10.0;
-      if (rel < 1e-10) {
-        converged = true;
-        break;
-      }
-    } else {
-      lambda *= 10.0;
-      if (lambda > 1e16) {
-        converged = true;
-        break;
-      }
-    }
+}
+
+__device__ __forceinline__ double sse_gauss(const double* __restrict__ y, int n, int lo,
+                                            double delta, double A, double m, double s) {
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double z = ((double)(lo + i) * delta - m) / s;
+    const double r = y[i] - A * exp(-0.5 * z * z);
+    acc += r * r;
   }
-  // identifiable only with centre and width inside the window (R28)
-  const double span = (double)half * delta;
-  if (!converged || !isfinite(s) || !(A > 0.0) || fabs(m) > span || fabs(s) > span)
-    return __longlong_as_double(0x7ff8000000000000ll);
-  return fabs(s);
+  return acc;
+}
+
+// One LM fit per thread over the job list of one K7 launch.
+__global__ void __launch_bounds__(128) k_fit(const FitJob* __restrict__ jobs,
+                                             const double* __restrict__ ys, uint32_t stride,
+                                             const unsigned* __restrict__ count, int half,
+                                             double delta, double s0,
+                                             helios_return* __restrict__ ret) {
+  const unsigned nj = *count;
+  for (unsigned j = blockIdx.x * blockDim.x + threadIdx.x; j < nj; j += gridDim.x * blockDim.x) {
+    const FitJob job = jobs[j];
+    const double* y = ys + (size_t)j * stride;
+    const int n = job.n;
+    const int lo = job.lo;  // first window bin relative to the peak: x_i = (lo + i) Delta
+    double A = job.peak, m = 0.0, s = s0, lambda = 1e-3;
+    double cur = sse_gauss(y, n, lo, delta, A, m, s);
+    bool converged = false;
+    for (int it = 0; it < 100; ++it) {
+      double h00 = 0, h01 = 0, h02 = 0, h11 = 0, h12 = 0, h22 = 0, g0 = 0, g1 = 0, g2 = 0;
+      for (int i = 0; i < n; ++i) {
+        const double z = ((double)(lo + i) * delta - m) / s;
+        const double e = exp(-0.5 * z * z);
+        const double j0 = e, j1 = A * e * z / s, j2 = A * e * z * z / s;
+        const double r = y[i] - A * e;
+        g0 += j0 * r; g1 += j1 * r; g2 += j2 * r;
+        h00 += j0 * j0; h01 += j0 * j1; h02 += j0 * j2;
+        h11 += j1 * j1; h12 += j1 * j2; h22 += j2 * j2;
+      }
+      const double m00 = h00 + lambda * h00, m11 = h11 + lambda * h11, m22 = h22 + lambda * h22;
+      const double m01 = h01, m02 = h02, m12 = h12;  // symmetric
+      const double c00 = m11 * m22 - m12 * m12, c01 = m01 * m22 - m12 * m02,
+                   c02 = m01 * m12 - m11 * m02;
+      const double det = m00 * c00 - m01 * c01 + m02 * c02;
+      if (!(fabs(det) > 0.0) || !isfinite(det)) break;
+      // Cramer's rule: column c of M replaced by g
+      const double d0 = (g0 * c00 - m01 * (g1 * m22 - m12 * g2) + m02 * (g1 * m12 - m11 * g2)) / det;
+      const double d1 = (m00 * (g1 * m22 - m12 * g2) - g0 * c01 + m02 * (m01 * g2 - g1 * m02)) / det;
+      const double d2 = (m00 * (m11 * g2 - g1 * m12) - m01 * (m01 * g2 - g1 * m02) + g0 * c02) / det;
+      const double nA = A + d0, nm = m + d1, ns = s + d2;
+      const double next = sse_gauss(y, n, lo, delta, nA, nm, ns);
+      if (isfinite(next) && next < cur) {
+        const double rel = fmax(fmax(fabs(d0) / (fabs(A) + 1e-12), fabs(d1) / (fabs(m) + 1e-12)),
+                                fabs(d2) / (fabs(s) + 1e-12));
+        A = nA;
+        m = nm;
+        s = ns;
+        cur = next;
+        lambda /= 10.0;
+        if (rel < 1e-10) {
+          converged = true;
+          break;
+        }
+      } else {
+        lambda *= 10.0;
+        if (lambda > 1e16) {
+          converged = true;
+          break;
+        }
+      }
+    }
+    // identifiable only with centre and width inside the window (R28)
+    const double span = (double)half * delta;
+    const bool ok = converged && isfinite(s) && A > 0.0 && fabs(m) <= span && fabs(s) <= span;
+    ret[job.slot].echo_width_ns = ok ? (float)fabs(s) : __int_as_float(0x7fc00000);
+  }
 }
 
 // Support length of each pulse's waveform (compact output): one warp per
@@ -242,10 +256,7 @@ __host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
   return L;
 }
 
-// FIT: the echo-width fit is compiled into a separate instance so the plain
-// path keeps its register budget (the fp64 LM needs ~2.5x the registers).
-template <bool FIT>
-__global__ void __launch_bounds__(kMaxWarps * 32, FIT ? 1 : 5) k_waveform(const WaveArgs a,
+__global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a,
                                                              double* __restrict__ gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -371,9 +382,25 @@ __global__ void __launch_bounds__(kMaxWarps * 32, FIT ? 1 : 5) k_waveform(const 
               bs = s2;
             }
           }
-          const double width = FIT ? fit_echo_width(W, S, nb, (int)kk, a.fit_half, a.delta_ns,
-                                                    a.fit_s0)
-                                   : __longlong_as_double(0x7ff8000000000000ll);
+          if (a.fit) {
+            // echo-width job (R28): the echo's window, fitted later by k_fit
+            int lo, hi;
+            echo_window(W, S, nb, (int)kk, a.fit_half, lo, hi);
+            unsigned job = 0;
+            if (lane == 0) job = atomicAdd(a.fit_count, 1u);
+            job = __shfl_sync(0xffffffffu, job, 0);
+            double* y = a.fit_y + (size_t)job * a.fit_stride;
+            for (int i = lane; i <= hi - lo; i += 32)
+              y[i] = (uint32_t)(lo + i) < S ? W[lo + i] : 0.0;
+            if (lane == 0) {
+              FitJob fj;
+              fj.slot = (uint32_t)(p * a.max_returns + nret);
+              fj.lo = (int16_t)(lo - (int)kk);
+              fj.n = (uint16_t)(hi - lo + 1);
+              fj.peak = W[kk];
+              a.fit_jobs[job] = fj;
+            }
+          }
           if (lane == 0) {
             helios_return r;
             r.range_m = 0.5 * kC * ((double)(k0 + (long long)kk - (long long)a.jstar) + 0.5) *
@@ -384,7 +411,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, FIT ? 1 : 5) k_waveform(const 
             r.return_number = (uint8_t)(nret + 1);
             r.n_returns = 0;  // patched below once the count is known
             r.pad[0] = r.pad[1] = 0;
-            r.echo_width_ns = (float)width;
+            r.echo_width_ns = __int_as_float(0x7fc00000);  // NaN until k_fit (R28)
             slots[nret] = r;
           }
           ++nret;
@@ -471,9 +498,9 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaFuncSetAttribute(k_waveform<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_waveform, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)pl.smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform<false>, warps * 32, pl.smem) !=
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform, warps * 32, pl.smem) !=
           cudaSuccess ||
       per_sm < 1) {
     cudaGetLastError();
@@ -523,23 +550,16 @@ cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scrat
   uint64_t grid = pl.grid;
   if (pl.grid_cap && pl.grid_cap < grid) grid = pl.grid_cap;
   if (want < grid) grid = want;
-  if (a.fit) {
-    // the fit instance has its own register budget: size its grid on its own
-    int dev = 0, sms = 148, ps = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(k_waveform<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_waveform<true>, pl.warps * 32,
-                                                        pl.smem);
-    if (e != cudaSuccess) return e;
-    if (ps < 1) return cudaErrorInvalidConfiguration;
-    const uint64_t g2 = std::min<uint64_t>(grid, (uint64_t)sms * ps);
-    k_waveform<true><<<(unsigned)g2, pl.warps * 32, pl.smem, s>>>(a, scratch);
-  } else {
-    k_waveform<false><<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
-  }
+  k_waveform<<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !a.fit) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t jobs_max = a.n_pulses * a.max_returns;
+  const uint64_t fb = std::min<uint64_t>((jobs_max + 127) / 128, (uint64_t)sms * 16);
+  k_fit<<<(unsigned)fb, 128, 0, s>>>(a.fit_jobs, a.fit_y, a.fit_stride, a.fit_count, a.fit_half,
+                                     a.delta_ns, a.fit_s0, a.returns);
   return cudaGetLastError();
 }
 
