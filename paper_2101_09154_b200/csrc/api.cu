@@ -44,13 +44,15 @@ struct helios_scene_s {
     bool busy;
     cudaStream_t copy;  // non-blocking copy stream for host staging (lazy)
     cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
+    cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
     uint64_t* pinned;   // 4 pinned words: per chunk slot (first, last) row offset (lazy)
   };
   std::mutex mu;
   std::vector<Slot> slots;
 
   cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy,
-                      cudaStream_t* wave, uint64_t** pinned = nullptr) {
+                      cudaStream_t* wave, uint64_t** pinned = nullptr,
+                      cudaStream_t* fit = nullptr) {
     std::lock_guard<std::mutex> g(mu);
     Slot* use = nullptr;
     for (Slot& sl : slots)
@@ -59,7 +61,7 @@ struct helios_scene_s {
         break;
       }
     if (!use) {
-      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr});
+      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
@@ -82,6 +84,13 @@ struct helios_scene_s {
       if (e != cudaSuccess) return e;
     }
     *wave = use->wave;
+    if (fit) {
+      if (!use->fit) {
+        cudaError_t e = cudaStreamCreateWithFlags(&use->fit, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+      }
+      *fit = use->fit;
+    }
     if (!use->pinned) {
       cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * sizeof(uint64_t));
       if (e != cudaSuccess) return e;
@@ -110,6 +119,10 @@ struct helios_scene_s {
       if (sl.wave) {
         cudaStreamSynchronize(sl.wave);
         cudaStreamDestroy(sl.wave);
+      }
+      if (sl.fit) {
+        cudaStreamSynchronize(sl.fit);
+        cudaStreamDestroy(sl.fit);
       }
       cudaFree(sl.ptr);
       if (sl.pinned) cudaFreeHost(sl.pinned);
@@ -558,20 +571,25 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const uint32_t fit_stride = 2u * (uint32_t)std::ceil(3.0 * params->pulse_length_ns /
                                                         params->bin_width_ns) + 1u;
   const bool fit = params->fit_echo_width != 0;
-  const size_t o_fjob = carve(fit ? sizeof(FitJob) * chunk * R : 0);
-  const size_t o_fy = carve(fit ? sizeof(double) * fit_stride * chunk * R : 0);
-  const size_t o_fcnt = carve(fit ? sizeof(unsigned) : 0);
+  // two job buffers: k_fit(c) on its own stream overlaps K7(c+1) and K6(c+2)
+  const size_t o_fjob[2] = {carve(fit ? sizeof(FitJob) * chunk * R : 0),
+                            carve(fit ? sizeof(FitJob) * chunk * R : 0)};
+  const size_t o_fy[2] = {carve(fit ? sizeof(double) * fit_stride * chunk * R : 0),
+                          carve(fit ? sizeof(double) * fit_stride * chunk * R : 0)};
+  const size_t o_fcnt = carve(fit ? 2 * sizeof(unsigned) : 0);
   const size_t o_cst[2] = {carve(compact_staged ? 4ull * d.n_bins * chunk : 0),
                            carve(compact_staged ? 4ull * d.n_bins * chunk : 0)};
 
   char* buf = nullptr;
-  cudaStream_t cs = nullptr, ws = nullptr;
+  cudaStream_t cs = nullptr, ws = nullptr, fs = nullptr;
   uint64_t* pin = nullptr;  // [slot][first, last] row offsets of a staged compact chunk
-  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr, &ws, &pin);
+  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr, &ws, &pin,
+                              fit ? &fs : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
     cudaStreamSynchronize(ws);
+    if (fs) cudaStreamSynchronize(fs);
     if (cs) cudaStreamSynchronize(cs);
     sc->release(s);
   };
@@ -637,10 +655,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   wa.fit_s0 = params->pulse_length_ns / (2.0 * std::sqrt(2.0 * std::log(2.0)));
   wa.counters = counters ? d_cnt + 4 : nullptr;
   wa.noise_sd = params->range_noise_sd_m;
-  wa.fit_jobs = reinterpret_cast<FitJob*>(buf + o_fjob);
-  wa.fit_y = reinterpret_cast<double*>(buf + o_fy);
   wa.fit_stride = fit_stride;
-  wa.fit_count = reinterpret_cast<unsigned*>(buf + o_fcnt);
   wa.compact = compact_staged ? nullptr : outputs->p_wf_compact;
   wa.compact_staged = compact_staged ? 1 : 0;
   wa.capacity = outputs->p_wf_compact ? outputs->wf_compact_capacity : 0;
@@ -664,8 +679,10 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   // so K7(c) runs concurrently with K6(c+1) and the copies with both.
   cudaEvent_t in_done[2] = {}, t_done[2] = {}, w_done[2] = {}, out_done[2] = {};
   cudaEvent_t off_done[2] = {}, cd_done[2] = {};  // compact: offsets of chunk known / drained
+  cudaEvent_t k7_done[2] = {};                     // fit: K7 of the chunk done, jobs listed
   for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess && fit) e = cudaEventCreateWithFlags(&k7_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess && compact_staged) {
       e = cudaEventCreateWithFlags(&off_done[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cd_done[k], cudaEventDisableTiming);
@@ -791,16 +808,33 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     wa.waveform = (float*)dev_ptr(arrs[6], slot, b);
     wa.offs = want_offs ? d_offs + b : nullptr;
     if (compact_staged) wa.compact = reinterpret_cast<float*>(buf + o_cst[slot]);
+    if (fit) {
+      wa.fit_jobs = reinterpret_cast<FitJob*>(buf + o_fjob[slot]);
+      wa.fit_y = reinterpret_cast<double*>(buf + o_fy[slot]);
+      wa.fit_count = reinterpret_cast<unsigned*>(buf + o_fcnt) + slot;
+      // the slot's jobs of chunk c-2 must be fitted before they are overwritten
+      if (c >= 2 && ws != s) e = cudaStreamWaitEvent(ws, w_done[slot], 0);
+      if (e == cudaSuccess) e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
+    }
     mark(ev_w, ws);
-    if (fit) e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
     if (e == cudaSuccess) e = launch_waveform(wa, plan, d_wscratch, ws);
-    if (fit) ++launches;
     if (e == cudaSuccess && wa.noise_sd > 0.0) {
       e = launch_range_noise(wa, ws);
       ++launches;
     }
     mark(ev_w, ws);
-    if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], ws);
+    if (e == cudaSuccess && fit) {
+      // echo-width fits on their own stream (their tail overlaps later chunks);
+      // the chunk's outputs are complete once they are done
+      cudaStream_t f = ws == s ? s : fs;
+      if (f != ws) e = cudaEventRecord(k7_done[slot], ws);
+      if (e == cudaSuccess && f != ws) e = cudaStreamWaitEvent(f, k7_done[slot], 0);
+      if (e == cudaSuccess) e = launch_fit(wa, f);
+      ++launches;
+      if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], f);
+    } else if (e == cudaSuccess) {
+      e = cudaEventRecord(w_done[slot], ws);
+    }
     launches += 2;
     if (e == cudaSuccess && compact_staged && c >= 1) e = drain_compact(c - 1);
     if (e != cudaSuccess || !any_staged) continue;
@@ -842,6 +876,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && cs) e = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws);
+  if (e == cudaSuccess && fs) e = cudaStreamSynchronize(fs);
   double t_trace = 0.0, t_wave = 0.0;
   for (size_t i = 0; i + 1 < ev_t.size(); i += 2) {
     float a = 0.f;
@@ -860,6 +895,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     if (out_done[k]) cudaEventDestroy(out_done[k]);
     if (off_done[k]) cudaEventDestroy(off_done[k]);
     if (cd_done[k]) cudaEventDestroy(cd_done[k]);
+    if (k7_done[k]) cudaEventDestroy(k7_done[k]);
   }
   cudaGetLastError();
   cleanup();

@@ -151,6 +151,8 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);
 cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_pulses,
                            uint32_t n_bins, uint32_t taps, double delta_ns, uint64_t* len,
                            cudaStream_t s);
+// echo-width fits of the jobs one K7 launch appended (after it; any stream)
+cudaError_t launch_fit(const WaveArgs& a, cudaStream_t s);
 // ranging error on the returns of one launch (after K7, same stream)
 cudaError_t launch_range_noise(const WaveArgs& a, cudaStream_t s);
 // offs[1 + i] += offs[0] for i < m (carry of the previous chunks)

@@ -79,7 +79,9 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // Split in two: K7 finds each return's echo window (warp ballots over the
 // fp64 waveform in shared memory) and appends a job {slot, window} to a
 // per-launch list; k_fit then runs one LM per THREAD, summing the window
-// sequentially in bin order (no warp reductions on the critical path).
+// sequentially in bin order (no warp reductions on the critical path; 1/s
+// once per pass instead of a division per bin -- same optimum, rounding-level
+// differences from the oracle's (x - m) / s).
 
 // window [k + lo, k + hi] of the echo at k (all lanes; result warp-uniform)
 __device__ __forceinline__ void echo_window(const double* __restrict__ W, uint32_t S, uint32_t nb,
@@ -110,8 +112,10 @@ __device__ __forceinline__ void echo_window(const double* __restrict__ W, uint32
 __device__ __forceinline__ double sse_gauss(const double* __restrict__ y, int n, int lo,
                                             double delta, double A, double m, double s) {
   double acc = 0.0;
+  const double is = 1.0 / s;
+#pragma unroll 4
   for (int i = 0; i < n; ++i) {
-    const double z = ((double)(lo + i) * delta - m) / s;
+    const double z = ((double)(lo + i) * delta - m) * is;
     const double r = y[i] - A * exp(-0.5 * z * z);
     acc += r * r;
   }
@@ -119,7 +123,7 @@ __device__ __forceinline__ double sse_gauss(const double* __restrict__ y, int n,
 }
 
 // One LM fit per thread over the job list of one K7 launch.
-__global__ void __launch_bounds__(128) k_fit(const FitJob* __restrict__ jobs,
+__global__ void __launch_bounds__(64) k_fit(const FitJob* __restrict__ jobs,
                                              const double* __restrict__ ys, uint32_t stride,
                                              const unsigned* __restrict__ count, int half,
                                              double delta, double s0,
@@ -132,17 +136,25 @@ __global__ void __launch_bounds__(128) k_fit(const FitJob* __restrict__ jobs,
     const int lo = job.lo;  // first window bin relative to the peak: x_i = (lo + i) Delta
     double A = job.peak, m = 0.0, s = s0, lambda = 1e-3;
     double cur = sse_gauss(y, n, lo, delta, A, m, s);
-    bool converged = false;
+    bool converged = false, need_h = true;
+    double h00 = 0, h01 = 0, h02 = 0, h11 = 0, h12 = 0, h22 = 0, g0 = 0, g1 = 0, g2 = 0;
     for (int it = 0; it < 100; ++it) {
-      double h00 = 0, h01 = 0, h02 = 0, h11 = 0, h12 = 0, h22 = 0, g0 = 0, g1 = 0, g2 = 0;
+      // J^T J and J^T r depend on (A, m, s) only: a rejected step (only lambda
+      // changes) reuses them -- the same values the oracle recomputes
+      if (need_h) {
+      need_h = false;
+      h00 = h01 = h02 = h11 = h12 = h22 = g0 = g1 = g2 = 0.0;
+      const double is = 1.0 / s, Ais = A * is;  // one division per pass, not per bin
+#pragma unroll 4
       for (int i = 0; i < n; ++i) {
-        const double z = ((double)(lo + i) * delta - m) / s;
+        const double z = ((double)(lo + i) * delta - m) * is;
         const double e = exp(-0.5 * z * z);
-        const double j0 = e, j1 = A * e * z / s, j2 = A * e * z * z / s;
+        const double j0 = e, j1 = Ais * e * z, j2 = j1 * z;
         const double r = y[i] - A * e;
         g0 += j0 * r; g1 += j1 * r; g2 += j2 * r;
         h00 += j0 * j0; h01 += j0 * j1; h02 += j0 * j2;
         h11 += j1 * j1; h12 += j1 * j2; h22 += j2 * j2;
+      }
       }
       const double m00 = h00 + lambda * h00, m11 = h11 + lambda * h11, m22 = h22 + lambda * h22;
       const double m01 = h01, m02 = h02, m12 = h12;  // symmetric
@@ -164,6 +176,7 @@ __global__ void __launch_bounds__(128) k_fit(const FitJob* __restrict__ jobs,
         s = ns;
         cur = next;
         lambda /= 10.0;
+        need_h = true;
         if (rel < 1e-10) {
           converged = true;
           break;
@@ -551,15 +564,18 @@ cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scrat
   if (pl.grid_cap && pl.grid_cap < grid) grid = pl.grid_cap;
   if (want < grid) grid = want;
   k_waveform<<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || !a.fit) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fit(const WaveArgs& a, cudaStream_t s) {
+  if (a.n_pulses == 0 || !a.fit) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t jobs_max = a.n_pulses * a.max_returns;
-  const uint64_t fb = std::min<uint64_t>((jobs_max + 127) / 128, (uint64_t)sms * 16);
-  k_fit<<<(unsigned)fb, 128, 0, s>>>(a.fit_jobs, a.fit_y, a.fit_stride, a.fit_count, a.fit_half,
-                                     a.delta_ns, a.fit_s0, a.returns);
+  const uint64_t fb = std::min<uint64_t>((jobs_max + 63) / 64, (uint64_t)sms * 32);
+  k_fit<<<(unsigned)fb, 64, 0, s>>>(a.fit_jobs, a.fit_y, a.fit_stride, a.fit_count, a.fit_half,
+                                    a.delta_ns, a.fit_s0, a.returns);
   return cudaGetLastError();
 }
 

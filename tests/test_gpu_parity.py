@@ -106,3 +106,26 @@ def test_range_noise():
     dz = (b["returns"]["range_m"] - a["returns"]["range_m"])[used] / 0.05
     assert used.sum() > 300 and 0.7 < dz.std() < 1.3 and abs(dz.mean()) < 0.2
     assert np.array_equal(a["waveform"], b["waveform"])
+
+
+def test_echo_width_host_staged_multi_chunk_matches_device():
+    # the fits run on their own stream, one chunk behind K7; staged host
+    # outputs must still carry every chunk's widths
+    import torch
+    import paper_2101_09154_b200 as h
+    from dataclasses import replace
+    from gpu_util import scene_for
+    w = workload("C3", 0.03)
+    p = replace(w.params, subray_count=279, fit_echo_width=1)
+    n = 25000
+    o, d, t = w.pulses(100, n)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    a, _ = h.simulate(scene_for(w), p, dev(o), dev(d), dev(t), pulse_index_base=100)
+    a = a.numpy()
+    out = h.alloc_outputs(n, h.make_params(p), device="cpu", pin_memory=True)
+    h.simulate(scene_for(w), p, *(torch.from_numpy(x).pin_memory() for x in (o, d, t)),
+               pulse_index_base=100, outputs=out)
+    b = out.numpy()
+    assert np.array_equal(a["returns"].view(np.uint8), b["returns"].view(np.uint8))
+    used = np.arange(a["returns"].shape[1])[None, :] < a["n_returns"][:, None]
+    assert np.isfinite(a["returns"]["echo_width_ns"][used]).mean() > 0.9
