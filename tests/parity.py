@@ -210,7 +210,8 @@ def gpu_invariants(gpu: dict, max_returns: int, thr: float) -> list:
     idx = np.arange(R)[None, :]
     used = idx < nr[:, None]
     rng = ret["range_m"]
-    inc = np.diff(np.where(used, rng, np.inf), axis=1)
+    with np.errstate(invalid="ignore"):
+        inc = np.diff(np.where(used, rng, np.inf), axis=1)
     if np.any((inc <= 0) & used[:, 1:]):
         errs.append("return ranges not increasing")
     raw = ret.view(np.uint8).reshape(ret.shape[0], R, 32) if ret.dtype.itemsize == 32 else None
