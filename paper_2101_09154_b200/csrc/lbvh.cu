@@ -14,9 +14,13 @@
 // fp32 min/max of fp32 vertices is exact, so every box contains its
 // triangles exactly; traversal adds the conservative slack (trace.cu).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <vector>
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -264,6 +268,185 @@ __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict
   out[k] = rec;
 }
 
+// ---- PLOC (parallel locally-ordered clustering, Meister & Bittner 2018) ----
+// Alternative hierarchy (HELIOS_BUILDER=ploc): clusters start as the sorted
+// triangles; each iteration every cluster finds, among the 2R clusters around
+// it in Morton order, the one whose merged box has the smallest surface area
+// (ties -> lower index); mutual nearest neighbours merge (the lower index
+// keeps the slot), the array is compacted (one 64-bit scan carries both the
+// compaction and the node-allocation counts: deterministic ids), until one
+// cluster is left.  Leaves are then ordered depth-first (offsets top-down,
+// iteration by iteration) so collapsed subtrees are contiguous triangle runs.
+constexpr int kPlocBlock = 256;
+#ifndef HELIOS_DEFAULT_PLOC
+#define HELIOS_DEFAULT_PLOC 0
+#endif
+constexpr bool kDefaultPloc = HELIOS_DEFAULT_PLOC != 0;
+
+__device__ __forceinline__ float merged_area(const float* a, const float* b) {
+  const float dx = fmaxf(a[3], b[3]) - fminf(a[0], b[0]);
+  const float dy = fmaxf(a[4], b[4]) - fminf(a[1], b[1]);
+  const float dz = fmaxf(a[5], b[5]) - fminf(a[2], b[2]);
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_ploc_init(const float* __restrict__ xyz, const uint32_t* __restrict__ sorted_idx,
+                            uint32_t n, int* __restrict__ cid, float* __restrict__ cbox,
+                            uint32_t* __restrict__ size) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const Box b = tri_box(xyz, sorted_idx[k]);
+  cid[k] = (int)k;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cbox[6ull * k + a] = b.lo[a];
+    cbox[6ull * k + 3 + a] = b.hi[a];
+  }
+  size[k] = 1;
+}
+
+__global__ void k_ploc_nn(const float* __restrict__ cbox, uint32_t m, int r, int* __restrict__ nn) {
+  extern __shared__ float sb[];
+  const int b0 = blockIdx.x * kPlocBlock;
+  const int lo = max(0, b0 - r), hi = min((int)m, b0 + kPlocBlock + r);
+  for (int t = threadIdx.x; t < (hi - lo) * 6; t += blockDim.x) sb[t] = cbox[6ll * lo + t];
+  __syncthreads();
+  const int i = b0 + threadIdx.x;
+  if (i >= (int)m) return;
+  const float* bi = sb + 6 * (i - lo);
+  float best = INFINITY;
+  int bj = -1;
+  const int j0 = max(0, i - r), j1 = min((int)m - 1, i + r);
+  for (int j = j0; j <= j1; ++j) {
+    if (j == i) continue;
+    const float a = merged_area(bi, sb + 6 * (j - lo));
+    if (a < best) {
+      best = a;
+      bj = j;
+    }
+  }
+  nn[i] = bj;
+}
+
+// low 32 bits: cluster survives; high 32 bits: cluster creates a node
+__global__ void k_ploc_flags(const int* __restrict__ nn, uint32_t m,
+                             unsigned long long* __restrict__ flags) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int j = nn[i];
+  const bool mutual = j >= 0 && nn[j] == (int)i;
+  const unsigned long long keep = (mutual && (int)i > j) ? 0ull : 1ull;
+  const unsigned long long create = (mutual && (int)i < j) ? 1ull : 0ull;
+  flags[i] = keep | (create << 32);
+}
+
+__global__ void k_ploc_merge(const int* __restrict__ nn, uint32_t m,
+                             const unsigned long long* __restrict__ flags,
+                             const unsigned long long* __restrict__ incl, uint32_t n,
+                             uint32_t node_base, const int* __restrict__ cid,
+                             const float* __restrict__ cbox, int* __restrict__ cid2,
+                             float* __restrict__ cbox2, int* __restrict__ child,
+                             float* __restrict__ nodebox, uint32_t* __restrict__ size,
+                             int* __restrict__ parent) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const unsigned long long f = flags[i];
+  if (!(f & 0xFFFFFFFFull)) return;
+  const unsigned long long ex = incl[i] - f;  // exclusive prefix
+  const uint32_t dst = (uint32_t)(ex & 0xFFFFFFFFull);
+  const float* bi = cbox + 6ull * i;
+  if (f >> 32) {
+    const int j = nn[i];
+    const uint32_t u = node_base + (uint32_t)(ex >> 32);  // internal node index
+    const int v = (int)(n + u);
+    const int a = cid[i], b = cid[j];
+    const float* bj = cbox + 6ull * j;
+    float ub[6];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      ub[q] = fminf(bi[q], bj[q]);
+      ub[3 + q] = fmaxf(bi[3 + q], bj[3 + q]);
+    }
+    child[2 * u] = a;
+    child[2 * u + 1] = b;
+    size[v] = size[a] + size[b];
+    parent[a] = v;
+    parent[b] = v;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      nodebox[6ull * u + q] = ub[q];
+      cbox2[6ull * dst + q] = ub[q];
+    }
+    cid2[dst] = v;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) cbox2[6ull * dst + q] = bi[q];
+    cid2[dst] = cid[i];
+  }
+}
+
+// top-down leaf offsets for the nodes created in one PLOC iteration (their
+// parents were created later, so are already placed); depth of kept nodes
+__global__ void k_ploc_offsets(uint32_t u0, uint32_t cnt, uint32_t n,
+                               const int* __restrict__ child, const uint32_t* __restrict__ size,
+                               uint32_t* __restrict__ off, uint32_t* __restrict__ depth,
+                               unsigned* __restrict__ max_depth) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const uint32_t u = u0 + t, v = n + u;
+  const int a = child[2 * u], b = child[2 * u + 1];
+  const uint32_t o = off[v], d = depth[v];
+  off[a] = o;
+  off[b] = o + size[a];
+  depth[a] = d + 1;
+  depth[b] = d + 1;
+  if (size[v] > (uint32_t)kLeafMax) atomicMax(max_depth, d);
+}
+
+__global__ void k_ploc_order(const uint32_t* __restrict__ sorted_idx, uint32_t n,
+                             const uint32_t* __restrict__ off, uint32_t* __restrict__ order,
+                             float* __restrict__ leafbox, const float* __restrict__ xyz) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  order[off[k]] = sorted_idx[k];
+  const Box b = tri_box(xyz, sorted_idx[k]);
+  store_box(leafbox + 6ull * k, b);
+}
+
+__device__ __forceinline__ int32_t ploc_ref(int c, uint32_t n, const uint32_t* __restrict__ size,
+                                            const uint32_t* __restrict__ off) {
+  const uint32_t sz = size[c];
+  if (sz <= (uint32_t)kLeafMax) return leaf_ref(off[c], sz);
+  return (int32_t)((uint32_t)c - n);
+}
+
+__global__ void k_ploc_layout(uint32_t n, const int* __restrict__ child,
+                              const uint32_t* __restrict__ size, const uint32_t* __restrict__ off,
+                              const float* __restrict__ leafbox, const float* __restrict__ nodebox,
+                              Node* __restrict__ nodes) {
+  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n - 1) return;
+  if (size[n + u] <= (uint32_t)kLeafMax) return;  // collapsed into its parent's leaf
+  const int c0 = child[2 * u], c1 = child[2 * u + 1];
+  const float* q0 = c0 < (int)n ? leafbox + 6ull * c0 : nodebox + 6ull * (c0 - n);
+  const float* q1 = c1 < (int)n ? leafbox + 6ull * c1 : nodebox + 6ull * (c1 - n);
+  float b0[6], b1[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b0[a] = __fsub_rd(q0[a], fmaf(fabsf(q0[a]), 1e-6f, 1e-30f));
+    b0[3 + a] = __fadd_ru(q0[3 + a], fmaf(fabsf(q0[3 + a]), 1e-6f, 1e-30f));
+    b1[a] = __fsub_rd(q1[a], fmaf(fabsf(q1[a]), 1e-6f, 1e-30f));
+    b1[3 + a] = __fadd_ru(q1[3 + a], fmaf(fabsf(q1[3 + a]), 1e-6f, 1e-30f));
+  }
+  Node nd;
+  nd.xy0 = make_float4(b0[0], b0[3], b0[1], b0[4]);
+  nd.xy1 = make_float4(b1[0], b1[3], b1[1], b1[4]);
+  nd.z01 = make_float4(b0[2], b0[5], b1[2], b1[5]);
+  nd.ref = make_float4(__int_as_float(ploc_ref(c0, n, size, off)),
+                       __int_as_float(ploc_ref(c1, n, size, off)), 0.0f, 0.0f);
+  nodes[u] = nd;
+}
+
 // ---- 4-wide collapse (top-down, one kernel per level) ----------------------
 // Each queue entry (binary node b, wide node w) expands b's children greedily:
 // while fewer than 4, replace the internal child with the largest box surface
@@ -391,12 +574,25 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   const unsigned ni = n > 1 ? (n - 1 + T - 1) / T : 1;
   unsigned init_bounds[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
   unsigned hdepth = 0;
+  uint32_t* idx_s_final = nullptr;  // leaf order (PLOC), else the Morton order
   // tuning knobs for measurements (DESIGN.md s.8): HELIOS_MORTON_BITS (1..21),
   // HELIOS_MORTON_ANISO=1 (per-axis normalisation)
   int bits = kMortonBits, isotropic = 1;
   if (const char* v = getenv("HELIOS_MORTON_BITS")) bits = atoi(v);
   if (bits < 1 || bits > 21) bits = kMortonBits;
   if (const char* v = getenv("HELIOS_MORTON_ANISO")) isotropic = atoi(v) ? 0 : 1;
+  // hierarchy: HELIOS_BUILDER=lbvh (Karras) | ploc (default: see DESIGN.md s.7.1)
+  bool use_ploc = kDefaultPloc;
+  if (const char* v = getenv("HELIOS_BUILDER")) use_ploc = strcmp(v, "lbvh") != 0;
+  int ploc_r = 16;
+  if (const char* v = getenv("HELIOS_PLOC_R")) ploc_r = atoi(v);
+  if (ploc_r < 1 || ploc_r > 256) ploc_r = 16;
+  int *pcid = nullptr, *pcid2 = nullptr, *pnn = nullptr, *pparent = nullptr;
+  float *pbox = nullptr, *pbox2 = nullptr;
+  uint32_t *psize = nullptr, *poff = nullptr, *pdepth = nullptr, *porder = nullptr;
+  unsigned long long *pflags = nullptr, *pincl = nullptr;
+  void* ptemp = nullptr;
+  size_t ptemp_bytes = 0;
 
 #define CK(x)                 \
   do {                        \
@@ -430,6 +626,79 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     out->root = leaf_ref(0, n);
     out->root4 = out->root;
     out->max_depth = 0;
+  } else if (use_ploc) {
+    CK(dalloc(&pcid, n, s));
+    CK(dalloc(&pcid2, n, s));
+    CK(dalloc(&pnn, n, s));
+    CK(dalloc(&pbox, 6ull * n, s));
+    CK(dalloc(&pbox2, 6ull * n, s));
+    CK(dalloc(&pflags, n, s));
+    CK(dalloc(&pincl, n, s));
+    CK(dalloc(&psize, 2ull * n - 1, s));
+    CK(dalloc(&pparent, 2ull * n - 1, s));
+    CK(dalloc(&poff, 2ull * n - 1, s));
+    CK(dalloc(&pdepth, 2ull * n - 1, s));
+    CK(dalloc(&porder, n, s));
+    CK(dalloc(&child, 2ull * (n - 1), s));
+    CK(dalloc(&leafbox, 6ull * n, s));
+    CK(dalloc(&nodebox, 6ull * (n - 1), s));
+    CK(dalloc(&dmax, 1, s));
+    CK(dalloc(&out->nodes, n - 1, s));
+    CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned), s));
+    CK(cub::DeviceScan::InclusiveSum(nullptr, ptemp_bytes, pflags, pincl, (int)n, s));
+    CK(cudaMallocAsync(&ptemp, ptemp_bytes ? ptemp_bytes : 1, s));
+    k_ploc_init<<<nb, T, 0, s>>>(xyz, idx_s, n, pcid, pbox, psize);
+    CK(cudaGetLastError());
+    {
+      uint32_t m = n, base = 0;
+      std::vector<uint32_t> it_base, it_cnt;
+      const size_t smem = sizeof(float) * 6 * (kPlocBlock + 2 * ploc_r);
+      while (m > 1) {
+        const unsigned gb = (m + kPlocBlock - 1) / kPlocBlock;
+        k_ploc_nn<<<gb, kPlocBlock, smem, s>>>(pbox, m, ploc_r, pnn);
+        CK(cudaGetLastError());
+        k_ploc_flags<<<(m + T - 1) / T, T, 0, s>>>(pnn, m, pflags);
+        CK(cudaGetLastError());
+        size_t tb = ptemp_bytes;
+        CK(cub::DeviceScan::InclusiveSum(ptemp, tb, pflags, pincl, (int)m, s));
+        k_ploc_merge<<<(m + T - 1) / T, T, 0, s>>>(pnn, m, pflags, pincl, n, base, pcid, pbox,
+                                                  pcid2, pbox2, child, nodebox, psize, pparent);
+        CK(cudaGetLastError());
+        unsigned long long tot = 0;
+        CK(cudaMemcpyAsync(&tot, pincl + (m - 1), sizeof(tot), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint32_t made = (uint32_t)(tot >> 32), keep = (uint32_t)(tot & 0xFFFFFFFFull);
+        if (made == 0) {
+          snprintf(err, err_len, "build_ploc: no merge in an iteration (m = %u)", m);
+          e = cudaErrorUnknown;
+          goto done;
+        }
+        it_base.push_back(base);
+        it_cnt.push_back(made);
+        base += made;
+        m = keep;
+        std::swap(pcid, pcid2);
+        std::swap(pbox, pbox2);
+      }
+      // depth-first leaf offsets, top-down: iterations in reverse creation order
+      const uint32_t root_v = n + (n - 2);
+      const uint32_t one = 1, zero = 0;
+      CK(cudaMemcpyAsync(poff + root_v, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(pdepth + root_v, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+      for (size_t t = it_base.size(); t-- > 0;) {
+        k_ploc_offsets<<<(it_cnt[t] + T - 1) / T, T, 0, s>>>(it_base[t], it_cnt[t], n, child,
+                                                            psize, poff, pdepth, dmax);
+        CK(cudaGetLastError());
+      }
+    }
+    k_ploc_order<<<nb, T, 0, s>>>(idx_s, n, poff, porder, leafbox, xyz);
+    CK(cudaGetLastError());
+    k_ploc_layout<<<ni, T, 0, s>>>(n, child, psize, poff, leafbox, nodebox, out->nodes);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&hdepth, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    out->n_nodes = n - 1;
+    out->root = (int32_t)(n - 2);
+    idx_s_final = porder;
   } else {
     CK(dalloc(&child, 2ull * (n - 1), s));
     CK(dalloc(&range, 2ull * (n - 1), s));
@@ -489,7 +758,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     out->root4 = 0;
     }
   }
-  k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s, n, out->tris);
+  k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s_final ? idx_s_final : idx_s, n, out->tris);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
@@ -520,6 +789,19 @@ done:
   cudaFreeAsync(qa, s);
   cudaFreeAsync(qb, s);
   cudaFreeAsync(wide_tmp, s);
+  cudaFreeAsync(pcid, s);
+  cudaFreeAsync(pcid2, s);
+  cudaFreeAsync(pnn, s);
+  cudaFreeAsync(pbox, s);
+  cudaFreeAsync(pbox2, s);
+  cudaFreeAsync(pflags, s);
+  cudaFreeAsync(pincl, s);
+  cudaFreeAsync(psize, s);
+  cudaFreeAsync(pparent, s);
+  cudaFreeAsync(poff, s);
+  cudaFreeAsync(pdepth, s);
+  cudaFreeAsync(porder, s);
+  cudaFreeAsync(ptemp, s);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   if (e != cudaSuccess) {

@@ -28,9 +28,12 @@ def _soup(n, seed, extent=10.0, size=1.0):
     return (c + rng.uniform(-size, size, (n, 3, 3))).astype(np.float32)
 
 
+@pytest.mark.parametrize("builder", ["lbvh", "ploc"])
 @pytest.mark.parametrize("n_tris", [1, 2, 3, 4, 5, 17, 1000, 10000])
-def test_bvh_equals_brute_force_random_soup(n_tris):
+def test_bvh_equals_brute_force_random_soup(n_tris, builder, monkeypatch):
     # S:87/S:725 shape: random rays vs random triangles; ids exact, t within 1e-9
+    # (both hierarchies: Karras LBVH and PLOC, HELIOS_BUILDER)
+    monkeypatch.setenv("HELIOS_BUILDER", builder)
     h = _h()
     tris = _soup(n_tris, n_tris, size=2.0 if n_tris < 100 else 0.7)
     refl = np.random.default_rng(1).uniform(0.1, 0.9, n_tris).astype(np.float32)
