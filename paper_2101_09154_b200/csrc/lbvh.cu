@@ -279,7 +279,7 @@ __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict
 // iteration by iteration) so collapsed subtrees are contiguous triangle runs.
 constexpr int kPlocBlock = 256;
 #ifndef HELIOS_DEFAULT_PLOC
-#define HELIOS_DEFAULT_PLOC 0
+#define HELIOS_DEFAULT_PLOC 1
 #endif
 constexpr bool kDefaultPloc = HELIOS_DEFAULT_PLOC != 0;
 
