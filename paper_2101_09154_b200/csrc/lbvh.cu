@@ -584,9 +584,9 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   // hierarchy: HELIOS_BUILDER=lbvh (Karras) | ploc (default: see DESIGN.md s.7.1)
   bool use_ploc = kDefaultPloc;
   if (const char* v = getenv("HELIOS_BUILDER")) use_ploc = strcmp(v, "lbvh") != 0;
-  int ploc_r = 16;
+  int ploc_r = 32;
   if (const char* v = getenv("HELIOS_PLOC_R")) ploc_r = atoi(v);
-  if (ploc_r < 1 || ploc_r > 256) ploc_r = 16;
+  if (ploc_r < 1 || ploc_r > 256) ploc_r = 32;
   int *pcid = nullptr, *pcid2 = nullptr, *pnn = nullptr, *pparent = nullptr;
   float *pbox = nullptr, *pbox2 = nullptr;
   uint32_t *psize = nullptr, *poff = nullptr, *pdepth = nullptr, *porder = nullptr;
