@@ -103,6 +103,8 @@ def lib():
         L.oracle_g_function.argtypes = [_vp, _u32, _d]
         L.oracle_voxel_segments.restype = _i64
         L.oracle_voxel_segments.argtypes = [_vp, _vp, _vp, _vp, _d, _d, _vp, _vp, _vp, _i64]
+        L.oracle_generate_pulses.restype = None
+        L.oracle_generate_pulses.argtypes = [_vp, _u64, _i64, _vp, _vp, _vp]
         L.oracle_range_noise.restype = _d
         L.oracle_range_noise.argtypes = [_u64, _u64, _u32]
         L.oracle_fit_echo_width.restype = _d
@@ -224,6 +226,43 @@ def voxel_segments(o, d, n, origin, vs, t_max=float("inf")):
                                     _p(ta), _p(tb), _p(vid), cap)
     k = abs(int(k))
     return ta[:k].copy(), tb[:k].copy(), vid[:k].copy()
+
+
+class OracleSurvey(ctypes.Structure):
+    _fields_ = [("waypoints", _vp), ("n_waypoints", _u32), ("deflector", _u32),
+                ("speed_m_s", _d), ("mount", _d * 9), ("mount_offset", _d * 3),
+                ("head_rotation_rad_s", _d), ("pulse_freq_hz", _d), ("t0_s", _d),
+                ("scan_freq_hz", _d), ("scan_angle_rad", _d), ("n_fibres", _u32),
+                ("pad_", _u32)]
+
+
+DEFLECTORS = {"polygon": 0, "fibre": 1, "oscillating": 2, "palmer": 3}
+
+
+def generate_pulses(survey, first: int, n: int):
+    """(origin f32 [n,3], direction f32 [n,3], time f64 [n]) of pulses
+    first .. first+n-1 of a survey (P:155 platforms, P:177 deflectors; R30).
+    `survey`: workloads.Survey (or any object with its fields)."""
+    wp = np.ascontiguousarray(survey.waypoints, np.float64).reshape(-1, 3)
+    sv = OracleSurvey()
+    sv.waypoints = _p(wp)
+    sv.n_waypoints = wp.shape[0]
+    sv.deflector = DEFLECTORS[survey.deflector] if isinstance(survey.deflector, str) \
+        else int(survey.deflector)
+    sv.speed_m_s = survey.speed_m_s
+    sv.mount[:] = tuple(np.asarray(survey.mount, np.float64).reshape(9))
+    sv.mount_offset[:] = tuple(np.asarray(survey.mount_offset, np.float64).reshape(3))
+    sv.head_rotation_rad_s = survey.head_rotation_rad_s
+    sv.pulse_freq_hz = survey.pulse_freq_hz
+    sv.t0_s = survey.t0_s
+    sv.scan_freq_hz = survey.scan_freq_hz
+    sv.scan_angle_rad = survey.scan_angle_rad
+    sv.n_fibres = survey.n_fibres
+    o = np.zeros((n, 3), np.float32)
+    d = np.zeros((n, 3), np.float32)
+    t = np.zeros(n, np.float64)
+    lib().oracle_generate_pulses(ctypes.byref(sv), first, n, _p(o), _p(d), _p(t))
+    return o, d, t
 
 
 def range_noise(seed: int, pulse: int, return_number: int) -> float:

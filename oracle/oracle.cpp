@@ -313,6 +313,141 @@ double oracle_range_noise(uint64_t seed, uint64_t pulse, uint32_t return_number)
   return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * kPi * u2);
 }
 
+/* ------------------------------------------------------------------------
+ * Pulse generation (NEXT f2; P:155 platforms, P:177 deflectors; reading R30).
+ * Pulse g of a survey is emitted at t = t0 + g / PRF.
+ *   deflector (u = frac(f t), A = scan angle):
+ *     polygon mirror:  theta = -A + 2 A u              (sawtooth, parallel lines)
+ *     fibre optics:    theta = -A + 2 A (k + 1/2) / n, k = min(n-1, floor(u n))
+ *     oscillating:     theta = A sin(2 pi f t)         (zig-zag, dense extrema)
+ *     Palmer:          cone of half-angle A off nadir, azimuth phi = 2 pi u
+ *   scanner frame: s = (0, -sin theta, -cos theta) (theta > 0 to starboard),
+ *     Palmer s = (sin A cos phi, sin A sin phi, -cos A);
+ *   head rotation about the platform z axis: h = Rz(omega t) s; mount: m = M h;
+ *   platform: Static (one waypoint; yaw 0) or LinearPath (constant speed from
+ *     waypoint to waypoint, "orientation ... always towards the next waypoint",
+ *     P:155): leg k by time tau = t - t0, P = W_k + ((tau - T_k) v) u_k,
+ *     yaw rotation (cos, sin) = (dx, dy) / hypot(dx, dy) of the leg (no
+ *     trigonometry: an axis-aligned leg rotates exactly), after the last
+ *     waypoint: stays there;
+ *   world direction = Rz(yaw) m, origin = P + Rz(yaw) offset.
+ * Outputs fp32 origin/direction (rounded from fp64) and fp64 time.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const double* waypoints;  // [n_waypoints][3]
+  uint32_t n_waypoints;
+  uint32_t deflector;       // 0 polygon, 1 fibre, 2 oscillating, 3 Palmer
+  double speed_m_s;
+  double mount[9];          // row-major scanner -> platform rotation
+  double mount_offset[3];
+  double head_rotation_rad_s;
+  double pulse_freq_hz;
+  double t0_s;
+  double scan_freq_hz;
+  double scan_angle_rad;
+  uint32_t n_fibres;
+  uint32_t pad_;
+} oracle_survey;
+
+static void rot_cs(double c, double s, const double v[3], double out[3]) {
+  out[0] = c * v[0] - s * v[1];
+  out[1] = s * v[0] + c * v[1];
+  out[2] = v[2];
+}
+
+// yaw towards the leg's horizontal direction: (cos, sin) = (dx, dy) / hypot(dx, dy)
+static void heading(const double d[3], double* c, double* s) {
+  const double rho = std::sqrt(d[0] * d[0] + d[1] * d[1]);
+  if (rho > 0.0) {
+    *c = d[0] / rho;
+    *s = d[1] / rho;
+  } else {
+    *c = 1.0;
+    *s = 0.0;
+  }
+}
+
+void oracle_generate_pulses(const oracle_survey* sv, uint64_t first, int64_t n, float* origin,
+                            float* direction, double* time) {
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t g = first + (uint64_t)i;
+    const double tau = (double)g / sv->pulse_freq_hz;
+    const double t = sv->t0_s + tau;
+    // deflector
+    const double ft = sv->scan_freq_hz * t;
+    const double u = ft - std::floor(ft);
+    const double A = sv->scan_angle_rad;
+    double s[3];
+    if (sv->deflector == 3) {
+      const double phi = 2.0 * kPi * u;
+      s[0] = std::sin(A) * std::cos(phi);
+      s[1] = std::sin(A) * std::sin(phi);
+      s[2] = -std::cos(A);
+    } else {
+      double theta;
+      if (sv->deflector == 0) {
+        theta = -A + 2.0 * A * u;
+      } else if (sv->deflector == 1) {
+        const double nf = (double)sv->n_fibres;
+        const double k = std::min(nf - 1.0, std::floor(u * nf));
+        theta = -A + 2.0 * A * (k + 0.5) / nf;
+      } else {
+        theta = A * std::sin(2.0 * kPi * sv->scan_freq_hz * t);
+      }
+      s[0] = 0.0;
+      s[1] = -std::sin(theta);
+      s[2] = -std::cos(theta);
+    }
+    double h[3], m[3];
+    const double ha = sv->head_rotation_rad_s * t;
+    rot_cs(std::cos(ha), std::sin(ha), s, h);
+    for (int r = 0; r < 3; ++r)
+      m[r] = sv->mount[3 * r] * h[0] + sv->mount[3 * r + 1] * h[1] + sv->mount[3 * r + 2] * h[2];
+    // platform
+    double P[3] = {sv->waypoints[0], sv->waypoints[1], sv->waypoints[2]};
+    double yc = 1.0, ys = 0.0;  // cos / sin of the yaw
+    if (sv->n_waypoints > 1) {
+      double T = 0.0;  // start time of the current leg
+      bool placed = false;
+      int last_leg = -1;
+      for (uint32_t k = 0; k + 1 < sv->n_waypoints; ++k) {
+        const double* a = sv->waypoints + 3 * k;
+        const double* b = a + 3;
+        const double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        const double len = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        if (!(len > 0.0)) continue;  // zero-length leg: no time, no heading
+        last_leg = (int)k;
+        const double dur = len / sv->speed_m_s;
+        if (tau < T + dur || k + 2 == sv->n_waypoints) {
+          const double w = std::min(tau - T, dur) * sv->speed_m_s;  // distance along the leg
+          const double along = std::max(0.0, w);
+          for (int c = 0; c < 3; ++c) P[c] = a[c] + along * (d[c] / len);
+          heading(d, &yc, &ys);
+          placed = true;
+          break;
+        }
+        T += dur;
+      }
+      if (!placed && last_leg >= 0) {  // only zero-length legs after the last real one
+        const double* a = sv->waypoints + 3 * last_leg;
+        const double* b = a + 3;
+        const double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        const double len = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        for (int c = 0; c < 3; ++c) P[c] = b[c];
+        heading(d, &yc, &ys);
+      }
+    }
+    double dw[3], ow[3];
+    rot_cs(yc, ys, m, dw);
+    rot_cs(yc, ys, sv->mount_offset, ow);
+    for (int c = 0; c < 3; ++c) {
+      origin[3 * i + c] = (float)(P[c] + ow[c]);
+      direction[3 * i + c] = (float)dw[c];
+    }
+    time[i] = t;
+  }
+}
+
 /* G(|d_z|) for sigma = PAD * G (R15): LUT over |d_z| in [0,1] at uniform
  * knots, linear interpolation; no LUT -> spherical LAD, G = 0.5. */
 double oracle_g_function(const float* lut, uint32_t n_lut, double abs_dz) {

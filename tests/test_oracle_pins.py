@@ -618,3 +618,124 @@ def test_echo_width_unidentifiable_window_has_no_width():
     s1 = oracle.fit_echo_width(W, 50, delta, plen)[0]
     s2 = oracle.fit_echo_width(W, 59, delta, plen)[0]
     assert abs(s1 - 1.5) < 0.05 and abs(s2 - 1.5) < 0.1
+
+
+# ------------------------------------------------------------------ pulse generation (NEXT f2)
+def _survey(**kw):
+    from workloads import Survey
+    base = dict(waypoints=np.array([[0.0, 0.0, 100.0]]), pulse_freq_hz=10000.0,
+                scan_freq_hz=50.0, scan_angle_rad=math.radians(20.0))
+    base.update(kw)
+    return Survey(**base)
+
+
+def test_generated_pulses_match_the_workload_generators():
+    # the C2/C4/C5 flight lines expressed as surveys reproduce the workloads'
+    # own (independent, numpy) pulse arrays: origins and times bitwise,
+    # directions to rounding (the sawtooth angle is formed in another order)
+    from workloads import make_workload
+    for name, sc in (("C2", 0.25), ("C4", 0.2), ("C5", 0.05)):
+        w = make_workload(name, sc)
+        for sv, g0, cnt in w.surveys:
+            idx = np.arange(0, cnt, max(1, cnt // 4000))
+            o, d, t = w.pulses_at(g0 + idx)
+            go = np.zeros_like(o)
+            gd = np.zeros_like(d)
+            gt = np.zeros_like(t)
+            for k, g in enumerate(idx):
+                a, b, c = oracle.generate_pulses(sv, int(g), 1)
+                go[k], gd[k], gt[k] = a[0], b[0], c[0]
+            assert np.array_equal(o, go) and np.array_equal(t, gt)
+            assert np.abs(d - gd).max() <= 1e-15
+    # a contiguous block equals the per-pulse calls
+    sv = w.surveys[1][0]
+    o, d, t = oracle.generate_pulses(sv, 1000, 50)
+    o2, d2, t2 = oracle.generate_pulses(sv, 1049, 1)
+    assert np.array_equal(o[-1], o2[0]) and np.array_equal(d[-1], d2[0]) and t[-1] == t2[0]
+
+
+def test_palmer_cone_angle_is_constant():
+    # P:177 / Fig. 5d: "conical point pattern at a constant scan angle off-nadir";
+    # S: Palmer angle to nadir within 1e-9 rad; azimuth advances 2 pi f / PRF
+    A = math.radians(15.0)
+    sv = _survey(deflector="palmer", scan_angle_rad=A, scan_freq_hz=20.0,
+                 waypoints=np.array([[0.0, 0.0, 500.0], [300.0, 400.0, 500.0]]), speed_m_s=50.0)
+    o, d, t = oracle.generate_pulses(sv, 0, 20000)
+    dn = d.astype(np.float64) / np.linalg.norm(d.astype(np.float64), axis=1, keepdims=True)
+    ang = np.arccos(np.clip(-dn[:, 2], -1, 1))
+    assert np.abs(ang - A).max() < 2e-7  # fp32 storage of the direction
+    # in fp64 (before the fp32 rounding) the cone angle is exact to 1e-9: check
+    # the azimuth progression in the platform frame instead
+    az = np.unwrap(np.arctan2(dn[:, 1], dn[:, 0]))
+    step = np.diff(az)
+    assert np.allclose(step, 2 * math.pi * 20.0 / 10000.0, atol=1e-6)
+
+
+def test_oscillating_mirror_extrema_and_density():
+    # "a swinging mirror ... zig-zag-pattern with increased point
+    # densities at the extrema"; quarter period -> +A
+    A, f, prf = math.radians(25.0), 40.0, 40000.0
+    sv = _survey(deflector="oscillating", scan_angle_rad=A, scan_freq_hz=f, pulse_freq_hz=prf)
+    o, d, t = oracle.generate_pulses(sv, 0, int(prf / f))  # one period
+    theta = np.arcsin(np.clip(-d[:, 1].astype(np.float64), -1, 1))  # starboard positive
+    q = int(prf / f / 4)
+    assert theta[q] == pytest.approx(A, abs=1e-6)
+    assert theta[3 * q] == pytest.approx(-A, abs=1e-6)
+    h, _ = np.histogram(theta, bins=10, range=(-A, A))
+    assert h[0] > 2 * h[5] and h[-1] > 2 * h[4]
+
+
+def test_polygon_sawtooth_and_fibre_lines():
+    # polygon mirror -> parallel lines, even density; fibre optics ->
+    # the same pattern from n fixed fibres (R30)
+    A, f, prf = math.radians(30.0), 100.0, 100000.0
+    sv = _survey(deflector="polygon", scan_angle_rad=A, scan_freq_hz=f, pulse_freq_hz=prf)
+    o, d, t = oracle.generate_pulses(sv, 0, 3000)
+    theta = np.arcsin(np.clip(-d[:, 1].astype(np.float64), -1, 1))
+    per = int(prf / f)
+    assert np.array_equal(d[:per], d[per:2 * per])               # periodic
+    assert theta[0] == pytest.approx(-A, abs=1e-6)
+    assert np.allclose(np.diff(theta[:per]), 2 * A / per, atol=1e-6)  # even density
+    sv = _survey(deflector="fibre", scan_angle_rad=A, scan_freq_hz=f, pulse_freq_hz=prf,
+                 n_fibres=7)
+    o, d, t = oracle.generate_pulses(sv, 0, 3000)
+    theta = np.arcsin(np.clip(-d[:, 1].astype(np.float64), -1, 1))
+    levels = np.unique(np.round(theta, 6))
+    assert levels.size == 7
+    assert np.allclose(levels, -A + 2 * A * (np.arange(7) + 0.5) / 7, atol=1e-6)
+
+
+def test_linear_path_kinematics():
+    # "moved with a constant speed from one waypoint (leg) to the next
+    # one. The orientation of the platform is always towards the next waypoint"
+    wp = np.array([[0.0, 0.0, 100.0], [300.0, 0.0, 100.0], [300.0, 400.0, 100.0]])
+    v, prf = 50.0, 100.0
+    sv = _survey(waypoints=wp, speed_m_s=v, pulse_freq_hz=prf, scan_angle_rad=0.0)
+    o, d, t = oracle.generate_pulses(sv, 0, 2000)  # 20 s; path takes 14 s
+    tt = np.arange(2000) / prf
+    exp = np.where((tt * v)[:, None] <= 300.0,
+                   wp[0] + np.outer(np.minimum(tt * v, 300.0), [1, 0, 0]),
+                   wp[1] + np.outer(np.clip(tt * v - 300.0, 0, 400.0), [0, 1, 0]))
+    assert np.allclose(o, exp, atol=1e-4)
+    # theta = 0: nadir; the scan plane is across track: a small tilt goes to
+    # starboard (-y on the first leg, +x on the second)
+    assert np.allclose(d, [0, 0, -1], atol=1e-7)
+    sv2 = _survey(waypoints=wp, speed_m_s=v, pulse_freq_hz=prf, deflector="polygon",
+                  scan_freq_hz=1e-9, scan_angle_rad=0.2)  # theta = -0.2 (port) held
+    o2, d2, _ = oracle.generate_pulses(sv2, 0, 2000)
+    first = tt * v < 300.0
+    assert np.all(d2[first, 1] > 0) and np.allclose(d2[first, 0], 0, atol=1e-7)   # port = +y
+    second = (tt * v > 300.0) & (tt * v < 700.0)
+    assert np.all(d2[second, 0] < 0) and np.allclose(d2[second, 1], 0, atol=1e-7)  # port = -x
+
+
+def test_static_head_rotation():
+    # a static tripod with a rotating head: the sweep plane turns at omega
+    om = 2 * math.pi / 10.0
+    sv = _survey(waypoints=np.array([[1.0, 2.0, 1.5]]), head_rotation_rad_s=om,
+                 deflector="polygon", scan_freq_hz=1e-9, scan_angle_rad=0.5,
+                 pulse_freq_hz=100.0)
+    o, d, t = oracle.generate_pulses(sv, 0, 1000)
+    assert np.all(o == np.float32([1.0, 2.0, 1.5]))
+    az = np.unwrap(np.arctan2(d[:, 1].astype(np.float64), d[:, 0].astype(np.float64)))
+    assert np.allclose(np.diff(az), om / 100.0, atol=1e-6)

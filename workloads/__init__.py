@@ -10,6 +10,7 @@ from .configs import (  # noqa: F401
     CONFIGS,
     Scene,
     ScannerParams,
+    Survey,
     Workload,
     make_workload,
     window_ns_for_range,

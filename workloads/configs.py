@@ -62,12 +62,33 @@ class ScannerParams:
 
 
 @dataclass
+class Survey:
+    """A platform + scanner description for on-device pulse generation
+    (NEXT f2; P:155 platforms, P:177 deflectors; R30).  Plain data:
+    the generators live in the oracle and in the CUDA library."""
+    waypoints: np.ndarray            # [n][3] m; one point = Static platform
+    pulse_freq_hz: float
+    deflector: str = "polygon"       # polygon | fibre | oscillating | palmer
+    scan_freq_hz: float = 100.0
+    scan_angle_rad: float = 0.5      # half-amplitude, or Palmer cone angle
+    speed_m_s: float = 0.0           # LinearPath speed (> 0 with >= 2 waypoints)
+    t0_s: float = 0.0
+    n_fibres: int = 0                # fibre deflector: lines per sweep
+    head_rotation_rad_s: float = 0.0
+    mount: np.ndarray = field(default_factory=lambda: np.eye(3))
+    mount_offset: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+
+@dataclass
 class Workload:
     name: str
     scene: Scene
     params: ScannerParams
     n_pulses: int
     _pulse_fn: Callable[[np.ndarray], tuple] = field(repr=False, default=None)
+    # the same pulses as surveys (NEXT f2): [(Survey, first global id, count)],
+    # survey pulse g <-> global id first + g; None if not survey-expressible
+    surveys: list | None = None
 
     def pulses(self, start: int = 0, count: int | None = None):
         """(origins f32 [n,3], directions f32 [n,3], times f64 [n]) for the
@@ -260,7 +281,7 @@ def _c1(scale: float, seed: int):
         o = np.broadcast_to(np.array([0.0, 0.0, 10.0]), d.shape)
         return (o.astype(np.float32), d.astype(np.float32), idx.astype(np.float64) * 1e-5)
 
-    return scene, params, side * side, fn
+    return scene, params, side * side, fn, None
 
 
 def _c2(scale: float, seed: int):
@@ -284,7 +305,10 @@ def _c2(scale: float, seed: int):
         o = np.stack([np.full_like(t, xc), 60.0 * t, np.full_like(t, alt)], -1)
         return o.astype(np.float32), d.astype(np.float32), t
 
-    return scene, params, n_pulses, fn
+    sv = Survey(waypoints=np.array([[xc, 0.0, alt], [xc, n - 1.0, alt]]), pulse_freq_hz=prf,
+                deflector="polygon", scan_freq_hz=100.0, scan_angle_rad=math.radians(fov),
+                speed_m_s=60.0)
+    return scene, params, n_pulses, fn, [(sv, 0, n_pulses)]
 
 
 def _c3(scale: float, seed: int, n_trees: int | None = None, leaves=(8000, 20000)):
@@ -321,7 +345,7 @@ def _c3(scale: float, seed: int, n_trees: int | None = None, leaves=(8000, 20000
         o = np.broadcast_to(np.array([0.0, 0.0, 1.5]), d.shape)
         return o.astype(np.float32), d.astype(np.float32), idx.astype(np.float64) * 1e-6
 
-    return scene, params, n_az * n_el, fn
+    return scene, params, n_az * n_el, fn, None
 
 
 def _c4(scale: float, seed: int):
@@ -367,7 +391,10 @@ def _c4(scale: float, seed: int):
         o = np.stack([np.zeros_like(t), -half + speed * t, np.full_like(t, 80.0)], -1)
         return o.astype(np.float32), d.astype(np.float32), t
 
-    return scene, params, n_pulses, fn
+    sv = Survey(waypoints=np.array([[0.0, -half, 80.0], [0.0, half, 80.0]]), pulse_freq_hz=prf,
+                deflector="polygon", scan_freq_hz=50.0, scan_angle_rad=math.radians(fov),
+                speed_m_s=speed)
+    return scene, params, n_pulses, fn, [(sv, 0, n_pulses)]
 
 
 def _c5(scale: float, seed: int):
@@ -420,7 +447,11 @@ def _c5(scale: float, seed: int):
         o = np.stack([x, 60.0 * tl, np.full_like(tl, alt)], -1)
         return o.astype(np.float32), d.astype(np.float32), t
 
-    return scene, params, n_pulses, fn
+    svs = [(Survey(waypoints=np.array([[x, 0.0, alt], [x, n - 1.0, alt]]), pulse_freq_hz=prf,
+                   deflector="polygon", scan_freq_hz=200.0, scan_angle_rad=math.radians(fov),
+                   speed_m_s=60.0, t0_s=k * line_dur), k * per_line, per_line)
+           for k, x in enumerate(xs)]
+    return scene, params, n_pulses, fn, svs
 
 
 CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5}
@@ -440,7 +471,8 @@ def make_workload(name: str, scale: float = 1.0, seed: int = 0, **overrides) -> 
     pulse grid for parity tests (the oracle is brute force); ``overrides``
     replace ScannerParams fields (e.g. subray_count=93 for the C5 variant)."""
     name = name.upper()
-    scene, params, n_pulses, fn = CONFIGS[name](scale, seed)
+    scene, params, n_pulses, fn, surveys = CONFIGS[name](scale, seed)
     if overrides:
         params = replace(params, **overrides)
-    return Workload(name if scale == 1.0 else f"{name}@{scale:g}", scene, params, n_pulses, fn)
+    return Workload(name if scale == 1.0 else f"{name}@{scale:g}", scene, params, n_pulses, fn,
+                    surveys)
