@@ -214,6 +214,12 @@ typedef struct {
   float* p_wf_compact;         /* [wf_compact_capacity] or NULL                     */
   uint64_t* p_wf_offset;       /* [n_pulses + 1] or NULL                            */
   uint64_t wf_compact_capacity;
+  /* Beam export of helios_simulate_survey ("the beam origin and the
+   * beam direction" of every beam): the generated pulses as simulated.
+   * Ignored by helios_simulate (the caller has its pulses).                 */
+  float* p_beam_origin;        /* [n_pulses][3] or NULL                             */
+  float* p_beam_direction;     /* [n_pulses][3] or NULL                             */
+  double* p_beam_time;         /* [n_pulses] or NULL                                */
 } helios_outputs;
 
 /* Optional per-call accounting.  Inputs: collect_counters.  Everything else
@@ -247,6 +253,60 @@ typedef struct {
 helios_status helios_simulate(helios_scene scene, const helios_scanner_params* params,
                               const helios_pulses* pulses, const helios_outputs* outputs,
                               helios_stream stream, helios_stats* stats);
+
+/* ------------------------------------------------------------------------
+ * On-device pulse generation (P:155 platforms, P:177 scan deflectors;
+ * reading R30 of DESIGN.md s.3).  Pulse g of a survey is emitted at
+ * t = t0_s + g / pulse_freq_hz.  Deflector angle with u = frac(f t),
+ * A = scan_angle_rad:
+ *   POLYGON      theta = -A + 2 A u                       (parallel lines)
+ *   FIBRE        theta = -A + 2 A (k + 1/2) / n_fibres, k = floor(u n_fibres)
+ *   OSCILLATING  theta = A sin(2 pi f t)                  (zig-zag)
+ *   PALMER       cone of half-angle A around nadir, azimuth 2 pi u
+ * Scanner-frame beam (0, -sin theta, -cos theta) (theta > 0 to starboard;
+ * Palmer (sin A cos phi, sin A sin phi, -cos A)), rotated by the head
+ * (Rz(head_rotation_rad_s t)), by the mount matrix, and by the platform yaw:
+ * Static (one waypoint, yaw 0) or LinearPath (constant speed along the
+ * waypoints, "orientation ... always towards the next waypoint"; at
+ * the last waypoint it stays).  Origin = platform position + rotated
+ * mount_offset.  All in fp64, stored as fp32 origin/direction + fp64 time.
+ * ---------------------------------------------------------------------- */
+typedef enum {
+  HELIOS_DEFLECTOR_POLYGON = 0,
+  HELIOS_DEFLECTOR_FIBRE = 1,
+  HELIOS_DEFLECTOR_OSCILLATING = 2,
+  HELIOS_DEFLECTOR_PALMER = 3
+} helios_deflector;
+
+typedef struct {
+  const double* h_waypoints;  /* [n_waypoints][3] (m), host memory, copied per call   */
+  uint32_t n_waypoints;       /* >= 1; 1 = Static platform                           */
+  uint32_t deflector;         /* helios_deflector                                    */
+  double speed_m_s;           /* LinearPath speed, > 0 when n_waypoints > 1          */
+  double mount[9];            /* scanner -> platform rotation, row-major (identity:
+                                 scan plane across track, nadir at theta = 0)        */
+  double mount_offset[3];     /* scanner position in the platform frame (m)          */
+  double head_rotation_rad_s; /* rotation of the scanner head about platform z       */
+  double pulse_freq_hz;       /* PRF, > 0                                            */
+  double t0_s;                /* emission time of survey pulse 0                     */
+  double scan_freq_hz;        /* sweeps (lines / cone turns / periods) per s, > 0    */
+  double scan_angle_rad;      /* A in [0, pi/2): half-amplitude or cone angle        */
+  uint32_t n_fibres;          /* FIBRE: lines per sweep, >= 1                        */
+  uint32_t reserved_;         /* must be 0                                           */
+} helios_survey;
+
+/* Simulate survey pulses first_pulse .. first_pulse + n_pulses - 1, generated
+ * on the device (no pulse arrays cross the boundary); pulse_index_base is the
+ * global id of the first one (Philox counter, output pulse id).  Outputs and
+ * errors as helios_simulate, plus INVALID_ARGUMENT for an invalid survey
+ * (NULL, no waypoint, non-finite values, speed <= 0 with > 1 waypoint,
+ * PRF / scan frequency <= 0, angle outside [0, pi/2), n_fibres == 0 with
+ * FIBRE, unknown deflector).  p_beam_* receive the generated pulses. */
+helios_status helios_simulate_survey(helios_scene scene, const helios_scanner_params* params,
+                                     const helios_survey* survey, uint64_t first_pulse,
+                                     uint64_t n_pulses, uint64_t pulse_index_base,
+                                     const helios_outputs* outputs, helios_stream stream,
+                                     helios_stats* stats);
 
 #ifdef __cplusplus
 }

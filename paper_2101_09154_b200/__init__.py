@@ -18,9 +18,11 @@ from .helios import (  # noqa: F401
     helios_scene_destroy,
     helios_scene_get_info,
     helios_simulate,
+    helios_simulate_survey,
     helios_version,
     helios_waveform_bins,
     lib,
     make_params,
     simulate,
+    simulate_survey,
 )

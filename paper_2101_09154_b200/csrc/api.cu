@@ -477,12 +477,54 @@ uint32_t helios_pulse_taps(const helios_scanner_params* params) {
   return validate_params(params, &d) == HELIOS_OK ? d.taps : 0;
 }
 
-helios_status helios_simulate(helios_scene sc, const helios_scanner_params* params,
-                              const helios_pulses* pulses, const helios_outputs* outputs,
-                              helios_stream stream, helios_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+helios_status validate_survey(const helios_survey* v) {
+  if (!v) return fail(HELIOS_ERR_INVALID_ARGUMENT, "survey is NULL");
+  if (!v->h_waypoints || v->n_waypoints < 1)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "survey needs >= 1 waypoint");
+  for (uint32_t i = 0; i < 3 * v->n_waypoints; ++i)
+    if (!std::isfinite(v->h_waypoints[i]))
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "survey waypoint %u is not finite", i / 3);
+  for (int i = 0; i < 9; ++i)
+    if (!std::isfinite(v->mount[i])) return fail(HELIOS_ERR_INVALID_ARGUMENT, "mount not finite");
+  for (int i = 0; i < 3; ++i)
+    if (!std::isfinite(v->mount_offset[i]))
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "mount_offset not finite");
+  if (v->n_waypoints > 1 && !(v->speed_m_s > 0.0 && std::isfinite(v->speed_m_s)))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "speed_m_s must be > 0 with > 1 waypoint");
+  if (!(v->pulse_freq_hz > 0.0) || !std::isfinite(v->pulse_freq_hz))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulse_freq_hz must be > 0");
+  if (!(v->scan_freq_hz > 0.0) || !std::isfinite(v->scan_freq_hz))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "scan_freq_hz must be > 0");
+  if (!(v->scan_angle_rad >= 0.0 && v->scan_angle_rad < 0.5 * kPi))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "scan_angle_rad must be in [0, pi/2)");
+  if (!std::isfinite(v->t0_s) || !std::isfinite(v->head_rotation_rad_s))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "t0_s / head_rotation_rad_s not finite");
+  if (v->deflector > HELIOS_DEFLECTOR_PALMER)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "unknown deflector %u", v->deflector);
+  if (v->deflector == HELIOS_DEFLECTOR_FIBRE && v->n_fibres == 0)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "n_fibres must be >= 1 with FIBRE");
+  if (v->reserved_ != 0) return fail(HELIOS_ERR_INVALID_ARGUMENT, "survey reserved_ must be 0");
+  return HELIOS_OK;
+}
+
+// helios_simulate (survey == nullptr: pulses from the caller's arrays) and
+// helios_simulate_survey (pulses generated on the device, survey pulse
+// first_pulse + i for pulse i of the call).
+helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params,
+                            const helios_pulses* pulses, const helios_survey* survey,
+                            uint64_t first_pulse, const helios_outputs* outputs,
+                            helios_stream stream, helios_stats* stats) {
   g_err.clear();
   if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
   if (!pulses || !outputs) return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs is NULL");
+  if (survey) {
+    const helios_status vs = validate_survey(survey);
+    if (vs != HELIOS_OK) return vs;
+  }
   Derived d;
   helios_status st = validate_params(params, &d);
   if (st != HELIOS_OK) return st;
@@ -494,7 +536,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   }
   const uint64_t n = pulses->n_pulses;
   if (n == 0) return HELIOS_OK;
-  if (!pulses->p_origin || !pulses->p_direction)
+  if (!survey && (!pulses->p_origin || !pulses->p_direction))
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_origin/p_direction is NULL");
   if (!outputs->p_n_returns || !outputs->p_returns || !outputs->p_wf_first_bin)
     return fail(HELIOS_ERR_INVALID_ARGUMENT,
@@ -524,20 +566,27 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     bool in;      // host->device before the chunk's kernels, else device->host after
     bool staged;  // host memory: two chunk buffers in scratch (double buffering)
     size_t off[2];
+    bool gen;     // pulse array written by the on-device generator (survey mode)
   };
+  const bool gen = survey != nullptr;
   Arr arrs[] = {
-      {pulses->p_origin, 12, true, false, {0, 0}},
-      {pulses->p_direction, 12, true, false, {0, 0}},
-      {pulses->p_time_s, 8, true, false, {0, 0}},
-      {outputs->p_n_returns, 1, false, false, {0, 0}},
-      {outputs->p_returns, sizeof(helios_return) * R, false, false, {0, 0}},
-      {outputs->p_wf_first_bin, 8, false, false, {0, 0}},
-      {outputs->p_waveform, 4ull * d.n_bins, false, false, {0, 0}},
-      {outputs->p_subray_hits, sizeof(helios_subray_hit) * N, false, false, {0, 0}},
+      {gen ? (const void*)outputs->p_beam_origin : pulses->p_origin, 12, !gen, false, {0, 0}, gen},
+      {gen ? (const void*)outputs->p_beam_direction : pulses->p_direction, 12, !gen, false,
+       {0, 0}, gen},
+      {gen ? (const void*)outputs->p_beam_time : pulses->p_time_s, 8, !gen, false, {0, 0}, gen},
+      {outputs->p_n_returns, 1, false, false, {0, 0}, false},
+      {outputs->p_returns, sizeof(helios_return) * R, false, false, {0, 0}, false},
+      {outputs->p_wf_first_bin, 8, false, false, {0, 0}, false},
+      {outputs->p_waveform, 4ull * d.n_bins, false, false, {0, 0}, false},
+      {outputs->p_subray_hits, sizeof(helios_subray_hit) * N, false, false, {0, 0}, false},
   };
   bool any_staged = compact_staged;
+  bool gen_staged = false;  // a generated array is copied out to host memory
   for (Arr& a : arrs)
-    if (a.user && !device_accessible(a.user)) a.staged = any_staged = true;
+    if (a.user && !device_accessible(a.user)) {
+      a.staged = any_staged = true;
+      gen_staged |= a.gen;
+    }
 
   // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
   const uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
@@ -557,8 +606,9 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   const size_t o_rec[2] = {carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0),
                            carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0)};
   for (Arr& a : arrs)
-    if (a.staged)
+    if (a.staged || (a.gen && !a.user))  // staged, or generated with no export
       for (int k = 0; k < 2; ++k) a.off[k] = carve(a.per_pulse * chunk);
+  const size_t o_wp = carve(gen ? sizeof(double) * 3 * survey->n_waypoints : 0);
   // compact output: per-pulse lengths, call-wide offsets, scan temp, staging
   size_t scan_bytes = 0;
   if (want_offs)
@@ -609,6 +659,28 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   if (e != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "helios_simulate (setup)");
+  }
+
+  SurveyArgs sa{};
+  if (gen && e == cudaSuccess) {
+    sa.waypoints = reinterpret_cast<const double*>(buf + o_wp);
+    e = cudaMemcpyAsync(buf + o_wp, survey->h_waypoints, sizeof(double) * 3 * survey->n_waypoints,
+                        cudaMemcpyHostToDevice, s);
+    sa.n_waypoints = survey->n_waypoints;
+    sa.deflector = survey->deflector;
+    sa.speed = survey->speed_m_s;
+    for (int i = 0; i < 9; ++i) sa.mount[i] = survey->mount[i];
+    for (int i = 0; i < 3; ++i) sa.offset[i] = survey->mount_offset[i];
+    sa.head = survey->head_rotation_rad_s;
+    sa.prf = survey->pulse_freq_hz;
+    sa.t0 = survey->t0_s;
+    sa.f = survey->scan_freq_hz;
+    sa.A = survey->scan_angle_rad;
+    sa.n_fibres = survey->n_fibres;
+    if (e != cudaSuccess) {
+      cleanup();
+      return cuda_fail(e, "helios_simulate_survey (waypoints)");
+    }
   }
 
   TraceArgs ta{};
@@ -699,6 +771,7 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, t_done[1], 0);
   }
   auto dev_ptr = [&](const Arr& a, int slot, uint64_t b) -> char* {
+    if (a.gen && !a.user) return buf + a.off[slot];
     if (!a.user) return nullptr;
     if (a.staged) return buf + a.off[slot];
     return (char*)a.user + a.per_pulse * b;
@@ -767,6 +840,16 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
     const int slot = (int)(c & 1);
     if (any_staged) e = cudaStreamWaitEvent(s, in_done[slot], 0);
     if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(s, w_done[slot], 0);
+    // generated pulses of this chunk (into the slot chunk c-2 used: its copy-out
+    // must be done when the export is host memory)
+    if (e == cudaSuccess && gen) {
+      if (gen_staged && c >= 2) e = cudaStreamWaitEvent(s, out_done[slot], 0);
+      if (e == cudaSuccess)
+        e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(arrs[0], slot, b),
+                            (float*)dev_ptr(arrs[1], slot, b), (double*)dev_ptr(arrs[2], slot, b),
+                            s);
+      ++launches;
+    }
     if (e != cudaSuccess) break;
     ta.origin = (const float*)dev_ptr(arrs[0], slot, b);
     ta.direction = (const float*)dev_ptr(arrs[1], slot, b);
@@ -923,4 +1006,28 @@ helios_status helios_simulate(helios_scene sc, const helios_scanner_params* para
   return HELIOS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+helios_status helios_simulate(helios_scene sc, const helios_scanner_params* params,
+                              const helios_pulses* pulses, const helios_outputs* outputs,
+                              helios_stream stream, helios_stats* stats) {
+  return simulate_impl(sc, params, pulses, nullptr, 0, outputs, stream, stats);
+}
+
+helios_status helios_simulate_survey(helios_scene sc, const helios_scanner_params* params,
+                                     const helios_survey* survey, uint64_t first_pulse,
+                                     uint64_t n_pulses, uint64_t pulse_index_base,
+                                     const helios_outputs* outputs, helios_stream stream,
+                                     helios_stats* stats) {
+  g_err.clear();
+  if (!survey) return fail(HELIOS_ERR_INVALID_ARGUMENT, "survey is NULL");
+  helios_pulses p{};
+  p.n_pulses = n_pulses;
+  p.pulse_index_base = pulse_index_base;
+  return simulate_impl(sc, params, &p, survey, first_pulse, outputs, stream, stats);
+}
+
 }  // extern "C"
+

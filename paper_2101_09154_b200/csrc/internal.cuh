@@ -135,6 +135,22 @@ struct WaveArgs {
   uint64_t pulse_base;           // global id of pulse 0 of this launch
 };
 
+// On-device pulse generation (survey.cu; NEXT f2, R30).  Plain values copied
+// from helios_survey; waypoints in device memory.
+struct SurveyArgs {
+  const double* waypoints;  // [n_waypoints][3] device
+  uint32_t n_waypoints;
+  uint32_t deflector;       // helios_deflector
+  double speed;
+  double mount[9];
+  double offset[3];
+  double head;              // head rotation rad/s
+  double prf, t0, f, A;
+  uint32_t n_fibres;
+};
+cudaError_t launch_generate(const SurveyArgs& a, uint64_t first, uint64_t n, float* origin,
+                            float* direction, double* time, cudaStream_t s);
+
 // launchers (trace.cu / waveform.cu)
 // mode: 0 per-ray binary, 1 packet binary, 2 packet 4-wide
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s);

@@ -31,7 +31,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OUT_OF_MEMORY", 3: "CUDA", 4: "NO
 
 EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helios_build_accel",
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
-            "helios_pulse_taps", "helios_simulate")
+            "helios_pulse_taps", "helios_simulate", "helios_simulate_survey")
 
 
 class HeliosError(RuntimeError):
@@ -66,7 +66,19 @@ class helios_pulses(ctypes.Structure):
 class helios_outputs(ctypes.Structure):
     _fields_ = [("p_n_returns", _vp), ("p_returns", _vp), ("p_wf_first_bin", _vp),
                 ("p_waveform", _vp), ("p_subray_hits", _vp), ("p_wf_compact", _vp),
-                ("p_wf_offset", _vp), ("wf_compact_capacity", _u64)]
+                ("p_wf_offset", _vp), ("wf_compact_capacity", _u64), ("p_beam_origin", _vp),
+                ("p_beam_direction", _vp), ("p_beam_time", _vp)]
+
+
+DEFLECTORS = {"polygon": 0, "fibre": 1, "oscillating": 2, "palmer": 3}
+
+
+class helios_survey(ctypes.Structure):
+    _fields_ = [("h_waypoints", _vp), ("n_waypoints", _u32), ("deflector", _u32),
+                ("speed_m_s", _d), ("mount", _d * 9), ("mount_offset", _d * 3),
+                ("head_rotation_rad_s", _d), ("pulse_freq_hz", _d), ("t0_s", _d),
+                ("scan_freq_hz", _d), ("scan_angle_rad", _d), ("n_fibres", _u32),
+                ("reserved_", _u32)]
 
 
 class helios_stats(ctypes.Structure):
@@ -115,6 +127,11 @@ def lib() -> ctypes.CDLL:
         L.helios_waveform_bins.argtypes = [ctypes.POINTER(helios_scanner_params)]
         L.helios_pulse_taps.restype = _u32
         L.helios_pulse_taps.argtypes = [ctypes.POINTER(helios_scanner_params)]
+        L.helios_simulate_survey.restype = ctypes.c_int
+        L.helios_simulate_survey.argtypes = [_vp, ctypes.POINTER(helios_scanner_params),
+                                             ctypes.POINTER(helios_survey), _u64, _u64, _u64,
+                                             ctypes.POINTER(helios_outputs), _vp,
+                                             ctypes.POINTER(helios_stats)]
         L.helios_simulate.restype = ctypes.c_int
         L.helios_simulate.argtypes = [_vp, ctypes.POINTER(helios_scanner_params),
                                       ctypes.POINTER(helios_pulses),
@@ -189,6 +206,16 @@ def helios_simulate(scene: int, params: helios_scanner_params, pulses: helios_pu
     _check(lib().helios_simulate(scene, ctypes.byref(params), ctypes.byref(pulses),
                                  ctypes.byref(outputs), _stream(stream),
                                  None if stats is None else ctypes.byref(stats)))
+
+
+def helios_simulate_survey(scene: int, params: helios_scanner_params, survey: helios_survey,
+                           first_pulse: int, n_pulses: int, pulse_index_base: int,
+                           outputs: helios_outputs, stream=None,
+                           stats: helios_stats | None = None):
+    _check(lib().helios_simulate_survey(scene, ctypes.byref(params), ctypes.byref(survey),
+                                        first_pulse, n_pulses, pulse_index_base,
+                                        ctypes.byref(outputs), _stream(stream),
+                                        None if stats is None else ctypes.byref(stats)))
 
 
 # ------------------------------------------------------------------ object layer
@@ -270,6 +297,9 @@ class Outputs:
     subray_hits: object    # uint8 [n, N, 16] (SUBRAY_DTYPE records) or None
     wf_compact: object = None  # float32 [capacity] packed support rows, or None
     wf_offset: object = None   # uint64 [n + 1] row offsets into wf_compact, or None
+    beam_origin: object = None     # float32 [n, 3] generated pulses (survey mode), or None
+    beam_direction: object = None  # float32 [n, 3]
+    beam_time: object = None       # float64 [n]
 
     def compact_row(self, p: int):
         """Support row p as a host numpy array: W[0 .. len_p) of the dense row."""
@@ -291,13 +321,16 @@ class Outputs:
         out["subray_hits"] = None if h is None else np.ascontiguousarray(h).view(
             SUBRAY_DTYPE)[..., 0]
         out["wf_offset"] = host(self.wf_offset)
+        out["beam_origin"] = host(self.beam_origin)
+        out["beam_direction"] = host(self.beam_direction)
+        out["beam_time"] = host(self.beam_time)
         out["wf_compact"] = host(self.wf_compact)
         return out
 
 
 def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=False,
                   pin_memory=False, compact: bool = False,
-                  compact_capacity: int | None = None) -> Outputs:
+                  compact_capacity: int | None = None, beams: bool = False) -> Outputs:
     """Caller-owned outputs.  compact=True adds the packed support rows
     (default capacity n * (L_p + 64) floats; helios_simulate reports
     HELIOS_ERR_CAPACITY with the exact need if that is too small)."""
@@ -320,6 +353,9 @@ def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=Fals
                                    n * (helios_pulse_taps(hp) + 64)), dtype=torch.float32, **kw)
         if compact else None,
         wf_offset=torch.empty(n + 1, dtype=torch.int64, **kw) if compact else None,
+        beam_origin=torch.empty((n, 3), dtype=torch.float32, **kw) if beams else None,
+        beam_direction=torch.empty((n, 3), dtype=torch.float32, **kw) if beams else None,
+        beam_time=torch.empty(n, dtype=torch.float64, **kw) if beams else None,
     )
 
 
@@ -349,21 +385,61 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     p.p_time_s = _ptr(time_s)
     p.n_pulses = n
     p.pulse_index_base = int(pulse_index_base)
-    o = helios_outputs()
-    o.p_n_returns = _ptr(outputs.n_returns)
-    o.p_returns = _ptr(outputs.returns)
-    o.p_wf_first_bin = _ptr(outputs.wf_first_bin)
-    o.p_waveform = _ptr(outputs.waveform)
-    o.p_subray_hits = _ptr(outputs.subray_hits)
-    o.p_wf_compact = _ptr(outputs.wf_compact)
-    o.p_wf_offset = _ptr(outputs.wf_offset)
-    o.wf_compact_capacity = 0 if outputs.wf_compact is None else int(outputs.wf_compact.numel()
-                                                                     if hasattr(outputs.wf_compact, "numel") else outputs.wf_compact.size)
+    o = _marshal_outputs(outputs)
     st = helios_stats() if (stats or counters) else None
     if st is not None:
         st.collect_counters = 1 if counters else 0
+    _run_with_capacity_retry(lambda: helios_simulate(scene.handle, hp, p, o, stream, st),
+                             outputs, o)
+    return outputs, st
+
+
+def make_survey(sv) -> tuple:
+    """helios_survey from a workloads.Survey-like object; returns (struct, keep-alive)."""
+    wp = np.ascontiguousarray(np.asarray(sv.waypoints, np.float64).reshape(-1, 3))
+    c = helios_survey()
+    c.h_waypoints = wp.ctypes.data
+    c.n_waypoints = wp.shape[0]
+    c.deflector = DEFLECTORS[sv.deflector] if isinstance(sv.deflector, str) else int(sv.deflector)
+    c.speed_m_s = float(sv.speed_m_s)
+    c.mount[:] = tuple(float(x) for x in np.asarray(sv.mount, np.float64).reshape(9))
+    c.mount_offset[:] = tuple(float(x) for x in np.asarray(sv.mount_offset, np.float64).reshape(3))
+    c.head_rotation_rad_s = float(sv.head_rotation_rad_s)
+    c.pulse_freq_hz = float(sv.pulse_freq_hz)
+    c.t0_s = float(sv.t0_s)
+    c.scan_freq_hz = float(sv.scan_freq_hz)
+    c.scan_angle_rad = float(sv.scan_angle_rad)
+    c.n_fibres = int(sv.n_fibres)
+    return c, wp
+
+
+def simulate_survey(scene: Scene, params, survey, first_pulse: int, n_pulses: int,
+                    pulse_index_base: int | None = None, outputs: Outputs | None = None,
+                    device="cuda", waveform: bool = True, subray_hits: bool = False,
+                    beams: bool = False, compact: bool = False, stream=None,
+                    stats: bool = False, counters: bool = False):
+    """helios_simulate_survey: pulses first_pulse .. +n_pulses of `survey`
+    generated on the device.  Returns (Outputs, helios_stats | None)."""
+    hp = params if isinstance(params, helios_scanner_params) else make_params(params)
+    if outputs is None:
+        outputs = alloc_outputs(n_pulses, hp, device, waveform, subray_hits, compact=compact,
+                                beams=beams)
+    sv, keep = make_survey(survey)
+    o = _marshal_outputs(outputs)
+    st = helios_stats() if (stats or counters) else None
+    if st is not None:
+        st.collect_counters = 1 if counters else 0
+    base = first_pulse if pulse_index_base is None else pulse_index_base
+    _run_with_capacity_retry(
+        lambda: helios_simulate_survey(scene.handle, hp, sv, first_pulse, n_pulses, base, o,
+                                       stream, st), outputs, o)
+    del keep
+    return outputs, st
+
+
+def _run_with_capacity_retry(call, outputs, o):
     try:
-        helios_simulate(scene.handle, hp, p, o, stream, st)
+        call()
     except HeliosError as err:
         if err.status != HELIOS_ERR_CAPACITY:
             raise
@@ -375,5 +451,22 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
                                          pin_memory=bool(getattr(old, "is_pinned", lambda: False)()))
         o.p_wf_compact = _ptr(outputs.wf_compact)
         o.wf_compact_capacity = need
-        helios_simulate(scene.handle, hp, p, o, stream, st)
-    return outputs, st
+        call()
+
+
+def _marshal_outputs(outputs: Outputs) -> helios_outputs:
+    o = helios_outputs()
+    o.p_n_returns = _ptr(outputs.n_returns)
+    o.p_returns = _ptr(outputs.returns)
+    o.p_wf_first_bin = _ptr(outputs.wf_first_bin)
+    o.p_waveform = _ptr(outputs.waveform)
+    o.p_subray_hits = _ptr(outputs.subray_hits)
+    o.p_wf_compact = _ptr(outputs.wf_compact)
+    o.p_wf_offset = _ptr(outputs.wf_offset)
+    wc = outputs.wf_compact
+    o.wf_compact_capacity = 0 if wc is None else int(wc.numel() if hasattr(wc, "numel")
+                                                     else wc.size)
+    o.p_beam_origin = _ptr(outputs.beam_origin)
+    o.p_beam_direction = _ptr(outputs.beam_direction)
+    o.p_beam_time = _ptr(outputs.beam_time)
+    return o

@@ -87,7 +87,8 @@ def test_struct_layouts_match_the_header(tmp_path):
     structs = {"helios_scene_desc": hh.helios_scene_desc,
                "helios_scanner_params": hh.helios_scanner_params,
                "helios_pulses": hh.helios_pulses, "helios_outputs": hh.helios_outputs,
-               "helios_stats": hh.helios_stats, "helios_scene_info": hh.helios_scene_info}
+               "helios_stats": hh.helios_stats, "helios_scene_info": hh.helios_scene_info,
+               "helios_survey": hh.helios_survey}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "helios.h"', "int main(){"]
     for name, cls in structs.items():
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
