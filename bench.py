@@ -332,6 +332,56 @@ def run_ours(args):
         e2e = run_e2e(True)
         e2e_dense = run_e2e(False)
 
+    # ---- on-device pulse generation (helios_simulate_survey, NEXT f2): the
+    # same pulses, generated from the workload's flight-line description, no
+    # pulse arrays at all; device-resident outputs (as `value`) and, end to
+    # end, host outputs with packed waveform rows (as `e2e`)
+    survey = None
+    if w.surveys and not args.no_survey:
+        def seg_of(start):
+            for sv, g0, cnt in w.surveys:
+                if g0 <= start < g0 + cnt:
+                    return sv, start - g0, min(B, g0 + cnt - start)
+            return None
+        segs = [seg_of(batches[i][0]) for i in range(steps_total)]
+        if all(sg is not None and sg[2] == B for sg in segs):
+            def sstep(i, outs):
+                sv, first, cnt = segs[i]
+                h.simulate_survey(scene, hp, sv, first, cnt, batches[i][0], outputs=outs)
+            for i in range(args.warmup):
+                sstep(i, out)
+            torch.cuda.synchronize()
+            barrier(world)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.warmup, steps_total):
+                sstep(i, out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+            survey = {"value": B * N * args.steps * world / (sms / 1e3) / 1e6, "unit": "Mrays/s",
+                      "ms_per_step": sms / args.steps,
+                      "pulses": "generated on the device from the flight lines (R30)"}
+            if not args.no_e2e:
+                hout = h.alloc_outputs(B, hp, device="cpu", waveform=False, pin_memory=True,
+                                       compact=True, compact_capacity=B * n_bins)
+                sstep(args.warmup, hout)
+                torch.cuda.synchronize()
+                barrier(world)
+                e0.record(stream)
+                for i in range(args.steps):
+                    sstep(args.warmup, hout)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
+                d2h = B * (1 + 8 + 32 * p.max_returns) + 8 * (B + 1) + 4 * int(hout.wf_offset[-1])
+                survey["e2e"] = {"value": B * N * args.steps * world / (ems / 1e3) / 1e6,
+                                 "unit": "Mrays/s", "h2d_bytes_per_step": 0,
+                                 "d2h_bytes_per_step": d2h,
+                                 "waveform_output": "packed support rows (lossless)"}
+                del hout
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -374,6 +424,7 @@ def run_ours(args):
             "clocks": clk,
             "e2e": e2e,
             "e2e_dense_rows": e2e_dense,
+            "device_pulse_generation": survey,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -393,6 +444,8 @@ def main():
     ap.add_argument("--config", default=os.environ.get("HELIOS_BENCH_CONFIG", "C5"))
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-survey", action="store_true",
+                    help="skip the on-device pulse generation measurement")
     ap.add_argument("--fit-echo-width", action="store_true",
                     help="optional Gaussian echo-width fit per return (P:280)")
     ap.add_argument("--range-noise", type=float, default=0.0,
