@@ -62,7 +62,8 @@ class OracleScene(ctypes.Structure):
     _fields_ = [
         ("tris", _vp), ("refl", _vp), ("n_tris", _u32), ("pad", _vp),
         ("n", _u32 * 3), ("origin", _d * 3), ("voxel_size", _d),
-        ("g_lut", _vp), ("n_lut", _u32),
+        ("g_lut", _vp), ("n_lut", _u32), ("voxel_mode", _u32), ("voxel_reflectance", _d),
+        ("pad_max", _d), ("scale_alpha", _d), ("scale_shift", _u32), ("pad2_", _u32),
     ]
 
 
@@ -105,6 +106,9 @@ def lib():
         L.oracle_voxel_segments.argtypes = [_vp, _vp, _vp, _vp, _d, _d, _vp, _vp, _vp, _i64]
         L.oracle_generate_pulses.restype = None
         L.oracle_generate_pulses.argtypes = [_vp, _u64, _i64, _vp, _vp, _vp]
+        L.oracle_voxel_cube.restype = None
+        L.oracle_voxel_cube.argtypes = [_vp, _vp, _d, _u32, _d, _u32, _d, _d, _u32, _u64, _vp,
+                                        _vp]
         L.oracle_range_noise.restype = _d
         L.oracle_range_noise.argtypes = [_u64, _u64, _u32]
         L.oracle_fit_echo_width.restype = _d
@@ -237,6 +241,7 @@ class OracleSurvey(ctypes.Structure):
 
 
 DEFLECTORS = {"polygon": 0, "fibre": 1, "oscillating": 2, "palmer": 3}
+VOXEL_MODES = {"transmissive": 0, "opaque": 1, "scaled": 2}
 
 
 def generate_pulses(survey, first: int, n: int):
@@ -263,6 +268,20 @@ def generate_pulses(survey, first: int, n: int):
     t = np.zeros(n, np.float64)
     lib().oracle_generate_pulses(ctypes.byref(sv), first, n, _p(o), _p(d), _p(t))
     return o, d, t
+
+
+def voxel_cube(n, origin, voxel_size, vid, pad, mode, pad_max=1.0, alpha=1.0, shift=0,
+               seed=0):
+    """(lo[3], side) of the opaque / scaled cube of voxel `vid` (P:231-239,
+    Eq. 5; R31)."""
+    nn = (_u32 * 3)(*n)
+    org = (_d * 3)(*origin)
+    lo = (_d * 3)()
+    side = _d()
+    lib().oracle_voxel_cube(nn, org, voxel_size, vid, pad,
+                            VOXEL_MODES[mode] if isinstance(mode, str) else mode, pad_max,
+                            alpha, shift, seed, lo, ctypes.byref(side))
+    return np.array(lo[:]), side.value
 
 
 def range_noise(seed: int, pulse: int, return_number: int) -> float:
@@ -340,6 +359,11 @@ def simulate(scene, params, origins, directions, times, pulse_ids,
         sc.voxel_size = float(scene.voxel_size)
     sc.g_lut = _p(lut)
     sc.n_lut = 0 if lut is None else lut.size
+    sc.voxel_mode = VOXEL_MODES[getattr(scene, "voxel_mode", "transmissive")]
+    sc.voxel_reflectance = float(getattr(scene, "voxel_reflectance", 0.5))
+    sc.pad_max = float(getattr(scene, "pad_max", 1.0))
+    sc.scale_alpha = float(getattr(scene, "scale_alpha", 1.0))
+    sc.scale_shift = int(getattr(scene, "scale_shift", 0))
     pr = OracleParams()
     for f, _ in OracleParams._fields_:
         if f != "pad_":

@@ -448,6 +448,66 @@ void oracle_generate_pulses(const oracle_survey* sv, uint64_t first, int64_t n, 
   }
 }
 
+/* Opaque voxels (reading R31).  Cube of voxel id: side a and
+ * minimum corner.  Opaque mode: the voxel itself.  Scaled mode (Eq. 5):
+ * a = a0 (min(1, PAD / PAD_max))^alpha centred in the voxel, optionally
+ * shifted by (u_k - 1/2)(a0 - a) per axis with u_k = (x_k >> 8) 2^-24 from
+ * Philox-4x32-10, key (seed_lo, seed_hi ^ 2) (stream tag 2), counter
+ * (voxel id, 0, 0, 0) -- "random but reproducible". */
+void oracle_voxel_cube(const uint32_t n[3], const double org[3], double a0, uint32_t id,
+                       double PAD, uint32_t mode, double pad_max, double alpha,
+                       uint32_t shift, uint64_t seed, double lo[3], double* side) {
+  const uint32_t ix = id % n[0], iy = (id / n[0]) % n[1], iz = id / (n[0] * n[1]);
+  const uint32_t idx[3] = {ix, iy, iz};
+  if (mode != 2) {
+    for (int a = 0; a < 3; ++a) lo[a] = org[a] + (double)idx[a] * a0;
+    *side = a0;
+    return;
+  }
+  const double a = a0 * std::pow(std::min(1.0, PAD / pad_max), alpha);
+  double sh[3] = {0.0, 0.0, 0.0};
+  if (shift) {
+    uint32_t ctr[4] = {id, 0u, 0u, 0u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32) ^ 2u};
+    uint32_t x[4];
+    oracle_philox4x32_10(ctr, key, x);
+    for (int k = 0; k < 3; ++k)
+      sh[k] = ((double)(x[k] >> 8) * (1.0 / 16777216.0) - 0.5) * (a0 - a);
+  }
+  for (int k = 0; k < 3; ++k) {
+    const double centre = org[k] + ((double)idx[k] + 0.5) * a0;
+    lo[k] = centre + sh[k] - 0.5 * a;
+  }
+  *side = a;
+}
+
+/* Ray vs axis-aligned cube [lo, lo + side]^3 (slab test, fp64): entry t and
+ * the entry axis (largest near-plane time, lowest axis on ties); returns
+ * false when the ray misses or the cube does not lie ahead (entry <= 0). */
+static bool ray_cube(const double o[3], const double d[3], const double lo[3], double side,
+                     double* t_enter, int* axis) {
+  double tn = -kInf, tf = kInf;
+  int ax = -1;
+  for (int a = 0; a < 3; ++a) {
+    const double l = lo[a], h = lo[a] + side;
+    if (d[a] == 0.0) {
+      if (o[a] < l || o[a] > h) return false;
+      continue;
+    }
+    double t0 = (l - o[a]) / d[a], t1 = (h - o[a]) / d[a];
+    if (t0 > t1) std::swap(t0, t1);
+    if (t0 > tn) {
+      tn = t0;
+      ax = a;
+    }
+    tf = std::min(tf, t1);
+  }
+  if (!(tn <= tf) || !(tn > 0.0) || ax < 0) return false;
+  *t_enter = tn;
+  *axis = ax;
+  return true;
+}
+
 /* G(|d_z|) for sigma = PAD * G (R15): LUT over |d_z| in [0,1] at uniform
  * knots, linear interpolation; no LUT -> spherical LAD, G = 0.5. */
 double oracle_g_function(const float* lut, uint32_t n_lut, double abs_dz) {
@@ -673,6 +733,14 @@ typedef struct {
   double voxel_size;
   const float* g_lut;
   uint32_t n_lut;
+  // voxel interpretation (NEXT f3, reading R31):
+  // 0 transmissive, 1 opaque cubes, 2 PAD-scaled opaque cubes (Eq. 5)
+  uint32_t voxel_mode;
+  double voxel_reflectance;  // rho of opaque / scaled cubes
+  double pad_max;            // PAD_max of Eq. 5
+  double scale_alpha;        // alpha of Eq. 5
+  uint32_t scale_shift;      // 1: reproducible random shift of each scaled cube
+  uint32_t pad2_;
 } oracle_scene;
 
 typedef struct {
@@ -739,7 +807,31 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
       double t_vox = 0.0, sigma_vox = 0.0;
       uint32_t vox_id = 0;
       double um = kInf;
-      if (sc->pad) {
+      if (sc->pad && sc->voxel_mode != 0) {
+        // O3': opaque / scaled cubes (Eq. 5; R31): the first cube
+        // the subray enters, before the triangle
+        double tmax = tid >= 0 ? t_tri : kInf;
+        int64_t cap = (int64_t)sc->n[0] + sc->n[1] + sc->n[2] + 2;
+        std::vector<double> ta(cap), tb(cap);
+        std::vector<uint32_t> vid(cap);
+        int64_t ns = oracle_voxel_segments(o, ds, sc->n, sc->origin, sc->voxel_size,
+                                           tmax, ta.data(), tb.data(), vid.data(), cap);
+        if (ns < 0) ns = -ns;
+        for (int64_t k = 0; k < ns; ++k) {
+          double PAD = sc->pad[vid[k]];
+          if (!(PAD > 0.0)) continue;
+          double lo[3], side, te;
+          int ax;
+          oracle_voxel_cube(sc->n, sc->origin, sc->voxel_size, vid[k], PAD, sc->voxel_mode,
+                            sc->pad_max, sc->scale_alpha, sc->scale_shift, pr->seed, lo, &side);
+          if (!ray_cube(o, ds, lo, side, &te, &ax) || !(te < tmax)) continue;
+          vox_hit = true;
+          t_vox = te;
+          sigma_vox = sc->voxel_reflectance * std::fabs(ds[ax]);  // R31: Lambertian face
+          vox_id = vid[k];
+          break;
+        }
+      } else if (sc->pad) {
         double tmax = tid >= 0 ? t_tri : kInf;
         int64_t cap = (int64_t)sc->n[0] + sc->n[1] + sc->n[2] + 2;
         std::vector<double> ta(cap), tb(cap);

@@ -739,3 +739,114 @@ def test_static_head_rotation():
     assert np.all(o == np.float32([1.0, 2.0, 1.5]))
     az = np.unwrap(np.arctan2(d[:, 1].astype(np.float64), d[:, 0].astype(np.float64)))
     assert np.allclose(np.diff(az), om / 100.0, atol=1e-6)
+
+
+# ------------------------------------------------------------------ opaque / scaled voxels (NEXT f3)
+def _cube_tris(lo, a):
+    """12 triangles of the axis-aligned cube [lo, lo + a]^3."""
+    x0, y0, z0 = lo
+    x1, y1, z1 = lo[0] + a, lo[1] + a, lo[2] + a
+    v = np.array([[x0, y0, z0], [x1, y0, z0], [x1, y1, z0], [x0, y1, z0],
+                  [x0, y0, z1], [x1, y0, z1], [x1, y1, z1], [x0, y1, z1]])
+    f = [(0, 1, 2), (0, 2, 3), (4, 6, 5), (4, 7, 6), (0, 5, 1), (0, 4, 5),
+         (3, 2, 6), (3, 6, 7), (0, 3, 7), (0, 7, 4), (1, 5, 6), (1, 6, 2)]
+    return v[np.array(f)]
+
+
+def _voxel_scene(mode, seed=3, **kw):
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = 9, 7, 5
+    pad = np.zeros((nz, ny, nx), np.float32)
+    occ = rng.random(pad.shape) < 0.12
+    pad[occ] = rng.uniform(0.05, 1.6, occ.sum()).astype(np.float32)
+    ground = np.array([[[-50, -50, -1.0], [50, -50, -1.0], [50, 50, -1.0]],
+                       [[-50, -50, -1.0], [50, 50, -1.0], [-50, 50, -1.0]]], np.float32)
+    sc = Scene(ground, np.full(2, 0.3, np.float32), pad, (-2.0, -1.5, 0.0), 0.5, None,
+               voxel_mode=mode, voxel_reflectance=0.75, **kw)
+    return sc, pad
+
+
+def test_voxel_cube_geometry_eq5():
+    # Eq. 5: a = a0 (PAD / PAD_max)^alpha; PAD >= PAD_max -> a0; alpha = 0 -> a0;
+    # opaque mode: the voxel itself; the shift keeps the cube inside its voxel,
+    # is reproducible, uniform, and absent when disabled (P:231-239; R31)
+    n, org, a0 = (9, 7, 5), (-2.0, -1.5, 0.0), 0.5
+    vid = 3 + 9 * (4 + 7 * 2)
+    lo, a = oracle.voxel_cube(n, org, a0, vid, 0.4, "opaque")
+    assert a == a0 and np.allclose(lo, [-2 + 3 * 0.5, -1.5 + 4 * 0.5, 2 * 0.5])
+    for pad, pm, al, want in ((0.25, 1.0, 0.5, 0.25), (0.4, 1.6, 1.0, 0.125), (2.0, 1.0, 0.7, 0.5),
+                              (0.3, 1.0, 0.0, 0.5)):
+        lo, a = oracle.voxel_cube(n, org, a0, vid, pad, "scaled", pm, al)
+        assert a == pytest.approx(want, rel=1e-15)
+        centre = np.array([-2 + 3.5 * 0.5, -1.5 + 4.5 * 0.5, 2.5 * 0.5])
+        assert np.allclose(lo + a / 2, centre, atol=1e-15)
+    sh = []
+    for v in range(2000):
+        lo, a = oracle.voxel_cube(n, org, a0, v, 0.09, "scaled", 1.0, 0.5, shift=1, seed=11)
+        lo2, _ = oracle.voxel_cube(n, org, a0, v, 0.09, "scaled", 1.0, 0.5, shift=1, seed=11)
+        assert np.array_equal(lo, lo2)
+        ix, iy, iz = v % 9, (v // 9) % 7, v // 63
+        vlo = np.array(org) + np.array([ix, iy, iz]) * a0
+        assert np.all(lo >= vlo - 1e-12) and np.all(lo + a <= vlo + a0 + 1e-12)
+        sh.append((lo + a / 2 - (vlo + a0 / 2)) / (a0 - a))
+    sh = np.array(sh)  # uniform on [-1/2, 1/2): mean 0, variance 1/12
+    assert np.abs(sh.mean(axis=0)).max() < 0.03 and np.abs(sh.var(axis=0) - 1 / 12).max() < 0.01
+
+
+@pytest.mark.parametrize("mode,kw", [("opaque", {}),
+                                     ("scaled", dict(pad_max=1.2, scale_alpha=0.6, scale_shift=1))])
+def test_opaque_voxels_equal_their_cube_meshes(mode, kw):
+    # the voxel path against the (pinned) triangle path: every occupied voxel's
+    # cube as 12 triangles of reflectance rho_v; same first event, range, and
+    # Lambertian amplitude (face normal = the entry axis)
+    sc, pad = _voxel_scene(mode, **kw)
+    seed = 5
+    tris, refl, owner = [sc.tri_xyz], [sc.tri_reflectance], []
+    for vid in np.nonzero(pad.reshape(-1) > 0)[0]:
+        lo, a = oracle.voxel_cube((9, 7, 5), sc.grid_origin, sc.voxel_size, int(vid),
+                                  float(pad.reshape(-1)[vid]), mode, kw.get("pad_max", 1.0),
+                                  kw.get("scale_alpha", 1.0), kw.get("scale_shift", 0), seed)
+        tris.append(_cube_tris(lo, a).astype(np.float32))
+        refl.append(np.full(12, 0.75, np.float32))
+        owner.append(np.full(12, vid))
+    mesh = Scene(np.concatenate(tris), np.concatenate(refl))
+    owner = np.concatenate([[-1, -1]] + owner)
+    rng = np.random.default_rng(2)
+    n = 400
+    o = np.column_stack([rng.uniform(-3, 3, n), rng.uniform(-3, 3, n), rng.uniform(4, 8, n)])
+    tgt = np.column_stack([rng.uniform(-2, 2.5, n), rng.uniform(-1.5, 2, n), rng.uniform(0, 2.5, n)])
+    d = tgt - o
+    p = ScannerParams(subray_count=7, divergence_rad=2e-3, seed=seed)
+    a = _run(sc, p, o, d)
+    b = _run(mesh, p, o, d)
+    vox = a.sub_prim >= 2
+    assert vox.sum() > 300 and (~vox & (a.sub_prim != 0xFFFFFFFF)).sum() > 100
+    # first event and range
+    hit_b = b.sub_prim != 0xFFFFFFFF
+    assert np.array_equal(a.sub_prim != 0xFFFFFFFF, hit_b)
+    tie = b.sub_ncand > 1  # cube edges / corners
+    same = ~tie & hit_b
+    va = np.where(vox, a.sub_prim.astype(np.int64) - 2, -1)      # voxel id, -1 = ground
+    vb = owner[np.where(hit_b, b.sub_prim, 0).astype(np.int64)]   # cube's voxel, -1 = ground
+    assert np.array_equal(va[same], vb[same])
+    # opaque cubes have fp32-exact corners; scaled ones are rounded to fp32 in the mesh
+    tol = 1e-12 if mode == "opaque" else 1e-6
+    assert np.allclose(a.sub_range[hit_b], b.sub_range[hit_b], rtol=0, atol=tol)
+    assert np.allclose(a.sub_amp[same], b.sub_amp[same], rtol=1e-9 if mode == "opaque" else 1e-5)
+
+
+def test_opaque_voxel_closed_form_and_inside_start():
+    # a nadir ray onto an occupied voxel's top face: R = h - z_top,
+    # A = K rho_v |d_z| I / R^4 (R31; Eq. 7 with the Lambertian face); a ray
+    # starting inside an occupied voxel does not hit it (t > 0, R21)
+    pad = np.zeros((1, 1, 1), np.float32)
+    pad[0, 0, 0] = 0.5
+    sc = Scene(np.zeros((0, 3, 3), np.float32), None, pad, (0.0, 0.0, 0.0), 2.0, None,
+               voxel_mode="opaque", voxel_reflectance=0.8)
+    p = ScannerParams(subray_count=1, divergence_rad=1e-3)
+    r = _run(sc, p, [1.0, 1.0, 10.0], [0, 0, -1])
+    assert r.sub_range[0, 0] == pytest.approx(8.0, rel=1e-15)
+    K = 1.0 / (4 * math.pi * 1e-6)
+    assert r.sub_amp[0, 0] == pytest.approx(K * 0.8 * 1.0 / 8.0 ** 4, rel=1e-12)
+    r = _run(sc, p, [1.0, 1.0, 1.0], [0, 0, -1])
+    assert r.sub_prim[0, 0] == 0xFFFFFFFF

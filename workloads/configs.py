@@ -34,6 +34,12 @@ class Scene:
     grid_origin: tuple = (0.0, 0.0, 0.0)
     voxel_size: float = 1.0
     g_lut: np.ndarray | None = None
+    # voxel interpretation (Eq. 5; R31)
+    voxel_mode: str = "transmissive"   # transmissive | opaque | scaled
+    voxel_reflectance: float = 0.5     # rho of opaque / scaled cubes
+    pad_max: float = 1.0               # PAD_max of Eq. 5
+    scale_alpha: float = 1.0           # alpha of Eq. 5
+    scale_shift: int = 0               # 1: reproducible random shift of scaled cubes
 
     @property
     def n_tris(self) -> int:
