@@ -85,14 +85,32 @@ typedef struct {
    * G = 0.5.  n_lut == 1 is invalid; n_lut <= 4096.                         */
   const float* h_g_lut;
   uint32_t n_lut;
+  /* How the grid is interpreted (reading R31):
+   *   HELIOS_VOXEL_TRANSMISSIVE  extinction + Beer-Lambert draws (default)
+   *   HELIOS_VOXEL_OPAQUE        every voxel with PAD > 0 is a solid cube
+   *   HELIOS_VOXEL_SCALED        solid cube of side a = a0 min(1, PAD/pad_max)^scale_alpha
+   *                              (Eq. 5) centred in its voxel, optionally shifted
+   *                              by a reproducible random offset (scale_shift = 1)
+   * Opaque / scaled cubes return at their entry point with sigma_eff =
+   * voxel_reflectance |cos| of the entry face (Lambertian).                  */
+  uint32_t voxel_mode;
+  float voxel_reflectance;  /* [0, 1] (opaque / scaled)                            */
+  double pad_max;           /* > 0 (scaled)                                        */
+  double scale_alpha;       /* >= 0 (scaled)                                       */
+  uint32_t scale_shift;     /* 0 or 1 (scaled)                                     */
+  uint32_t reserved_;       /* must be 0                                           */
 } helios_scene_desc;
+
+enum { HELIOS_VOXEL_TRANSMISSIVE = 0, HELIOS_VOXEL_OPAQUE = 1, HELIOS_VOXEL_SCALED = 2 };
 
 /* Copy the scene into library-owned device memory (the caller may free its
  * arrays on return; the stream is synchronised).
  * Errors: INVALID_ARGUMENT (NULL desc/out, NULL triangles with n_tris > 0,
  * non-finite vertex, reflectance outside [0,1], PAD < 0 or non-finite,
  * voxel_size <= 0, n_tris + nx*ny*nz >= 2^32 - 1, n_lut == 1 or > 4096,
- * n_tris >= 2^28); EMPTY_SCENE (no triangles and no grid);
+ * n_tris >= 2^28, unknown voxel_mode, voxel_reflectance outside [0,1],
+ * scaled mode with pad_max <= 0 or scale_alpha < 0, scale_shift > 1,
+ * reserved_ != 0); EMPTY_SCENE (no triangles and no grid);
  * OUT_OF_MEMORY; CUDA. */
 helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream stream,
                                   helios_scene* out);

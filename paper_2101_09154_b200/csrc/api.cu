@@ -31,6 +31,9 @@ struct helios_scene_s {
   double vs = 0;
   float* d_lut = nullptr;
   uint32_t n_lut = 0;
+  uint32_t voxel_mode = HELIOS_VOXEL_TRANSMISSIVE;  // R31
+  double voxel_refl = 0.5, pad_max = 1.0, scale_alpha = 1.0;
+  uint32_t scale_shift = 0;
   bool built = false;
   BuildResult bvh{};
   int device = 0;
@@ -355,6 +358,17 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
   }
   if (desc->n_tris == 0 && !grid)
     return fail(HELIOS_ERR_EMPTY_SCENE, "scene has no triangles and no voxel grid");
+  if (desc->voxel_mode > HELIOS_VOXEL_SCALED)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "unknown voxel_mode %u", desc->voxel_mode);
+  if (desc->reserved_ != 0) return fail(HELIOS_ERR_INVALID_ARGUMENT, "reserved_ must be 0");
+  if (desc->voxel_mode != HELIOS_VOXEL_TRANSMISSIVE &&
+      !(desc->voxel_reflectance >= 0.0f && desc->voxel_reflectance <= 1.0f))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "voxel_reflectance must be in [0, 1]");
+  if (desc->voxel_mode == HELIOS_VOXEL_SCALED &&
+      (!(desc->pad_max > 0.0) || !std::isfinite(desc->pad_max) || !(desc->scale_alpha >= 0.0) ||
+       !std::isfinite(desc->scale_alpha) || desc->scale_shift > 1))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                "scaled voxels need pad_max > 0, scale_alpha >= 0, scale_shift 0/1");
   if (desc->n_lut == 1 || desc->n_lut > (uint32_t)kMaxLut)
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "n_lut must be 0 or in [2, %d]", kMaxLut);
   if (desc->n_lut > 0 && !desc->h_g_lut)
@@ -392,6 +406,11 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
       sc->nz = desc->nz;
       for (int a = 0; a < 3; ++a) sc->origin[a] = desc->grid_origin[a];
       sc->vs = desc->voxel_size;
+      sc->voxel_mode = desc->voxel_mode;
+      sc->voxel_refl = desc->voxel_reflectance;
+      sc->pad_max = desc->pad_max;
+      sc->scale_alpha = desc->scale_alpha;
+      sc->scale_shift = desc->scale_shift;
       if ((e = copy_in(&sc->d_pad, desc->p_voxel_pad, nvox, s)) != cudaSuccess) break;
     }
     if (desc->n_lut) {
@@ -700,6 +719,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.vs = sc->vs;
   ta.g_lut = sc->d_lut;
   ta.n_lut = sc->n_lut;
+  ta.voxel_mode = sc->voxel_mode;
+  ta.voxel_refl = sc->voxel_refl;
+  ta.pad_max = sc->pad_max;
+  ta.scale_alpha = sc->scale_alpha;
+  ta.scale_shift = sc->scale_shift;
   ta.sub = d_tab;
   ta.N = N;
   ta.seed = params->seed;

@@ -77,6 +77,9 @@ struct TraceArgs {
   double gx0, gy0, gz0, vs;
   const float* g_lut;
   uint32_t n_lut;
+  uint32_t voxel_mode;   // HELIOS_VOXEL_* (R31)
+  double voxel_refl, pad_max, scale_alpha;
+  uint32_t scale_shift;
   const SubrayConst* sub;
   uint32_t N;            // subrays per pulse
   const float* origin;   // [n][3]

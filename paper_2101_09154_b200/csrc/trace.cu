@@ -158,6 +158,68 @@ __device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, dou
   return __ddiv_rn(__dsub_rn(__dadd_rn(org, __dmul_rn((double)k, vs)), o), d);
 }
 
+// Opaque / scaled voxel cube (Eq. 5; R31): minimum corner and side
+// of voxel (ix, iy, iz), the oracle's operation order.
+__device__ __forceinline__ double voxel_cube(const TraceArgs& a, const int idx[3], uint32_t id,
+                                             float pad, double lo[3]) {
+  const double org[3] = {a.gx0, a.gy0, a.gz0};
+  if (a.voxel_mode != HELIOS_VOXEL_SCALED) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) lo[k] = __dadd_rn(org[k], __dmul_rn((double)idx[k], a.vs));
+    return a.vs;
+  }
+  const double side = __dmul_rn(a.vs, pow(fmin(1.0, __ddiv_rn((double)pad, a.pad_max)),
+                                          a.scale_alpha));
+  double sh[3] = {0.0, 0.0, 0.0};
+  if (a.scale_shift) {
+    // stream tag 2: key (seed_lo, seed_hi ^ 2), counter (voxel id, 0, 0, 0)
+    const uint4 x = philox4x32_10(make_uint4(id, 0u, 0u, 0u),
+                                  make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32) ^ 2u));
+    const uint32_t xs[3] = {x.x, x.y, x.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      sh[k] = __dmul_rn(__dsub_rn(__dmul_rn((double)(xs[k] >> 8), 1.0 / 16777216.0), 0.5),
+                        __dsub_rn(a.vs, side));
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double centre = __dadd_rn(org[k], __dmul_rn(__dadd_rn((double)idx[k], 0.5), a.vs));
+    lo[k] = __dsub_rn(__dadd_rn(centre, sh[k]), __dmul_rn(0.5, side));
+  }
+  return side;
+}
+
+// fp64 slab test of a cube: entry t (> 0) and entry axis (largest near-plane
+// time, lowest axis on ties) -- the oracle's ray_cube.
+__device__ __forceinline__ bool ray_cube(const double o[3], const double d[3], const double lo[3],
+                                         double side, double* t_enter, int* axis) {
+  double tn = -INFINITY, tf = INFINITY;
+  int ax = -1;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double l = lo[k], h = __dadd_rn(lo[k], side);
+    if (d[k] == 0.0) {
+      if (o[k] < l || o[k] > h) return false;
+      continue;
+    }
+    double t0 = __ddiv_rn(__dsub_rn(l, o[k]), d[k]), t1 = __ddiv_rn(__dsub_rn(h, o[k]), d[k]);
+    if (t0 > t1) {
+      const double tt = t0;
+      t0 = t1;
+      t1 = tt;
+    }
+    if (t0 > tn) {
+      tn = t0;
+      ax = k;
+    }
+    tf = fmin(tf, t1);
+  }
+  if (!(tn <= tf) || !(tn > 0.0) || ax < 0) return false;
+  *t_enter = tn;
+  *axis = ax;
+  return true;
+}
+
 // Per-ray traversal (one thread walks its own subray; "while-while", stack in
 // local memory).  Returns through t_best / best_id / best_k.
 template <bool INSTR>
@@ -445,7 +507,10 @@ __device__ __forceinline__ void traverse_packet4(const TraceArgs& a, unsigned m,
 #ifndef HELIOS_TRACE_MIN_BLOCKS
 #define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
 #endif
-template <bool INSTR, bool PACKET, bool WIDE>
+// GRID: 0 no voxel grid, 1 transmissive voxels, 2 opaque / scaled cubes --
+// the A4 march is compiled in only where needed, so each scene kind keeps
+// the traversal's register budget
+template <bool INSTR, bool PACKET, bool WIDE, int GRID>
 __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t total = a.n_pulses * (uint64_t)a.N;
@@ -522,7 +587,7 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   bool vox_hit = false;
   double t_vox = 0.0, sigma_vox = 0.0;
   uint32_t vox_id = 0;
-  if (a.pad != nullptr) {
+  if (GRID != 0 && a.pad != nullptr) {
     const double org[3] = {a.gx0, a.gy0, a.gz0};
     const uint32_t nn[3] = {a.nx, a.ny, a.nz};
     const double o3[3] = {O.x, O.y, O.z}, d3v[3] = {D.x, D.y, D.z};
@@ -547,7 +612,7 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
     if (inside && t_in < t_out) {
       // G(|d_z|) (R15)
       double G = 0.5;
-      if (a.g_lut != nullptr) {
+      if (GRID == 1 && a.g_lut != nullptr) {
         const double x = fabs(D.z) * (double)(a.n_lut - 1);
         int64_t k = (int64_t)floor(x);
         k = k < 0 ? 0 : (k > (int64_t)a.n_lut - 2 ? (int64_t)a.n_lut - 2 : k);
@@ -578,7 +643,21 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         if (L > 0.0) {
           const uint32_t id = (uint32_t)idx[0] + a.nx * ((uint32_t)idx[1] + a.ny * (uint32_t)idx[2]);
           const float pad = __ldg(a.pad + id);
-          if (pad > 0.0f) {
+          if (GRID == 2 && pad > 0.0f) {
+            // opaque / scaled cube (R31): the first one entered ahead of the triangle
+            double lo[3], te;
+            int eax;
+            const double side = voxel_cube(a, idx, id, pad, lo);
+            const double t_lim = (best_id != 0xFFFFFFFFu) ? t_best : INFINITY;
+            if (ray_cube(o3, d3v, lo, side, &te, &eax) && te < t_lim) {
+              vox_hit = true;
+              t_vox = te;
+              sigma_vox = __dmul_rn(a.voxel_refl, fabs(d3v[eax]));  // Lambertian face
+              vox_id = id;
+              if (INSTR) ++c_voxret;
+              break;
+            }
+          } else if (GRID == 1 && pad > 0.0f) {
             const double sigma = (double)pad * G;  // Eq. 4 via the G LUT
             const double u = transmission_u(a.seed, a.pulse_base + p, s, id);
             if (!(u < exp(-sigma * L))) {  // s = -ln(u)/sigma <= L: echo (R17)
@@ -652,14 +731,23 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaSt
   const uint64_t blocks = (total + T - 1) / T;
   if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
+  const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
+#define HELIOS_TRACE_CASE(I, P, W)                                        \
+  if (grid == 1)                                                          \
+    k_trace<I, P, W, 1><<<g, T, 0, s>>>(a);                               \
+  else if (grid == 2)                                                     \
+    k_trace<I, P, W, 2><<<g, T, 0, s>>>(a);                               \
+  else                                                                    \
+    k_trace<I, P, W, 0><<<g, T, 0, s>>>(a);
   switch (mode * 2 + (instrumented ? 1 : 0)) {
-    case 0: k_trace<false, false, false><<<g, T, 0, s>>>(a); break;
-    case 1: k_trace<true, false, false><<<g, T, 0, s>>>(a); break;
-    case 2: k_trace<false, true, false><<<g, T, 0, s>>>(a); break;
-    case 3: k_trace<true, true, false><<<g, T, 0, s>>>(a); break;
-    case 4: k_trace<false, true, true><<<g, T, 0, s>>>(a); break;
-    default: k_trace<true, true, true><<<g, T, 0, s>>>(a); break;
+    case 0: HELIOS_TRACE_CASE(false, false, false) break;
+    case 1: HELIOS_TRACE_CASE(true, false, false) break;
+    case 2: HELIOS_TRACE_CASE(false, true, false) break;
+    case 3: HELIOS_TRACE_CASE(true, true, false) break;
+    case 4: HELIOS_TRACE_CASE(false, true, true) break;
+    default: HELIOS_TRACE_CASE(true, true, true) break;
   }
+#undef HELIOS_TRACE_CASE
   return cudaGetLastError();
 }
 

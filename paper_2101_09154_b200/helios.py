@@ -46,7 +46,12 @@ _d, _u32, _u64, _vp, _f = ctypes.c_double, ctypes.c_uint32, ctypes.c_uint64, cty
 class helios_scene_desc(ctypes.Structure):
     _fields_ = [("p_tri_xyz", _vp), ("p_tri_reflectance", _vp), ("n_tris", _u32),
                 ("p_voxel_pad", _vp), ("nx", _u32), ("ny", _u32), ("nz", _u32),
-                ("grid_origin", _d * 3), ("voxel_size", _d), ("h_g_lut", _vp), ("n_lut", _u32)]
+                ("grid_origin", _d * 3), ("voxel_size", _d), ("h_g_lut", _vp), ("n_lut", _u32),
+                ("voxel_mode", _u32), ("voxel_reflectance", _f), ("pad_max", _d),
+                ("scale_alpha", _d), ("scale_shift", _u32), ("reserved_", _u32)]
+
+
+VOXEL_MODES = {"transmissive": 0, "opaque": 1, "scaled": 2}
 
 
 class helios_scanner_params(ctypes.Structure):
@@ -231,7 +236,8 @@ class Scene:
     """A built scene.  Arrays may be torch tensors (CUDA or CPU) or numpy."""
 
     def __init__(self, tri_xyz, tri_reflectance=None, voxel_pad=None, grid_origin=(0, 0, 0),
-                 voxel_size=1.0, g_lut=None, stream=None, build=True):
+                 voxel_size=1.0, g_lut=None, stream=None, build=True, voxel_mode="transmissive",
+                 voxel_reflectance=0.5, pad_max=1.0, scale_alpha=1.0, scale_shift=0):
         keep = []
 
         def arr(x, dtype):
@@ -261,6 +267,11 @@ class Scene:
             d.voxel_size = float(voxel_size)
         d.h_g_lut = _ptr(lut)
         d.n_lut = 0 if lut is None else int(lut.size)
+        d.voxel_mode = VOXEL_MODES[voxel_mode] if isinstance(voxel_mode, str) else int(voxel_mode)
+        d.voxel_reflectance = float(voxel_reflectance)
+        d.pad_max = float(pad_max)
+        d.scale_alpha = float(scale_alpha)
+        d.scale_shift = int(scale_shift)
         self.n_tris = d.n_tris
         self.handle = helios_scene_create(d, stream)
         if build:
@@ -271,7 +282,11 @@ class Scene:
         import torch
         t = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(device)
         return cls(t(sc.tri_xyz), t(sc.tri_reflectance), t(sc.voxel_pad), sc.grid_origin,
-                   sc.voxel_size, sc.g_lut, stream=stream)
+                   sc.voxel_size, sc.g_lut, stream=stream,
+                   voxel_mode=getattr(sc, "voxel_mode", "transmissive"),
+                   voxel_reflectance=getattr(sc, "voxel_reflectance", 0.5),
+                   pad_max=getattr(sc, "pad_max", 1.0), scale_alpha=getattr(sc, "scale_alpha", 1.0),
+                   scale_shift=getattr(sc, "scale_shift", 0))
 
     def info(self) -> helios_scene_info:
         return helios_scene_get_info(self.handle)

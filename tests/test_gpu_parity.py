@@ -129,3 +129,17 @@ def test_echo_width_host_staged_multi_chunk_matches_device():
     assert np.array_equal(a["returns"].view(np.uint8), b["returns"].view(np.uint8))
     used = np.arange(a["returns"].shape[1])[None, :] < a["n_returns"][:, None]
     assert np.isfinite(a["returns"]["echo_width_ns"][used]).mean() > 0.9
+
+
+@pytest.mark.parametrize("mode,kw", [("opaque", dict(voxel_reflectance=0.6)),
+                                     ("scaled", dict(voxel_reflectance=0.6, pad_max=0.8,
+                                                     scale_alpha=0.5, scale_shift=1)),
+                                     ("scaled", dict(voxel_reflectance=0.4, pad_max=0.5,
+                                                     scale_alpha=1.5, scale_shift=0))])
+def test_opaque_and_scaled_voxels(mode, kw):
+    # NEXT f3 (Eq. 5; R31): the C4 canopy as opaque / scaled cubes
+    from dataclasses import replace
+    w = workload("C4", 0.1)
+    w2 = replace(w, scene=replace(w.scene, voxel_mode=mode, **kw))
+    rep, hits = _parity(w2, 3000, 3000, params=replace(w.params, seed=9))
+    assert hits > 0.5
