@@ -21,17 +21,21 @@ def workload(name: str, scale: float = 1.0, **kw):
     return make_workload(name, scale, **kw)
 
 
-_scenes = {}
+_scenes = {}  # id(workload scene) -> (workload scene, built Scene); the key object is kept
+             # alive so its id cannot be reused by a later (different) scene
 
 
 def scene_for(w):
     import paper_2101_09154_b200 as h
     key = id(w.scene)
-    if key not in _scenes:
+    hit = _scenes.get(key)
+    if hit is None or hit[0] is not w.scene:
+        if hit is not None:
+            _scenes.pop(key)[1].destroy()
         if len(_scenes) >= 3:
-            _scenes.pop(next(iter(_scenes))).destroy()
-        _scenes[key] = h.Scene.from_workload_scene(w.scene)
-    return _scenes[key]
+            _scenes.pop(next(iter(_scenes)))[1].destroy()
+        _scenes[key] = (w.scene, h.Scene.from_workload_scene(w.scene))
+    return _scenes[key][1]
 
 
 def gpu_run(w, start: int, count: int, waveform=True, subray_hits=True, params=None,
