@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Mrays/s traced and pulses/s with full waveform on 1 B200; % of HBM roofline"
 DEFAULT_BATCH = {"C1": 10_000, "C2": 1_000_000, "C3": 1_000_000, "C4": 1_000_000,
-                 "C5": 1_000_000}
+                 "C5": 1_000_000, "C6": 1_000_000}
 
 
 def peaks():

@@ -308,7 +308,9 @@ typedef struct {
   double pulse_freq_hz;       /* PRF, > 0                                            */
   double t0_s;                /* emission time of survey pulse 0                     */
   double scan_freq_hz;        /* sweeps (lines / cone turns / periods) per s, > 0    */
-  double scan_angle_rad;      /* A in [0, pi/2): half-amplitude or cone angle        */
+  double scan_angle_rad;      /* A: half-amplitude in [0, pi) (a 330-degree line
+                                 scanner has A = 165 deg), Palmer cone angle in
+                                 [0, pi/2)                                          */
   uint32_t n_fibres;          /* FIBRE: lines per sweep, >= 1                        */
   uint32_t reserved_;         /* must be 0                                           */
 } helios_survey;
@@ -318,7 +320,7 @@ typedef struct {
  * global id of the first one (Philox counter, output pulse id).  Outputs and
  * errors as helios_simulate, plus INVALID_ARGUMENT for an invalid survey
  * (NULL, no waypoint, non-finite values, speed <= 0 with > 1 waypoint,
- * PRF / scan frequency <= 0, angle outside [0, pi/2), n_fibres == 0 with
+ * PRF / scan frequency <= 0, angle outside its range, n_fibres == 0 with
  * FIBRE, unknown deflector).  p_beam_* receive the generated pulses. */
 helios_status helios_simulate_survey(helios_scene scene, const helios_scanner_params* params,
                                      const helios_survey* survey, uint64_t first_pulse,

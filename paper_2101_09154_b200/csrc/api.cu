@@ -518,8 +518,10 @@ helios_status validate_survey(const helios_survey* v) {
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulse_freq_hz must be > 0");
   if (!(v->scan_freq_hz > 0.0) || !std::isfinite(v->scan_freq_hz))
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "scan_freq_hz must be > 0");
-  if (!(v->scan_angle_rad >= 0.0 && v->scan_angle_rad < 0.5 * kPi))
-    return fail(HELIOS_ERR_INVALID_ARGUMENT, "scan_angle_rad must be in [0, pi/2)");
+  const double amax = v->deflector == HELIOS_DEFLECTOR_PALMER ? 0.5 * kPi : kPi;
+  if (!(v->scan_angle_rad >= 0.0 && v->scan_angle_rad < amax))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                "scan_angle_rad must be in [0, pi) (Palmer: [0, pi/2))");
   if (!std::isfinite(v->t0_s) || !std::isfinite(v->head_rotation_rad_s))
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "t0_s / head_rotation_rad_s not finite");
   if (v->deflector > HELIOS_DEFLECTOR_PALMER)

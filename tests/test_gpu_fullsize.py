@@ -60,3 +60,8 @@ def test_c4_full_voxel_canopy():
 
 def test_c5_full_city_terrain():
     _full("C5", 50_000_000 - 400_000, 10)
+
+
+def test_c6_full_mls_street():
+    g, rep = _full("C6", 2_500_000, 2000)
+    assert (g["wf_first_bin"] >= 0).mean() > 0.5

@@ -63,6 +63,14 @@ def test_c5_city_terrain_reduced_hex91_and_paper93():
     _parity(w, 500, 700, params=p93)
 
 
+def test_c6_mls_street_reduced():
+    # Table 3 Scene 2 stand-in: car-mounted oblique 330-degree scanner between
+    # prisms / cylinders / pyramids; 0.25 ns bins x 100 (paper defaults)
+    w = workload("C6", 0.2)
+    rep, hits = _parity(w, 40000, 6000)
+    assert hits > 0.4
+
+
 def test_eq2_beam_width_and_g_lut():
     # Eq. 2 (beam waist > 0) and a non-trivial G LUT on the voxel canopy
     from dataclasses import replace

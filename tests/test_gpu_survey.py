@@ -136,7 +136,7 @@ def test_survey_host_outputs_multi_chunk_and_batch_split():
 def test_survey_validation():
     h = _h()
     w = workload("C3", 0.03)
-    bad = [dict(pulse_freq_hz=0.0), dict(scan_freq_hz=-1.0), dict(scan_angle_rad=2.0),
+    bad = [dict(pulse_freq_hz=0.0), dict(scan_freq_hz=-1.0), dict(scan_angle_rad=1.6),
            dict(deflector="fibre", n_fibres=0),
            dict(waypoints=np.array([[0, 0, 0], [1, 0, 0.0]]), speed_m_s=0.0),
            dict(waypoints=np.array([[0, 0, np.nan]]))]

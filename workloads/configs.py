@@ -460,7 +460,86 @@ def _c5(scale: float, seed: int):
     return scene, params, n_pulses, fn, svs
 
 
-CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5}
+def _prism(cx, cy, z0, h, r, sides, yaw, cap=True):
+    """Vertical prism over a regular `sides`-gon of circumradius r (walls, and
+    the roof as a triangle fan when cap)."""
+    a = yaw + 2 * np.pi * np.arange(sides) / sides
+    ring = np.stack([cx + r * np.cos(a), cy + r * np.sin(a)], -1)
+    out = []
+    for k in range(sides):
+        p0, p1 = ring[k], ring[(k + 1) % sides]
+        b0, b1 = [*p0, z0], [*p1, z0]
+        t0, t1 = [*p0, z0 + h], [*p1, z0 + h]
+        out += [[b0, b1, t1], [b0, t1, t0]]
+        if cap:
+            out.append([[cx, cy, z0 + h], t0, t1])
+    return np.array(out)
+
+
+def _pyramid(cx, cy, z0, h, half, yaw):
+    a = yaw + np.pi / 4 + np.pi / 2 * np.arange(4)
+    r = half * np.sqrt(2.0)
+    base = np.stack([cx + r * np.cos(a), cy + r * np.sin(a), np.full(4, z0)], -1)
+    apex = [cx, cy, z0 + h]
+    return np.array([[base[k], base[(k + 1) % 4], apex] for k in range(4)])
+
+
+def _c6(scale: float, seed: int):
+    """MLS stand-in for Table 3 Scene 2: a car driving 208 m at
+    20 m/s between downtown buildings modelled as prisms, cylinders and
+    pyramids; oblique-mounted 330-degree line scanner (VUX-1UAV-like: 550 kHz,
+    200 lines/s, 0.5 mrad); paper waveform defaults beamSampleQuality 3
+    (37 subrays), bin 0.25 ns, 100 bins."""
+    rng = _rng(seed, 6, 1)
+    length = 208.0
+    objs, refl = [], []
+    n_slots = max(2, int(round(15 * scale)))
+    for side in (-1.0, 1.0):
+        for row, (ylo, yhi) in enumerate(((12.0, 24.0), (28.0, 42.0))):
+            for k in range(n_slots):
+                cx = (k + 0.5) * length / n_slots + rng.uniform(-1.5, 1.5)
+                cy = side * rng.uniform(ylo + 5.0, yhi - 5.0)
+                kind = rng.integers(0, 3)
+                yaw = rng.uniform(0, np.pi / 2)
+                if kind == 0:    # box prism
+                    t = _prism(cx, cy, 0.0, rng.uniform(6.0, 40.0), rng.uniform(3.5, 6.5), 4, yaw)
+                elif kind == 1:  # cylinder (24-gon)
+                    t = _prism(cx, cy, 0.0, rng.uniform(5.0, 30.0), rng.uniform(3.0, 5.5), 24, yaw)
+                else:            # pyramid
+                    t = _pyramid(cx, cy, 0.0, rng.uniform(5.0, 20.0), rng.uniform(3.0, 6.0), yaw)
+                objs.append(t)
+                refl.append(np.full(len(t), rng.uniform(0.1, 0.6)))
+    ground = np.array([[[-50, -60, 0.0], [260, -60, 0.0], [260, 60, 0.0]],
+                       [[-50, -60, 0.0], [260, 60, 0.0], [-50, 60, 0.0]]])
+    tri = np.concatenate([ground] + objs).astype(np.float32)
+    rf = np.concatenate([np.full(2, 0.3)] + refl).astype(np.float32)
+    scene = Scene(tri, rf)
+    params = ScannerParams(divergence_rad=0.5e-3, subray_count=37, bin_width_ns=0.25,
+                           max_fullwave_range_ns=25.0, seed=seed)
+    speed, prf, f = 20.0, 550_000.0, 200.0
+    A = math.radians(165.0)                      # 330-degree field of view
+    yaw_m = math.radians(45.0)                   # oblique mount: scan plane turned 45 deg
+    mount = np.array([[math.cos(yaw_m), -math.sin(yaw_m), 0.0],
+                      [math.sin(yaw_m), math.cos(yaw_m), 0.0], [0.0, 0.0, 1.0]])
+    n_pulses = max(2000, int(round(length / speed * prf * scale)))
+    dur = n_pulses / prf
+
+    def fn(idx):
+        t = idx.astype(np.float64) / prf
+        u = np.mod(f * t, 1.0)
+        th = -A + 2.0 * A * u
+        s = np.stack([np.zeros_like(th), -np.sin(th), -np.cos(th)], -1)
+        d = s @ mount.T
+        o = np.stack([speed * t, np.zeros_like(t), np.full_like(t, 2.0)], -1)
+        return o.astype(np.float32), d.astype(np.float32), t
+
+    sv = Survey(waypoints=np.array([[0.0, 0.0, 2.0], [speed * dur, 0.0, 2.0]]), pulse_freq_hz=prf,
+                deflector="polygon", scan_freq_hz=f, scan_angle_rad=A, speed_m_s=speed,
+                mount=mount)
+    return scene, params, n_pulses, fn, [(sv, 0, n_pulses)]
+
+
+CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5, "C6": _c6}
 
 DESCRIPTIONS = {
     "C1": "tiny TLS plane: 2 tris, 10k pulses, 19 subrays, 0.3 mrad, 1 ns bins",
@@ -469,6 +548,8 @@ DESCRIPTIONS = {
     "C4": "transmissive voxel canopy 400x400x40 (6.4M voxels) + ground, 5M pulses, "
           "19 subrays, 0.5 ns bins",
     "C5": "ALS city+terrain (~49.8M tris), 100M pulses, 91 subrays (hex q=5), 0.5 mrad",
+    "C6": "MLS street of prisms / cylinders / pyramids (Table 3 Scene 2 stand-in), 5.72M "
+          "pulses, 37 subrays, 0.25 ns bins x 100, oblique 330-degree line scanner",
 }
 
 
