@@ -308,14 +308,12 @@ __device__ __forceinline__ void traverse_ray(const TraceArgs& a, const D3& O, co
 // tests both child boxes against its own ray and t_best; a child is visited
 // with the mask of the lanes that hit it (ballot), the far child is pushed
 // with its own mask.  Control flow is warp-uniform, the node load is one
-// broadcast per warp, and the stack of (node, mask) pairs lives in the warp's
-// slice of shared memory (one lane pushes, every lane reads the popped entry
-// as a broadcast; the 64-register budget leaves no room for it in registers).
+// broadcast per warp, and the stack of (node, mask) pairs is distributed over
+// the lanes' registers (entry i lives in lane i % 32), so no local memory.
 // Every lane visits a superset of the nodes its own per-ray traversal would
 // visit, so the result is identical.
 template <bool INSTR, bool FUSED>
-__device__ __forceinline__ void traverse_packet(const TraceArgs& a, int2* __restrict__ stk,
-                                                unsigned m, const D3& O,
+__device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, const D3& O,
                                                 const D3& D, const F3& O32, const F3& D32,
                                                 float dl1, float ix, float iy, float iz,
                                                 double& t_best, uint32_t& best_id,
@@ -324,6 +322,8 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, int2* __rest
                                                 unsigned long long& c_f64) {
   const unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  int32_t stA_r = 0, stB_r = 0;
+  unsigned stA_m = 0, stB_m = 0;
   int sp = 0;
   int32_t ref = a.root;
   // -(o / d) per axis for the fused slab form
@@ -353,10 +353,8 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, int2* __rest
       }
       if (sp == 0) break;
       --sp;
-      __syncwarp();
-      const int2 e = stk[sp];
-      ref = e.x;
-      m = (unsigned)e.y;
+      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
       continue;
     }
     const Node* nd = a.nodes + ref;
@@ -387,7 +385,15 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, int2* __rest
       const bool near0 = both ? (2 * __popc(pref1) <= __popc(both)) : (__popc(m0) >= __popc(m1));
       const int32_t far_r = near0 ? r1 : r0;
       const unsigned far_m = near0 ? m1 : m0;
-      if (lane == 0) stk[sp] = make_int2(far_r, (int)far_m);
+      if (lane == (sp & 31)) {
+        if (sp < 32) {
+          stA_r = far_r;
+          stA_m = far_m;
+        } else {
+          stB_r = far_r;
+          stB_m = far_m;
+        }
+      }
       ++sp;
       ref = near0 ? r0 : r1;
       m = near0 ? m0 : m1;
@@ -400,10 +406,8 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, int2* __rest
     } else {
       if (sp == 0) break;
       --sp;
-      __syncwarp();
-      const int2 e = stk[sp];
-      ref = e.x;
-      m = (unsigned)e.y;
+      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
     }
   }
 }
@@ -529,11 +533,6 @@ __device__ __forceinline__ void traverse_packet4(const TraceArgs& a, unsigned m,
   }
 }
 
-#ifndef HELIOS_FUSED_SLAB
-#define HELIOS_FUSED_SLAB 0  // both slab forms in one kernel cost registers (DESIGN.md s.7.1)
-#endif
-constexpr bool kFusedSlab = HELIOS_FUSED_SLAB != 0;
-
 #ifndef HELIOS_TRACE_MIN_BLOCKS
 #define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
 #endif
@@ -594,22 +593,17 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
     const F3 D32 = {(float)D.x, (float)D.y, (float)D.z};
     const float dl1 = l1(D32);
     if (PACKET) {
-      // per-warp traversal stack (4 warps per 128-thread block)
-      __shared__ int2 s_stack[4][kStackSize];
-      int2* stk = s_stack[threadIdx.x >> 5];
       const unsigned m = __ballot_sync(0xffffffffu, valid);
       if (m) {
         if (WIDE)
           traverse_packet4<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
                                   c_nodes, c_tris, c_f64);
-        else if (kFusedSlab &&
-                 __all_sync(0xffffffffu, !valid || fmaxf(fmaxf(fabsf(ox), fabsf(oy)),
+        else if (__all_sync(0xffffffffu, !valid || fmaxf(fmaxf(fabsf(ox), fabsf(oy)),
                                                           fabsf(oz)) <= a.o_limit))
-          traverse_packet<INSTR, true>(a, stk, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id,
+          traverse_packet<INSTR, true>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id,
                                        best_k, c_nodes, c_tris, c_f64);
         else
-          traverse_packet<INSTR, false>(a, stk, m, O, D, O32, D32, dl1, ix, iy, iz, t_best,
-                                        best_id,
+          traverse_packet<INSTR, false>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id,
                                         best_k, c_nodes, c_tris, c_f64);
       }
     } else {
