@@ -708,9 +708,6 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.tris = sc->bvh.tris;
   ta.nodes = sc->bvh.nodes;
   ta.root = sc->bvh.root;
-  ta.o_limit = sc->bvh.o_limit;
-  if (const char* v = getenv("HELIOS_FUSED_SLAB"))  // A/B switch (default on)
-    if (!atoi(v)) ta.o_limit = 0.0f;
   ta.nodes4 = sc->bvh.nodes4;
   ta.root4 = sc->bvh.root4;
   ta.n_tris = sc->n_tris;

@@ -69,7 +69,6 @@ struct TraceArgs {
   const TriRecord* tris;
   const Node* nodes;
   int32_t root;          // root node ref (internal index or leaf ref)
-  float o_limit;         // fused-slab fast path for |origin| <= o_limit (0: never)
   const Node4* nodes4;
   int32_t root4;
   uint32_t n_tris;
@@ -192,7 +191,6 @@ struct BuildResult {
   Node4* nodes4;     // device, 4-wide collapse (nullptr if not built)
   uint32_t n_nodes4;
   int32_t root4;
-  float o_limit;     // rays with max |origin coord| <= o_limit may use the fused slab test
 };
 cudaError_t build_lbvh(const float* d_tri_xyz, const float* d_refl, uint32_t n,
                        cudaStream_t s, BuildResult* out, char* err, size_t err_len);

@@ -18,9 +18,7 @@
 
 #include <vector>
 
-#include <cmath>
 #include <cstdio>
-#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -209,25 +207,6 @@ __global__ void k_refit(const float* __restrict__ xyz, const uint32_t* __restric
   }
 }
 
-// Node boxes are padded outward (directed rounding) by 1e-6 relative -- a ray
-// lying exactly on a face of a flat or axis-aligned box (zero direction
-// component) is never culled -- plus an ABSOLUTE pad P = 2^-21 R, R the
-// largest |coordinate| of the scene: it absorbs the u |o| absolute error of
-// the fused slab form fma(b, 1/d, -o/d) for ray origins with |o| <= 7.5 R
-// (trace.cu, DESIGN.md s.7.1).
-__device__ __forceinline__ float abs_pad(const float* __restrict__ root) {
-  float r = 0.0f;
-#pragma unroll
-  for (int k = 0; k < 6; ++k) r = fmaxf(r, fabsf(root[k]));
-  return r * 4.76837158203125e-7f;  // 2^-21
-}
-__device__ __forceinline__ float pad_lo(float q, float P) {
-  return __fsub_rd(q, __fadd_ru(fmaf(fabsf(q), 1e-6f, 1e-30f), P));
-}
-__device__ __forceinline__ float pad_hi(float q, float P) {
-  return __fadd_ru(q, __fadd_ru(fmaf(fabsf(q), 1e-6f, 1e-30f), P));
-}
-
 __device__ __forceinline__ int32_t make_ref(int c, const int* __restrict__ range) {
   if (c < 0) return leaf_ref((uint32_t)(~c), 1u);
   int first = range[2 * c], last = range[2 * c + 1];
@@ -238,20 +217,21 @@ __device__ __forceinline__ int32_t make_ref(int c, const int* __restrict__ range
 
 __global__ void k_layout(int n, const int* __restrict__ child, const int* __restrict__ range,
                          const float* __restrict__ leafbox, const float* __restrict__ nodebox,
-                         const float* __restrict__ rootbox, Node* __restrict__ nodes) {
+                         Node* __restrict__ nodes) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
   int c0 = child[2 * i], c1 = child[2 * i + 1];
   const float* q0 = c0 < 0 ? leafbox + 6ull * (~c0) : nodebox + 6ull * c0;
   const float* q1 = c1 < 0 ? leafbox + 6ull * (~c1) : nodebox + 6ull * c1;
+  // boxes padded outward (directed rounding): a ray lying exactly on a face of
+  // a flat or axis-aligned box (zero direction component) is never culled
   float b0[6], b1[6];
-  const float P = abs_pad(rootbox);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    b0[a] = pad_lo(q0[a], P);
-    b0[3 + a] = pad_hi(q0[3 + a], P);
-    b1[a] = pad_lo(q1[a], P);
-    b1[3 + a] = pad_hi(q1[3 + a], P);
+    b0[a] = __fsub_rd(q0[a], fmaf(fabsf(q0[a]), 1e-6f, 1e-30f));
+    b0[3 + a] = __fadd_ru(q0[3 + a], fmaf(fabsf(q0[3 + a]), 1e-6f, 1e-30f));
+    b1[a] = __fsub_rd(q1[a], fmaf(fabsf(q1[a]), 1e-6f, 1e-30f));
+    b1[3 + a] = __fadd_ru(q1[3 + a], fmaf(fabsf(q1[3 + a]), 1e-6f, 1e-30f));
   }
   Node nd;
   nd.xy0 = make_float4(b0[0], b0[3], b0[1], b0[4]);
@@ -443,7 +423,7 @@ __device__ __forceinline__ int32_t ploc_ref(int c, uint32_t n, const uint32_t* _
 __global__ void k_ploc_layout(uint32_t n, const int* __restrict__ child,
                               const uint32_t* __restrict__ size, const uint32_t* __restrict__ off,
                               const float* __restrict__ leafbox, const float* __restrict__ nodebox,
-                              const float* __restrict__ rootbox, Node* __restrict__ nodes) {
+                              Node* __restrict__ nodes) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n - 1) return;
   if (size[n + u] <= (uint32_t)kLeafMax) return;  // collapsed into its parent's leaf
@@ -451,13 +431,12 @@ __global__ void k_ploc_layout(uint32_t n, const int* __restrict__ child,
   const float* q0 = c0 < (int)n ? leafbox + 6ull * c0 : nodebox + 6ull * (c0 - n);
   const float* q1 = c1 < (int)n ? leafbox + 6ull * c1 : nodebox + 6ull * (c1 - n);
   float b0[6], b1[6];
-  const float P = abs_pad(rootbox);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    b0[a] = pad_lo(q0[a], P);
-    b0[3 + a] = pad_hi(q0[3 + a], P);
-    b1[a] = pad_lo(q1[a], P);
-    b1[3 + a] = pad_hi(q1[3 + a], P);
+    b0[a] = __fsub_rd(q0[a], fmaf(fabsf(q0[a]), 1e-6f, 1e-30f));
+    b0[3 + a] = __fadd_ru(q0[3 + a], fmaf(fabsf(q0[3 + a]), 1e-6f, 1e-30f));
+    b1[a] = __fsub_rd(q1[a], fmaf(fabsf(q1[a]), 1e-6f, 1e-30f));
+    b1[3 + a] = __fadd_ru(q1[3 + a], fmaf(fabsf(q1[3 + a]), 1e-6f, 1e-30f));
   }
   Node nd;
   nd.xy0 = make_float4(b0[0], b0[3], b0[1], b0[4]);
@@ -576,7 +555,6 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   out->nodes4 = nullptr;
   out->n_nodes4 = 0;
   out->root4 = kEmptyRef;
-  out->o_limit = 0.0f;
   if (n == 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -597,8 +575,6 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   unsigned init_bounds[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
   unsigned hdepth = 0;
   uint32_t* idx_s_final = nullptr;  // leaf order (PLOC), else the Morton order
-  const float* root_box = nullptr;  // device [6] scene bounds (absolute box padding)
-  float hroot[6] = {0, 0, 0, 0, 0, 0};
   // tuning knobs for measurements (DESIGN.md s.8): HELIOS_MORTON_BITS (1..21),
   // HELIOS_MORTON_ANISO=1 (per-axis normalisation)
   int bits = kMortonBits, isotropic = 1;
@@ -717,8 +693,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     }
     k_ploc_order<<<nb, T, 0, s>>>(idx_s, n, poff, porder, leafbox, xyz);
     CK(cudaGetLastError());
-    k_ploc_layout<<<ni, T, 0, s>>>(n, child, psize, poff, leafbox, nodebox, pbox, out->nodes);
-    root_box = pbox;  // the last cluster
+    k_ploc_layout<<<ni, T, 0, s>>>(n, child, psize, poff, leafbox, nodebox, out->nodes);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&hdepth, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     out->n_nodes = n - 1;
@@ -741,8 +716,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     k_refit<<<nb, T, 0, s>>>(xyz, idx_s, (int)n, child, parent_int, parent_leaf, leafbox, nodebox,
                              flags);
     CK(cudaGetLastError());
-    k_layout<<<ni, T, 0, s>>>((int)n, child, range, leafbox, nodebox, nodebox, out->nodes);
-    root_box = nodebox;  // node 0 is the root
+    k_layout<<<ni, T, 0, s>>>((int)n, child, range, leafbox, nodebox, out->nodes);
     CK(cudaGetLastError());
     k_depth<<<ni, T, 0, s>>>((int)n, range, parent_int, dmax);
     CK(cudaGetLastError());
@@ -786,16 +760,9 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   }
   k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s_final ? idx_s_final : idx_s, n, out->tris);
   CK(cudaGetLastError());
-  if (root_box) CK(cudaMemcpyAsync(hroot, root_box, sizeof(hroot), cudaMemcpyDeviceToHost, s));
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
   CK(cudaEventElapsedTime(&out->ms, e0, e1));
-  {
-    // origins with |o| <= 7.5 R may use the fused slab form (P = 2^-21 R >= 1.01 u |o|)
-    float R = 0.0f;
-    for (int k = 0; k < 6; ++k) R = std::max(R, std::fabs(hroot[k]));
-    out->o_limit = root_box ? 7.5f * R : 0.0f;
-  }
   if (n > (uint32_t)kLeafMax) out->max_depth = hdepth;
   if (out->max_depth > (uint32_t)kStackSize) {
     snprintf(err, err_len, "build_lbvh: tree depth %u exceeds the traversal stack (%d)",

@@ -77,25 +77,6 @@ __device__ __forceinline__ float box_enter(float lox, float hix, float loy, floa
   return (tmin <= tmax * kWiden) ? tmin : INFINITY;
 }
 
-// Fused slab form: t = fma(b, 1/d, -(o/d)) with o/d precomputed per ray -- one
-// FFMA per plane instead of FADD + FMUL.  Its error has, besides the relative
-// part covered by kBoxSlack, an ABSOLUTE part u |o / d| (the rounding of o/d),
-// i.e. u |o| along the axis in space; the build pads every box by
-// P = 2^-21 R >= 1.01 u |o| for |o| <= 7.5 R (lbvh.cu abs_pad), so a warp takes
-// this path only when all its origins satisfy |o| <= o_limit = 7.5 R.
-__device__ __forceinline__ float box_enter_fused(float lox, float hix, float loy, float hiy,
-                                                 float loz, float hiz, float ix, float iy,
-                                                 float iz, float nox, float noy, float noz,
-                                                 float tbest) {
-  const float tx0 = fmaf(lox, ix, nox), tx1 = fmaf(hix, ix, nox);
-  const float ty0 = fmaf(loy, iy, noy), ty1 = fmaf(hiy, iy, noy);
-  const float tz0 = fmaf(loz, iz, noz), tz1 = fmaf(hiz, iz, noz);
-  const float tmin = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
-  const float tmax = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tbest));
-  constexpr float kWiden = (1.0f + kBoxSlack) / (1.0f - kBoxSlack);
-  return (tmin <= tmax * kWiden) ? tmin : INFINITY;
-}
-
 // fp64 Moller-Trumbore (the oracle's definition and operation order, R21):
 // t or -1.  The degeneracy cut |det| <= 1e-12 |e1||e2| is evaluated squared
 // (no square roots); it differs from the oracle's form only for rays within
@@ -312,7 +293,7 @@ __device__ __forceinline__ void traverse_ray(const TraceArgs& a, const D3& O, co
 // the lanes' registers (entry i lives in lane i % 32), so no local memory.
 // Every lane visits a superset of the nodes its own per-ray traversal would
 // visit, so the result is identical.
-template <bool INSTR, bool FUSED>
+template <bool INSTR>
 __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, const D3& O,
                                                 const D3& D, const F3& O32, const F3& D32,
                                                 float dl1, float ix, float iy, float iz,
@@ -326,9 +307,6 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   unsigned stA_m = 0, stB_m = 0;
   int sp = 0;
   int32_t ref = a.root;
-  // -(o / d) per axis for the fused slab form
-  const float nox = FUSED ? -(O32.x * ix) : 0.0f, noy = FUSED ? -(O32.y * iy) : 0.0f,
-              noz = FUSED ? -(O32.z * iz) : 0.0f;
   for (;;) {
     const bool mine = (m >> lane) & 1u;
     if (ref_is_leaf(ref)) {
@@ -364,17 +342,10 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
     if (mine) {
       if (INSTR) ++c_nodes;
       const float tb = (float)t_best;
-      if (FUSED) {
-        t0 = box_enter_fused(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, ix, iy, iz, nox, noy, noz,
-                             tb);
-        t1 = box_enter_fused(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, ix, iy, iz, nox, noy, noz,
-                             tb);
-      } else {
-        t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy, iz,
-                       tb);
-        t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy, iz,
-                       tb);
-      }
+      t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy, iz,
+                     tb);
+      t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy, iz,
+                     tb);
     }
     const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
     const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
@@ -598,13 +569,9 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         if (WIDE)
           traverse_packet4<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
                                   c_nodes, c_tris, c_f64);
-        else if (__all_sync(0xffffffffu, !valid || fmaxf(fmaxf(fabsf(ox), fabsf(oy)),
-                                                          fabsf(oz)) <= a.o_limit))
-          traverse_packet<INSTR, true>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id,
-                                       best_k, c_nodes, c_tris, c_f64);
         else
-          traverse_packet<INSTR, false>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id,
-                                        best_k, c_nodes, c_tris, c_f64);
+          traverse_packet<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
+                                 c_nodes, c_tris, c_f64);
       }
     } else {
       traverse_ray<INSTR>(a, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k, c_nodes,
