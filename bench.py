@@ -225,7 +225,11 @@ def run_ours(args):
         o, d, t = w.pulses(start, cnt)
         to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
         batches.append((start, to(o), to(d), to(t)))
-    out = h.alloc_outputs(B, hp, device=dev, waveform=True)
+    # device outputs of the timed steps: dense waveform rows (default), the
+    # lossless packed support rows, or neither (binning still runs)
+    out = h.alloc_outputs(B, hp, device=dev, waveform=args.waveform == "dense",
+                          compact=args.waveform == "compact",
+                          compact_capacity=B * n_bins if args.waveform == "compact" else None)
     torch.cuda.synchronize()
 
     def step(i, st=False, counters=False):
@@ -406,6 +410,7 @@ def run_ours(args):
                        "bvh_nodes": info.n_nodes, "bvh_depth": info.max_depth,
                        "build_ms": round(info.build_ms, 2), "gen_s": round(t_gen, 1),
                        "fit_echo_width": int(args.fit_echo_width),
+                       "waveform_output": args.waveform,
                        "range_noise_sd_m": args.range_noise},
             "roofline": {"bound": "hbm", "kernel": "k_trace", "achieved": ach_trace,
                          "peak": peak, "unit": "GB/s", "frac": ach_trace / peak,
@@ -443,6 +448,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=os.environ.get("HELIOS_BENCH_CONFIG", "C5"))
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--waveform", default="dense", choices=["dense", "compact", "none"],
+                    help="waveform output of the device-resident steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-survey", action="store_true",
                     help="skip the on-device pulse generation measurement")

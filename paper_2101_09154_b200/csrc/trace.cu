@@ -27,6 +27,9 @@ constexpr float kBoxSlack = 1e-6f;  // >> 4 * 2^-24 relative error of an fp32 sl
 // lazy culling of popped stack entries compares the stored (already widened)
 // entry distance with t_best rounded to fp32, widened again
 constexpr float kCullSlack = 1.0f + 4.0f * kBoxSlack;
+#ifndef HELIOS_LAZY_CULL
+#define HELIOS_LAZY_CULL 0
+#endif
 
 // fp64 helpers with explicit round-to-nearest intrinsics: no FMA contraction,
 // so every expression below evaluates exactly like the oracle's (same
@@ -307,6 +310,26 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   unsigned stA_m = 0, stB_m = 0;
   int sp = 0;
   int32_t ref = a.root;
+#if HELIOS_LAZY_CULL
+  float tstk[kStackSize];  // this lane's entry distance into every pushed child
+#endif
+  // pop; with HELIOS_LAZY_CULL, lanes whose t_best is already nearer than
+  // their entry into the child leave its mask, and emptied entries are
+  // skipped without loading the node
+  auto pop = [&]() -> bool {
+    for (;;) {
+      if (sp == 0) return false;
+      --sp;
+      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+#if HELIOS_LAZY_CULL
+      m = __ballot_sync(kFull, ((m >> lane) & 1u) && !(tstk[sp] > (float)t_best * kCullSlack));
+      if (m) return true;
+#else
+      return true;
+#endif
+    }
+  };
   for (;;) {
     const bool mine = (m >> lane) & 1u;
     if (ref_is_leaf(ref)) {
@@ -329,10 +352,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
           }
         }
       }
-      if (sp == 0) break;
-      --sp;
-      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
-      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+      if (!pop()) break;
       continue;
     }
     const Node* nd = a.nodes + ref;
@@ -365,6 +385,9 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
           stB_m = far_m;
         }
       }
+#if HELIOS_LAZY_CULL
+      tstk[sp] = near0 ? t1 : t0;
+#endif
       ++sp;
       ref = near0 ? r0 : r1;
       m = near0 ? m0 : m1;
@@ -375,10 +398,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
       ref = r1;
       m = m1;
     } else {
-      if (sp == 0) break;
-      --sp;
-      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
-      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+      if (!pop()) break;
     }
   }
 }
@@ -517,8 +537,10 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   const bool in_range = gid < total;
   if (!PACKET && !in_range) return;
   const uint64_t g = in_range ? gid : 0;  // out-of-range lanes ride along (packet mode)
-  const uint64_t p = g / a.N;
-  const uint32_t s = (uint32_t)(g - p * a.N);
+  // one launch covers < 2^32 subrays (launch_trace checks): 32-bit division
+  const uint32_t g32 = (uint32_t)g;
+  const uint64_t p = g32 / a.N;
+  const uint32_t s = g32 - (uint32_t)p * a.N;
   unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;
 
   helios_subray_hit rec;
@@ -729,7 +751,7 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaSt
   if (total == 0) return cudaSuccess;
   const unsigned T = 128;
   const uint64_t blocks = (total + T - 1) / T;
-  if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
   const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
 #define HELIOS_TRACE_CASE(I, P, W)                                        \

@@ -325,12 +325,36 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
       W = (S <= (uint32_t)kWCap) ? Ws : Wg;
       __syncwarp();
       if (maxoff < kAggCap) {
-        // amplitude per offset group, each group summed in subray order
-        for (int o = lane; o <= maxoff; o += 32) {
+        // amplitude per offset group.  Few groups (G <= 16, the usual case):
+        // lane (o, c) sums group o over subray chunk c of C = 32 / G chunks,
+        // then lane o adds its chunks' partials in chunk order; else one lane
+        // per group over all subrays.  Either way a fixed order: deterministic.
+        const int G = maxoff + 1;
+        if (G <= 16) {
+          const int C = 32 / G, o = lane % G, c = lane / G;
           double acc = 0.0;
-          for (uint32_t s = 0; s < N; ++s)
-            if (off[s] == o) acc += (double)amp[s];
-          agg[o] = acc;
+          if (c < C) {
+            const uint32_t s0 = (uint32_t)((N * (uint32_t)c) / (uint32_t)C);
+            const uint32_t s1 = (uint32_t)((N * (uint32_t)(c + 1)) / (uint32_t)C);
+            for (uint32_t s = s0; s < s1; ++s)
+              if (off[s] == o) acc += (double)amp[s];
+            agg[c * G + o] = acc;  // C * G <= 32 <= kAggCap
+          }
+          __syncwarp();
+          if (lane < G) {
+            double sum = agg[lane];
+            for (int q = 1; q < C; ++q) sum += agg[q * G + lane];
+            acc = sum;
+          }
+          __syncwarp();
+          if (lane < G) agg[lane] = acc;
+        } else {
+          for (int o = lane; o <= maxoff; o += 32) {
+            double acc = 0.0;
+            for (uint32_t s = 0; s < N; ++s)
+              if (off[s] == o) acc += (double)amp[s];
+            agg[o] = acc;
+          }
         }
         __syncwarp();
         for (uint32_t k = lane; k < S; k += 32) {
