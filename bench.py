@@ -309,7 +309,9 @@ def run_ours(args):
             ho, hd, ht = (x.cpu().pin_memory() for x in (o, d, t))
             hout = h.alloc_outputs(B, hp, device="cpu", waveform=not compact, pin_memory=True,
                                    compact=compact,
-                                   compact_capacity=B * n_bins if compact else None)
+                                   compact_capacity=B * n_bins if compact else None,
+                                   packed_returns=compact, slots=not compact,
+                                   returns_capacity=B * p.max_returns if compact else None)
             h.simulate(scene, hp, ho, hd, ht, pulse_index_base=start, outputs=hout)
             torch.cuda.synchronize()
             barrier(world)
@@ -322,17 +324,18 @@ def run_ours(args):
             torch.cuda.synchronize()
             ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
             h2d = B * (12 + 12 + 8)
-            d2h = B * (1 + 8 + 32 * p.max_returns)
-            if compact:
-                d2h += 8 * (B + 1) + 4 * int(hout.wf_offset[-1])
+            d2h = B * (1 + 8)
+            if compact:  # packed returns + packed waveform rows, with their offsets
+                d2h += 16 * (B + 1) + 32 * int(hout.return_offset[-1]) + \
+                    4 * int(hout.wf_offset[-1])
             else:
-                d2h += 4 * n_bins * B
+                d2h += 32 * p.max_returns * B + 4 * n_bins * B
             del hout
             return {"value": B * N * args.steps * world / (ems / 1e3) / 1e6, "unit": "Mrays/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "pulses_per_s": B * args.steps * world / (ems / 1e3),
-                    "waveform_output": "packed support rows (lossless)" if compact
-                    else "dense rows"}
+                    "waveform_output": "packed support rows + packed returns (lossless)"
+                    if compact else "dense rows + fixed return slots"}
         e2e = run_e2e(True)
         e2e_dense = run_e2e(False)
 
@@ -369,7 +372,9 @@ def run_ours(args):
                       "pulses": "generated on the device from the flight lines (R30)"}
             if not args.no_e2e:
                 hout = h.alloc_outputs(B, hp, device="cpu", waveform=False, pin_memory=True,
-                                       compact=True, compact_capacity=B * n_bins)
+                                       compact=True, compact_capacity=B * n_bins,
+                                       packed_returns=True, slots=False,
+                                       returns_capacity=B * p.max_returns)
                 sstep(args.warmup, hout)
                 torch.cuda.synchronize()
                 barrier(world)
@@ -379,11 +384,13 @@ def run_ours(args):
                 e1.record(stream)
                 torch.cuda.synchronize()
                 ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
-                d2h = B * (1 + 8 + 32 * p.max_returns) + 8 * (B + 1) + 4 * int(hout.wf_offset[-1])
+                d2h = B * (1 + 8) + 16 * (B + 1) + 32 * int(hout.return_offset[-1]) + \
+                    4 * int(hout.wf_offset[-1])
                 survey["e2e"] = {"value": B * N * args.steps * world / (ems / 1e3) / 1e6,
                                  "unit": "Mrays/s", "h2d_bytes_per_step": 0,
                                  "d2h_bytes_per_step": d2h,
-                                 "waveform_output": "packed support rows (lossless)"}
+                                 "waveform_output": "packed support rows + packed returns "
+                                                    "(lossless)"}
                 del hout
 
     cpu = None

@@ -214,7 +214,8 @@ typedef struct {
 
 typedef struct {
   uint8_t* p_n_returns;        /* [n_pulses]                                        */
-  helios_return* p_returns;    /* [n_pulses][max_returns]; unused slots zeroed     */
+  helios_return* p_returns;    /* [n_pulses][max_returns]; unused slots zeroed;
+                                  may be NULL when p_returns_packed is given       */
   int64_t* p_wf_first_bin;     /* [n_pulses] absolute bin k0 of waveform[0]; -1 = no hit */
   float* p_waveform;           /* [n_pulses][n_bins] or NULL (binning still runs) */
   helios_subray_hit* p_subray_hits; /* [n_pulses][subray_count] or NULL              */
@@ -238,6 +239,15 @@ typedef struct {
   float* p_beam_origin;        /* [n_pulses][3] or NULL                             */
   float* p_beam_direction;     /* [n_pulses][3] or NULL                             */
   double* p_beam_time;         /* [n_pulses] or NULL                                */
+  /* Packed returns: the used return slots only, pulse after pulse (pulse p's
+   * returns are p_returns_packed[p_return_offset[p] .. p_return_offset[p+1]),
+   * p_return_offset[0] = 0, offsets relative to this call).  With packed
+   * returns p_returns may be NULL.  If p_return_offset[n_pulses] >
+   * returns_capacity the call returns HELIOS_ERR_CAPACITY (everything else
+   * complete; returns past the capacity not written).                       */
+  helios_return* p_returns_packed; /* [returns_capacity] or NULL                    */
+  uint64_t* p_return_offset;       /* [n_pulses + 1]; required with p_returns_packed */
+  uint64_t returns_capacity;
 } helios_outputs;
 
 /* Optional per-call accounting.  Inputs: collect_counters.  Everything else

@@ -48,7 +48,8 @@ struct helios_scene_s {
     cudaStream_t copy;  // non-blocking copy stream for host staging (lazy)
     cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
     cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
-    uint64_t* pinned;   // 4 pinned words: per chunk slot (first, last) row offset (lazy)
+    uint64_t* pinned;   // 8 pinned words: per chunk slot (first, last) offsets of the
+                        // packed waveform rows [0..3] and packed returns [4..7] (lazy)
   };
   std::mutex mu;
   std::vector<Slot> slots;
@@ -95,7 +96,7 @@ struct helios_scene_s {
       *fit = use->fit;
     }
     if (!use->pinned) {
-      cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * sizeof(uint64_t));
+      cudaError_t e = cudaMallocHost((void**)&use->pinned, 8 * sizeof(uint64_t));
       if (e != cudaSuccess) return e;
     }
     use->busy = true;
@@ -559,9 +560,12 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (n == 0) return HELIOS_OK;
   if (!survey && (!pulses->p_origin || !pulses->p_direction))
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_origin/p_direction is NULL");
-  if (!outputs->p_n_returns || !outputs->p_returns || !outputs->p_wf_first_bin)
+  if (!outputs->p_n_returns || !outputs->p_wf_first_bin ||
+      (!outputs->p_returns && !outputs->p_returns_packed))
     return fail(HELIOS_ERR_INVALID_ARGUMENT,
-                "p_n_returns/p_returns/p_wf_first_bin must not be NULL");
+                "p_n_returns/p_wf_first_bin and p_returns or p_returns_packed must not be NULL");
+  if (outputs->p_returns_packed && !outputs->p_return_offset)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_returns_packed needs p_return_offset");
   if (outputs->p_wf_compact && !outputs->p_wf_offset)
     return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_wf_compact needs p_wf_offset");
   const uint32_t N = params->subray_count;
@@ -569,6 +573,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const cudaStream_t s = (cudaStream_t)stream;
   const bool want_offs = outputs->p_wf_offset != nullptr;
   const bool compact_staged = outputs->p_wf_compact && !device_accessible(outputs->p_wf_compact);
+  const bool packed = outputs->p_returns_packed != nullptr;
+  const bool packed_staged = packed && !device_accessible(outputs->p_returns_packed);
 
   // ---- host tables
   const std::vector<SubrayConst> tab = subray_table(N, params->divergence_rad, d.pt);
@@ -587,7 +593,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     bool in;      // host->device before the chunk's kernels, else device->host after
     bool staged;  // host memory: two chunk buffers in scratch (double buffering)
     size_t off[2];
-    bool gen;     // pulse array written by the on-device generator (survey mode)
+    bool gen;     // pulse array written by the on-device generator (survey mode), or
+                  // any array the kernels need: internal slots when the user passes NULL
   };
   const bool gen = survey != nullptr;
   Arr arrs[] = {
@@ -596,12 +603,12 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
        {0, 0}, gen},
       {gen ? (const void*)outputs->p_beam_time : pulses->p_time_s, 8, !gen, false, {0, 0}, gen},
       {outputs->p_n_returns, 1, false, false, {0, 0}, false},
-      {outputs->p_returns, sizeof(helios_return) * R, false, false, {0, 0}, false},
+      {outputs->p_returns, sizeof(helios_return) * R, false, false, {0, 0}, packed},
       {outputs->p_wf_first_bin, 8, false, false, {0, 0}, false},
       {outputs->p_waveform, 4ull * d.n_bins, false, false, {0, 0}, false},
       {outputs->p_subray_hits, sizeof(helios_subray_hit) * N, false, false, {0, 0}, false},
   };
-  bool any_staged = compact_staged;
+  bool any_staged = compact_staged || packed_staged;
   bool gen_staged = false;  // a generated array is copied out to host memory
   for (Arr& a : arrs)
     if (a.user && !device_accessible(a.user)) {
@@ -650,6 +657,17 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const size_t o_fcnt = carve(fit ? 2 * sizeof(unsigned) : 0);
   const size_t o_cst[2] = {carve(compact_staged ? 4ull * d.n_bins * chunk : 0),
                            carve(compact_staged ? 4ull * d.n_bins * chunk : 0)};
+  // packed returns: lengths, call-wide offsets, scan temp (own: runs on K7's
+  // stream concurrently with the waveform scan), staging
+  const size_t o_rlen = carve(packed ? sizeof(uint64_t) * chunk : 0);
+  const size_t o_roffs = carve(packed ? sizeof(uint64_t) * (n + 1) : 0);
+  size_t rscan_bytes = 0;
+  if (packed)
+    cub::DeviceScan::InclusiveSum(nullptr, rscan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (int)chunk, s);
+  const size_t o_rscan = carve(packed ? rscan_bytes : 0);
+  const size_t o_rst[2] = {carve(packed_staged ? sizeof(helios_return) * R * chunk : 0),
+                           carve(packed_staged ? sizeof(helios_return) * R * chunk : 0)};
 
   char* buf = nullptr;
   cudaStream_t cs = nullptr, ws = nullptr, fs = nullptr;
@@ -677,6 +695,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   uint64_t* d_len = reinterpret_cast<uint64_t*>(buf + o_len);
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(buf + o_offs);
   if (e == cudaSuccess && want_offs) e = cudaMemsetAsync(d_offs, 0, sizeof(uint64_t), s);
+  uint64_t* d_rlen = reinterpret_cast<uint64_t*>(buf + o_rlen);
+  uint64_t* d_roffs = reinterpret_cast<uint64_t*>(buf + o_roffs);
+  if (e == cudaSuccess && packed) e = cudaMemsetAsync(d_roffs, 0, sizeof(uint64_t), s);
   if (e != cudaSuccess) {
     cleanup();
     return cuda_fail(e, "helios_simulate (setup)");
@@ -778,9 +799,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   cudaEvent_t in_done[2] = {}, t_done[2] = {}, w_done[2] = {}, out_done[2] = {};
   cudaEvent_t off_done[2] = {}, cd_done[2] = {};  // compact: offsets of chunk known / drained
   cudaEvent_t k7_done[2] = {};                     // fit: K7 of the chunk done, jobs listed
+  cudaEvent_t roff_done[2] = {}, rd_done[2] = {};  // packed returns: range known / drained
   for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess && fit) e = cudaEventCreateWithFlags(&k7_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess && packed_staged) {
+      e = cudaEventCreateWithFlags(&roff_done[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&rd_done[k], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess && compact_staged) {
       e = cudaEventCreateWithFlags(&off_done[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cd_done[k], cudaEventDisableTiming);
@@ -828,6 +854,21 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       r = cudaMemcpyAsync(outputs->p_wf_compact + first, buf + o_cst[sl],
                           sizeof(float) * (last - first), cudaMemcpyDeviceToHost, cs);
     if (r == cudaSuccess) r = cudaEventRecord(cd_done[sl], cs);
+    return r;
+  };
+
+  // staged packed returns of chunk c (same scheme as drain_compact)
+  const uint64_t rcap = outputs->returns_capacity;
+  auto drain_returns = [&](uint64_t c) -> cudaError_t {
+    const int sl = (int)(c & 1);
+    cudaError_t r = cudaEventSynchronize(roff_done[sl]);
+    if (r != cudaSuccess) return r;
+    const uint64_t first = pin[4 + 2 * sl], last = std::min(pin[4 + 2 * sl + 1], rcap);
+    r = cudaStreamWaitEvent(cs, w_done[sl], 0);
+    if (r == cudaSuccess && last > first)
+      r = cudaMemcpyAsync(outputs->p_returns_packed + first, buf + o_rst[sl],
+                          sizeof(helios_return) * (last - first), cudaMemcpyDeviceToHost, cs);
+    if (r == cudaSuccess) r = cudaEventRecord(rd_done[sl], cs);
     return r;
   };
 
@@ -932,6 +973,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       ++launches;
     }
     mark(ev_w, ws);
+    // the stream that finishes the chunk's returns: fits (own stream) or K7's
+    cudaStream_t post = ws;
     if (e == cudaSuccess && fit) {
       // echo-width fits on their own stream (their tail overlaps later chunks);
       // the chunk's outputs are complete once they are done
@@ -940,12 +983,31 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       if (e == cudaSuccess && f != ws) e = cudaStreamWaitEvent(f, k7_done[slot], 0);
       if (e == cudaSuccess) e = launch_fit(wa, f);
       ++launches;
-      if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], f);
-    } else if (e == cudaSuccess) {
-      e = cudaEventRecord(w_done[slot], ws);
+      post = f;
     }
+    if (e == cudaSuccess && packed) {
+      // packed returns: scan of the counts, copy of the used slots
+      if (packed_staged && c >= 2) e = cudaStreamWaitEvent(post, rd_done[slot], 0);
+      helios_return* dst = packed_staged ? reinterpret_cast<helios_return*>(buf + o_rst[slot])
+                                         : outputs->p_returns_packed;
+      if (e == cudaSuccess)
+        e = launch_pack_returns(wa.returns, wa.n_returns, m, R, d_rlen, d_roffs + b,
+                                buf + o_rscan, rscan_bytes, dst, packed_staged ? 1 : 0, rcap,
+                                post);
+      launches += 4;
+      if (e == cudaSuccess && packed_staged) {
+        e = cudaMemcpyAsync(pin + 4 + 2 * slot, d_roffs + b, sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, post);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(pin + 5 + 2 * slot, d_roffs + b + m, sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, post);
+        if (e == cudaSuccess) e = cudaEventRecord(roff_done[slot], post);
+      }
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], post);
     launches += 2;
     if (e == cudaSuccess && compact_staged && c >= 1) e = drain_compact(c - 1);
+    if (e == cudaSuccess && packed_staged && c >= 1) e = drain_returns(c - 1);
     if (e != cudaSuccess || !any_staged) continue;
     // prefetch the next chunk's inputs into the other slot once chunk c-1's
     // kernels (K6 reads origin/direction, K7 reads time) are done with it
@@ -962,6 +1024,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], cs);
   }
   if (e == cudaSuccess && compact_staged && n_chunks > 0) e = drain_compact(n_chunks - 1);
+  if (e == cudaSuccess && packed_staged && n_chunks > 0) e = drain_returns(n_chunks - 1);
   // call-wide offsets to the caller (device or host memory)
   if (e == cudaSuccess && want_offs) {
     for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess && ws != s; ++k)
@@ -970,16 +1033,25 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       e = cudaMemcpyAsync(outputs->p_wf_offset, d_offs, sizeof(uint64_t) * (n + 1),
                           cudaMemcpyDefault, s);
   }
+  if (e == cudaSuccess && packed) {
+    for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
+      e = cudaStreamWaitEvent(s, w_done[k], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(outputs->p_return_offset, d_roffs, sizeof(uint64_t) * (n + 1),
+                          cudaMemcpyDefault, s);
+  }
   // join: the caller's stream is ordered after every kernel of this call
   if (e == cudaSuccess && ws != s && n_chunks > 0)
     for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
       e = cudaStreamWaitEvent(s, w_done[k], 0);
   unsigned herr = 0;
   unsigned long long hcnt[8] = {0};
-  uint64_t htotal = 0;
+  uint64_t htotal = 0, hrtotal = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && want_offs)
     e = cudaMemcpyAsync(&htotal, d_offs + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && packed)
+    e = cudaMemcpyAsync(&hrtotal, d_roffs + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && counters)
     e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -1004,6 +1076,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (out_done[k]) cudaEventDestroy(out_done[k]);
     if (off_done[k]) cudaEventDestroy(off_done[k]);
     if (cd_done[k]) cudaEventDestroy(cd_done[k]);
+    if (roff_done[k]) cudaEventDestroy(roff_done[k]);
+    if (rd_done[k]) cudaEventDestroy(rd_done[k]);
     if (k7_done[k]) cudaEventDestroy(k7_done[k]);
   }
   cudaGetLastError();
@@ -1026,6 +1100,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   }
   if (herr & 4u) return fail(HELIOS_ERR_CUDA, "internal: compact row length mismatch");
   if (herr & 1u) return fail(HELIOS_ERR_INVALID_ARGUMENT, "a pulse direction has zero length");
+  if (packed && hrtotal > outputs->returns_capacity)
+    return fail(HELIOS_ERR_CAPACITY, "packed returns need %llu slots, capacity %llu",
+                (unsigned long long)hrtotal, (unsigned long long)outputs->returns_capacity);
   if (outputs->p_wf_compact && htotal > outputs->wf_compact_capacity)
     return fail(HELIOS_ERR_CAPACITY, "compact waveform needs %llu floats, capacity %llu",
                 (unsigned long long)htotal, (unsigned long long)outputs->wf_compact_capacity);

@@ -174,6 +174,13 @@ cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_
 cudaError_t launch_fit(const WaveArgs& a, cudaStream_t s);
 // ranging error on the returns of one launch (after K7, same stream)
 cudaError_t launch_range_noise(const WaveArgs& a, cudaStream_t s);
+// packed returns of one launch: len = n_returns, inclusive scan into
+// offs[1..m] + carry offs[0], copy of the used slots to dst (staged: dst is a
+// chunk buffer based at offs[0]); entries at or past `capacity` are skipped
+cudaError_t launch_pack_returns(const helios_return* slots, const uint8_t* nr, uint64_t m,
+                                uint32_t R, uint64_t* len, uint64_t* offs, void* scan_temp,
+                                size_t scan_bytes, helios_return* dst, int staged,
+                                uint64_t capacity, cudaStream_t s);
 // offs[1 + i] += offs[0] for i < m (carry of the previous chunks)
 cudaError_t launch_add_carry(uint64_t* offs, uint64_t m, cudaStream_t s);
 bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps);

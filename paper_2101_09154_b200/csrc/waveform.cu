@@ -26,6 +26,8 @@
 
 #include <algorithm>
 
+#include <cub/device/device_scan.cuh>
+
 #include "internal.cuh"
 #include "philox.cuh"
 
@@ -569,6 +571,49 @@ cudaError_t launch_range_noise(const WaveArgs& a, cudaStream_t s) {
   const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148ull * 8);
   k_range_noise<<<(unsigned)blocks, 256, 0, s>>>(a.returns, a.n_returns, a.n_pulses,
                                                   a.max_returns, a.noise_sd, a.seed, a.pulse_base);
+  return cudaGetLastError();
+}
+
+// Packed returns: lengths (= n_returns) and the copy of the used slots.
+__global__ void k_ret_len(const uint8_t* __restrict__ nr, uint64_t m, uint64_t* __restrict__ len) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    len[i] = nr[i];
+}
+
+__global__ void k_pack_returns(const helios_return* __restrict__ slots,
+                               const uint8_t* __restrict__ nr, uint64_t m, uint32_t R,
+                               const uint64_t* __restrict__ offs, helios_return* __restrict__ dst,
+                               int staged, uint64_t capacity) {
+  const uint64_t base = staged ? offs[0] : 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m * R;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = i / R;
+    const uint32_t j = (uint32_t)(i - p * R);
+    if (j >= nr[p]) continue;
+    const uint64_t g = offs[p] + j;
+    if (g >= capacity) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(slots + i);
+    uint4* out = reinterpret_cast<uint4*>(dst + (g - base));
+    out[0] = src[0];
+    out[1] = src[1];
+  }
+}
+
+cudaError_t launch_pack_returns(const helios_return* slots, const uint8_t* nr, uint64_t m,
+                                uint32_t R, uint64_t* len, uint64_t* offs, void* scan_temp,
+                                size_t scan_bytes, helios_return* dst, int staged,
+                                uint64_t capacity, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  const unsigned b1 = (unsigned)std::min<uint64_t>((m + 255) / 256, 148ull * 8);
+  k_ret_len<<<b1, 256, 0, s>>>(nr, m, len);
+  cudaError_t e = cudaGetLastError();
+  size_t tb = scan_bytes;
+  if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(scan_temp, tb, len, offs + 1, (int)m, s);
+  if (e == cudaSuccess) e = launch_add_carry(offs, m, s);
+  if (e != cudaSuccess) return e;
+  const unsigned b2 = (unsigned)std::min<uint64_t>((m * R + 255) / 256, 148ull * 16);
+  k_pack_returns<<<b2, 256, 0, s>>>(slots, nr, m, R, offs, dst, staged, capacity);
   return cudaGetLastError();
 }
 

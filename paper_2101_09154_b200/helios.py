@@ -72,7 +72,8 @@ class helios_outputs(ctypes.Structure):
     _fields_ = [("p_n_returns", _vp), ("p_returns", _vp), ("p_wf_first_bin", _vp),
                 ("p_waveform", _vp), ("p_subray_hits", _vp), ("p_wf_compact", _vp),
                 ("p_wf_offset", _vp), ("wf_compact_capacity", _u64), ("p_beam_origin", _vp),
-                ("p_beam_direction", _vp), ("p_beam_time", _vp)]
+                ("p_beam_direction", _vp), ("p_beam_time", _vp), ("p_returns_packed", _vp),
+                ("p_return_offset", _vp), ("returns_capacity", _u64)]
 
 
 DEFLECTORS = {"polygon": 0, "fibre": 1, "oscillating": 2, "palmer": 3}
@@ -315,6 +316,8 @@ class Outputs:
     beam_origin: object = None     # float32 [n, 3] generated pulses (survey mode), or None
     beam_direction: object = None  # float32 [n, 3]
     beam_time: object = None       # float64 [n]
+    returns_packed: object = None  # uint8 [capacity, 32] used return slots, pulse after pulse
+    return_offset: object = None   # uint64 [n + 1] offsets into returns_packed
 
     def compact_row(self, p: int):
         """Support row p as a host numpy array: W[0 .. len_p) of the dense row."""
@@ -331,7 +334,7 @@ class Outputs:
         out = {"n_returns": host(self.n_returns), "wf_first_bin": host(self.wf_first_bin),
                "waveform": host(self.waveform)}
         r = host(self.returns)
-        out["returns"] = np.ascontiguousarray(r).view(RETURN_DTYPE)[..., 0]
+        out["returns"] = None if r is None else np.ascontiguousarray(r).view(RETURN_DTYPE)[..., 0]
         h = host(self.subray_hits)
         out["subray_hits"] = None if h is None else np.ascontiguousarray(h).view(
             SUBRAY_DTYPE)[..., 0]
@@ -339,13 +342,19 @@ class Outputs:
         out["beam_origin"] = host(self.beam_origin)
         out["beam_direction"] = host(self.beam_direction)
         out["beam_time"] = host(self.beam_time)
+        rp = host(self.returns_packed)
+        out["returns_packed"] = None if rp is None else np.ascontiguousarray(rp).view(
+            RETURN_DTYPE)[..., 0]
+        out["return_offset"] = host(self.return_offset)
         out["wf_compact"] = host(self.wf_compact)
         return out
 
 
 def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=False,
                   pin_memory=False, compact: bool = False,
-                  compact_capacity: int | None = None, beams: bool = False) -> Outputs:
+                  compact_capacity: int | None = None, beams: bool = False,
+                  packed_returns: bool = False, returns_capacity: int | None = None,
+                  slots: bool = True) -> Outputs:
     """Caller-owned outputs.  compact=True adds the packed support rows
     (default capacity n * (L_p + 64) floats; helios_simulate reports
     HELIOS_ERR_CAPACITY with the exact need if that is too small)."""
@@ -360,7 +369,7 @@ def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=Fals
     R, N = int(hp.max_returns), int(hp.subray_count)
     return Outputs(
         n_returns=torch.empty(n, dtype=torch.uint8, **kw),
-        returns=torch.empty((n, R, 32), dtype=torch.uint8, **kw),
+        returns=torch.empty((n, R, 32), dtype=torch.uint8, **kw) if slots else None,
         wf_first_bin=torch.empty(n, dtype=torch.int64, **kw),
         waveform=torch.empty((n, nb), dtype=torch.float32, **kw) if waveform else None,
         subray_hits=torch.empty((n, N, 16), dtype=torch.uint8, **kw) if subray_hits else None,
@@ -371,12 +380,17 @@ def alloc_outputs(n: int, params, device="cuda", waveform=True, subray_hits=Fals
         beam_origin=torch.empty((n, 3), dtype=torch.float32, **kw) if beams else None,
         beam_direction=torch.empty((n, 3), dtype=torch.float32, **kw) if beams else None,
         beam_time=torch.empty(n, dtype=torch.float64, **kw) if beams else None,
+        returns_packed=torch.empty((int(returns_capacity if returns_capacity is not None
+                                        else 2 * n), 32), dtype=torch.uint8, **kw)
+        if packed_returns else None,
+        return_offset=torch.empty(n + 1, dtype=torch.int64, **kw) if packed_returns else None,
     )
 
 
 def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_base: int = 0,
              outputs: Outputs | None = None, waveform: bool = True, subray_hits: bool = False,
-             stream=None, stats: bool = False, counters: bool = False, compact: bool = False):
+             stream=None, stats: bool = False, counters: bool = False, compact: bool = False,
+             packed_returns: bool = False):
     """Run helios_simulate.  origin/direction: [n,3] float32 (CUDA tensors, or
     host tensors / numpy arrays -- staged by the library).  Returns
     (Outputs, helios_stats | None).  stats=True: per-kernel device times;
@@ -393,7 +407,8 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     n = int(origin.shape[0])
     if outputs is None:
         dev = "cuda" if (not isinstance(origin, np.ndarray) and origin.is_cuda) else "cpu"
-        outputs = alloc_outputs(n, hp, dev, waveform, subray_hits, compact=compact)
+        outputs = alloc_outputs(n, hp, dev, waveform, subray_hits, compact=compact,
+                                packed_returns=packed_returns)
     p = helios_pulses()
     p.p_origin = _ptr(origin)
     p.p_direction = _ptr(direction)
@@ -453,19 +468,30 @@ def simulate_survey(scene: Scene, params, survey, first_pulse: int, n_pulses: in
 
 
 def _run_with_capacity_retry(call, outputs, o):
+    """Run; on HELIOS_ERR_CAPACITY grow the packed buffer(s) to the exact need
+    reported in the offsets and run again."""
     try:
         call()
     except HeliosError as err:
         if err.status != HELIOS_ERR_CAPACITY:
             raise
-        # grow the packed buffer to the exact need reported in the offsets and rerun
         import torch
-        need = int(outputs.wf_offset[-1])
-        old = outputs.wf_compact
-        outputs.wf_compact = torch.empty(need, dtype=torch.float32, device=old.device,
-                                         pin_memory=bool(getattr(old, "is_pinned", lambda: False)()))
-        o.p_wf_compact = _ptr(outputs.wf_compact)
-        o.wf_compact_capacity = need
+        pin = lambda t: bool(getattr(t, "is_pinned", lambda: False)())
+        if outputs.wf_compact is not None and int(outputs.wf_offset[-1]) > o.wf_compact_capacity:
+            need = int(outputs.wf_offset[-1])
+            old = outputs.wf_compact
+            outputs.wf_compact = torch.empty(need, dtype=torch.float32, device=old.device,
+                                             pin_memory=pin(old))
+            o.p_wf_compact = _ptr(outputs.wf_compact)
+            o.wf_compact_capacity = need
+        if (outputs.returns_packed is not None and
+                int(outputs.return_offset[-1]) > o.returns_capacity):
+            need = int(outputs.return_offset[-1])
+            old = outputs.returns_packed
+            outputs.returns_packed = torch.empty((need, 32), dtype=torch.uint8, device=old.device,
+                                                 pin_memory=pin(old))
+            o.p_returns_packed = _ptr(outputs.returns_packed)
+            o.returns_capacity = need
         call()
 
 
@@ -484,4 +510,8 @@ def _marshal_outputs(outputs: Outputs) -> helios_outputs:
     o.p_beam_origin = _ptr(outputs.beam_origin)
     o.p_beam_direction = _ptr(outputs.beam_direction)
     o.p_beam_time = _ptr(outputs.beam_time)
+    o.p_returns_packed = _ptr(outputs.returns_packed)
+    o.p_return_offset = _ptr(outputs.return_offset)
+    rp = outputs.returns_packed
+    o.returns_capacity = 0 if rp is None else int(rp.shape[0])
     return o

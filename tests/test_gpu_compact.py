@@ -143,3 +143,61 @@ def test_offsets_only_and_compact_without_dense_rows():
     tot = int(ref["wf_offset"][-1])
     assert np.array_equal(ref["wf_compact"][:tot], g["wf_compact"][:tot])
     assert np.array_equal(ref["returns"].view(np.uint8), g["returns"].view(np.uint8))
+
+
+def _check_packed(g):
+    nr = g["n_returns"].astype(np.int64)
+    off = g["return_offset"].astype(np.int64)
+    assert off[0] == 0 and np.array_equal(np.diff(off), nr)
+    if g["returns"] is not None:
+        used = np.arange(g["returns"].shape[1])[None, :] < nr[:, None]
+        a = g["returns"][used]
+        b = g["returns_packed"][:off[-1]]
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("fit", [0, 1])
+def test_packed_returns_device_and_host(fit):
+    # packed returns (used slots only) == the fixed slots, on the device and
+    # through the host staging pipeline over several chunks, with and without
+    # the echo-width fits (which finish the returns on their own stream)
+    import torch
+    h = _h()
+    w = workload("C3", 0.03)
+    p = replace(w.params, subray_count=279, fit_echo_width=fit, range_noise_sd_m=0.02)
+    n = 25000
+    o, d, t = w.pulses(100, n)
+    a, _ = h.simulate(scene_for(w), p, _dev(o), _dev(d), _dev(t), pulse_index_base=100,
+                      packed_returns=True)
+    a = a.numpy()
+    _check_packed(a)
+    assert a["return_offset"][-1] > 1000
+    for pin in (False, True):
+        out = h.alloc_outputs(n, h.make_params(p), device="cpu", pin_memory=pin,
+                              packed_returns=True, slots=False, waveform=False)
+        args = [torch.from_numpy(x).pin_memory() for x in (o, d, t)] if pin else [o, d, t]
+        h.simulate(scene_for(w), p, *args, pulse_index_base=100, outputs=out)
+        b = out.numpy()
+        assert b["returns"] is None
+        assert np.array_equal(a["return_offset"], b["return_offset"])
+        tot = int(a["return_offset"][-1])
+        assert np.array_equal(a["returns_packed"][:tot].view(np.uint8),
+                              b["returns_packed"][:tot].view(np.uint8))
+
+
+def test_packed_returns_capacity_and_retry():
+    h = _h()
+    w = workload("C2", 0.125)
+    n = 3000
+    o, d, t = (_dev(x) for x in w.pulses(0, n))
+    ref, _ = h.simulate(scene_for(w), w.params, o, d, t, packed_returns=True)
+    ref = ref.numpy()
+    need = int(ref["return_offset"][-1])
+    out = h.alloc_outputs(n, w.params, packed_returns=True, returns_capacity=need // 3,
+                          compact=True, compact_capacity=7)
+    out, _ = h.simulate(scene_for(w), w.params, o, d, t, outputs=out)  # grows both, reruns
+    g = out.numpy()
+    assert g["returns_packed"].shape[0] == need
+    assert np.array_equal(ref["returns_packed"][:need].view(np.uint8),
+                          g["returns_packed"][:need].view(np.uint8))
+    _check_packed(g)
