@@ -45,7 +45,8 @@ struct helios_scene_s {
     char* ptr;
     size_t bytes;
     bool busy;
-    cudaStream_t copy;  // non-blocking copy stream for host staging (lazy)
+    cudaStream_t copy;  // non-blocking host->device copy stream for host staging (lazy)
+    cudaStream_t copy_out;  // device->host copies (own stream: PCIe is full duplex)
     cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
     cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
     uint64_t* pinned;   // 8 pinned words: per chunk slot (first, last) offsets of the
@@ -65,7 +66,7 @@ struct helios_scene_s {
         break;
       }
     if (!use) {
-      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr});
+      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr, nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
@@ -81,7 +82,12 @@ struct helios_scene_s {
         cudaError_t e = cudaStreamCreateWithFlags(&use->copy, cudaStreamNonBlocking);
         if (e != cudaSuccess) return e;
       }
-      *copy = use->copy;
+      if (!use->copy_out) {
+        cudaError_t e = cudaStreamCreateWithFlags(&use->copy_out, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+      }
+      copy[0] = use->copy;
+      copy[1] = use->copy_out;
     }
     if (!use->wave) {
       cudaError_t e = cudaStreamCreateWithFlags(&use->wave, cudaStreamNonBlocking);
@@ -119,6 +125,10 @@ struct helios_scene_s {
       if (sl.copy) {
         cudaStreamSynchronize(sl.copy);
         cudaStreamDestroy(sl.copy);
+      }
+      if (sl.copy_out) {
+        cudaStreamSynchronize(sl.copy_out);
+        cudaStreamDestroy(sl.copy_out);
       }
       if (sl.wave) {
         cudaStreamSynchronize(sl.wave);
@@ -670,16 +680,20 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
                            carve(packed_staged ? sizeof(helios_return) * R * chunk : 0)};
 
   char* buf = nullptr;
-  cudaStream_t cs = nullptr, ws = nullptr, fs = nullptr;
+  cudaStream_t cs = nullptr, co = nullptr, ws = nullptr, fs = nullptr;  // co: D2H copies
+  cudaStream_t cpair[2] = {nullptr, nullptr};
   uint64_t* pin = nullptr;  // [slot][first, last] row offsets of a staged compact chunk
-  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? &cs : nullptr, &ws, &pin,
+  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? cpair : nullptr, &ws, &pin,
                               fit ? &fs : nullptr);
+  cs = cpair[0];
+  co = cpair[1];
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
     cudaStreamSynchronize(ws);
     if (fs) cudaStreamSynchronize(fs);
     if (cs) cudaStreamSynchronize(cs);
+    if (co) cudaStreamSynchronize(co);
     sc->release(s);
   };
   SubrayConst* d_tab = reinterpret_cast<SubrayConst*>(buf + o_tab);
@@ -794,7 +808,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   // Stream graph per chunk c (slot = c & 1):
   //   s  : [wait in_done]  [wait w_done(c-2)]  K6(c)  -> t_done
   //   ws : wait t_done  [wait out_done(c-2)]   K7(c)  -> w_done
-  //   cs : wait w_done(c-1) -> H2D(c+1) -> in_done ; wait w_done(c) -> D2H(c) -> out_done
+  //   cs : wait w_done(c-1) -> H2D(c+1) -> in_done
+  //   co : wait w_done(c) -> D2H(c) -> out_done   (own stream: PCIe is full duplex)
   // so K7(c) runs concurrently with K6(c+1) and the copies with both.
   cudaEvent_t in_done[2] = {}, t_done[2] = {}, w_done[2] = {}, out_done[2] = {};
   cudaEvent_t off_done[2] = {}, cd_done[2] = {};  // compact: offsets of chunk known / drained
@@ -821,6 +836,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (any_staged && e == cudaSuccess) {
     e = cudaEventRecord(t_done[1], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, t_done[1], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(co, t_done[1], 0);
   }
   auto dev_ptr = [&](const Arr& a, int slot, uint64_t b) -> char* {
     if (a.gen && !a.user) return buf + a.off[slot];
@@ -849,11 +865,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     cudaError_t r = cudaEventSynchronize(off_done[sl]);
     if (r != cudaSuccess) return r;
     const uint64_t first = pin[2 * sl], last = std::min(pin[2 * sl + 1], cap);
-    r = cudaStreamWaitEvent(cs, w_done[sl], 0);
+    r = cudaStreamWaitEvent(co, w_done[sl], 0);
     if (r == cudaSuccess && last > first)
       r = cudaMemcpyAsync(outputs->p_wf_compact + first, buf + o_cst[sl],
-                          sizeof(float) * (last - first), cudaMemcpyDeviceToHost, cs);
-    if (r == cudaSuccess) r = cudaEventRecord(cd_done[sl], cs);
+                          sizeof(float) * (last - first), cudaMemcpyDeviceToHost, co);
+    if (r == cudaSuccess) r = cudaEventRecord(cd_done[sl], co);
     return r;
   };
 
@@ -864,11 +880,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     cudaError_t r = cudaEventSynchronize(roff_done[sl]);
     if (r != cudaSuccess) return r;
     const uint64_t first = pin[4 + 2 * sl], last = std::min(pin[4 + 2 * sl + 1], rcap);
-    r = cudaStreamWaitEvent(cs, w_done[sl], 0);
+    r = cudaStreamWaitEvent(co, w_done[sl], 0);
     if (r == cudaSuccess && last > first)
       r = cudaMemcpyAsync(outputs->p_returns_packed + first, buf + o_rst[sl],
-                          sizeof(helios_return) * (last - first), cudaMemcpyDeviceToHost, cs);
-    if (r == cudaSuccess) r = cudaEventRecord(rd_done[sl], cs);
+                          sizeof(helios_return) * (last - first), cudaMemcpyDeviceToHost, co);
+    if (r == cudaSuccess) r = cudaEventRecord(rd_done[sl], co);
     return r;
   };
 
@@ -1016,12 +1032,12 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       if (e == cudaSuccess) e = copy_in(b + chunk, slot ^ 1);
     }
     // drain this chunk's outputs
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, w_done[slot], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(co, w_done[slot], 0);
     for (const Arr& a : arrs)
       if (e == cudaSuccess && a.staged && !a.in)
         e = cudaMemcpyAsync((char*)a.user + a.per_pulse * b, buf + a.off[slot], a.per_pulse * m,
-                            cudaMemcpyDeviceToHost, cs);
-    if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], cs);
+                            cudaMemcpyDeviceToHost, co);
+    if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], co);
   }
   if (e == cudaSuccess && compact_staged && n_chunks > 0) e = drain_compact(n_chunks - 1);
   if (e == cudaSuccess && packed_staged && n_chunks > 0) e = drain_returns(n_chunks - 1);
@@ -1056,6 +1072,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && cs) e = cudaStreamSynchronize(cs);
+  if (e == cudaSuccess && co) e = cudaStreamSynchronize(co);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws);
   if (e == cudaSuccess && fs) e = cudaStreamSynchronize(fs);
   double t_trace = 0.0, t_wave = 0.0;
