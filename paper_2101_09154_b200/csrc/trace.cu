@@ -30,6 +30,9 @@ constexpr float kCullSlack = 1.0f + 4.0f * kBoxSlack;
 #ifndef HELIOS_LAZY_CULL
 #define HELIOS_LAZY_CULL 0
 #endif
+#ifndef HELIOS_PREDICATED_BOX
+#define HELIOS_PREDICATED_BOX 0
+#endif
 
 // fp64 helpers with explicit round-to-nearest intrinsics: no FMA contraction,
 // so every expression below evaluates exactly like the oracle's (same
@@ -358,6 +361,17 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
     const Node* nd = a.nodes + ref;
     const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
                  rf = __ldg(&nd->ref);
+    // every lane tests (the warp issues the instructions either way); lanes
+    // outside the mask are masked out of the result -- no divergent branch
+#if HELIOS_PREDICATED_BOX
+    if (INSTR && mine) ++c_nodes;
+    const float tb = (float)t_best;
+    float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy,
+                         iz, tb);
+    float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy,
+                         iz, tb);
+    if (!mine) t0 = t1 = INFINITY;
+#else
     float t0 = INFINITY, t1 = INFINITY;
     if (mine) {
       if (INSTR) ++c_nodes;
@@ -367,6 +381,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
       t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy, iz,
                      tb);
     }
+#endif
     const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
     const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
     const unsigned m0 = __ballot_sync(kFull, h0), m1 = __ballot_sync(kFull, h1);
