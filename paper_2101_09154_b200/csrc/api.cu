@@ -897,7 +897,6 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (const char* v = getenv("HELIOS_TRAVERSAL")) {
     if (!strcmp(v, "ray")) mode = 0;
     else if (!strcmp(v, "packet4") && (sc->bvh.nodes4 || ref_is_leaf(sc->bvh.root))) mode = 2;
-    else if (!strcmp(v, "pulse")) mode = 3;  // one warp per pulse (N in (32, 96], triangles)
   }
   // K7 overlaps K6 on its own stream, except on voxel scenes: there K6 is
   // ALU-bound (fp64 DDA + Philox) and a concurrent K7 costs more than it

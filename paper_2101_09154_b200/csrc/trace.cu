@@ -759,224 +759,6 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   }
 }
 
-// ---------------------------------------------------------------------------
-// Pulse-per-warp variant for wide beams (N > 64; C5's 91 subrays): one warp
-// holds ALL subrays of one pulse, K per lane (subray s = lane + 32 j).  The
-// warp walks one path through the tree for the whole beam, so the per-step
-// overhead (node load, ballots, branch, stack) is paid once per pulse instead
-// of once per 32 subrays, and no warp straddles two pulses (one origin).
-// Masks are per ray slot j; the (node, K masks) stack lives in shared memory;
-// the fp64 subray directions too (needed only at leaves).  Same per-ray tests
-// and decisions as k_trace (triangle scenes only).
-#ifndef HELIOS_PW_MIN_BLOCKS
-#define HELIOS_PW_MIN_BLOCKS 5  // K rays per lane need more registers than k_trace
-#endif
-template <bool INSTR, int K>
-__global__ void __launch_bounds__(128, HELIOS_PW_MIN_BLOCKS) k_trace_pw(const TraceArgs a) {
-  static_assert(K >= 2 && K <= 3, "2 or 3 subrays per lane");
-  __shared__ double sD[4][K * 32][3];
-  __shared__ int4 sStk[4][kStackSize];
-  const unsigned kFull = 0xffffffffu;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t p = (uint64_t)blockIdx.x * 4 + warp;
-  if (p >= a.n_pulses) return;  // warp-uniform
-  const uint32_t N = a.N;
-  unsigned long long c_nodes = 0, c_tris = 0, c_f64 = 0;
-
-  // ---- A2: fan-out (R2, R4), fp64, as k_trace
-  const float ox = __ldg(a.origin + 3 * p), oy = __ldg(a.origin + 3 * p + 1),
-              oz = __ldg(a.origin + 3 * p + 2);
-  D3 Dp = d3(__ldg(a.direction + 3 * p), __ldg(a.direction + 3 * p + 1),
-             __ldg(a.direction + 3 * p + 2));
-  const double dn = norm(Dp);
-  const bool ok = dn > 0.0 && isfinite(dn);
-  if (!ok) {
-    if (lane == 0) atomicOr(a.err_flag, 1u);
-    Dp = d3(0.0, 0.0, 1.0);
-  } else {
-    Dp = scale(Dp, __drcp_rn(dn));
-  }
-  const D3 axv = fabs(Dp.z) > 0.9 ? d3(1.0, 0.0, 0.0) : d3(0.0, 0.0, 1.0);
-  D3 U = cross(axv, Dp);
-  U = scale(U, __drcp_rn(norm(U)));
-  const D3 V = cross(Dp, U);
-  const D3 O = d3(ox, oy, oz);
-  const F3 O32 = {ox, oy, oz};
-
-  float ix[K], iy[K], iz[K];
-  double tb[K];
-  uint32_t bk[K];
-  unsigned msk[K];
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const uint32_t s = lane + 32u * j;
-    const bool valid = ok && s < N;
-    D3 D = d3(0.0, 0.0, 1.0);
-    if (s < N) {
-      const SubrayConst sc = a.sub[s];
-      const D3 ring = vadd(scale(U, sc.cos_p), scale(V, sc.sin_p));
-      D = vadd(scale(Dp, sc.cos_t), scale(ring, sc.sin_t));
-    }
-    sD[warp][lane + 32 * j][0] = D.x;
-    sD[warp][lane + 32 * j][1] = D.y;
-    sD[warp][lane + 32 * j][2] = D.z;
-    ix[j] = safe_inv((float)D.x);
-    iy[j] = safe_inv((float)D.y);
-    iz[j] = safe_inv((float)D.z);
-    tb[j] = INFINITY;
-    bk[j] = 0xFFFFFFFFu;
-    msk[j] = __ballot_sync(kFull, valid);
-  }
-  __syncwarp();
-
-  // ---- A3: the beam's walk through the tree
-  int4* stk = sStk[warp];
-  int sp = 0;
-  int32_t ref = a.root;
-  bool live = false;
-#pragma unroll
-  for (int j = 0; j < K; ++j) live |= msk[j] != 0;
-  if (a.n_tris == 0 || !live) ref = kEmptyRef;
-  while (ref != kEmptyRef) {
-    if (ref_is_leaf(ref)) {
-      const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
-      for (uint32_t k = first; k < first + cnt; ++k) {
-        const TriRecord tr = load_tri(a.tris, k);
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          if (!((msk[j] >> lane) & 1u)) continue;
-          const double* dd = sD[warp][lane + 32 * j];
-          const D3 D = d3(dd[0], dd[1], dd[2]);
-          const F3 D32 = {(float)D.x, (float)D.y, (float)D.z};
-          if (INSTR) ++c_tris;
-          if (mt32_definite_miss(O32, D32, l1(D32), tr, __double2float_ru(tb[j]))) continue;
-          if (INSTR) ++c_f64;
-          const double t = mt64(O, D, tr);
-          if (t > 0.0) {
-            bool take = t < tb[j];
-            if (!take && t == tb[j]) {  // exact tie: lower primitive id (R22)
-              const uint32_t cur = __float_as_uint(__ldg(&a.tris[bk[j]].a.w));
-              take = __float_as_uint(tr.a.w) < cur;
-            }
-            if (take) {
-              tb[j] = t;
-              bk[j] = k;
-            }
-          }
-        }
-      }
-      // pop
-      if (sp == 0) break;
-      --sp;
-      __syncwarp();
-      const int4 e = stk[sp];
-      ref = e.x;
-      msk[0] = (unsigned)e.y;
-      msk[1] = (unsigned)e.z;
-      if (K > 2) msk[K - 1] = (unsigned)e.w;
-      continue;
-    }
-    const Node* nd = a.nodes + ref;
-    const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01);
-    const float2 rf = __ldg(reinterpret_cast<const float2*>(&nd->ref));
-    unsigned m0[K], m1[K];
-    int both = 0, pref1 = 0, n0 = 0, n1 = 0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      float t0 = INFINITY, t1 = INFINITY;
-      if ((msk[j] >> lane) & 1u) {
-        if (INSTR) ++c_nodes;
-        const float tbf = (float)tb[j];
-        t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix[j],
-                       iy[j], iz[j], tbf);
-        t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix[j],
-                       iy[j], iz[j], tbf);
-      }
-      const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
-      m0[j] = __ballot_sync(kFull, h0);
-      m1[j] = __ballot_sync(kFull, h1);
-      both += __popc(m0[j] & m1[j]);
-      pref1 += __popc(__ballot_sync(kFull, h0 && h1 && t1 < t0));
-      n0 += __popc(m0[j]);
-      n1 += __popc(m1[j]);
-    }
-    const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
-    if (n0 && n1) {
-      const bool near0 = both ? (2 * pref1 <= both) : (n0 >= n1);
-      if (lane == 0) {
-        int4 e;
-        e.x = near0 ? r1 : r0;
-        e.y = (int)(near0 ? m1[0] : m0[0]);
-        e.z = (int)(near0 ? m1[1] : m0[1]);
-        e.w = K > 2 ? (int)(near0 ? m1[K - 1] : m0[K - 1]) : 0;
-        stk[sp] = e;
-      }
-      ++sp;
-      ref = near0 ? r0 : r1;
-#pragma unroll
-      for (int j = 0; j < K; ++j) msk[j] = near0 ? m0[j] : m1[j];
-    } else if (n0) {
-      ref = r0;
-#pragma unroll
-      for (int j = 0; j < K; ++j) msk[j] = m0[j];
-    } else if (n1) {
-      ref = r1;
-#pragma unroll
-      for (int j = 0; j < K; ++j) msk[j] = m1[j];
-    } else {
-      if (sp == 0) break;
-      --sp;
-      __syncwarp();
-      const int4 e = stk[sp];
-      ref = e.x;
-      msk[0] = (unsigned)e.y;
-      msk[1] = (unsigned)e.z;
-      if (K > 2) msk[K - 1] = (unsigned)e.w;
-    }
-  }
-
-  // ---- A5: range + radiometry per subray (Eq. 1, 2, 7; R5, R14), as k_trace
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const uint32_t s = lane + 32u * j;
-    if (s >= N) continue;
-    helios_subray_hit rec;
-    rec.range_m = __longlong_as_double(0x7FF8000000000000ll);
-    rec.amplitude = 0.0f;
-    rec.prim_id = 0xFFFFFFFFu;
-    if (ok && bk[j] != 0xFFFFFFFFu) {
-      const double* dd = sD[warp][s];
-      const D3 D = d3(dd[0], dd[1], dd[2]);
-      const SubrayConst sc = a.sub[s];
-      const TriRecord tr = load_tri(a.tris, bk[j]);
-      const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
-      const D3 n = cross(sub(d3(tr.b.x, tr.b.y, tr.b.z), v0), sub(d3(tr.c.x, tr.c.y, tr.c.z), v0));
-      const double cos_inc = __ddiv_rn(fabs(dot(n, D)), mul(norm(n), norm(D)));
-      const double R = tb[j];
-      const double sig_eff = (double)tr.b.w * cos_inc;
-      double I;
-      if (a.eq2) {
-        const double r = R * sc.sin_t;
-        const double om = a.lambda_m * R / (kPi * a.w0 * a.w0);
-        const double om0 = a.lambda_m * a.R0 / (kPi * a.w0 * a.w0);
-        const double w = a.w0 * sqrt(om0 * om0 + om * om);
-        I = (r == 0.0) ? a.I0 : a.I0 * exp(-2.0 * r * r / (w * w));
-      } else {
-        I = a.I0 * sc.w_far;
-      }
-      rec.range_m = R;
-      rec.amplitude = (float)(a.K * sig_eff * I / (R * R * R * R));
-      rec.prim_id = __float_as_uint(tr.a.w);
-    }
-    a.out[p * N + s] = rec;
-  }
-  if (INSTR) {
-    atomicAdd(a.counters + 0, c_nodes);
-    atomicAdd(a.counters + 1, c_tris);
-    atomicAdd(a.counters + 6, c_f64);
-  }
-}
-
 }  // namespace
 
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s) {
@@ -987,19 +769,6 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaSt
   if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
   const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
-  // wide beams on triangle scenes: one warp per pulse (mode 3 = auto, see api.cu)
-  if (mode == 3 && grid == 0 && a.N > 32 && a.N <= 96) {
-    const uint64_t pb = (a.n_pulses + 3) / 4;
-    if (a.N > 64) {
-      if (instrumented) k_trace_pw<true, 3><<<(unsigned)pb, T, 0, s>>>(a);
-      else k_trace_pw<false, 3><<<(unsigned)pb, T, 0, s>>>(a);
-    } else {
-      if (instrumented) k_trace_pw<true, 2><<<(unsigned)pb, T, 0, s>>>(a);
-      else k_trace_pw<false, 2><<<(unsigned)pb, T, 0, s>>>(a);
-    }
-    return cudaGetLastError();
-  }
-  if (mode == 3) mode = 1;
 #define HELIOS_TRACE_CASE(I, P, W)                                        \
   if (grid == 1)                                                          \
     k_trace<I, P, W, 1><<<g, T, 0, s>>>(a);                               \
