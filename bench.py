@@ -298,6 +298,34 @@ def run_ours(args):
         pass
     r1 = (b_ray + b_pulse) / (ms / 1e3) / 1e9 / peak
 
+    # ---- the same device-resident steps with the lossless packed outputs
+    # (packed returns + packed waveform support rows instead of 7 fixed return
+    # slots and dense rows: the zero fill of dense rows is HBM traffic, 10.7 KB
+    # per pulse on C4)
+    packed = None
+    if args.waveform == "dense" and not args.no_packed:
+        pout = h.alloc_outputs(B, hp, device=dev, waveform=False, compact=True,
+                               compact_capacity=B * n_bins, packed_returns=True, slots=False,
+                               returns_capacity=B * p.max_returns)
+        for i in range(min(args.warmup, 2)):
+            start, o, d, t = batches[i]
+            h.simulate(scene, hp, o, d, t, pulse_index_base=start, outputs=pout)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.warmup, steps_total):
+            start, o, d, t = batches[i]
+            h.simulate(scene, hp, o, d, t, pulse_index_base=start, outputs=pout)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        pms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+        packed = {"value": subrays / (pms / 1e3) / 1e6, "unit": "Mrays/s",
+                  "ms_per_step": pms / args.steps,
+                  "outputs": "packed returns + packed waveform support rows (lossless)"}
+        del pout
+
     # ---- end to end through the C ABI with host buffers (copies inside):
     # every step copies its pulses host->device and the full result back
     # (returns + the complete waveform, as lossless packed support rows; the
@@ -436,6 +464,7 @@ def run_ours(args):
             "clocks": clk,
             "e2e": e2e,
             "e2e_dense_rows": e2e_dense,
+            "packed_outputs": packed,
             "device_pulse_generation": survey,
             "cpu_baseline": cpu,
         }
@@ -458,6 +487,8 @@ def main():
     ap.add_argument("--waveform", default="dense", choices=["dense", "compact", "none"],
                     help="waveform output of the device-resident steps")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-packed", action="store_true",
+                    help="skip the device-resident packed-output measurement")
     ap.add_argument("--no-survey", action="store_true",
                     help="skip the on-device pulse generation measurement")
     ap.add_argument("--fit-echo-width", action="store_true",

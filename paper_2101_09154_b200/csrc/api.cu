@@ -943,26 +943,28 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     mark(ev_t, s);
     e = launch_trace(ta, counters, mode, s);
     mark(ev_t, s);
-    if (e == cudaSuccess && want_offs) {
-      // lengths -> inclusive scan into offs[b+1 ..] -> + offs[b] (previous chunks)
-      e = launch_support(ta.out, N, m, d.n_bins, d.taps, params->bin_width_ns, d_len, s);
-      size_t tb = scan_bytes;
-      if (e == cudaSuccess)
-        e = cub::DeviceScan::InclusiveSum(buf + o_scan, tb, d_len, d_offs + b + 1, (int)m, s);
-      if (e == cudaSuccess) e = launch_add_carry(d_offs + b, m, s);
-      launches += 3;
-      if (e == cudaSuccess && compact_staged) {
-        e = cudaMemcpyAsync(pin + 2 * slot, d_offs + b, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess)
-          e = cudaMemcpyAsync(pin + 2 * slot + 1, d_offs + b + m, sizeof(uint64_t),
-                              cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaEventRecord(off_done[slot], s);
-      }
-    }
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
     if (e == cudaSuccess && any_staged && c >= 2) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
     if (e == cudaSuccess && compact_staged && c >= 2) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
+    if (e == cudaSuccess && want_offs) {
+      // packed rows: lengths -> inclusive scan into offs[b+1 ..] -> + offs[b]
+      // (previous chunks), on K7's stream so the next chunk's K6 never waits
+      e = launch_support(ta.out, N, m, d.n_bins, d.taps, params->bin_width_ns, d_len, ws);
+      size_t tb = scan_bytes;
+      if (e == cudaSuccess)
+        e = cub::DeviceScan::InclusiveSum(buf + o_scan, tb, d_len, d_offs + b + 1, (int)m, ws);
+      if (e == cudaSuccess) e = launch_add_carry(d_offs + b, m, ws);
+      launches += 3;
+      if (e == cudaSuccess && compact_staged) {
+        e = cudaMemcpyAsync(pin + 2 * slot, d_offs + b, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                            ws);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(pin + 2 * slot + 1, d_offs + b + m, sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, ws);
+        if (e == cudaSuccess) e = cudaEventRecord(off_done[slot], ws);
+      }
+    }
     if (e != cudaSuccess) break;
     wa.rec = ta.out;
     wa.n_pulses = m;
