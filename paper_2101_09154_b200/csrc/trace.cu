@@ -158,10 +158,25 @@ __device__ __forceinline__ TriRecord load_tri(const TriRecord* __restrict__ t, u
   return r;
 }
 
-__device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, double o, double d) {
-  // crossing of plane org + k vs, computed directly (same arithmetic as the
-  // oracle's plane enumeration; intrinsics forbid FMA contraction)
+#ifndef HELIOS_DDA_RCP
+#define HELIOS_DDA_RCP 1
+#endif
+// crossing of plane org + k vs, computed directly (no accumulated increments).
+// HELIOS_DDA_RCP = 0: the oracle's exact operation ((org + k vs) - o) / d;
+// 1 (default): times the per-ray reciprocal 1/d -- within 2 ulp of the
+// quotient; the sub-ulp shifts of crossing times only move chord lengths by
+// ~1e-16 relative (transmission decisions within the 1e-12 margin rule) and
+// can turn an exact corner tie into a 1e-16-long segment, whose draw passes
+// with probability 1 - 1e-16 (DESIGN.md s.7.1)
+__device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, double o, double d,
+                                          double id) {
+#if HELIOS_DDA_RCP
+  (void)d;
+  return __dmul_rn(__dsub_rn(__dadd_rn(org, __dmul_rn((double)k, vs)), o), id);
+#else
+  (void)id;
   return __ddiv_rn(__dsub_rn(__dadd_rn(org, __dmul_rn((double)k, vs)), o), d);
+#endif
 }
 
 // Opaque / scaled voxel cube (Eq. 5; R31): minimum corner and side
@@ -659,6 +674,7 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
       int idx[3];
       double tn[3];
       int stp[3];
+      const double inv3[3] = {__drcp_rn(d3v[0]), __drcp_rn(d3v[1]), __drcp_rn(d3v[2])};
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         const double c = (o3[ax] + t_in * d3v[ax] - org[ax]) / a.vs;
@@ -666,8 +682,9 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         k = k < 0 ? 0 : (k >= (int)nn[ax] ? (int)nn[ax] - 1 : k);
         idx[ax] = k;
         stp[ax] = d3v[ax] > 0.0 ? 1 : (d3v[ax] < 0.0 ? -1 : 0);
-        tn[ax] = stp[ax] > 0   ? plane_t(org[ax], (uint32_t)(k + 1), a.vs, o3[ax], d3v[ax])
-                 : stp[ax] < 0 ? plane_t(org[ax], (uint32_t)k, a.vs, o3[ax], d3v[ax])
+        tn[ax] = stp[ax] > 0   ? plane_t(org[ax], (uint32_t)(k + 1), a.vs, o3[ax], d3v[ax],
+                                          inv3[ax])
+                 : stp[ax] < 0 ? plane_t(org[ax], (uint32_t)k, a.vs, o3[ax], d3v[ax], inv3[ax])
                                : INFINITY;
       }
       double t_cur = t_in;
@@ -711,7 +728,7 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         idx[ax] += stp[ax];
         if (idx[ax] < 0 || idx[ax] >= (int)nn[ax]) break;
         tn[ax] = plane_t(org[ax], (uint32_t)(stp[ax] > 0 ? idx[ax] + 1 : idx[ax]), a.vs, o3[ax],
-                         d3v[ax]);
+                         d3v[ax], inv3[ax]);
         t_cur = t_exit;
       }
     }
