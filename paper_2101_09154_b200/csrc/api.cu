@@ -26,6 +26,8 @@ struct helios_scene_s {
   float* d_xyz = nullptr;   // original order (build input)
   float* d_refl = nullptr;
   float* d_pad = nullptr;
+  uint8_t* d_bricks = nullptr;  // 4^3-brick occupancy of the grid
+  uint32_t nbx = 0, nby = 0, nbz = 0;
   uint32_t nx = 0, ny = 0, nz = 0;
   double origin[3] = {0, 0, 0};
   double vs = 0;
@@ -291,6 +293,18 @@ helios_status validate_params(const helios_scanner_params* p, Derived* d) {
   return HELIOS_OK;
 }
 
+// ---- 4^3-brick occupancy of the voxel grid (1 = some voxel has PAD > 0)
+__global__ void k_bricks(const float* __restrict__ pad, uint32_t nx, uint32_t ny, uint32_t nz,
+                         uint32_t nbx, uint32_t nby, uint8_t* __restrict__ bricks) {
+  const uint64_t n = (uint64_t)nx * ny * nz;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!(pad[i] > 0.0f)) continue;
+    const uint32_t x = (uint32_t)(i % nx), y = (uint32_t)((i / nx) % ny), z = (uint32_t)(i / ((uint64_t)nx * ny));
+    bricks[(x >> kBrickShift) + nbx * ((y >> kBrickShift) + nby * (z >> kBrickShift))] = 1;
+  }
+}
+
 // ---- validation kernel for scene arrays (finite vertices, rho in [0,1], PAD >= 0)
 __global__ void k_check_scene(const float* __restrict__ xyz, uint64_t n_xyz,
                               const float* __restrict__ refl, uint64_t n_refl,
@@ -323,6 +337,7 @@ void free_scene(helios_scene sc, cudaStream_t s) {
   cudaFreeAsync(sc->d_refl, s);
   cudaFreeAsync(sc->d_pad, s);
   cudaFreeAsync(sc->d_lut, s);
+  cudaFreeAsync(sc->d_bricks, s);
   cudaFreeAsync(sc->bvh.tris, s);
   cudaFreeAsync(sc->bvh.nodes, s);
   cudaFreeAsync(sc->bvh.nodes4, s);
@@ -423,6 +438,16 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
       sc->scale_alpha = desc->scale_alpha;
       sc->scale_shift = desc->scale_shift;
       if ((e = copy_in(&sc->d_pad, desc->p_voxel_pad, nvox, s)) != cudaSuccess) break;
+      // brick occupancy for empty-space skipping in the march
+      sc->nbx = (sc->nx + (1u << kBrickShift) - 1) >> kBrickShift;
+      sc->nby = (sc->ny + (1u << kBrickShift) - 1) >> kBrickShift;
+      sc->nbz = (sc->nz + (1u << kBrickShift) - 1) >> kBrickShift;
+      const size_t nbr = (size_t)sc->nbx * sc->nby * sc->nbz;
+      if ((e = cudaMallocAsync((void**)&sc->d_bricks, nbr, s)) != cudaSuccess) break;
+      if ((e = cudaMemsetAsync(sc->d_bricks, 0, nbr, s)) != cudaSuccess) break;
+      k_bricks<<<(unsigned)std::min<uint64_t>((nvox + 255) / 256, 148ull * 32), 256, 0, s>>>(
+          sc->d_pad, sc->nx, sc->ny, sc->nz, sc->nbx, sc->nby, sc->d_bricks);
+      if ((e = cudaGetLastError()) != cudaSuccess) break;
     }
     if (desc->n_lut) {
       sc->n_lut = desc->n_lut;
@@ -757,6 +782,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.g_lut = sc->d_lut;
   ta.n_lut = sc->n_lut;
   ta.voxel_mode = sc->voxel_mode;
+  ta.bricks = sc->d_bricks;
+  ta.nbx = sc->nbx;
+  ta.nby = sc->nby;
+  if (const char* v = getenv("HELIOS_BRICKS"))  // A/B switch (default on)
+    if (!atoi(v)) ta.bricks = nullptr;
   ta.voxel_refl = sc->voxel_refl;
   ta.pad_max = sc->pad_max;
   ta.scale_alpha = sc->scale_alpha;

@@ -27,6 +27,7 @@ constexpr int kStackSize = 64;        // LBVH depth bound (checked at build)
 constexpr int kLeafMax = HELIOS_LEAF_MAX;  // triangles per collapsed leaf (<= 8)
 constexpr int kMortonBits = 21;       // per axis (63-bit codes)
 constexpr int kMaxLut = 4096;
+constexpr int kBrickShift = 2;        // 4^3-voxel bricks for empty-space skipping
 constexpr int kMaxTaps = 8192;        // L_p bound (validated)
 constexpr double kC = 299792458.0;    // m/s
 constexpr double kPi = 3.14159265358979323846;
@@ -77,6 +78,8 @@ struct TraceArgs {
   double gx0, gy0, gz0, vs;
   const float* g_lut;
   uint32_t n_lut;
+  const uint8_t* bricks; // [nbz][nby][nbx] 1 = the 4^3 brick holds a voxel with PAD > 0
+  uint32_t nbx, nby;
   uint32_t voxel_mode;   // HELIOS_VOXEL_* (R31)
   double voxel_refl, pad_max, scale_alpha;
   uint32_t scale_shift;

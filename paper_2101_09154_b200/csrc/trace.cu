@@ -689,6 +689,44 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
       }
       double t_cur = t_in;
       for (;;) {
+        // empty 4^3 brick: jump to its exit crossing.  No decision happens in
+        // it (PAD = 0 everywhere), and the state after the jump is the one the
+        // cell-by-cell march would reach: every plane crossed before the exit
+        // (the tie order x < y < z included) is counted per axis.
+        if (a.bricks != nullptr) {
+          const int bx = idx[0] >> kBrickShift, by = idx[1] >> kBrickShift,
+                    bz = idx[2] >> kBrickShift;
+          if (!__ldg(a.bricks + bx + a.nbx * (by + a.nby * bz))) {
+            const int bi[3] = {bx, by, bz};
+            double tb[3];
+            int kb[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              kb[q] = stp[q] > 0 ? min((bi[q] + 1) << kBrickShift, (int)nn[q]) : bi[q] << kBrickShift;
+              tb[q] = stp[q] != 0 ? plane_t(org[q], (uint32_t)kb[q], a.vs, o3[q], d3v[q], inv3[q])
+                                  : INFINITY;
+            }
+            const int e = (tb[0] <= tb[1] && tb[0] <= tb[2]) ? 0 : (tb[1] <= tb[2] ? 1 : 2);
+            const double t_bx = tb[e];
+            if (INSTR) ++c_vox;
+            if (!(t_bx < t_out)) break;  // the ray ends inside the empty brick
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              if (q == e || stp[q] == 0) continue;
+              while (tn[q] < t_bx || (tn[q] == t_bx && q < e)) {
+                idx[q] += stp[q];
+                tn[q] = plane_t(org[q], (uint32_t)(stp[q] > 0 ? idx[q] + 1 : idx[q]), a.vs, o3[q],
+                                d3v[q], inv3[q]);
+              }
+            }
+            idx[e] = stp[e] > 0 ? kb[e] : kb[e] - 1;
+            if (idx[e] < 0 || idx[e] >= (int)nn[e]) break;
+            tn[e] = plane_t(org[e], (uint32_t)(stp[e] > 0 ? idx[e] + 1 : idx[e]), a.vs, o3[e],
+                            d3v[e], inv3[e]);
+            t_cur = t_bx;
+            continue;
+          }
+        }
         const int ax = (tn[0] <= tn[1] && tn[0] <= tn[2]) ? 0 : (tn[1] <= tn[2] ? 1 : 2);
         const double t_exit = tn[ax];
         const double t_end = fmin(t_exit, t_out);
