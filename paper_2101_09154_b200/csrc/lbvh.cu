@@ -723,16 +723,18 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     CK(cudaMemcpyAsync(&hdepth, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     out->n_nodes = n - 1;
     out->root = 0;
+  }
+  {
     // 4-wide collapse, level by level (opt-in: HELIOS_BVH4=1; measured no faster
     // than packet traversal of the binary tree, profiles/r01_wide_ab.txt)
     const char* w4 = getenv("HELIOS_BVH4");
-    if (w4 && atoi(w4)) {
+    if (w4 && atoi(w4) && n > (uint32_t)kLeafMax) {
     CK(dalloc(&qa, n - 1, s));
     CK(dalloc(&qb, n - 1, s));
     CK(dalloc(&wcnt, 2, s));
     CK(dalloc(&wide_tmp, n - 1, s));
     {
-      const int2 root_entry = make_int2(0, 0);
+      const int2 root_entry = make_int2(out->root, 0);
       const unsigned init[2] = {0u, 1u};  // next-queue size, wide nodes allocated
       CK(cudaMemcpyAsync(qa, &root_entry, sizeof(int2), cudaMemcpyHostToDevice, s));
       uint32_t n_in = 1;
