@@ -953,6 +953,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     const int slot = (int)(c & 1);
     if (any_staged) e = cudaStreamWaitEvent(s, in_done[slot], 0);
     if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(s, w_done[slot], 0);
+    // K6 writes the staged subray-hit slot chunk c-2 used: its copy-out (on the
+    // D2H stream, no longer ordered behind this chunk's H2D) must be done
+    if (e == cudaSuccess && any_staged && c >= 2) e = cudaStreamWaitEvent(s, out_done[slot], 0);
     // generated pulses of this chunk (into the slot chunk c-2 used: its copy-out
     // must be done when the export is host memory)
     if (e == cudaSuccess && gen) {
