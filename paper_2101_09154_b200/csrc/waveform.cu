@@ -258,15 +258,14 @@ __global__ void k_add_carry(uint64_t* __restrict__ offs, uint64_t m) {
 }
 
 struct Layout {
-  size_t ker_d, per_warp_d, w_off, agg_off, gval_off, off_off, amp_off;
+  size_t ker_d, per_warp_d, w_off, agg_off, off_off, amp_off;
 };
 __host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
   Layout L;
   L.ker_d = (taps + 1) & ~1u;
   L.w_off = 0;
   L.agg_off = kWCap;
-  L.gval_off = kWCap + kAggCap;                // int[kAggCap] group offsets (sparse path)
-  L.off_off = L.gval_off + kAggCap / 2;        // int[N] packed 2 per double
+  L.off_off = kWCap + kAggCap;                 // int[N] packed 2 per double
   L.amp_off = L.off_off + (N + 1) / 2;         // float[N]
   L.per_warp_d = L.amp_off + (N + 1) / 2;
   return L;
@@ -282,7 +281,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
   double* base = ker + L.ker_d + (size_t)warp * L.per_warp_d;
   double* Ws = base + L.w_off;
   double* agg = base + L.agg_off;
-  int* gval = reinterpret_cast<int*>(base + L.gval_off);
   int* off = reinterpret_cast<int*>(base + L.off_off);
   float* amp = reinterpret_cast<float*>(base + L.amp_off);
   double* Wg = gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
@@ -368,52 +366,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
           W[k] = w;
         }
       } else {
-        // wide footprint (offsets spread over >= kAggCap bins).  Wide beams
-        // (N > 32): the DISTINCT offsets are still few (a few surfaces), so
-        // group by distinct value -- ascending, by repeated warp minima --
-        // each group summed lane-strided then by a butterfly (fixed order);
-        // narrow beams, or more than kAggCap distinct offsets: per-subray
-        // accumulation in subray order.
-        int G = 0;
-        bool sparse = N > 32;
-        if (sparse) {
-          int prev = -1;
-          for (;;) {
-            int cand = INT_MAX;
-            for (uint32_t s = lane; s < N; s += 32) {
-              const int o = off[s];
-              if (o > prev && o < cand) cand = o;
-            }
-#pragma unroll
-            for (int q = 16; q > 0; q >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, q));
-            if (cand == INT_MAX) break;
-            if (G == kAggCap) {
-              sparse = false;
-              break;
-            }
-            double acc = 0.0;
-            for (uint32_t s = lane; s < N; s += 32)
-              if (off[s] == cand) acc += (double)amp[s];
-            acc = warp_sum_d(acc);
-            if (lane == 0) {
-              agg[G] = acc;
-              gval[G] = cand;
-            }
-            ++G;
-            prev = cand;
-          }
-          __syncwarp();
-        }
-        if (sparse) {
-          for (uint32_t k = lane; k < S; k += 32) {
-            double w = 0.0;
-            for (int g = 0; g < G; ++g) {
-              const int j = (int)k - gval[g];
-              if (j >= 0 && j < (int)taps) w += agg[g] * ker[j];
-            }
-            W[k] = w;
-          }
-        } else {
+        // wide footprint: per-subray accumulation in subray order
         for (uint32_t k = lane; k < S; k += 32) W[k] = 0.0;
         __syncwarp();
         for (uint32_t s = 0; s < N; ++s) {
@@ -425,7 +378,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
             if (k < S) W[k] += A * ker[j];
           }
           __syncwarp();
-        }
         }
       }
       __syncwarp();
