@@ -806,11 +806,16 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   a.out[gid] = rec;
 
   if (INSTR) {
-    atomicAdd(a.counters + 0, c_nodes);
-    atomicAdd(a.counters + 1, c_tris);
-    atomicAdd(a.counters + 2, c_vox);
-    atomicAdd(a.counters + 3, c_voxret);
-    atomicAdd(a.counters + 6, c_f64);
+    // warp-aggregated (one atomic per warp and counter; per-thread counts < 2^32)
+    const unsigned mask = __activemask();
+    const bool leader = (threadIdx.x & 31) == __ffs(mask) - 1;
+    const unsigned long long v[5] = {c_nodes, c_tris, c_vox, c_voxret, c_f64};
+    const int slot[5] = {0, 1, 2, 3, 6};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const unsigned w = __reduce_add_sync(mask, (unsigned)v[i]);
+      if (leader && w) atomicAdd(a.counters + slot[i], (unsigned long long)w);
+    }
   }
 }
 
