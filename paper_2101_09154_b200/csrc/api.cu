@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -51,8 +52,8 @@ struct helios_scene_s {
     cudaStream_t copy_out;  // device->host copies (own stream: PCIe is full duplex)
     cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
     cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
-    uint64_t* pinned;   // 8 pinned words: per chunk slot (first, last) offsets of the
-                        // packed waveform rows [0..3] and packed returns [4..7] (lazy)
+    uint64_t* pinned;   // 4 kSlots pinned words: per chunk slot (first, last) offsets of
+                        // the packed waveform rows [0, 2 kSlots) and packed returns (lazy)
   };
   std::mutex mu;
   std::vector<Slot> slots;
@@ -104,7 +105,7 @@ struct helios_scene_s {
       *fit = use->fit;
     }
     if (!use->pinned) {
-      cudaError_t e = cudaMallocHost((void**)&use->pinned, 8 * sizeof(uint64_t));
+      cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * kSlots * sizeof(uint64_t));
       if (e != cudaSuccess) return e;
     }
     use->busy = true;
@@ -150,6 +151,11 @@ struct helios_scene_s {
 namespace {
 
 thread_local std::string g_err;
+
+double now_ms() {
+  return 1e3 * (double)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                   std::chrono::steady_clock::now().time_since_epoch()).count() * 1e-9;
+}
 
 helios_status fail(helios_status st, const char* fmt, ...) {
   char buf[512];
@@ -627,7 +633,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     size_t per_pulse;
     bool in;      // host->device before the chunk's kernels, else device->host after
     bool staged;  // host memory: two chunk buffers in scratch (double buffering)
-    size_t off[2];
+    size_t off[kSlots];
     bool gen;     // pulse array written by the on-device generator (survey mode), or
                   // any array the kernels need: internal slots when the user passes NULL
   };
@@ -666,11 +672,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const size_t o_cnt = carve(sizeof(unsigned long long) * 8);
   const size_t o_ws = carve(plan.scratch_bytes);
   // two record buffers: K6 of chunk c+1 overlaps K7 of chunk c
-  const size_t o_rec[2] = {carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0),
-                           carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0)};
+  size_t o_rec[kSlots];
+  for (int k = 0; k < kSlots; ++k) o_rec[k] = carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0);
   for (Arr& a : arrs)
     if (a.staged || (a.gen && !a.user))  // staged, or generated with no export
-      for (int k = 0; k < 2; ++k) a.off[k] = carve(a.per_pulse * chunk);
+      for (int k = 0; k < kSlots; ++k) a.off[k] = carve(a.per_pulse * chunk);
   const size_t o_wp = carve(gen ? sizeof(double) * 3 * survey->n_waypoints : 0);
   // compact output: per-pulse lengths, call-wide offsets, scan temp, staging
   size_t scan_bytes = 0;
@@ -685,13 +691,12 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
                                                         params->bin_width_ns) + 1u;
   const bool fit = params->fit_echo_width != 0;
   // two job buffers: k_fit(c) on its own stream overlaps K7(c+1) and K6(c+2)
-  const size_t o_fjob[2] = {carve(fit ? sizeof(FitJob) * chunk * R : 0),
-                            carve(fit ? sizeof(FitJob) * chunk * R : 0)};
-  const size_t o_fy[2] = {carve(fit ? sizeof(double) * fit_stride * chunk * R : 0),
-                          carve(fit ? sizeof(double) * fit_stride * chunk * R : 0)};
-  const size_t o_fcnt = carve(fit ? 2 * sizeof(unsigned) : 0);
-  const size_t o_cst[2] = {carve(compact_staged ? 4ull * d.n_bins * chunk : 0),
-                           carve(compact_staged ? 4ull * d.n_bins * chunk : 0)};
+  size_t o_fjob[kSlots], o_fy[kSlots], o_cst[kSlots], o_rst[kSlots];
+  for (int k = 0; k < kSlots; ++k) o_fjob[k] = carve(fit ? sizeof(FitJob) * chunk * R : 0);
+  for (int k = 0; k < kSlots; ++k)
+    o_fy[k] = carve(fit ? sizeof(double) * fit_stride * chunk * R : 0);
+  const size_t o_fcnt = carve(fit ? kSlots * sizeof(unsigned) : 0);
+  for (int k = 0; k < kSlots; ++k) o_cst[k] = carve(compact_staged ? 4ull * d.n_bins * chunk : 0);
   // packed returns: lengths, call-wide offsets, scan temp (own: runs on K7's
   // stream concurrently with the waveform scan), staging
   const size_t o_rlen = carve(packed ? sizeof(uint64_t) * chunk : 0);
@@ -701,8 +706,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     cub::DeviceScan::InclusiveSum(nullptr, rscan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
                                   (int)chunk, s);
   const size_t o_rscan = carve(packed ? rscan_bytes : 0);
-  const size_t o_rst[2] = {carve(packed_staged ? sizeof(helios_return) * R * chunk : 0),
-                           carve(packed_staged ? sizeof(helios_return) * R * chunk : 0)};
+  for (int k = 0; k < kSlots; ++k)
+    o_rst[k] = carve(packed_staged ? sizeof(helios_return) * R * chunk : 0);
 
   char* buf = nullptr;
   cudaStream_t cs = nullptr, co = nullptr, ws = nullptr, fs = nullptr;  // co: D2H copies
@@ -835,17 +840,18 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       v.push_back(x);
     }
   };
-  // Stream graph per chunk c (slot = c & 1):
+  // Stream graph per chunk c (slot = c % kSlots; "c-K" = the chunk that last used the slot):
   //   s  : [wait in_done]  [wait w_done(c-2)]  K6(c)  -> t_done
   //   ws : wait t_done  [wait out_done(c-2)]   K7(c)  -> w_done
   //   cs : wait w_done(c-1) -> H2D(c+1) -> in_done
   //   co : wait w_done(c) -> D2H(c) -> out_done   (own stream: PCIe is full duplex)
   // so K7(c) runs concurrently with K6(c+1) and the copies with both.
-  cudaEvent_t in_done[2] = {}, t_done[2] = {}, w_done[2] = {}, out_done[2] = {};
-  cudaEvent_t off_done[2] = {}, cd_done[2] = {};  // compact: offsets of chunk known / drained
-  cudaEvent_t k7_done[2] = {};                     // fit: K7 of the chunk done, jobs listed
-  cudaEvent_t roff_done[2] = {}, rd_done[2] = {};  // packed returns: range known / drained
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+  cudaEvent_t in_done[kSlots] = {}, t_done[kSlots] = {}, w_done[kSlots] = {},
+              out_done[kSlots] = {};
+  cudaEvent_t off_done[kSlots] = {}, cd_done[kSlots] = {};  // packed rows: range known / drained
+  cudaEvent_t k7_done[kSlots] = {};                         // fit: K7 done, jobs listed
+  cudaEvent_t roff_done[kSlots] = {}, rd_done[kSlots] = {}; // packed returns: known / drained
+  for (int k = 0; k < kSlots && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess && fit) e = cudaEventCreateWithFlags(&k7_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess && packed_staged) {
@@ -885,14 +891,20 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     return cudaEventRecord(in_done[slot], cs);
   };
 
+  // HELIOS_TRACE_HOST=1: report the host's blocking time per call (stderr)
+  const bool host_trace = getenv("HELIOS_TRACE_HOST") != nullptr;
+  double host_wait_ms = 0.0;
+  const double call_t0 = host_trace ? now_ms() : 0.0;
   // staged compact rows of chunk c: the host learns the chunk's offset range
   // from the pinned mirror (written on `s` right after the chunk's scan), then
   // queues the copy behind K7(c) on the copy stream.  Called one iteration
   // late, so the GPU never waits for the host.
   const uint64_t cap = outputs->wf_compact_capacity;
   auto drain_compact = [&](uint64_t c) -> cudaError_t {
-    const int sl = (int)(c & 1);
+    const int sl = (int)(c % kSlots);
+    const double h0 = host_trace ? now_ms() : 0.0;
     cudaError_t r = cudaEventSynchronize(off_done[sl]);
+    if (host_trace) host_wait_ms += now_ms() - h0;
     if (r != cudaSuccess) return r;
     const uint64_t first = pin[2 * sl], last = std::min(pin[2 * sl + 1], cap);
     r = cudaStreamWaitEvent(co, w_done[sl], 0);
@@ -906,10 +918,13 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   // staged packed returns of chunk c (same scheme as drain_compact)
   const uint64_t rcap = outputs->returns_capacity;
   auto drain_returns = [&](uint64_t c) -> cudaError_t {
-    const int sl = (int)(c & 1);
+    const int sl = (int)(c % kSlots);
+    const double h0 = host_trace ? now_ms() : 0.0;
     cudaError_t r = cudaEventSynchronize(roff_done[sl]);
+    if (host_trace) host_wait_ms += now_ms() - h0;
     if (r != cudaSuccess) return r;
-    const uint64_t first = pin[4 + 2 * sl], last = std::min(pin[4 + 2 * sl + 1], rcap);
+    const uint64_t first = pin[2 * kSlots + 2 * sl],
+                   last = std::min(pin[2 * kSlots + 2 * sl + 1], rcap);
     r = cudaStreamWaitEvent(co, w_done[sl], 0);
     if (r == cudaSuccess && last > first)
       r = cudaMemcpyAsync(outputs->p_returns_packed + first, buf + o_rst[sl],
@@ -950,16 +965,16 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   for (uint64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
     const uint64_t b = c * chunk;
     const uint64_t m = std::min(chunk, n - b);
-    const int slot = (int)(c & 1);
+    const int slot = (int)(c % kSlots);
     if (any_staged) e = cudaStreamWaitEvent(s, in_done[slot], 0);
-    if (e == cudaSuccess && c >= 2) e = cudaStreamWaitEvent(s, w_done[slot], 0);
+    if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(s, w_done[slot], 0);
     // K6 writes the staged subray-hit slot chunk c-2 used: its copy-out (on the
     // D2H stream, no longer ordered behind this chunk's H2D) must be done
-    if (e == cudaSuccess && any_staged && c >= 2) e = cudaStreamWaitEvent(s, out_done[slot], 0);
+    if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(s, out_done[slot], 0);
     // generated pulses of this chunk (into the slot chunk c-2 used: its copy-out
     // must be done when the export is host memory)
     if (e == cudaSuccess && gen) {
-      if (gen_staged && c >= 2) e = cudaStreamWaitEvent(s, out_done[slot], 0);
+      if (gen_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(s, out_done[slot], 0);
       if (e == cudaSuccess)
         e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(arrs[0], slot, b),
                             (float*)dev_ptr(arrs[1], slot, b), (double*)dev_ptr(arrs[2], slot, b),
@@ -978,8 +993,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     mark(ev_t, s);
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
-    if (e == cudaSuccess && any_staged && c >= 2) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
-    if (e == cudaSuccess && compact_staged && c >= 2) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
+    if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
+    if (e == cudaSuccess && compact_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
     if (e == cudaSuccess && want_offs) {
       // packed rows: lengths -> inclusive scan into offs[b+1 ..] -> + offs[b]
       // (previous chunks), on K7's stream so the next chunk's K6 never waits
@@ -1014,7 +1029,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       wa.fit_y = reinterpret_cast<double*>(buf + o_fy[slot]);
       wa.fit_count = reinterpret_cast<unsigned*>(buf + o_fcnt) + slot;
       // the slot's jobs of chunk c-2 must be fitted before they are overwritten
-      if (c >= 2 && ws != s) e = cudaStreamWaitEvent(ws, w_done[slot], 0);
+      if (c >= (uint64_t)kSlots && ws != s) e = cudaStreamWaitEvent(ws, w_done[slot], 0);
       if (e == cudaSuccess) e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
     }
     mark(ev_w, ws);
@@ -1038,7 +1053,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     }
     if (e == cudaSuccess && packed) {
       // packed returns: scan of the counts, copy of the used slots
-      if (packed_staged && c >= 2) e = cudaStreamWaitEvent(post, rd_done[slot], 0);
+      if (packed_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(post, rd_done[slot], 0);
       helios_return* dst = packed_staged ? reinterpret_cast<helios_return*>(buf + o_rst[slot])
                                          : outputs->p_returns_packed;
       if (e == cudaSuccess)
@@ -1047,10 +1062,10 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
                                 post);
       launches += 4;
       if (e == cudaSuccess && packed_staged) {
-        e = cudaMemcpyAsync(pin + 4 + 2 * slot, d_roffs + b, sizeof(uint64_t),
+        e = cudaMemcpyAsync(pin + 2 * kSlots + 2 * slot, d_roffs + b, sizeof(uint64_t),
                             cudaMemcpyDeviceToHost, post);
         if (e == cudaSuccess)
-          e = cudaMemcpyAsync(pin + 5 + 2 * slot, d_roffs + b + m, sizeof(uint64_t),
+          e = cudaMemcpyAsync(pin + 2 * kSlots + 2 * slot + 1, d_roffs + b + m, sizeof(uint64_t),
                               cudaMemcpyDeviceToHost, post);
         if (e == cudaSuccess) e = cudaEventRecord(roff_done[slot], post);
       }
@@ -1063,8 +1078,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     // prefetch the next chunk's inputs into the other slot once chunk c-1's
     // kernels (K6 reads origin/direction, K7 reads time) are done with it
     if (c + 1 < n_chunks) {
-      if (c >= 1) e = cudaStreamWaitEvent(cs, w_done[slot ^ 1], 0);
-      if (e == cudaSuccess) e = copy_in(b + chunk, slot ^ 1);
+      const int nslot = (int)((c + 1) % kSlots);
+      if (c + 1 >= (uint64_t)kSlots) e = cudaStreamWaitEvent(cs, w_done[nslot], 0);
+      if (e == cudaSuccess) e = copy_in(b + chunk, nslot);
     }
     // drain this chunk's outputs
     if (e == cudaSuccess) e = cudaStreamWaitEvent(co, w_done[slot], 0);
@@ -1078,14 +1094,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (e == cudaSuccess && packed_staged && n_chunks > 0) e = drain_returns(n_chunks - 1);
   // call-wide offsets to the caller (device or host memory)
   if (e == cudaSuccess && want_offs) {
-    for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess && ws != s; ++k)
+    for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess && ws != s; ++k)
       e = cudaStreamWaitEvent(s, w_done[k], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(outputs->p_wf_offset, d_offs, sizeof(uint64_t) * (n + 1),
                           cudaMemcpyDefault, s);
   }
   if (e == cudaSuccess && packed) {
-    for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
+    for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
       e = cudaStreamWaitEvent(s, w_done[k], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(outputs->p_return_offset, d_roffs, sizeof(uint64_t) * (n + 1),
@@ -1093,7 +1109,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   }
   // join: the caller's stream is ordered after every kernel of this call
   if (e == cudaSuccess && ws != s && n_chunks > 0)
-    for (int k = 0; k < 2 && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
+    for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
       e = cudaStreamWaitEvent(s, w_done[k], 0);
   unsigned herr = 0;
   unsigned long long hcnt[8] = {0};
@@ -1110,6 +1126,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (e == cudaSuccess && co) e = cudaStreamSynchronize(co);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws);
   if (e == cudaSuccess && fs) e = cudaStreamSynchronize(fs);
+  if (host_trace)
+    fprintf(stderr, "helios_simulate: %llu pulses, %llu chunks, host %.3f ms, blocked in drains %.3f ms\n",
+            (unsigned long long)n, (unsigned long long)n_chunks, now_ms() - call_t0, host_wait_ms);
   double t_trace = 0.0, t_wave = 0.0;
   for (size_t i = 0; i + 1 < ev_t.size(); i += 2) {
     float a = 0.f;
@@ -1121,7 +1140,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   }
   for (cudaEvent_t x : ev_t) cudaEventDestroy(x);
   for (cudaEvent_t x : ev_w) cudaEventDestroy(x);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kSlots; ++k) {
     if (in_done[k]) cudaEventDestroy(in_done[k]);
     if (t_done[k]) cudaEventDestroy(t_done[k]);
     if (w_done[k]) cudaEventDestroy(w_done[k]);

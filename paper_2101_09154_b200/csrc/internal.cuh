@@ -28,6 +28,10 @@ constexpr int kLeafMax = HELIOS_LEAF_MAX;  // triangles per collapsed leaf (<= 8
 constexpr int kMortonBits = 21;       // per axis (63-bit codes)
 constexpr int kMaxLut = 4096;
 constexpr int kBrickShift = 2;        // 4^3-voxel bricks for empty-space skipping
+#ifndef HELIOS_SLOTS
+#define HELIOS_SLOTS 3
+#endif
+constexpr int kSlots = HELIOS_SLOTS;  // chunk buffers in flight (records, staging, jobs)
 constexpr int kMaxTaps = 8192;        // L_p bound (validated)
 constexpr double kC = 299792458.0;    // m/s
 constexpr double kPi = 3.14159265358979323846;

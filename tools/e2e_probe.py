@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--batch", type=int, default=1_000_000)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--start", type=int, default=0)
+    ap.add_argument("--stats", action="store_true", help="also time with stats=True")
     args = ap.parse_args()
     import torch
     import paper_2101_09154_b200 as h
@@ -27,7 +29,7 @@ def main():
     hp = h.make_params(w.params)
     nb = h.helios_waveform_bins(hp)
     B = min(args.batch, w.n_pulses)
-    o, d, t = w.pulses(0, B)
+    o, d, t = w.pulses(args.start, B)
     dev_in = [torch.from_numpy(x).cuda() for x in (o, d, t)]
     host_in = [torch.from_numpy(x).pin_memory() for x in (o, d, t)]
     N = w.params.subray_count
@@ -39,13 +41,13 @@ def main():
                                packed_returns=packed, slots=not packed,
                                returns_capacity=B * w.params.max_returns if packed else None)
 
-    def timed(inp, out):
-        h.simulate(sc, hp, *inp, outputs=out)
+    def timed(inp, out, stats=False):
+        h.simulate(sc, hp, *inp, outputs=out, stats=stats)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            h.simulate(sc, hp, *inp, outputs=out)
+            h.simulate(sc, hp, *inp, outputs=out, stats=stats)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
@@ -57,7 +59,13 @@ def main():
                                    ("dev in, host out, packed", dev_in, "cpu", True),
                                    ("host in, host out, packed", host_in, "cpu", True)):
         ms, mr = timed(inp, outs(dev, packed))
-        print(f"{args.config} {name:28s} {ms:8.2f} ms/step  {mr:8.1f} Mrays/s", flush=True)
+        _, st = h.simulate(sc, hp, *inp, outputs=outs(dev, packed), stats=True)
+        print(f"{args.config} {name:28s} {ms:8.2f} ms/step  {mr:8.1f} Mrays/s  "
+              f"K6 {st.trace_ms:6.2f} ms  K7 {st.waveform_ms:6.2f} ms", flush=True)
+        if args.stats:
+            ms, mr = timed(inp, outs(dev, packed), stats=True)
+            print(f"{args.config} {name + ' +stats':28s} {ms:8.2f} ms/step  {mr:8.1f} Mrays/s",
+                  flush=True)
     sc.destroy()
 
 
