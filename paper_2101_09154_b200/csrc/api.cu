@@ -52,6 +52,8 @@ struct helios_scene_s {
     cudaStream_t copy_out;  // device->host copies (own stream: PCIe is full duplex)
     cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
     cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
+    cudaStream_t trace2;  // second K6 stream: odd chunks, so a chunk's K6 fills the SMs
+                          // while the previous one's last wave drains (lazy)
     uint64_t* pinned;   // 4 kSlots pinned words: per chunk slot (first, last) offsets of
                         // the packed waveform rows [0, 2 kSlots) and packed returns (lazy)
   };
@@ -60,7 +62,7 @@ struct helios_scene_s {
 
   cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy,
                       cudaStream_t* wave, uint64_t** pinned = nullptr,
-                      cudaStream_t* fit = nullptr) {
+                      cudaStream_t* fit = nullptr, cudaStream_t* trace2 = nullptr) {
     std::lock_guard<std::mutex> g(mu);
     Slot* use = nullptr;
     for (Slot& sl : slots)
@@ -69,7 +71,8 @@ struct helios_scene_s {
         break;
       }
     if (!use) {
-      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr, nullptr});
+      slots.push_back(
+          Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
@@ -103,6 +106,13 @@ struct helios_scene_s {
         if (e != cudaSuccess) return e;
       }
       *fit = use->fit;
+    }
+    if (trace2) {
+      if (!use->trace2) {
+        cudaError_t e = cudaStreamCreateWithFlags(&use->trace2, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+      }
+      *trace2 = use->trace2;
     }
     if (!use->pinned) {
       cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * kSlots * sizeof(uint64_t));
@@ -140,6 +150,10 @@ struct helios_scene_s {
       if (sl.fit) {
         cudaStreamSynchronize(sl.fit);
         cudaStreamDestroy(sl.fit);
+      }
+      if (sl.trace2) {
+        cudaStreamSynchronize(sl.trace2);
+        cudaStreamDestroy(sl.trace2);
       }
       cudaFree(sl.ptr);
       if (sl.pinned) cudaFreeHost(sl.pinned);
@@ -711,10 +725,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
 
   char* buf = nullptr;
   cudaStream_t cs = nullptr, co = nullptr, ws = nullptr, fs = nullptr;  // co: D2H copies
+  cudaStream_t ts2 = nullptr;  // K6 of odd chunks
   cudaStream_t cpair[2] = {nullptr, nullptr};
   uint64_t* pin = nullptr;  // [slot][first, last] row offsets of a staged compact chunk
   cudaError_t e = sc->acquire(s, total, &buf, any_staged ? cpair : nullptr, &ws, &pin,
-                              fit ? &fs : nullptr);
+                              fit ? &fs : nullptr, &ts2);
   cs = cpair[0];
   co = cpair[1];
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
@@ -722,6 +737,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     cudaStreamSynchronize(s);
     cudaStreamSynchronize(ws);
     if (fs) cudaStreamSynchronize(fs);
+    if (ts2) cudaStreamSynchronize(ts2);
     if (cs) cudaStreamSynchronize(cs);
     if (co) cudaStreamSynchronize(co);
     sc->release(s);
@@ -949,6 +965,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   bool serial = sc->d_pad != nullptr;
   if (const char* v = getenv("HELIOS_SERIAL")) serial = atoi(v) != 0;
   if (serial) ws = s;
+  // K6 on two alternating streams (HELIOS_DUAL_TRACE=0/1 forces)
+  bool dual_trace = !serial;
+  if (const char* v = getenv("HELIOS_DUAL_TRACE")) dual_trace = atoi(v) != 0;
+  if (dual_trace && e == cudaSuccess) {
+    // ts2 must not start before the setup work on `s`
+    e = cudaEventRecord(t_done[0], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ts2, t_done[0], 0);
+  }
   if (ws != s) {
     // optional cap on K7's persistent grid while it shares the SMs with K6
     // (HELIOS_WAVE_BLOCKS_PER_SM; default: full grid, measured best)
@@ -966,19 +990,23 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     const uint64_t b = c * chunk;
     const uint64_t m = std::min(chunk, n - b);
     const int slot = (int)(c % kSlots);
-    if (any_staged) e = cudaStreamWaitEvent(s, in_done[slot], 0);
-    if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(s, w_done[slot], 0);
-    // K6 writes the staged subray-hit slot chunk c-2 used: its copy-out (on the
-    // D2H stream, no longer ordered behind this chunk's H2D) must be done
-    if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(s, out_done[slot], 0);
-    // generated pulses of this chunk (into the slot chunk c-2 used: its copy-out
+    // K6 of odd chunks on the second trace stream (chunks are independent);
+    // voxel scenes stay on one stream (measured: K6 is ALU-bound there)
+    const cudaStream_t ts = (dual_trace && (c & 1)) ? ts2 : s;
+    if (any_staged) e = cudaStreamWaitEvent(ts, in_done[slot], 0);
+    if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ts, w_done[slot], 0);
+    // K6 writes the staged subray-hit slot chunk c-K used: its copy-out (on the
+    // D2H stream, not ordered behind this chunk's H2D) must be done
+    if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots)
+      e = cudaStreamWaitEvent(ts, out_done[slot], 0);
+    // generated pulses of this chunk (into the slot chunk c-K used: its copy-out
     // must be done when the export is host memory)
     if (e == cudaSuccess && gen) {
-      if (gen_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(s, out_done[slot], 0);
+      if (gen_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ts, out_done[slot], 0);
       if (e == cudaSuccess)
         e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(arrs[0], slot, b),
                             (float*)dev_ptr(arrs[1], slot, b), (double*)dev_ptr(arrs[2], slot, b),
-                            s);
+                            ts);
       ++launches;
     }
     if (e != cudaSuccess) break;
@@ -988,10 +1016,10 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     ta.pulse_base = pulses->pulse_index_base + b;
     ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec[slot])
                      : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
-    mark(ev_t, s);
-    e = launch_trace(ta, counters, mode, s);
-    mark(ev_t, s);
-    if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], s);
+    mark(ev_t, ts);
+    e = launch_trace(ta, counters, mode, ts);
+    mark(ev_t, ts);
+    if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], ts);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
     if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
     if (e == cudaSuccess && compact_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
