@@ -1100,8 +1100,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     }
     if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], post);
     launches += 2;
-    if (e == cudaSuccess && compact_staged && c >= 1) e = drain_compact(c - 1);
-    if (e == cudaSuccess && packed_staged && c >= 1) e = drain_returns(c - 1);
+    // packed copy-outs run kSlots-1 chunks behind, so the host never blocks on
+    // a chunk whose K7 may still be queued behind the K6 it just enqueued
+    constexpr uint64_t kLag = kSlots - 1;
+    if (e == cudaSuccess && compact_staged && c >= kLag) e = drain_compact(c - kLag);
+    if (e == cudaSuccess && packed_staged && c >= kLag) e = drain_returns(c - kLag);
     if (e != cudaSuccess || !any_staged) continue;
     // prefetch the next chunk's inputs into the other slot once chunk c-1's
     // kernels (K6 reads origin/direction, K7 reads time) are done with it
@@ -1118,8 +1121,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
                             cudaMemcpyDeviceToHost, co);
     if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], co);
   }
-  if (e == cudaSuccess && compact_staged && n_chunks > 0) e = drain_compact(n_chunks - 1);
-  if (e == cudaSuccess && packed_staged && n_chunks > 0) e = drain_returns(n_chunks - 1);
+  for (uint64_t c = n_chunks > (uint64_t)(kSlots - 1) ? n_chunks - (kSlots - 1) : 0;
+       c < n_chunks && e == cudaSuccess; ++c) {
+    if (compact_staged) e = drain_compact(c);
+    if (e == cudaSuccess && packed_staged) e = drain_returns(c);
+  }
   // call-wide offsets to the caller (device or host memory)
   if (e == cudaSuccess && want_offs) {
     for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess && ws != s; ++k)
