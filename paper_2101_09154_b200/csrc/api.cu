@@ -204,6 +204,25 @@ bool device_accessible(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Kernels may store straight into page-locked host memory mapped into the
+// device address space (UVA: the same address).  Used for the packed
+// outputs, whose per-chunk extent is only known on the device: the packing
+// kernels write them over PCIe with coalesced 128-byte stores, and the host
+// never has to learn a chunk's range before its copy (HELIOS_DIRECT_HOST=0
+// stages them instead).
+bool kernel_writable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return true;
+  const char* v = getenv("HELIOS_DIRECT_HOST");
+  if (v && !atoi(v)) return false;
+  return at.type == cudaMemoryTypeHost && at.devicePointer == p;
+}
+
 // ---- subray pattern (P:199 / R1): paper rule floor(2 pi i), or hexagonal 6i
 struct Pattern {
   int q = -1;
@@ -627,9 +646,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const uint32_t R = params->max_returns;
   const cudaStream_t s = (cudaStream_t)stream;
   const bool want_offs = outputs->p_wf_offset != nullptr;
-  const bool compact_staged = outputs->p_wf_compact && !device_accessible(outputs->p_wf_compact);
+  const bool compact_staged = outputs->p_wf_compact && !kernel_writable(outputs->p_wf_compact);
   const bool packed = outputs->p_returns_packed != nullptr;
-  const bool packed_staged = packed && !device_accessible(outputs->p_returns_packed);
+  const bool packed_staged = packed && !kernel_writable(outputs->p_returns_packed);
 
   // ---- host tables
   const std::vector<SubrayConst> tab = subray_table(N, params->divergence_rad, d.pt);
