@@ -208,8 +208,9 @@ bool device_accessible(const void* p) {
 // device address space (UVA: the same address).  Used for the packed
 // outputs, whose per-chunk extent is only known on the device: the packing
 // kernels write them over PCIe with coalesced 128-byte stores, and the host
-// never has to learn a chunk's range before its copy (HELIOS_DIRECT_HOST=0
-// stages them instead).
+// never has to learn a chunk's range before its copy.  Opt-in
+// (HELIOS_DIRECT_HOST=1): measured slower than the staged copies (C2 e2e
+// 7.9 -> 9.4 ms per 1 M pulses, profiles/r01s2_e2e.txt).
 bool kernel_writable(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -218,8 +219,8 @@ bool kernel_writable(const void* p) {
     return false;
   }
   if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return true;
-  const char* v = getenv("HELIOS_DIRECT_HOST");
-  if (v && !atoi(v)) return false;
+  const char* v = getenv("HELIOS_DIRECT_HOST");  // opt-in: measured slower than staging
+  if (!v || !atoi(v)) return false;
   return at.type == cudaMemoryTypeHost && at.devicePointer == p;
 }
 
@@ -691,7 +692,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     }
 
   // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
-  const uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
+  uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
+  if (const char* v = getenv("HELIOS_CHUNK_PULSES"))  // experiments: chunk size override
+    if (atoll(v) >= 1024) chunk = std::min<uint64_t>(n, (uint64_t)atoll(v));
   const bool own_rec = outputs->p_subray_hits == nullptr;
   size_t total = 0;
   auto carve = [&](size_t bytes) {
