@@ -249,13 +249,14 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     trace_ms = wave_ms = 0.0
-    launches = 0
+    launches = trace_launches = 0
     ev0.record(stream)
     for i in range(args.warmup, steps_total):
         st = step(i, st=True)
         trace_ms += st.trace_ms
         wave_ms += st.waveform_ms
         launches += st.kernel_launches
+        trace_launches += st.trace_launches
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -268,7 +269,7 @@ def run_ours(args):
     value = subrays / (ms_max / 1e3) / 1e6
 
     # ---- algorithmic bytes (instrumented, untimed re-run of the same batches)
-    nodes = tris = vox = f64 = 0
+    nodes = tris = vox = f64 = beam_nodes = 0
     node_bytes = 64
     for i in range(args.warmup, steps_total):
         st = step(i, counters=True)
@@ -277,13 +278,16 @@ def run_ours(args):
         tris += st.tris_tested
         vox += st.voxel_steps
         f64 += st.fp64_tests
+        beam_nodes += st.beam_nodes
     sub_rank = B * N * args.steps
-    b_ray = node_bytes * nodes + 48 * tris + 4 * vox
+    # per subray: nodes K6 tests, triangles, voxel steps; per pulse: nodes the
+    # beam pre-pass K6a tests (once for all the pulse's subrays)
+    b_ray = node_bytes * nodes + 48 * tris + 4 * vox + 64 * beam_nodes
     b_trace = b_ray + 24 * B * args.steps + 16 * sub_rank  # + pulse inputs + records
     b_pulse = (32 + 8 + 1 + 4 * n_bins + 32 * p.max_returns) * B * args.steps
     peak, peak_src = peaks()
     ach_trace = b_trace / (trace_ms / 1e3) / 1e9
-    n_trace_launches = max(1, launches // 2)
+    n_trace_launches = max(1, trace_launches)
     traffic, limiter = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -456,6 +460,7 @@ def run_ours(args):
                          "share_of_step": trace_ms / ms if ms > 0 else None,
                          "waveform_share_of_step": wave_ms / ms if ms > 0 else None,
                          "nodes_per_ray": nodes / sub_rank, "node_bytes": node_bytes,
+                         "beam_nodes_per_pulse": beam_nodes / (B * args.steps),
                          "tris_per_ray": tris / sub_rank,
                          "voxel_steps_per_ray": vox / sub_rank,
                          "fp64_tests_per_ray": f64 / sub_rank,

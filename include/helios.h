@@ -258,13 +258,14 @@ typedef struct {
                                 for roofline byte accounting only)               */
   uint32_t kernel_launches;  /* out: kernels launched by this call               */
   uint32_t node_bytes;       /* out: bytes per BVH node of the traversal that ran */
-  uint32_t reserved_;
+  uint32_t trace_launches;   /* out: K6 launches (one per chunk of pulses)        */
   uint64_t pulses, subrays;
   uint64_t subray_hits, voxel_returns, returns;     /* only with collect_counters */
   uint64_t nodes_visited, tris_tested, voxel_steps; /* only with collect_counters */
   uint64_t fp64_tests; /* triangles the fp32 prefilter could not reject (collect_counters) */
   double trace_ms;    /* out: summed device time of the trace launches (K6), CUDA events */
   double waveform_ms; /* out: summed device time of the waveform launches (K7)          */
+  uint64_t beam_nodes; /* BVH nodes tested by the per-pulse beam pre-pass K6a (collect_counters) */
 } helios_stats;
 
 /* Simulate n_pulses pulses (the hot path: subray fan-out, nearest hit against

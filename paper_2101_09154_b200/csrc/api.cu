@@ -714,6 +714,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (a.staged || (a.gen && !a.user))  // staged, or generated with no export
       for (int k = 0; k < kSlots; ++k) a.off[k] = carve(a.per_pulse * chunk);
   const size_t o_wp = carve(gen ? sizeof(double) * 3 * survey->n_waypoints : 0);
+  // beam pre-pass K6a (packet traversal of a tree with internal nodes, beams of
+  // >= 7 subrays); HELIOS_BEAM=0/1 forces, HELIOS_BEAM_K sets the hand-over size
+  // (small scenes: the pre-pass costs more than the few levels it saves; measured on C6)
+  const bool beam_ok = N >= 7 && sc->n_tris > 0 && !ref_is_leaf(sc->bvh.root);
+  bool beam = beam_ok && sc->n_tris >= 65536;
+  if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
+  size_t o_ent[kSlots];
+  for (int k = 0; k < kSlots; ++k) o_ent[k] = carve(beam ? sizeof(int2) * kEntryStride * chunk : 0);
   // compact output: per-pulse lengths, call-wide offsets, scan temp, staging
   size_t scan_bytes = 0;
   if (want_offs)
@@ -845,6 +853,16 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.R0 = params->focus_range_m;
   ta.err_flag = d_err;
   ta.counters = d_cnt;
+  {
+    double smax = 0.0;
+    for (const SubrayConst& t : tab) smax = std::max(smax, t.sin_t);
+    ta.cone_sin = smax * (1.0 + 1e-9) + 1e-12;  // widened: covers the fp64 subray directions
+    ta.beam_k = 8.0;  // measured (profiles/r01s3_beam_ab.txt)
+    if (const char* v = getenv("HELIOS_BEAM_K")) ta.beam_k = atof(v);
+    ta.entry_max = kEntryMax;
+    if (const char* v = getenv("HELIOS_BEAM_ENTRIES"))
+      ta.entry_max = std::max(2, std::min(kEntryMax, atoi(v)));
+  }
 
   WaveArgs wa{};
   wa.N = N;
@@ -1005,7 +1023,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (bps > 0) plan.grid_cap = (uint32_t)(sms * bps);
   }
-  uint32_t launches = 0;
+  uint32_t launches = 0, trace_launches = 0;
   const uint64_t n_chunks = (n + chunk - 1) / chunk;
   if (any_staged && e == cudaSuccess) e = copy_in(0, 0);
   for (uint64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
@@ -1039,7 +1057,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec[slot])
                      : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
     mark(ev_t, ts);
-    e = launch_trace(ta, counters, mode, ts);
+    ta.entries = nullptr;
+    if (beam && mode == 1) {
+      ta.entries = reinterpret_cast<int2*>(buf + o_ent[slot]);
+      e = launch_beam(ta, counters, ts);
+      ++launches;
+    }
+    if (e == cudaSuccess) e = launch_trace(ta, counters, mode, ts);
+    ++trace_launches;
     mark(ev_t, ts);
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], ts);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
@@ -1214,6 +1239,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     stats->pulses = n;
     stats->subrays = n * N;
     stats->kernel_launches = launches;
+    stats->trace_launches = trace_launches;
+    stats->beam_nodes = hcnt[7];
     stats->node_bytes = mode == 2 ? (uint32_t)sizeof(Node4) : (uint32_t)sizeof(Node);
     stats->trace_ms = t_trace;
     stats->waveform_ms = t_wave;

@@ -33,6 +33,12 @@ constexpr int kBrickShift = 2;        // 4^3-voxel bricks for empty-space skippi
 #endif
 constexpr int kSlots = HELIOS_SLOTS;  // chunk buffers in flight (records, staging, jobs)
 constexpr int kMaxTaps = 8192;        // L_p bound (validated)
+// beam entry lists (K6a k_beam -> K6): per pulse one 256-B row of int2,
+// row[0].x = entry count, row[1 .. count] = (subtree ref, bits of a float lower
+// bound on every subray's entry distance into its box), near-first order
+constexpr int kEntryStride = 32;
+constexpr int kEntryMax = kEntryStride - 1;  // runtime cap TraceArgs::entry_max <= this
+static_assert(kEntryMax <= 32, "K6a keeps its emit flags in 32 bits");
 constexpr double kC = 299792458.0;    // m/s
 constexpr double kPi = 3.14159265358979323846;
 
@@ -101,6 +107,11 @@ struct TraceArgs {
   helios_subray_hit* out;  // [n][N]
   unsigned int* err_flag;  // set on zero-length direction
   unsigned long long* counters;  // instrumented variant: [nodes, tris, voxel steps, voxel returns]
+  // beam pre-pass (K6a): per-pulse cone over all subrays; nullptr = K6 starts at the root
+  int2* entries;         // [n_pulses][kEntryStride] (K6a writes, K6 reads)
+  int entry_max;         // list cap, 2 .. kEntryMax
+  double cone_sin;       // sin of the (widened) cone half-angle: max_i sin(theta_i)
+  double beam_k;         // a node is handed to K6 once extent <= beam_k * cone radius
 };
 
 // One echo-width fit job (R28), appended by K7, solved by k_fit.
@@ -164,6 +175,8 @@ cudaError_t launch_generate(const SurveyArgs& a, uint64_t first, uint64_t n, flo
 // launchers (trace.cu / waveform.cu)
 // mode: 0 per-ray binary, 1 packet binary, 2 packet 4-wide
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s);
+// K6a: per-pulse beam entry lists into a.entries (before launch_trace, same stream)
+cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s);
 
 struct WavePlan {
   int warps;            // warps per block (0 = does not fit)

@@ -315,10 +315,10 @@ __device__ __forceinline__ void traverse_ray(const TraceArgs& a, const D3& O, co
 // Every lane visits a superset of the nodes its own per-ray traversal would
 // visit, so the result is identical.
 template <bool INSTR>
-__device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, const D3& O,
-                                                const D3& D, const F3& O32, const F3& D32,
-                                                float dl1, float ix, float iy, float iz,
-                                                double& t_best, uint32_t& best_id,
+__device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, int32_t ref,
+                                                const D3& O, const D3& D, const F3& O32,
+                                                const F3& D32, float dl1, float ix, float iy,
+                                                float iz, double& t_best, uint32_t& best_id,
                                                 uint32_t& best_k, unsigned long long& c_nodes,
                                                 unsigned long long& c_tris,
                                                 unsigned long long& c_f64) {
@@ -327,7 +327,6 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   int32_t stA_r = 0, stB_r = 0;
   unsigned stA_m = 0, stB_m = 0;
   int sp = 0;
-  int32_t ref = a.root;
 #if HELIOS_LAZY_CULL
   float tstk[kStackSize];  // this lane's entry distance into every pushed child
 #endif
@@ -554,6 +553,143 @@ __device__ __forceinline__ void traverse_packet4(const TraceArgs& a, unsigned m,
   }
 }
 
+// ---- K6a: beam pre-pass.  The subrays of a pulse share its origin and lie in
+// the cone of half-angle max_i theta_i about its axis (R2).  One
+// thread per pulse walks the top of the tree with that cone and lists the
+// subtrees K6 must enter, near-first: a node is listed once it is small next
+// to the cone's cross-section (extent <= beam_k * radius at its entry
+// distance; below that the per-subray tests of K6 cull better than the cone)
+// or when it is a leaf.  K6 then starts its packet walks at the listed nodes
+// instead of at the root, so the top levels are tested once per pulse
+// instead of once per warp of subrays.
+//
+// Conservative by construction: the listed subtrees cover every node whose
+// box an fp64 subray enters.  The cone is replaced by the box of directions
+// (per axis, the exact component range over the cone, widened by 1e-9): for a
+// box [bl, bh], t * [lo, hi] must meet [bl - o, bh - o] on every axis for
+// some t >= 0 -- the interval form of the slab test, in fp64 with a 1e-12
+// relative slack (each bound carries <= 3 roundings of 2^-53).
+struct Cone {
+  double o[3];
+  double rl[3], rh[3];  // 1 / lo, 1 / hi of the direction interval per axis
+  int mode[3];          // 0: lo > 0, 1: hi < 0, 2: interval contains 0
+};
+
+__device__ __forceinline__ bool cone_box(const Cone& c, float lx, float hx, float ly, float hy,
+                                         float lz, float hz, double& t_enter) {
+  const float bl[3] = {lx, ly, lz}, bh[3] = {hx, hy, hz};
+  double tlo = 0.0, thi = INFINITY;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double e0 = (double)bl[k] - c.o[k], e1 = (double)bh[k] - c.o[k];
+    if (c.mode[k] == 0) {         // t lo <= e1, t hi >= e0
+      tlo = fmax(tlo, e0 * c.rh[k]);
+      thi = fmin(thi, e1 * c.rl[k]);
+    } else if (c.mode[k] == 1) {  // both negative: the inequalities flip
+      tlo = fmax(tlo, e1 * c.rl[k]);
+      thi = fmin(thi, e0 * c.rh[k]);
+    } else {                      // lo < 0 < hi: lower bounds only
+      tlo = fmax(tlo, fmax(e1 * c.rl[k], e0 * c.rh[k]));
+    }
+  }
+  t_enter = tlo;
+  return tlo <= thi * (1.0 + 1e-12);
+}
+
+template <bool INSTR>
+__global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.n_pulses) return;
+  int2* row = a.entries + p * kEntryStride;
+  // the pulse axis exactly as K6 normalises it
+  D3 Dp = d3(__ldg(a.direction + 3 * p), __ldg(a.direction + 3 * p + 1),
+             __ldg(a.direction + 3 * p + 2));
+  const double dn = norm(Dp);
+  if (!(dn > 0.0) || !isfinite(dn)) {  // K6 reports the pulse as hitless
+    row[0] = make_int2(0, 0);
+    return;
+  }
+  Dp = scale(Dp, __drcp_rn(dn));
+  Cone c;
+  const double dd[3] = {Dp.x, Dp.y, Dp.z};
+  const double sa = a.cone_sin;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c.o[k] = (double)__ldg(a.origin + 3 * p + k);
+    // over the cone, component k lies in d_k cos(a) -+ sqrt(1 - d_k^2) sin(a);
+    // 1 - cos(a) <= sin^2(a)
+    const double h = sqrt(fmax(0.0, 1.0 - dd[k] * dd[k])) * sa + fabs(dd[k]) * sa * sa + 1e-9;
+    double lo = dd[k] - h, hi = dd[k] + h;
+    if (lo > 0.0) {
+      c.mode[k] = 0;
+    } else if (hi < 0.0) {
+      c.mode[k] = 1;
+    } else {
+      c.mode[k] = 2;
+      if (lo == 0.0) lo = -1e-300;  // widening is conservative
+      if (hi == 0.0) hi = 1e-300;
+    }
+    c.rl[k] = 1.0 / lo;
+    c.rh[k] = 1.0 / hi;
+  }
+  unsigned long long c_nodes = 0;
+  // work stack of (ref, entry distance); bit i of `emit` marks entry i as
+  // final (listed when popped).  Invariant: count + sp <= entry_max, so the
+  // list never overflows: a node is expanded only while both children still
+  // fit, else it is listed whole (coarser, still exact).  Listed distances are
+  // rounded down and shrunk by 1e-6: K6 drops a lane from an entry only when
+  // its nearest hit is strictly nearer than any point of the box.
+  int32_t stk[kEntryMax];
+  float stt[kEntryMax];
+  uint32_t emit = 0;
+  int sp = 0, cnt = 0;
+  const int cap = a.entry_max;
+  stk[0] = a.root;
+  stt[0] = 0.0f;
+  sp = 1;
+  while (sp > 0) {
+    --sp;
+    const int32_t ref = stk[sp];
+    if (((emit >> sp) & 1u) || ref_is_leaf(ref) || cnt + sp + 2 > cap) {
+      row[1 + cnt++] = make_int2(ref, __float_as_int(stt[sp]));
+      continue;
+    }
+    const Node* nd = a.nodes + ref;
+    const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
+                 rf = __ldg(&nd->ref);
+    if (INSTR) ++c_nodes;
+    double t0, t1;
+    const bool h0 = cone_box(c, xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, t0);
+    const bool h1 = cone_box(c, xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, t1);
+    const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
+    // listed as a whole once the node is small next to the cone's cross-section
+    const float e0 = fmaxf(fmaxf(xy0.y - xy0.x, xy0.w - xy0.z), z01.y - z01.x);
+    const float e1 = fmaxf(fmaxf(xy1.y - xy1.x, xy1.w - xy1.z), z01.w - z01.z);
+    const bool f0 = (double)e0 <= a.beam_k * t0 * sa, f1 = (double)e1 <= a.beam_k * t1 * sa;
+    const bool near0 = !h1 || (h0 && t0 <= t1);
+    auto push = [&](int32_t r, double t, bool f) {
+      stk[sp] = r;
+      stt[sp] = __double2float_rd(t) * (1.0f - 1e-6f);
+      emit = f ? emit | (1u << sp) : emit & ~(1u << sp);
+      ++sp;
+    };
+    // push far first, then near (popped first: near-first order)
+    if (near0) {
+      if (h1) push(r1, t1, f1);
+      if (h0) push(r0, t0, f0);
+    } else {
+      if (h0) push(r0, t0, f0);
+      push(r1, t1, f1);
+    }
+  }
+  row[0] = make_int2(cnt, 0);
+  if (INSTR) {
+    const unsigned mask = __activemask();
+    const unsigned w = __reduce_add_sync(mask, (unsigned)c_nodes);
+    if ((threadIdx.x & 31) == __ffs(mask) - 1 && w) atomicAdd(a.counters + 7, (unsigned long long)w);
+  }
+}
+
 #ifndef HELIOS_TRACE_MIN_BLOCKS
 #define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
 #endif
@@ -621,9 +757,35 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         if (WIDE)
           traverse_packet4<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
                                   c_nodes, c_tris, c_f64);
-        else
-          traverse_packet<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
-                                 c_nodes, c_tris, c_f64);
+        else {
+          // beam entry lists (K6a): the warp walks, pulse by pulse, the subtrees
+          // the pulse's cone reaches, each with the lanes of that pulse; without
+          // lists, one walk from the root with every lane
+          unsigned rem = m;
+          while (rem) {
+            unsigned mq = rem;
+            if (a.entries == nullptr) {
+              traverse_packet<INSTR>(a, mq, a.root, O, D, O32, D32, dl1, ix, iy, iz, t_best,
+                                     best_id, best_k, c_nodes, c_tris, c_f64);
+              break;
+            }
+            const uint32_t pq = __shfl_sync(0xffffffffu, (uint32_t)p, __ffs(rem) - 1);
+            const bool mine_q = valid && (uint32_t)p == pq;
+            mq = __ballot_sync(0xffffffffu, mine_q);
+            rem &= ~mq;
+            const int2* row = a.entries + (uint64_t)pq * kEntryStride;
+            const int cnt = __ldg(&row->x);
+            for (int i = 1; i <= cnt; ++i) {
+              const int2 en = __ldg(row + i);
+              // lanes whose nearest hit is already nearer than the box drop out
+              const unsigned me =
+                  __ballot_sync(0xffffffffu, mine_q && !(t_best < (double)__int_as_float(en.y)));
+              if (me)
+                traverse_packet<INSTR>(a, me, en.x, O, D, O32, D32, dl1, ix, iy, iz, t_best,
+                                       best_id, best_k, c_nodes, c_tris, c_f64);
+            }
+          }
+        }
       }
     } else {
       traverse_ray<INSTR>(a, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k, c_nodes,
@@ -820,6 +982,19 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
 }
 
 }  // namespace
+
+cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
+  if (a.n_pulses == 0) return cudaSuccess;
+  if (a.entries == nullptr || ref_is_leaf(a.root)) return cudaErrorInvalidValue;
+  const unsigned T = 128;
+  const uint64_t blocks = (a.n_pulses + T - 1) / T;
+  if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  if (instrumented)
+    k_beam<true><<<(unsigned)blocks, T, 0, s>>>(a);
+  else
+    k_beam<false><<<(unsigned)blocks, T, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s) {
   const uint64_t total = a.n_pulses * (uint64_t)a.N;

@@ -89,11 +89,11 @@ class helios_survey(ctypes.Structure):
 
 class helios_stats(ctypes.Structure):
     _fields_ = ([("collect_counters", _u32), ("kernel_launches", _u32), ("node_bytes", _u32),
-                 ("reserved_", _u32)] +
+                 ("trace_launches", _u32)] +
                 [(n, _u64) for n in ("pulses", "subrays", "subray_hits", "voxel_returns",
                                      "returns", "nodes_visited", "tris_tested", "voxel_steps",
                                      "fp64_tests")] +
-                [("trace_ms", _d), ("waveform_ms", _d)])
+                [("trace_ms", _d), ("waveform_ms", _d), ("beam_nodes", _u64)])
 
 
 class helios_scene_info(ctypes.Structure):

@@ -2,7 +2,9 @@
 same seeded pulses."""
 from __future__ import annotations
 
+import contextlib
 import functools
+import os
 
 import numpy as np
 
@@ -64,3 +66,17 @@ def take(gpu: dict, idx) -> dict:
     for k, v in gpu.items():
         out[k] = None if v is None else v[idx]
     return out
+
+
+@contextlib.contextmanager
+def beam_env(value: str):
+    """HELIOS_BEAM=0/1 for the calls inside (read by helios_simulate per call)."""
+    old = os.environ.get("HELIOS_BEAM")
+    os.environ["HELIOS_BEAM"] = value
+    try:
+        yield
+    finally:
+        if old is None:
+            os.environ.pop("HELIOS_BEAM", None)
+        else:
+            os.environ["HELIOS_BEAM"] = old

@@ -4,13 +4,17 @@ import numpy as np
 import pytest
 
 from parity import compare, gpu_invariants
-from gpu_util import gpu_run, oracle_run, take, workload
+from gpu_util import beam_env, gpu_run, oracle_run, take, workload
 
 pytestmark = pytest.mark.gpu
 
 
 def _parity(w, start, count, sample=None, params=None, seed=0):
-    g = gpu_run(w, start, count, params=params)
+    # the reduced scenes are below the library's beam pre-pass threshold
+    # (65 536 triangles): force K6a on so parity covers it (the default path
+    # without it is checked bitwise against this one in test_beam_prepass_*)
+    with beam_env("1"):
+        g = gpu_run(w, start, count, params=params)
     p = params or w.params
     errs = gpu_invariants(g, p.max_returns, p.detection_threshold)
     assert not errs, errs
@@ -151,3 +155,24 @@ def test_opaque_and_scaled_voxels(mode, kw):
     w2 = replace(w, scene=replace(w.scene, voxel_mode=mode, **kw))
     rep, hits = _parity(w2, 3000, 3000, params=replace(w.params, seed=9))
     assert hits > 0.5
+
+
+@pytest.mark.parametrize("name,scale,start,count", [("C2", 0.125, 0, 20000),
+                                                    ("C3", 0.03, 1000, 20000),
+                                                    ("C5", 0.03, 0, 8000),
+                                                    ("C6", 0.2, 40000, 20000)])
+def test_beam_prepass_bitwise(name, scale, start, count):
+    """K6a (per-pulse cone pre-pass, entry lists) only changes where K6's walks
+    start: every output must be bitwise identical with and without it."""
+    w = workload(name, scale)
+    with beam_env("0"):
+        a, sa = gpu_run(w, start, count, stats=True)
+    with beam_env("1"):
+        b, sb = gpu_run(w, start, count, stats=True)
+    for k in a:
+        if a[k] is None:
+            continue
+        assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+    assert sa.beam_nodes == 0 and sb.beam_nodes > 0
+    # the pre-pass replaces per-subray node tests near the root
+    assert sb.nodes_visited < sa.nodes_visited
