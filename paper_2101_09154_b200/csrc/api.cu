@@ -722,6 +722,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
   size_t o_ent[kSlots];
   for (int k = 0; k < kSlots; ++k) o_ent[k] = carve(beam ? sizeof(int2) * kEntryStride * chunk : 0);
+  size_t o_frm[kSlots];  // K6a's pulse frames (10 doubles per pulse)
+  for (int k = 0; k < kSlots; ++k) o_frm[k] = carve(beam ? sizeof(double) * 10 * chunk : 0);
   // compact output: per-pulse lengths, call-wide offsets, scan temp, staging
   size_t scan_bytes = 0;
   if (want_offs)
@@ -1058,8 +1060,10 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
                      : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
     mark(ev_t, ts);
     ta.entries = nullptr;
+    ta.frames = nullptr;
     if (beam && mode == 1) {
       ta.entries = reinterpret_cast<int2*>(buf + o_ent[slot]);
+      ta.frames = reinterpret_cast<double*>(buf + o_frm[slot]);
       e = launch_beam(ta, counters, ts);
       ++launches;
     }

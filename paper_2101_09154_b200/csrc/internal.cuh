@@ -110,6 +110,7 @@ struct TraceArgs {
   // beam pre-pass (K6a): per-pulse cone over all subrays; nullptr = K6 starts at the root
   int2* entries;         // [n_pulses][kEntryStride] (K6a writes, K6 reads)
   int entry_max;         // list cap, 2 .. kEntryMax
+  double* frames;        // [n_pulses][10] pulse frames d, u, v + valid flag (K6a writes) or nullptr
   double cone_sin;       // sin of the (widened) cone half-angle: max_i sin(theta_i)
   double beam_k;         // a node is handed to K6 once extent <= beam_k * cone radius
 };

@@ -60,7 +60,9 @@ __device__ __forceinline__ double norm(D3 a) { return __dsqrt_rn(dot(a, a)); }
 __device__ __forceinline__ float safe_inv(float d) {
   // a zero component would give (b - o) * inf = NaN on a box face through the
   // origin; 1e-30 keeps the slab finite and the test conservative
-  return 1.0f / (fabsf(d) < 1e-30f ? copysignf(1e-30f, d) : d);
+  // (__frcp_rn: the correctly rounded reciprocal, the value of 1.0f / x without
+  // the general division sequence)
+  return __frcp_rn(fabsf(d) < 1e-30f ? copysignf(1e-30f, d) : d);
 }
 
 // Slab test of one child box; returns the entry distance (or +inf on a miss).
@@ -553,6 +555,26 @@ __device__ __forceinline__ void traverse_packet4(const TraceArgs& a, unsigned m,
   }
 }
 
+// Pulse frame (R4, R24): d = the direction normalised in fp64 (false
+// and a placeholder frame for a zero / non-finite direction: the pulse reports
+// no hit); a = x if |d_z| > 0.9 else z; u = normalize(a x d); v = d x u.
+__device__ __forceinline__ bool pulse_frame(const float* dir, D3& Dp, D3& U, D3& V) {
+  Dp = d3(__ldg(dir), __ldg(dir + 1), __ldg(dir + 2));
+  const double dn = norm(Dp);
+  bool ok = true;
+  if (!(dn > 0.0) || !isfinite(dn)) {
+    ok = false;
+    Dp = d3(0.0, 0.0, 1.0);  // placeholder
+  } else {
+    Dp = scale(Dp, __drcp_rn(dn));
+  }
+  const D3 ax = fabs(Dp.z) > 0.9 ? d3(1.0, 0.0, 0.0) : d3(0.0, 0.0, 1.0);
+  U = cross(ax, Dp);
+  U = scale(U, __drcp_rn(norm(U)));
+  V = cross(Dp, U);
+  return ok;
+}
+
 // ---- K6a: beam pre-pass.  The subrays of a pulse share its origin and lie in
 // the cone of half-angle max_i theta_i about its axis (R2).  One
 // thread per pulse walks the top of the tree with that cone and lists the
@@ -601,15 +623,19 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= a.n_pulses) return;
   int2* row = a.entries + p * kEntryStride;
-  // the pulse axis exactly as K6 normalises it
-  D3 Dp = d3(__ldg(a.direction + 3 * p), __ldg(a.direction + 3 * p + 1),
-             __ldg(a.direction + 3 * p + 2));
-  const double dn = norm(Dp);
-  if (!(dn > 0.0) || !isfinite(dn)) {  // K6 reports the pulse as hitless
+  // the pulse frame, once per pulse for all its subrays in K6
+  D3 Dp, U, V;
+  const bool ok = pulse_frame(a.direction + 3 * p, Dp, U, V);
+  double2* f = reinterpret_cast<double2*>(a.frames) + p * 5;
+  f[0] = make_double2(Dp.x, Dp.y);
+  f[1] = make_double2(Dp.z, U.x);
+  f[2] = make_double2(U.y, U.z);
+  f[3] = make_double2(V.x, V.y);
+  f[4] = make_double2(V.z, ok ? 1.0 : 0.0);
+  if (!ok) {  // K6 reports the pulse as hitless
     row[0] = make_int2(0, 0);
     return;
   }
-  Dp = scale(Dp, __drcp_rn(dn));
   Cone c;
   const double dd[3] = {Dp.x, Dp.y, Dp.z};
   const double sa = a.cone_sin;
@@ -717,26 +743,24 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   // ---- A2: subray fan-out (R2, R4), fp64
   const float ox = __ldg(a.origin + 3 * p), oy = __ldg(a.origin + 3 * p + 1),
               oz = __ldg(a.origin + 3 * p + 2);
-  D3 Dp = d3(__ldg(a.direction + 3 * p), __ldg(a.direction + 3 * p + 1),
-             __ldg(a.direction + 3 * p + 2));
-  const double dn = norm(Dp);
+  D3 Dp, U, V;
   bool valid = in_range;
-  if (!(dn > 0.0) || !isfinite(dn)) {
-    if (in_range && s == 0) atomicOr(a.err_flag, 1u);
-    valid = false;
-    Dp = d3(0.0, 0.0, 1.0);  // placeholder; the lane reports a miss
+  if (a.frames != nullptr) {  // the pulse frame K6a computed (bitwise the same values)
+    const double2* f = reinterpret_cast<const double2*>(a.frames) + p * 5;
+    const double2 f0 = __ldg(f), f1 = __ldg(f + 1), f2 = __ldg(f + 2), f3 = __ldg(f + 3),
+                  f4 = __ldg(f + 4);
+    Dp = d3(f0.x, f0.y, f1.x);
+    U = d3(f1.y, f2.x, f2.y);
+    V = d3(f3.x, f3.y, f4.x);
+    if (!(f4.y > 0.0)) valid = false;
   } else {
-    Dp = scale(Dp, __drcp_rn(dn));
+    valid = pulse_frame(a.direction + 3 * p, Dp, U, V) && in_range;
   }
+  if (in_range && !valid && s == 0) atomicOr(a.err_flag, 1u);
   if (!PACKET && !valid) {
     a.out[gid] = rec;
     return;
   }
-  // frame (R4): a = x if |d_z| > 0.9 else z; u = normalize(a x d); v = d x u
-  const D3 ax = fabs(Dp.z) > 0.9 ? d3(1.0, 0.0, 0.0) : d3(0.0, 0.0, 1.0);
-  D3 U = cross(ax, Dp);
-  U = scale(U, __drcp_rn(norm(U)));
-  const D3 V = cross(Dp, U);
   const SubrayConst sc = a.sub[s];
   // d_s = cos(theta) d + sin(theta) (cos(phi) u + sin(phi) v)
   const D3 ring = vadd(scale(U, sc.cos_p), scale(V, sc.sin_p));
@@ -985,7 +1009,8 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
 
 cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
   if (a.n_pulses == 0) return cudaSuccess;
-  if (a.entries == nullptr || ref_is_leaf(a.root)) return cudaErrorInvalidValue;
+  if (a.entries == nullptr || a.frames == nullptr || ref_is_leaf(a.root))
+    return cudaErrorInvalidValue;
   const unsigned T = 128;
   const uint64_t blocks = (a.n_pulses + T - 1) / T;
   if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
