@@ -784,30 +784,54 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         else {
           // beam entry lists (K6a): the warp walks, pulse by pulse, the subtrees
           // the pulse's cone reaches, each with the lanes of that pulse; without
-          // lists, one walk from the root with every lane
-          unsigned rem = m;
+          // lists, one walk from the root with every lane.  A warp can hold the subrays of two or more pulses.  Walking the
+          // leader pulse's entries, the lanes of the next pulse join any entry
+          // its own list shares (lane j holds that pulse's entry j; a vote
+          // finds it), and that entry is skipped when the next pulse leads.
+          const int lane = threadIdx.x & 31;
+          unsigned rem = m, skip = 0;
           while (rem) {
-            unsigned mq = rem;
             if (a.entries == nullptr) {
-              traverse_packet<INSTR>(a, mq, a.root, O, D, O32, D32, dl1, ix, iy, iz, t_best,
+              traverse_packet<INSTR>(a, rem, a.root, O, D, O32, D32, dl1, ix, iy, iz, t_best,
                                      best_id, best_k, c_nodes, c_tris, c_f64);
               break;
             }
             const uint32_t pq = __shfl_sync(0xffffffffu, (uint32_t)p, __ffs(rem) - 1);
-            const bool mine_q = valid && (uint32_t)p == pq;
-            mq = __ballot_sync(0xffffffffu, mine_q);
-            rem &= ~mq;
+            const bool in_q = valid && (uint32_t)p == pq;
+            rem &= ~__ballot_sync(0xffffffffu, in_q);
+            bool in_r = false;
+            int2 er = make_int2(0, 0);
+            int cntr = 0;
+            if (rem) {  // the next pulse of the warp
+              const uint32_t pr = __shfl_sync(0xffffffffu, (uint32_t)p, __ffs(rem) - 1);
+              in_r = valid && (uint32_t)p == pr;
+              const int2* rowr = a.entries + (uint64_t)pr * kEntryStride;
+              cntr = __ldg(&rowr->x);
+              if (lane < cntr) er = __ldg(rowr + 1 + lane);
+            }
+            unsigned taken = 0;  // entries of the next pulse walked here
             const int2* row = a.entries + (uint64_t)pq * kEntryStride;
             const int cnt = __ldg(&row->x);
             for (int i = 1; i <= cnt; ++i) {
+              if ((skip >> (i - 1)) & 1u) continue;
               const int2 en = __ldg(row + i);
               // lanes whose nearest hit is already nearer than the box drop out
-              const unsigned me =
-                  __ballot_sync(0xffffffffu, mine_q && !(t_best < (double)__int_as_float(en.y)));
+              bool go = in_q && !(t_best < (double)__int_as_float(en.y));
+              if (cntr) {
+                const unsigned hit = __ballot_sync(0xffffffffu, lane < cntr && er.x == en.x) & ~taken;
+                if (hit) {
+                  const int j = __ffs(hit) - 1;
+                  taken |= 1u << j;
+                  const float tr = __int_as_float(__shfl_sync(0xffffffffu, er.y, j));
+                  go = go || (in_r && !(t_best < (double)tr));
+                }
+              }
+              const unsigned me = __ballot_sync(0xffffffffu, go);
               if (me)
                 traverse_packet<INSTR>(a, me, en.x, O, D, O32, D32, dl1, ix, iy, iz, t_best,
                                        best_id, best_k, c_nodes, c_tris, c_f64);
             }
+            skip = taken;
           }
         }
       }
