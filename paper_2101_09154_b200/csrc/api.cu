@@ -1066,6 +1066,10 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       ta.frames = reinterpret_cast<double*>(buf + o_frm[slot]);
       e = launch_beam(ta, counters, ts);
       ++launches;
+      // measurement only: HELIOS_BEAM_REPEAT=k launches K6a k extra times (its
+      // marginal cost in the pipeline = step time delta / k)
+      if (const char* v = getenv("HELIOS_BEAM_REPEAT"))
+        for (int r = 0; r < atoi(v) && e == cudaSuccess; ++r) e = launch_beam(ta, false, ts);
     }
     if (e == cudaSuccess) e = launch_trace(ta, counters, mode, ts);
     ++trace_launches;

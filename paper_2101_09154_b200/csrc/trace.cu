@@ -23,7 +23,7 @@
 namespace helios {
 namespace {
 
-constexpr float kBoxSlack = 1e-6f;  // >> 4 * 2^-24 relative error of an fp32 slab value
+constexpr float kBoxSlack = 1e-6f;  // >> 5 * 2^-24 relative error of an fp32 slab value
 // lazy culling of popped stack entries compares the stored (already widened)
 // entry distance with t_best rounded to fp32, widened again
 constexpr float kCullSlack = 1.0f + 4.0f * kBoxSlack;
@@ -57,18 +57,28 @@ __device__ __forceinline__ D3 cross(D3 a, D3 b) {
 }
 __device__ __forceinline__ double norm(D3 a) { return __dsqrt_rn(dot(a, a)); }
 
+#ifndef HELIOS_RCP_APPROX
+#define HELIOS_RCP_APPROX 1
+#endif
 __device__ __forceinline__ float safe_inv(float d) {
   // a zero component would give (b - o) * inf = NaN on a box face through the
   // origin; 1e-30 keeps the slab finite and the test conservative
-  // (__frcp_rn: the correctly rounded reciprocal, the value of 1.0f / x without
-  // the general division sequence)
-  return __frcp_rn(fabsf(d) < 1e-30f ? copysignf(1e-30f, d) : d);
+  const float x = fabsf(d) < 1e-30f ? copysignf(1e-30f, d) : d;
+#if HELIOS_RCP_APPROX
+  // rcp.approx: <= 1 ulp (2^-23 relative; |x| >= 1e-30 is never subnormal), so
+  // a slab value carries <= 5 u of relative error, still << kBoxSlack
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+#else
+  return __frcp_rn(x);  // correctly rounded: the value of 1.0f / x
+#endif
 }
 
 // Slab test of one child box; returns the entry distance (or +inf on a miss).
-// t = (b - o) * inv per slab has a purely RELATIVE error <= 4u (u = 2^-24:
-// difference, reciprocal, product, and the fp32 rounding of the fp64
-// direction), whatever the direction (zero components are replaced by
+// t = (b - o) * inv per slab has a purely RELATIVE error <= 5u (u = 2^-24:
+// difference, approximate reciprocal (2u), product, and the fp32 rounding of
+// the fp64 direction), whatever the direction (zero components are replaced by
 // +-1e-30, so no NaN); the interval is widened by the relative slack
 // kBoxSlack >> 4u: the fp32 test never culls a box the fp64 ray enters.
 // (An fma(b, inv, -o*inv) form saves 6 instructions but carries an absolute
@@ -587,35 +597,35 @@ __device__ __forceinline__ bool pulse_frame(const float* dir, D3& Dp, D3& U, D3&
 //
 // Conservative by construction: the listed subtrees cover every node whose
 // box an fp64 subray enters.  The cone is replaced by the box of directions
-// (per axis, the exact component range over the cone, widened by 1e-9): for a
-// box [bl, bh], t * [lo, hi] must meet [bl - o, bh - o] on every axis for
-// some t >= 0 -- the interval form of the slab test, in fp64 with a 1e-12
-// relative slack (each bound carries <= 3 roundings of 2^-53).
+// (per axis, the exact component range over the cone, widened by 1e-9 and
+// rounded outward to fp32): for a box [bl, bh], t * [lo, hi] must meet
+// [bl - o, bh - o] on every axis for some t >= 0 -- the interval form of the
+// slab test.  In fp32: each bound (b - o) * (1 / lo or hi) carries <= 3u of
+// purely relative error (u = 2^-24; difference, correctly rounded reciprocal,
+// product; signs exact), so widening by the relative slack kBoxSlack keeps
+// the test conservative (the same argument as K6's box test).
 struct Cone {
-  double o[3];
-  double rl[3], rh[3];  // 1 / lo, 1 / hi of the direction interval per axis
-  int mode[3];          // 0: lo > 0, 1: hi < 0, 2: interval contains 0
+  float o[3];
+  float rl[3], rh[3];  // 1 / lo, 1 / hi of the direction interval per axis
+  int mode[3];         // 0: lo > 0, 1: hi < 0, 2: interval contains 0
 };
 
-__device__ __forceinline__ bool cone_box(const Cone& c, float lx, float hx, float ly, float hy,
-                                         float lz, float hz, double& t_enter) {
+// entry distance (a lower bound of every subray's entry parameter) or +inf
+__device__ __forceinline__ float cone_box(const Cone& c, float lx, float hx, float ly, float hy,
+                                          float lz, float hz) {
   const float bl[3] = {lx, ly, lz}, bh[3] = {hx, hy, hz};
-  double tlo = 0.0, thi = INFINITY;
+  float tlo = 0.0f, thi = INFINITY;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double e0 = (double)bl[k] - c.o[k], e1 = (double)bh[k] - c.o[k];
-    if (c.mode[k] == 0) {         // t lo <= e1, t hi >= e0
-      tlo = fmax(tlo, e0 * c.rh[k]);
-      thi = fmin(thi, e1 * c.rl[k]);
-    } else if (c.mode[k] == 1) {  // both negative: the inequalities flip
-      tlo = fmax(tlo, e1 * c.rl[k]);
-      thi = fmin(thi, e0 * c.rh[k]);
-    } else {                      // lo < 0 < hi: lower bounds only
-      tlo = fmax(tlo, fmax(e1 * c.rl[k], e0 * c.rh[k]));
-    }
+    // P = e1 / lo, Q = e0 / hi.  mode 0 (lo > 0): t in [Q, P]; mode 1 (hi < 0,
+    // the inequalities flip): t in [P, Q]; mode 2 (lo < 0 < hi): t >= P, Q
+    const float P = (bh[k] - c.o[k]) * c.rl[k], Q = (bl[k] - c.o[k]) * c.rh[k];
+    const int m = c.mode[k];
+    tlo = fmaxf(tlo, m == 0 ? Q : (m == 1 ? P : fmaxf(P, Q)));
+    thi = fminf(thi, m == 0 ? P : (m == 1 ? Q : INFINITY));
   }
-  t_enter = tlo;
-  return tlo <= thi * (1.0 + 1e-12);
+  constexpr float kWiden = (1.0f + kBoxSlack) / (1.0f - kBoxSlack);
+  return tlo <= thi * kWiden ? tlo * (1.0f - kBoxSlack) : INFINITY;
 }
 
 template <bool INSTR>
@@ -641,30 +651,31 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   const double sa = a.cone_sin;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    c.o[k] = (double)__ldg(a.origin + 3 * p + k);
+    c.o[k] = __ldg(a.origin + 3 * p + k);
     // over the cone, component k lies in d_k cos(a) -+ sqrt(1 - d_k^2) sin(a);
     // 1 - cos(a) <= sin^2(a)
     const double h = sqrt(fmax(0.0, 1.0 - dd[k] * dd[k])) * sa + fabs(dd[k]) * sa * sa + 1e-9;
-    double lo = dd[k] - h, hi = dd[k] + h;
-    if (lo > 0.0) {
+    float lo = __double2float_rd(dd[k] - h), hi = __double2float_ru(dd[k] + h);
+    if (lo >= 1e-30f) {
       c.mode[k] = 0;
-    } else if (hi < 0.0) {
+    } else if (hi <= -1e-30f) {
       c.mode[k] = 1;
-    } else {
+    } else {  // contains 0 (or nearly): widen to |lo|, |hi| >= 1e-30 (finite reciprocals)
       c.mode[k] = 2;
-      if (lo == 0.0) lo = -1e-300;  // widening is conservative
-      if (hi == 0.0) hi = 1e-300;
+      lo = fminf(lo, -1e-30f);
+      hi = fmaxf(hi, 1e-30f);
     }
-    c.rl[k] = 1.0 / lo;
-    c.rh[k] = 1.0 / hi;
+    c.rl[k] = __frcp_rn(lo);
+    c.rh[k] = __frcp_rn(hi);
   }
+  const float kr = (float)(a.beam_k * sa);  // hand-over: extent <= beam_k * cone radius
   unsigned long long c_nodes = 0;
   // work stack of (ref, entry distance); bit i of `emit` marks entry i as
   // final (listed when popped).  Invariant: count + sp <= entry_max, so the
   // list never overflows: a node is expanded only while both children still
   // fit, else it is listed whole (coarser, still exact).  Listed distances are
-  // rounded down and shrunk by 1e-6: K6 drops a lane from an entry only when
-  // its nearest hit is strictly nearer than any point of the box.
+  // shrunk by kBoxSlack: K6 drops a lane from an entry only when its nearest
+  // hit is strictly nearer than any point of the box.
   int32_t stk[kEntryMax];
   float stt[kEntryMax];
   uint32_t emit = 0;
@@ -684,18 +695,18 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
     const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
                  rf = __ldg(&nd->ref);
     if (INSTR) ++c_nodes;
-    double t0, t1;
-    const bool h0 = cone_box(c, xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, t0);
-    const bool h1 = cone_box(c, xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, t1);
+    const float t0 = cone_box(c, xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y);
+    const float t1 = cone_box(c, xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w);
+    const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
     const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
     // listed as a whole once the node is small next to the cone's cross-section
     const float e0 = fmaxf(fmaxf(xy0.y - xy0.x, xy0.w - xy0.z), z01.y - z01.x);
     const float e1 = fmaxf(fmaxf(xy1.y - xy1.x, xy1.w - xy1.z), z01.w - z01.z);
-    const bool f0 = (double)e0 <= a.beam_k * t0 * sa, f1 = (double)e1 <= a.beam_k * t1 * sa;
+    const bool f0 = e0 <= kr * t0, f1 = e1 <= kr * t1;
     const bool near0 = !h1 || (h0 && t0 <= t1);
-    auto push = [&](int32_t r, double t, bool f) {
+    auto push = [&](int32_t r, float t, bool f) {
       stk[sp] = r;
-      stt[sp] = __double2float_rd(t) * (1.0f - 1e-6f);
+      stt[sp] = t;
       emit = f ? emit | (1u << sp) : emit & ~(1u << sp);
       ++sp;
     };

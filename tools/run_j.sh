@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/j_build.log 2>&1 || { tail -30 gpurun_out/j_build.log; exit 1; }
+timeout 900 python -m pytest tests -x -q -m gpu -k "beam or parity or edge" 2>&1 | tail -3
+VARIANTS="f32:HELIOS_BEAM=1 rep1:HELIOS_BEAM_REPEAT=1" CFGS="C5 C3 C2" bash tools/env_ab.sh
