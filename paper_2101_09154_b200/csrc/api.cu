@@ -54,6 +54,7 @@ struct helios_scene_s {
     cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
     cudaStream_t trace2;  // second K6 stream: odd chunks, so a chunk's K6 fills the SMs
                           // while the previous one's last wave drains (lazy)
+    cudaStream_t beam[2];  // K6a streams (normal / high priority; HELIOS_BEAM_STREAM, lazy)
     uint64_t* pinned;   // 4 kSlots pinned words: per chunk slot (first, last) offsets of
                         // the packed waveform rows [0, 2 kSlots) and packed returns (lazy)
   };
@@ -62,7 +63,8 @@ struct helios_scene_s {
 
   cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy,
                       cudaStream_t* wave, uint64_t** pinned = nullptr,
-                      cudaStream_t* fit = nullptr, cudaStream_t* trace2 = nullptr) {
+                      cudaStream_t* fit = nullptr, cudaStream_t* trace2 = nullptr,
+                      cudaStream_t* beam = nullptr, int beam_prio = 0) {
     std::lock_guard<std::mutex> g(mu);
     Slot* use = nullptr;
     for (Slot& sl : slots)
@@ -71,8 +73,8 @@ struct helios_scene_s {
         break;
       }
     if (!use) {
-      slots.push_back(
-          Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           {nullptr, nullptr}, nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
@@ -113,6 +115,16 @@ struct helios_scene_s {
         if (e != cudaSuccess) return e;
       }
       *trace2 = use->trace2;
+    }
+    if (beam) {
+      cudaStream_t& b = use->beam[beam_prio ? 1 : 0];
+      if (!b) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi: numerically lowest = highest
+        cudaError_t e = cudaStreamCreateWithPriority(&b, cudaStreamNonBlocking, beam_prio ? hi : lo);
+        if (e != cudaSuccess) return e;
+      }
+      *beam = b;
     }
     if (!use->pinned) {
       cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * kSlots * sizeof(uint64_t));
@@ -155,6 +167,11 @@ struct helios_scene_s {
         cudaStreamSynchronize(sl.trace2);
         cudaStreamDestroy(sl.trace2);
       }
+      for (cudaStream_t b : sl.beam)
+        if (b) {
+          cudaStreamSynchronize(b);
+          cudaStreamDestroy(b);
+        }
       cudaFree(sl.ptr);
       if (sl.pinned) cudaFreeHost(sl.pinned);
     }
@@ -760,8 +777,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   cudaStream_t ts2 = nullptr;  // K6 of odd chunks
   cudaStream_t cpair[2] = {nullptr, nullptr};
   uint64_t* pin = nullptr;  // [slot][first, last] row offsets of a staged compact chunk
+  // K6a stream: 0 = the chunk's trace stream (default, measured best), 1 = own
+  // stream, 2 = own high-priority stream (HELIOS_BEAM_STREAM, A/B)
+  int beam_stream = 0;
+  if (const char* v = getenv("HELIOS_BEAM_STREAM")) beam_stream = atoi(v);
+  cudaStream_t bs = nullptr;
   cudaError_t e = sc->acquire(s, total, &buf, any_staged ? cpair : nullptr, &ws, &pin,
-                              fit ? &fs : nullptr, &ts2);
+                              fit ? &fs : nullptr, &ts2, beam && beam_stream ? &bs : nullptr,
+                              beam_stream == 2);
   cs = cpair[0];
   co = cpair[1];
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
@@ -770,6 +793,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     cudaStreamSynchronize(ws);
     if (fs) cudaStreamSynchronize(fs);
     if (ts2) cudaStreamSynchronize(ts2);
+    if (bs) cudaStreamSynchronize(bs);
     if (cs) cudaStreamSynchronize(cs);
     if (co) cudaStreamSynchronize(co);
     sc->release(s);
@@ -862,6 +886,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     ta.beam_k = 8.0;  // measured (profiles/r01s3_beam_ab.txt)
     if (const char* v = getenv("HELIOS_BEAM_K")) ta.beam_k = atof(v);
     ta.entry_max = kEntryMax;
+    ta.beam_budget = 1 << 30;
+    if (const char* v = getenv("HELIOS_BEAM_BUDGET")) ta.beam_budget = std::max(1, atoi(v));
     if (const char* v = getenv("HELIOS_BEAM_ENTRIES"))
       ta.entry_max = std::max(2, std::min(kEntryMax, atoi(v)));
   }
@@ -908,6 +934,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
               out_done[kSlots] = {};
   cudaEvent_t off_done[kSlots] = {}, cd_done[kSlots] = {};  // packed rows: range known / drained
   cudaEvent_t k7_done[kSlots] = {};                         // fit: K7 done, jobs listed
+  cudaEvent_t b_done[kSlots] = {};                          // K6a done: entry lists ready
   cudaEvent_t roff_done[kSlots] = {}, rd_done[kSlots] = {}; // packed returns: known / drained
   for (int k = 0; k < kSlots && e == cudaSuccess; ++k) {
     e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
@@ -921,6 +948,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cd_done[k], cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess && bs) e = cudaEventCreateWithFlags(&b_done[k], cudaEventDisableTiming);
     if (e == cudaSuccess && any_staged) {
       e = cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
@@ -1010,10 +1038,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   // K6 on two alternating streams (HELIOS_DUAL_TRACE=0/1 forces)
   bool dual_trace = !serial;
   if (const char* v = getenv("HELIOS_DUAL_TRACE")) dual_trace = atoi(v) != 0;
-  if (dual_trace && e == cudaSuccess) {
-    // ts2 must not start before the setup work on `s`
+  if ((dual_trace || bs) && e == cudaSuccess) {
+    // ts2 and bs must not start before the setup work on `s`
     e = cudaEventRecord(t_done[0], s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ts2, t_done[0], 0);
+    if (e == cudaSuccess && dual_trace) e = cudaStreamWaitEvent(ts2, t_done[0], 0);
+    if (e == cudaSuccess && bs) e = cudaStreamWaitEvent(bs, t_done[0], 0);
   }
   if (ws != s) {
     // optional cap on K7's persistent grid while it shares the SMs with K6
@@ -1035,7 +1064,18 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     // K6 of odd chunks on the second trace stream (chunks are independent);
     // voxel scenes stay on one stream (measured: K6 is ALU-bound there)
     const cudaStream_t ts = (dual_trace && (c & 1)) ? ts2 : s;
-    if (any_staged) e = cudaStreamWaitEvent(ts, in_done[slot], 0);
+    // with its own stream, K6a and the chunk's pulse generation only wait for
+    // the chunk's inputs and for the slot's previous user (K7 of chunk c-K,
+    // hence also its K6)
+    const bool use_beam = beam && mode == 1;
+    const cudaStream_t gs = (use_beam && bs) ? bs : ts;
+    if (gs != ts) {
+      if (any_staged) e = cudaStreamWaitEvent(bs, in_done[slot], 0);
+      if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(bs, w_done[slot], 0);
+      if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots)
+        e = cudaStreamWaitEvent(bs, out_done[slot], 0);
+    }
+    if (e == cudaSuccess && any_staged) e = cudaStreamWaitEvent(ts, in_done[slot], 0);
     if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ts, w_done[slot], 0);
     // K6 writes the staged subray-hit slot chunk c-K used: its copy-out (on the
     // D2H stream, not ordered behind this chunk's H2D) must be done
@@ -1044,11 +1084,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     // generated pulses of this chunk (into the slot chunk c-K used: its copy-out
     // must be done when the export is host memory)
     if (e == cudaSuccess && gen) {
-      if (gen_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ts, out_done[slot], 0);
+      if (gen_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(gs, out_done[slot], 0);
       if (e == cudaSuccess)
         e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(arrs[0], slot, b),
                             (float*)dev_ptr(arrs[1], slot, b), (double*)dev_ptr(arrs[2], slot, b),
-                            ts);
+                            gs);
       ++launches;
     }
     if (e != cudaSuccess) break;
@@ -1058,19 +1098,25 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     ta.pulse_base = pulses->pulse_index_base + b;
     ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec[slot])
                      : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
-    mark(ev_t, ts);
     ta.entries = nullptr;
     ta.frames = nullptr;
-    if (beam && mode == 1) {
+    if (use_beam) {
       ta.entries = reinterpret_cast<int2*>(buf + o_ent[slot]);
       ta.frames = reinterpret_cast<double*>(buf + o_frm[slot]);
-      e = launch_beam(ta, counters, ts);
+      mark(ev_t, gs);
+      if (e == cudaSuccess) e = launch_beam(ta, counters, gs);
       ++launches;
       // measurement only: HELIOS_BEAM_REPEAT=k launches K6a k extra times (its
       // marginal cost in the pipeline = step time delta / k)
       if (const char* v = getenv("HELIOS_BEAM_REPEAT"))
-        for (int r = 0; r < atoi(v) && e == cudaSuccess; ++r) e = launch_beam(ta, false, ts);
+        for (int r = 0; r < atoi(v) && e == cudaSuccess; ++r) e = launch_beam(ta, false, gs);
+      mark(ev_t, gs);
+      if (gs != ts) {
+        if (e == cudaSuccess) e = cudaEventRecord(b_done[slot], bs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ts, b_done[slot], 0);
+      }
     }
+    mark(ev_t, ts);
     if (e == cudaSuccess) e = launch_trace(ta, counters, mode, ts);
     ++trace_launches;
     mark(ev_t, ts);
@@ -1239,6 +1285,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (roff_done[k]) cudaEventDestroy(roff_done[k]);
     if (rd_done[k]) cudaEventDestroy(rd_done[k]);
     if (k7_done[k]) cudaEventDestroy(k7_done[k]);
+    if (b_done[k]) cudaEventDestroy(b_done[k]);
   }
   cudaGetLastError();
   cleanup();

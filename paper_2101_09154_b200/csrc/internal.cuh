@@ -113,6 +113,7 @@ struct TraceArgs {
   double* frames;        // [n_pulses][10] pulse frames d, u, v + valid flag (K6a writes) or nullptr
   double cone_sin;       // sin of the (widened) cone half-angle: max_i sin(theta_i)
   double beam_k;         // a node is handed to K6 once extent <= beam_k * cone radius
+  int beam_budget;       // node tests per pulse, after which the rest is listed coarse
 };
 
 // One echo-width fit job (R28), appended by K7, solved by k_fit.

@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
     c.rh[k] = __frcp_rn(hi);
   }
   const float kr = (float)(a.beam_k * sa);  // hand-over: extent <= beam_k * cone radius
-  unsigned long long c_nodes = 0;
+  int visits = 0;
   // work stack of (ref, entry distance); bit i of `emit` marks entry i as
   // final (listed when popped).  Invariant: count + sp <= entry_max, so the
   // list never overflows: a node is expanded only while both children still
@@ -687,14 +687,17 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   while (sp > 0) {
     --sp;
     const int32_t ref = stk[sp];
-    if (((emit >> sp) & 1u) || ref_is_leaf(ref) || cnt + sp + 2 > cap) {
+    // listed: final entries, leaves, nodes whose children would not fit, and
+    // everything left once the walk has spent its node budget (bounds the
+    // walk's latency: K6 walks coarse entries itself)
+    if (((emit >> sp) & 1u) || ref_is_leaf(ref) || cnt + sp + 2 > cap || visits >= a.beam_budget) {
       row[1 + cnt++] = make_int2(ref, __float_as_int(stt[sp]));
       continue;
     }
     const Node* nd = a.nodes + ref;
     const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
                  rf = __ldg(&nd->ref);
-    if (INSTR) ++c_nodes;
+    ++visits;
     const float t0 = cone_box(c, xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y);
     const float t1 = cone_box(c, xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w);
     const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
@@ -722,7 +725,7 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   row[0] = make_int2(cnt, 0);
   if (INSTR) {
     const unsigned mask = __activemask();
-    const unsigned w = __reduce_add_sync(mask, (unsigned)c_nodes);
+    const unsigned w = __reduce_add_sync(mask, (unsigned)visits);
     if ((threadIdx.x & 31) == __ffs(mask) - 1 && w) atomicAdd(a.counters + 7, (unsigned long long)w);
   }
 }
