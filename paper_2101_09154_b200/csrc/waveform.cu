@@ -37,7 +37,20 @@ namespace {
 constexpr int kMaxWarps = 8;
 constexpr int kWCap = 512;    // fp64 bins per warp in shared memory
 constexpr int kAggCap = 64;   // offset groups handled by the grouped path
+constexpr int kGroupCap = kAggCap * 2 / 3;  // sparse groups (8 + 4 B) in the same space
 constexpr size_t kSmemCap = 200 * 1024;
+
+// Absolute bin k_s = floor(2 R / c / (Delta 1e-9)) -- the oracle's two
+// correctly rounded divisions, bit for bit -- at the cost of one multiply:
+// q = 2R * inv_bin (inv_bin = 1 / (c Delta 1e-9)) is within a few ulp of the
+// same exact quotient, so its floor is the oracle's whenever q is farther than
+// 1e-13 q from an integer; only then (never, in practice) the divisions run.
+__device__ __forceinline__ long long bin_of(double range_m, double delta_ns, double inv_bin) {
+  const double q = 2.0 * range_m * inv_bin;
+  const double f = floor(q);
+  if (q - f > 1e-13 * q && (f + 1.0) - q > 1e-13 * q) return (long long)f;
+  return (long long)floor(2.0 * range_m / kC / (delta_ns * 1e-9));
+}
 
 __device__ __forceinline__ long long warp_min_ll(long long v) {
 #pragma unroll
@@ -205,13 +218,14 @@ __global__ void k_support(const helios_subray_hit* __restrict__ rec, uint32_t N,
                           uint64_t* __restrict__ len) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const double inv_bin = 1.0 / (kC * (delta_ns * 1e-9));
   for (uint64_t p = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += warps) {
     const helios_subray_hit* r = rec + p * N;
     long long kmin = LLONG_MAX, kmax_all = -1;
     for (uint32_t s = lane; s < N; s += 32) {
       const helios_subray_hit h = r[s];
       if (h.prim_id != 0xFFFFFFFFu) {
-        const long long k = (long long)floor(2.0 * h.range_m / kC / (delta_ns * 1e-9));
+        const long long k = bin_of(h.range_m, delta_ns, inv_bin);
         kmin = k < kmin ? k : kmin;
       }
     }
@@ -221,7 +235,7 @@ __global__ void k_support(const helios_subray_hit* __restrict__ rec, uint32_t N,
       for (uint32_t s = lane; s < N; s += 32) {
         const helios_subray_hit h = r[s];
         if (h.prim_id != 0xFFFFFFFFu) {
-          const long long o = (long long)floor(2.0 * h.range_m / kC / (delta_ns * 1e-9)) - k0;
+          const long long o = bin_of(h.range_m, delta_ns, inv_bin) - k0;
           if (o < (long long)nb && o > kmax_all) kmax_all = o;
         }
       }
@@ -287,6 +301,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
 
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
   __syncthreads();
+  const double inv_bin = 1.0 / (kC * (a.delta_ns * 1e-9));
 
   for (uint64_t p = (uint64_t)blockIdx.x * nw + warp; p < a.n_pulses;
        p += (uint64_t)gridDim.x * nw) {
@@ -297,7 +312,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
       const helios_subray_hit r = rec[s];
       long long k = -1;
       if (r.prim_id != 0xFFFFFFFFu) {
-        k = (long long)floor(2.0 * r.range_m / kC / (a.delta_ns * 1e-9));
+        k = bin_of(r.range_m, a.delta_ns, inv_bin);
         kmin = k < kmin ? k : kmin;
       }
       off[s] = (int)k;  // absolute bin for now (R < 3e8 m fits an int)
@@ -366,18 +381,53 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
           W[k] = w;
         }
       } else {
-        // wide footprint: per-subray accumulation in subray order
+        // wide footprint (offsets spread over >= kAggCap bins, e.g. a crown and
+        // the ground below it).  Groups: within each 32-subray chunk the lanes
+        // with equal offsets (match_any); the lowest lane sums its members in
+        // subray order.  Groups are kept in (chunk, lane) order and added one
+        // after the other: deterministic.  More than kGroupCap groups (or
+        // none fitting) -> per-subray accumulation in subray order.
+        double* gsum = agg;
+        int* goff = reinterpret_cast<int*>(agg + kGroupCap);
+        int G = 0;
+        for (uint32_t c0 = 0; c0 < N; c0 += 32) {
+          const uint32_t s = c0 + lane;
+          const int o = s < N ? off[s] : -1;
+          const unsigned peers = __match_any_sync(0xffffffffu, o);
+          const bool lead = o >= 0 && (int)(__ffs(peers) - 1) == lane;
+          const unsigned leads = __ballot_sync(0xffffffffu, lead);
+          const int idx = G + __popc(leads & ((1u << lane) - 1u));
+          if (lead && idx < kGroupCap) {
+            double acc = 0.0;
+            for (unsigned b = peers; b; b &= b - 1u) acc += (double)amp[c0 + __ffs(b) - 1];
+            gsum[idx] = acc;
+            goff[idx] = o;
+          }
+          G += __popc(leads);
+        }
         for (uint32_t k = lane; k < S; k += 32) W[k] = 0.0;
         __syncwarp();
-        for (uint32_t s = 0; s < N; ++s) {
-          const int o = off[s];
-          if (o < 0) continue;
-          const double A = (double)amp[s];
-          for (uint32_t j = lane; j < taps; j += 32) {
-            const uint32_t k = (uint32_t)o + j;
-            if (k < S) W[k] += A * ker[j];
+        if (G <= kGroupCap) {
+          for (int g = 0; g < G; ++g) {
+            const uint32_t o = (uint32_t)goff[g];
+            const double A = gsum[g];
+            for (uint32_t j = lane; j < taps; j += 32) {
+              const uint32_t k = o + j;
+              if (k < S) W[k] += A * ker[j];
+            }
+            __syncwarp();
           }
-          __syncwarp();
+        } else {
+          for (uint32_t s = 0; s < N; ++s) {
+            const int o = off[s];
+            if (o < 0) continue;
+            const double A = (double)amp[s];
+            for (uint32_t j = lane; j < taps; j += 32) {
+              const uint32_t k = (uint32_t)o + j;
+              if (k < S) W[k] += A * ker[j];
+            }
+            __syncwarp();
+          }
         }
       }
       __syncwarp();
