@@ -288,7 +288,7 @@ def run_ours(args):
     peak, peak_src = peaks()
     ach_trace = b_trace / (trace_ms / 1e3) / 1e9
     n_trace_launches = max(1, trace_launches)
-    traffic, limiter = None, None
+    traffic, limiter, issue = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(args.config)
@@ -298,6 +298,18 @@ def run_ours(args):
             limiter = {"issue_slots_busy": kt["issue_slots_busy"],
                        "dram_bytes_per_subray": kt["dram_bytes"] / kt["units"],
                        "l1_hit": kt["l1_hit"], "source": tj["source"]}
+            if "warp_inst" in kt:
+                # the bound that binds: SM instruction issue (4 warp instructions
+                # per clock per SM).  Instructions per subray of K6a + K6 from the
+                # ncu capture, scaled to this run's launches and event times.
+                wi = kt["warp_inst"] / kt["units"]
+                sms = torch.cuda.get_device_properties(dev).multi_processor_count
+                mhz = (clk or {}).get("sm_mhz") or 1965.0
+                peak_issue = sms * 4 * mhz * 1e6
+                ach = wi * sub_rank / (trace_ms / 1e3)
+                issue = {"bound": "issue", "achieved": ach / 1e9, "peak": peak_issue / 1e9,
+                         "unit": "G warp-instructions/s", "frac": ach / peak_issue,
+                         "warp_inst_per_subray": wi, "source": tj["source"]}
     except Exception:
         pass
     r1 = (b_ray + b_pulse) / (ms / 1e3) / 1e9 / peak
@@ -451,12 +463,13 @@ def run_ours(args):
                        "fit_echo_width": int(args.fit_echo_width),
                        "waveform_output": args.waveform,
                        "range_noise_sd_m": args.range_noise},
-            "roofline": {"bound": "hbm", "kernel": "k_trace", "achieved": ach_trace,
+            "roofline": {"bound": "hbm", "kernel": "k_beam + k_trace", "achieved": ach_trace,
                          "peak": peak, "unit": "GB/s", "frac": ach_trace / peak,
                          "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": b_trace / n_trace_launches,
                          "avg_launch_ms": trace_ms / n_trace_launches,
                          "ncu_limiter": limiter,
+                         "issue_roofline": issue,
                          "share_of_step": trace_ms / ms if ms > 0 else None,
                          "waveform_share_of_step": wave_ms / ms if ms > 0 else None,
                          "nodes_per_ray": nodes / sub_rank, "node_bytes": node_bytes,
