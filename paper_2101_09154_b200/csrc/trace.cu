@@ -162,6 +162,64 @@ __device__ __forceinline__ bool mt32_definite_miss(const F3& o, const F3& d, flo
   return false;
 }
 
+// The same filter with a third outcome: 2 = a DEFINITE hit (u >= 0, v >= 0,
+// u + v <= 1 and t > 0 each hold beyond the error bound, so the fp64 test
+// accepts it) with t in [tlo, tup]; 1 = decide in fp64; 0 = not a candidate.
+// A definite hit's fp64 evaluation can wait: its interval already bounds the
+// ray's nearest hit from above (packet traversal, deferred decision).
+__device__ __forceinline__ int mt32_classify(const F3& o, const F3& d, float dl1,
+                                             const TriRecord& tr, float t_hi, float& tlo,
+                                             float& tup) {
+  constexpr float kU = 32.0f * 5.9604645e-8f;
+  const F3 v0 = {tr.a.x, tr.a.y, tr.a.z};
+  const F3 e1 = fsub({tr.b.x, tr.b.y, tr.b.z}, v0);
+  const F3 e2 = fsub({tr.c.x, tr.c.y, tr.c.z}, v0);
+  const F3 sv = fsub(o, v0);
+  const float A = l1(e1), B = l1(e2), S = l1(sv);
+  const F3 p = fcross(d, e2);
+  const float det = fdot(e1, p);
+  const float err_det = kU * A * dl1 * B;
+  const float adet = fabsf(det);
+  if (!(adet > err_det)) return 1;  // sign of det uncertain (or NaN): decide in fp64
+  const float sg = det > 0.0f ? 1.0f : -1.0f;
+  const float nu = fdot(sv, p) * sg;
+  const F3 q = fcross(sv, e1);
+  const float nv = fdot(d, q) * sg;
+  const float nt = fdot(e2, q) * sg;
+  const float err_u = kU * S * dl1 * B, err_v = kU * S * A * dl1, err_t = kU * B * S * A;
+  if (nu < -err_u || nv < -err_v || nt < -err_t) return 0;  // u < 0, v < 0, t < 0
+  if (nu - adet > err_u + err_det) return 0;                 // u > 1
+  const float esum = (err_u + err_v + err_det) * 1.0001f;
+  if ((nu + nv) - adet > esum) return 0;                     // u + v > 1
+  if (t_hi < 3.0e38f && nt - t_hi * adet > (err_t + t_hi * err_det) * 1.0001f + 1e-30f) return 0;
+  if (nu >= err_u && nv >= err_v && nt > err_t && (nu + nv) + esum <= adet) {
+    tlo = __fdividef(nt - err_t, adet + err_det) * (1.0f - 1e-6f);
+    tup = __fdividef(nt + err_t, adet - err_det) * (1.0f + 1e-6f);
+    return 2;
+  }
+  return 1;
+}
+
+// Per-lane nearest-hit state of the packet traversal: the exact (fp64
+// decided) nearest so far, at most one deferred definite hit, and `bound`, an
+// fp32 upper bound of the final nearest t (culls boxes, triangles, entries).
+struct HitState {
+  double t_best;
+  uint32_t best_id, best_k;
+  uint32_t def_k;  // deferred definite hit (triangle slot) or kNoTri
+  float def_lo;    // its t interval's lower end
+  float bound;
+};
+constexpr uint32_t kNoTri = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void take_hit(HitState& hs, double t, uint32_t id, uint32_t k) {
+  if (t < hs.t_best || (t == hs.t_best && id < hs.best_id)) {
+    hs.t_best = t;
+    hs.best_id = id;
+    hs.best_k = k;
+  }
+}
+
 __device__ __forceinline__ TriRecord load_tri(const TriRecord* __restrict__ t, uint32_t k) {
   TriRecord r;
   r.a = __ldg(&t[k].a);
@@ -330,8 +388,8 @@ template <bool INSTR>
 __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, int32_t ref,
                                                 const D3& O, const D3& D, const F3& O32,
                                                 const F3& D32, float dl1, float ix, float iy,
-                                                float iz, double& t_best, uint32_t& best_id,
-                                                uint32_t& best_k, unsigned long long& c_nodes,
+                                                float iz, HitState& hs,
+                                                unsigned long long& c_nodes,
                                                 unsigned long long& c_tris,
                                                 unsigned long long& c_f64) {
   const unsigned kFull = 0xffffffffu;
@@ -352,7 +410,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
       ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
       m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
 #if HELIOS_LAZY_CULL
-      m = __ballot_sync(kFull, ((m >> lane) & 1u) && !(tstk[sp] > (float)t_best * kCullSlack));
+      m = __ballot_sync(kFull, ((m >> lane) & 1u) && !(tstk[sp] > hs.bound * kCullSlack));
       if (m) return true;
 #else
       return true;
@@ -364,20 +422,25 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
     if (ref_is_leaf(ref)) {
       if (mine) {
         const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
-        const float t_hi = __double2float_ru(t_best);
         for (uint32_t k = first; k < first + cnt; ++k) {
           const TriRecord tr = load_tri(a.tris, k);
           if (INSTR) ++c_tris;
-          if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
+          float tlo, tup;
+          const int cls = mt32_classify(O32, D32, dl1, tr, hs.bound, tlo, tup);
+          if (cls == 0) continue;
+          // a definite hit is deferred when it is the first, or surely nearer
+          // than the deferred one (which then cannot be the nearest)
+          if (cls == 2 && (hs.def_k == kNoTri || tup < hs.def_lo)) {
+            hs.def_k = k;
+            hs.def_lo = tlo;
+            hs.bound = fminf(hs.bound, tup);
+            continue;
+          }
           if (INSTR) ++c_f64;
           const double t = mt64(O, D, tr);
           if (t > 0.0) {
-            const uint32_t id = __float_as_uint(tr.a.w);
-            if (t < t_best || (t == t_best && id < best_id)) {
-              t_best = t;
-              best_id = id;
-              best_k = k;
-            }
+            take_hit(hs, t, __float_as_uint(tr.a.w), k);
+            hs.bound = fminf(hs.bound, __double2float_ru(t));
           }
         }
       }
@@ -391,7 +454,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
     // outside the mask are masked out of the result -- no divergent branch
 #if HELIOS_PREDICATED_BOX
     if (INSTR && mine) ++c_nodes;
-    const float tb = (float)t_best;
+    const float tb = hs.bound;
     float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy,
                          iz, tb);
     float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy,
@@ -401,7 +464,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
     float t0 = INFINITY, t1 = INFINITY;
     if (mine) {
       if (INSTR) ++c_nodes;
-      const float tb = (float)t_best;
+      const float tb = hs.bound;
       t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy, iz,
                      tb);
       t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy, iz,
@@ -606,8 +669,14 @@ __device__ __forceinline__ bool pulse_frame(const float* dir, D3& Dp, D3& U, D3&
 // the test conservative (the same argument as K6's box test).
 struct Cone {
   float o[3];
-  float rl[3], rh[3];  // 1 / lo, 1 / hi of the direction interval per axis
-  int mode[3];         // 0: lo > 0, 1: hi < 0, 2: interval contains 0
+  // per axis, with P = (bh - o) / lo and Q = (bl - o) / hi (lo, hi: the
+  // direction interval): mode lo > 0 -> t in [Q, P]; hi < 0 (the inequalities
+  // flip) -> t in [P, Q]; lo < 0 < hi -> t >= P, Q.  Branch-free: a lower-bound
+  // term that does not apply gets multiplier 0 (-> 0, harmless under max with
+  // t >= 0); an upper-bound term that does not apply is fma(e, 0, +inf).
+  float lp[3], lq[3];  // lower-bound multipliers of (bh - o) and (bl - o)
+  float up[3], uq[3];  // upper-bound multipliers
+  float cp[3], cq[3];  // upper-bound addends: 0 or +inf
 };
 
 // entry distance (a lower bound of every subray's entry parameter) or +inf
@@ -617,12 +686,9 @@ __device__ __forceinline__ float cone_box(const Cone& c, float lx, float hx, flo
   float tlo = 0.0f, thi = INFINITY;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    // P = e1 / lo, Q = e0 / hi.  mode 0 (lo > 0): t in [Q, P]; mode 1 (hi < 0,
-    // the inequalities flip): t in [P, Q]; mode 2 (lo < 0 < hi): t >= P, Q
-    const float P = (bh[k] - c.o[k]) * c.rl[k], Q = (bl[k] - c.o[k]) * c.rh[k];
-    const int m = c.mode[k];
-    tlo = fmaxf(tlo, m == 0 ? Q : (m == 1 ? P : fmaxf(P, Q)));
-    thi = fminf(thi, m == 0 ? P : (m == 1 ? Q : INFINITY));
+    const float ep = bh[k] - c.o[k], eq = bl[k] - c.o[k];
+    tlo = fmaxf(tlo, fmaxf(ep * c.lp[k], eq * c.lq[k]));
+    thi = fminf(thi, fminf(fmaf(ep, c.up[k], c.cp[k]), fmaf(eq, c.uq[k], c.cq[k])));
   }
   constexpr float kWiden = (1.0f + kBoxSlack) / (1.0f - kBoxSlack);
   return tlo <= thi * kWiden ? tlo * (1.0f - kBoxSlack) : INFINITY;
@@ -656,17 +722,23 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
     // 1 - cos(a) <= sin^2(a)
     const double h = sqrt(fmax(0.0, 1.0 - dd[k] * dd[k])) * sa + fabs(dd[k]) * sa * sa + 1e-9;
     float lo = __double2float_rd(dd[k] - h), hi = __double2float_ru(dd[k] + h);
+    int mode;
     if (lo >= 1e-30f) {
-      c.mode[k] = 0;
+      mode = 0;
     } else if (hi <= -1e-30f) {
-      c.mode[k] = 1;
+      mode = 1;
     } else {  // contains 0 (or nearly): widen to |lo|, |hi| >= 1e-30 (finite reciprocals)
-      c.mode[k] = 2;
+      mode = 2;
       lo = fminf(lo, -1e-30f);
       hi = fmaxf(hi, 1e-30f);
     }
-    c.rl[k] = __frcp_rn(lo);
-    c.rh[k] = __frcp_rn(hi);
+    const float rl = __frcp_rn(lo), rh = __frcp_rn(hi);
+    c.lp[k] = mode == 0 ? 0.0f : rl;
+    c.lq[k] = mode == 1 ? 0.0f : rh;
+    c.up[k] = mode == 0 ? rl : 0.0f;
+    c.cp[k] = mode == 0 ? 0.0f : INFINITY;
+    c.uq[k] = mode == 1 ? rh : 0.0f;
+    c.cq[k] = mode == 1 ? 0.0f : INFINITY;
   }
   const float kr = (float)(a.beam_k * sa);  // hand-over: extent <= beam_k * cone radius
   int visits = 0;
@@ -798,16 +870,24 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
         else {
           // beam entry lists (K6a): the warp walks, pulse by pulse, the subtrees
           // the pulse's cone reaches, each with the lanes of that pulse; without
-          // lists, one walk from the root with every lane.  A warp can hold the subrays of two or more pulses.  Walking the
-          // leader pulse's entries, the lanes of the next pulse join any entry
-          // its own list shares (lane j holds that pulse's entry j; a vote
-          // finds it), and that entry is skipped when the next pulse leads.
+          // lists, one walk from the root with every lane.  A warp can hold the
+          // subrays of two or more pulses.  Walking the leader pulse's entries,
+          // the lanes of the next pulse join any entry its own list shares (lane
+          // j holds that pulse's entry j; a vote finds it), and that entry is
+          // skipped when the next pulse leads.
+          HitState hs;
+          hs.t_best = INFINITY;
+          hs.best_id = 0xFFFFFFFFu;
+          hs.best_k = 0;
+          hs.def_k = kNoTri;
+          hs.def_lo = INFINITY;
+          hs.bound = INFINITY;
           const int lane = threadIdx.x & 31;
           unsigned rem = m, skip = 0;
           while (rem) {
             if (a.entries == nullptr) {
-              traverse_packet<INSTR>(a, rem, a.root, O, D, O32, D32, dl1, ix, iy, iz, t_best,
-                                     best_id, best_k, c_nodes, c_tris, c_f64);
+              traverse_packet<INSTR>(a, rem, a.root, O, D, O32, D32, dl1, ix, iy, iz, hs,
+                                     c_nodes, c_tris, c_f64);
               break;
             }
             const uint32_t pq = __shfl_sync(0xffffffffu, (uint32_t)p, __ffs(rem) - 1);
@@ -830,23 +910,33 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
               if ((skip >> (i - 1)) & 1u) continue;
               const int2 en = __ldg(row + i);
               // lanes whose nearest hit is already nearer than the box drop out
-              bool go = in_q && !(t_best < (double)__int_as_float(en.y));
+              bool go = in_q && !(hs.bound < __int_as_float(en.y));
               if (cntr) {
                 const unsigned hit = __ballot_sync(0xffffffffu, lane < cntr && er.x == en.x) & ~taken;
                 if (hit) {
                   const int j = __ffs(hit) - 1;
                   taken |= 1u << j;
                   const float tr = __int_as_float(__shfl_sync(0xffffffffu, er.y, j));
-                  go = go || (in_r && !(t_best < (double)tr));
+                  go = go || (in_r && !(hs.bound < tr));
                 }
               }
               const unsigned me = __ballot_sync(0xffffffffu, go);
               if (me)
-                traverse_packet<INSTR>(a, me, en.x, O, D, O32, D32, dl1, ix, iy, iz, t_best,
-                                       best_id, best_k, c_nodes, c_tris, c_f64);
+                traverse_packet<INSTR>(a, me, en.x, O, D, O32, D32, dl1, ix, iy, iz, hs,
+                                       c_nodes, c_tris, c_f64);
             }
             skip = taken;
           }
+          // the deferred definite hit is decided last (in step across the warp)
+          if (hs.def_k != kNoTri) {
+            const TriRecord tr = load_tri(a.tris, hs.def_k);
+            if (INSTR) ++c_f64;
+            const double t = mt64(O, D, tr);
+            if (t > 0.0) take_hit(hs, t, __float_as_uint(tr.a.w), hs.def_k);
+          }
+          t_best = hs.t_best;
+          best_id = hs.best_id;
+          best_k = hs.best_k;
         }
       }
     } else {
