@@ -708,8 +708,22 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       gen_staged |= a.gen;
     }
 
-  // chunk so the K6 -> K7 records (16 B per subray) stay L2-resident
+  // beam pre-pass K6a (packet traversal of a tree with internal nodes, beams of
+  // >= 7 subrays); HELIOS_BEAM=0/1 forces, HELIOS_BEAM_K sets the hand-over size
+  // (small scenes: the pre-pass costs more than the few levels it saves; measured on C6)
+  const bool beam_ok = N >= 7 && sc->n_tris > 0 && !ref_is_leaf(sc->bvh.root);
+  bool beam = beam_ok && sc->n_tris >= 65536;
+  if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
+  // Chunk size.  Without the pre-pass: the K6 -> K7 records (16 B per subray)
+  // stay L2-resident.  With it, per-chunk tails (K6a's longest cone walks, K6's
+  // last wave) dominate: chunks of up to kBeamChunkSubrays subrays, balanced
+  // (measured: profiles/r01s3_beam_ab.txt, C3 +33 %, C5 +13 %).
   uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
+  if (beam && n > 0) {
+    constexpr uint64_t kBeamChunkSubrays = 32ull << 20;
+    const uint64_t k = (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays;
+    chunk = std::max(chunk, (n + k - 1) / k);
+  }
   if (const char* v = getenv("HELIOS_CHUNK_PULSES"))  // experiments: chunk size override
     if (atoll(v) >= 1024) chunk = std::min<uint64_t>(n, (uint64_t)atoll(v));
   const bool own_rec = outputs->p_subray_hits == nullptr;
@@ -731,12 +745,6 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (a.staged || (a.gen && !a.user))  // staged, or generated with no export
       for (int k = 0; k < kSlots; ++k) a.off[k] = carve(a.per_pulse * chunk);
   const size_t o_wp = carve(gen ? sizeof(double) * 3 * survey->n_waypoints : 0);
-  // beam pre-pass K6a (packet traversal of a tree with internal nodes, beams of
-  // >= 7 subrays); HELIOS_BEAM=0/1 forces, HELIOS_BEAM_K sets the hand-over size
-  // (small scenes: the pre-pass costs more than the few levels it saves; measured on C6)
-  const bool beam_ok = N >= 7 && sc->n_tris > 0 && !ref_is_leaf(sc->bvh.root);
-  bool beam = beam_ok && sc->n_tris >= 65536;
-  if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
   size_t o_ent[kSlots];
   for (int k = 0; k < kSlots; ++k) o_ent[k] = carve(beam ? sizeof(int2) * kEntryStride * chunk : 0);
   size_t o_frm[kSlots];  // K6a's pulse frames (10 doubles per pulse)
