@@ -71,13 +71,6 @@ __device__ __forceinline__ double warp_max_d(double v) {
   return v;
 }
 
-__device__ __forceinline__ double warp_sum_d(double v) {
-  // xor butterfly: every lane ends with the bitwise-identical sum (fp64 addition
-  // is commutative), so the LM decisions below are warp-uniform.
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // Echo width ("Optionally, a Gaussian may be fitted to the resulting
 // waveform, to get a measure of echo width (i.e. standard deviation of the

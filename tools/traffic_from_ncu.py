@@ -3,10 +3,11 @@
 profiles/traffic.json under the config's key (bench.py reads it for the
 roofline 'traffic', 'ncu_limiter' and 'issue_roofline' fields).
 
-  python tools/traffic_from_ncu.py gpurun_out/x/full.ncu-rep C5 "<source text>"
+  python tools/traffic_from_ncu.py gpurun_out/x/full.ncu-rep C5 "<source text>" [pulses]
 
-Units: K6a + K6 per subray (pulses of the captured chunk x N), K7 per pulse.
-The chunk size follows the library's rule (48 MiB of 16-B subray records).
+Units: K6a + K6 per subray (pulses of the captured launch x N), K7 per pulse.
+`pulses`: pulses per captured launch (default: the library's chunk rule for a
+beam scene, <= 32 Mi subrays, capped by tools/profile_step.py's --batch 100000).
 """
 import csv
 import io
@@ -29,7 +30,7 @@ def scale(unit, v):
     return float(v.replace(",", "")) * f.get(unit, 1)
 
 
-def main(rep, cfg, source):
+def main(rep, cfg, source, pulses=None):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -45,7 +46,7 @@ def main(rep, cfg, source):
             continue
         per[key] = {c: scale(units[idx[c]], r[idx[c]]) for c in COLS}
     N = N_OF[cfg]
-    chunk = max(1024, (48 << 20) // (16 * N))
+    chunk = int(pulses) if pulses else min(100000, (32 << 20) // N)
     subrays = chunk * N
     t = per["k_trace"]
     b = per.get("k_beam", {c: 0.0 for c in COLS})
@@ -83,4 +84,5 @@ def main(rep, cfg, source):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else sys.argv[1])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else sys.argv[1],
+         sys.argv[4] if len(sys.argv) > 4 else None)
