@@ -98,7 +98,15 @@ struct helios_scene_s {
       copy[1] = use->copy_out;
     }
     if (!use->wave) {
-      cudaError_t e = cudaStreamCreateWithFlags(&use->wave, cudaStreamNonBlocking);
+      // K7 (and the packed-output scans, fits and copies it feeds) at high
+      // priority: its blocks are scheduled ahead of the queued blocks of the
+      // next chunks' K6 grids, so a chunk's outputs do not wait for them to
+      // drain (HELIOS_WAVE_PRIO=0: normal priority, A/B)
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      int prio = hi;
+      if (const char* v = getenv("HELIOS_WAVE_PRIO")) prio = atoi(v) ? hi : lo;
+      cudaError_t e = cudaStreamCreateWithPriority(&use->wave, cudaStreamNonBlocking, prio);
       if (e != cudaSuccess) return e;
     }
     *wave = use->wave;
@@ -721,7 +729,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
   if (beam && n > 0) {
     constexpr uint64_t kBeamChunkSubrays = 32ull << 20;
-    const uint64_t k = (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays;
+    uint64_t k = (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays;
+    // host outputs: at least a few chunks, so copy-outs overlap later chunks'
+    // kernels (HELIOS_STAGED_MIN_CHUNKS, default 4)
+    if (any_staged) {
+      uint64_t kmin = 4;
+      if (const char* v = getenv("HELIOS_STAGED_MIN_CHUNKS")) kmin = std::max(1, atoi(v));
+      k = std::max(k, kmin);
+    }
     chunk = std::max(chunk, (n + k - 1) / k);
   }
   if (const char* v = getenv("HELIOS_CHUNK_PULSES"))  // experiments: chunk size override
@@ -989,6 +1004,19 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const bool host_trace = getenv("HELIOS_TRACE_HOST") != nullptr;
   double host_wait_ms = 0.0;
   const double call_t0 = host_trace ? now_ms() : 0.0;
+  // HELIOS_TRACE_HOST: device-side spans of the copy-out stream, the trace
+  // streams and K7 (timing events; reported relative to a start event on s)
+  std::vector<std::pair<char, cudaEvent_t>> tev;
+  cudaEvent_t tev0 = nullptr;
+  auto tmark = [&](char tag, cudaStream_t st) {
+    if (!host_trace) return;
+    cudaEvent_t x;
+    if (cudaEventCreate(&x) == cudaSuccess) {
+      cudaEventRecord(x, st);
+      tev.emplace_back(tag, x);
+    }
+  };
+  if (host_trace && cudaEventCreate(&tev0) == cudaSuccess) cudaEventRecord(tev0, s);
   // staged compact rows of chunk c: the host learns the chunk's offset range
   // from the pinned mirror (written on `s` right after the chunk's scan), then
   // queues the copy behind K7(c) on the copy stream.  Called one iteration
@@ -1002,10 +1030,28 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (r != cudaSuccess) return r;
     const uint64_t first = pin[2 * sl], last = std::min(pin[2 * sl + 1], cap);
     r = cudaStreamWaitEvent(co, w_done[sl], 0);
+    tmark('c', co);
     if (r == cudaSuccess && last > first)
       r = cudaMemcpyAsync(outputs->p_wf_compact + first, buf + o_cst[sl],
                           sizeof(float) * (last - first), cudaMemcpyDeviceToHost, co);
+    tmark('C', co);
     if (r == cudaSuccess) r = cudaEventRecord(cd_done[sl], co);
+    return r;
+  };
+
+  // staged fixed-size outputs of chunk c (counts, first bins, return slots,
+  // dense rows, subray hits, beam export) -> host; out_done marks the slot free
+  auto drain_fixed = [&](uint64_t c) -> cudaError_t {
+    const int sl = (int)(c % kSlots);
+    const uint64_t b = c * chunk, m = std::min(chunk, n - b);
+    cudaError_t r = cudaStreamWaitEvent(co, w_done[sl], 0);
+    tmark('f', co);
+    for (const Arr& a : arrs)
+      if (r == cudaSuccess && a.staged && !a.in)
+        r = cudaMemcpyAsync((char*)a.user + a.per_pulse * b, buf + a.off[sl], a.per_pulse * m,
+                            cudaMemcpyDeviceToHost, co);
+    tmark('F', co);
+    if (r == cudaSuccess) r = cudaEventRecord(out_done[sl], co);
     return r;
   };
 
@@ -1125,7 +1171,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       }
     }
     mark(ev_t, ts);
+    tmark('t', ts);
     if (e == cudaSuccess) e = launch_trace(ta, counters, mode, ts);
+    tmark('T', ts);
     ++trace_launches;
     mark(ev_t, ts);
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], ts);
@@ -1170,7 +1218,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       if (e == cudaSuccess) e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
     }
     mark(ev_w, ws);
+    tmark('w', ws);
     if (e == cudaSuccess) e = launch_waveform(wa, plan, d_wscratch, ws);
+    tmark('W', ws);
     if (e == cudaSuccess && wa.noise_sd > 0.0) {
       e = launch_range_noise(wa, ws);
       ++launches;
@@ -1212,8 +1262,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     // packed copy-outs run kSlots-1 chunks behind, so the host never blocks on
     // a chunk whose K7 may still be queued behind the K6 it just enqueued
     constexpr uint64_t kLag = kSlots - 1;
+    // (the fixed-size staged outputs too: all copy-outs of a chunk leave in
+    // one go, in chunk order, so none queues behind a later chunk's K7)
     if (e == cudaSuccess && compact_staged && c >= kLag) e = drain_compact(c - kLag);
     if (e == cudaSuccess && packed_staged && c >= kLag) e = drain_returns(c - kLag);
+    if (e == cudaSuccess && any_staged && c >= kLag) e = drain_fixed(c - kLag);
     if (e != cudaSuccess || !any_staged) continue;
     // prefetch the next chunk's inputs into the other slot once chunk c-1's
     // kernels (K6 reads origin/direction, K7 reads time) are done with it
@@ -1222,18 +1275,12 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       if (c + 1 >= (uint64_t)kSlots) e = cudaStreamWaitEvent(cs, w_done[nslot], 0);
       if (e == cudaSuccess) e = copy_in(b + chunk, nslot);
     }
-    // drain this chunk's outputs
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(co, w_done[slot], 0);
-    for (const Arr& a : arrs)
-      if (e == cudaSuccess && a.staged && !a.in)
-        e = cudaMemcpyAsync((char*)a.user + a.per_pulse * b, buf + a.off[slot], a.per_pulse * m,
-                            cudaMemcpyDeviceToHost, co);
-    if (e == cudaSuccess) e = cudaEventRecord(out_done[slot], co);
   }
   for (uint64_t c = n_chunks > (uint64_t)(kSlots - 1) ? n_chunks - (kSlots - 1) : 0;
        c < n_chunks && e == cudaSuccess; ++c) {
     if (compact_staged) e = drain_compact(c);
     if (e == cudaSuccess && packed_staged) e = drain_returns(c);
+    if (e == cudaSuccess && any_staged) e = drain_fixed(c);
   }
   // call-wide offsets to the caller (device or host memory)
   if (e == cudaSuccess && want_offs) {
@@ -1269,6 +1316,19 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (e == cudaSuccess && co) e = cudaStreamSynchronize(co);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws);
   if (e == cudaSuccess && fs) e = cudaStreamSynchronize(fs);
+  if (host_trace && tev0) {
+    std::string line;
+    for (auto& pr : tev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev0, pr.second);
+      char b[32];
+      snprintf(b, sizeof b, " %c%.2f", pr.first, ms);
+      line += b;
+      cudaEventDestroy(pr.second);
+    }
+    cudaEventDestroy(tev0);
+    fprintf(stderr, "helios_simulate spans (ms from call start; t/T K6, w/W K7, f/F fixed copy-out, c/C rows copy-out):%s\n", line.c_str());
+  }
   if (host_trace)
     fprintf(stderr, "helios_simulate: %llu pulses, %llu chunks, host %.3f ms, blocked in drains %.3f ms\n",
             (unsigned long long)n, (unsigned long long)n_chunks, now_ms() - call_t0, host_wait_ms);
