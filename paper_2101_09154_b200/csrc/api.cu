@@ -741,6 +741,19 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   }
   if (const char* v = getenv("HELIOS_CHUNK_PULSES"))  // experiments: chunk size override
     if (atoll(v) >= 1024) chunk = std::min<uint64_t>(n, (uint64_t)atoll(v));
+  // chunk c covers pulses [cstart[c], cstart[c+1]).  Option: split the last
+  // chunk so its K7, which nothing overlaps, is short (HELIOS_TAIL_FRAC of it
+  // last; measured: C5 +2 %, C3 -6 % -> off by default)
+  std::vector<uint64_t> cstart;
+  for (uint64_t b = 0; b < n; b += chunk) cstart.push_back(b);
+  if (beam && cstart.size() >= 2) {
+    double f = 0.0;
+    if (const char* v = getenv("HELIOS_TAIL_FRAC")) f = atof(v);
+    const uint64_t last = cstart.back(), len = n - last;
+    const uint64_t tail = (uint64_t)(f * (double)len);
+    if (f > 0.0 && tail >= 4096 && tail < len) cstart.push_back(n - tail);
+  }
+  cstart.push_back(n);
   const bool own_rec = outputs->p_subray_hits == nullptr;
   size_t total = 0;
   auto carve = [&](size_t bytes) {
@@ -989,8 +1002,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (a.staged) return buf + a.off[slot];
     return (char*)a.user + a.per_pulse * b;
   };
-  auto copy_in = [&](uint64_t b, int slot) -> cudaError_t {
-    const uint64_t m = std::min(chunk, n - b);
+  auto copy_in = [&](uint64_t c, int slot) -> cudaError_t {
+    const uint64_t b = cstart[c], m = cstart[c + 1] - b;
     for (const Arr& a : arrs)
       if (a.staged && a.in) {
         cudaError_t r = cudaMemcpyAsync(buf + a.off[slot], (const char*)a.user + a.per_pulse * b,
@@ -1043,7 +1056,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   // dense rows, subray hits, beam export) -> host; out_done marks the slot free
   auto drain_fixed = [&](uint64_t c) -> cudaError_t {
     const int sl = (int)(c % kSlots);
-    const uint64_t b = c * chunk, m = std::min(chunk, n - b);
+    const uint64_t b = cstart[c], m = cstart[c + 1] - b;
     cudaError_t r = cudaStreamWaitEvent(co, w_done[sl], 0);
     tmark('f', co);
     for (const Arr& a : arrs)
@@ -1109,11 +1122,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (bps > 0) plan.grid_cap = (uint32_t)(sms * bps);
   }
   uint32_t launches = 0, trace_launches = 0;
-  const uint64_t n_chunks = (n + chunk - 1) / chunk;
+  const uint64_t n_chunks = cstart.size() - 1;
   if (any_staged && e == cudaSuccess) e = copy_in(0, 0);
   for (uint64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
-    const uint64_t b = c * chunk;
-    const uint64_t m = std::min(chunk, n - b);
+    const uint64_t b = cstart[c];
+    const uint64_t m = cstart[c + 1] - b;
     const int slot = (int)(c % kSlots);
     // K6 of odd chunks on the second trace stream (chunks are independent);
     // voxel scenes stay on one stream (measured: K6 is ALU-bound there)
@@ -1273,7 +1286,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (c + 1 < n_chunks) {
       const int nslot = (int)((c + 1) % kSlots);
       if (c + 1 >= (uint64_t)kSlots) e = cudaStreamWaitEvent(cs, w_done[nslot], 0);
-      if (e == cudaSuccess) e = copy_in(b + chunk, nslot);
+      if (e == cudaSuccess) e = copy_in(c + 1, nslot);
     }
   }
   for (uint64_t c = n_chunks > (uint64_t)(kSlots - 1) ? n_chunks - (kSlots - 1) : 0;
