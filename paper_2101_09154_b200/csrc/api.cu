@@ -294,7 +294,48 @@ std::vector<SubrayConst> subray_table(uint32_t count, double beta, Pattern pt) {
     const double theta = (double)i / (double)pt.q * beta;  // R2
     for (int j = 0; j < n; ++j) push(theta, 2.0 * kPi * (double)j / (double)n);  // R4
   }
+  for (uint32_t s = 0; s < (uint32_t)t.size(); ++s) t[s].index = s;
   return t;
+}
+
+// Lane order of the subrays in K6 (a permutation of the table; each entry
+// keeps its index s, which alone defines the subray: directions, Philox
+// counters and output slots are unchanged).  R4's order runs ring by ring, so
+// any 32 consecutive subrays of a 91-subray pulse span a whole annulus and
+// their warp walks every leaf of the footprint.  Ordered along a Hilbert curve
+// over the footprint disc instead, consecutive subrays form compact patches:
+// each warp visits the leaves of its patch only.
+uint32_t hilbert_d(uint32_t n, uint32_t x, uint32_t y) {
+  uint32_t d = 0;
+  for (uint32_t s = n / 2; s > 0; s /= 2) {
+    const uint32_t rx = (x & s) > 0, ry = (y & s) > 0;
+    d += s * s * ((3 * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = n - 1 - x;
+        y = n - 1 - y;
+      }
+      std::swap(x, y);
+    }
+  }
+  return d;
+}
+std::vector<SubrayConst> lane_order(const std::vector<SubrayConst>& t) {
+  double rmax = 0.0;
+  for (const SubrayConst& c : t) rmax = std::max(rmax, c.sin_t);
+  std::vector<std::pair<uint32_t, uint32_t>> key;
+  const uint32_t G = 256;
+  for (const SubrayConst& c : t) {
+    const double x = rmax > 0.0 ? c.sin_t * c.cos_p / rmax : 0.0;  // [-1, 1]
+    const double y = rmax > 0.0 ? c.sin_t * c.sin_p / rmax : 0.0;
+    const uint32_t gx = std::min(G - 1, (uint32_t)((x + 1.0) * 0.5 * G));
+    const uint32_t gy = std::min(G - 1, (uint32_t)((y + 1.0) * 0.5 * G));
+    key.emplace_back(hilbert_d(G, gx, gy), c.index);
+  }
+  std::stable_sort(key.begin(), key.end());
+  std::vector<SubrayConst> o;
+  for (const auto& k : key) o.push_back(t[k.second]);
+  return o;
 }
 
 struct Derived {
@@ -678,6 +719,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
 
   // ---- host tables
   const std::vector<SubrayConst> tab = subray_table(N, params->divergence_rad, d.pt);
+  std::vector<SubrayConst> lanes;  // K6's lane order of tab (set below)
   const double beta = params->divergence_rad;
   const double K = params->efficiency * params->receiver_diameter_m * params->receiver_diameter_m /
                    (4.0 * kPi * beta * beta);  // Eq. 7 (R14)
@@ -839,7 +881,13 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   unsigned* d_err = reinterpret_cast<unsigned*>(buf + o_err);
   unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(buf + o_cnt);
   double* d_wscratch = reinterpret_cast<double*>(buf + o_ws);
-  e = cudaMemcpyAsync(d_tab, tab.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
+  {
+    // K6's lane order (HELIOS_SUBRAY_ORDER=0: the table order of R4, A/B)
+    bool hil = true;
+    if (const char* v = getenv("HELIOS_SUBRAY_ORDER")) hil = atoi(v) != 0;
+    lanes = hil ? lane_order(tab) : tab;
+  }
+  e = cudaMemcpyAsync(d_tab, lanes.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_ker, d.kernel.data(), sizeof(double) * d.taps, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, sizeof(unsigned), s);

@@ -72,8 +72,11 @@ struct SubrayConst {
   double cos_p;     // cos(phi)
   double sin_p;     // sin(phi)
   double w_far;     // far-field weight exp(-2 sin^2 theta / tan^2 beta) (R5)
-  double pad_[3];
+  uint32_t index;   // the subray's index s (R4 order: Philox counter word, output slot)
+  uint32_t pad32_;
+  double pad_[2];
 };
+static_assert(sizeof(SubrayConst) == 64, "SubrayConst layout");
 
 // Everything a trace launch needs, passed by value (kernel parameter space).
 struct TraceArgs {

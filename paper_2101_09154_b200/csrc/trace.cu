@@ -818,7 +818,12 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   // one launch covers < 2^32 subrays (launch_trace checks): 32-bit division
   const uint32_t g32 = (uint32_t)g;
   const uint64_t p = g32 / a.N;
-  const uint32_t s = g32 - (uint32_t)p * a.N;
+  // lane position j of the pulse -> subray s (the table is in K6's lane order,
+  // each entry carries its index; the record goes to slot s)
+  const uint32_t j = g32 - (uint32_t)p * a.N;
+  const SubrayConst sc = a.sub[j];
+  const uint32_t s = sc.index;
+  helios_subray_hit* const out_rec = a.out + p * a.N + s;
   unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;
 
   helios_subray_hit rec;
@@ -844,10 +849,9 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
   }
   if (in_range && !valid && s == 0) atomicOr(a.err_flag, 1u);
   if (!PACKET && !valid) {
-    a.out[gid] = rec;
+    *out_rec = rec;
     return;
   }
-  const SubrayConst sc = a.sub[s];
   // d_s = cos(theta) d + sin(theta) (cos(phi) u + sin(phi) v)
   const D3 ring = vadd(scale(U, sc.cos_p), scale(V, sc.sin_p));
   const D3 D = vadd(scale(Dp, sc.cos_t), scale(ring, sc.sin_t));
@@ -945,7 +949,7 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
     }
   }
   if (!valid) {
-    if (in_range) a.out[gid] = rec;
+    if (in_range) *out_rec = rec;
     return;
   }
 
@@ -1117,7 +1121,7 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
     rec.amplitude = (float)(a.K * sig_eff * I / (R * R * R * R));
     rec.prim_id = pid;
   }
-  a.out[gid] = rec;
+  *out_rec = rec;
 
   if (INSTR) {
     // warp-aggregated (one atomic per warp and counter; per-thread counts < 2^32)
