@@ -1109,7 +1109,10 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
     const TriRecord tr = load_tri(a.tris, best_k);
     const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
     const D3 n = cross(sub(d3(tr.b.x, tr.b.y, tr.b.z), v0), sub(d3(tr.c.x, tr.c.y, tr.c.z), v0));
-    const double cos_inc = __ddiv_rn(fabs(dot(n, D)), mul(norm(n), norm(D)));
+    // |n.d| / (|n| |d|): only the amplitude depends on it (tolerance 1e-4
+    // relative), so |d| = 1 (+-1e-16) is dropped and 1/|n| is the fp64 rsqrt
+    // (<= 2 ulp) instead of a square root and a division
+    const double cos_inc = fabs(dot(n, D)) * rsqrt(dot(n, n));
     R = t_best;
     sig_eff = (double)tr.b.w * cos_inc;
     pid = best_id;
@@ -1126,7 +1129,8 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
       I = a.I0 * sc.w_far;
     }
     rec.range_m = R;
-    rec.amplitude = (float)(a.K * sig_eff * I / (R * R * R * R));
+    const double r2 = R * R;
+    rec.amplitude = (float)(a.K * sig_eff * I * __drcp_rn(r2 * r2));
     rec.prim_id = pid;
   }
   *out_rec = rec;
