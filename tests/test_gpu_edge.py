@@ -235,7 +235,7 @@ def test_invariants_on_a_full_reduced_run():
     assert (g["wf_first_bin"] >= 0).mean() > 0.9
 
 
-@pytest.mark.parametrize("N,beta", [(19, 1e-3), (91, 5e-4), (37, 1e-7)])
+@pytest.mark.parametrize("N,beta", [(19, 1e-3), (91, 5e-4), (37, 1e-7), (37, 0.05), (7, 0.099)])
 def test_beam_prepass_axis_aligned_and_grazing(N, beta, monkeypatch):
     """K6a's interval cone test on its hard cases: pulse axes exactly along
     +-x, +-y, +-z (direction intervals straddling 0 on two axes), axis-plane
