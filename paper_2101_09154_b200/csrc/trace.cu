@@ -170,10 +170,14 @@ __device__ __forceinline__ bool mt32_definite_miss(const F3& o, const F3& d, flo
 __device__ __forceinline__ int mt32_classify(const F3& o, const F3& d, float dl1,
                                              const TriRecord& tr, float t_hi, float& tlo,
                                              float& tup) {
-  // the same bounds as mt32_definite_miss (32u slack on 8u), factored as
-  // (kU |d|_1)(|e1|_1 |e2|_1) etc., and tested as soon as each value exists:
-  // the coherent lanes of a packet mostly leave together
-  constexpr float kU = 32.0f * 5.9604645e-8f;
+  // the bounds of mt32_definite_miss, factored as (kU |d|_1)(|e1|_1 |e2|_1)
+  // etc., and tested as soon as each value exists (the coherent lanes of a
+  // packet mostly leave together).  kU = HELIOS_FILTER_U x u on the 8u
+  // first-order bound (default 32: 4x slack)
+#ifndef HELIOS_FILTER_U
+#define HELIOS_FILTER_U 32.0f
+#endif
+  constexpr float kU = HELIOS_FILTER_U * 5.9604645e-8f;
   const F3 v0 = {tr.a.x, tr.a.y, tr.a.z};
   const F3 e1 = fsub({tr.b.x, tr.b.y, tr.b.z}, v0);
   const F3 e2 = fsub({tr.c.x, tr.c.y, tr.c.z}, v0);
