@@ -337,8 +337,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
       if (maxoff < kAggCap) {
         // amplitude per offset group.  Few groups (G <= 16, the usual case):
         // lane (o, c) sums group o over subray chunk c of C = 32 / G chunks,
-        // then lane o adds its chunks' partials in chunk order; else one lane
-        // per group over all subrays.  Either way a fixed order: deterministic.
+        // then a fixed binary tree over the chunks combines the partials; else
+        // one lane per group over all subrays.  Either way a fixed order:
+        // deterministic.
         const int G = maxoff + 1;
         if (G <= 16) {
           const int C = 32 / G, o = lane % G, c = lane / G;
@@ -348,15 +349,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
             const uint32_t s1 = (uint32_t)((N * (uint32_t)(c + 1)) / (uint32_t)C);
             for (uint32_t s = s0; s < s1; ++s)
               if (off[s] == o) acc += (double)amp[s];
-            agg[c * G + o] = acc;  // C * G <= 32 <= kAggCap
           }
-          __syncwarp();
-          if (lane < G) {
-            double sum = agg[lane];
-            for (int q = 1; q < C; ++q) sum += agg[q * G + lane];
-            acc = sum;
+          // chunk partials of each group combined by a fixed binary tree over
+          // the chunks (lane c G + o takes lane (c + st) G + o): deterministic
+          for (int st = 1; st < C; st <<= 1) {
+            const double other = __shfl_down_sync(0xffffffffu, acc, st * G);
+            if (c < C && (c & (2 * st - 1)) == 0 && c + st < C) acc += other;
           }
-          __syncwarp();
           if (lane < G) agg[lane] = acc;
         } else {
           for (int o = lane; o <= maxoff; o += 32) {
