@@ -769,7 +769,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   // last wave) dominate: chunks of up to kBeamChunkSubrays subrays, balanced
   // (measured: profiles/r01s3_beam_ab.txt, C3 +33 %, C5 +13 %).
   uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
-  if (beam && n > 0) {
+  // (the same for voxel scenes, whose K6 and K7 run serially: C4 +7 %)
+  if ((beam || sc->d_pad != nullptr) && n > 0) {
     constexpr uint64_t kBeamChunkSubrays = 32ull << 20;
     uint64_t k = (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays;
     // host outputs: at least a few chunks, so copy-outs overlap later chunks'
