@@ -538,19 +538,19 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a
       if (lane < head) row[lane] = lane < S ? (float)W[lane] : 0.0f;
       const uint32_t nvec = (nb - head) >> 2;
       float4* body = reinterpret_cast<float4*>(row + head);
-      for (uint32_t q = lane; q < nvec; q += 32) {
+      // vectors touching the support, then a plain zero-store loop
+      const uint32_t qs = S > head ? min(nvec, (S - head + 3u) >> 2) : 0u;
+      for (uint32_t q = lane; q < qs; q += 32) {
         const uint32_t k = head + 4 * q;
         float4 v;
-        if (k >= S) {
-          v = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-          v.x = (float)W[k];
-          v.y = k + 1 < S ? (float)W[k + 1] : 0.0f;
-          v.z = k + 2 < S ? (float)W[k + 2] : 0.0f;
-          v.w = k + 3 < S ? (float)W[k + 3] : 0.0f;
-        }
+        v.x = (float)W[k];
+        v.y = k + 1 < S ? (float)W[k + 1] : 0.0f;
+        v.z = k + 2 < S ? (float)W[k + 2] : 0.0f;
+        v.w = k + 3 < S ? (float)W[k + 3] : 0.0f;
         body[q] = v;
       }
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t q = qs + lane; q < nvec; q += 32) body[q] = z4;
       const uint32_t t0 = head + 4 * nvec;
       if (t0 + lane < nb) row[t0 + lane] = t0 + lane < S ? (float)W[t0 + lane] : 0.0f;
     }
