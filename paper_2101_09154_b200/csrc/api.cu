@@ -789,6 +789,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   // last; measured: C5 +2 %, C3 -6 % -> off by default)
   std::vector<uint64_t> cstart;
   for (uint64_t b = 0; b < n; b += chunk) cstart.push_back(b);
+  // option: a short first chunk (HELIOS_HEAD_FRAC of a chunk), so the first
+  // K6 starts after a short K6a (A/B)
+  if (beam && cstart.size() >= 2) {
+    double f = 0.0;
+    if (const char* v = getenv("HELIOS_HEAD_FRAC")) f = atof(v);
+    const uint64_t head = (uint64_t)(f * (double)chunk);
+    if (f > 0.0 && head >= 4096 && head < chunk) cstart.insert(cstart.begin() + 1, head);
+  }
   if (beam && cstart.size() >= 2) {
     double f = 0.0;
     if (const char* v = getenv("HELIOS_TAIL_FRAC")) f = atof(v);
