@@ -300,16 +300,22 @@ def run_ours(args):
                        "l1_hit": kt["l1_hit"], "source": tj["source"]}
             if "warp_inst" in kt:
                 # the bound that binds: SM instruction issue (4 warp instructions
-                # per clock per SM).  Instructions per subray of K6a + K6 from the
-                # ncu capture, scaled to this run's launches and event times.
+                # per clock per SM).  Warp instructions per subray of K6a + K6 and
+                # per pulse of K7 from the ncu capture, times this step's subrays
+                # and pulses, over the step time (the kernels overlap on several
+                # streams, so the whole step is the unit)
                 wi = kt["warp_inst"] / kt["units"]
+                kw = tj.get("k_waveform", {})
+                wp = kw["warp_inst"] / kw["units"] if "warp_inst" in kw else 0.0
                 sms = torch.cuda.get_device_properties(dev).multi_processor_count
                 mhz = (clk or {}).get("sm_mhz") or 1965.0
                 peak_issue = sms * 4 * mhz * 1e6
-                ach = wi * sub_rank / (trace_ms / 1e3)
-                issue = {"bound": "issue", "achieved": ach / 1e9, "peak": peak_issue / 1e9,
+                ach = (wi * sub_rank + wp * B * args.steps) / (ms / 1e3)
+                issue = {"bound": "issue", "kernel": "k_beam + k_trace + k_waveform (whole step)",
+                         "achieved": ach / 1e9, "peak": peak_issue / 1e9,
                          "unit": "G warp-instructions/s", "frac": ach / peak_issue,
-                         "warp_inst_per_subray": wi, "source": tj["source"]}
+                         "warp_inst_per_subray": wi, "waveform_warp_inst_per_pulse": wp,
+                         "source": tj["source"]}
     except Exception:
         pass
     r1 = (b_ray + b_pulse) / (ms / 1e3) / 1e9 / peak
