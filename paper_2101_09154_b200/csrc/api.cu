@@ -766,13 +766,16 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
   // Chunk size.  Without the pre-pass: the K6 -> K7 records (16 B per subray)
   // stay L2-resident.  With it, per-chunk tails (K6a's longest cone walks, K6's
-  // last wave) dominate: chunks of up to kBeamChunkSubrays subrays, balanced
+  // last wave) dominate: few chunks of up to kBeamChunkSubrays subrays, balanced
   // (measured: profiles/r01s3_beam_ab.txt, C3 +33 %, C5 +13 %).
   uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
   // (the same for voxel scenes, whose K6 and K7 run serially: C4 +7 %)
   if ((beam || sc->d_pad != nullptr) && n > 0) {
-    constexpr uint64_t kBeamChunkSubrays = 32ull << 20;
-    uint64_t k = (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays;
+    constexpr uint64_t kBeamChunkSubrays = 64ull << 20;
+    // at least 2 chunks (K7 of the first overlaps K6 of the second); measured
+    // per 1M-pulse call: C5 1/2/3 chunks 7361/7214/7135, C3 2 best (9300),
+    // C2 2 best (6703) -- profiles/r01s3_beam_ab.txt item 27
+    uint64_t k = std::max<uint64_t>(2, (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
     // host outputs: at least a few chunks, so copy-outs overlap later chunks'
     // kernels (HELIOS_STAGED_MIN_CHUNKS, default 4)
     if (any_staged) {
