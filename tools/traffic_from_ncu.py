@@ -7,7 +7,7 @@ roofline 'traffic', 'ncu_limiter' and 'issue_roofline' fields).
 
 Units: K6a + K6 per subray (pulses of the captured launch x N), K7 per pulse.
 `pulses`: pulses per captured launch (default: the library's chunk rule for a
-beam scene, <= 32 Mi subrays, capped by tools/profile_step.py's --batch 100000).
+beam scene, capped by tools/profile_step.py's --batch 100000).
 """
 import csv
 import io
