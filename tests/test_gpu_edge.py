@@ -86,6 +86,28 @@ def test_batch_split_and_repeat_are_bitwise_identical():
         assert np.array_equal(a[k].view(np.uint8), cat.view(np.uint8)), k
 
 
+def test_beam_scene_chunking_and_batch_split_are_bitwise_identical(monkeypatch):
+    """Beam pre-pass scene (C5 reduced): the chunk schedule (library rule, or
+    forced 1024- and 3000-pulse chunks) and a split into two calls must not
+    change a bit of the output (Philox counters, lane order, entry lists and
+    deferred hits are all per pulse / per subray)."""
+    w = workload("C5", 0.03)
+    monkeypatch.setenv("HELIOS_BEAM", "1")
+    a = gpu_run(w, 300, 7000)
+    runs = []
+    for chunk in ("1024", "3000"):
+        monkeypatch.setenv("HELIOS_CHUNK_PULSES", chunk)
+        runs.append(gpu_run(w, 300, 7000))
+    monkeypatch.delenv("HELIOS_CHUNK_PULSES")
+    c1 = gpu_run(w, 300, 2500)
+    c2 = gpu_run(w, 2800, 4500)
+    for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
+        for b in runs:
+            assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+        cat = np.concatenate([c1[k], c2[k]])
+        assert np.array_equal(a[k].view(np.uint8), cat.view(np.uint8)), k
+
+
 @pytest.mark.parametrize("subrays,n", [(37, 3000), (279, 25000)])
 def test_host_buffers_match_device_buffers(subrays, n):
     # host (pageable numpy / pinned torch) buffers go through the library's
