@@ -966,6 +966,14 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.scale_shift = sc->scale_shift;
   ta.sub = d_tab;
   ta.N = N;
+  {
+    // pad a pulse to whole warps when that wastes <= 6 % of the lanes (91 -> 96):
+    // every warp then walks one pulse's patch (HELIOS_PAD_LANES=0/1 forces)
+    const uint32_t padded = (N + 31u) / 32u * 32u;
+    bool pad = (padded - N) * 100u <= 6u * N;
+    if (const char* v = getenv("HELIOS_PAD_LANES")) pad = atoi(v) != 0;
+    ta.lanes = pad ? padded : N;
+  }
   ta.seed = params->seed;
   ta.K = K;
   ta.I0 = params->peak_power_w;

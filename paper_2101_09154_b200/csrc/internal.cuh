@@ -98,6 +98,7 @@ struct TraceArgs {
   uint32_t scale_shift;
   const SubrayConst* sub;
   uint32_t N;            // subrays per pulse
+  uint32_t lanes;        // K6 threads per pulse: N, or N padded to whole warps
   const float* origin;   // [n][3]
   const float* direction;
   uint64_t n_pulses;

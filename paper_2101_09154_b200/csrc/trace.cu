@@ -823,16 +823,20 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
 template <bool INSTR, bool PACKET, bool WIDE, int GRID>
 __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t total = a.n_pulses * (uint64_t)a.N;
-  const bool in_range = gid < total;
+  // a pulse occupies a.lanes (>= N) consecutive threads: N, or N padded to
+  // whole warps when that wastes few lanes (then no warp holds two pulses)
+  const uint32_t NL = a.lanes;
+  const uint64_t total = a.n_pulses * (uint64_t)NL;
+  // one launch covers < 2^32 lanes (launch_trace checks): 32-bit division
+  const uint32_t gq = (uint32_t)(gid < total ? gid : 0);
+  const uint64_t pq0 = gq / NL;
+  const bool in_range = gid < total && gq - (uint32_t)pq0 * NL < a.N;
   if (!PACKET && !in_range) return;
-  const uint64_t g = in_range ? gid : 0;  // out-of-range lanes ride along (packet mode)
-  // one launch covers < 2^32 subrays (launch_trace checks): 32-bit division
-  const uint32_t g32 = (uint32_t)g;
-  const uint64_t p = g32 / a.N;
+  const uint32_t g32 = in_range ? gq : 0;  // padding / out-of-range lanes ride along
+  const uint64_t p = g32 / NL;
   // lane position j of the pulse -> subray s (the table is in K6's lane order,
   // each entry carries its index; the record goes to slot s)
-  const uint32_t j = g32 - (uint32_t)p * a.N;
+  const uint32_t j = g32 - (uint32_t)p * NL;
   const SubrayConst sc = a.sub[j];
   const uint32_t s = sc.index;
   helios_subray_hit* const out_rec = a.out + p * a.N + s;
@@ -1170,7 +1174,8 @@ cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
 }
 
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s) {
-  const uint64_t total = a.n_pulses * (uint64_t)a.N;
+  if (a.lanes < a.N) return cudaErrorInvalidValue;
+  const uint64_t total = a.n_pulses * (uint64_t)a.lanes;
   if (total == 0) return cudaSuccess;
   const unsigned T = 128;
   const uint64_t blocks = (total + T - 1) / T;
