@@ -1239,7 +1239,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       ta.entries = reinterpret_cast<int2*>(buf + o_ent[slot]);
       ta.frames = reinterpret_cast<double*>(buf + o_frm[slot]);
       mark(ev_t, gs);
+      tmark('b', gs);
       if (e == cudaSuccess) e = launch_beam(ta, counters, gs);
+      tmark('B', gs);
       ++launches;
       // measurement only: HELIOS_BEAM_REPEAT=k launches K6a k extra times (its
       // marginal cost in the pipeline = step time delta / k)
@@ -1408,7 +1410,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       cudaEventDestroy(pr.second);
     }
     cudaEventDestroy(tev0);
-    fprintf(stderr, "helios_simulate spans (ms from call start; t/T K6, w/W K7, f/F fixed copy-out, c/C rows copy-out):%s\n", line.c_str());
+    fprintf(stderr, "helios_simulate spans (ms from call start; b/B K6a, t/T K6, w/W K7, f/F fixed copy-out, c/C rows copy-out):%s\n", line.c_str());
   }
   if (host_trace)
     fprintf(stderr, "helios_simulate: %llu pulses, %llu chunks, host %.3f ms, blocked in drains %.3f ms\n",
