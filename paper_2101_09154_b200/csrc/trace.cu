@@ -240,6 +240,9 @@ __device__ __forceinline__ TriRecord load_tri(const TriRecord* __restrict__ t, u
   return r;
 }
 
+#ifndef HELIOS_EXP_FILTER
+#define HELIOS_EXP_FILTER 1
+#endif
 #ifndef HELIOS_DDA_RCP
 #define HELIOS_DDA_RCP 1
 #endif
@@ -1086,7 +1089,19 @@ __global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const Tr
           } else if (GRID == 1 && pad > 0.0f) {
             const double sigma = (double)pad * G;  // Eq. 4 via the G LUT
             const double u = transmission_u(a.seed, a.pulse_base + p, s, id);
-            if (!(u < exp(-sigma * L))) {  // s = -ln(u)/sigma <= L: echo (R17)
+            // u < exp(-sigma L) decided by an fp32 estimate whenever u is
+            // farther from it than its error bound (__expf <= 2 + 1.17|x| ulp,
+            // plus the fp32 rounding of x: < 1e-5 relative for x < 80), else
+            // by the fp64 exp -- the decision is the fp64 one either way
+            const double x = sigma * L;
+            bool pass;
+            if (HELIOS_EXP_FILTER && x < 80.0) {
+              const double e32 = (double)__expf(-(float)x);
+              pass = fabs(u - e32) > 1e-5 * e32 ? u < e32 : u < exp(-x);
+            } else {
+              pass = u < exp(-x);
+            }
+            if (!pass) {  // s = -ln(u)/sigma <= L: echo (R17)
               vox_hit = true;
               t_vox = t_cur + (-log(u)) / sigma;  // Eq. 6
               sigma_vox = sigma;
