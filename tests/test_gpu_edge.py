@@ -309,3 +309,24 @@ def test_beam_prepass_axis_aligned_and_grazing(N, beta, monkeypatch):
     assert hit.mean() > 0.2
     dr = np.abs(sh["range_m"][hit] - r.sub_range[hit])
     assert np.all(dr <= 1e-6 * r.sub_range[hit] + 1e-5)
+
+
+@pytest.mark.parametrize("name,scale,start,count", [("C5", 0.03, 100, 3000), ("C3", 0.03, 500, 6000)])
+def test_lane_order_and_padding_are_bitwise_invariant(name, scale, start, count, monkeypatch):
+    """K6's lane order (R4 ring order vs the Hilbert patch order) and the lane
+    padding to whole warps only change which lane computes which subray: every
+    output must be bitwise identical (with the beam pre-pass on and off)."""
+    w = workload(name, scale)
+    ref = None
+    for beam in ("0", "1"):
+        for order in ("0", "1"):
+            for pad in ("0", "1"):
+                monkeypatch.setenv("HELIOS_BEAM", beam)
+                monkeypatch.setenv("HELIOS_SUBRAY_ORDER", order)
+                monkeypatch.setenv("HELIOS_PAD_LANES", pad)
+                g = gpu_run(w, start, count)
+                if ref is None:
+                    ref = g
+                    continue
+                for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
+                    assert np.array_equal(ref[k].view(np.uint8), g[k].view(np.uint8)), (k, beam, order, pad)
