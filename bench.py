@@ -269,7 +269,7 @@ def run_ours(args):
     value = subrays / (ms_max / 1e3) / 1e6
 
     # ---- algorithmic bytes (instrumented, untimed re-run of the same batches)
-    nodes = tris = vox = f64 = beam_nodes = 0
+    nodes = tris = vox = f64 = beam_nodes = n_ret = 0
     node_bytes = 64
     for i in range(args.warmup, steps_total):
         st = step(i, counters=True)
@@ -279,6 +279,7 @@ def run_ours(args):
         vox += st.voxel_steps
         f64 += st.fp64_tests
         beam_nodes += st.beam_nodes
+        n_ret += st.returns
     sub_rank = B * N * args.steps
     # per subray: nodes K6 tests, triangles, voxel steps; per pulse: nodes the
     # beam pre-pass K6a tests (once for all the pulse's subrays)
@@ -461,6 +462,8 @@ def run_ours(args):
             "dtype": "f64 decisions / f32 storage",
             "data": "synthetic (seeded generators, workloads/; paper datasets unavailable)",
             "pulses_per_s": pulses / (ms_max / 1e3),
+            # discrete returns of the timed steps (rank 0 counts, instrumented re-run; x world)
+            "returns_per_s": n_ret * world / (ms_max / 1e3),
             "config": {"workload": args.config, "pulses_per_step_per_gpu": B,
                        "subrays_per_pulse": N, "n_tris": w.scene.n_tris,
                        "n_bins": n_bins, "l2": "inputs larger than L2 (scene + outputs)",
