@@ -759,10 +759,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     }
 
   // beam pre-pass K6a (packet traversal of a tree with internal nodes, beams of
-  // >= 7 subrays); HELIOS_BEAM=0/1 forces, HELIOS_BEAM_K sets the hand-over size
-  // (small scenes: the pre-pass costs more than the few levels it saves; measured on C6)
+  // >= 7 subrays); HELIOS_BEAM=0/1 forces, HELIOS_BEAM_K sets the hand-over size.
+  // (An early version cost 6 % on C6's 1 622 triangles; with the later K6/K6a
+  // changes it gains 19 % there: no scene-size threshold.)
   const bool beam_ok = N >= 7 && sc->n_tris > 0 && !ref_is_leaf(sc->bvh.root);
-  bool beam = beam_ok && sc->n_tris >= 65536;
+  bool beam = beam_ok;
   if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
   // Chunk size.  Without the pre-pass: the K6 -> K7 records (16 B per subray)
   // stay L2-resident.  With it, per-chunk tails (K6a's longest cone walks, K6's

@@ -10,9 +10,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _parity(w, start, count, sample=None, params=None, seed=0):
-    # the reduced scenes are below the library's beam pre-pass threshold
-    # (65 536 triangles): force K6a on so parity covers it (the default path
-    # without it is checked bitwise against this one in test_beam_prepass_*)
+    # K6a on (the library default for trees with internal nodes; forced so the
+    # parity runs cover it whatever the default; the path without it is checked
+    # bitwise against this one in test_beam_prepass_*)
     with beam_env("1"):
         g = gpu_run(w, start, count, params=params)
     p = params or w.params
