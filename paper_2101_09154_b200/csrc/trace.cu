@@ -817,6 +817,9 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   }
 }
 
+#ifndef HELIOS_TRACE_T
+#define HELIOS_TRACE_T 128  // K6 threads per block
+#endif
 #ifndef HELIOS_TRACE_MIN_BLOCKS
 #define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
 #endif
@@ -824,7 +827,7 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
 // the A4 march is compiled in only where needed, so each scene kind keeps
 // the traversal's register budget
 template <bool INSTR, bool PACKET, bool WIDE, int GRID>
-__global__ void __launch_bounds__(128, HELIOS_TRACE_MIN_BLOCKS) k_trace(const TraceArgs a) {
+__global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 / HELIOS_TRACE_T) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // a pulse occupies a.lanes (>= N) consecutive threads: N, or N padded to
   // whole warps when that wastes few lanes (then no warp holds two pulses)
@@ -1192,7 +1195,7 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaSt
   if (a.lanes < a.N) return cudaErrorInvalidValue;
   const uint64_t total = a.n_pulses * (uint64_t)a.lanes;
   if (total == 0) return cudaSuccess;
-  const unsigned T = 128;
+  const unsigned T = HELIOS_TRACE_T;
   const uint64_t blocks = (total + T - 1) / T;
   if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
