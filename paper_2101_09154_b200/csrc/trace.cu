@@ -264,6 +264,20 @@ __device__ __forceinline__ double plane_t(double org, uint32_t k, double vs, dou
 #endif
 }
 
+// a[i] for a runtime i in {0, 1, 2} by selects: the 3-element state arrays of
+// the voxel march stay in registers (a runtime subscript would put them in
+// local memory)
+template <class T>
+__device__ __forceinline__ T pick3(const T (&a)[3], int i) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
+}
+template <class T>
+__device__ __forceinline__ void put3(T (&a)[3], int i, T v) {
+  a[0] = i == 0 ? v : a[0];
+  a[1] = i == 1 ? v : a[1];
+  a[2] = i == 2 ? v : a[2];
+}
+
 // Opaque / scaled voxel cube (Eq. 5; R31): minimum corner and side
 // of voxel (ix, iy, iz), the oracle's operation order.
 __device__ __forceinline__ double voxel_cube(const TraceArgs& a, const int idx[3], uint32_t id,
@@ -1047,7 +1061,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
                                   : INFINITY;
             }
             const int e = (tb[0] <= tb[1] && tb[0] <= tb[2]) ? 0 : (tb[1] <= tb[2] ? 1 : 2);
-            const double t_bx = tb[e];
+            const double t_bx = pick3(tb, e);
             if (INSTR) ++c_vox;
             if (!(t_bx < t_out)) break;  // the ray ends inside the empty brick
 #pragma unroll
@@ -1059,16 +1073,19 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
                                 d3v[q], inv3[q]);
               }
             }
-            idx[e] = stp[e] > 0 ? kb[e] : kb[e] - 1;
-            if (idx[e] < 0 || idx[e] >= (int)nn[e]) break;
-            tn[e] = plane_t(org[e], (uint32_t)(stp[e] > 0 ? idx[e] + 1 : idx[e]), a.vs, o3[e],
-                            d3v[e], inv3[e]);
+            const int ste = pick3(stp, e), kbe = pick3(kb, e);
+            const int ie = ste > 0 ? kbe : kbe - 1;
+            if (ie < 0 || ie >= (int)pick3(nn, e)) break;
+            put3(idx, e, ie);
+            put3(tn, e,
+                 plane_t(pick3(org, e), (uint32_t)(ste > 0 ? ie + 1 : ie), a.vs, pick3(o3, e),
+                         pick3(d3v, e), pick3(inv3, e)));
             t_cur = t_bx;
             continue;
           }
         }
         const int ax = (tn[0] <= tn[1] && tn[0] <= tn[2]) ? 0 : (tn[1] <= tn[2] ? 1 : 2);
-        const double t_exit = tn[ax];
+        const double t_exit = pick3(tn, ax);
         const double t_end = fmin(t_exit, t_out);
         const double L = t_end - t_cur;
         if (INSTR) ++c_vox;
@@ -1115,10 +1132,12 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
           }
         }
         if (t_exit >= t_out) break;
-        idx[ax] += stp[ax];
-        if (idx[ax] < 0 || idx[ax] >= (int)nn[ax]) break;
-        tn[ax] = plane_t(org[ax], (uint32_t)(stp[ax] > 0 ? idx[ax] + 1 : idx[ax]), a.vs, o3[ax],
-                         d3v[ax], inv3[ax]);
+        const int sta = pick3(stp, ax), ia = pick3(idx, ax) + sta;
+        if (ia < 0 || ia >= (int)pick3(nn, ax)) break;
+        put3(idx, ax, ia);
+        put3(tn, ax,
+             plane_t(pick3(org, ax), (uint32_t)(sta > 0 ? ia + 1 : ia), a.vs, pick3(o3, ax),
+                     pick3(d3v, ax), pick3(inv3, ax)));
         t_cur = t_exit;
       }
     }
