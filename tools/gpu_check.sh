@@ -16,5 +16,5 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 cat $O/bench.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv \
   --log-file $O/launches.csv python bench.py --no-cpu-baseline --no-e2e > $O/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_beam|k_trace|k_waveform' -s 3 -c 3 \
+HELIOS_CHUNK_PULSES=50000 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_beam|k_trace|k_waveform' -s 3 -c 3 \
   -o $O/full python tools/profile_step.py --config C5 --batch 100000 --steps 4 > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"

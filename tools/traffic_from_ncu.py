@@ -6,8 +6,8 @@ roofline 'traffic', 'ncu_limiter' and 'issue_roofline' fields).
   python tools/traffic_from_ncu.py gpurun_out/x/full.ncu-rep C5 "<source text>" [pulses]
 
 Units: K6a + K6 per subray (pulses of the captured launch x N), K7 per pulse.
-`pulses`: pulses per captured launch (default: the library's chunk rule for a
-beam scene, capped by tools/profile_step.py's --batch 100000).
+`pulses`: pulses per captured launch -- capture with HELIOS_CHUNK_PULSES=50000 (as
+tools/gpu_check.sh does) so that every launch covers exactly 50000 pulses.
 """
 import csv
 import io
@@ -46,7 +46,7 @@ def main(rep, cfg, source, pulses=None):
             continue
         per[key] = {c: scale(units[idx[c]], r[idx[c]]) for c in COLS}
     N = N_OF[cfg]
-    chunk = int(pulses) if pulses else min(100000, (32 << 20) // N)
+    chunk = int(pulses) if pulses else 50000
     subrays = chunk * N
     t = per["k_trace"]
     b = per.get("k_beam", {c: 0.0 for c in COLS})
