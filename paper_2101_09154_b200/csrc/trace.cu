@@ -1,8 +1,14 @@
-// trace.cu -- K6: subray fan-out + nearest hit + transmissive voxels + radiometry.
+// trace.cu -- K6a (beam pre-pass) and K6: subray fan-out + nearest hit +
+// transmissive voxels + radiometry.
 //
-// One thread per (pulse, subray), subray fastest, so the lanes of a warp
-// carry the nearly-parallel subrays of one or two pulses and
-// walk the same BVH nodes: coherent float4 node loads served from L1.
+// K6a: one thread per pulse walks the top of the BVH with the cone of all its
+// subrays and lists the subtrees K6 must enter (near-first, with a lower bound
+// of the entry distance), plus the pulse frame (DESIGN.md s.7.0).
+// K6: one thread per (pulse, subray) -- lanes mapped to subrays along a Hilbert
+// curve over the footprint, pulses padded to whole warps when that is cheap --
+// so the lanes of a warp carry a compact patch of nearly parallel subrays
+// and walk the same BVH nodes as a masked packet from K6a's
+// entries: coherent float4 node loads served from L1.
 //
 // Precision contract (DESIGN.md s.3 C-0):
 //   * subray directions in fp64 (P:199 pattern, R2/R4 frame);
@@ -10,7 +16,9 @@
 //     fp32 ray never culls a box the fp64 ray enters;
 //   * every leaf triangle is decided by fp64 Moller-Trumbore on the fp32
 //     vertices (the exact definition the oracle uses), nearest by fp64 t,
-//     exact ties -> lower primitive id (R22);
+//     exact ties -> lower primitive id (R22); an fp32 filter with a forward
+//     error bound rejects definite misses and recognises definite hits, whose
+//     fp64 decision is deferred to the end of the walk;
 //   * the voxel march (3D-DDA) computes each plane crossing directly in fp64
 //     (no accumulated increments), chord lengths, exp(-sigma L), -ln(u)/sigma
 //     in fp64 (R17-R20);
