@@ -21,7 +21,12 @@ RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
        "sm__inst_executed_pipe_fp64.sum", "sm__inst_executed_pipe_alu.sum",
        "smsp__average_warp_latency_issue_stalled_long_scoreboard",
-       "dram__throughput.avg.pct_of_peak_sustained_elapsed")
+       "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+       "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+       "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active")
 
 
 def main(path):
