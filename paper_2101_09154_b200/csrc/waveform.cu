@@ -35,7 +35,13 @@ namespace helios {
 namespace {
 
 constexpr int kMaxWarps = 8;
-constexpr int kWCap = 512;    // fp64 bins per warp in shared memory
+#ifndef HELIOS_WAVE_WCAP
+#define HELIOS_WAVE_WCAP 512
+#endif
+#ifndef HELIOS_WAVE_MIN_BLOCKS
+#define HELIOS_WAVE_MIN_BLOCKS 5
+#endif
+constexpr int kWCap = HELIOS_WAVE_WCAP;  // fp64 bins per warp in shared memory
 constexpr int kAggCap = 64;   // offset groups handled by the grouped path
 constexpr int kGroupCap = kAggCap * 2 / 3;  // sparse groups (8 + 4 B) in the same space
 constexpr size_t kSmemCap = 200 * 1024;
@@ -278,7 +284,7 @@ __host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
   return L;
 }
 
-__global__ void __launch_bounds__(kMaxWarps * 32, 5) k_waveform(const WaveArgs a,
+__global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_waveform(const WaveArgs a,
                                                              double* __restrict__ gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
