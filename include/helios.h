@@ -116,10 +116,17 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
                                   helios_scene* out);
 
 /* Build the acceleration structure on the device (replaces the paper's
- * kd-tree, by an LBVH): 30-bit Morton codes of triangle centroids,
- * radix sort, Karras hierarchy, bottom-up AABB refit, 64-B child-pair nodes,
- * triangles permuted to leaf order.  Idempotent.  Synchronises the stream.
- * Errors: INVALID_ARGUMENT (NULL scene), OUT_OF_MEMORY, CUDA. */
+ * kd-tree, "prior art, not the blueprint"): a binary BVH over the
+ * triangles -- 63-bit Morton codes of the centroids on an ISOTROPIC grid (21
+ * bits per axis; the north star's 30-bit per-axis codes measured 2.3x slower
+ * on C5, DESIGN.md s.7.1), a stable LSD radix sort (hand-written), then the
+ * hierarchy: PLOC agglomerative clustering (default) or the Karras LBVH
+ * (helios_tuning.builder = 1) with bottom-up AABB refit; 64-B child-pair
+ * nodes, subtrees of <= 2 triangles collapsed into leaves, triangles permuted
+ * to depth-first leaf order (48 B each).  Deterministic (same arrays -> same
+ * tree).  Idempotent.  Synchronises the stream.
+ * Errors: INVALID_ARGUMENT (NULL scene), OUT_OF_MEMORY, CUDA (incl. a tree
+ * deeper than the 64-entry traversal stack). */
 helios_status helios_build_accel(helios_scene scene, helios_stream stream);
 
 /* Free everything the scene owns.  NULL is a no-op.  Must not race with a
@@ -266,6 +273,9 @@ typedef struct {
   double trace_ms;    /* out: summed device time of the trace launches (K6), CUDA events */
   double waveform_ms; /* out: summed device time of the waveform launches (K7)          */
   uint64_t beam_nodes; /* BVH nodes tested by the per-pulse beam pre-pass K6a (collect_counters) */
+  double beam_ms;     /* out: summed device time of the beam pre-pass launches (K6a)     */
+  uint32_t batches;   /* out: pulse batches of the call                                  */
+  uint32_t chunks;    /* out: pipeline chunks of the call                                */
 } helios_stats;
 
 /* Simulate n_pulses pulses (the hot path: subray fan-out, nearest hit against
@@ -282,6 +292,44 @@ typedef struct {
 helios_status helios_simulate(helios_scene scene, const helios_scanner_params* params,
                               const helios_pulses* pulses, const helios_outputs* outputs,
                               helios_stream stream, helios_stats* stats);
+
+/* Simulate n_batches independent pulse batches in ONE call: pulses[i] with
+ * outputs[i] (each exactly as one helios_simulate call: its own pulse ids,
+ * its own packed offsets relative to the batch, its own capacities).  The
+ * batches run through one chunk pipeline, so the head of a batch overlaps the
+ * tail of the previous one and host copies of one batch overlap kernels of
+ * the next (pulses are independent).  Results are bitwise those of
+ * n_batches separate helios_simulate calls.  Blocking, like helios_simulate.
+ * Output arrays of different batches must not overlap.  Errors as
+ * helios_simulate (the message names the batch); HELIOS_ERR_CAPACITY is
+ * returned if any batch's packed buffer was too small (all other outputs of
+ * every batch complete). */
+helios_status helios_simulate_batches(helios_scene scene, const helios_scanner_params* params,
+                                      const helios_pulses* pulses, const helios_outputs* outputs,
+                                      uint32_t n_batches, helios_stream stream,
+                                      helios_stats* stats);
+
+/* ------------------------------------------------------------------------
+ * Process-wide tuning / test switches.  Not needed for correct use: every
+ * value only changes how the same results are computed (the tests check the
+ * outputs bitwise invariant to them).  Read by a call when it starts.  At the
+ * first use they are seeded once from the environment (HELIOS_BEAM,
+ * HELIOS_BUILDER=lbvh|ploc, HELIOS_LANE_ORDER, HELIOS_PAD_LANES,
+ * HELIOS_SERIALIZE, HELIOS_TRACE_SPANS, HELIOS_CHUNK_PULSES).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t beam_prepass; /* K6a: -1 or 1 on wherever it applies (trees with internal nodes,
+                           beams of >= 7 subrays), 0 off                                  */
+  int32_t builder;      /* helios_build_accel hierarchy: 0 PLOC (default), 1 Karras LBVH     */
+  int32_t lane_order;   /* K6 lanes <-> subrays: 1 Hilbert patches (default), 0 ring order R4 */
+  int32_t pad_lanes;    /* pad a pulse's lanes to whole warps: -1 auto (<= 6 % waste), 0, 1  */
+  int32_t serialize;    /* 1: every kernel on the caller's stream, no overlap (exclusive
+                           per-kernel device times in helios_stats); 0 default             */
+  int32_t trace_spans;  /* 1: print per-stream device spans of every call to stderr         */
+  uint64_t chunk_pulses;/* 0 auto, else pulses per pipeline chunk (>= 1024)                 */
+} helios_tuning;
+helios_status helios_get_tuning(helios_tuning* out);
+helios_status helios_set_tuning(const helios_tuning* tuning); /* INVALID_ARGUMENT if out of range */
 
 /* ------------------------------------------------------------------------
  * On-device pulse generation (P:155 platforms, P:177 scan deflectors;

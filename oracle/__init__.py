@@ -72,7 +72,11 @@ class OracleOutputs(ctypes.Structure):
         "n_returns", "k0", "waveform", "ret_range", "ret_time", "ret_intensity",
         "ret_prim", "ret_number", "ret_width", "peak_margin", "attr_margin", "sub_range",
         "sub_amp", "sub_prim", "sub_k", "sub_ncand", "sub_gap", "sub_kmargin",
-        "sub_umargin")]
+        "sub_umargin", "sub_cand", "ret_cand")]
+
+MAX_CAND = 8   # kMaxCand: triangle candidates per subray (C-4)
+MAX_ATTR = 4   # kMaxAttr: attribution candidates per return (C-4)
+DECISION_EPS = 2.5e-7  # kDecisionEps: margins below this may flip on the CUDA path
 
 
 def lib():
@@ -96,6 +100,19 @@ def lib():
         L.oracle_ray_triangle.argtypes = [_vp, _vp, _vp, _vp]
         L.oracle_nearest_triangle.restype = _i64
         L.oracle_nearest_triangle.argtypes = [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp]
+        L.oracle_nearest_candidates.restype = _i64
+        L.oracle_nearest_candidates.argtypes = [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp,
+                                                ctypes.c_int32]
+        L.oracle_cone_may_hit.restype = ctypes.c_int
+        L.oracle_cone_may_hit.argtypes = [_vp, _vp, _d, _vp]
+        L.oracle_bin_of.restype = _i64
+        L.oracle_bin_of.argtypes = [_d, _d, _vp]
+        L.oracle_transmits.restype = ctypes.c_int
+        L.oracle_transmits.argtypes = [_d, _d, _d, _vp]
+        L.oracle_waveform_peaks.restype = ctypes.c_int
+        L.oracle_waveform_peaks.argtypes = [ctypes.POINTER(OracleParams), _vp, _vp, _vp, _d, _u64,
+                                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                            _vp, _vp]
         L.oracle_philox4x32_10.restype = None
         L.oracle_philox4x32_10.argtypes = [_vp, _vp, _vp]
         L.oracle_transmission_u.restype = _d
@@ -196,6 +213,48 @@ def nearest_triangle(o, d, tris):
                                       ctypes.byref(t), ctypes.byref(c),
                                       ctypes.byref(nc), ctypes.byref(g))
     return int(i), t.value, c.value, nc.value, g.value
+
+
+def nearest_candidates(o, d, tris):
+    """(id, t, n_cand, candidate ids by (t, id)) of the nearest hit (C-4:
+    every triangle within 1e-6 m of the nearest)."""
+    o = np.ascontiguousarray(o, np.float64)
+    d = np.ascontiguousarray(d, np.float64)
+    tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
+    t = ctypes.c_double()
+    c = ctypes.c_double()
+    nc = ctypes.c_int32()
+    g = ctypes.c_double()
+    cand = np.zeros(MAX_CAND, np.uint32)
+    i = lib().oracle_nearest_candidates(_p(o), _p(d), _p(tris), tris.shape[0], ctypes.byref(t),
+                                        ctypes.byref(c), ctypes.byref(nc), ctypes.byref(g),
+                                        _p(cand), MAX_CAND)
+    return int(i), t.value, nc.value, cand[:min(nc.value, MAX_CAND)].copy()
+
+
+def cone_may_hit(o, d, theta: float, tri9) -> bool:
+    """False only if no ray from o within angle theta of unit d can hit the
+    triangle (its bounding sphere lies outside the cone): the per-pulse skip
+    of oracle_simulate's brute force."""
+    o = np.ascontiguousarray(o, np.float64)
+    d = np.ascontiguousarray(d, np.float64)
+    tri = np.ascontiguousarray(tri9, np.float32).reshape(9)
+    return bool(lib().oracle_cone_may_hit(_p(o), _p(d), theta, _p(tri)))
+
+
+def bin_of(R: float, delta_ns: float):
+    """(k, margin): k = floor(2R / c / Delta) (R8, R9), margin = distance of
+    2R / c / Delta from the nearest integer."""
+    m = ctypes.c_double()
+    k = lib().oracle_bin_of(R, delta_ns, ctypes.byref(m))
+    return int(k), m.value
+
+
+def transmits(u: float, sigma: float, L: float):
+    """(passes, margin): u < exp(-sigma L) (R17), margin |u - exp(-sigma L)|."""
+    m = ctypes.c_double()
+    r = lib().oracle_transmits(u, sigma, L, ctypes.byref(m))
+    return bool(r), m.value
 
 
 def philox4x32_10(ctr, key) -> np.ndarray:
@@ -305,6 +364,48 @@ def waveform_bins(window_ns: float, bin_ns: float) -> int:
 
 
 # ---------------------------------------------------------------- simulate
+def _oracle_params(params) -> OracleParams:
+    pr = OracleParams()
+    for f, _ in OracleParams._fields_:
+        if f != "pad_":
+            setattr(pr, f, getattr(params, f, 0))
+    # the threshold crosses the C ABI as a float (helios_scanner_params): the
+    # oracle thresholds with that same value
+    pr.detection_threshold = float(np.float32(params.detection_threshold))
+    return pr
+
+
+def waveform_peaks(params, A, k, prim, time_s: float = 0.0, pulse_id: int = 0):
+    """Steps O6-O8 for ONE pulse from per-subray amplitudes A[s], bins k[s]
+    (-1 = no event) and prims (R9-R13).  Returns a dict with
+    n_returns, k0, waveform, ret_range/time/intensity/prim/number/width,
+    ret_cand and the decision margins peak_margin / attr_margin."""
+    pr = _oracle_params(params)
+    N = int(params.subray_count)
+    R = int(params.max_returns)
+    A = np.ascontiguousarray(A, np.float64).reshape(N)
+    k = np.ascontiguousarray(k, np.int64).reshape(N)
+    prim = np.ascontiguousarray(prim, np.uint32).reshape(N)
+    nb = waveform_bins(params.max_fullwave_range_ns, params.bin_width_ns)
+    out = dict(waveform=np.zeros(nb), ret_range=np.zeros(R), ret_time=np.zeros(R),
+               ret_intensity=np.zeros(R), ret_prim=np.zeros(R, np.uint32),
+               ret_number=np.zeros(R, np.int32), ret_width=np.full(R, np.nan),
+               ret_cand=np.full((R, MAX_ATTR), 0xFFFFFFFF, np.uint32))
+    nr = ctypes.c_int32()
+    k0 = ctypes.c_int64()
+    pm = ctypes.c_double()
+    am = ctypes.c_double()
+    rc = lib().oracle_waveform_peaks(
+        ctypes.byref(pr), _p(A), _p(k), _p(prim), time_s, pulse_id, ctypes.byref(nr),
+        ctypes.byref(k0), _p(out["waveform"]), _p(out["ret_range"]), _p(out["ret_time"]),
+        _p(out["ret_intensity"]), _p(out["ret_prim"]), _p(out["ret_number"]),
+        _p(out["ret_width"]), _p(out["ret_cand"]), ctypes.byref(pm), ctypes.byref(am))
+    if rc != 0:
+        raise ValueError("oracle_waveform_peaks: invalid parameters")
+    out.update(n_returns=nr.value, k0=k0.value, peak_margin=pm.value, attr_margin=am.value)
+    return out
+
+
 @dataclass
 class OracleResult:
     n_returns: np.ndarray
@@ -326,6 +427,8 @@ class OracleResult:
     sub_gap: np.ndarray
     sub_kmargin: np.ndarray
     sub_umargin: np.ndarray
+    sub_cand: np.ndarray   # [n, N, MAX_CAND] triangle candidates (C-4), UINT32_MAX-padded
+    ret_cand: np.ndarray   # [n, R, MAX_ATTR] attribution candidates (C-4), UINT32_MAX-padded
 
 
 def simulate(scene, params, origins, directions, times, pulse_ids,
@@ -364,10 +467,7 @@ def simulate(scene, params, origins, directions, times, pulse_ids,
     sc.pad_max = float(getattr(scene, "pad_max", 1.0))
     sc.scale_alpha = float(getattr(scene, "scale_alpha", 1.0))
     sc.scale_shift = int(getattr(scene, "scale_shift", 0))
-    pr = OracleParams()
-    for f, _ in OracleParams._fields_:
-        if f != "pad_":
-            setattr(pr, f, getattr(params, f, 0))
+    pr = _oracle_params(params)
     o = np.ascontiguousarray(origins, np.float32).reshape(n, 3)
     d = np.ascontiguousarray(directions, np.float32).reshape(n, 3)
     t = np.ascontiguousarray(times, np.float64).reshape(n)
@@ -382,7 +482,9 @@ def simulate(scene, params, origins, directions, times, pulse_ids,
         attr_margin=np.zeros(n), sub_range=np.zeros((n, N)), sub_amp=np.zeros((n, N)),
         sub_prim=np.zeros((n, N), np.uint32), sub_k=np.zeros((n, N), np.int64),
         sub_ncand=np.zeros((n, N), np.int32), sub_gap=np.zeros((n, N)),
-        sub_kmargin=np.zeros((n, N)), sub_umargin=np.zeros((n, N)))
+        sub_kmargin=np.zeros((n, N)), sub_umargin=np.zeros((n, N)),
+        sub_cand=np.zeros((n, N, MAX_CAND), np.uint32),
+        ret_cand=np.zeros((n, R, MAX_ATTR), np.uint32))
     out = OracleOutputs()
     for f, _ in OracleOutputs._fields_:
         setattr(out, f, _p(getattr(res, f)))

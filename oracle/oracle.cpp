@@ -37,6 +37,17 @@ const double kPi = 3.14159265358979323846;
 const double kC = 299792458.0;  // speed of light, m/s (Sec. 3.4)
 const double kInf = std::numeric_limits<double>::infinity();
 const double kNaN = std::numeric_limits<double>::quiet_NaN();
+// C-4 exports: at most kMaxCand triangle candidates per subray, kMaxAttr
+// attribution candidates per return
+const int32_t kMaxCand = 8;
+const int32_t kMaxAttr = 4;
+// Decision margins below which the CUDA path may legitimately decide the
+// other way (C-4; DESIGN.md s.4): it bins the fp32-rounded amplitudes
+// (relative error <= 2^-24 = 6e-8 per term, all terms >= 0, so every bin and
+// every contribution is within 6e-8 relative of the oracle's), so a
+// comparison of two such values can flip only within 1.2e-7 relative;
+// 2.5e-7 leaves a factor 2.
+const double kDecisionEps = 2.5e-7;
 
 struct V3 {
   double x, y, z;
@@ -182,18 +193,16 @@ double oracle_eq7_intensity(double lambda_eff, double sigma, double P,
  * or degenerate triangle).  Returns t, or -1 on a miss; *cos_inc receives
  * |n . d| / |d| (incidence folded to [0, pi/2]).
  * ---------------------------------------------------------------------- */
-double oracle_ray_triangle(const double o_in[3], const double d_in[3],
-                           const float* tri9, double* cos_inc) {
-  V3 o = {o_in[0], o_in[1], o_in[2]};
-  V3 d = {d_in[0], d_in[1], d_in[2]};
-  V3 v0 = {tri9[0], tri9[1], tri9[2]};
-  V3 v1 = {tri9[3], tri9[4], tri9[5]};
-  V3 v2 = {tri9[6], tri9[7], tri9[8]};
-  V3 e1 = sub(v1, v0);
-  V3 e2 = sub(v2, v0);
+}  // extern "C"
+
+// The Moller-Trumbore test proper, given the triangle's v0, e1 = v1 - v0,
+// e2 = v2 - v0 and cut = 1e-12 |e1| |e2| (computed once per triangle by the
+// callers, in oracle_ray_triangle's order: the same values, the same result).
+static double ray_triangle_pre(const V3& o, const V3& d, const V3& v0, const V3& e1,
+                               const V3& e2, double cut) {
   V3 p = cross(d, e2);
   double det = dot(e1, p);
-  if (std::fabs(det) <= 1e-12 * norm(e1) * norm(e2)) return -1.0;
+  if (std::fabs(det) <= cut) return -1.0;
   double inv = 1.0 / det;
   V3 s = sub(o, v0);
   double u = dot(s, p) * inv;
@@ -203,51 +212,137 @@ double oracle_ray_triangle(const double o_in[3], const double d_in[3],
   if (v < 0.0 || u + v > 1.0) return -1.0;
   double t = dot(e2, q) * inv;
   if (!(t > 0.0)) return -1.0;
+  return t;
+}
+
+struct TriPre {
+  V3 v0, e1, e2;
+  double cut;
+};
+static TriPre tri_pre(const float* tri9) {
+  TriPre r;
+  r.v0 = {tri9[0], tri9[1], tri9[2]};
+  V3 v1 = {tri9[3], tri9[4], tri9[5]};
+  V3 v2 = {tri9[6], tri9[7], tri9[8]};
+  r.e1 = sub(v1, r.v0);
+  r.e2 = sub(v2, r.v0);
+  r.cut = 1e-12 * norm(r.e1) * norm(r.e2);
+  return r;
+}
+
+extern "C" {
+
+double oracle_ray_triangle(const double o_in[3], const double d_in[3],
+                           const float* tri9, double* cos_inc) {
+  V3 o = {o_in[0], o_in[1], o_in[2]};
+  V3 d = {d_in[0], d_in[1], d_in[2]};
+  const TriPre tp = tri_pre(tri9);
+  const double t = ray_triangle_pre(o, d, tp.v0, tp.e1, tp.e2, tp.cut);
+  if (t < 0.0) return -1.0;
   if (cos_inc) {
-    V3 n = cross(e1, e2);
+    V3 n = cross(tp.e1, tp.e2);
     *cos_inc = std::fabs(dot(n, d)) / (norm(n) * norm(d));
   }
   return t;
 }
 
-/* Nearest hit by brute force over EVERY triangle ("minimum distance
- * intersection"; R22 ties -> lower id).  Returns the id or -1 (miss).
- * *t_out, *cos_out, *n_cand (#triangles with t <= t_min + 1e-6 m) and *gap
- * (t_second - t_min over distinct triangles, +inf if none). */
-int64_t oracle_nearest_triangle(const double o[3], const double d[3],
-                                const float* tris, uint32_t n_tris,
-                                double* t_out, double* cos_out,
-                                int32_t* n_cand, double* gap) {
-  double best = kInf, best_cos = 0.0;
-  int64_t best_id = -1;
-  std::vector<double> hits;  // t of every triangle the ray hits
-  for (uint32_t i = 0; i < n_tris; ++i) {
-    double c = 0.0;
-    double t = oracle_ray_triangle(o, d, tris + 9ull * i, &c);
-    if (t < 0.0) continue;
-    hits.push_back(t);
-    if (t < best) {  // strict: the lower id wins an exact tie (R22)
-      best = t;
-      best_id = i;
-      best_cos = c;
-    }
-  }
-  int32_t cand = 0;
+}  // extern "C"
+
+// Can any ray from o whose direction lies within angle theta of the unit
+// vector d hit the triangle?  False only when the triangle's bounding sphere
+// (centroid c, radius r = the largest vertex distance) lies entirely outside
+// that one-sided cone: with v = c - o, a = v.d, rho = |v - a d|, the
+// distance from c to the cone is rho cos(theta) - a sin(theta) when the
+// nearest cone point is on its mantle (a cos(theta) + rho sin(theta) >= 0),
+// else |v| (the apex).  Used to skip, per pulse, the triangles none of its
+// subrays can reach (the brute force then tests every other triangle with
+// every subray); theta and r are widened so rounding cannot reject a hit.
+static bool cone_may_hit(const V3& o, const V3& d, double cos_t, double sin_t,
+                         const TriPre& tp) {
+  const V3 v1 = add(tp.v0, tp.e1), v2 = add(tp.v0, tp.e2);
+  const V3 c = scale(add(add(tp.v0, v1), v2), 1.0 / 3.0);
+  double r2 = dot(sub(tp.v0, c), sub(tp.v0, c));
+  r2 = std::max(r2, dot(sub(v1, c), sub(v1, c)));
+  r2 = std::max(r2, dot(sub(v2, c), sub(v2, c)));
+  const double r = std::sqrt(r2) * (1.0 + 1e-9) + 1e-9;
+  const V3 v = sub(c, o);
+  const double a = dot(v, d);
+  const V3 w = sub(v, scale(d, a));
+  const double rho = norm(w);
+  if (a * cos_t + rho * sin_t >= 0.0) return rho * cos_t - a * sin_t <= r;
+  return norm(v) <= r;
+}
+
+typedef std::vector<std::pair<double, uint32_t>> HitList;  // (t, triangle id) of every hit
+
+// The nearest hit and its candidate set from the list of EVERY hit of a ray
+// (the definition: minimum of (t, id); C_tri = {t <= t_min + 1e-6 m}).
+static int64_t nearest_from_hits(HitList& hits, double* t_out, int32_t* n_cand, double* gap,
+                                 uint32_t* cand, int32_t max_cand) {
+  std::sort(hits.begin(), hits.end());  // by t, then the lower id (R22)
+  const int64_t best_id = hits.empty() ? -1 : (int64_t)hits[0].second;
+  const double best = hits.empty() ? kInf : hits[0].first;
+  int32_t nc = 0;
   double second = kInf;
-  bool skipped_best = false;
-  for (double t : hits) {
-    if (t <= best + 1e-6) ++cand;
-    if (t == best && !skipped_best) {
-      skipped_best = true;
-      continue;
+  for (const auto& h : hits) {
+    if (h.first <= best + 1e-6) {
+      if (cand && nc < max_cand) cand[nc] = h.second;
+      ++nc;
     }
-    second = std::min(second, t);
+    if ((int64_t)h.second != best_id) second = std::min(second, h.first);
   }
-  if (t_out) *t_out = best_id >= 0 ? best : kInf;
-  if (cos_out) *cos_out = best_cos;
-  if (n_cand) *n_cand = cand;
+  if (cand)
+    for (int32_t k = nc; k < max_cand; ++k) cand[k] = 0xFFFFFFFFu;
+  if (t_out) *t_out = best;
+  if (n_cand) *n_cand = nc;
   if (gap) *gap = second - best;
   return best_id;
+}
+
+extern "C" {
+
+int64_t oracle_nearest_candidates(const double o[3], const double d[3], const float* tris,
+                                  uint32_t n_tris, double* t_out, double* cos_out,
+                                  int32_t* n_cand, double* gap, uint32_t* cand,
+                                  int32_t max_cand) {
+  HitList hits;
+  for (uint32_t i = 0; i < n_tris; ++i) {
+    double t = oracle_ray_triangle(o, d, tris + 9ull * i, nullptr);
+    if (t >= 0.0) hits.push_back({t, i});
+  }
+  const int64_t id = nearest_from_hits(hits, t_out, n_cand, gap, cand, max_cand);
+  double c = 0.0;
+  if (id >= 0) oracle_ray_triangle(o, d, tris + 9ull * id, &c);  // the same t, its cos
+  if (cos_out) *cos_out = c;
+  return id;
+}
+
+int oracle_cone_may_hit(const double o[3], const double d[3], double theta, const float* tri9) {
+  return cone_may_hit(V3{o[0], o[1], o[2]}, V3{d[0], d[1], d[2]}, std::cos(theta),
+                      std::sin(theta), tri_pre(tri9));
+}
+
+int64_t oracle_nearest_triangle(const double o[3], const double d[3], const float* tris,
+                                uint32_t n_tris, double* t_out, double* cos_out,
+                                int32_t* n_cand, double* gap) {
+  return oracle_nearest_candidates(o, d, tris, n_tris, t_out, cos_out, n_cand, gap, nullptr, 0);
+}
+
+/* Bin of a range (R8, R9): x = 2R / c / Delta (two-way time in bins),
+ * k = floor(x); *margin = |x - nearest integer| (C-4: how far the decision
+ * floor(x) is from flipping). */
+int64_t oracle_bin_of(double R, double delta_ns, double* margin) {
+  const double x = 2.0 * R / kC / (delta_ns * 1e-9);
+  if (margin) *margin = std::fabs(x - std::nearbyint(x));
+  return (int64_t)std::floor(x);
+}
+
+/* Transmission decision (Eq. 6; R17): the subray passes the voxel
+ * iff u < exp(-sigma L); *margin = |u - exp(-sigma L)| (C-4). */
+int oracle_transmits(double u, double sigma, double L, double* margin) {
+  const double pass_p = std::exp(-sigma * L);
+  if (margin) *margin = std::fabs(u - pass_p);
+  return u < pass_p;
 }
 
 /* ------------------------------------------------------------------------
@@ -765,6 +860,8 @@ typedef struct {
   double* sub_gap;
   double* sub_kmargin;   // |2R/(c Delta) - round(.)|
   double* sub_umargin;   // min |u - exp(-sigma L)| over this subray's decisions
+  uint32_t* sub_cand;    // [n][N][kMaxCand] candidate ids (C_tri by (t, id)) or NULL
+  uint32_t* ret_cand;    // [n][max_returns][kMaxAttr] attribution candidates or NULL
 } oracle_outputs;
 
 uint32_t oracle_waveform_bins(double window_ns, double bin_ns) {
@@ -777,7 +874,7 @@ uint32_t oracle_waveform_bins(double window_ns, double bin_ns) {
 static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
                             const float* origin, const float* direction, uint64_t pulse_id,
                             int64_t i, uint32_t s, const double* theta, const double* phi,
-                            const oracle_outputs* out) {
+                            HitList& hits, const oracle_outputs* out) {
   const uint32_t N = pr->subray_count;
   const double beta = pr->divergence_rad;
   const double delta = pr->bin_width_ns;
@@ -790,6 +887,8 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
 
   double Rs_out = kNaN, A_out = 0.0, gap_out = kInf, kmarg_out = kInf, umarg_out = kInf;
   uint32_t prim_out = 0xFFFFFFFFu;
+  uint32_t cand_out[kMaxCand];
+  for (int32_t c = 0; c < kMaxCand; ++c) cand_out[c] = 0xFFFFFFFFu;
   int64_t k_out = -1;
   int32_t ncand_out = 0;
   if (dn > 0.0) {
@@ -797,11 +896,13 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
       // O1: subray direction.
       double ds[3];
       oracle_subray_direction(d, theta[s], phi[s], ds);
-      // O2: nearest triangle, brute force.
+      // O2: nearest triangle, brute force: `hits` holds the ray's hit on EVERY
+      // triangle it meets (phase 1 of oracle_simulate)
       double t_tri = kInf, cos_inc = 0.0, gap = kInf;
       int32_t nc = 0;
-      int64_t tid = oracle_nearest_triangle(o, ds, sc->tris, sc->n_tris, &t_tri,
-                                            &cos_inc, &nc, &gap);
+      uint32_t cand[kMaxCand];
+      int64_t tid = nearest_from_hits(hits, &t_tri, &nc, &gap, cand, kMaxCand);
+      if (tid >= 0) oracle_ray_triangle(o, ds, sc->tris + 9ull * tid, &cos_inc);
       // O3: transmissive voxels before the triangle.
       bool vox_hit = false;
       double t_vox = 0.0, sigma_vox = 0.0;
@@ -846,9 +947,10 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
           double sigma = PAD * G;        // Eq. 4 via the G-LUT (R15)
           double L = tb[k] - ta[k];
           double u = oracle_transmission_u(pr->seed, pulse_id, s, vid[k]);
-          double pass_p = std::exp(-sigma * L);
-          um = std::min(um, std::fabs(u - pass_p));
-          if (u < pass_p) continue;      // s = -ln(u)/sigma > L: transmit (R17)
+          double margin = kInf;
+          const int pass = oracle_transmits(u, sigma, L, &margin);
+          um = std::min(um, margin);
+          if (pass) continue;            // s = -ln(u)/sigma > L: transmit (R17)
           vox_hit = true;                 // Eq. 6: echo at distance s into the voxel
           t_vox = ta[k] + (-std::log(u)) / sigma;
           sigma_vox = sigma;
@@ -876,11 +978,14 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
         A_out = K * sig_eff * Is / (Rs * Rs * Rs * Rs);                // Eq. 7
         Rs_out = Rs;
         prim_out = pid;
-        double x = 2.0 * Rs / kC / (delta * 1e-9);  // two-way time in bins (R8, R9)
-        k_out = (int64_t)std::floor(x);
-        kmarg_out = std::fabs(x - std::nearbyint(x));
+        k_out = oracle_bin_of(Rs, delta, &kmarg_out);  // two-way time in bins (R8, R9)
         ncand_out = vox_hit ? 1 : nc;
         gap_out = vox_hit ? kInf : gap;
+        if (vox_hit) {
+          cand_out[0] = pid;
+        } else {
+          for (int32_t c = 0; c < kMaxCand; ++c) cand_out[c] = cand[c];
+        }
       }
       umarg_out = um;
     }
@@ -894,20 +999,43 @@ static void simulate_subray(const oracle_scene* sc, const oracle_params* pr,
   out->sub_gap[x] = gap_out;
   out->sub_kmargin[x] = kmarg_out;
   out->sub_umargin[x] = umarg_out;
+  if (out->sub_cand)
+    for (int32_t c = 0; c < kMaxCand; ++c) out->sub_cand[x * kMaxCand + c] = cand_out[c];
 }
 
-/* Pulse i after all its subrays: steps O6..O8 (waveform, peaks, returns). */
-static void finish_pulse(const oracle_params* pr, double time_s, uint64_t pulse_id, int64_t i,
-                         const oracle_outputs* out) {
+/* Steps O6..O8 for ONE pulse from its subrays' amplitudes A[s], bins ks[s]
+ * (-1 = no event) and prims prim[s], s < N: the full waveform (Eq. 3, P:215,
+ * P:408), the local-maximum peaks (R11-R13) and the returns.
+ * Outputs (per pulse): *n_returns, *k0, W[n_bins] (may be NULL), the return
+ * arrays [max_returns] (range, time, intensity, prim, number, width) and
+ * ret_cand [max_returns][kMaxAttr] (may be NULL), *peak_margin, *attr_margin.
+ *
+ * Decision margins (C-4), what the CUDA path's arithmetic could flip:
+ *  - peak_margin: min over bins k of the margin of the decision "k is a
+ *    peak".  The decision is a > l AND a > r AND a >= thr M (a = W[k]); the
+ *    signed relative margins are (a - l)/max(a, l), (a - r)/max(a, r),
+ *    (a - thr M)/M.  A true decision flips if ANY conjunct flips: its margin
+ *    is the smallest |margin| of the three; a false one only if EVERY false
+ *    conjunct flips: its margin is the largest |margin| among them (a
+ *    comparison of two zero bins is false by any margin).
+ *  - attribution (R13): the prim of the largest contribution A_s p[k - o_s]
+ *    (ties -> lowest s); ret_cand lists the distinct prims whose contribution
+ *    is >= c_max (1 - kDecisionEps) (by contribution, then s); attr_margin =
+ *    min over returns of (c_max - c_other) / c_max, c_other = the largest
+ *    contribution of a DIFFERENT prim (+inf if none). */
+int oracle_waveform_peaks(const oracle_params* pr, const double* A, const int64_t* ks,
+                          const uint32_t* prim, double time_s, uint64_t pulse_id,
+                          int32_t* n_returns_out, int64_t* k0_out, double* W_out,
+                          double* ret_range, double* ret_time, double* ret_intensity,
+                          uint32_t* ret_prim, int32_t* ret_number, double* ret_width,
+                          uint32_t* ret_cand, double* peak_margin, double* attr_margin) {
   const uint32_t N = pr->subray_count;
   const double delta = pr->bin_width_ns;
   const double tau = pr->pulse_length_ns / 1.75;
   const uint32_t n_bins = oracle_waveform_bins(pr->max_fullwave_range_ns, delta);
+  if (n_bins == 0 || pr->max_returns < 1) return -1;
   const int64_t Lp = (int64_t)std::ceil(20.0 * tau / delta);           // R9
   const uint32_t maxr = pr->max_returns;
-  const double* A = out->sub_amp + i * (int64_t)N;
-  const uint32_t* prim = out->sub_prim + i * (int64_t)N;
-  const int64_t* ks = out->sub_k + i * (int64_t)N;
 
   // O6: full waveform (Eq. 3).
   int64_t k0 = -1;
@@ -947,16 +1075,30 @@ static void finish_pulse(const oracle_params* pr, double time_s, uint64_t pulse_
   int32_t nret = 0;
   double pmarg = kInf, amarg = kInf;
   for (int64_t k = 1; k + 1 < (int64_t)n_bins; ++k) {
-    // decision margins of the comparisons that involve a non-zero bin
     double a = W[k], l = W[k - 1], r = W[k + 1];
-    if (std::max(a, l) > 0.0) pmarg = std::min(pmarg, std::fabs(a - l) / std::max(a, l));
-    if (std::max(a, r) > 0.0) pmarg = std::min(pmarg, std::fabs(a - r) / std::max(a, r));
-    if (a > 0.0 && M > 0.0) pmarg = std::min(pmarg, std::fabs(a - thr) / M);
     bool peak = a > l && a > r && a >= thr;
+    // margin of this decision (see above)
+    {
+      const bool c[3] = {a > l, a > r, a >= thr};
+      const double m[3] = {
+          std::max(a, l) > 0.0 ? std::fabs(a - l) / std::max(a, l) : kInf,
+          std::max(a, r) > 0.0 ? std::fabs(a - r) / std::max(a, r) : kInf,
+          M > 0.0 ? std::fabs(a - thr) / M : kInf};
+      double mk;
+      if (peak) {
+        mk = std::min(m[0], std::min(m[1], m[2]));
+      } else {
+        mk = 0.0;
+        for (int q = 0; q < 3; ++q)
+          if (!c[q]) mk = std::max(mk, m[q]);
+      }
+      pmarg = std::min(pmarg, mk);
+    }
     if (!peak) continue;
     if ((uint32_t)nret >= maxr) continue;  // keep the earliest max_returns
     // Attribution (R13): subray with the largest contribution to bin k.
-    double c1 = -1.0, c2 = -1.0;
+    std::vector<std::pair<double, uint32_t>> contrib;  // (c, s)
+    double c1 = -1.0;
     uint32_t who = 0xFFFFFFFFu;
     for (uint32_t s = 0; s < N; ++s) {
       if (ks[s] < 0) continue;
@@ -965,26 +1107,42 @@ static void finish_pulse(const oracle_params* pr, double time_s, uint64_t pulse_
       int64_t j = k - off;
       if (j < 0 || j >= Lp) continue;
       double c = oracle_eq3_pulse(A[s], ((double)j + 0.5) * delta, tau);
+      contrib.push_back({c, s});
       if (c > c1) {
-        c2 = c1;
         c1 = c;
         who = prim[s];
-      } else if (c > c2) {
-        c2 = c;
       }
     }
-    if (c1 > 0.0 && c2 >= 0.0) amarg = std::min(amarg, (c1 - c2) / c1);
-    int64_t slot = i * (int64_t)maxr + nret;
-    out->ret_range[slot] =
-        0.5 * kC * ((double)(k0 + k - jstar) + 0.5) * delta * 1e-9;  // R12
+    double c_other = -1.0;
+    for (const auto& cs : contrib)
+      if (prim[cs.second] != who) c_other = std::max(c_other, cs.first);
+    if (c1 > 0.0 && c_other >= 0.0) amarg = std::min(amarg, (c1 - c_other) / c1);
+    int64_t slot = nret;
+    if (ret_cand) {
+      // distinct prims within kDecisionEps of the top, by (contribution desc, s)
+      std::sort(contrib.begin(), contrib.end(), [](const std::pair<double, uint32_t>& x,
+                                                   const std::pair<double, uint32_t>& y) {
+        return x.first > y.first || (x.first == y.first && x.second < y.second);
+      });
+      int32_t nc = 0;
+      for (int32_t q = 0; q < kMaxAttr; ++q) ret_cand[slot * kMaxAttr + q] = 0xFFFFFFFFu;
+      for (const auto& cs : contrib) {
+        if (!(cs.first >= c1 * (1.0 - kDecisionEps))) break;
+        const uint32_t pid = prim[cs.second];
+        bool seen = false;
+        for (int32_t q = 0; q < nc; ++q) seen |= ret_cand[slot * kMaxAttr + q] == pid;
+        if (!seen && nc < kMaxAttr) ret_cand[slot * kMaxAttr + nc++] = pid;
+      }
+    }
+    ret_range[slot] = 0.5 * kC * ((double)(k0 + k - jstar) + 0.5) * delta * 1e-9;  // R12
     if (pr->range_noise_sd_m > 0.0)  // P:288, R29
-      out->ret_range[slot] += pr->range_noise_sd_m *
-                              oracle_range_noise(pr->seed, pulse_id, (uint32_t)(nret + 1));
-    out->ret_time[slot] = time_s;
-    out->ret_intensity[slot] = a;
-    out->ret_prim[slot] = who;
-    out->ret_number[slot] = nret + 1;
-    out->ret_width[slot] =
+      ret_range[slot] += pr->range_noise_sd_m *
+                         oracle_range_noise(pr->seed, pulse_id, (uint32_t)(nret + 1));
+    ret_time[slot] = time_s;
+    ret_intensity[slot] = a;
+    ret_prim[slot] = who;
+    ret_number[slot] = nret + 1;
+    ret_width[slot] =
         pr->fit_echo_width
             ? oracle_fit_echo_width(W.data(), n_bins, k, delta, pr->pulse_length_ns, nullptr, nullptr)
             : kNaN;
@@ -992,12 +1150,29 @@ static void finish_pulse(const oracle_params* pr, double time_s, uint64_t pulse_
   }
 
   // O8: emit.
-  out->n_returns[i] = nret;
-  out->k0[i] = k0;
-  if (out->waveform)
-    for (uint32_t k = 0; k < n_bins; ++k) out->waveform[i * (int64_t)n_bins + k] = W[k];
-  out->peak_margin[i] = pmarg;
-  out->attr_margin[i] = amarg;
+  *n_returns_out = nret;
+  *k0_out = k0;
+  if (W_out)
+    for (uint32_t k = 0; k < n_bins; ++k) W_out[k] = W[k];
+  *peak_margin = pmarg;
+  *attr_margin = amarg;
+  return 0;
+}
+
+/* Pulse i after all its subrays: steps O6..O8 on the pulse's row of the
+ * per-subray outputs. */
+static void finish_pulse(const oracle_params* pr, double time_s, uint64_t pulse_id, int64_t i,
+                         const oracle_outputs* out) {
+  const uint32_t N = pr->subray_count;
+  const uint32_t n_bins = oracle_waveform_bins(pr->max_fullwave_range_ns, pr->bin_width_ns);
+  const int64_t R = pr->max_returns;
+  oracle_waveform_peaks(pr, out->sub_amp + i * (int64_t)N, out->sub_k + i * (int64_t)N,
+                        out->sub_prim + i * (int64_t)N, time_s, pulse_id, out->n_returns + i,
+                        out->k0 + i, out->waveform ? out->waveform + i * (int64_t)n_bins : nullptr,
+                        out->ret_range + i * R, out->ret_time + i * R, out->ret_intensity + i * R,
+                        out->ret_prim + i * R, out->ret_number + i * R, out->ret_width + i * R,
+                        out->ret_cand ? out->ret_cand + i * R * kMaxAttr : nullptr,
+                        out->peak_margin + i, out->attr_margin + i);
 }
 
 /* Simulate the listed pulses (a seeded subset or all of them).  pulse_ids
@@ -1027,12 +1202,15 @@ int oracle_simulate(const oracle_scene* sc, const oracle_params* pr,
       out->ret_prim[x] = 0;
       out->ret_number[x] = 0;
       out->ret_width[x] = kNaN;
+      if (out->ret_cand)
+        for (int32_t q = 0; q < kMaxAttr; ++q) out->ret_cand[x * kMaxAttr + q] = 0xFFFFFFFFu;
     }
   }
   if (n_threads < 1) n_threads = 1;
-  // Phase 1: every (pulse, subray) pair is independent; phase 2:
-  // every pulse's waveform and peaks.  Plain thread pool with an atomic work
-  // counter; nothing is reduced across threads (thread-count independent).
+  // Every (pulse, subray) pair is independent, then every pulse's
+  // waveform and peaks.  Plain thread pool with an atomic work counter;
+  // nothing is reduced across threads in a thread-dependent order
+  // (thread-count independent).
   auto run_pool = [&](int64_t n_items, auto&& body) {
     std::atomic<int64_t> next(0);
     auto worker = [&]() {
@@ -1047,11 +1225,65 @@ int oracle_simulate(const oracle_scene* sc, const oracle_params* pr,
     worker();
     for (auto& th : pool) th.join();
   };
+  // Phase 1: the hits of every subray on every triangle.  Work items are
+  // (pulse, block of triangles): each triangle of the block is tested
+  // against every subray of the pulse (one read of the scene per pulse).  A
+  // subray's hits from all blocks are concatenated; the nearest is the
+  // minimum of (t, id) over them, whatever their order.
+  const uint32_t kBlock = 1u << 18;
+  const int64_t nblk = sc->n_tris ? ((int64_t)sc->n_tris + kBlock - 1) / kBlock : 0;
+  // A triangle none of a pulse's subrays can reach (its bounding sphere
+  // outside the cone of half-angle max theta_i around the pulse axis) is
+  // skipped for that pulse (cone_may_hit; widened by 1e-6 relative + 1e-12).
+  double th_max = 0.0;
+  for (uint32_t s = 0; s < N; ++s) th_max = std::max(th_max, theta[s]);
+  th_max = th_max * (1.0 + 1e-6) + 1e-12;
+  const double cos_c = std::cos(th_max), sin_c = std::sin(th_max);
+  std::vector<double> dirs((size_t)n_pulses * N * 3, 0.0), axis((size_t)n_pulses * 3, 0.0);
+  std::vector<char> dir_ok(n_pulses, 0);
+  for (int64_t i = 0; i < n_pulses; ++i) {
+    const float* dv = directions + 3 * i;
+    const double d[3] = {dv[0], dv[1], dv[2]};
+    const double dn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    dir_ok[i] = dn > 0.0;
+    if (!dir_ok[i]) continue;
+    for (int c = 0; c < 3; ++c) axis[3 * i + c] = d[c] / dn;
+    for (uint32_t s = 0; s < N; ++s)
+      oracle_subray_direction(d, theta[s], phi[s], &dirs[((size_t)i * N + s) * 3]);  // O1
+  }
+  std::vector<HitList> blk_hits((size_t)n_pulses * nblk * N);
+  run_pool(n_pulses * nblk, [&](int64_t item) {
+    const int64_t i = item / nblk, b = item % nblk;
+    if (!dir_ok[i]) return;
+    const double o[3] = {origins[3 * i], origins[3 * i + 1], origins[3 * i + 2]};
+    const uint32_t t0 = (uint32_t)(b * kBlock);
+    const uint32_t t1 = (uint32_t)std::min<int64_t>((int64_t)sc->n_tris, (b + 1) * (int64_t)kBlock);
+    HitList* h = &blk_hits[((size_t)i * nblk + b) * N];
+    const V3 ov = {o[0], o[1], o[2]};
+    const V3 ax = {axis[3 * i], axis[3 * i + 1], axis[3 * i + 2]};
+    for (uint32_t t = t0; t < t1; ++t) {
+      const TriPre tp = tri_pre(sc->tris + 9ull * t);  // oracle_ray_triangle's first steps
+      if (!cone_may_hit(ov, ax, cos_c, sin_c, tp)) continue;
+      for (uint32_t s = 0; s < N; ++s) {
+        const double* dd = &dirs[((size_t)i * N + s) * 3];
+        const double tt = ray_triangle_pre(ov, V3{dd[0], dd[1], dd[2]}, tp.v0, tp.e1, tp.e2,
+                                           tp.cut);
+        if (tt >= 0.0) h[s].push_back({tt, t});
+      }
+    }
+  });
+  // Phase 2: per subray, steps O2 (from its hits) .. O5
   run_pool(n_pulses * (int64_t)N, [&](int64_t k) {
     const int64_t i = k / N;
     const uint32_t s = (uint32_t)(k % N);
+    HitList hits;
+    for (int64_t b = 0; b < nblk; ++b) {
+      HitList& hb = blk_hits[((size_t)i * nblk + b) * N + s];
+      hits.insert(hits.end(), hb.begin(), hb.end());
+      HitList().swap(hb);
+    }
     simulate_subray(sc, pr, origins + 3 * i, directions + 3 * i, pulse_ids[i], i, s,
-                    theta.data(), phi.data(), out);
+                    theta.data(), phi.data(), hits, out);
   });
   run_pool(n_pulses, [&](int64_t i) { finish_pulse(pr, times ? times[i] : 0.0, pulse_ids[i], i, out);
   });

@@ -17,8 +17,16 @@ from .helios import (  # noqa: F401
     helios_scene_create,
     helios_scene_destroy,
     helios_scene_get_info,
+    helios_get_tuning,
+    helios_set_tuning,
     helios_simulate,
+    helios_simulate_batches,
     helios_simulate_survey,
+    helios_tuning,
+    simulate_batches,
+    tuning,
+    util_scan_u64,
+    util_sort_pairs_u64,
     helios_version,
     helios_waveform_bins,
     lib,

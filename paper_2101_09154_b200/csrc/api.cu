@@ -1,7 +1,7 @@
 // api.cu -- the C ABI of libhelios.so (include/helios.h) and its host runtime:
 // argument validation, scene ownership, the beam-pattern tables, scratch
-// management (stream-ordered cudaMallocAsync), host<->device staging, pulse
-// chunking so the K6->K7 subray records stay L2-resident, and launches.
+// management (a library-private stream-ordered memory pool), host<->device
+// staging, the chunk pipeline over one or more pulse batches, and launches.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -12,15 +12,91 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <list>
 #include <mutex>
 #include <string>
 #include <vector>
 
-#include <cub/device/device_scan.cuh>
-
 #include "internal.cuh"
 
 using namespace helios;
+
+// ---- library-private device memory pool (one per device): every library
+// allocation is stream-ordered from it, and its release threshold is raised
+// so freed blocks stay mapped across synchronisations -- without touching the
+// device's default pool, which other libraries in the process share.
+namespace {
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+}  // namespace
+
+namespace helios {
+cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pool[dev]) {
+      cudaMemPoolProps pp{};
+      pp.allocType = cudaMemAllocationTypePinned;
+      pp.handleTypes = cudaMemHandleTypeNone;
+      pp.location.type = cudaMemLocationTypeDevice;
+      pp.location.id = dev;
+      e = cudaMemPoolCreate(&g_pool[dev], &pp);
+      if (e != cudaSuccess) return e;
+      uint64_t keep = std::numeric_limits<uint64_t>::max();
+      cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = g_pool[dev];
+  }
+  return cudaMallocFromPoolAsync(p, bytes ? bytes : 256, pool, s);
+}
+}  // namespace helios
+
+// ---- process-wide tuning switches (helios_set_tuning), seeded once from the
+// environment at first use; every call takes a snapshot when it starts
+namespace {
+std::mutex g_tune_mu;
+bool g_tune_init = false;
+helios_tuning g_tune{};
+
+helios_tuning tuning_defaults() {
+  helios_tuning t{};
+  t.beam_prepass = -1;
+  t.builder = 0;
+  t.lane_order = 1;
+  t.pad_lanes = -1;
+  t.serialize = 0;
+  t.trace_spans = 0;
+  t.chunk_pulses = 0;
+  return t;
+}
+
+helios_tuning tuning_snapshot() {
+  std::lock_guard<std::mutex> g(g_tune_mu);
+  if (!g_tune_init) {
+    g_tune = tuning_defaults();
+    auto env = [](const char* name, int64_t* v) {
+      const char* s = getenv(name);
+      if (s && *s) *v = atoll(s);
+      return s != nullptr;
+    };
+    int64_t v;
+    if (env("HELIOS_BEAM", &v)) g_tune.beam_prepass = (int32_t)v;
+    if (const char* b = getenv("HELIOS_BUILDER")) g_tune.builder = strcmp(b, "lbvh") == 0 ? 1 : 0;
+    if (env("HELIOS_LANE_ORDER", &v)) g_tune.lane_order = (int32_t)v;
+    if (env("HELIOS_PAD_LANES", &v)) g_tune.pad_lanes = (int32_t)v;
+    if (env("HELIOS_SERIALIZE", &v)) g_tune.serialize = (int32_t)v;
+    if (env("HELIOS_TRACE_SPANS", &v)) g_tune.trace_spans = (int32_t)v;
+    if (env("HELIOS_CHUNK_PULSES", &v)) g_tune.chunk_pulses = (uint64_t)std::max<int64_t>(0, v);
+    g_tune_init = true;
+  }
+  return g_tune;
+}
+}  // namespace
 
 struct helios_scene_s {
   uint32_t n_tris = 0;
@@ -41,148 +117,109 @@ struct helios_scene_s {
   BuildResult bvh{};
   int device = 0;
 
-  // Scratch cache: one device buffer per stream, grown on demand, reused by
-  // later calls on the same stream, freed by helios_scene_destroy.
+  // Scratch cache: one device buffer (+ the call's internal streams and a
+  // pinned mirror) per caller stream, grown on demand and reused by later
+  // calls on that stream.  Idle entries beyond kMaxIdle are evicted, least
+  // recently used first; destroy frees the rest.  Only streams the library
+  // created are ever synchronised here (never a caller's stream, which may
+  // no longer exist).
   struct Slot {
-    cudaStream_t stream;
+    cudaStream_t key;  // caller stream (not owned, never used after the call)
     char* ptr;
     size_t bytes;
     bool busy;
-    cudaStream_t copy;  // non-blocking host->device copy stream for host staging (lazy)
-    cudaStream_t copy_out;  // device->host copies (own stream: PCIe is full duplex)
-    cudaStream_t wave;  // non-blocking stream for K7, overlapping K6 (lazy)
-    cudaStream_t fit;   // non-blocking stream for the echo-width fits (lazy)
-    cudaStream_t trace2;  // second K6 stream: odd chunks, so a chunk's K6 fills the SMs
-                          // while the previous one's last wave drains (lazy)
-    cudaStream_t beam[2];  // K6a streams (normal / high priority; HELIOS_BEAM_STREAM, lazy)
-    uint64_t* pinned;   // 4 kSlots pinned words: per chunk slot (first, last) offsets of
-                        // the packed waveform rows [0, 2 kSlots) and packed returns (lazy)
+    uint64_t last_use;
+    cudaStream_t copy_in, copy_out, wave, fit, trace2;  // owned, created lazily
+    uint64_t* pinned;  // 4 kSlots words: per chunk slot (first, last) packed offsets
   };
+  static constexpr int kMaxIdle = 4;
   std::mutex mu;
-  std::vector<Slot> slots;
+  std::list<Slot> slots;  // stable addresses: a call keeps its Slot* while others acquire
+  uint64_t use_clock = 0;
 
-  cudaError_t acquire(cudaStream_t s, size_t bytes, char** out, cudaStream_t* copy,
-                      cudaStream_t* wave, uint64_t** pinned = nullptr,
-                      cudaStream_t* fit = nullptr, cudaStream_t* trace2 = nullptr,
-                      cudaStream_t* beam = nullptr, int beam_prio = 0) {
+  static void release_slot(Slot& sl) {
+    cudaStream_t own[5] = {sl.copy_in, sl.copy_out, sl.wave, sl.fit, sl.trace2};
+    for (cudaStream_t x : own)
+      if (x) cudaStreamSynchronize(x);
+    if (sl.ptr) {
+      // freed on an owned stream (or synchronously): the last use of the
+      // buffer was ordered before the end of the call that used it
+      if (sl.wave) {
+        cudaFreeAsync(sl.ptr, sl.wave);
+        cudaStreamSynchronize(sl.wave);
+      } else {
+        cudaFree(sl.ptr);
+      }
+    }
+    for (cudaStream_t x : own)
+      if (x) cudaStreamDestroy(x);
+    if (sl.pinned) cudaFreeHost(sl.pinned);
+    cudaGetLastError();
+  }
+
+  cudaError_t acquire(cudaStream_t s, size_t bytes, Slot** out) {
     std::lock_guard<std::mutex> g(mu);
     Slot* use = nullptr;
     for (Slot& sl : slots)
-      if (sl.stream == s && !sl.busy) {
+      if (sl.key == s && !sl.busy) {
         use = &sl;
         break;
       }
     if (!use) {
-      slots.push_back(Slot{s, nullptr, 0, false, nullptr, nullptr, nullptr, nullptr, nullptr,
-                           {nullptr, nullptr}, nullptr});
+      // evict the least recently used idle entries first (keeps the cache bounded)
+      int idle = 0;
+      for (const Slot& sl : slots) idle += !sl.busy;
+      while (idle >= kMaxIdle) {
+        auto lru = slots.end();
+        for (auto it = slots.begin(); it != slots.end(); ++it)
+          if (!it->busy && (lru == slots.end() || it->last_use < lru->last_use)) lru = it;
+        release_slot(*lru);
+        slots.erase(lru);
+        --idle;
+      }
+      slots.push_back(Slot{s, nullptr, 0, false, 0, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           nullptr});
       use = &slots.back();
     }
     if (use->bytes < bytes) {
       if (use->ptr) cudaFreeAsync(use->ptr, s);
       use->ptr = nullptr;
       use->bytes = 0;
-      cudaError_t e = cudaMallocAsync((void**)&use->ptr, bytes ? bytes : 256, s);
+      cudaError_t e = dev_alloc((void**)&use->ptr, bytes, s);
       if (e != cudaSuccess) return e;
       use->bytes = bytes;
     }
-    if (copy) {
-      if (!use->copy) {
-        cudaError_t e = cudaStreamCreateWithFlags(&use->copy, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return e;
-      }
-      if (!use->copy_out) {
-        cudaError_t e = cudaStreamCreateWithFlags(&use->copy_out, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return e;
-      }
-      copy[0] = use->copy;
-      copy[1] = use->copy_out;
-    }
-    if (!use->wave) {
-      // K7 (and the packed-output scans, fits and copies it feeds) at high
-      // priority: its blocks are scheduled ahead of the queued blocks of the
-      // next chunks' K6 grids, so a chunk's outputs do not wait for them to
-      // drain (HELIOS_WAVE_PRIO=0: normal priority, A/B)
+    auto make = [](cudaStream_t* st, int prio_hi) -> cudaError_t {
+      if (*st) return cudaSuccess;
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      int prio = hi;
-      if (const char* v = getenv("HELIOS_WAVE_PRIO")) prio = atoi(v) ? hi : lo;
-      cudaError_t e = cudaStreamCreateWithPriority(&use->wave, cudaStreamNonBlocking, prio);
-      if (e != cudaSuccess) return e;
-    }
-    *wave = use->wave;
-    if (fit) {
-      if (!use->fit) {
-        cudaError_t e = cudaStreamCreateWithFlags(&use->fit, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return e;
-      }
-      *fit = use->fit;
-    }
-    if (trace2) {
-      if (!use->trace2) {
-        cudaError_t e = cudaStreamCreateWithFlags(&use->trace2, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return e;
-      }
-      *trace2 = use->trace2;
-    }
-    if (beam) {
-      cudaStream_t& b = use->beam[beam_prio ? 1 : 0];
-      if (!b) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi: numerically lowest = highest
-        cudaError_t e = cudaStreamCreateWithPriority(&b, cudaStreamNonBlocking, beam_prio ? hi : lo);
-        if (e != cudaSuccess) return e;
-      }
-      *beam = b;
-    }
+      return cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, prio_hi ? hi : lo);
+    };
+    cudaError_t e;
+    // K7 (and the scans, fits and copies it feeds) at high priority: its
+    // blocks are scheduled ahead of the queued blocks of the next chunks' K6
+    // grids, so a chunk's outputs do not wait for them to drain
+    if ((e = make(&use->wave, 1)) != cudaSuccess) return e;
+    if ((e = make(&use->copy_in, 0)) != cudaSuccess) return e;
+    if ((e = make(&use->copy_out, 0)) != cudaSuccess) return e;
+    if ((e = make(&use->fit, 0)) != cudaSuccess) return e;
+    if ((e = make(&use->trace2, 0)) != cudaSuccess) return e;
     if (!use->pinned) {
-      cudaError_t e = cudaMallocHost((void**)&use->pinned, 4 * kSlots * sizeof(uint64_t));
+      e = cudaMallocHost((void**)&use->pinned, 4 * kSlots * sizeof(uint64_t));
       if (e != cudaSuccess) return e;
     }
     use->busy = true;
-    *out = use->ptr;
-    if (pinned) *pinned = use->pinned;
+    use->last_use = ++use_clock;
+    *out = use;
     return cudaSuccess;
   }
-  void release(cudaStream_t s) {
+  void release(Slot* sl) {
     std::lock_guard<std::mutex> g(mu);
-    for (Slot& sl : slots)
-      if (sl.stream == s && sl.busy) {
-        sl.busy = false;
-        return;
-      }
+    sl->busy = false;
   }
   void free_slots() {
     std::lock_guard<std::mutex> g(mu);
-    for (Slot& sl : slots) {
-      cudaStreamSynchronize(sl.stream);
-      if (sl.copy) {
-        cudaStreamSynchronize(sl.copy);
-        cudaStreamDestroy(sl.copy);
-      }
-      if (sl.copy_out) {
-        cudaStreamSynchronize(sl.copy_out);
-        cudaStreamDestroy(sl.copy_out);
-      }
-      if (sl.wave) {
-        cudaStreamSynchronize(sl.wave);
-        cudaStreamDestroy(sl.wave);
-      }
-      if (sl.fit) {
-        cudaStreamSynchronize(sl.fit);
-        cudaStreamDestroy(sl.fit);
-      }
-      if (sl.trace2) {
-        cudaStreamSynchronize(sl.trace2);
-        cudaStreamDestroy(sl.trace2);
-      }
-      for (cudaStream_t b : sl.beam)
-        if (b) {
-          cudaStreamSynchronize(b);
-          cudaStreamDestroy(b);
-        }
-      cudaFree(sl.ptr);
-      if (sl.pinned) cudaFreeHost(sl.pinned);
-    }
+    for (Slot& sl : slots) release_slot(sl);
     slots.clear();
   }
 };
@@ -213,12 +250,6 @@ helios_status cuda_fail(cudaError_t e, const char* what) {
   return fail(HELIOS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-#define TRY_CUDA(expr, what)                        \
-  do {                                              \
-    cudaError_t e_ = (expr);                        \
-    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
-  } while (0)
-
 bool device_accessible(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -227,26 +258,6 @@ bool device_accessible(const void* p) {
     return false;
   }
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
-}
-
-// Kernels may store straight into page-locked host memory mapped into the
-// device address space (UVA: the same address).  Used for the packed
-// outputs, whose per-chunk extent is only known on the device: the packing
-// kernels write them over PCIe with coalesced 128-byte stores, and the host
-// never has to learn a chunk's range before its copy.  Opt-in
-// (HELIOS_DIRECT_HOST=1): measured slower than the staged copies (C2 e2e
-// 7.9 -> 9.4 ms per 1 M pulses, profiles/r01s2_e2e.txt).
-bool kernel_writable(const void* p) {
-  if (!p) return false;
-  cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return true;
-  const char* v = getenv("HELIOS_DIRECT_HOST");  // opt-in: measured slower than staging
-  if (!v || !atoi(v)) return false;
-  return at.type == cudaMemoryTypeHost && at.devicePointer == p;
 }
 
 // ---- subray pattern (P:199 / R1): paper rule floor(2 pi i), or hexagonal 6i
@@ -429,9 +440,10 @@ __global__ void k_check_scene(const float* __restrict__ xyz, uint64_t n_xyz,
   }
 }
 
+
 template <class T>
 cudaError_t copy_in(T** dst, const T* src, size_t count, cudaStream_t s) {
-  cudaError_t e = cudaMallocAsync((void**)dst, sizeof(T) * (count ? count : 1), s);
+  cudaError_t e = dev_alloc((void**)dst, sizeof(T) * (count ? count : 1), s);
   if (e != cudaSuccess) return e;
   if (count) e = cudaMemcpyAsync(*dst, src, sizeof(T) * count, cudaMemcpyDefault, s);
   return e;
@@ -446,15 +458,8 @@ void free_scene(helios_scene sc, cudaStream_t s) {
   cudaFreeAsync(sc->d_bricks, s);
   cudaFreeAsync(sc->bvh.tris, s);
   cudaFreeAsync(sc->bvh.nodes, s);
-  cudaFreeAsync(sc->bvh.nodes4, s);
   cudaStreamSynchronize(s);
 }
-
-// one argument array: device-accessible as given, or staged through scratch
-struct Staged {
-  void* dev = nullptr;
-  bool owned = false;
-};
 
 }  // namespace
 
@@ -462,7 +467,7 @@ extern "C" {
 
 const char* helios_last_error(void) { return g_err.c_str(); }
 
-const char* helios_version(void) { return "helios-b200 0.1 sm_100a"; }
+const char* helios_version(void) { return "helios-b200 0.2 sm_100a"; }
 
 helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream stream,
                                   helios_scene* out) {
@@ -512,15 +517,6 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
   helios_scene sc = new (std::nothrow) helios_scene_s();
   if (!sc) return fail(HELIOS_ERR_OUT_OF_MEMORY, "host allocation failed");
   cudaGetDevice(&sc->device);
-  {
-    // keep stream-ordered allocations mapped across synchronisations
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, sc->device) == cudaSuccess) {
-      uint64_t keep = std::numeric_limits<uint64_t>::max();
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-  }
   sc->n_tris = desc->n_tris;
   cudaError_t e = cudaSuccess;
   unsigned* d_bad = nullptr;
@@ -549,7 +545,7 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
       sc->nby = (sc->ny + (1u << kBrickShift) - 1) >> kBrickShift;
       sc->nbz = (sc->nz + (1u << kBrickShift) - 1) >> kBrickShift;
       const size_t nbr = (size_t)sc->nbx * sc->nby * sc->nbz;
-      if ((e = cudaMallocAsync((void**)&sc->d_bricks, nbr, s)) != cudaSuccess) break;
+      if ((e = dev_alloc((void**)&sc->d_bricks, nbr, s)) != cudaSuccess) break;
       if ((e = cudaMemsetAsync(sc->d_bricks, 0, nbr, s)) != cudaSuccess) break;
       k_bricks<<<(unsigned)std::min<uint64_t>((nvox + 255) / 256, 148ull * 32), 256, 0, s>>>(
           sc->d_pad, sc->nx, sc->ny, sc->nz, sc->nbx, sc->nby, sc->d_bricks);
@@ -559,7 +555,7 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
       sc->n_lut = desc->n_lut;
       if ((e = copy_in(&sc->d_lut, desc->h_g_lut, desc->n_lut, s)) != cudaSuccess) break;
     }
-    if ((e = cudaMallocAsync((void**)&d_bad, sizeof(unsigned), s)) != cudaSuccess) break;
+    if ((e = dev_alloc((void**)&d_bad, sizeof(unsigned), s)) != cudaSuccess) break;
     if ((e = cudaMemsetAsync(d_bad, 0, sizeof(unsigned), s)) != cudaSuccess) break;
     k_check_scene<<<148 * 4, 256, 0, s>>>(sc->d_xyz, 9ull * sc->n_tris, sc->d_refl,
                                          sc->d_refl ? sc->n_tris : 0, sc->d_pad,
@@ -593,7 +589,9 @@ helios_status helios_build_accel(helios_scene sc, helios_stream stream) {
   if (sc->built) return HELIOS_OK;
   const cudaStream_t s = (cudaStream_t)stream;
   char err[256] = {0};
-  cudaError_t e = build_lbvh(sc->d_xyz, sc->d_refl, sc->n_tris, s, &sc->bvh, err, sizeof(err));
+  const helios_tuning tu = tuning_snapshot();
+  cudaError_t e = build_lbvh(sc->d_xyz, sc->d_refl, sc->n_tris, tu.builder, s, &sc->bvh, err,
+                             sizeof(err));
   if (e != cudaSuccess) {
     cudaGetLastError();
     if (e == cudaErrorMemoryAllocation)
@@ -674,16 +672,36 @@ helios_status validate_survey(const helios_survey* v) {
   return HELIOS_OK;
 }
 
-// helios_simulate (survey == nullptr: pulses from the caller's arrays) and
-// helios_simulate_survey (pulses generated on the device, survey pulse
-// first_pulse + i for pulse i of the call).
+
+// ---------------------------------------------------------------------------
+// The chunk pipeline.  One call simulates one or more pulse batches ("jobs":
+// helios_simulate = 1, helios_simulate_batches = n, helios_simulate_survey =
+// 1 generated on the device).  Every job is cut into chunks; the chunks of all
+// jobs form ONE pipeline over kSlots rotating scratch slots, so the head of a
+// batch (its first K6a + K6) overlaps the tail of the previous one (its last
+// K7 and copy-outs).  Per chunk c (slot = c % kSlots):
+//   s  (or ts2 for odd c) : [wait inputs]  K0 (survey)  K6a  K6        -> t_done
+//   ws (high priority)    : wait t_done    support scan  K7  [noise]   -> w_done
+//   fs                    : echo-width fits (optional)                 -> w_done
+//   cs                    : H2D of chunk c+1's host inputs             -> in_done
+//   co                    : D2H of chunk c-2's host outputs            -> out_done
+// ---------------------------------------------------------------------------
+struct Job {
+  const helios_pulses* pulses;
+  const helios_outputs* out;
+};
+
+enum Arr { A_ORIGIN = 0, A_DIR, A_TIME, A_NRET, A_RET, A_K0, A_WF, A_HITS, A_COUNT };
+
 helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params,
-                            const helios_pulses* pulses, const helios_survey* survey,
-                            uint64_t first_pulse, const helios_outputs* outputs,
-                            helios_stream stream, helios_stats* stats) {
+                            const Job* jobs, uint32_t n_jobs, const helios_survey* survey,
+                            uint64_t first_pulse, helios_stream stream, helios_stats* stats) {
   g_err.clear();
   if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
-  if (!pulses || !outputs) return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs is NULL");
+  if (!jobs || n_jobs == 0) return fail(HELIOS_ERR_INVALID_ARGUMENT, "no pulse batch given");
+  for (uint32_t j = 0; j < n_jobs; ++j)
+    if (!jobs[j].pulses || !jobs[j].out)
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs of batch %u is NULL", j);
   if (survey) {
     const helios_status vs = validate_survey(survey);
     if (vs != HELIOS_OK) return vs;
@@ -692,34 +710,118 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   helios_status st = validate_params(params, &d);
   if (st != HELIOS_OK) return st;
   if (!sc->built) return fail(HELIOS_ERR_NOT_BUILT, "helios_build_accel has not been called");
+  const helios_tuning tu = tuning_snapshot();
   const bool counters = stats && stats->collect_counters;
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->collect_counters = counters ? 1u : 0u;
   }
-  const uint64_t n = pulses->n_pulses;
-  if (n == 0) return HELIOS_OK;
-  if (!survey && (!pulses->p_origin || !pulses->p_direction))
-    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_origin/p_direction is NULL");
-  if (!outputs->p_n_returns || !outputs->p_wf_first_bin ||
-      (!outputs->p_returns && !outputs->p_returns_packed))
-    return fail(HELIOS_ERR_INVALID_ARGUMENT,
-                "p_n_returns/p_wf_first_bin and p_returns or p_returns_packed must not be NULL");
-  if (outputs->p_returns_packed && !outputs->p_return_offset)
-    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_returns_packed needs p_return_offset");
-  if (outputs->p_wf_compact && !outputs->p_wf_offset)
-    return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_wf_compact needs p_wf_offset");
   const uint32_t N = params->subray_count;
   const uint32_t R = params->max_returns;
+  const bool gen = survey != nullptr;
+  uint64_t total_n = 0;
+  for (uint32_t j = 0; j < n_jobs; ++j) {
+    const helios_pulses* P = jobs[j].pulses;
+    const helios_outputs* O = jobs[j].out;
+    if (P->n_pulses == 0) continue;
+    total_n += P->n_pulses;
+    if (!gen && (!P->p_origin || !P->p_direction))
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "p_origin/p_direction of batch %u is NULL", j);
+    if (!O->p_n_returns || !O->p_wf_first_bin || (!O->p_returns && !O->p_returns_packed))
+      return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                  "batch %u: p_n_returns/p_wf_first_bin and p_returns or p_returns_packed must "
+                  "not be NULL", j);
+    if (O->p_returns_packed && !O->p_return_offset)
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "batch %u: p_returns_packed needs p_return_offset", j);
+    if (O->p_wf_compact && !O->p_wf_offset)
+      return fail(HELIOS_ERR_INVALID_ARGUMENT, "batch %u: p_wf_compact needs p_wf_offset", j);
+  }
+  if (total_n == 0) return HELIOS_OK;
   const cudaStream_t s = (cudaStream_t)stream;
-  const bool want_offs = outputs->p_wf_offset != nullptr;
-  const bool compact_staged = outputs->p_wf_compact && !kernel_writable(outputs->p_wf_compact);
-  const bool packed = outputs->p_returns_packed != nullptr;
-  const bool packed_staged = packed && !kernel_writable(outputs->p_returns_packed);
+
+  // ---- per-job argument arrays: device-accessible as given, else staged
+  // per chunk through the slot's scratch buffers
+  const size_t per_pulse[A_COUNT] = {12, 12, 8, 1, sizeof(helios_return) * R, 8, 4ull * d.n_bins,
+                                     sizeof(helios_subray_hit) * N};
+  const bool is_in[A_COUNT] = {!gen, !gen, !gen, false, false, false, false, false};
+  std::vector<const void*> user(n_jobs * A_COUNT);
+  std::vector<char> staged(n_jobs * A_COUNT, 0);
+  std::vector<char> want_offs(n_jobs), compact_staged(n_jobs), packed(n_jobs),
+      packed_staged(n_jobs), job_staged(n_jobs);
+  bool stage_any[A_COUNT] = {false};
+  bool any_staged = false, any_offs = false, any_packed = false, any_cstaged = false,
+       any_pstaged = false;
+  for (uint32_t j = 0; j < n_jobs; ++j) {
+    const helios_pulses* P = jobs[j].pulses;
+    const helios_outputs* O = jobs[j].out;
+    const void* u[A_COUNT] = {gen ? (const void*)O->p_beam_origin : P->p_origin,
+                              gen ? (const void*)O->p_beam_direction : P->p_direction,
+                              gen ? (const void*)O->p_beam_time : P->p_time_s,
+                              O->p_n_returns, O->p_returns, O->p_wf_first_bin, O->p_waveform,
+                              O->p_subray_hits};
+    for (int a = 0; a < A_COUNT; ++a) {
+      user[j * A_COUNT + a] = u[a];
+      if (P->n_pulses && u[a] && !device_accessible(u[a])) {
+        staged[j * A_COUNT + a] = 1;
+        stage_any[a] = true;
+        job_staged[j] = 1;
+      }
+    }
+    want_offs[j] = O->p_wf_offset != nullptr;
+    compact_staged[j] = O->p_wf_compact && !device_accessible(O->p_wf_compact);
+    packed[j] = O->p_returns_packed != nullptr;
+    packed_staged[j] = packed[j] && !device_accessible(O->p_returns_packed);
+    job_staged[j] |= compact_staged[j] | packed_staged[j];
+    any_offs |= want_offs[j] != 0;
+    any_packed |= packed[j] != 0;
+    any_cstaged |= compact_staged[j] != 0;
+    any_pstaged |= packed_staged[j] != 0;
+    any_staged |= job_staged[j] != 0;
+  }
+  // arrays the kernels need although the caller passed none: generated pulses
+  // without an export (survey), fixed return slots with packed returns only
+  auto internal = [&](uint32_t j, int a) {
+    return !user[(size_t)j * A_COUNT + a] && ((gen && a <= A_TIME) || a == A_RET);
+  };
+  bool internal_any[A_COUNT] = {false};
+  for (uint32_t j = 0; j < n_jobs; ++j)
+    for (int a = 0; a < A_COUNT; ++a) internal_any[a] |= jobs[j].pulses->n_pulses && internal(j, a);
+
+  // ---- beam pre-pass K6a (packet traversal from per-pulse entry lists; trees
+  // with internal nodes, beams of >= 7 subrays) unless switched off
+  const bool beam_ok = N >= 7 && sc->n_tris > 0 && !ref_is_leaf(sc->bvh.root);
+  const bool beam = beam_ok && tu.beam_prepass != 0;
+
+  // ---- chunks.  Without the pre-pass: the K6 -> K7 records (12 B per subray)
+  // stay L2-resident.  With it (or a voxel grid), per-chunk tails dominate:
+  // >= 2 chunks per batch of <= 64 Mi subrays (>= 4 when it has host outputs)
+  struct Chunk {
+    uint32_t job;
+    uint64_t b, m;
+  };
+  std::vector<Chunk> chunks;
+  uint64_t chunk_max = 0;
+  for (uint32_t j = 0; j < n_jobs; ++j) {
+    const uint64_t n = jobs[j].pulses->n_pulses;
+    if (n == 0) continue;
+    uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (12ull * N)));
+    if (beam || sc->d_pad != nullptr) {
+      constexpr uint64_t kBeamChunkSubrays = 64ull << 20;
+      uint64_t k = std::max<uint64_t>(2, (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
+      if (job_staged[j]) k = std::max<uint64_t>(k, 4);
+      chunk = std::max(chunk, (n + k - 1) / k);
+    }
+    if (tu.chunk_pulses >= 1024) chunk = std::min<uint64_t>(n, tu.chunk_pulses);
+    for (uint64_t b = 0; b < n; b += chunk) chunks.push_back({j, b, std::min(chunk, n - b)});
+    chunk_max = std::max(chunk_max, chunk);
+  }
+  // per-job bases of the call-wide offset arrays (packed outputs)
+  std::vector<uint64_t> job_off(n_jobs + 1, 0);
+  for (uint32_t j = 0; j < n_jobs; ++j) job_off[j + 1] = job_off[j] + jobs[j].pulses->n_pulses + 1;
 
   // ---- host tables
   const std::vector<SubrayConst> tab = subray_table(N, params->divergence_rad, d.pt);
-  std::vector<SubrayConst> lanes;  // K6's lane order of tab (set below)
+  const std::vector<SubrayConst> lanes = tu.lane_order ? lane_order(tab) : tab;
   const double beta = params->divergence_rad;
   const double K = params->efficiency * params->receiver_diameter_m * params->receiver_diameter_m /
                    (4.0 * kPi * beta * beta);  // Eq. 7 (R14)
@@ -727,197 +829,96 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (plan.warps == 0)
     return fail(HELIOS_ERR_CUDA, "helios_simulate: waveform kernel cannot be configured");
 
-  // ---- argument arrays: device-accessible as given, or staged per chunk.
-  // Per-pulse bytes of each array; chunk-local offsets are (b * per_pulse).
-  struct Arr {
-    const void* user;
-    size_t per_pulse;
-    bool in;      // host->device before the chunk's kernels, else device->host after
-    bool staged;  // host memory: two chunk buffers in scratch (double buffering)
-    size_t off[kSlots];
-    bool gen;     // pulse array written by the on-device generator (survey mode), or
-                  // any array the kernels need: internal slots when the user passes NULL
-  };
-  const bool gen = survey != nullptr;
-  Arr arrs[] = {
-      {gen ? (const void*)outputs->p_beam_origin : pulses->p_origin, 12, !gen, false, {0, 0}, gen},
-      {gen ? (const void*)outputs->p_beam_direction : pulses->p_direction, 12, !gen, false,
-       {0, 0}, gen},
-      {gen ? (const void*)outputs->p_beam_time : pulses->p_time_s, 8, !gen, false, {0, 0}, gen},
-      {outputs->p_n_returns, 1, false, false, {0, 0}, false},
-      {outputs->p_returns, sizeof(helios_return) * R, false, false, {0, 0}, packed},
-      {outputs->p_wf_first_bin, 8, false, false, {0, 0}, false},
-      {outputs->p_waveform, 4ull * d.n_bins, false, false, {0, 0}, false},
-      {outputs->p_subray_hits, sizeof(helios_subray_hit) * N, false, false, {0, 0}, false},
-  };
-  bool any_staged = compact_staged || packed_staged;
-  bool gen_staged = false;  // a generated array is copied out to host memory
-  for (Arr& a : arrs)
-    if (a.user && !device_accessible(a.user)) {
-      a.staged = any_staged = true;
-      gen_staged |= a.gen;
-    }
-
-  // beam pre-pass K6a (packet traversal of a tree with internal nodes, beams of
-  // >= 7 subrays); HELIOS_BEAM=0/1 forces, HELIOS_BEAM_K sets the hand-over size.
-  // (An early version cost 6 % on C6's 1 622 triangles; with the later K6/K6a
-  // changes it gains 19 % there: no scene-size threshold.)
-  const bool beam_ok = N >= 7 && sc->n_tris > 0 && !ref_is_leaf(sc->bvh.root);
-  bool beam = beam_ok;
-  if (const char* v = getenv("HELIOS_BEAM")) beam = beam_ok && atoi(v) != 0;
-  // Chunk size.  Without the pre-pass: the K6 -> K7 records (16 B per subray)
-  // stay L2-resident.  With it, per-chunk tails (K6a's longest cone walks, K6's
-  // last wave) dominate: few chunks of up to kBeamChunkSubrays subrays, balanced
-  // (measured: profiles/r01s3_beam_ab.txt, C3 +33 %, C5 +13 %).
-  uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (16ull * N)));
-  // (the same for voxel scenes, whose K6 and K7 run serially: C4 +7 %)
-  if ((beam || sc->d_pad != nullptr) && n > 0) {
-    constexpr uint64_t kBeamChunkSubrays = 64ull << 20;
-    // at least 2 chunks (K7 of the first overlaps K6 of the second); measured
-    // per 1M-pulse call: C5 1/2/3 chunks 7361/7214/7135, C3 2 best (9300),
-    // C2 2 best (6703) -- profiles/r01s3_beam_ab.txt item 27
-    uint64_t k = std::max<uint64_t>(2, (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
-    // host outputs: at least a few chunks, so copy-outs overlap later chunks'
-    // kernels (HELIOS_STAGED_MIN_CHUNKS, default 4)
-    if (any_staged) {
-      uint64_t kmin = 4;
-      if (const char* v = getenv("HELIOS_STAGED_MIN_CHUNKS")) kmin = std::max(1, atoi(v));
-      k = std::max(k, kmin);
-    }
-    chunk = std::max(chunk, (n + k - 1) / k);
-  }
-  if (const char* v = getenv("HELIOS_CHUNK_PULSES"))  // experiments: chunk size override
-    if (atoll(v) >= 1024) chunk = std::min<uint64_t>(n, (uint64_t)atoll(v));
-  // chunk c covers pulses [cstart[c], cstart[c+1]).  Option: split the last
-  // chunk so its K7, which nothing overlaps, is short (HELIOS_TAIL_FRAC of it
-  // last; measured: C5 +2 %, C3 -6 % -> off by default)
-  std::vector<uint64_t> cstart;
-  for (uint64_t b = 0; b < n; b += chunk) cstart.push_back(b);
-  // option: a short first chunk (HELIOS_HEAD_FRAC of a chunk), so the first
-  // K6 starts after a short K6a (A/B)
-  if (beam && cstart.size() >= 2) {
-    double f = 0.0;
-    if (const char* v = getenv("HELIOS_HEAD_FRAC")) f = atof(v);
-    const uint64_t head = (uint64_t)(f * (double)chunk);
-    if (f > 0.0 && head >= 4096 && head < chunk) cstart.insert(cstart.begin() + 1, head);
-  }
-  if (beam && cstart.size() >= 2) {
-    double f = 0.0;
-    if (const char* v = getenv("HELIOS_TAIL_FRAC")) f = atof(v);
-    const uint64_t last = cstart.back(), len = n - last;
-    const uint64_t tail = (uint64_t)(f * (double)len);
-    if (f > 0.0 && tail >= 4096 && tail < len) cstart.push_back(n - tail);
-  }
-  cstart.push_back(n);
-  const bool own_rec = outputs->p_subray_hits == nullptr;
+  // ---- scratch layout
   size_t total = 0;
   auto carve = [&](size_t bytes) {
     const size_t at = total;
     total += (bytes + 255) & ~(size_t)255;
     return at;
   };
+  const uint64_t C = chunk_max;
   const size_t o_tab = carve(sizeof(SubrayConst) * N);
   const size_t o_ker = carve(sizeof(double) * d.taps);
   const size_t o_err = carve(sizeof(unsigned));
   const size_t o_cnt = carve(sizeof(unsigned long long) * 8);
   const size_t o_ws = carve(plan.scratch_bytes);
-  // two record buffers: K6 of chunk c+1 overlaps K7 of chunk c
-  size_t o_rec[kSlots];
-  for (int k = 0; k < kSlots; ++k) o_rec[k] = carve(own_rec ? sizeof(helios_subray_hit) * N * chunk : 0);
-  for (Arr& a : arrs)
-    if (a.staged || (a.gen && !a.user))  // staged, or generated with no export
-      for (int k = 0; k < kSlots; ++k) a.off[k] = carve(a.per_pulse * chunk);
+  size_t o_wrec[kSlots], o_prim[kSlots], o_arr[A_COUNT][kSlots] = {}, o_ent[kSlots],
+      o_frm[kSlots], o_fjob[kSlots], o_fy[kSlots], o_cst[kSlots], o_rst[kSlots];
+  for (int k = 0; k < kSlots; ++k) {
+    o_wrec[k] = carve(sizeof(WaveRec) * N * C);
+    o_prim[k] = carve(sizeof(uint32_t) * N * C);
+  }
+  for (int a = 0; a < A_COUNT; ++a)
+    if (stage_any[a] || internal_any[a])
+      for (int k = 0; k < kSlots; ++k) o_arr[a][k] = carve(per_pulse[a] * C);
   const size_t o_wp = carve(gen ? sizeof(double) * 3 * survey->n_waypoints : 0);
-  size_t o_ent[kSlots];
-  for (int k = 0; k < kSlots; ++k) o_ent[k] = carve(beam ? sizeof(int2) * kEntryStride * chunk : 0);
-  size_t o_frm[kSlots];  // K6a's pulse frames (10 doubles per pulse)
-  for (int k = 0; k < kSlots; ++k) o_frm[k] = carve(beam ? sizeof(double) * 10 * chunk : 0);
-  // compact output: per-pulse lengths, call-wide offsets, scan temp, staging
-  size_t scan_bytes = 0;
-  if (want_offs)
-    cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (int)chunk, s);
-  const size_t o_len = carve(want_offs ? sizeof(uint64_t) * chunk : 0);
-  const size_t o_offs = carve(want_offs ? sizeof(uint64_t) * (n + 1) : 0);
-  const size_t o_scan = carve(want_offs ? scan_bytes : 0);
-  // echo-width jobs of one K7 launch (K7 and k_fit are serial on their stream)
+  for (int k = 0; k < kSlots; ++k) {
+    o_ent[k] = carve(beam ? sizeof(int2) * kEntryStride * C : 0);
+    o_frm[k] = carve(beam ? sizeof(double) * 10 * C : 0);
+  }
+  const size_t scan_bytes = scan_temp_bytes(C, sizeof(uint64_t));
+  const size_t o_len = carve(any_offs ? sizeof(uint64_t) * C : 0);
+  const size_t o_offs = carve(any_offs ? sizeof(uint64_t) * job_off[n_jobs] : 0);
+  const size_t o_scan = carve(any_offs ? scan_bytes : 0);
   const uint32_t fit_stride = 2u * (uint32_t)std::ceil(3.0 * params->pulse_length_ns /
                                                         params->bin_width_ns) + 1u;
   const bool fit = params->fit_echo_width != 0;
-  // two job buffers: k_fit(c) on its own stream overlaps K7(c+1) and K6(c+2)
-  size_t o_fjob[kSlots], o_fy[kSlots], o_cst[kSlots], o_rst[kSlots];
-  for (int k = 0; k < kSlots; ++k) o_fjob[k] = carve(fit ? sizeof(FitJob) * chunk * R : 0);
-  for (int k = 0; k < kSlots; ++k)
-    o_fy[k] = carve(fit ? sizeof(double) * fit_stride * chunk * R : 0);
+  for (int k = 0; k < kSlots; ++k) {
+    o_fjob[k] = carve(fit ? sizeof(FitJob) * C * R : 0);
+    o_fy[k] = carve(fit ? sizeof(double) * fit_stride * C * R : 0);
+    o_cst[k] = carve(any_cstaged ? 4ull * d.n_bins * C : 0);
+    o_rst[k] = carve(any_pstaged ? sizeof(helios_return) * R * C : 0);
+  }
   const size_t o_fcnt = carve(fit ? kSlots * sizeof(unsigned) : 0);
-  for (int k = 0; k < kSlots; ++k) o_cst[k] = carve(compact_staged ? 4ull * d.n_bins * chunk : 0);
-  // packed returns: lengths, call-wide offsets, scan temp (own: runs on K7's
-  // stream concurrently with the waveform scan), staging
-  const size_t o_rlen = carve(packed ? sizeof(uint64_t) * chunk : 0);
-  const size_t o_roffs = carve(packed ? sizeof(uint64_t) * (n + 1) : 0);
-  size_t rscan_bytes = 0;
-  if (packed)
-    cub::DeviceScan::InclusiveSum(nullptr, rscan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (int)chunk, s);
-  const size_t o_rscan = carve(packed ? rscan_bytes : 0);
-  for (int k = 0; k < kSlots; ++k)
-    o_rst[k] = carve(packed_staged ? sizeof(helios_return) * R * chunk : 0);
+  const size_t o_rlen = carve(any_packed ? sizeof(uint64_t) * C : 0);
+  const size_t o_roffs = carve(any_packed ? sizeof(uint64_t) * job_off[n_jobs] : 0);
+  const size_t o_rscan = carve(any_packed ? scan_bytes : 0);
 
-  char* buf = nullptr;
-  cudaStream_t cs = nullptr, co = nullptr, ws = nullptr, fs = nullptr;  // co: D2H copies
-  cudaStream_t ts2 = nullptr;  // K6 of odd chunks
-  cudaStream_t cpair[2] = {nullptr, nullptr};
-  uint64_t* pin = nullptr;  // [slot][first, last] row offsets of a staged compact chunk
-  // K6a stream: 0 = the chunk's trace stream (default, measured best), 1 = own
-  // stream, 2 = own high-priority stream (HELIOS_BEAM_STREAM, A/B)
-  int beam_stream = 0;
-  if (const char* v = getenv("HELIOS_BEAM_STREAM")) beam_stream = atoi(v);
-  cudaStream_t bs = nullptr;
-  cudaError_t e = sc->acquire(s, total, &buf, any_staged ? cpair : nullptr, &ws, &pin,
-                              fit ? &fs : nullptr, &ts2, beam && beam_stream ? &bs : nullptr,
-                              beam_stream == 2);
-  cs = cpair[0];
-  co = cpair[1];
+  helios_scene_s::Slot* slot_ = nullptr;
+  cudaError_t e = sc->acquire(s, total, &slot_);
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate (scratch)");
-  auto cleanup = [&]() {
+  char* buf = slot_->ptr;
+  uint64_t* pin = slot_->pinned;
+  const bool serial_all = tu.serialize != 0;
+  // K7 overlaps K6 on its own stream, except on voxel scenes: there K6 is
+  // ALU-bound (fp64 DDA + Philox) and a concurrent K7 costs more than it hides
+  // (measured: profiles/r01_overlap_ab.txt); serialize = 1 puts every kernel
+  // on the caller's stream (exclusive per-kernel times for the roofline)
+  const bool serial = serial_all || sc->d_pad != nullptr;
+  const cudaStream_t ws = serial ? s : slot_->wave;
+  const cudaStream_t fs = serial ? s : slot_->fit;
+  const cudaStream_t ts2 = serial ? s : slot_->trace2;  // K6 of odd chunks
+  const cudaStream_t cs = slot_->copy_in, co = slot_->copy_out;
+  auto sync_all = [&]() {
     cudaStreamSynchronize(s);
     cudaStreamSynchronize(ws);
-    if (fs) cudaStreamSynchronize(fs);
-    if (ts2) cudaStreamSynchronize(ts2);
-    if (bs) cudaStreamSynchronize(bs);
-    if (cs) cudaStreamSynchronize(cs);
-    if (co) cudaStreamSynchronize(co);
-    sc->release(s);
+    cudaStreamSynchronize(fs);
+    cudaStreamSynchronize(ts2);
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(co);
   };
   SubrayConst* d_tab = reinterpret_cast<SubrayConst*>(buf + o_tab);
   double* d_ker = reinterpret_cast<double*>(buf + o_ker);
   unsigned* d_err = reinterpret_cast<unsigned*>(buf + o_err);
   unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(buf + o_cnt);
   double* d_wscratch = reinterpret_cast<double*>(buf + o_ws);
-  {
-    // K6's lane order (HELIOS_SUBRAY_ORDER=0: the table order of R4, A/B)
-    bool hil = true;
-    if (const char* v = getenv("HELIOS_SUBRAY_ORDER")) hil = atoi(v) != 0;
-    lanes = hil ? lane_order(tab) : tab;
-  }
+  uint64_t* d_len = reinterpret_cast<uint64_t*>(buf + o_len);
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(buf + o_offs);
+  uint64_t* d_rlen = reinterpret_cast<uint64_t*>(buf + o_rlen);
+  uint64_t* d_roffs = reinterpret_cast<uint64_t*>(buf + o_roffs);
   e = cudaMemcpyAsync(d_tab, lanes.data(), sizeof(SubrayConst) * N, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_ker, d.kernel.data(), sizeof(double) * d.taps, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, sizeof(unsigned), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, s);
-  uint64_t* d_len = reinterpret_cast<uint64_t*>(buf + o_len);
-  uint64_t* d_offs = reinterpret_cast<uint64_t*>(buf + o_offs);
-  if (e == cudaSuccess && want_offs) e = cudaMemsetAsync(d_offs, 0, sizeof(uint64_t), s);
-  uint64_t* d_rlen = reinterpret_cast<uint64_t*>(buf + o_rlen);
-  uint64_t* d_roffs = reinterpret_cast<uint64_t*>(buf + o_roffs);
-  if (e == cudaSuccess && packed) e = cudaMemsetAsync(d_roffs, 0, sizeof(uint64_t), s);
-  if (e != cudaSuccess) {
-    cleanup();
-    return cuda_fail(e, "helios_simulate (setup)");
+  // offs[job base] = 0: the carry the first chunk of each batch starts from
+  for (uint32_t j = 0; j < n_jobs && e == cudaSuccess; ++j) {
+    if (any_offs) e = cudaMemsetAsync(d_offs + job_off[j], 0, sizeof(uint64_t), s);
+    if (e == cudaSuccess && any_packed)
+      e = cudaMemsetAsync(d_roffs + job_off[j], 0, sizeof(uint64_t), s);
   }
-
   SurveyArgs sa{};
-  if (gen && e == cudaSuccess) {
+  if (e == cudaSuccess && gen) {
     sa.waypoints = reinterpret_cast<const double*>(buf + o_wp);
     e = cudaMemcpyAsync(buf + o_wp, survey->h_waypoints, sizeof(double) * 3 * survey->n_waypoints,
                         cudaMemcpyHostToDevice, s);
@@ -932,18 +933,17 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     sa.f = survey->scan_freq_hz;
     sa.A = survey->scan_angle_rad;
     sa.n_fibres = survey->n_fibres;
-    if (e != cudaSuccess) {
-      cleanup();
-      return cuda_fail(e, "helios_simulate_survey (waypoints)");
-    }
+  }
+  if (e != cudaSuccess) {
+    sync_all();
+    sc->release(slot_);
+    return cuda_fail(e, "helios_simulate (setup)");
   }
 
   TraceArgs ta{};
   ta.tris = sc->bvh.tris;
   ta.nodes = sc->bvh.nodes;
   ta.root = sc->bvh.root;
-  ta.nodes4 = sc->bvh.nodes4;
-  ta.root4 = sc->bvh.root4;
   ta.n_tris = sc->n_tris;
   ta.pad = sc->d_pad;
   ta.nx = sc->nx;
@@ -959,8 +959,6 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.bricks = sc->d_bricks;
   ta.nbx = sc->nbx;
   ta.nby = sc->nby;
-  if (const char* v = getenv("HELIOS_BRICKS"))  // A/B switch (default on)
-    if (!atoi(v)) ta.bricks = nullptr;
   ta.voxel_refl = sc->voxel_refl;
   ta.pad_max = sc->pad_max;
   ta.scale_alpha = sc->scale_alpha;
@@ -969,10 +967,9 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.N = N;
   {
     // pad a pulse to whole warps when that wastes <= 6 % of the lanes (91 -> 96):
-    // every warp then walks one pulse's patch (HELIOS_PAD_LANES=0/1 forces)
+    // every warp then walks one pulse's patch
     const uint32_t padded = (N + 31u) / 32u * 32u;
-    bool pad = (padded - N) * 100u <= 6u * N;
-    if (const char* v = getenv("HELIOS_PAD_LANES")) pad = atoi(v) != 0;
+    const bool pad = tu.pad_lanes < 0 ? (padded - N) * 100u <= 6u * N : tu.pad_lanes != 0;
     ta.lanes = pad ? padded : N;
   }
   ta.seed = params->seed;
@@ -984,17 +981,13 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   ta.R0 = params->focus_range_m;
   ta.err_flag = d_err;
   ta.counters = d_cnt;
+  ta.delta_ns = params->bin_width_ns;
+  ta.inv_bin = 1.0 / (kC * (params->bin_width_ns * 1e-9));
   {
     double smax = 0.0;
     for (const SubrayConst& t : tab) smax = std::max(smax, t.sin_t);
     ta.cone_sin = smax * (1.0 + 1e-9) + 1e-12;  // widened: covers the fp64 subray directions
     ta.beam_k = 8.0;  // measured (profiles/r01s3_beam_ab.txt)
-    if (const char* v = getenv("HELIOS_BEAM_K")) ta.beam_k = atof(v);
-    ta.entry_max = kEntryMax;
-    ta.beam_budget = 1 << 30;
-    if (const char* v = getenv("HELIOS_BEAM_BUDGET")) ta.beam_budget = std::max(1, atoi(v));
-    if (const char* v = getenv("HELIOS_BEAM_ENTRIES"))
-      ta.entry_max = std::max(2, std::min(kEntryMax, atoi(v)));
   }
 
   WaveArgs wa{};
@@ -1013,14 +1006,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   wa.counters = counters ? d_cnt + 4 : nullptr;
   wa.noise_sd = params->range_noise_sd_m;
   wa.fit_stride = fit_stride;
-  wa.compact = compact_staged ? nullptr : outputs->p_wf_compact;
-  wa.compact_staged = compact_staged ? 1 : 0;
-  wa.capacity = outputs->p_wf_compact ? outputs->wf_compact_capacity : 0;
   wa.err_flag = d_err;
   wa.seed = params->seed;
 
   // per-kernel device time (CUDA events on each kernel's stream)
-  std::vector<cudaEvent_t> ev_t, ev_w;
+  std::vector<cudaEvent_t> ev_b, ev_t, ev_w;
   auto mark = [&](std::vector<cudaEvent_t>& v, cudaStream_t st) {
     if (!stats) return;
     cudaEvent_t x;
@@ -1029,277 +1019,216 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       v.push_back(x);
     }
   };
-  // Stream graph per chunk c (slot = c % kSlots; "c-K" = the chunk that last used the slot):
-  //   s  : [wait in_done]  [wait w_done(c-2)]  K6(c)  -> t_done
-  //   ws : wait t_done  [wait out_done(c-2)]   K7(c)  -> w_done
-  //   cs : wait w_done(c-1) -> H2D(c+1) -> in_done
-  //   co : wait w_done(c) -> D2H(c) -> out_done   (own stream: PCIe is full duplex)
-  // so K7(c) runs concurrently with K6(c+1) and the copies with both.
-  cudaEvent_t in_done[kSlots] = {}, t_done[kSlots] = {}, w_done[kSlots] = {},
-              out_done[kSlots] = {};
-  cudaEvent_t off_done[kSlots] = {}, cd_done[kSlots] = {};  // packed rows: range known / drained
-  cudaEvent_t k7_done[kSlots] = {};                         // fit: K7 done, jobs listed
-  cudaEvent_t b_done[kSlots] = {};                          // K6a done: entry lists ready
-  cudaEvent_t roff_done[kSlots] = {}, rd_done[kSlots] = {}; // packed returns: known / drained
-  for (int k = 0; k < kSlots && e == cudaSuccess; ++k) {
-    e = cudaEventCreateWithFlags(&t_done[k], cudaEventDisableTiming);
-    if (e == cudaSuccess && fit) e = cudaEventCreateWithFlags(&k7_done[k], cudaEventDisableTiming);
-    if (e == cudaSuccess && packed_staged) {
-      e = cudaEventCreateWithFlags(&roff_done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&rd_done[k], cudaEventDisableTiming);
-    }
-    if (e == cudaSuccess && compact_staged) {
-      e = cudaEventCreateWithFlags(&off_done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cd_done[k], cudaEventDisableTiming);
-    }
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w_done[k], cudaEventDisableTiming);
-    if (e == cudaSuccess && bs) e = cudaEventCreateWithFlags(&b_done[k], cudaEventDisableTiming);
-    if (e == cudaSuccess && any_staged) {
-      e = cudaEventCreateWithFlags(&in_done[k], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&out_done[k], cudaEventDisableTiming);
-    }
-  }
-  // the copy stream must not start before the setup work on `s`
-  if (any_staged && e == cudaSuccess) {
-    e = cudaEventRecord(t_done[1], s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, t_done[1], 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(co, t_done[1], 0);
-  }
-  auto dev_ptr = [&](const Arr& a, int slot, uint64_t b) -> char* {
-    if (a.gen && !a.user) return buf + a.off[slot];
-    if (!a.user) return nullptr;
-    if (a.staged) return buf + a.off[slot];
-    return (char*)a.user + a.per_pulse * b;
-  };
-  auto copy_in = [&](uint64_t c, int slot) -> cudaError_t {
-    const uint64_t b = cstart[c], m = cstart[c + 1] - b;
-    for (const Arr& a : arrs)
-      if (a.staged && a.in) {
-        cudaError_t r = cudaMemcpyAsync(buf + a.off[slot], (const char*)a.user + a.per_pulse * b,
-                                        a.per_pulse * m, cudaMemcpyHostToDevice, cs);
-        if (r != cudaSuccess) return r;
-      }
-    return cudaEventRecord(in_done[slot], cs);
-  };
-
-  // HELIOS_TRACE_HOST=1: report the host's blocking time per call (stderr)
-  const bool host_trace = getenv("HELIOS_TRACE_HOST") != nullptr;
-  double host_wait_ms = 0.0;
-  const double call_t0 = host_trace ? now_ms() : 0.0;
-  // HELIOS_TRACE_HOST: device-side spans of the copy-out stream, the trace
-  // streams and K7 (timing events; reported relative to a start event on s)
+  // trace_spans: device-side spans of the streams (stderr), for diagnosis
   std::vector<std::pair<char, cudaEvent_t>> tev;
   cudaEvent_t tev0 = nullptr;
   auto tmark = [&](char tag, cudaStream_t st) {
-    if (!host_trace) return;
+    if (!tu.trace_spans) return;
     cudaEvent_t x;
     if (cudaEventCreate(&x) == cudaSuccess) {
       cudaEventRecord(x, st);
       tev.emplace_back(tag, x);
     }
   };
-  if (host_trace && cudaEventCreate(&tev0) == cudaSuccess) cudaEventRecord(tev0, s);
-  // staged compact rows of chunk c: the host learns the chunk's offset range
-  // from the pinned mirror (written on `s` right after the chunk's scan), then
-  // queues the copy behind K7(c) on the copy stream.  Called one iteration
+  if (tu.trace_spans && cudaEventCreate(&tev0) == cudaSuccess) cudaEventRecord(tev0, s);
+  double host_wait_ms = 0.0;
+  const double call_t0 = tu.trace_spans ? now_ms() : 0.0;
+
+  cudaEvent_t in_done[kSlots] = {}, t_done[kSlots] = {}, w_done[kSlots] = {},
+              out_done[kSlots] = {}, off_done[kSlots] = {}, cd_done[kSlots] = {},
+              k7_done[kSlots] = {}, roff_done[kSlots] = {}, rd_done[kSlots] = {};
+  cudaEvent_t ev_setup = nullptr;
+  auto mk = [&](cudaEvent_t* x) {
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(x, cudaEventDisableTiming);
+  };
+  mk(&ev_setup);
+  for (int k = 0; k < kSlots; ++k) {
+    mk(&t_done[k]);
+    mk(&w_done[k]);
+    if (fit) mk(&k7_done[k]);
+    if (any_pstaged) {
+      mk(&roff_done[k]);
+      mk(&rd_done[k]);
+    }
+    if (any_cstaged) {
+      mk(&off_done[k]);
+      mk(&cd_done[k]);
+    }
+    if (any_staged) {
+      mk(&in_done[k]);
+      mk(&out_done[k]);
+    }
+  }
+  // every other stream starts after the setup work on `s`
+  if (e == cudaSuccess) e = cudaEventRecord(ev_setup, s);
+  for (cudaStream_t x : {ws, fs, ts2, cs, co})
+    if (e == cudaSuccess && x != s) e = cudaStreamWaitEvent(x, ev_setup, 0);
+
+  auto dev_ptr = [&](int a, int slot, const Chunk& ch) -> char* {
+    const size_t ix = (size_t)ch.job * A_COUNT + a;
+    if (staged[ix] || internal(ch.job, a)) return buf + o_arr[a][slot];
+    if (!user[ix]) return nullptr;
+    return (char*)user[ix] + per_pulse[a] * ch.b;
+  };
+  auto copy_in = [&](uint64_t c) -> cudaError_t {
+    const Chunk& ch = chunks[c];
+    const int slot = (int)(c % kSlots);
+    for (int a = 0; a < A_COUNT; ++a) {
+      const size_t ix = (size_t)ch.job * A_COUNT + a;
+      if (is_in[a] && staged[ix]) {
+        cudaError_t r = cudaMemcpyAsync(buf + o_arr[a][slot],
+                                        (const char*)user[ix] + per_pulse[a] * ch.b,
+                                        per_pulse[a] * ch.m, cudaMemcpyHostToDevice, cs);
+        if (r != cudaSuccess) return r;
+      }
+    }
+    return cudaEventRecord(in_done[slot], cs);
+  };
+  // staged packed rows of chunk c: the host learns the chunk's offset range
+  // from the pinned mirror (written on the waveform stream right after the
+  // chunk's scan), then queues the copy behind K7(c).  Called kSlots-1 chunks
   // late, so the GPU never waits for the host.
-  const uint64_t cap = outputs->wf_compact_capacity;
   auto drain_compact = [&](uint64_t c) -> cudaError_t {
+    const Chunk& ch = chunks[c];
+    if (!compact_staged[ch.job]) return cudaSuccess;
     const int sl = (int)(c % kSlots);
-    const double h0 = host_trace ? now_ms() : 0.0;
+    const double h0 = tu.trace_spans ? now_ms() : 0.0;
     cudaError_t r = cudaEventSynchronize(off_done[sl]);
-    if (host_trace) host_wait_ms += now_ms() - h0;
+    if (tu.trace_spans) host_wait_ms += now_ms() - h0;
     if (r != cudaSuccess) return r;
-    const uint64_t first = pin[2 * sl], last = std::min(pin[2 * sl + 1], cap);
+    const helios_outputs* O = jobs[ch.job].out;
+    const uint64_t first = pin[2 * sl], last = std::min(pin[2 * sl + 1], O->wf_compact_capacity);
     r = cudaStreamWaitEvent(co, w_done[sl], 0);
     tmark('c', co);
     if (r == cudaSuccess && last > first)
-      r = cudaMemcpyAsync(outputs->p_wf_compact + first, buf + o_cst[sl],
-                          sizeof(float) * (last - first), cudaMemcpyDeviceToHost, co);
+      r = cudaMemcpyAsync(O->p_wf_compact + first, buf + o_cst[sl], sizeof(float) * (last - first),
+                          cudaMemcpyDeviceToHost, co);
     tmark('C', co);
     if (r == cudaSuccess) r = cudaEventRecord(cd_done[sl], co);
     return r;
   };
-
-  // staged fixed-size outputs of chunk c (counts, first bins, return slots,
-  // dense rows, subray hits, beam export) -> host; out_done marks the slot free
-  auto drain_fixed = [&](uint64_t c) -> cudaError_t {
+  auto drain_returns = [&](uint64_t c) -> cudaError_t {
+    const Chunk& ch = chunks[c];
+    if (!packed_staged[ch.job]) return cudaSuccess;
     const int sl = (int)(c % kSlots);
-    const uint64_t b = cstart[c], m = cstart[c + 1] - b;
+    const double h0 = tu.trace_spans ? now_ms() : 0.0;
+    cudaError_t r = cudaEventSynchronize(roff_done[sl]);
+    if (tu.trace_spans) host_wait_ms += now_ms() - h0;
+    if (r != cudaSuccess) return r;
+    const helios_outputs* O = jobs[ch.job].out;
+    const uint64_t first = pin[2 * kSlots + 2 * sl],
+                   last = std::min(pin[2 * kSlots + 2 * sl + 1], O->returns_capacity);
+    r = cudaStreamWaitEvent(co, w_done[sl], 0);
+    if (r == cudaSuccess && last > first)
+      r = cudaMemcpyAsync(O->p_returns_packed + first, buf + o_rst[sl],
+                          sizeof(helios_return) * (last - first), cudaMemcpyDeviceToHost, co);
+    if (r == cudaSuccess) r = cudaEventRecord(rd_done[sl], co);
+    return r;
+  };
+  // staged fixed-size outputs of chunk c -> host; out_done marks the slot free
+  auto drain_fixed = [&](uint64_t c) -> cudaError_t {
+    const Chunk& ch = chunks[c];
+    const int sl = (int)(c % kSlots);
     cudaError_t r = cudaStreamWaitEvent(co, w_done[sl], 0);
     tmark('f', co);
-    for (const Arr& a : arrs)
-      if (r == cudaSuccess && a.staged && !a.in)
-        r = cudaMemcpyAsync((char*)a.user + a.per_pulse * b, buf + a.off[sl], a.per_pulse * m,
-                            cudaMemcpyDeviceToHost, co);
+    for (int a = 0; a < A_COUNT && r == cudaSuccess; ++a) {
+      const size_t ix = (size_t)ch.job * A_COUNT + a;
+      if (!is_in[a] && staged[ix])
+        r = cudaMemcpyAsync((char*)user[ix] + per_pulse[a] * ch.b, buf + o_arr[a][sl],
+                            per_pulse[a] * ch.m, cudaMemcpyDeviceToHost, co);
+    }
     tmark('F', co);
     if (r == cudaSuccess) r = cudaEventRecord(out_done[sl], co);
     return r;
   };
 
-  // staged packed returns of chunk c (same scheme as drain_compact)
-  const uint64_t rcap = outputs->returns_capacity;
-  auto drain_returns = [&](uint64_t c) -> cudaError_t {
-    const int sl = (int)(c % kSlots);
-    const double h0 = host_trace ? now_ms() : 0.0;
-    cudaError_t r = cudaEventSynchronize(roff_done[sl]);
-    if (host_trace) host_wait_ms += now_ms() - h0;
-    if (r != cudaSuccess) return r;
-    const uint64_t first = pin[2 * kSlots + 2 * sl],
-                   last = std::min(pin[2 * kSlots + 2 * sl + 1], rcap);
-    r = cudaStreamWaitEvent(co, w_done[sl], 0);
-    if (r == cudaSuccess && last > first)
-      r = cudaMemcpyAsync(outputs->p_returns_packed + first, buf + o_rst[sl],
-                          sizeof(helios_return) * (last - first), cudaMemcpyDeviceToHost, co);
-    if (r == cudaSuccess) r = cudaEventRecord(rd_done[sl], co);
-    return r;
-  };
-
-  // traversal mode: warp-cooperative packets (default) or per-ray threads;
-  // HELIOS_TRAVERSAL=ray selects the latter (A/B measurements).
-  // traversal: 1 = packet over the binary tree (default, measured best),
-  // 2 = packet over the 4-wide tree (needs HELIOS_BVH4=1 at build time),
-  // 0 = per-ray threads; HELIOS_TRAVERSAL=packet2|packet4|ray
-  int mode = 1;
-  if (const char* v = getenv("HELIOS_TRAVERSAL")) {
-    if (!strcmp(v, "ray")) mode = 0;
-    else if (!strcmp(v, "packet4") && (sc->bvh.nodes4 || ref_is_leaf(sc->bvh.root))) mode = 2;
-  }
-  // K7 overlaps K6 on its own stream, except on voxel scenes: there K6 is
-  // ALU-bound (fp64 DDA + Philox) and a concurrent K7 costs more than it
-  // hides (measured: profiles/r01_overlap_ab.txt).  HELIOS_SERIAL=0/1 forces.
-  bool serial = sc->d_pad != nullptr;
-  if (const char* v = getenv("HELIOS_SERIAL")) serial = atoi(v) != 0;
-  if (serial) ws = s;
-  // K6 on two alternating streams (HELIOS_DUAL_TRACE=0/1 forces)
-  bool dual_trace = !serial;
-  if (const char* v = getenv("HELIOS_DUAL_TRACE")) dual_trace = atoi(v) != 0;
-  if ((dual_trace || bs) && e == cudaSuccess) {
-    // ts2 and bs must not start before the setup work on `s`
-    e = cudaEventRecord(t_done[0], s);
-    if (e == cudaSuccess && dual_trace) e = cudaStreamWaitEvent(ts2, t_done[0], 0);
-    if (e == cudaSuccess && bs) e = cudaStreamWaitEvent(bs, t_done[0], 0);
-  }
-  if (ws != s) {
-    // optional cap on K7's persistent grid while it shares the SMs with K6
-    // (HELIOS_WAVE_BLOCKS_PER_SM; default: full grid, measured best)
-    int bps = 0;
-    if (const char* v = getenv("HELIOS_WAVE_BLOCKS_PER_SM")) bps = atoi(v);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (bps > 0) plan.grid_cap = (uint32_t)(sms * bps);
-  }
   uint32_t launches = 0, trace_launches = 0;
-  const uint64_t n_chunks = cstart.size() - 1;
-  if (any_staged && e == cudaSuccess) e = copy_in(0, 0);
+  const uint64_t n_chunks = chunks.size();
+  const bool dual_trace = !serial;
+  if (any_staged && e == cudaSuccess) e = copy_in(0);
   for (uint64_t c = 0; c < n_chunks && e == cudaSuccess; ++c) {
-    const uint64_t b = cstart[c];
-    const uint64_t m = cstart[c + 1] - b;
+    const Chunk& ch = chunks[c];
+    const helios_pulses* P = jobs[ch.job].pulses;
+    const helios_outputs* O = jobs[ch.job].out;
+    const uint64_t b = ch.b, m = ch.m;
     const int slot = (int)(c % kSlots);
-    // K6 of odd chunks on the second trace stream (chunks are independent);
-    // voxel scenes stay on one stream (measured: K6 is ALU-bound there)
     const cudaStream_t ts = (dual_trace && (c & 1)) ? ts2 : s;
-    // with its own stream, K6a and the chunk's pulse generation only wait for
-    // the chunk's inputs and for the slot's previous user (K7 of chunk c-K,
-    // hence also its K6)
-    const bool use_beam = beam && mode == 1;
-    const cudaStream_t gs = (use_beam && bs) ? bs : ts;
-    if (gs != ts) {
-      if (any_staged) e = cudaStreamWaitEvent(bs, in_done[slot], 0);
-      if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(bs, w_done[slot], 0);
-      if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots)
-        e = cudaStreamWaitEvent(bs, out_done[slot], 0);
-    }
-    if (e == cudaSuccess && any_staged) e = cudaStreamWaitEvent(ts, in_done[slot], 0);
-    if (e == cudaSuccess && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ts, w_done[slot], 0);
-    // K6 writes the staged subray-hit slot chunk c-K used: its copy-out (on the
-    // D2H stream, not ordered behind this chunk's H2D) must be done
-    if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots)
-      e = cudaStreamWaitEvent(ts, out_done[slot], 0);
-    // generated pulses of this chunk (into the slot chunk c-K used: its copy-out
-    // must be done when the export is host memory)
+    const bool reuse = c >= (uint64_t)kSlots;  // the slot's previous user: chunk c - kSlots
+    if (any_staged) e = cudaStreamWaitEvent(ts, in_done[slot], 0);
+    if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(ts, w_done[slot], 0);
+    // K6 / K0 overwrite staged slot buffers chunk c-K copies out: wait for that
+    if (e == cudaSuccess && any_staged && reuse) e = cudaStreamWaitEvent(ts, out_done[slot], 0);
     if (e == cudaSuccess && gen) {
-      if (gen_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(gs, out_done[slot], 0);
-      if (e == cudaSuccess)
-        e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(arrs[0], slot, b),
-                            (float*)dev_ptr(arrs[1], slot, b), (double*)dev_ptr(arrs[2], slot, b),
-                            gs);
+      e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(A_ORIGIN, slot, ch),
+                          (float*)dev_ptr(A_DIR, slot, ch), (double*)dev_ptr(A_TIME, slot, ch), ts);
       ++launches;
     }
     if (e != cudaSuccess) break;
-    ta.origin = (const float*)dev_ptr(arrs[0], slot, b);
-    ta.direction = (const float*)dev_ptr(arrs[1], slot, b);
+    ta.origin = (const float*)dev_ptr(A_ORIGIN, slot, ch);
+    ta.direction = (const float*)dev_ptr(A_DIR, slot, ch);
     ta.n_pulses = m;
-    ta.pulse_base = pulses->pulse_index_base + b;
-    ta.out = own_rec ? reinterpret_cast<helios_subray_hit*>(buf + o_rec[slot])
-                     : (helios_subray_hit*)dev_ptr(arrs[7], slot, b);
+    ta.pulse_base = P->pulse_index_base + b;
+    ta.wrec = reinterpret_cast<WaveRec*>(buf + o_wrec[slot]);
+    ta.prim = reinterpret_cast<uint32_t*>(buf + o_prim[slot]);
+    ta.out = (helios_subray_hit*)dev_ptr(A_HITS, slot, ch);
     ta.entries = nullptr;
     ta.frames = nullptr;
-    if (use_beam) {
+    if (beam) {
       ta.entries = reinterpret_cast<int2*>(buf + o_ent[slot]);
       ta.frames = reinterpret_cast<double*>(buf + o_frm[slot]);
-      mark(ev_t, gs);
-      tmark('b', gs);
-      if (e == cudaSuccess) e = launch_beam(ta, counters, gs);
-      tmark('B', gs);
+      mark(ev_b, ts);
+      tmark('b', ts);
+      e = launch_beam(ta, counters, ts);
+      tmark('B', ts);
+      mark(ev_b, ts);
       ++launches;
-      // measurement only: HELIOS_BEAM_REPEAT=k launches K6a k extra times (its
-      // marginal cost in the pipeline = step time delta / k)
-      if (const char* v = getenv("HELIOS_BEAM_REPEAT"))
-        for (int r = 0; r < atoi(v) && e == cudaSuccess; ++r) e = launch_beam(ta, false, gs);
-      mark(ev_t, gs);
-      if (gs != ts) {
-        if (e == cudaSuccess) e = cudaEventRecord(b_done[slot], bs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(ts, b_done[slot], 0);
-      }
     }
     mark(ev_t, ts);
     tmark('t', ts);
-    if (e == cudaSuccess) e = launch_trace(ta, counters, mode, ts);
+    if (e == cudaSuccess) e = launch_trace(ta, counters, ts);
     tmark('T', ts);
-    ++trace_launches;
     mark(ev_t, ts);
+    ++launches;
+    ++trace_launches;
     if (e == cudaSuccess) e = cudaEventRecord(t_done[slot], ts);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
-    if (e == cudaSuccess && any_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
-    if (e == cudaSuccess && compact_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
-    if (e == cudaSuccess && want_offs) {
-      // packed rows: lengths -> inclusive scan into offs[b+1 ..] -> + offs[b]
-      // (previous chunks), on K7's stream so the next chunk's K6 never waits
-      e = launch_support(ta.out, N, m, d.n_bins, d.taps, params->bin_width_ns, d_len, ws);
-      size_t tb = scan_bytes;
-      if (e == cudaSuccess)
-        e = cub::DeviceScan::InclusiveSum(buf + o_scan, tb, d_len, d_offs + b + 1, (int)m, ws);
-      if (e == cudaSuccess) e = launch_add_carry(d_offs + b, m, ws);
-      launches += 3;
-      if (e == cudaSuccess && compact_staged) {
-        e = cudaMemcpyAsync(pin + 2 * slot, d_offs + b, sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                            ws);
+    if (e == cudaSuccess && ws != ts) e = cudaStreamWaitEvent(ws, t_done[slot], 0);
+    if (e == cudaSuccess && any_staged && reuse) e = cudaStreamWaitEvent(ws, out_done[slot], 0);
+    if (e == cudaSuccess && any_cstaged && reuse) e = cudaStreamWaitEvent(ws, cd_done[slot], 0);
+    uint64_t* offs = want_offs[ch.job] ? d_offs + job_off[ch.job] + b : nullptr;
+    if (e == cudaSuccess && offs) {
+      // packed rows: support lengths -> inclusive scan into offs[1..m] seeded
+      // with offs[0] (the previous chunks of this batch), on K7's stream
+      e = launch_support(ta.wrec, N, m, d.n_bins, d.taps, d_len, ws);
+      if (e == cudaSuccess) e = scan_u64(d_len, offs + 1, m, true, buf + o_scan, scan_bytes, ws, offs);
+      launches += 4;
+      if (e == cudaSuccess && compact_staged[ch.job]) {
+        e = cudaMemcpyAsync(pin + 2 * slot, offs, sizeof(uint64_t), cudaMemcpyDeviceToHost, ws);
         if (e == cudaSuccess)
-          e = cudaMemcpyAsync(pin + 2 * slot + 1, d_offs + b + m, sizeof(uint64_t),
+          e = cudaMemcpyAsync(pin + 2 * slot + 1, offs + m, sizeof(uint64_t),
                               cudaMemcpyDeviceToHost, ws);
         if (e == cudaSuccess) e = cudaEventRecord(off_done[slot], ws);
       }
     }
     if (e != cudaSuccess) break;
-    wa.rec = ta.out;
+    wa.rec = ta.wrec;
+    wa.prim = ta.prim;
     wa.n_pulses = m;
     wa.pulse_base = ta.pulse_base;
-    wa.time_s = (const double*)dev_ptr(arrs[2], slot, b);
-    wa.n_returns = (uint8_t*)dev_ptr(arrs[3], slot, b);
-    wa.returns = (helios_return*)dev_ptr(arrs[4], slot, b);
-    wa.first_bin = (int64_t*)dev_ptr(arrs[5], slot, b);
-    wa.waveform = (float*)dev_ptr(arrs[6], slot, b);
-    wa.offs = want_offs ? d_offs + b : nullptr;
-    if (compact_staged) wa.compact = reinterpret_cast<float*>(buf + o_cst[slot]);
+    wa.time_s = (const double*)dev_ptr(A_TIME, slot, ch);
+    wa.n_returns = (uint8_t*)dev_ptr(A_NRET, slot, ch);
+    wa.returns = (helios_return*)dev_ptr(A_RET, slot, ch);
+    wa.first_bin = (int64_t*)dev_ptr(A_K0, slot, ch);
+    wa.waveform = (float*)dev_ptr(A_WF, slot, ch);
+    wa.offs = offs;
+    wa.compact = compact_staged[ch.job] ? reinterpret_cast<float*>(buf + o_cst[slot])
+                                        : O->p_wf_compact;
+    wa.compact_staged = compact_staged[ch.job] ? 1 : 0;
+    wa.capacity = O->p_wf_compact ? O->wf_compact_capacity : 0;
     if (fit) {
       wa.fit_jobs = reinterpret_cast<FitJob*>(buf + o_fjob[slot]);
       wa.fit_y = reinterpret_cast<double*>(buf + o_fy[slot]);
       wa.fit_count = reinterpret_cast<unsigned*>(buf + o_fcnt) + slot;
-      // the slot's jobs of chunk c-2 must be fitted before they are overwritten
-      if (c >= (uint64_t)kSlots && ws != s) e = cudaStreamWaitEvent(ws, w_done[slot], 0);
-      if (e == cudaSuccess) e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
+      e = cudaMemsetAsync(wa.fit_count, 0, sizeof(unsigned), ws);
     }
     mark(ev_w, ws);
     tmark('w', ws);
@@ -1310,146 +1239,138 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       ++launches;
     }
     mark(ev_w, ws);
-    // the stream that finishes the chunk's returns: fits (own stream) or K7's
-    cudaStream_t post = ws;
+    ++launches;
+    cudaStream_t post = ws;  // the stream that completes the chunk's returns
     if (e == cudaSuccess && fit) {
-      // echo-width fits on their own stream (their tail overlaps later chunks);
-      // the chunk's outputs are complete once they are done
-      cudaStream_t f = ws == s ? s : fs;
-      if (f != ws) e = cudaEventRecord(k7_done[slot], ws);
-      if (e == cudaSuccess && f != ws) e = cudaStreamWaitEvent(f, k7_done[slot], 0);
-      if (e == cudaSuccess) e = launch_fit(wa, f);
+      // echo-width fits on their own stream (their tail overlaps later chunks)
+      if (fs != ws) e = cudaEventRecord(k7_done[slot], ws);
+      if (e == cudaSuccess && fs != ws) e = cudaStreamWaitEvent(fs, k7_done[slot], 0);
+      if (e == cudaSuccess) e = launch_fit(wa, fs);
       ++launches;
-      post = f;
+      post = fs;
     }
-    if (e == cudaSuccess && packed) {
+    if (e == cudaSuccess && packed[ch.job]) {
       // packed returns: scan of the counts, copy of the used slots
-      if (packed_staged && c >= (uint64_t)kSlots) e = cudaStreamWaitEvent(post, rd_done[slot], 0);
-      helios_return* dst = packed_staged ? reinterpret_cast<helios_return*>(buf + o_rst[slot])
-                                         : outputs->p_returns_packed;
+      if (packed_staged[ch.job] && reuse) e = cudaStreamWaitEvent(post, rd_done[slot], 0);
+      helios_return* dst = packed_staged[ch.job]
+                               ? reinterpret_cast<helios_return*>(buf + o_rst[slot])
+                               : O->p_returns_packed;
+      uint64_t* roffs = d_roffs + job_off[ch.job] + b;
       if (e == cudaSuccess)
-        e = launch_pack_returns(wa.returns, wa.n_returns, m, R, d_rlen, d_roffs + b,
-                                buf + o_rscan, rscan_bytes, dst, packed_staged ? 1 : 0, rcap,
-                                post);
-      launches += 4;
-      if (e == cudaSuccess && packed_staged) {
-        e = cudaMemcpyAsync(pin + 2 * kSlots + 2 * slot, d_roffs + b, sizeof(uint64_t),
+        e = launch_pack_returns(wa.returns, wa.n_returns, m, R, d_rlen, roffs, buf + o_rscan,
+                                scan_bytes, dst, packed_staged[ch.job] ? 1 : 0,
+                                O->returns_capacity, post);
+      launches += 5;
+      if (e == cudaSuccess && packed_staged[ch.job]) {
+        e = cudaMemcpyAsync(pin + 2 * kSlots + 2 * slot, roffs, sizeof(uint64_t),
                             cudaMemcpyDeviceToHost, post);
         if (e == cudaSuccess)
-          e = cudaMemcpyAsync(pin + 2 * kSlots + 2 * slot + 1, d_roffs + b + m, sizeof(uint64_t),
+          e = cudaMemcpyAsync(pin + 2 * kSlots + 2 * slot + 1, roffs + m, sizeof(uint64_t),
                               cudaMemcpyDeviceToHost, post);
         if (e == cudaSuccess) e = cudaEventRecord(roff_done[slot], post);
       }
     }
     if (e == cudaSuccess) e = cudaEventRecord(w_done[slot], post);
-    launches += 2;
-    // packed copy-outs run kSlots-1 chunks behind, so the host never blocks on
-    // a chunk whose K7 may still be queued behind the K6 it just enqueued
+    // copy-outs run kSlots-1 chunks behind, so the host never blocks on a
+    // chunk whose K7 may still be queued behind the K6 it just enqueued; all
+    // copy-outs of a chunk leave in one go, in chunk order
     constexpr uint64_t kLag = kSlots - 1;
-    // (the fixed-size staged outputs too: all copy-outs of a chunk leave in
-    // one go, in chunk order, so none queues behind a later chunk's K7)
-    if (e == cudaSuccess && compact_staged && c >= kLag) e = drain_compact(c - kLag);
-    if (e == cudaSuccess && packed_staged && c >= kLag) e = drain_returns(c - kLag);
-    if (e == cudaSuccess && any_staged && c >= kLag) e = drain_fixed(c - kLag);
-    if (e != cudaSuccess || !any_staged) continue;
-    // prefetch the next chunk's inputs into the other slot once chunk c-1's
-    // kernels (K6 reads origin/direction, K7 reads time) are done with it
-    if (c + 1 < n_chunks) {
+    if (c >= kLag) {
+      const uint64_t cc = c - kLag;
+      if (e == cudaSuccess && any_cstaged) e = drain_compact(cc);
+      if (e == cudaSuccess && any_pstaged) e = drain_returns(cc);
+      if (e == cudaSuccess && any_staged) e = drain_fixed(cc);
+    }
+    // prefetch the next chunk's inputs into its slot once that slot's previous
+    // user (chunk c+1-kSlots) is done with it
+    if (e == cudaSuccess && any_staged && c + 1 < n_chunks) {
       const int nslot = (int)((c + 1) % kSlots);
       if (c + 1 >= (uint64_t)kSlots) e = cudaStreamWaitEvent(cs, w_done[nslot], 0);
-      if (e == cudaSuccess) e = copy_in(c + 1, nslot);
+      if (e == cudaSuccess) e = copy_in(c + 1);
     }
   }
   for (uint64_t c = n_chunks > (uint64_t)(kSlots - 1) ? n_chunks - (kSlots - 1) : 0;
        c < n_chunks && e == cudaSuccess; ++c) {
-    if (compact_staged) e = drain_compact(c);
-    if (e == cudaSuccess && packed_staged) e = drain_returns(c);
+    if (any_cstaged) e = drain_compact(c);
+    if (e == cudaSuccess && any_pstaged) e = drain_returns(c);
     if (e == cudaSuccess && any_staged) e = drain_fixed(c);
   }
-  // call-wide offsets to the caller (device or host memory)
-  if (e == cudaSuccess && want_offs) {
-    for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess && ws != s; ++k)
-      e = cudaStreamWaitEvent(s, w_done[k], 0);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(outputs->p_wf_offset, d_offs, sizeof(uint64_t) * (n + 1),
+  // join: the caller's stream is ordered after every kernel and copy of the call
+  for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
+    e = cudaStreamWaitEvent(s, w_done[k], 0);
+  // call-wide offsets of every batch to the caller (device or host memory)
+  for (uint32_t j = 0; j < n_jobs && e == cudaSuccess; ++j) {
+    const helios_outputs* O = jobs[j].out;
+    const uint64_t n = jobs[j].pulses->n_pulses;
+    if (n == 0) continue;
+    if (O->p_wf_offset)
+      e = cudaMemcpyAsync(O->p_wf_offset, d_offs + job_off[j], sizeof(uint64_t) * (n + 1),
+                          cudaMemcpyDefault, s);
+    if (e == cudaSuccess && O->p_return_offset)
+      e = cudaMemcpyAsync(O->p_return_offset, d_roffs + job_off[j], sizeof(uint64_t) * (n + 1),
                           cudaMemcpyDefault, s);
   }
-  if (e == cudaSuccess && packed) {
-    for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
-      e = cudaStreamWaitEvent(s, w_done[k], 0);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(outputs->p_return_offset, d_roffs, sizeof(uint64_t) * (n + 1),
-                          cudaMemcpyDefault, s);
-  }
-  // join: the caller's stream is ordered after every kernel of this call
-  if (e == cudaSuccess && ws != s && n_chunks > 0)
-    for (int k = 0; k < kSlots && (uint64_t)k < n_chunks && e == cudaSuccess; ++k)
-      e = cudaStreamWaitEvent(s, w_done[k], 0);
   unsigned herr = 0;
   unsigned long long hcnt[8] = {0};
-  uint64_t htotal = 0, hrtotal = 0;
+  std::vector<uint64_t> htot(n_jobs, 0), hrtot(n_jobs, 0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && want_offs)
-    e = cudaMemcpyAsync(&htotal, d_offs + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && packed)
-    e = cudaMemcpyAsync(&hrtotal, d_roffs + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  for (uint32_t j = 0; j < n_jobs && e == cudaSuccess; ++j) {
+    const uint64_t n = jobs[j].pulses->n_pulses;
+    if (n == 0) continue;
+    if (want_offs[j])
+      e = cudaMemcpyAsync(&htot[j], d_offs + job_off[j] + n, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && packed[j])
+      e = cudaMemcpyAsync(&hrtot[j], d_roffs + job_off[j] + n, 8, cudaMemcpyDeviceToHost, s);
+  }
   if (e == cudaSuccess && counters)
     e = cudaMemcpyAsync(hcnt, d_cnt, sizeof(hcnt), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess && cs) e = cudaStreamSynchronize(cs);
-  if (e == cudaSuccess && co) e = cudaStreamSynchronize(co);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ws);
-  if (e == cudaSuccess && fs) e = cudaStreamSynchronize(fs);
-  if (host_trace && tev0) {
+  if (e == cudaSuccess) e = cudaStreamSynchronize(co);
+  if (tu.trace_spans && tev0) {
     std::string line;
     for (auto& pr : tev) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, tev0, pr.second);
-      char b[32];
-      snprintf(b, sizeof b, " %c%.2f", pr.first, ms);
-      line += b;
+      char bb[32];
+      snprintf(bb, sizeof bb, " %c%.2f", pr.first, ms);
+      line += bb;
       cudaEventDestroy(pr.second);
     }
     cudaEventDestroy(tev0);
-    fprintf(stderr, "helios_simulate spans (ms from call start; b/B K6a, t/T K6, w/W K7, f/F fixed copy-out, c/C rows copy-out):%s\n", line.c_str());
+    fprintf(stderr, "helios_simulate spans (ms from call start; b/B K6a, t/T K6, w/W K7, f/F "
+                    "fixed copy-out, c/C rows copy-out):%s\n", line.c_str());
+    fprintf(stderr, "helios_simulate: %llu pulses, %u batches, %llu chunks, host %.3f ms, "
+                    "blocked in drains %.3f ms\n", (unsigned long long)total_n, n_jobs,
+            (unsigned long long)n_chunks, now_ms() - call_t0, host_wait_ms);
   }
-  if (host_trace)
-    fprintf(stderr, "helios_simulate: %llu pulses, %llu chunks, host %.3f ms, blocked in drains %.3f ms\n",
-            (unsigned long long)n, (unsigned long long)n_chunks, now_ms() - call_t0, host_wait_ms);
-  double t_trace = 0.0, t_wave = 0.0;
-  for (size_t i = 0; i + 1 < ev_t.size(); i += 2) {
-    float a = 0.f;
-    if (cudaEventElapsedTime(&a, ev_t[i], ev_t[i + 1]) == cudaSuccess) t_trace += a;
-  }
-  for (size_t i = 0; i + 1 < ev_w.size(); i += 2) {
-    float a = 0.f;
-    if (cudaEventElapsedTime(&a, ev_w[i], ev_w[i + 1]) == cudaSuccess) t_wave += a;
-  }
-  for (cudaEvent_t x : ev_t) cudaEventDestroy(x);
-  for (cudaEvent_t x : ev_w) cudaEventDestroy(x);
-  for (int k = 0; k < kSlots; ++k) {
-    if (in_done[k]) cudaEventDestroy(in_done[k]);
-    if (t_done[k]) cudaEventDestroy(t_done[k]);
-    if (w_done[k]) cudaEventDestroy(w_done[k]);
-    if (out_done[k]) cudaEventDestroy(out_done[k]);
-    if (off_done[k]) cudaEventDestroy(off_done[k]);
-    if (cd_done[k]) cudaEventDestroy(cd_done[k]);
-    if (roff_done[k]) cudaEventDestroy(roff_done[k]);
-    if (rd_done[k]) cudaEventDestroy(rd_done[k]);
-    if (k7_done[k]) cudaEventDestroy(k7_done[k]);
-    if (b_done[k]) cudaEventDestroy(b_done[k]);
-  }
+  auto sum_ms = [](std::vector<cudaEvent_t>& v) {
+    double t = 0.0;
+    for (size_t i = 0; i + 1 < v.size(); i += 2) {
+      float a = 0.f;
+      if (cudaEventElapsedTime(&a, v[i], v[i + 1]) == cudaSuccess) t += a;
+    }
+    for (cudaEvent_t x : v) cudaEventDestroy(x);
+    return t;
+  };
+  const double t_beam = sum_ms(ev_b), t_trace = sum_ms(ev_t), t_wave = sum_ms(ev_w);
+  for (cudaEvent_t* arr : {in_done, t_done, w_done, out_done, off_done, cd_done, k7_done,
+                           roff_done, rd_done})
+    for (int k = 0; k < kSlots; ++k)
+      if (arr[k]) cudaEventDestroy(arr[k]);
+  if (ev_setup) cudaEventDestroy(ev_setup);
   cudaGetLastError();
-  cleanup();
+  sync_all();
+  sc->release(slot_);
   if (e != cudaSuccess) return cuda_fail(e, "helios_simulate");
   if (stats) {
-    stats->pulses = n;
-    stats->subrays = n * N;
+    stats->pulses = total_n;
+    stats->subrays = total_n * N;
     stats->kernel_launches = launches;
     stats->trace_launches = trace_launches;
     stats->beam_nodes = hcnt[7];
-    stats->node_bytes = mode == 2 ? (uint32_t)sizeof(Node4) : (uint32_t)sizeof(Node);
+    stats->node_bytes = (uint32_t)sizeof(Node);
     stats->trace_ms = t_trace;
+    stats->beam_ms = t_beam;
     stats->waveform_ms = t_wave;
     stats->nodes_visited = hcnt[0];
     stats->tris_tested = hcnt[1];
@@ -1458,15 +1379,20 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     stats->fp64_tests = hcnt[6];
     stats->subray_hits = hcnt[4];
     stats->returns = hcnt[5];
+    stats->batches = n_jobs;
+    stats->chunks = (uint32_t)n_chunks;
   }
   if (herr & 4u) return fail(HELIOS_ERR_CUDA, "internal: compact row length mismatch");
   if (herr & 1u) return fail(HELIOS_ERR_INVALID_ARGUMENT, "a pulse direction has zero length");
-  if (packed && hrtotal > outputs->returns_capacity)
-    return fail(HELIOS_ERR_CAPACITY, "packed returns need %llu slots, capacity %llu",
-                (unsigned long long)hrtotal, (unsigned long long)outputs->returns_capacity);
-  if (outputs->p_wf_compact && htotal > outputs->wf_compact_capacity)
-    return fail(HELIOS_ERR_CAPACITY, "compact waveform needs %llu floats, capacity %llu",
-                (unsigned long long)htotal, (unsigned long long)outputs->wf_compact_capacity);
+  for (uint32_t j = 0; j < n_jobs; ++j) {
+    const helios_outputs* O = jobs[j].out;
+    if (packed[j] && hrtot[j] > O->returns_capacity)
+      return fail(HELIOS_ERR_CAPACITY, "batch %u: packed returns need %llu slots, capacity %llu",
+                  j, (unsigned long long)hrtot[j], (unsigned long long)O->returns_capacity);
+    if (O->p_wf_compact && htot[j] > O->wf_compact_capacity)
+      return fail(HELIOS_ERR_CAPACITY, "batch %u: compact waveform needs %llu floats, capacity %llu",
+                  j, (unsigned long long)htot[j], (unsigned long long)O->wf_compact_capacity);
+  }
   return HELIOS_OK;
 }
 
@@ -1477,7 +1403,22 @@ extern "C" {
 helios_status helios_simulate(helios_scene sc, const helios_scanner_params* params,
                               const helios_pulses* pulses, const helios_outputs* outputs,
                               helios_stream stream, helios_stats* stats) {
-  return simulate_impl(sc, params, pulses, nullptr, 0, outputs, stream, stats);
+  g_err.clear();
+  if (!pulses || !outputs) return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs is NULL");
+  const Job j{pulses, outputs};
+  return simulate_impl(sc, params, &j, 1, nullptr, 0, stream, stats);
+}
+
+helios_status helios_simulate_batches(helios_scene sc, const helios_scanner_params* params,
+                                      const helios_pulses* pulses, const helios_outputs* outputs,
+                                      uint32_t n_batches, helios_stream stream,
+                                      helios_stats* stats) {
+  g_err.clear();
+  if (n_batches == 0) return HELIOS_OK;
+  if (!pulses || !outputs) return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs is NULL");
+  std::vector<Job> jobs(n_batches);
+  for (uint32_t i = 0; i < n_batches; ++i) jobs[i] = Job{pulses + i, outputs + i};
+  return simulate_impl(sc, params, jobs.data(), n_batches, nullptr, 0, stream, stats);
 }
 
 helios_status helios_simulate_survey(helios_scene sc, const helios_scanner_params* params,
@@ -1487,11 +1428,33 @@ helios_status helios_simulate_survey(helios_scene sc, const helios_scanner_param
                                      helios_stats* stats) {
   g_err.clear();
   if (!survey) return fail(HELIOS_ERR_INVALID_ARGUMENT, "survey is NULL");
+  if (!outputs) return fail(HELIOS_ERR_INVALID_ARGUMENT, "outputs is NULL");
   helios_pulses p{};
   p.n_pulses = n_pulses;
   p.pulse_index_base = pulse_index_base;
-  return simulate_impl(sc, params, &p, survey, first_pulse, outputs, stream, stats);
+  const Job j{&p, outputs};
+  return simulate_impl(sc, params, &j, 1, survey, first_pulse, stream, stats);
+}
+
+helios_status helios_get_tuning(helios_tuning* out) {
+  g_err.clear();
+  if (!out) return fail(HELIOS_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = tuning_snapshot();
+  return HELIOS_OK;
+}
+
+helios_status helios_set_tuning(const helios_tuning* t) {
+  g_err.clear();
+  if (!t) return fail(HELIOS_ERR_INVALID_ARGUMENT, "tuning is NULL");
+  if (t->beam_prepass < -1 || t->beam_prepass > 1 || t->builder < 0 || t->builder > 1 ||
+      t->lane_order < 0 || t->lane_order > 1 || t->pad_lanes < -1 || t->pad_lanes > 1 ||
+      t->serialize < 0 || t->serialize > 1 || t->trace_spans < 0 || t->trace_spans > 1 ||
+      (t->chunk_pulses != 0 && t->chunk_pulses < 1024))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "tuning value out of range");
+  tuning_snapshot();  // seed from the environment first, then override
+  std::lock_guard<std::mutex> g(g_tune_mu);
+  g_tune = *t;
+  return HELIOS_OK;
 }
 
 }  // extern "C"
-

@@ -16,8 +16,12 @@
 #include <stdint.h>
 
 #include "../../include/helios.h"
+#include "../../include/helios_util.h"
 
 namespace helios {
+
+// stream-ordered allocation from the library's private pool (api.cu)
+cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s);
 
 constexpr int kMaxSubrays = 512;      // >= largest supported count (279)
 constexpr int kStackSize = 64;        // LBVH depth bound (checked at build)
@@ -37,7 +41,7 @@ constexpr int kMaxTaps = 8192;        // L_p bound (validated)
 // row[0].x = entry count, row[1 .. count] = (subtree ref, bits of a float lower
 // bound on every subray's entry distance into its box), near-first order
 constexpr int kEntryStride = 32;
-constexpr int kEntryMax = kEntryStride - 1;  // runtime cap TraceArgs::entry_max <= this
+constexpr int kEntryMax = kEntryStride - 1;  // list cap of K6a
 static_assert(kEntryMax <= 32, "K6a keeps its emit flags in 32 bits");
 constexpr double kC = 299792458.0;    // m/s
 constexpr double kPi = 3.14159265358979323846;
@@ -48,11 +52,26 @@ struct __align__(16) TriRecord {
 struct __align__(16) Node {
   float4 xy0, xy1, z01, ref;
 };
-// 4-wide node (128 B = 8 x float4), SoA over the 4 children; unused slots
-// carry kEmptyRef.  Collapsed on the device from the binary LBVH.
-struct __align__(16) Node4 {
-  float4 lox, hix, loy, hiy, loz, hiz, ref, pad;
+// K6 -> K7 waveform record, 8 B per subray: the absolute bin
+// k_s = floor(2 R_s / (c Delta)) (R8, R9; -1 = no event) and the fp32
+// amplitude A_s (Eq. 7).  The prim ids travel in a separate uint32 array that
+// K7 reads only to attribute a return (R13).
+struct __align__(8) WaveRec {
+  int32_t k;
+  float amp;
 };
+
+// Absolute bin k_s = floor(2 R / c / (Delta 1e-9)) -- the oracle's two
+// correctly rounded divisions, bit for bit -- at the cost of one multiply:
+// q = 2R * inv_bin (inv_bin = 1 / (c Delta 1e-9)) is within a few ulp of the
+// same exact quotient, so its floor is the oracle's whenever q is farther than
+// 1e-13 q from an integer; only then (never, in practice) the divisions run.
+__device__ __forceinline__ long long bin_of(double range_m, double delta_ns, double inv_bin) {
+  const double q = 2.0 * range_m * inv_bin;
+  const double f = floor(q);
+  if (q - f > 1e-13 * q && (f + 1.0) - q > 1e-13 * q) return (long long)f;
+  return (long long)floor(2.0 * range_m / 299792458.0 / (delta_ns * 1e-9));
+}
 
 // leaf reference: bit 31 set, bits [3,31) = first triangle, bits [0,3) = count-1
 __host__ __device__ inline int32_t leaf_ref(uint32_t first, uint32_t count) {
@@ -83,8 +102,6 @@ struct TraceArgs {
   const TriRecord* tris;
   const Node* nodes;
   int32_t root;          // root node ref (internal index or leaf ref)
-  const Node4* nodes4;
-  int32_t root4;
   uint32_t n_tris;
   const float* pad;      // voxel grid or nullptr
   uint32_t nx, ny, nz;
@@ -108,16 +125,18 @@ struct TraceArgs {
   double I0;
   int eq2;               // 1: Eq. 2 beam width; 0: far field
   double w0, lambda_m, R0;
-  helios_subray_hit* out;  // [n][N]
+  WaveRec* wrec;          // [n][N] K6 -> K7 records (k_s, A_s)
+  uint32_t* prim;         // [n][N] prim id per subray (UINT32_MAX: no event)
+  helios_subray_hit* out; // [n][N] optional export, or nullptr
+  double delta_ns;        // bin width Delta (k_s in K6)
+  double inv_bin;         // 1 / (c Delta 1e-9)
   unsigned int* err_flag;  // set on zero-length direction
   unsigned long long* counters;  // instrumented variant: [nodes, tris, voxel steps, voxel returns]
   // beam pre-pass (K6a): per-pulse cone over all subrays; nullptr = K6 starts at the root
   int2* entries;         // [n_pulses][kEntryStride] (K6a writes, K6 reads)
-  int entry_max;         // list cap, 2 .. kEntryMax
   double* frames;        // [n_pulses][10] pulse frames d, u, v + valid flag (K6a writes) or nullptr
   double cone_sin;       // sin of the (widened) cone half-angle: max_i sin(theta_i)
   double beam_k;         // a node is handed to K6 once extent <= beam_k * cone radius
-  int beam_budget;       // node tests per pulse, after which the rest is listed coarse
 };
 
 // One echo-width fit job (R28), appended by K7, solved by k_fit.
@@ -129,7 +148,8 @@ struct FitJob {
 };
 
 struct WaveArgs {
-  const helios_subray_hit* rec;  // [n][N]
+  const WaveRec* rec;            // [n][N] (k_s, A_s) from K6
+  const uint32_t* prim;          // [n][N] prim ids (attribution only)
   uint32_t N;
   uint64_t n_pulses;
   uint32_t n_bins;
@@ -179,8 +199,7 @@ cudaError_t launch_generate(const SurveyArgs& a, uint64_t first, uint64_t n, flo
                             float* direction, double* time, cudaStream_t s);
 
 // launchers (trace.cu / waveform.cu)
-// mode: 0 per-ray binary, 1 packet binary, 2 packet 4-wide
-cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s);
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s);
 // K6a: per-pulse beam entry lists into a.entries (before launch_trace, same stream)
 cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s);
 
@@ -193,25 +212,36 @@ struct WavePlan {
 };
 WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);
 // support length len_p of every pulse's waveform (for the compact output)
-cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_pulses,
-                           uint32_t n_bins, uint32_t taps, double delta_ns, uint64_t* len,
-                           cudaStream_t s);
+cudaError_t launch_support(const WaveRec* rec, uint32_t N, uint64_t n_pulses, uint32_t n_bins,
+                           uint32_t taps, uint64_t* len, cudaStream_t s);
 // echo-width fits of the jobs one K7 launch appended (after it; any stream)
 cudaError_t launch_fit(const WaveArgs& a, cudaStream_t s);
 // ranging error on the returns of one launch (after K7, same stream)
 cudaError_t launch_range_noise(const WaveArgs& a, cudaStream_t s);
 // packed returns of one launch: len = n_returns, inclusive scan into
-// offs[1..m] + carry offs[0], copy of the used slots to dst (staged: dst is a
-// chunk buffer based at offs[0]); entries at or past `capacity` are skipped
+// offs[1..m] seeded with the carry offs[0], copy of the used slots to dst
+// (staged: dst is a chunk buffer based at offs[0]); entries at or past
+// `capacity` are skipped
 cudaError_t launch_pack_returns(const helios_return* slots, const uint8_t* nr, uint64_t m,
                                 uint32_t R, uint64_t* len, uint64_t* offs, void* scan_temp,
                                 size_t scan_bytes, helios_return* dst, int staged,
                                 uint64_t capacity, cudaStream_t s);
-// offs[1 + i] += offs[0] for i < m (carry of the previous chunks)
-cudaError_t launch_add_carry(uint64_t* offs, uint64_t m, cudaStream_t s);
 bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps);
 cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scratch,
                             cudaStream_t s);
+
+// prefix sums and the radix sort (sort_scan.cu): temp sizes, then the calls
+// (stream-ordered; in == out allowed for the scans)
+size_t scan_temp_bytes(uint64_t n, size_t elem);
+// seed (device, nullable): *seed is added to every output (chunk carry)
+cudaError_t scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, bool inclusive, void* temp,
+                     size_t temp_bytes, cudaStream_t s, const uint64_t* seed = nullptr);
+cudaError_t scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, bool inclusive, void* temp,
+                     size_t temp_bytes, cudaStream_t s);
+size_t sort_temp_bytes(uint64_t n);
+// stable LSD radix sort of (keys, vals) in place by the low `bits` bits of the keys
+cudaError_t sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t n, int bits, void* temp,
+                           size_t temp_bytes, cudaStream_t s);
 
 // LBVH build (lbvh.cu)
 struct BuildResult {
@@ -221,11 +251,9 @@ struct BuildResult {
   int32_t root;
   uint32_t max_depth;
   float ms;
-  Node4* nodes4;     // device, 4-wide collapse (nullptr if not built)
-  uint32_t n_nodes4;
-  int32_t root4;
 };
-cudaError_t build_lbvh(const float* d_tri_xyz, const float* d_refl, uint32_t n,
+// builder: 0 = PLOC over Morton order (default), 1 = Karras LBVH
+cudaError_t build_lbvh(const float* d_tri_xyz, const float* d_refl, uint32_t n, int builder,
                        cudaStream_t s, BuildResult* out, char* err, size_t err_len);
 
 }  // namespace helios

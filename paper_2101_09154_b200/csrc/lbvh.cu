@@ -5,7 +5,7 @@
 //   K1 centroid bounds (block reduce + ordered-int atomics)
 //   K1 Morton codes of the centroids: 3 x kMortonBits bits over an isotropic
 //      grid (kMortonBits = 21 -> 63-bit codes; DESIGN.md s.8 says why not 30)
-//   K2 radix sort of (code, index)   [CUB onesweep, library sort]
+//   K2 stable LSD radix sort of (code, index), 8 bits per pass (sort_scan.cu)
 //   K3 Karras hierarchy: N-1 internal nodes, delta = clz(code_i ^ code_j),
 //      index tie-break (64 + clz(i ^ j)) for duplicate codes
 //   K4 bottom-up AABB refit (second-arriving child computes the parent)
@@ -13,9 +13,6 @@
 //      collapsed into leaves, triangles permuted to leaf order (48 B).
 // fp32 min/max of fp32 vertices is exact, so every box contains its
 // triangles exactly; traversal adds the conservative slack (trace.cu).
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include <vector>
 
 #include <cstdio>
@@ -269,7 +266,7 @@ __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict
 }
 
 // ---- PLOC (parallel locally-ordered clustering, Meister & Bittner 2018) ----
-// Alternative hierarchy (HELIOS_BUILDER=ploc): clusters start as the sorted
+// The default hierarchy (the Karras LBVH stays available as builder 1): clusters start as the sorted
 // triangles; each iteration every cluster finds, among the 2R clusters around
 // it in Morton order, the one whose merged box has the smallest surface area
 // (ties -> lower index); mutual nearest neighbours merge (the lower index
@@ -278,10 +275,6 @@ __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict
 // cluster is left.  Leaves are then ordered depth-first (offsets top-down,
 // iteration by iteration) so collapsed subtrees are contiguous triangle runs.
 constexpr int kPlocBlock = 256;
-#ifndef HELIOS_DEFAULT_PLOC
-#define HELIOS_DEFAULT_PLOC 1
-#endif
-constexpr bool kDefaultPloc = HELIOS_DEFAULT_PLOC != 0;
 
 __device__ __forceinline__ float merged_area(const float* a, const float* b) {
   const float dx = fmaxf(a[3], b[3]) - fminf(a[0], b[0]);
@@ -447,114 +440,21 @@ __global__ void k_ploc_layout(uint32_t n, const int* __restrict__ child,
   nodes[u] = nd;
 }
 
-// ---- 4-wide collapse (top-down, one kernel per level) ----------------------
-// Each queue entry (binary node b, wide node w) expands b's children greedily:
-// while fewer than 4, replace the internal child with the largest box surface
-// area by its two children.  Internal children of the result become new wide
-// nodes (queued for the next level).
-__device__ __forceinline__ float box_area(const float* b) {
-  const float dx = b[1] - b[0], dy = b[3] - b[2], dz = b[5] - b[4];
-  return dx * dy + dy * dz + dz * dx;
-}
-
-__device__ __forceinline__ void child_of(const Node& nd, int k, int32_t* ref, float* b) {
-  if (k == 0) {
-    b[0] = nd.xy0.x; b[1] = nd.xy0.y; b[2] = nd.xy0.z; b[3] = nd.xy0.w;
-    b[4] = nd.z01.x; b[5] = nd.z01.y;
-    *ref = __float_as_int(nd.ref.x);
-  } else {
-    b[0] = nd.xy1.x; b[1] = nd.xy1.y; b[2] = nd.xy1.z; b[3] = nd.xy1.w;
-    b[4] = nd.z01.z; b[5] = nd.z01.w;
-    *ref = __float_as_int(nd.ref.y);
-  }
-}
-
-__global__ void k_collapse4(const Node* __restrict__ nodes, const int2* __restrict__ qin,
-                            uint32_t n_in, int2* __restrict__ qout, unsigned* __restrict__ n_out,
-                            unsigned* __restrict__ n_wide, Node4* __restrict__ wide) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_in) return;
-  const int2 e = qin[t];
-  int32_t ref[4];
-  float box[4][6];
-  int cnt = 2;
-  {
-    const Node nd = nodes[e.x];
-    child_of(nd, 0, &ref[0], box[0]);
-    child_of(nd, 1, &ref[1], box[1]);
-  }
-  while (cnt < 4) {
-    int pick = -1;
-    float best = -1.0f;
-    for (int i = 0; i < cnt; ++i)
-      if (!ref_is_leaf(ref[i])) {
-        const float a = box_area(box[i]);
-        if (a > best) {
-          best = a;
-          pick = i;
-        }
-      }
-    if (pick < 0) break;
-    const Node nd = nodes[ref[pick]];
-    child_of(nd, 0, &ref[pick], box[pick]);
-    child_of(nd, 1, &ref[cnt], box[cnt]);
-    ++cnt;
-  }
-  float lo[3][4], hi[3][4];
-  int32_t out_ref[4];
-  for (int i = 0; i < 4; ++i) {
-    if (i < cnt) {
-      for (int a = 0; a < 3; ++a) {
-        lo[a][i] = box[i][2 * a];
-        hi[a][i] = box[i][2 * a + 1];
-      }
-      if (ref_is_leaf(ref[i])) {
-        out_ref[i] = ref[i];
-      } else {
-        const unsigned w = atomicAdd(n_wide, 1u);
-        const unsigned q = atomicAdd(n_out, 1u);
-        qout[q] = make_int2(ref[i], (int)w);
-        out_ref[i] = (int32_t)w;
-      }
-    } else {
-      for (int a = 0; a < 3; ++a) {
-        lo[a][i] = 0.0f;
-        hi[a][i] = 0.0f;
-      }
-      out_ref[i] = kEmptyRef;
-    }
-  }
-  Node4 w;
-  w.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-  w.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-  w.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-  w.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-  w.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-  w.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
-  w.ref = make_float4(__int_as_float(out_ref[0]), __int_as_float(out_ref[1]),
-                      __int_as_float(out_ref[2]), __int_as_float(out_ref[3]));
-  w.pad = make_float4(0.f, 0.f, 0.f, 0.f);
-  wide[e.y] = w;
-}
-
 template <class T>
 cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
-  return cudaMallocAsync((void**)p, sizeof(T) * (count ? count : 1), s);
+  return dev_alloc((void**)p, sizeof(T) * (count ? count : 1), s);
 }
 
 }  // namespace
 
-cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStream_t s,
-                       BuildResult* out, char* err, size_t err_len) {
+cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int builder,
+                       cudaStream_t s, BuildResult* out, char* err, size_t err_len) {
   out->tris = nullptr;
   out->nodes = nullptr;
   out->n_nodes = 0;
   out->root = kEmptyRef;
   out->max_depth = 0;
   out->ms = 0.f;
-  out->nodes4 = nullptr;
-  out->n_nodes4 = 0;
-  out->root4 = kEmptyRef;
   if (n == 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -563,10 +463,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   uint32_t *idx = nullptr, *idx_s = nullptr;
   int *child = nullptr, *parent_int = nullptr, *parent_leaf = nullptr, *range = nullptr;
   float *leafbox = nullptr, *nodebox = nullptr;
-  unsigned *flags = nullptr, *dmax = nullptr, *wcnt = nullptr;
-  int2 *qa = nullptr, *qb = nullptr;
-  Node4* wide_tmp = nullptr;
-  unsigned hw[2] = {0, 0};
+  unsigned *flags = nullptr, *dmax = nullptr;
   void* temp = nullptr;
   size_t temp_bytes = 0;
   const int T = 256;
@@ -575,18 +472,11 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   unsigned init_bounds[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
   unsigned hdepth = 0;
   uint32_t* idx_s_final = nullptr;  // leaf order (PLOC), else the Morton order
-  // tuning knobs for measurements (DESIGN.md s.8): HELIOS_MORTON_BITS (1..21),
-  // HELIOS_MORTON_ANISO=1 (per-axis normalisation)
-  int bits = kMortonBits, isotropic = 1;
-  if (const char* v = getenv("HELIOS_MORTON_BITS")) bits = atoi(v);
-  if (bits < 1 || bits > 21) bits = kMortonBits;
-  if (const char* v = getenv("HELIOS_MORTON_ANISO")) isotropic = atoi(v) ? 0 : 1;
-  // hierarchy: HELIOS_BUILDER=lbvh (Karras) | ploc (default: see DESIGN.md s.7.1)
-  bool use_ploc = kDefaultPloc;
-  if (const char* v = getenv("HELIOS_BUILDER")) use_ploc = strcmp(v, "lbvh") != 0;
-  int ploc_r = 32;
-  if (const char* v = getenv("HELIOS_PLOC_R")) ploc_r = atoi(v);
-  if (ploc_r < 1 || ploc_r > 256) ploc_r = 32;
+  // isotropic 63-bit Morton codes (DESIGN.md s.7.1); hierarchy: PLOC with
+  // radius 32 (default) or Karras (builder = 1)
+  const int bits = kMortonBits, isotropic = 1;
+  const bool use_ploc = builder != 1;
+  constexpr int ploc_r = 32;
   int *pcid = nullptr, *pcid2 = nullptr, *pnn = nullptr, *pparent = nullptr;
   float *pbox = nullptr, *pbox2 = nullptr;
   uint32_t *psize = nullptr, *poff = nullptr, *pdepth = nullptr, *porder = nullptr;
@@ -610,21 +500,20 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
   CK(cudaMemcpyAsync(bounds, init_bounds, sizeof(init_bounds), cudaMemcpyHostToDevice, s));
   CK(dalloc(&codes, n, s));
   CK(dalloc(&idx, n, s));
-  CK(dalloc(&codes_s, n, s));
-  CK(dalloc(&idx_s, n, s));
   CK(dalloc(&out->tris, n, s));
   k_centroid_bounds<<<min(nb, 148u * 8u), T, 0, s>>>(xyz, n, bounds);
   CK(cudaGetLastError());
   k_morton<<<nb, T, 0, s>>>(xyz, n, bounds, codes, idx, bits, isotropic);
   CK(cudaGetLastError());
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0,
-                                     3 * bits, s));
-  CK(cudaMallocAsync(&temp, temp_bytes ? temp_bytes : 1, s));
-  CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, codes, codes_s, idx, idx_s, (int)n, 0,
-                                     3 * bits, s));
+  temp_bytes = sort_temp_bytes(n);
+  CK(dev_alloc(&temp, temp_bytes, s));
+  CK(sort_pairs_u64(codes, idx, n, 3 * bits, temp, temp_bytes, s));
+  codes_s = codes;  // sorted in place
+  idx_s = idx;
+  codes = nullptr;
+  idx = nullptr;
   if (n <= (uint32_t)kLeafMax) {
     out->root = leaf_ref(0, n);
-    out->root4 = out->root;
     out->max_depth = 0;
   } else if (use_ploc) {
     CK(dalloc(&pcid, n, s));
@@ -645,8 +534,8 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     CK(dalloc(&dmax, 1, s));
     CK(dalloc(&out->nodes, n - 1, s));
     CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned), s));
-    CK(cub::DeviceScan::InclusiveSum(nullptr, ptemp_bytes, pflags, pincl, (int)n, s));
-    CK(cudaMallocAsync(&ptemp, ptemp_bytes ? ptemp_bytes : 1, s));
+    ptemp_bytes = scan_temp_bytes(n, sizeof(unsigned long long));
+    CK(dev_alloc(&ptemp, ptemp_bytes, s));
     k_ploc_init<<<nb, T, 0, s>>>(xyz, idx_s, n, pcid, pbox, psize);
     CK(cudaGetLastError());
     {
@@ -660,7 +549,8 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
         k_ploc_flags<<<(m + T - 1) / T, T, 0, s>>>(pnn, m, pflags);
         CK(cudaGetLastError());
         size_t tb = ptemp_bytes;
-        CK(cub::DeviceScan::InclusiveSum(ptemp, tb, pflags, pincl, (int)m, s));
+        CK(scan_u64(reinterpret_cast<const uint64_t*>(pflags), reinterpret_cast<uint64_t*>(pincl),
+                    m, true, ptemp, tb, s));
         k_ploc_merge<<<(m + T - 1) / T, T, 0, s>>>(pnn, m, pflags, pincl, n, base, pcid, pbox,
                                                   pcid2, pbox2, child, nodebox, psize, pparent);
         CK(cudaGetLastError());
@@ -724,42 +614,6 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, cudaStre
     out->n_nodes = n - 1;
     out->root = 0;
   }
-  {
-    // 4-wide collapse, level by level (opt-in: HELIOS_BVH4=1; measured no faster
-    // than packet traversal of the binary tree, profiles/r01_wide_ab.txt)
-    const char* w4 = getenv("HELIOS_BVH4");
-    if (w4 && atoi(w4) && n > (uint32_t)kLeafMax) {
-    CK(dalloc(&qa, n - 1, s));
-    CK(dalloc(&qb, n - 1, s));
-    CK(dalloc(&wcnt, 2, s));
-    CK(dalloc(&wide_tmp, n - 1, s));
-    {
-      const int2 root_entry = make_int2(out->root, 0);
-      const unsigned init[2] = {0u, 1u};  // next-queue size, wide nodes allocated
-      CK(cudaMemcpyAsync(qa, &root_entry, sizeof(int2), cudaMemcpyHostToDevice, s));
-      uint32_t n_in = 1;
-      while (n_in > 0) {
-        CK(cudaMemcpyAsync(wcnt, init, sizeof(unsigned), cudaMemcpyHostToDevice, s));
-        if (hw[1] == 0) CK(cudaMemcpyAsync(wcnt + 1, init + 1, sizeof(unsigned),
-                                           cudaMemcpyHostToDevice, s));
-        k_collapse4<<<(n_in + T - 1) / T, T, 0, s>>>(out->nodes, qa, n_in, qb, wcnt, wcnt + 1,
-                                                    wide_tmp);
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(hw, wcnt, sizeof(hw), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        n_in = hw[0];
-        int2* tq = qa;
-        qa = qb;
-        qb = tq;
-      }
-    }
-    out->n_nodes4 = hw[1];
-    CK(dalloc(&out->nodes4, out->n_nodes4, s));
-    CK(cudaMemcpyAsync(out->nodes4, wide_tmp, sizeof(Node4) * out->n_nodes4,
-                       cudaMemcpyDeviceToDevice, s));
-    out->root4 = 0;
-    }
-  }
   k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s_final ? idx_s_final : idx_s, n, out->tris);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e1, s));
@@ -787,10 +641,6 @@ done:
   cudaFreeAsync(nodebox, s);
   cudaFreeAsync(flags, s);
   cudaFreeAsync(dmax, s);
-  cudaFreeAsync(wcnt, s);
-  cudaFreeAsync(qa, s);
-  cudaFreeAsync(qb, s);
-  cudaFreeAsync(wide_tmp, s);
   cudaFreeAsync(pcid, s);
   cudaFreeAsync(pcid2, s);
   cudaFreeAsync(pnn, s);
@@ -809,10 +659,8 @@ done:
   if (e != cudaSuccess) {
     cudaFreeAsync(out->tris, s);
     cudaFreeAsync(out->nodes, s);
-    cudaFreeAsync(out->nodes4, s);
     out->tris = nullptr;
     out->nodes = nullptr;
-    out->nodes4 = nullptr;
   }
   cudaStreamSynchronize(s);
   return e;

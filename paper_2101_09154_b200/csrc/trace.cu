@@ -32,15 +32,6 @@ namespace helios {
 namespace {
 
 constexpr float kBoxSlack = 1e-6f;  // >> 5 * 2^-24 relative error of an fp32 slab value
-// lazy culling of popped stack entries compares the stored (already widened)
-// entry distance with t_best rounded to fp32, widened again
-constexpr float kCullSlack = 1.0f + 4.0f * kBoxSlack;
-#ifndef HELIOS_LAZY_CULL
-#define HELIOS_LAZY_CULL 0
-#endif
-#ifndef HELIOS_PREDICATED_BOX
-#define HELIOS_PREDICATED_BOX 0
-#endif
 
 // fp64 helpers with explicit round-to-nearest intrinsics: no FMA contraction,
 // so every expression below evaluates exactly like the oracle's (same
@@ -142,33 +133,6 @@ __device__ __forceinline__ F3 fcross(F3 a, F3 b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 __device__ __forceinline__ float l1(F3 a) { return fabsf(a.x) + fabsf(a.y) + fabsf(a.z); }
-
-__device__ __forceinline__ bool mt32_definite_miss(const F3& o, const F3& d, float dl1,
-                                                   const TriRecord& tr, float t_hi) {
-  constexpr float kU = 32.0f * 5.9604645e-8f;
-  const F3 v0 = {tr.a.x, tr.a.y, tr.a.z};
-  const F3 e1 = fsub({tr.b.x, tr.b.y, tr.b.z}, v0);
-  const F3 e2 = fsub({tr.c.x, tr.c.y, tr.c.z}, v0);
-  const F3 sv = fsub(o, v0);
-  const float A = l1(e1), B = l1(e2), S = l1(sv);
-  const F3 p = fcross(d, e2);
-  const float det = fdot(e1, p);
-  const float err_det = kU * A * dl1 * B;
-  const float adet = fabsf(det);
-  if (!(adet > err_det)) return false;  // sign of det uncertain (or NaN): decide in fp64
-  const float sg = det > 0.0f ? 1.0f : -1.0f;
-  const float nu = fdot(sv, p) * sg;
-  const F3 q = fcross(sv, e1);
-  const float nv = fdot(d, q) * sg;
-  const float nt = fdot(e2, q) * sg;
-  const float err_u = kU * S * dl1 * B, err_v = kU * S * A * dl1, err_t = kU * B * S * A;
-  if (nu < -err_u || nv < -err_v || nt < -err_t) return true;  // u < 0, v < 0, t < 0
-  if (nu - adet > err_u + err_det) return true;                 // u > 1
-  if ((nu + nv) - adet > (err_u + err_v + err_det) * 1.0001f) return true;  // u + v > 1
-  // t = nt / adet > t_hi (cannot be the nearest hit)
-  if (t_hi < 3.0e38f && nt - t_hi * adet > (err_t + t_hi * err_det) * 1.0001f + 1e-30f) return true;
-  return false;
-}
 
 // The same filter with a third outcome: 2 = a DEFINITE hit (u >= 0, v >= 0,
 // u + v <= 1 and t > 0 each hold beyond the error bound, so the fp64 test
@@ -348,68 +312,6 @@ __device__ __forceinline__ bool ray_cube(const double o[3], const double d[3], c
   return true;
 }
 
-// Per-ray traversal (one thread walks its own subray; "while-while", stack in
-// local memory).  Returns through t_best / best_id / best_k.
-template <bool INSTR>
-__device__ __forceinline__ void traverse_ray(const TraceArgs& a, const D3& O, const D3& D,
-                                             const F3& O32, const F3& D32, float dl1, float ix,
-                                             float iy, float iz, double& t_best,
-                                             uint32_t& best_id, uint32_t& best_k,
-                                             unsigned long long& c_nodes,
-                                             unsigned long long& c_tris,
-                                             unsigned long long& c_f64) {
-  int32_t stack[kStackSize];
-  int sp = 0;
-  int32_t ref = a.root;
-  for (;;) {
-    if (ref_is_leaf(ref)) {
-      const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
-      const float t_hi = __double2float_ru(t_best);
-      for (uint32_t k = first; k < first + cnt; ++k) {
-        const TriRecord tr = load_tri(a.tris, k);
-        if (INSTR) ++c_tris;
-        if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
-        if (INSTR) ++c_f64;
-        const double t = mt64(O, D, tr);
-        if (t > 0.0) {
-          const uint32_t id = __float_as_uint(tr.a.w);
-          if (t < t_best || (t == t_best && id < best_id)) {
-            t_best = t;
-            best_id = id;
-            best_k = k;
-          }
-        }
-      }
-      if (sp == 0) break;
-      ref = stack[--sp];
-      continue;
-    }
-    const Node* nd = a.nodes + ref;
-    const float4 xy0 = __ldg(&nd->xy0), xy1 = __ldg(&nd->xy1), z01 = __ldg(&nd->z01),
-                 rf = __ldg(&nd->ref);
-    if (INSTR) ++c_nodes;
-    const float tb = (float)t_best;
-    const float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix,
-                               iy, iz, tb);
-    const float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix,
-                               iy, iz, tb);
-    const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
-    const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
-    if (h0 && h1) {
-      const bool near0 = t0 <= t1;
-      ref = near0 ? r0 : r1;
-      stack[sp++] = near0 ? r1 : r0;
-    } else if (h0) {
-      ref = r0;
-    } else if (h1) {
-      ref = r1;
-    } else {
-      if (sp == 0) break;
-      ref = stack[--sp];
-    }
-  }
-}
-
 // Warp-cooperative masked packet traversal.  The 32 lanes of a warp hold
 // consecutive (pulse, subray) rays -- the nearly parallel subrays of one or
 // two pulses (beam divergence <= 0.5 mrad here).  The warp walks ONE
@@ -434,25 +336,12 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   int32_t stA_r = 0, stB_r = 0;
   unsigned stA_m = 0, stB_m = 0;
   int sp = 0;
-#if HELIOS_LAZY_CULL
-  float tstk[kStackSize];  // this lane's entry distance into every pushed child
-#endif
-  // pop; with HELIOS_LAZY_CULL, lanes whose t_best is already nearer than
-  // their entry into the child leave its mask, and emptied entries are
-  // skipped without loading the node
   auto pop = [&]() -> bool {
-    for (;;) {
-      if (sp == 0) return false;
-      --sp;
-      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
-      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
-#if HELIOS_LAZY_CULL
-      m = __ballot_sync(kFull, ((m >> lane) & 1u) && !(tstk[sp] > hs.bound * kCullSlack));
-      if (m) return true;
-#else
-      return true;
-#endif
-    }
+    if (sp == 0) return false;
+    --sp;
+    ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
+    m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
+    return true;
   };
   for (;;) {
     const bool mine = (m >> lane) & 1u;
@@ -489,15 +378,6 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
                  rf = __ldg(&nd->ref);
     // every lane tests (the warp issues the instructions either way); lanes
     // outside the mask are masked out of the result -- no divergent branch
-#if HELIOS_PREDICATED_BOX
-    if (INSTR && mine) ++c_nodes;
-    const float tb = hs.bound;
-    float t0 = box_enter(xy0.x, xy0.y, xy0.z, xy0.w, z01.x, z01.y, O32.x, O32.y, O32.z, ix, iy,
-                         iz, tb);
-    float t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy,
-                         iz, tb);
-    if (!mine) t0 = t1 = INFINITY;
-#else
     float t0 = INFINITY, t1 = INFINITY;
     if (mine) {
       if (INSTR) ++c_nodes;
@@ -507,7 +387,6 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
       t1 = box_enter(xy1.x, xy1.y, xy1.z, xy1.w, z01.z, z01.w, O32.x, O32.y, O32.z, ix, iy, iz,
                      tb);
     }
-#endif
     const int32_t r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y);
     const bool h0 = t0 < INFINITY, h1 = t1 < INFINITY;
     const unsigned m0 = __ballot_sync(kFull, h0), m1 = __ballot_sync(kFull, h1);
@@ -526,9 +405,6 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
           stB_m = far_m;
         }
       }
-#if HELIOS_LAZY_CULL
-      tstk[sp] = near0 ? t1 : t0;
-#endif
       ++sp;
       ref = near0 ? r0 : r1;
       m = near0 ? m0 : m1;
@@ -541,127 +417,6 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
     } else {
       if (!pop()) break;
     }
-  }
-}
-
-// 4-wide variant of the packet traversal: each step tests the 4 children of
-// a Node4 (one 128-B broadcast load), visits the hit children nearest-first
-// (ordered by the entry distance of the lowest lane that hits each child) and
-// pushes the others with their lane masks.
-template <bool INSTR>
-__device__ __forceinline__ void traverse_packet4(const TraceArgs& a, unsigned m, const D3& O,
-                                                 const D3& D, const F3& O32, const F3& D32,
-                                                 float dl1, float ix, float iy, float iz,
-                                                 double& t_best, uint32_t& best_id,
-                                                 uint32_t& best_k, unsigned long long& c_nodes,
-                                                 unsigned long long& c_tris,
-                                                 unsigned long long& c_f64) {
-  const unsigned kFull = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  int32_t stA_r = 0, stB_r = 0;
-  unsigned stA_m = 0, stB_m = 0;
-  int sp = 0;
-  int32_t ref = a.root4;
-  float tstk[kStackSize];  // this lane's entry distance of every pushed child
-  auto push = [&](int32_t r, unsigned mk, float tl) {
-    if (lane == (sp & 31)) {
-      if (sp < 32) {
-        stA_r = r;
-        stA_m = mk;
-      } else {
-        stB_r = r;
-        stB_m = mk;
-      }
-    }
-    tstk[sp] = tl;
-    ++sp;
-  };
-  // pop with lazy culling: lanes whose t_best is already nearer than their
-  // entry distance into the child leave its mask; empty entries are skipped
-  // without loading the node.  Returns false when the stack is exhausted.
-  auto pop = [&]() -> bool {
-    for (;;) {
-      if (sp == 0) return false;
-      --sp;
-      ref = __shfl_sync(kFull, sp < 32 ? stA_r : stB_r, sp & 31);
-      m = __shfl_sync(kFull, sp < 32 ? stA_m : stB_m, sp & 31);
-      const bool keep = ((m >> lane) & 1u) && !(tstk[sp] > (float)t_best * kCullSlack);
-      m = __ballot_sync(kFull, keep);
-      if (m) return true;
-    }
-  };
-  for (;;) {
-    const bool mine = (m >> lane) & 1u;
-    if (ref_is_leaf(ref)) {
-      if (mine) {
-        const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
-        const float t_hi = __double2float_ru(t_best);
-        for (uint32_t k = first; k < first + cnt; ++k) {
-          const TriRecord tr = load_tri(a.tris, k);
-          if (INSTR) ++c_tris;
-          if (mt32_definite_miss(O32, D32, dl1, tr, t_hi)) continue;
-          if (INSTR) ++c_f64;
-          const double t = mt64(O, D, tr);
-          if (t > 0.0) {
-            const uint32_t id = __float_as_uint(tr.a.w);
-            if (t < t_best || (t == t_best && id < best_id)) {
-              t_best = t;
-              best_id = id;
-              best_k = k;
-            }
-          }
-        }
-      }
-      if (!pop()) break;
-      continue;
-    }
-    const Node4* nd = a.nodes4 + ref;
-    const float4 lx = __ldg(&nd->lox), hx = __ldg(&nd->hix), ly = __ldg(&nd->loy),
-                 hy = __ldg(&nd->hiy), lz = __ldg(&nd->loz), hz = __ldg(&nd->hiz),
-                 rf = __ldg(&nd->ref);
-    const int32_t r[4] = {__float_as_int(rf.x), __float_as_int(rf.y), __float_as_int(rf.z),
-                          __float_as_int(rf.w)};
-    float t[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-    if (mine) {
-      if (INSTR) ++c_nodes;
-      const float tb = (float)t_best;
-      t[0] = box_enter(lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, O32.x, O32.y, O32.z, ix, iy, iz, tb);
-      t[1] = box_enter(lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, O32.x, O32.y, O32.z, ix, iy, iz, tb);
-      if (r[2] != kEmptyRef)
-        t[2] = box_enter(lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, O32.x, O32.y, O32.z, ix, iy, iz, tb);
-      if (r[3] != kEmptyRef)
-        t[3] = box_enter(lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, O32.x, O32.y, O32.z, ix, iy, iz, tb);
-    }
-    // per child: lane mask and a warp-uniform ordering key
-    unsigned mk[4];
-    float key[4];
-    int32_t rr[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      mk[i] = __ballot_sync(kFull, t[i] < INFINITY);
-      const float ti = __shfl_sync(kFull, t[i], mk[i] ? (__ffs(mk[i]) - 1) : 0);
-      key[i] = mk[i] ? ti : INFINITY;
-      rr[i] = r[i];
-    }
-    // sort the 4 (key, ref, mask, own t) tuples ascending (5-exchange network)
-#define HELIOS_CSWAP(i, j)                                            \
-    if (key[j] < key[i]) {                                            \
-      const float tk = key[i]; key[i] = key[j]; key[j] = tk;          \
-      const int32_t trf = rr[i]; rr[i] = rr[j]; rr[j] = trf;          \
-      const unsigned tm = mk[i]; mk[i] = mk[j]; mk[j] = tm;           \
-      const float tt = t[i]; t[i] = t[j]; t[j] = tt;                  \
-    }
-    HELIOS_CSWAP(0, 1) HELIOS_CSWAP(2, 3) HELIOS_CSWAP(0, 2) HELIOS_CSWAP(1, 3) HELIOS_CSWAP(1, 2)
-#undef HELIOS_CSWAP
-    if (!mk[0]) {  // nothing hit (keys of misses are +inf, sorted last)
-      if (!pop()) break;
-      continue;
-    }
-    if (mk[3]) push(rr[3], mk[3], t[3]);
-    if (mk[2]) push(rr[2], mk[2], t[2]);
-    if (mk[1]) push(rr[1], mk[1], t[1]);
-    ref = rr[0];
-    m = mk[0];
   }
 }
 
@@ -780,7 +535,7 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   const float kr = (float)(a.beam_k * sa);  // hand-over: extent <= beam_k * cone radius
   int visits = 0;
   // work stack of (ref, entry distance); bit i of `emit` marks entry i as
-  // final (listed when popped).  Invariant: count + sp <= entry_max, so the
+  // final (listed when popped).  Invariant: count + sp <= kEntryMax, so the
   // list never overflows: a node is expanded only while both children still
   // fit, else it is listed whole (coarser, still exact).  Listed distances are
   // shrunk by kBoxSlack: K6 drops a lane from an entry only when its nearest
@@ -789,17 +544,15 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   float stt[kEntryMax];
   uint32_t emit = 0;
   int sp = 0, cnt = 0;
-  const int cap = a.entry_max;
+  constexpr int cap = kEntryMax;
   stk[0] = a.root;
   stt[0] = 0.0f;
   sp = 1;
   while (sp > 0) {
     --sp;
     const int32_t ref = stk[sp];
-    // listed: final entries, leaves, nodes whose children would not fit, and
-    // everything left once the walk has spent its node budget (bounds the
-    // walk's latency: K6 walks coarse entries itself)
-    if (((emit >> sp) & 1u) || ref_is_leaf(ref) || cnt + sp + 2 > cap || visits >= a.beam_budget) {
+    // listed: final entries, leaves, and nodes whose children would not fit
+    if (((emit >> sp) & 1u) || ref_is_leaf(ref) || cnt + sp + 2 > cap) {
       row[1 + cnt++] = make_int2(ref, __float_as_int(stt[sp]));
       continue;
     }
@@ -839,6 +592,27 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
   }
 }
 
+// A5 -> A6 hand-over of one subray's event (range R, amplitude A_s, prim; a
+// miss has prim UINT32_MAX): the 8-B waveform record {k_s, A_s} K7 bins
+// (k_s = floor(2 R / (c Delta)), R8/R9, computed here in fp64), the prim id
+// K7 reads only to attribute a return (R13), and the optional 16-B export.
+__device__ __forceinline__ void store_event(const TraceArgs& a, uint64_t slot, double R,
+                                            float amp, uint32_t pid) {
+  const bool hit = pid != 0xFFFFFFFFu;
+  WaveRec w;
+  w.k = hit ? (int32_t)bin_of(R, a.delta_ns, a.inv_bin) : -1;
+  w.amp = hit ? amp : 0.0f;
+  *reinterpret_cast<int2*>(a.wrec + slot) = make_int2(w.k, __float_as_int(w.amp));
+  a.prim[slot] = pid;
+  if (a.out) {
+    helios_subray_hit h;
+    h.range_m = hit ? R : __longlong_as_double(0x7FF8000000000000ll);  // NaN on a miss
+    h.amplitude = w.amp;
+    h.prim_id = pid;
+    a.out[slot] = h;
+  }
+}
+
 #ifndef HELIOS_TRACE_T
 #define HELIOS_TRACE_T 128  // K6 threads per block
 #endif
@@ -848,7 +622,7 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
 // GRID: 0 no voxel grid, 1 transmissive voxels, 2 opaque / scaled cubes --
 // the A4 march is compiled in only where needed, so each scene kind keeps
 // the traversal's register budget
-template <bool INSTR, bool PACKET, bool WIDE, int GRID>
+template <bool INSTR, int GRID>
 __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 / HELIOS_TRACE_T) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // a pulse occupies a.lanes (>= N) consecutive threads: N, or N padded to
@@ -859,7 +633,6 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
   const uint32_t gq = (uint32_t)(gid < total ? gid : 0);
   const uint64_t pq0 = gq / NL;
   const bool in_range = gid < total && gq - (uint32_t)pq0 * NL < a.N;
-  if (!PACKET && !in_range) return;
   const uint32_t g32 = in_range ? gq : 0;  // padding / out-of-range lanes ride along
   const uint64_t p = g32 / NL;
   // lane position j of the pulse -> subray s (the table is in K6's lane order,
@@ -867,13 +640,9 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
   const uint32_t j = g32 - (uint32_t)p * NL;
   const SubrayConst sc = a.sub[j];
   const uint32_t s = sc.index;
-  helios_subray_hit* const out_rec = a.out + p * a.N + s;
+  const uint64_t slot = p * a.N + s;  // [pulse][subray] (R4 order) in every output
   unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;
 
-  helios_subray_hit rec;
-  rec.range_m = __longlong_as_double(0x7FF8000000000000ll);  // NaN
-  rec.amplitude = 0.0f;
-  rec.prim_id = 0xFFFFFFFFu;
 
   // ---- A2: subray fan-out (R2, R4), fp64
   const float ox = __ldg(a.origin + 3 * p), oy = __ldg(a.origin + 3 * p + 1),
@@ -892,10 +661,6 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
     valid = pulse_frame(a.direction + 3 * p, Dp, U, V) && in_range;
   }
   if (in_range && !valid && s == 0) atomicOr(a.err_flag, 1u);
-  if (!PACKET && !valid) {
-    *out_rec = rec;
-    return;
-  }
   // d_s = cos(theta) d + sin(theta) (cos(phi) u + sin(phi) v)
   const D3 ring = vadd(scale(U, sc.cos_p), scale(V, sc.sin_p));
   const D3 D = vadd(scale(Dp, sc.cos_t), scale(ring, sc.sin_t));
@@ -909,13 +674,10 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
     const F3 O32 = {ox, oy, oz};
     const F3 D32 = {(float)D.x, (float)D.y, (float)D.z};
     const float dl1 = l1(D32);
-    if (PACKET) {
+    {
       const unsigned m = __ballot_sync(0xffffffffu, valid);
       if (m) {
-        if (WIDE)
-          traverse_packet4<INSTR>(a, m, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k,
-                                  c_nodes, c_tris, c_f64);
-        else {
+        {
           // beam entry lists (K6a): the warp walks, pulse by pulse, the subtrees
           // the pulse's cone reaches, each with the lanes of that pulse; without
           // lists, one walk from the root with every lane.  A warp can hold the
@@ -987,13 +749,10 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
           best_k = hs.best_k;
         }
       }
-    } else {
-      traverse_ray<INSTR>(a, O, D, O32, D32, dl1, ix, iy, iz, t_best, best_id, best_k, c_nodes,
-                          c_tris, c_f64);
     }
   }
   if (!valid) {
-    if (in_range) *out_rec = rec;
+    if (in_range) store_event(a, slot, 0.0, 0.0f, 0xFFFFFFFFu);
     return;
   }
 
@@ -1170,6 +929,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
     sig_eff = (double)tr.b.w * cos_inc;
     pid = best_id;
   }
+  float amp = 0.0f;
   if (pid != 0xFFFFFFFFu) {
     double I;
     if (a.eq2) {
@@ -1181,23 +941,21 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
     } else {
       I = a.I0 * sc.w_far;
     }
-    rec.range_m = R;
     const double r2 = R * R;
-    rec.amplitude = (float)(a.K * sig_eff * I * __drcp_rn(r2 * r2));
-    rec.prim_id = pid;
+    amp = (float)(a.K * sig_eff * I * __drcp_rn(r2 * r2));
   }
-  *out_rec = rec;
+  store_event(a, slot, R, amp, pid);
 
   if (INSTR) {
     // warp-aggregated (one atomic per warp and counter; per-thread counts < 2^32)
     const unsigned mask = __activemask();
     const bool leader = (threadIdx.x & 31) == __ffs(mask) - 1;
     const unsigned long long v[5] = {c_nodes, c_tris, c_vox, c_voxret, c_f64};
-    const int slot[5] = {0, 1, 2, 3, 6};
+    const int cslot[5] = {0, 1, 2, 3, 6};
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       const unsigned w = __reduce_add_sync(mask, (unsigned)v[i]);
-      if (leader && w) atomicAdd(a.counters + slot[i], (unsigned long long)w);
+      if (leader && w) atomicAdd(a.counters + cslot[i], (unsigned long long)w);
     }
   }
 }
@@ -1218,7 +976,7 @@ cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaStream_t s) {
+cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) {
   if (a.lanes < a.N) return cudaErrorInvalidValue;
   const uint64_t total = a.n_pulses * (uint64_t)a.lanes;
   if (total == 0) return cudaSuccess;
@@ -1227,22 +985,15 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, int mode, cudaSt
   if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
   const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
-#define HELIOS_TRACE_CASE(I, P, W)                                        \
-  if (grid == 1)                                                          \
-    k_trace<I, P, W, 1><<<g, T, 0, s>>>(a);                               \
-  else if (grid == 2)                                                     \
-    k_trace<I, P, W, 2><<<g, T, 0, s>>>(a);                               \
-  else                                                                    \
-    k_trace<I, P, W, 0><<<g, T, 0, s>>>(a);
-  switch (mode * 2 + (instrumented ? 1 : 0)) {
-    case 0: HELIOS_TRACE_CASE(false, false, false) break;
-    case 1: HELIOS_TRACE_CASE(true, false, false) break;
-    case 2: HELIOS_TRACE_CASE(false, true, false) break;
-    case 3: HELIOS_TRACE_CASE(true, true, false) break;
-    case 4: HELIOS_TRACE_CASE(false, true, true) break;
-    default: HELIOS_TRACE_CASE(true, true, true) break;
+  if (instrumented) {
+    if (grid == 1) k_trace<true, 1><<<g, T, 0, s>>>(a);
+    else if (grid == 2) k_trace<true, 2><<<g, T, 0, s>>>(a);
+    else k_trace<true, 0><<<g, T, 0, s>>>(a);
+  } else {
+    if (grid == 1) k_trace<false, 1><<<g, T, 0, s>>>(a);
+    else if (grid == 2) k_trace<false, 2><<<g, T, 0, s>>>(a);
+    else k_trace<false, 0><<<g, T, 0, s>>>(a);
   }
-#undef HELIOS_TRACE_CASE
   return cudaGetLastError();
 }
 

@@ -1,11 +1,12 @@
 // waveform.cu -- K7: full-waveform binning + local-maximum peaks -> returns.
 //
-// One warp per pulse (grid-stride).  The pulse's subray records (16 B each,
-// written by K6) are read once.  P:215: "the recorded power for each bin is
-// taken as the sum of the subray's waveforms, shifted according to the
-// different ranges of the subrays":
+// One warp per pulse (grid-stride).  The pulse's 8-B subray records
+// {k_s, A_s} (written by K6, which computes k_s from the fp64 range) are read
+// once; the prim ids only when a return is attributed.  P:215: "the recorded
+// power for each bin is taken as the sum of the subray's waveforms, shifted
+// according to the different ranges of the subrays":
 //
-//   k_s  = floor(2 R_s / c / Delta)                  (R8, R9; the oracle's fp64 operations)
+//   k_s  = floor(2 R_s / c / Delta)                  (R8, R9; in K6, the oracle's fp64 operations)
 //   k0   = min_s k_s                                  (window anchor, R9)
 //   W[k] = sum_s A_s p[k - (k_s - k0)],  p[j] = f((j + 1/2) Delta / tau),
 //          f(x) = x^2 e^-x  (Eq. 3),  j < L_p = ceil(20 tau / Delta)
@@ -17,7 +18,8 @@
 // into few distinct bin offsets o_s = k_s - k0 (coherent footprint), so the
 // amplitudes are first summed per offset group (each group in subray order),
 // then each lane computes its bins W[k] = sum_o A_o p[k - o] directly.  Pulses
-// whose offsets spread over >= kAggCap bins use the per-subray accumulation.
+// whose offsets spread over >= kAggCap bins use match_any groups (or, past
+// kGroupCap groups, the per-subray accumulation).
 // The waveform window lives in a small per-warp shared-memory buffer; a pulse
 // whose support exceeds it (rare: a footprint spanning > kWCap - L_p bins)
 // uses a per-warp global scratch row.  Rows are stored as fp32 with 16-byte
@@ -25,8 +27,6 @@
 #include <math.h>
 
 #include <algorithm>
-
-#include <cub/device/device_scan.cuh>
 
 #include "internal.cuh"
 #include "philox.cuh"
@@ -45,38 +45,6 @@ constexpr int kWCap = HELIOS_WAVE_WCAP;  // fp64 bins per warp in shared memory
 constexpr int kAggCap = 64;   // offset groups handled by the grouped path
 constexpr int kGroupCap = kAggCap * 2 / 3;  // sparse groups (8 + 4 B) in the same space
 constexpr size_t kSmemCap = 200 * 1024;
-
-// Absolute bin k_s = floor(2 R / c / (Delta 1e-9)) -- the oracle's two
-// correctly rounded divisions, bit for bit -- at the cost of one multiply:
-// q = 2R * inv_bin (inv_bin = 1 / (c Delta 1e-9)) is within a few ulp of the
-// same exact quotient, so its floor is the oracle's whenever q is farther than
-// 1e-13 q from an integer; only then (never, in practice) the divisions run.
-__device__ __forceinline__ long long bin_of(double range_m, double delta_ns, double inv_bin) {
-  const double q = 2.0 * range_m * inv_bin;
-  const double f = floor(q);
-  if (q - f > 1e-13 * q && (f + 1.0) - q > 1e-13 * q) return (long long)f;
-  return (long long)floor(2.0 * range_m / kC / (delta_ns * 1e-9));
-}
-
-__device__ __forceinline__ long long warp_min_ll(long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    long long w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w < v ? w : v;
-  }
-  return v;
-}
-__device__ __forceinline__ int warp_max_i(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_max_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
 
 // Echo width ("Optionally, a Gaussian may be fitted to the resulting
 // waveform, to get a measure of echo width (i.e. standard deviation of the
@@ -211,39 +179,28 @@ __global__ void __launch_bounds__(64) k_fit(const FitJob* __restrict__ jobs,
 }
 
 // Support length of each pulse's waveform (compact output): one warp per
-// pulse, the same k_s / k0 / offset rules as K7's pass 1 (R9).
-__global__ void k_support(const helios_subray_hit* __restrict__ rec, uint32_t N, uint64_t n,
-                          uint32_t nb, uint32_t taps, double delta_ns,
-                          uint64_t* __restrict__ len) {
+// pulse, the same k0 / offset rules as K7 (R9).
+__global__ void k_support(const WaveRec* __restrict__ rec, uint32_t N, uint64_t n, uint32_t nb,
+                          uint32_t taps, uint64_t* __restrict__ len) {
   const int lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const double inv_bin = 1.0 / (kC * (delta_ns * 1e-9));
   for (uint64_t p = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += warps) {
-    const helios_subray_hit* r = rec + p * N;
-    long long kmin = LLONG_MAX, kmax_all = -1;
+    const int2* r = reinterpret_cast<const int2*>(rec + p * N);
+    int kmin = INT_MAX;
     for (uint32_t s = lane; s < N; s += 32) {
-      const helios_subray_hit h = r[s];
-      if (h.prim_id != 0xFFFFFFFFu) {
-        const long long k = bin_of(h.range_m, delta_ns, inv_bin);
-        kmin = k < kmin ? k : kmin;
-      }
+      const int k = r[s].x;
+      if (k >= 0) kmin = min(kmin, k);
     }
-    const long long k0 = warp_min_ll(kmin);
+    const int k0 = __reduce_min_sync(0xffffffffu, kmin);
     uint64_t L = 0;
-    if (k0 != LLONG_MAX) {
+    if (k0 != INT_MAX) {
+      int kmax = 0;
       for (uint32_t s = lane; s < N; s += 32) {
-        const helios_subray_hit h = r[s];
-        if (h.prim_id != 0xFFFFFFFFu) {
-          const long long o = bin_of(h.range_m, delta_ns, inv_bin) - k0;
-          if (o < (long long)nb && o > kmax_all) kmax_all = o;
-        }
+        const int k = r[s].x;
+        if (k >= 0 && k - k0 < (int)nb) kmax = max(kmax, k - k0);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const long long v = __shfl_xor_sync(0xffffffffu, kmax_all, o);
-        kmax_all = v > kmax_all ? v : kmax_all;
-      }
-      L = (uint64_t)min((long long)nb, kmax_all + (long long)taps);
+      kmax = __reduce_max_sync(0xffffffffu, kmax);
+      L = (uint64_t)min(nb, (uint32_t)kmax + taps);
     }
     if (lane == 0) len[p] = L;
   }
@@ -263,13 +220,6 @@ __global__ void k_range_noise(helios_return* __restrict__ ret, const uint8_t* __
   }
 }
 
-__global__ void k_add_carry(uint64_t* __restrict__ offs, uint64_t m) {
-  const uint64_t c = offs[0];
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    offs[1 + i] += c;
-}
-
 struct Layout {
   size_t ker_d, per_warp_d, w_off, agg_off, off_off, amp_off;
 };
@@ -284,6 +234,21 @@ __host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
   return L;
 }
 
+// maximum of non-negative doubles over the warp: their bit patterns order
+// like the values, so two 32-bit warp reductions (high words, then the low
+// words of the lanes holding the highest high word) give it exactly
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned hmax = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned lmax = __reduce_max_sync(0xffffffffu, hi == hmax ? lo : 0u);
+  return __hiloint2double((int)hmax, (int)lmax);
+}
+
+// K7: one warp per pulse, persistent grid-stride loop.  Reads the pulse's
+// 8-B records (k_s, A_s) once, k0 = min k_s (one warp reduction), the
+// per-offset amplitude sums A_o (deterministic order), the support
+// W[k] = sum_o A_o p[k - o] (k < S = maxoff + L_p) in fp64 shared memory,
+// maximum, local maxima and returns, then the output row.
 __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_waveform(const WaveArgs a,
                                                              double* __restrict__ gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -296,49 +261,43 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
   double* agg = base + L.agg_off;
   int* off = reinterpret_cast<int*>(base + L.off_off);
   float* amp = reinterpret_cast<float*>(base + L.amp_off);
-  double* Wg = gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
+  const unsigned kFull = 0xffffffffu;
 
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
   __syncthreads();
-  const double inv_bin = 1.0 / (kC * (a.delta_ns * 1e-9));
 
   for (uint64_t p = (uint64_t)blockIdx.x * nw + warp; p < a.n_pulses;
        p += (uint64_t)gridDim.x * nw) {
-    const helios_subray_hit* rec = a.rec + p * N;
-    // pass 1: absolute bins k_s (fp64, the oracle's operation order) and k0
-    long long kmin = LLONG_MAX;
+    const int2* rec = reinterpret_cast<const int2*>(a.rec + p * N);
+    // pass 1: records -> shared memory (read once, streaming), k0 = min k_s
+    int kmin = INT_MAX;
     for (uint32_t s = lane; s < N; s += 32) {
-      const helios_subray_hit r = rec[s];
-      long long k = -1;
-      if (r.prim_id != 0xFFFFFFFFu) {
-        k = bin_of(r.range_m, a.delta_ns, inv_bin);
-        kmin = k < kmin ? k : kmin;
-      }
-      off[s] = (int)k;  // absolute bin for now (R < 3e8 m fits an int)
-      amp[s] = r.amplitude;
+      const int2 r = __ldcs(rec + s);
+      off[s] = r.x;
+      amp[s] = __int_as_float(r.y);
+      if (r.x >= 0) kmin = min(kmin, r.x);
     }
-    __syncwarp();
-    const long long k0 = warp_min_ll(kmin);
+    const int k0 = __reduce_min_sync(kFull, kmin);
     helios_return* slots = a.returns + p * a.max_returns;
     float* row = a.waveform ? a.waveform + p * (uint64_t)nb : nullptr;
     uint32_t S = 0;
     double* W = Ws;
-    uint8_t nret = 0;
-    if (k0 != LLONG_MAX) {
+    uint32_t nret = 0;
+    if (k0 != INT_MAX) {
       // offsets within the window; beyond maxFullwaveRange -> discarded
       int maxoff = 0;
       for (uint32_t s = lane; s < N; s += 32) {
         int o = off[s];
         if (o >= 0) {
-          o = (int)((long long)o - k0);
+          o -= k0;
           if (o >= (int)nb) o = -2;
           else maxoff = max(maxoff, o);
           off[s] = o;
         }
       }
-      maxoff = warp_max_i(maxoff);
+      maxoff = __reduce_max_sync(kFull, maxoff);
       S = min(nb, (uint32_t)maxoff + taps);
-      W = (S <= (uint32_t)kWCap) ? Ws : Wg;
+      W = (S <= (uint32_t)kWCap) ? Ws : gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
       __syncwarp();
       if (maxoff < kAggCap) {
         // amplitude per offset group.  Few groups (G <= 16, the usual case):
@@ -356,10 +315,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
             for (uint32_t s = s0; s < s1; ++s)
               if (off[s] == o) acc += (double)amp[s];
           }
-          // chunk partials of each group combined by a fixed binary tree over
-          // the chunks (lane c G + o takes lane (c + st) G + o): deterministic
           for (int st = 1; st < C; st <<= 1) {
-            const double other = __shfl_down_sync(0xffffffffu, acc, st * G);
+            const double other = __shfl_down_sync(kFull, acc, st * G);
             if (c < C && (c & (2 * st - 1)) == 0 && c + st < C) acc += other;
           }
           if (lane < G) agg[lane] = acc;
@@ -375,7 +332,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         for (uint32_t k = lane; k < S; k += 32) {
           const int olo = max(0, (int)k - (int)taps + 1), ohi = min(maxoff, (int)k);
           double w = 0.0;
-          for (int o = olo; o <= ohi; ++o) w += agg[o] * ker[k - o];
+          for (int o = olo; o <= ohi; ++o) w = fma(agg[o], ker[k - o], w);
           W[k] = w;
         }
       } else {
@@ -391,9 +348,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         for (uint32_t c0 = 0; c0 < N; c0 += 32) {
           const uint32_t s = c0 + lane;
           const int o = s < N ? off[s] : -1;
-          const unsigned peers = __match_any_sync(0xffffffffu, o);
+          const unsigned peers = __match_any_sync(kFull, o);
           const bool lead = o >= 0 && (int)(__ffs(peers) - 1) == lane;
-          const unsigned leads = __ballot_sync(0xffffffffu, lead);
+          const unsigned leads = __ballot_sync(kFull, lead);
           const int idx = G + __popc(leads & ((1u << lane) - 1u));
           if (lead && idx < kGroupCap) {
             double acc = 0.0;
@@ -411,7 +368,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
             const double A = gsum[g];
             for (uint32_t j = lane; j < taps; j += 32) {
               const uint32_t k = o + j;
-              if (k < S) W[k] += A * ker[j];
+              if (k < S) W[k] = fma(A, ker[j], W[k]);
             }
             __syncwarp();
           }
@@ -422,17 +379,17 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
             const double A = (double)amp[s];
             for (uint32_t j = lane; j < taps; j += 32) {
               const uint32_t k = (uint32_t)o + j;
-              if (k < S) W[k] += A * ker[j];
+              if (k < S) W[k] = fma(A, ker[j], W[k]);
             }
             __syncwarp();
           }
         }
       }
       __syncwarp();
-      // maximum
+      // maximum (all W >= 0)
       double M = 0.0;
       for (uint32_t k = lane; k < S; k += 32) M = fmax(M, W[k]);
-      M = warp_max_d(M);
+      M = warp_max_nonneg(M);
       const double thr = (double)a.thr * M;
       // local maxima in time order (ballot over 32 consecutive bins)
       for (uint32_t b0 = 0; b0 < S && nret < a.max_returns; b0 += 32) {
@@ -442,40 +399,33 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           const double w = W[k], wl = W[k - 1], wr = (k + 1 < S) ? W[k + 1] : 0.0;
           pk = w > wl && w > wr && w >= thr;
         }
-        unsigned m = __ballot_sync(0xffffffffu, pk);
+        unsigned m = __ballot_sync(kFull, pk);
         while (m && nret < a.max_returns) {
           const uint32_t kk = b0 + (__ffs(m) - 1);
           m &= m - 1;
-          // attribution (R13): largest contribution A_s p[kk - o_s], ties -> lowest s
-          double bc = -1.0;
+          // attribution (R13): largest contribution A_s p[kk - o_s], ties ->
+          // lowest s: exact max over the warp, then the lowest s holding it
+          double bc = 0.0;
           uint32_t bs = 0xFFFFFFFFu;
           for (uint32_t s = lane; s < N; s += 32) {
             const int o = off[s];
-            if (o < 0) continue;
             const int j = (int)kk - o;
-            if (j < 0 || j >= (int)taps) continue;
+            if (o < 0 || j < 0 || j >= (int)taps) continue;
             const double c = (double)amp[s] * ker[j];
-            if (c > bc) {
+            if (bs == 0xFFFFFFFFu || c > bc) {
               bc = c;
               bs = s;
             }
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double c2 = __shfl_xor_sync(0xffffffffu, bc, o);
-            const uint32_t s2 = __shfl_xor_sync(0xffffffffu, bs, o);
-            if (c2 > bc || (c2 == bc && s2 < bs)) {
-              bc = c2;
-              bs = s2;
-            }
-          }
+          const double cmax = warp_max_nonneg(bs == 0xFFFFFFFFu ? 0.0 : bc);
+          bs = __reduce_min_sync(kFull, (bs != 0xFFFFFFFFu && bc == cmax) ? bs : 0xFFFFFFFFu);
           if (a.fit) {
             // echo-width job (R28): the echo's window, fitted later by k_fit
             int lo, hi;
             echo_window(W, S, nb, (int)kk, a.fit_half, lo, hi);
             unsigned job = 0;
             if (lane == 0) job = atomicAdd(a.fit_count, 1u);
-            job = __shfl_sync(0xffffffffu, job, 0);
+            job = __shfl_sync(kFull, job, 0);
             double* y = a.fit_y + (size_t)job * a.fit_stride;
             for (int i = lane; i <= hi - lo; i += 32)
               y[i] = (uint32_t)(lo + i) < S ? W[lo + i] : 0.0;
@@ -490,11 +440,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           }
           if (lane == 0) {
             helios_return r;
-            r.range_m = 0.5 * kC * ((double)(k0 + (long long)kk - (long long)a.jstar) + 0.5) *
+            r.range_m = 0.5 * kC * ((double)((long long)k0 + (long long)kk - (long long)a.jstar) + 0.5) *
                         a.delta_ns * 1e-9;
             r.gps_time_s = a.time_s ? a.time_s[p] : 0.0;
             r.intensity = (float)W[kk];
-            r.prim_id = rec[bs].prim_id;
+            r.prim_id = a.prim[p * N + bs];
             r.return_number = (uint8_t)(nret + 1);
             r.n_returns = 0;  // patched below once the count is known
             r.pad[0] = r.pad[1] = 0;
@@ -509,7 +459,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
     // return slots: patch the count, zero the unused ones
     for (uint32_t r = lane; r < a.max_returns; r += 32) {
       if (r < nret) {
-        slots[r].n_returns = nret;
+        slots[r].n_returns = (uint8_t)nret;
       } else {
         double2* q = reinterpret_cast<double2*>(slots + r);
         q[0] = make_double2(0.0, 0.0);
@@ -517,16 +467,17 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
     }
     if (lane == 0) {
-      a.first_bin[p] = (k0 == LLONG_MAX) ? -1 : k0;
-      a.n_returns[p] = nret;
-      if (a.counters) atomicAdd(a.counters + 1, (unsigned long long)nret);
+      a.first_bin[p] = (k0 == INT_MAX) ? -1 : (int64_t)k0;
+      a.n_returns[p] = (uint8_t)nret;
     }
     if (a.counters) {
       unsigned h = 0;
-      for (uint32_t s = lane; s < N; s += 32) h += (rec[s].prim_id != 0xFFFFFFFFu);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-      if (lane == 0) atomicAdd(a.counters + 0, (unsigned long long)h);
+      for (uint32_t s = lane; s < N; s += 32) h += (off[s] != -1);
+      h = __reduce_add_sync(kFull, h);
+      if (lane == 0) {
+        atomicAdd(a.counters + 0, (unsigned long long)h);
+        atomicAdd(a.counters + 1, (unsigned long long)nret);
+      }
     }
     if (a.offs) {
       // compact row: W[0 .. len) at its packed offset (lossless; bins >= len are 0)
@@ -538,13 +489,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
     }
     if (row) {
-      // dense fp32 row: scalar head/tail, 16-byte stores for the aligned body
+      // dense fp32 row: scalar head/tail, 16-byte streaming stores for the
+      // aligned body (the support converted from W, then zeros)
       const uint32_t mis = (uint32_t)(((uintptr_t)row >> 2) & 3u);
       const uint32_t head = min(nb, (4u - mis) & 3u);
       if (lane < head) row[lane] = lane < S ? (float)W[lane] : 0.0f;
       const uint32_t nvec = (nb - head) >> 2;
       float4* body = reinterpret_cast<float4*>(row + head);
-      // vectors touching the support, then a plain zero-store loop
       const uint32_t qs = S > head ? min(nvec, (S - head + 3u) >> 2) : 0u;
       for (uint32_t q = lane; q < qs; q += 32) {
         const uint32_t k = head + 4 * q;
@@ -553,10 +504,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         v.y = k + 1 < S ? (float)W[k + 1] : 0.0f;
         v.z = k + 2 < S ? (float)W[k + 2] : 0.0f;
         v.w = k + 3 < S ? (float)W[k + 3] : 0.0f;
-        body[q] = v;
+        __stcs(body + q, v);
       }
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint32_t q = qs + lane; q < nvec; q += 32) body[q] = z4;
+      for (uint32_t q = qs + lane; q < nvec; q += 32) __stcs(body + q, z4);
       const uint32_t t0 = head + 4 * nvec;
       if (t0 + lane < nb) row[t0 + lane] = t0 + lane < S ? (float)W[t0 + lane] : 0.0f;
     }
@@ -604,12 +555,11 @@ bool waveform_fits(uint32_t n_bins, uint32_t N, uint32_t taps) {
   return smem_for(N, taps, 1) <= kSmemCap;
 }
 
-cudaError_t launch_support(const helios_subray_hit* rec, uint32_t N, uint64_t n_pulses,
-                           uint32_t n_bins, uint32_t taps, double delta_ns, uint64_t* len,
-                           cudaStream_t s) {
+cudaError_t launch_support(const WaveRec* rec, uint32_t N, uint64_t n_pulses, uint32_t n_bins,
+                           uint32_t taps, uint64_t* len, cudaStream_t s) {
   if (n_pulses == 0) return cudaSuccess;
   const uint64_t blocks = std::min<uint64_t>((n_pulses + 7) / 8, 148ull * 16);
-  k_support<<<(unsigned)blocks, 256, 0, s>>>(rec, N, n_pulses, n_bins, taps, delta_ns, len);
+  k_support<<<(unsigned)blocks, 256, 0, s>>>(rec, N, n_pulses, n_bins, taps, len);
   return cudaGetLastError();
 }
 
@@ -656,19 +606,11 @@ cudaError_t launch_pack_returns(const helios_return* slots, const uint8_t* nr, u
   const unsigned b1 = (unsigned)std::min<uint64_t>((m + 255) / 256, 148ull * 8);
   k_ret_len<<<b1, 256, 0, s>>>(nr, m, len);
   cudaError_t e = cudaGetLastError();
-  size_t tb = scan_bytes;
-  if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(scan_temp, tb, len, offs + 1, (int)m, s);
-  if (e == cudaSuccess) e = launch_add_carry(offs, m, s);
+  // offs[1 + i] = offs[0] + sum_{j <= i} len[j] (offs[0]: carry of the previous chunks)
+  if (e == cudaSuccess) e = scan_u64(len, offs + 1, m, true, scan_temp, scan_bytes, s, offs);
   if (e != cudaSuccess) return e;
   const unsigned b2 = (unsigned)std::min<uint64_t>((m * R + 255) / 256, 148ull * 16);
   k_pack_returns<<<b2, 256, 0, s>>>(slots, nr, m, R, offs, dst, staged, capacity);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_add_carry(uint64_t* offs, uint64_t m, cudaStream_t s) {
-  if (m == 0) return cudaSuccess;
-  const uint64_t blocks = std::min<uint64_t>((m + 255) / 256, 148ull * 8);
-  k_add_carry<<<(unsigned)blocks, 256, 0, s>>>(offs, m);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,9 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OUT_OF_MEMORY", 3: "CUDA", 4: "NO
 
 EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helios_build_accel",
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
-            "helios_pulse_taps", "helios_simulate", "helios_simulate_survey")
+            "helios_pulse_taps", "helios_simulate", "helios_simulate_batches",
+            "helios_simulate_survey", "helios_get_tuning", "helios_set_tuning",
+            "helios_util_sort_pairs_u64", "helios_util_scan_u64")
 
 
 class HeliosError(RuntimeError):
@@ -93,7 +95,15 @@ class helios_stats(ctypes.Structure):
                 [(n, _u64) for n in ("pulses", "subrays", "subray_hits", "voxel_returns",
                                      "returns", "nodes_visited", "tris_tested", "voxel_steps",
                                      "fp64_tests")] +
-                [("trace_ms", _d), ("waveform_ms", _d), ("beam_nodes", _u64)])
+                [("trace_ms", _d), ("waveform_ms", _d), ("beam_nodes", _u64), ("beam_ms", _d),
+                 ("batches", _u32), ("chunks", _u32)])
+
+
+class helios_tuning(ctypes.Structure):
+    _fields_ = [("beam_prepass", ctypes.c_int32), ("builder", ctypes.c_int32),
+                ("lane_order", ctypes.c_int32), ("pad_lanes", ctypes.c_int32),
+                ("serialize", ctypes.c_int32), ("trace_spans", ctypes.c_int32),
+                ("chunk_pulses", _u64)]
 
 
 class helios_scene_info(ctypes.Structure):
@@ -143,6 +153,19 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(helios_pulses),
                                       ctypes.POINTER(helios_outputs), _vp,
                                       ctypes.POINTER(helios_stats)]
+        L.helios_simulate_batches.restype = ctypes.c_int
+        L.helios_simulate_batches.argtypes = [_vp, ctypes.POINTER(helios_scanner_params),
+                                              ctypes.POINTER(helios_pulses),
+                                              ctypes.POINTER(helios_outputs), _u32, _vp,
+                                              ctypes.POINTER(helios_stats)]
+        L.helios_get_tuning.restype = ctypes.c_int
+        L.helios_get_tuning.argtypes = [ctypes.POINTER(helios_tuning)]
+        L.helios_set_tuning.restype = ctypes.c_int
+        L.helios_set_tuning.argtypes = [ctypes.POINTER(helios_tuning)]
+        L.helios_util_sort_pairs_u64.restype = ctypes.c_int
+        L.helios_util_sort_pairs_u64.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp]
+        L.helios_util_scan_u64.restype = ctypes.c_int
+        L.helios_util_scan_u64.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp]
         _lib = L
     return _lib
 
@@ -212,6 +235,65 @@ def helios_simulate(scene: int, params: helios_scanner_params, pulses: helios_pu
     _check(lib().helios_simulate(scene, ctypes.byref(params), ctypes.byref(pulses),
                                  ctypes.byref(outputs), _stream(stream),
                                  None if stats is None else ctypes.byref(stats)))
+
+
+def helios_simulate_batches(scene: int, params: helios_scanner_params, pulses, outputs,
+                            stream=None, stats: helios_stats | None = None):
+    """pulses / outputs: sequences of helios_pulses / helios_outputs (one per batch)."""
+    n = len(pulses)
+    assert len(outputs) == n
+    P = (helios_pulses * n)(*pulses)
+    O = (helios_outputs * n)(*outputs)
+    _check(lib().helios_simulate_batches(scene, ctypes.byref(params), P, O, n, _stream(stream),
+                                         None if stats is None else ctypes.byref(stats)))
+
+
+def helios_get_tuning() -> helios_tuning:
+    t = helios_tuning()
+    _check(lib().helios_get_tuning(ctypes.byref(t)))
+    return t
+
+
+def helios_set_tuning(t: helios_tuning) -> None:
+    _check(lib().helios_set_tuning(ctypes.byref(t)))
+
+
+class tuning:
+    """Context manager: tuning switches for the calls inside, e.g.
+    ``with tuning(beam_prepass=0): ...`` (restored on exit)."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = None
+
+    def __enter__(self):
+        self.old = helios_get_tuning()
+        t = helios_get_tuning()
+        for k, v in self.kw.items():
+            setattr(t, k, v)
+        helios_set_tuning(t)
+        return t
+
+    def __exit__(self, *exc):
+        helios_set_tuning(self.old)
+        return False
+
+
+def util_sort_pairs_u64(keys, vals, key_bits: int = 64, stream=None) -> None:
+    """In-place stable radix sort of CUDA tensors keys (int64/uint64) and vals (int32/uint32)."""
+    rc = lib().helios_util_sort_pairs_u64(_ptr(keys), _ptr(vals), int(keys.numel()), key_bits,
+                                          _stream(stream))
+    if rc:
+        raise HeliosError(HELIOS_ERR_CUDA if rc == 3 else HELIOS_ERR_INVALID_ARGUMENT,
+                          f"helios_util_sort_pairs_u64 returned {rc}")
+
+
+def util_scan_u64(src, dst, inclusive: bool = True, stream=None) -> None:
+    rc = lib().helios_util_scan_u64(_ptr(src), _ptr(dst), int(src.numel()), int(inclusive),
+                                    _stream(stream))
+    if rc:
+        raise HeliosError(HELIOS_ERR_CUDA if rc == 3 else HELIOS_ERR_INVALID_ARGUMENT,
+                          f"helios_util_scan_u64 returned {rc}")
 
 
 def helios_simulate_survey(scene: int, params: helios_scanner_params, survey: helios_survey,
@@ -422,6 +504,29 @@ def simulate(scene: Scene, params, origin, direction, time_s=None, pulse_index_b
     _run_with_capacity_retry(lambda: helios_simulate(scene.handle, hp, p, o, stream, st),
                              outputs, o)
     return outputs, st
+
+
+def simulate_batches(scene: Scene, params, batches, outputs, stream=None, stats: bool = False,
+                     counters: bool = False):
+    """helios_simulate_batches: `batches` = [(origin, direction, time_s, pulse_index_base)],
+    `outputs` = [Outputs] (one per batch, non-overlapping).  One call, one
+    chunk pipeline over all batches.  Returns helios_stats | None."""
+    hp = params if isinstance(params, helios_scanner_params) else make_params(params)
+    ps, keep = [], []
+    for (o, d, t, base) in batches:
+        p = helios_pulses()
+        p.p_origin, p.p_direction, p.p_time_s = _ptr(o), _ptr(d), _ptr(t)
+        p.n_pulses = int(o.shape[0])
+        p.pulse_index_base = int(base)
+        ps.append(p)
+        keep.append((o, d, t))
+    os_ = [_marshal_outputs(x) for x in outputs]
+    st = helios_stats() if (stats or counters) else None
+    if st is not None:
+        st.collect_counters = 1 if counters else 0
+    helios_simulate_batches(scene.handle, hp, ps, os_, stream, st)
+    del keep
+    return st
 
 
 def make_survey(sv) -> tuple:

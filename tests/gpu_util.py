@@ -2,9 +2,7 @@
 same seeded pulses."""
 from __future__ import annotations
 
-import contextlib
 import functools
-import os
 
 import numpy as np
 
@@ -68,15 +66,8 @@ def take(gpu: dict, idx) -> dict:
     return out
 
 
-@contextlib.contextmanager
 def beam_env(value: str):
-    """HELIOS_BEAM=0/1 for the calls inside (read by helios_simulate per call)."""
-    old = os.environ.get("HELIOS_BEAM")
-    os.environ["HELIOS_BEAM"] = value
-    try:
-        yield
-    finally:
-        if old is None:
-            os.environ.pop("HELIOS_BEAM", None)
-        else:
-            os.environ["HELIOS_BEAM"] = old
+    """Beam pre-pass K6a off ("0") or on where it applies ("1") for the calls
+    inside (helios_set_tuning)."""
+    import paper_2101_09154_b200 as h
+    return h.tuning(beam_prepass=int(value))

@@ -1,17 +1,26 @@
-"""Parity comparator: CUDA path vs fp64 oracle (DESIGN.md s.4, rules C-4).
+"""Parity comparator: CUDA path vs fp64 oracle (DESIGN.md s.4).
 
 Tolerances (BASELINE.json north_star + the arithmetic):
-  * hit primitive ids and return counts bit-exact, except where two candidate
-    hits lie within 1e-6 m (oracle candidate set > 1);
+  * subray prim ids bit-exact; where the oracle's candidate set (every
+    triangle within 1e-6 m of the nearest, exported as ids) has more than one
+    member, a DIFFERENT id is accepted only if it lies in that set -- and that
+    subray is then "tie-taken": its amplitude is not compared and its pulse is
+    exempt from the waveform / return checks (the neighbour may have another
+    normal or reflectance);
   * ranges |dr| <= 1e-6 r + 1e-5 m;
-  * intensities / amplitudes / waveform bins within 1e-4 relative (zero must
+  * amplitudes / intensities / waveform bins within 1e-4 relative (zero must
     be exactly zero);
-  * voxel transmission decisions exact (shared Philox counter), except where
-    |u - exp(-sigma L)| <= 1e-12;
-  * k_s exact except where the oracle's k-margin <= 1e-9;
-  * peak decisions (count, attribution) exact except where a decision's
-    relative margin <= 1e-5 (both sides decide in fp64; the GPU's amplitudes
-    enter as fp32, relative error <= 6e-8 per term).
+  * voxel transmission decisions exact, except where |u - exp(-sigma L)| <=
+    1e-12 (exempt subray);
+  * k_s exact except where the oracle's k-margin <= 1e-9 (exempt subray);
+  * per pulse: k0 exact; n_returns exact unless a peak decision's margin is
+    <= DECISION_EPS = 2.5e-7 (the GPU bins fp32-rounded amplitudes: every bin
+    within 6e-8 relative, so a comparison flips only within 1.2e-7); return
+    ranges within 1e-12 relative, intensities within 1e-4; return prim ids in
+    the oracle's attribution set (the distinct prims whose contribution is
+    within DECISION_EPS of the largest; usually one);
+  * exemption budget: exempt pulses <= 1e-4 of the pulses compared
+    (Report.budget_ok), by reason in Report.exempt_pulses.
 """
 from __future__ import annotations
 
@@ -21,6 +30,8 @@ import numpy as np
 
 C = 299792458.0
 MISS = 0xFFFFFFFF
+DECISION_EPS = 2.5e-7
+EXEMPT_BUDGET = 1e-4
 
 
 @dataclass
@@ -29,6 +40,7 @@ class Report:
     subrays: int = 0
     exempt_subrays: dict = field(default_factory=dict)
     exempt_pulses: dict = field(default_factory=dict)
+    checked: dict = field(default_factory=dict)
     mismatches: list = field(default_factory=list)
     max_rel: dict = field(default_factory=dict)
 
@@ -47,10 +59,44 @@ class Report:
     def ok(self):
         return not self.mismatches
 
+    def n_exempt_pulses(self):
+        return sum(self.exempt_pulses.values())
+
+    def budget_ok(self, frac: float = EXEMPT_BUDGET):
+        """Exempt pulses within the C-4 budget (<= frac of those compared)."""
+        return self.n_exempt_pulses() <= frac * self.pulses
+
     def summary(self):
         return (f"pulses={self.pulses} subrays={self.subrays} exempt_subrays={self.exempt_subrays}"
-                f" exempt_pulses={self.exempt_pulses} max_rel={self.max_rel}"
-                f" mismatches={len(self.mismatches)}: {self.mismatches[:10]}")
+                f" exempt_pulses={self.exempt_pulses} checked={self.checked}"
+                f" max_rel={self.max_rel} mismatches={len(self.mismatches)}: {self.mismatches[:10]}")
+
+    def table_row(self, name: str) -> str:
+        ex = ", ".join(f"{k} {v}" for k, v in sorted(self.exempt_pulses.items()) if v) or "none"
+        exs = ", ".join(f"{k} {v}" for k, v in sorted(self.exempt_subrays.items()) if v) or "none"
+        mr = ", ".join(f"{k} {v:.2e}" for k, v in sorted(self.max_rel.items()))
+        return (f"| {name} | {self.pulses} | {self.subrays} | {exs} | {ex} | "
+                f"{self.n_exempt_pulses() / max(1, self.pulses):.1e} | {len(self.mismatches)} | {mr} |")
+
+
+def record(name: str, rep: Report) -> None:
+    """Append the report's row to the exemption table named by
+    $HELIOS_PARITY_TABLE (profiles/<round>_parity_exemptions.md), if set."""
+    import os
+    path = os.environ.get("HELIOS_PARITY_TABLE")
+    if not path:
+        return
+    new = not os.path.exists(path)
+    with open(path, "a") as f:
+        if new:
+            f.write("| case | pulses | subrays | exempt subrays | exempt pulses | exempt frac | "
+                    "mismatches | max rel |\n|---|---|---|---|---|---|---|---|\n")
+        f.write(rep.table_row(name) + "\n")
+
+
+def _in_set(ids: np.ndarray, sets: np.ndarray) -> np.ndarray:
+    """ids [...]: is ids[...] one of sets[..., :] (UINT32_MAX-padded)?"""
+    return np.any(sets == ids[..., None], axis=-1) & (ids != MISS)
 
 
 def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | None = None,
@@ -69,22 +115,30 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
     o_rng = orc.sub_range
     o_amp = orc.sub_amp
 
-    tie = (orc.sub_ncand > 1)
+    same = g_prim == o_prim
     umarg = orc.sub_umargin <= 1e-12
     kmarg = orc.sub_kmargin <= 1e-9
-    r.bump(r.exempt_subrays, "tie", tie.sum())
+    multi = orc.sub_ncand > 1
+    in_cand = _in_set(sh["prim_id"].astype(np.uint32), orc.sub_cand)
+    # a listed candidate other than the oracle's choice: legitimate, exempt
+    tie_taken = ~same & multi & in_cand & ~umarg
+    # more candidates than the oracle lists and the GPU's id not among them:
+    # cannot be verified by id; counted (expected 0) and checked by range
+    overflow = ~same & (orc.sub_ncand > orc.sub_cand.shape[-1]) & ~in_cand & ~umarg
+    r.bump(r.exempt_subrays, "tie_taken", tie_taken.sum())
+    r.bump(r.exempt_subrays, "tie_overflow", overflow.sum())
     r.bump(r.exempt_subrays, "u_margin", umarg.sum())
     r.bump(r.exempt_subrays, "k_margin", kmarg.sum())
-    sub_ex = tie | umarg
+    r.bump(r.checked, "tie_subrays_same_id", (same & multi).sum())
+    sub_ex = tie_taken | overflow | umarg
     # --- per subray: prim ids
-    both_hit = (g_prim != MISS) & (o_prim != MISS)
-    bad = (g_prim != o_prim) & ~sub_ex
-    # a tie-exempt subray must still hit a triangle at (almost) the same range
-    bad |= tie & ((g_prim == MISS) | (np.abs(g_rng - o_rng) > 1e-6 * np.abs(o_rng) + 1e-5))
+    bad = ~same & ~sub_ex
     for i, s in zip(*np.nonzero(bad)):
         r.fail("subray prim", (i, s), f"gpu={g_prim[i, s]} oracle={o_prim[i, s]} "
-                                      f"r_gpu={g_rng[i, s]} r_or={o_rng[i, s]}")
-    # --- ranges
+                                      f"r_gpu={g_rng[i, s]} r_or={o_rng[i, s]} "
+                                      f"cand={orc.sub_cand[i, s][:orc.sub_ncand[i, s]]}")
+    # --- ranges (every hit, incl. tie-taken ones: the candidates lie within 1e-6 m)
+    both_hit = (g_prim != MISS) & (o_prim != MISS)
     sel = both_hit & ~umarg
     dr = np.abs(g_rng[sel] - o_rng[sel])
     lim = 1e-6 * np.abs(o_rng[sel]) + 1e-5
@@ -93,7 +147,7 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
         for k in np.nonzero(dr > lim)[0][:10]:
             r.fail("subray range", k, f"{g_rng[sel][k]} vs {o_rng[sel][k]}")
     # --- amplitudes
-    sel = both_hit & ~sub_ex
+    sel = both_hit & same & ~umarg
     if sel.any():
         a, b = g_amp[sel], o_amp[sel]
         rel = np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
@@ -102,7 +156,7 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
         for k in np.nonzero(rel > 1e-4)[0][:10]:
             r.fail("subray amplitude", k, f"{a[k]} vs {b[k]}")
     # --- k_s
-    sel = both_hit & ~sub_ex & ~kmarg
+    sel = both_hit & same & ~umarg & ~kmarg
     g_k = np.floor(2.0 * g_rng[sel] / C / (bin_width_ns * 1e-9)).astype(np.int64)
     if sel.any():
         badk = g_k != orc.sub_k[sel]
@@ -111,11 +165,9 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
 
     # --- per pulse
     p_sub_ex = (sub_ex | kmarg).any(axis=1)
-    p_peak_ex = orc.peak_margin <= 1e-5
-    p_attr_ex = orc.attr_margin <= 1e-5
+    p_peak_ex = (orc.peak_margin <= DECISION_EPS) & ~p_sub_ex
     r.bump(r.exempt_pulses, "subray", p_sub_ex.sum())
-    r.bump(r.exempt_pulses, "peak_margin", (p_peak_ex & ~p_sub_ex).sum())
-    r.bump(r.exempt_pulses, "attribution", (p_attr_ex & ~p_sub_ex & ~p_peak_ex).sum())
+    r.bump(r.exempt_pulses, "peak_margin", p_peak_ex.sum())
     g_k0 = gpu["wf_first_bin"]
     g_nr = gpu["n_returns"].astype(np.int64)
     ret = gpu["returns"]
@@ -161,8 +213,15 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
             r.fail("return intensity", i)
         if not np.array_equal(gr["gps_time_s"], orc.ret_time[i, :m]):
             r.fail("return gps time", i)
-        if not p_attr_ex[i] and not np.array_equal(gr["prim_id"], orc.ret_prim[i, :m]):
-            r.fail("return prim", i, f"{gr['prim_id']} vs {orc.ret_prim[i, :m]}")
+        # attribution (R13): the GPU's prim must be in the oracle's set
+        gp = gr["prim_id"].astype(np.uint32)
+        okp = _in_set(gp, orc.ret_cand[i, :m])
+        r.bump(r.checked, "returns", m)
+        r.bump(r.checked, "returns_attr_tied", int((orc.ret_cand[i, :m, 1] != MISS).sum()))
+        r.bump(r.checked, "returns_attr_other_tied_prim",
+               int((okp & (gp != orc.ret_prim[i, :m])).sum()))
+        if not okp.all():
+            r.fail("return prim", i, f"{gp} vs {orc.ret_prim[i, :m]} sets {orc.ret_cand[i, :m]}")
         # echo width (R28): NaN <=> NaN (not requested / not
         # converged), else the same least-squares optimum within 1e-6 relative
         # (both fit in fp64 to a 1e-10 relative step; the GPU's fp32 record adds 6e-8)
@@ -174,7 +233,7 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
             fin = np.where(np.isnan(ow_), gw_, ow_)
             edge = (fit_span_ns is not None) & (np.abs(np.abs(fin) - (fit_span_ns or 0))
                                                  <= 1e-3 * (fit_span_ns or 1))
-            r.bump(r.exempt_pulses, "width_bound", int(edge.any()))
+            r.bump(r.checked, "width_bound", int(edge.any()))
             if np.any((np.isnan(gw_) != np.isnan(ow_)) & ~edge):
                 r.fail("echo width NaN pattern", i, f"{gw_} vs {ow_}")
             else:
@@ -188,7 +247,15 @@ def compare(gpu: dict, orc, n_tris: int, bin_width_ns: float, report: Report | N
     return r
 
 
-def gpu_invariants(gpu: dict, max_returns: int, thr: float) -> list:
+def jstar_of(params) -> int:
+    """j* = argmax_j p[j] of the binned outgoing pulse (R12), for the invariants."""
+    tau = params.pulse_length_ns / 1.75
+    taps = int(np.ceil(20.0 * tau / params.bin_width_ns))
+    x = (np.arange(taps) + 0.5) * params.bin_width_ns / tau
+    return int(np.argmax(x * x * np.exp(-x)))
+
+
+def gpu_invariants(gpu: dict, max_returns: int, thr: float, params=None) -> list:
     """Properties that hold for every pulse at any size (checked on whole runs)."""
     errs = []
     k0 = gpu["wf_first_bin"]
@@ -217,8 +284,25 @@ def gpu_invariants(gpu: dict, max_returns: int, thr: float) -> list:
     raw = ret.view(np.uint8).reshape(ret.shape[0], R, 32) if ret.dtype.itemsize == 32 else None
     if raw is not None and np.any(raw[~used].any(axis=-1)):
         errs.append("unused return slot not zeroed")
-    if wf is not None:
-        # each return's bin is a strict local max >= thr * max of the stored row
-        # (checked on rows where the fp32 row preserves the decision)
-        pass
+    if wf is not None and params is not None:
+        # each return's bin (from its range, R12) is a local maximum >= thr * max
+        # of the stored fp32 row (>=: fp32 rounding may equalise neighbours)
+        js = jstar_of(params)
+        half = 0.5 * C * params.bin_width_ns * 1e-9
+        p_idx, r_idx = np.nonzero(used)
+        kb = np.rint(rng[p_idx, r_idx] / half - 0.5 - k0[p_idx] + js).astype(np.int64)
+        nb = wf.shape[1]
+        if np.any((kb < 1) | (kb > nb - 2)):
+            errs.append("return bin outside [1, n_bins - 2]")
+        else:
+            w = wf[p_idx, kb].astype(np.float64)
+            wl = wf[p_idx, kb - 1].astype(np.float64)
+            wr = wf[p_idx, kb + 1].astype(np.float64)
+            M = wf.max(axis=1).astype(np.float64)[p_idx]
+            if np.any((w < wl) | (w < wr)):
+                errs.append("a return bin is not a local maximum of the stored row")
+            if np.any(w < np.float32(thr) * M * (1 - 1e-6)):
+                errs.append("a return bin is below the threshold of the stored row")
+            if not np.array_equal(ret["intensity"][p_idx, r_idx], wf[p_idx, kb]):
+                errs.append("return intensity != stored row at its bin")
     return errs

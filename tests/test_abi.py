@@ -17,9 +17,15 @@ def libpath():
 
 
 def _declared():
-    src = open(os.path.join(ROOT, "include", "helios.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(helios_[a-z_]+)\s*\(", src)))
+    """Every function include/*.h declares (helios.h: the hot path's ABI;
+    helios_util.h: the build's sort / scan primitives)."""
+    names = set()
+    for hdr in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if hdr.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", hdr)).read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            names |= set(re.findall(r"\b(helios_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_header_declares_the_north_star_calls():
@@ -88,7 +94,7 @@ def test_struct_layouts_match_the_header(tmp_path):
                "helios_scanner_params": hh.helios_scanner_params,
                "helios_pulses": hh.helios_pulses, "helios_outputs": hh.helios_outputs,
                "helios_stats": hh.helios_stats, "helios_scene_info": hh.helios_scene_info,
-               "helios_survey": hh.helios_survey}
+               "helios_survey": hh.helios_survey, "helios_tuning": hh.helios_tuning}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "helios.h"', "int main(){"]
     for name, cls in structs.items():
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')

@@ -30,14 +30,14 @@ def _soup(n, seed, extent=10.0, size=1.0):
 
 @pytest.mark.parametrize("builder", ["lbvh", "ploc"])
 @pytest.mark.parametrize("n_tris", [1, 2, 3, 4, 5, 17, 1000, 10000])
-def test_bvh_equals_brute_force_random_soup(n_tris, builder, monkeypatch):
+def test_bvh_equals_brute_force_random_soup(n_tris, builder):
     # S:87/S:725 shape: random rays vs random triangles; ids exact, t within 1e-9
-    # (both hierarchies: Karras LBVH and PLOC, HELIOS_BUILDER)
-    monkeypatch.setenv("HELIOS_BUILDER", builder)
+    # (both hierarchies: Karras LBVH and PLOC, helios_tuning.builder)
     h = _h()
     tris = _soup(n_tris, n_tris, size=2.0 if n_tris < 100 else 0.7)
     refl = np.random.default_rng(1).uniform(0.1, 0.9, n_tris).astype(np.float32)
-    sc = h.Scene(_dev(tris), _dev(refl))
+    with h.tuning(builder=1 if builder == "lbvh" else 0):
+        sc = h.Scene(_dev(tris), _dev(refl))
     rng = np.random.default_rng(7)
     m = 1000
     o = rng.uniform(-14, 14, (m, 3)).astype(np.float32)
@@ -86,19 +86,18 @@ def test_batch_split_and_repeat_are_bitwise_identical():
         assert np.array_equal(a[k].view(np.uint8), cat.view(np.uint8)), k
 
 
-def test_beam_scene_chunking_and_batch_split_are_bitwise_identical(monkeypatch):
+def test_beam_scene_chunking_and_batch_split_are_bitwise_identical():
     """Beam pre-pass scene (C5 reduced): the chunk schedule (library rule, or
     forced 1024- and 3000-pulse chunks) and a split into two calls must not
     change a bit of the output (Philox counters, lane order, entry lists and
     deferred hits are all per pulse / per subray)."""
     w = workload("C5", 0.03)
-    monkeypatch.setenv("HELIOS_BEAM", "1")
+    h = _h()
     a = gpu_run(w, 300, 7000)
     runs = []
-    for chunk in ("1024", "3000"):
-        monkeypatch.setenv("HELIOS_CHUNK_PULSES", chunk)
-        runs.append(gpu_run(w, 300, 7000))
-    monkeypatch.delenv("HELIOS_CHUNK_PULSES")
+    for chunk in (1024, 3000):
+        with h.tuning(chunk_pulses=chunk):
+            runs.append(gpu_run(w, 300, 7000))
     c1 = gpu_run(w, 300, 2500)
     c2 = gpu_run(w, 2800, 4500)
     for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
@@ -234,7 +233,10 @@ def test_degenerate_rays_on_edges_and_planes():
     o = oracle_run(w2, np.arange(n))
     rep = compare(g, o, w.scene.n_tris, w.params.bin_width_ns)
     assert rep.ok(), rep.summary()
-    assert rep.exempt_subrays.get("tie", 0) > 0  # the case is really exercised
+    # the case is really exercised: subrays with several candidates within 1e-6 m
+    # (the GPU's exact-replica fp64 test takes the oracle's own choice)
+    assert rep.checked.get("tie_subrays_same_id", 0) + rep.exempt_subrays.get("tie_taken", 0) > 0
+    assert rep.budget_ok(), rep.summary()
 
 
 def test_stats_counters():
@@ -252,13 +254,13 @@ def test_stats_counters():
 def test_invariants_on_a_full_reduced_run():
     w = workload("C5", 0.03)
     g = gpu_run(w, 0, w.n_pulses, subray_hits=False)
-    errs = gpu_invariants(g, w.params.max_returns, w.params.detection_threshold)
+    errs = gpu_invariants(g, w.params.max_returns, w.params.detection_threshold, w.params)
     assert not errs, errs
     assert (g["wf_first_bin"] >= 0).mean() > 0.9
 
 
 @pytest.mark.parametrize("N,beta", [(19, 1e-3), (91, 5e-4), (37, 1e-7), (37, 0.05), (7, 0.099)])
-def test_beam_prepass_axis_aligned_and_grazing(N, beta, monkeypatch):
+def test_beam_prepass_axis_aligned_and_grazing(N, beta):
     """K6a's interval cone test on its hard cases: pulse axes exactly along
     +-x, +-y, +-z (direction intervals straddling 0 on two axes), axis-plane
     triangles (flat, zero-thickness boxes), origins inside the scene, and a
@@ -290,9 +292,9 @@ def test_beam_prepass_axis_aligned_and_grazing(N, beta, monkeypatch):
     sc = h.Scene.from_workload_scene(scene)
     outs = {}
     for beam in ("0", "1"):
-        monkeypatch.setenv("HELIOS_BEAM", beam)
-        o, st = h.simulate(sc, p, _dev(org), _dev(dirs), _dev(tim), subray_hits=True,
-                           stats=True, counters=True)
+        with h.tuning(beam_prepass=int(beam)):
+            o, st = h.simulate(sc, p, _dev(org), _dev(dirs), _dev(tim), subray_hits=True,
+                               stats=True, counters=True)
         torch_cuda().cuda.synchronize()
         outs[beam] = (o.numpy(), st)
     sc.destroy()
@@ -312,19 +314,18 @@ def test_beam_prepass_axis_aligned_and_grazing(N, beta, monkeypatch):
 
 
 @pytest.mark.parametrize("name,scale,start,count", [("C5", 0.03, 100, 3000), ("C3", 0.03, 500, 6000)])
-def test_lane_order_and_padding_are_bitwise_invariant(name, scale, start, count, monkeypatch):
+def test_lane_order_and_padding_are_bitwise_invariant(name, scale, start, count):
     """K6's lane order (R4 ring order vs the Hilbert patch order) and the lane
     padding to whole warps only change which lane computes which subray: every
     output must be bitwise identical (with the beam pre-pass on and off)."""
     w = workload(name, scale)
+    h = _h()
     ref = None
     for beam in ("0", "1"):
         for order in ("0", "1"):
             for pad in ("0", "1"):
-                monkeypatch.setenv("HELIOS_BEAM", beam)
-                monkeypatch.setenv("HELIOS_SUBRAY_ORDER", order)
-                monkeypatch.setenv("HELIOS_PAD_LANES", pad)
-                g = gpu_run(w, start, count)
+                with h.tuning(beam_prepass=int(beam), lane_order=int(order), pad_lanes=int(pad)):
+                    g = gpu_run(w, start, count)
                 if ref is None:
                     ref = g
                     continue

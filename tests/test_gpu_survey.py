@@ -77,7 +77,7 @@ def test_hot_path_on_generated_pulses_matches_the_oracle(cfg, scale, surv):
     out, _ = h.simulate_survey(scene_for(w), w.params, sv, first, n, base, beams=True,
                                subray_hits=True)
     g = out.numpy()
-    errs = gpu_invariants(g, w.params.max_returns, w.params.detection_threshold)
+    errs = gpu_invariants(g, w.params.max_returns, w.params.detection_threshold, w.params)
     assert not errs, errs
     ids = np.arange(base, base + n, dtype=np.uint64)
     r = oracle.simulate(w.scene, w.params, g["beam_origin"], g["beam_direction"], g["beam_time"],

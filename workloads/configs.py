@@ -95,6 +95,9 @@ class Workload:
     # the same pulses as surveys (NEXT f2): [(Survey, first global id, count)],
     # survey pulse g <-> global id first + g; None if not survey-expressible
     surveys: list | None = None
+    # generator facts for test stratification (C5: building circles, tree
+    # positions, heightfield, pulses per flight line); inputs only
+    meta: dict | None = None
 
     def pulses(self, start: int = 0, count: int | None = None):
         """(origins f32 [n,3], directions f32 [n,3], times f64 [n]) for the
@@ -457,7 +460,8 @@ def _c5(scale: float, seed: int):
                    deflector="polygon", scan_freq_hz=200.0, scan_angle_rad=math.radians(fov),
                    speed_m_s=60.0, t0_s=k * line_dur), k * per_line, per_line)
            for k, x in enumerate(xs)]
-    return scene, params, n_pulses, fn, svs
+    meta = {"buildings": circ, "trees": xy, "heights": h, "per_line": per_line, "fov_deg": fov}
+    return scene, params, n_pulses, fn, svs, meta
 
 
 def _prism(cx, cy, z0, h, r, sides, yaw, cap=True):
@@ -558,8 +562,10 @@ def make_workload(name: str, scale: float = 1.0, seed: int = 0, **overrides) -> 
     pulse grid for parity tests (the oracle is brute force); ``overrides``
     replace ScannerParams fields (e.g. subray_count=93 for the C5 variant)."""
     name = name.upper()
-    scene, params, n_pulses, fn, surveys = CONFIGS[name](scale, seed)
+    built = CONFIGS[name](scale, seed)
+    scene, params, n_pulses, fn, surveys = built[:5]
+    meta = built[5] if len(built) > 5 else None
     if overrides:
         params = replace(params, **overrides)
     return Workload(name if scale == 1.0 else f"{name}@{scale:g}", scene, params, n_pulses, fn,
-                    surveys)
+                    surveys, meta)
