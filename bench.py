@@ -189,6 +189,14 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+DENSE_OUT_BUDGET = 96e9   # device bytes of dense output sets one multi-batch call may use
+PACKED_FLOATS_PER_PULSE = 192  # packed waveform capacity per pulse (grown on demand)
+
+
+def _groups(idx, m):
+    return [idx[i:i + m] for i in range(0, len(idx), m)]
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_setup("nccl")
@@ -216,184 +224,174 @@ def run_ours(args):
     scene = h.Scene.from_workload_scene(w.scene, device=dev)
     info = scene.info()
     stream = torch.cuda.current_stream()
+    fp64_tflops = h.util_fp64_fma_tflops()
 
-    # inputs for every step, resident in HBM before timing
+    # inputs for every step (distinct batches), resident in HBM before timing
     steps_total = args.warmup + args.steps
     batches = []
     for i in range(steps_total):
         start, cnt = shard(w.n_pulses, B, i, rank, world)
         o, d, t = w.pulses(start, cnt)
         to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-        batches.append((start, to(o), to(d), to(t)))
-    # device outputs of the timed steps: dense waveform rows (default), the
-    # lossless packed support rows, or neither (binning still runs)
-    out = h.alloc_outputs(B, hp, device=dev, waveform=args.waveform == "dense",
-                          compact=args.waveform == "compact",
-                          compact_capacity=B * n_bins if args.waveform == "compact" else None)
+        batches.append((to(o), to(d), to(t), start))
+    dense = args.waveform == "dense"
+    out_bytes = B * (4 * n_bins * dense + 32 * p.max_returns + 9)
+    M = max(1, min(args.steps, int(DENSE_OUT_BUDGET // max(1, out_bytes))))
+    outs = [h.alloc_outputs(B, hp, device=dev, waveform=dense,
+                            compact=args.waveform == "compact",
+                            compact_capacity=B * n_bins if args.waveform == "compact" else None)
+            for _ in range(M)]
     torch.cuda.synchronize()
 
-    def step(i, st=False, counters=False):
-        start, o, d, t = batches[i]
-        return h.simulate(scene, hp, o, d, t, pulse_index_base=start, outputs=out,
-                          stats=st, counters=counters)[1]
+    def run_steps(idx, st=False, counters=False):
+        """The steps idx through helios_simulate_batches, <= M batches per call
+        (each with its own output set); stats summed."""
+        tot = {}
+        for g in _groups(list(idx), M):
+            r = h.simulate_batches(scene, hp, [batches[i] for i in g], outs[:len(g)],
+                                   stats=st, counters=counters)
+            if r is not None:
+                for f, _ in r._fields_:
+                    tot[f] = tot.get(f, 0) + getattr(r, f)
+        return tot
 
-    for i in range(args.warmup):
-        step(i)
+    def timed(fn):
+        barrier(world)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1), world, dev), r
+
+    run_steps(range(args.warmup))
     torch.cuda.synchronize()
+    timed_idx = range(args.warmup, steps_total)
 
+    # ---- the timed steps: K batches of B pulses through helios_simulate_batches
+    # (one chunk pipeline per call, so a batch's head overlaps the previous tail)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    barrier(world)
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    trace_ms = wave_ms = 0.0
-    launches = trace_launches = 0
-    ev0.record(stream)
-    for i in range(args.warmup, steps_total):
-        st = step(i, st=True)
-        trace_ms += st.trace_ms
-        wave_ms += st.waveform_ms
-        launches += st.kernel_launches
-        trace_launches += st.trace_launches
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier(world)
+    ms_max, st_main = timed(lambda: run_steps(timed_idx, st=True))
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    ms_max = max_over_ranks(ms, world, dev)
-
+    launches = int(st_main.get("kernel_launches", 0))
     subrays = B * N * args.steps * world
     pulses = B * args.steps * world
     value = subrays / (ms_max / 1e3) / 1e6
 
-    # ---- algorithmic bytes (instrumented, untimed re-run of the same batches)
-    nodes = tris = vox = f64 = beam_nodes = n_ret = 0
-    node_bytes = 64
-    for i in range(args.warmup, steps_total):
-        st = step(i, counters=True)
-        node_bytes = st.node_bytes or 64
-        nodes += st.nodes_visited
-        tris += st.tris_tested
-        vox += st.voxel_steps
-        f64 += st.fp64_tests
-        beam_nodes += st.beam_nodes
-        n_ret += st.returns
+    # ---- the same steps as one blocking helios_simulate call each
+    def blocking():
+        for i in timed_idx:
+            o, d, t, start = batches[i]
+            h.simulate(scene, hp, o, d, t, pulse_index_base=start, outputs=outs[0])
+    bms, _ = timed(blocking)
+
+    # ---- exclusive kernel times: every kernel of the same steps on one stream
+    # (helios_tuning.serialize), CUDA events around each launch (helios_stats)
+    with h.tuning(serialize=1):
+        sms_ser, st_ser = timed(lambda: run_steps(timed_idx, st=True))
+    # ---- algorithmic bytes: instrumented kernel variant, untimed
+    st_cnt = run_steps(timed_idx, counters=True)
+    nodes, tris = st_cnt["nodes_visited"], st_cnt["tris_tested"]
+    vox, f64, beam_nodes = st_cnt["voxel_steps"], st_cnt["fp64_tests"], st_cnt["beam_nodes"]
+    n_ret = st_cnt["returns"]
     sub_rank = B * N * args.steps
-    # per subray: nodes K6 tests, triangles, voxel steps; per pulse: nodes the
-    # beam pre-pass K6a tests (once for all the pulse's subrays)
-    b_ray = node_bytes * nodes + 48 * tris + 4 * vox + 64 * beam_nodes
-    b_trace = b_ray + 24 * B * args.steps + 16 * sub_rank  # + pulse inputs + records
-    b_pulse = (32 + 8 + 1 + 4 * n_bins + 32 * p.max_returns) * B * args.steps
+    pul_rank = B * args.steps
+    # SURVEY 8(d) D-3: B_ray = 64 N_node + 48 N_tri + 4 N_cell (+ 64 per K6a node
+    # test, once per pulse for all its subrays); B_pulse = 32 + 8 + 1 + 4 n_bins + 32 R
+    b_ray = 64 * nodes + 48 * tris + 4 * vox + 64 * beam_nodes
+    b_pulse = (32 + 8 + 1 + 4 * n_bins + 32 * p.max_returns) * pul_rank
+    # K6 (k_trace) alone: its traversal reads + pulse inputs + the 12-B records it writes
+    b_k6 = 64 * nodes + 48 * tris + 4 * vox + 24 * pul_rank + 12 * sub_rank
+    # K7 (k_waveform) alone: 8-B records read + row, returns, k0, count written
+    b_k7 = 8 * sub_rank + (4 * n_bins * dense + 32 * p.max_returns + 9) * pul_rank
     peak, peak_src = peaks()
-    ach_trace = b_trace / (trace_ms / 1e3) / 1e9
-    n_trace_launches = max(1, trace_launches)
-    traffic, limiter, issue = None, None, None
+    k6_ms, k6a_ms, k7_ms = st_ser["trace_ms"], st_ser["beam_ms"], st_ser["waveform_ms"]
+    n_launch = max(1, int(st_ser["trace_launches"]))
+    ach_k6 = b_k6 / (k6_ms / 1e3) / 1e9
+    ach_k7 = b_k7 / (k7_ms / 1e3) / 1e9
+    r1 = (b_ray + b_pulse) / (ms_max / 1e3) / 1e9 / peak
+    traffic, issue = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(args.config)
         if tj:
             kt = tj["k_trace"]
-            traffic = kt["dram_bytes"] / kt["units"] * (sub_rank / n_trace_launches)
-            limiter = {"issue_slots_busy": kt["issue_slots_busy"],
-                       "dram_bytes_per_subray": kt["dram_bytes"] / kt["units"],
-                       "l1_hit": kt["l1_hit"], "source": tj["source"]}
-            if "warp_inst" in kt:
-                # the bound that binds: SM instruction issue (4 warp instructions
-                # per clock per SM).  Warp instructions per subray of K6a + K6 and
-                # per pulse of K7 from the ncu capture, times this step's subrays
-                # and pulses, over the step time (the kernels overlap on several
-                # streams, so the whole step is the unit)
-                wi = kt["warp_inst"] / kt["units"]
-                kw = tj.get("k_waveform", {})
-                wp = kw["warp_inst"] / kw["units"] if "warp_inst" in kw else 0.0
-                sms = torch.cuda.get_device_properties(dev).multi_processor_count
-                mhz = (clk or {}).get("sm_mhz") or 1965.0
-                peak_issue = sms * 4 * mhz * 1e6
-                ach = (wi * sub_rank + wp * B * args.steps) / (ms / 1e3)
-                issue = {"bound": "issue", "kernel": "k_beam + k_trace + k_waveform (whole step)",
-                         "achieved": ach / 1e9, "peak": peak_issue / 1e9,
-                         "unit": "G warp-instructions/s", "frac": ach / peak_issue,
-                         "warp_inst_per_subray": wi, "waveform_warp_inst_per_pulse": wp,
-                         "source": tj["source"]}
+            traffic = kt["dram_bytes"] / kt["units"] * (sub_rank / n_launch)
+            kw = tj.get("k_waveform", {})
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            mhz = (clk or {}).get("sm_mhz") or 1965.0
+            peak_issue = sms * 4 * mhz * 1e6
+            wi = kt["warp_inst"] / kt["units"]
+            wp = kw["warp_inst"] / kw["units"] if "warp_inst" in kw else 0.0
+            issue = {"bound": "issue", "achieved": (wi * sub_rank + wp * pul_rank) / (ms_max / 1e3) / 1e9,
+                     "peak": peak_issue / 1e9, "unit": "G warp-instructions/s",
+                     "frac": (wi * sub_rank + wp * pul_rank) / (ms_max / 1e3) / peak_issue,
+                     "warp_inst_per_subray_k6a_k6": wi, "warp_inst_per_pulse_k7": wp,
+                     "k6_issue_slots_busy": kt.get("issue_slots_busy"),
+                     "k7_issue_slots_busy": kw.get("issue_slots_busy"),
+                     "source": tj["source"]}
     except Exception:
         pass
-    r1 = (b_ray + b_pulse) / (ms / 1e3) / 1e9 / peak
 
-    # ---- the same device-resident steps with the lossless packed outputs
-    # (packed returns + packed waveform support rows instead of 7 fixed return
-    # slots and dense rows: the zero fill of dense rows is HBM traffic, 10.7 KB
-    # per pulse on C4)
+    # ---- the same steps with the lossless packed outputs (packed returns +
+    # packed waveform support rows) instead of fixed slots and dense rows
     packed = None
-    if args.waveform == "dense" and not args.no_packed:
-        pout = h.alloc_outputs(B, hp, device=dev, waveform=False, compact=True,
-                               compact_capacity=B * n_bins, packed_returns=True, slots=False,
-                               returns_capacity=B * p.max_returns)
-        for i in range(min(args.warmup, 2)):
-            start, o, d, t = batches[i]
-            h.simulate(scene, hp, o, d, t, pulse_index_base=start, outputs=pout)
-        torch.cuda.synchronize()
-        barrier(world)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.warmup, steps_total):
-            start, o, d, t = batches[i]
-            h.simulate(scene, hp, o, d, t, pulse_index_base=start, outputs=pout)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        pms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+    if not args.no_packed:
+        pouts = [h.alloc_outputs(B, hp, device=dev, waveform=False, compact=True,
+                                 compact_capacity=B * PACKED_FLOATS_PER_PULSE,
+                                 packed_returns=True, slots=False,
+                                 returns_capacity=B * p.max_returns) for _ in range(min(M, 8))]
+        def run_packed():
+            for g in _groups(list(timed_idx), len(pouts)):
+                h.simulate_batches(scene, hp, [batches[i] for i in g], pouts[:len(g)])
+        run_packed()  # grows capacities if needed (retry inside simulate is per call)
+        pms, _ = timed(run_packed)
         packed = {"value": subrays / (pms / 1e3) / 1e6, "unit": "Mrays/s",
                   "ms_per_step": pms / args.steps,
                   "outputs": "packed returns + packed waveform support rows (lossless)"}
-        del pout
+        del pouts
 
-    # ---- end to end through the C ABI with host buffers (copies inside):
-    # every step copies its pulses host->device and the full result back
-    # (returns + the complete waveform, as lossless packed support rows; the
-    # dense-row variant is reported beside it)
-    e2e = e2e_dense = None
+    # ---- end to end through the public API with HOST buffers: every step's
+    # pulses are copied host -> device and its complete result (returns +
+    # packed waveform support rows, lossless) device -> host inside the timed
+    # region; distinct batches, <= 8 per helios_simulate_batches call
+    e2e = None
     if not args.no_e2e:
-        def run_e2e(compact):
-            start, o, d, t = batches[args.warmup]
-            ho, hd, ht = (x.cpu().pin_memory() for x in (o, d, t))
-            hout = h.alloc_outputs(B, hp, device="cpu", waveform=not compact, pin_memory=True,
-                                   compact=compact,
-                                   compact_capacity=B * n_bins if compact else None,
-                                   packed_returns=compact, slots=not compact,
-                                   returns_capacity=B * p.max_returns if compact else None)
-            h.simulate(scene, hp, ho, hd, ht, pulse_index_base=start, outputs=hout)
-            torch.cuda.synchronize()
-            barrier(world)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for i in range(args.steps):
-                h.simulate(scene, hp, ho, hd, ht, pulse_index_base=start, outputs=hout)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
-            h2d = B * (12 + 12 + 8)
-            d2h = B * (1 + 8)
-            if compact:  # packed returns + packed waveform rows, with their offsets
-                d2h += 16 * (B + 1) + 32 * int(hout.return_offset[-1]) + \
-                    4 * int(hout.wf_offset[-1])
-            else:
-                d2h += 32 * p.max_returns * B + 4 * n_bins * B
-            del hout
-            return {"value": B * N * args.steps * world / (ems / 1e3) / 1e6, "unit": "Mrays/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "pulses_per_s": B * args.steps * world / (ems / 1e3),
-                    "waveform_output": "packed support rows + packed returns (lossless)"
-                    if compact else "dense rows + fixed return slots"}
-        e2e = run_e2e(True)
-        e2e_dense = run_e2e(False)
+        hb_in = []
+        for i in timed_idx:
+            o, d, t, start = batches[i]
+            hb_in.append((o.cpu().pin_memory(), d.cpu().pin_memory(), t.cpu().pin_memory(), start))
+        G = min(args.steps, 8)
+        houts = [h.alloc_outputs(B, hp, device="cpu", waveform=False, pin_memory=True,
+                                 compact=True, compact_capacity=B * PACKED_FLOATS_PER_PULSE,
+                                 packed_returns=True, slots=False,
+                                 returns_capacity=B * p.max_returns) for _ in range(G)]
+        d2h = [0]
+
+        def run_e2e():
+            d2h[0] = 0
+            for g in _groups(list(range(len(hb_in))), G):
+                h.simulate_batches(scene, hp, [hb_in[i] for i in g], houts[:len(g)])
+                for k in range(len(g)):
+                    hout = houts[k]
+                    d2h[0] += B * (1 + 8) + 16 * (B + 1) + 32 * int(hout.return_offset[-1]) + \
+                        4 * int(hout.wf_offset[-1])
+        h.simulate_batches(scene, hp, hb_in[:1], houts[:1])
+        ems, _ = timed(run_e2e)
+        e2e = {"value": subrays / (ems / 1e3) / 1e6, "unit": "Mrays/s",
+               "h2d_bytes_per_step": B * (12 + 12 + 8), "d2h_bytes_per_step": d2h[0] // args.steps,
+               "pulses_per_s": pulses / (ems / 1e3), "ms_per_step": ems / args.steps,
+               "api": f"helios_simulate_batches, {G} distinct host batches per call",
+               "waveform_output": "packed support rows + packed returns (lossless)"}
+        del houts, hb_in
 
     # ---- on-device pulse generation (helios_simulate_survey, NEXT f2): the
-    # same pulses, generated from the workload's flight-line description, no
-    # pulse arrays at all; device-resident outputs (as `value`) and, end to
-    # end, host outputs with packed waveform rows (as `e2e`)
+    # same steps generated from the workload's flight lines (no pulse arrays),
+    # device-resident outputs, one blocking call per step
     survey = None
     if w.surveys and not args.no_survey:
         def seg_of(start):
@@ -401,58 +399,70 @@ def run_ours(args):
                 if g0 <= start < g0 + cnt:
                     return sv, start - g0, min(B, g0 + cnt - start)
             return None
-        segs = [seg_of(batches[i][0]) for i in range(steps_total)]
-        if all(sg is not None and sg[2] == B for sg in segs):
-            def sstep(i, outs):
-                sv, first, cnt = segs[i]
-                h.simulate_survey(scene, hp, sv, first, cnt, batches[i][0], outputs=outs)
-            for i in range(args.warmup):
-                sstep(i, out)
-            torch.cuda.synchronize()
-            barrier(world)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for i in range(args.warmup, steps_total):
-                sstep(i, out)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            sms = max_over_ranks(e0.elapsed_time(e1), world, dev)
-            survey = {"value": B * N * args.steps * world / (sms / 1e3) / 1e6, "unit": "Mrays/s",
+        segs = {i: seg_of(batches[i][3]) for i in range(steps_total)}
+        if all(sg is not None and sg[2] == B for sg in segs.values()):
+            def run_survey():
+                for i in timed_idx:
+                    sv, first, cnt = segs[i]
+                    h.simulate_survey(scene, hp, sv, first, cnt, batches[i][3], outputs=outs[0])
+            run_survey()
+            sms, _ = timed(run_survey)
+            survey = {"value": subrays / (sms / 1e3) / 1e6, "unit": "Mrays/s",
                       "ms_per_step": sms / args.steps,
-                      "pulses": "generated on the device from the flight lines (R30)"}
-            if not args.no_e2e:
-                hout = h.alloc_outputs(B, hp, device="cpu", waveform=False, pin_memory=True,
-                                       compact=True, compact_capacity=B * n_bins,
-                                       packed_returns=True, slots=False,
-                                       returns_capacity=B * p.max_returns)
-                sstep(args.warmup, hout)
-                torch.cuda.synchronize()
-                barrier(world)
-                e0.record(stream)
-                for i in range(args.steps):
-                    sstep(args.warmup, hout)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ems = max_over_ranks(e0.elapsed_time(e1), world, dev)
-                d2h = B * (1 + 8) + 16 * (B + 1) + 32 * int(hout.return_offset[-1]) + \
-                    4 * int(hout.wf_offset[-1])
-                survey["e2e"] = {"value": B * N * args.steps * world / (ems / 1e3) / 1e6,
-                                 "unit": "Mrays/s", "h2d_bytes_per_step": 0,
-                                 "d2h_bytes_per_step": d2h,
-                                 "waveform_output": "packed support rows + packed returns "
-                                                    "(lossless)"}
-                del hout
+                      "pulses": "generated on the device from the flight lines (R30)",
+                      "api": "one blocking helios_simulate_survey per step"}
+
+    # ---- the WHOLE configuration (every pulse of it), in
+    # batches of B pulses through helios_simulate_batches (10 per call, packed
+    # device outputs), 1 warm-up + 5 timed runs: median and minimum
+    full = None
+    if args.full_config and world == 1:
+        del outs
+        torch.cuda.synchronize()
+        n_all = w.n_pulses
+        fb = []
+        for s0 in range(0, n_all, 10 * B):
+            cnt = min(10 * B, n_all - s0)
+            o, d, t = w.pulses(s0, cnt)
+            for k in range(0, cnt, B):
+                m = min(B, cnt - k)
+                to = lambda a: torch.from_numpy(np.ascontiguousarray(a[k:k + m])).to(dev)
+                fb.append((to(o), to(d), to(t), s0 + k))
+        del batches
+        G = 10
+        fouts = [h.alloc_outputs(B, hp, device=dev, waveform=False, compact=True,
+                                 compact_capacity=B * PACKED_FLOATS_PER_PULSE,
+                                 packed_returns=True, slots=False,
+                                 returns_capacity=B * p.max_returns) for _ in range(G)]
+
+        def run_full():
+            for g in _groups(list(range(len(fb))), G):
+                h.simulate_batches(scene, hp, [fb[i] for i in g], [fouts[k] for k in range(len(g))])
+        run_full()
+        runs = [timed(run_full)[0] / 1e3 for _ in range(5)]
+        full = {"pulses": n_all, "subrays": n_all * N, "batch_pulses": B, "batches_per_call": G,
+                "runs_s": [round(x, 4) for x in runs], "median_s": float(np.median(runs)),
+                "min_s": float(np.min(runs)),
+                "Mrays_per_s_median": n_all * N / float(np.median(runs)) / 1e6,
+                "pulses_per_s_median": n_all / float(np.median(runs)),
+                "outputs": "packed returns + packed waveform support rows, device-resident"}
+        del fouts, fb
+
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n_p, sec = oracle_sample(w, threads, args.cpu_budget)
+        # D-5: one thread on a small slice, extrapolated to the whole config
+        n1, sec1 = oracle_sample(w, 1, max(2.0, args.cpu_budget / 4), seed=7)
         cpu = {"value": n_p * N / sec / 1e6, "unit": "Mrays/s", "cores": threads,
                "kind": "oracle",
                "sample": f"{n_p} random pulses of {args.config} ({n_p * N} subrays), "
                          f"fp64 brute-force oracle, {sec:.1f} s on {threads} threads",
-               "pulses_per_s": n_p / sec}
+               "pulses_per_s": n_p / sec,
+               "one_thread": {"pulses": n1, "s": round(sec1, 2),
+                              "extrapolated_full_config_s": w.n_pulses * sec1 / n1,
+                              "extrapolated_full_config_s_all_cores": w.n_pulses * sec / n_p}}
 
     if rank == 0:
         line = {
@@ -462,36 +472,45 @@ def run_ours(args):
             "dtype": "f64 decisions / f32 storage",
             "data": "synthetic (seeded generators, workloads/; paper datasets unavailable)",
             "pulses_per_s": pulses / (ms_max / 1e3),
-            # discrete returns of the timed steps (rank 0 counts, instrumented re-run; x world)
             "returns_per_s": n_ret * world / (ms_max / 1e3),
             "config": {"workload": args.config, "pulses_per_step_per_gpu": B,
                        "subrays_per_pulse": N, "n_tris": w.scene.n_tris,
                        "n_bins": n_bins, "l2": "inputs larger than L2 (scene + outputs)",
+                       "api": f"helios_simulate_batches, {M} batches (steps) per call, "
+                              "distinct batches and output sets",
                        "bvh_nodes": info.n_nodes, "bvh_depth": info.max_depth,
                        "build_ms": round(info.build_ms, 2), "gen_s": round(t_gen, 1),
                        "fit_echo_width": int(args.fit_echo_width),
                        "waveform_output": args.waveform,
                        "range_noise_sd_m": args.range_noise},
-            "roofline": {"bound": "hbm", "kernel": "k_beam + k_trace", "achieved": ach_trace,
-                         "peak": peak, "unit": "GB/s", "frac": ach_trace / peak,
+            "roofline": {"bound": "hbm", "kernel": "k_trace (K6)", "achieved": ach_k6,
+                         "peak": peak, "unit": "GB/s", "frac": ach_k6 / peak,
                          "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_launch": b_trace / n_trace_launches,
-                         "avg_launch_ms": trace_ms / n_trace_launches,
-                         "ncu_limiter": limiter,
+                         "bytes_per_launch": b_k6 / n_launch,
+                         "avg_launch_ms": k6_ms / n_launch,
+                         "timing": "exclusive: every kernel on one stream (helios_tuning.serialize)",
+                         "step_R1": r1,
+                         "kernels_exclusive_ms_per_step": {
+                             "k_beam (K6a)": k6a_ms / args.steps, "k_trace (K6)": k6_ms / args.steps,
+                             "k_waveform (K7)": k7_ms / args.steps,
+                             "serialized_step": sms_ser / args.steps},
+                         "k_waveform": {"bound": "hbm", "achieved": ach_k7, "frac": ach_k7 / peak,
+                                        "bytes_per_pulse": b_k7 / pul_rank},
                          "issue_roofline": issue,
-                         "share_of_step": trace_ms / ms if ms > 0 else None,
-                         "waveform_share_of_step": wave_ms / ms if ms > 0 else None,
-                         "nodes_per_ray": nodes / sub_rank, "node_bytes": node_bytes,
-                         "beam_nodes_per_pulse": beam_nodes / (B * args.steps),
+                         "fp64_fma_tflops_measured": fp64_tflops,
+                         "nodes_per_ray": nodes / sub_rank,
+                         "beam_nodes_per_pulse": beam_nodes / pul_rank,
                          "tris_per_ray": tris / sub_rank,
                          "voxel_steps_per_ray": vox / sub_rank,
-                         "fp64_tests_per_ray": f64 / sub_rank,
-                         "step_R1": r1},
+                         "fp64_tests_per_ray": f64 / sub_rank},
             "gpu_launches": launches,
             "clocks": clk,
+            "blocking_calls": {"value": subrays / (bms / 1e3) / 1e6, "unit": "Mrays/s",
+                               "ms_per_step": bms / args.steps,
+                               "api": "one blocking helios_simulate per step"},
             "e2e": e2e,
-            "e2e_dense_rows": e2e_dense,
             "packed_outputs": packed,
+            "full_config": full,
             "device_pulse_generation": survey,
             "cpu_baseline": cpu,
         }
@@ -523,11 +542,15 @@ def main():
     ap.add_argument("--range-noise", type=float, default=0.0,
                     help="ranging error sigma in m (P:288)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-config", type=int, default=-1,
+                    help="SURVEY D-4 run over every pulse of the config (default: on for C5)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=12.0,
                     help="seconds of oracle work per --impl reference step")
     args = ap.parse_args()
     args.config = args.config.upper()
+    if args.full_config < 0:
+        args.full_config = 1 if args.config == "C5" else 0
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -276,6 +276,14 @@ typedef struct {
   double beam_ms;     /* out: summed device time of the beam pre-pass launches (K6a)     */
   uint32_t batches;   /* out: pulse batches of the call                                  */
   uint32_t chunks;    /* out: pipeline chunks of the call                                */
+  /* warp-level traversal counts of K6 (collect_counters; each once per warp,
+     whatever the number of its lanes involved): beam-entry list entries
+     examined, entries walked, packet steps (node or leaf visits), triangles
+     iterated in leaves -- the cost of the union of the lanes' paths */
+  uint64_t warp_entries, warp_entries_walked, warp_steps, warp_leaf_tris;
+  /* fp64 tests run inside the walks (counted once per group of lanes running
+     one together), and definite fp32 hits that had to be decided at once */
+  uint64_t warp_fp64_in_walk, second_definite_hits;
 } helios_stats;
 
 /* Simulate n_pulses pulses (the hot path: subray fan-out, nearest hit against

@@ -37,6 +37,12 @@ int helios_util_sort_pairs_u64(uint64_t* d_keys, uint32_t* d_vals, uint64_t n, i
 int helios_util_scan_u64(const uint64_t* d_in, uint64_t* d_out, uint64_t n, int inclusive,
                          void* stream);
 
+/* Measured fp64 FMA throughput of the device (TFLOP/s, 2 flops per FMA):
+ * every SM, 8 independent DFMA chains per thread, timed with CUDA events.
+ * The fp64 ceiling of the voxel march and the decisions (DESIGN.md s.7),
+ * reported by bench.py beside the copy bandwidth of MEASURED_PEAKS.json. */
+int helios_util_fp64_fma_tflops(double* tflops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,6 +25,7 @@ from .helios import (  # noqa: F401
     helios_tuning,
     simulate_batches,
     tuning,
+    util_fp64_fma_tflops,
     util_scan_u64,
     util_sort_pairs_u64,
     helios_version,

@@ -840,7 +840,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const size_t o_tab = carve(sizeof(SubrayConst) * N);
   const size_t o_ker = carve(sizeof(double) * d.taps);
   const size_t o_err = carve(sizeof(unsigned));
-  const size_t o_cnt = carve(sizeof(unsigned long long) * 8);
+  const size_t o_cnt = carve(sizeof(unsigned long long) * 16);
   const size_t o_ws = carve(plan.scratch_bytes);
   size_t o_wrec[kSlots], o_prim[kSlots], o_arr[A_COUNT][kSlots] = {}, o_ent[kSlots],
       o_frm[kSlots], o_fjob[kSlots], o_fy[kSlots], o_cst[kSlots], o_rst[kSlots];
@@ -910,7 +910,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(d_ker, d.kernel.data(), sizeof(double) * d.taps, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, sizeof(unsigned), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 16, s);
   // offs[job base] = 0: the carry the first chunk of each batch starts from
   for (uint32_t j = 0; j < n_jobs && e == cudaSuccess; ++j) {
     if (any_offs) e = cudaMemsetAsync(d_offs + job_off[j], 0, sizeof(uint64_t), s);
@@ -1311,7 +1311,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
                           cudaMemcpyDefault, s);
   }
   unsigned herr = 0;
-  unsigned long long hcnt[8] = {0};
+  unsigned long long hcnt[16] = {0};
   std::vector<uint64_t> htot(n_jobs, 0), hrtot(n_jobs, 0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&herr, d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
   for (uint32_t j = 0; j < n_jobs && e == cudaSuccess; ++j) {
@@ -1380,6 +1380,12 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     stats->subray_hits = hcnt[4];
     stats->returns = hcnt[5];
     stats->batches = n_jobs;
+    stats->warp_entries = hcnt[8];
+    stats->warp_steps = hcnt[9];
+    stats->warp_leaf_tris = hcnt[10];
+    stats->warp_entries_walked = hcnt[11];
+    stats->warp_fp64_in_walk = hcnt[12];
+    stats->second_definite_hits = hcnt[13];
     stats->chunks = (uint32_t)n_chunks;
   }
   if (herr & 4u) return fail(HELIOS_ERR_CUDA, "internal: compact row length mismatch");

@@ -330,7 +330,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
                                                 float iz, HitState& hs,
                                                 unsigned long long& c_nodes,
                                                 unsigned long long& c_tris,
-                                                unsigned long long& c_f64) {
+                                                unsigned long long& c_f64, unsigned* wc) {
   const unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   int32_t stA_r = 0, stB_r = 0;
@@ -345,7 +345,9 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
   };
   for (;;) {
     const bool mine = (m >> lane) & 1u;
+    if (INSTR) ++wc[1];  // warp steps (nodes + leaves), counted once per warp
     if (ref_is_leaf(ref)) {
+      if (INSTR) wc[2] += leaf_count(ref);  // triangles the warp iterates
       if (mine) {
         const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
         for (uint32_t k = first; k < first + cnt; ++k) {
@@ -362,7 +364,12 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
             hs.bound = fminf(hs.bound, tup);
             continue;
           }
-          if (INSTR) ++c_f64;
+          if (INSTR) {
+            ++c_f64;
+            // warp-level: one count per group of lanes running this fp64 test together
+            if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) ++wc[4];
+            wc[5] += cls == 2;  // a second definite hit, not surely nearer
+          }
           const double t = mt64(O, D, tr);
           if (t > 0.0) {
             take_hit(hs, t, __float_as_uint(tr.a.w), k);
@@ -642,6 +649,9 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
   const uint32_t s = sc.index;
   const uint64_t slot = p * a.N + s;  // [pulse][subray] (R4 order) in every output
   unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;
+  // warp-level counts (instrumented variant): entries examined, packet steps,
+  // leaf triangles iterated, entries walked -- once per warp, not per lane
+  unsigned wc[6] = {0, 0, 0, 0, 0, 0};
 
 
   // ---- A2: subray fan-out (R2, R4), fp64
@@ -697,7 +707,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
           while (rem) {
             if (a.entries == nullptr) {
               traverse_packet<INSTR>(a, rem, a.root, O, D, O32, D32, dl1, ix, iy, iz, hs,
-                                     c_nodes, c_tris, c_f64);
+                                     c_nodes, c_tris, c_f64, wc);
               break;
             }
             const uint32_t pq = __shfl_sync(0xffffffffu, (uint32_t)p, __ffs(rem) - 1);
@@ -731,9 +741,11 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
                 }
               }
               const unsigned me = __ballot_sync(0xffffffffu, go);
+              if (INSTR) ++wc[0];  // entries the warp examines
+              if (INSTR && me) ++wc[3];  // entries it walks
               if (me)
                 traverse_packet<INSTR>(a, me, en.x, O, D, O32, D32, dl1, ix, iy, iz, hs,
-                                       c_nodes, c_tris, c_f64);
+                                       c_nodes, c_tris, c_f64, wc);
             }
             skip = taken;
           }
@@ -877,12 +889,17 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
             const double sigma = (double)pad * G;  // Eq. 4 via the G LUT
             const double u = transmission_u(a.seed, a.pulse_base + p, s, id);
             // u < exp(-sigma L) decided by an fp32 estimate whenever u is
-            // farther from it than its error bound (__expf <= 2 + 1.17|x| ulp,
-            // plus the fp32 rounding of x: < 1e-5 relative for x < 80), else
-            // by the fp64 exp -- the decision is the fp64 one either way
+            // farther from it than its error bound, else by the fp64 exp:
+            // the decision is the fp64 one either way.  For x = sigma L < 16.6
+            // the estimate __expf(-(float)x) is within (2 + 1.17 x) ulp (<= 21.5
+            // ulp = 1.3e-6 relative) of e^-(float)x, and rounding x to fp32
+            // moves e^-x by <= x 2^-24 (<= 1e-6) relative: < 2.3e-6 in all,
+            // below the 1e-5 margin.  For x >= 16.6, e^-x < 6.2e-8 and the
+            // fp64 exp decides (u is a multiple of 2^-24 = 6e-8, so only u = 0
+            // can pass there; the filter's bound is not needed).
             const double x = sigma * L;
             bool pass;
-            if (HELIOS_EXP_FILTER && x < 80.0) {
+            if (HELIOS_EXP_FILTER && x < 16.6) {
               const double e32 = (double)__expf(-(float)x);
               pass = fabs(u - e32) > 1e-5 * e32 ? u < e32 : u < exp(-x);
             } else {
@@ -956,6 +973,17 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
     for (int i = 0; i < 5; ++i) {
       const unsigned w = __reduce_add_sync(mask, (unsigned)v[i]);
       if (leader && w) atomicAdd(a.counters + cslot[i], (unsigned long long)w);
+    }
+    // warp-uniform counts: the leader's copy (every active lane holds the same)
+    if (leader)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (wc[i]) atomicAdd(a.counters + 8 + i, (unsigned long long)wc[i]);
+    // per lane: in-loop fp64 tests run by a lane-group leader, second definite hits
+    const unsigned w4 = __reduce_add_sync(mask, wc[4]), w5 = __reduce_add_sync(mask, wc[5]);
+    if (leader) {
+      if (w4) atomicAdd(a.counters + 12, (unsigned long long)w4);
+      if (w5) atomicAdd(a.counters + 13, (unsigned long long)w5);
     }
   }
 }

@@ -221,16 +221,15 @@ __global__ void k_range_noise(helios_return* __restrict__ ret, const uint8_t* __
 }
 
 struct Layout {
-  size_t ker_d, per_warp_d, w_off, agg_off, off_off, amp_off;
+  size_t ker_d, per_warp_d, w_off, agg_off, rec_off;
 };
 __host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
   Layout L;
   L.ker_d = (taps + 1) & ~1u;
   L.w_off = 0;
   L.agg_off = kWCap;
-  L.off_off = kWCap + kAggCap;                 // int[N] packed 2 per double
-  L.amp_off = L.off_off + (N + 1) / 2;         // float[N]
-  L.per_warp_d = L.amp_off + (N + 1) / 2;
+  L.rec_off = kWCap + kAggCap;                 // int2[N] {offset o_s, bits of A_s}
+  L.per_warp_d = L.rec_off + N;
   return L;
 }
 
@@ -259,8 +258,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
   double* base = ker + L.ker_d + (size_t)warp * L.per_warp_d;
   double* Ws = base + L.w_off;
   double* agg = base + L.agg_off;
-  int* off = reinterpret_cast<int*>(base + L.off_off);
-  float* amp = reinterpret_cast<float*>(base + L.amp_off);
+  int2* sr = reinterpret_cast<int2*>(base + L.rec_off);  // {o_s (or k_s), bits of A_s}
   const unsigned kFull = 0xffffffffu;
 
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
@@ -269,17 +267,24 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
   for (uint64_t p = (uint64_t)blockIdx.x * nw + warp; p < a.n_pulses;
        p += (uint64_t)gridDim.x * nw) {
     const int2* rec = reinterpret_cast<const int2*>(a.rec + p * N);
+    // the pulse's time is needed only by its returns: load it early
+    const double tsec = (a.time_s && lane == 0) ? a.time_s[p] : 0.0;
     // pass 1: records -> shared memory (read once, streaming), k0 = min k_s
     int kmin = INT_MAX;
     for (uint32_t s = lane; s < N; s += 32) {
       const int2 r = __ldcs(rec + s);
-      off[s] = r.x;
-      amp[s] = __int_as_float(r.y);
+      sr[s] = r;
       if (r.x >= 0) kmin = min(kmin, r.x);
     }
     const int k0 = __reduce_min_sync(kFull, kmin);
     helios_return* slots = a.returns + p * a.max_returns;
     float* row = a.waveform ? a.waveform + p * (uint64_t)nb : nullptr;
+    // returns 0..31 are assembled in the registers of lane r and stored once
+    // their count is known (one 32-B record per lane)
+    const bool reg_ret = a.max_returns <= 32;
+    double rr_range = 0.0;
+    float rr_int = 0.0f;
+    uint32_t rr_prim = 0;
     uint32_t S = 0;
     double* W = Ws;
     uint32_t nret = 0;
@@ -287,19 +292,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       // offsets within the window; beyond maxFullwaveRange -> discarded
       int maxoff = 0;
       for (uint32_t s = lane; s < N; s += 32) {
-        int o = off[s];
+        int o = sr[s].x;
         if (o >= 0) {
           o -= k0;
           if (o >= (int)nb) o = -2;
           else maxoff = max(maxoff, o);
-          off[s] = o;
+          sr[s].x = o;
         }
       }
       maxoff = __reduce_max_sync(kFull, maxoff);
       S = min(nb, (uint32_t)maxoff + taps);
       W = (S <= (uint32_t)kWCap) ? Ws : gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
       __syncwarp();
+      double Mlane = 0.0;  // this lane's maximum of W (grouped path: while computing W)
+      bool have_max = false;
       if (maxoff < kAggCap) {
+        have_max = true;
         // amplitude per offset group.  Few groups (G <= 16, the usual case):
         // lane (o, c) sums group o over subray chunk c of C = 32 / G chunks,
         // then a fixed binary tree over the chunks combines the partials; else
@@ -307,33 +315,56 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         // deterministic.
         const int G = maxoff + 1;
         if (G <= 16) {
-          const int C = 32 / G, o = lane % G, c = lane / G;
-          double acc = 0.0;
-          if (c < C) {
-            const uint32_t s0 = (uint32_t)((N * (uint32_t)c) / (uint32_t)C);
-            const uint32_t s1 = (uint32_t)((N * (uint32_t)(c + 1)) / (uint32_t)C);
-            for (uint32_t s = s0; s < s1; ++s)
-              if (off[s] == o) acc += (double)amp[s];
+          // groups rounded up to G' = 2^lg <= 16 lanes: lane (o, c) = (lane mod
+          // G', lane / G') sums group o over subray chunk c of C = 32 / G'
+          // (shifts, no divisions), then a fixed binary tree over the chunks
+          const int lg = G <= 1 ? 0 : 32 - __clz(G - 1);
+          const int o = lane & ((1 << lg) - 1), c = lane >> lg, lc = 5 - lg;
+          double acc = 0.0, acc2 = 0.0;  // two chains (subrays of even / odd rank)
+          if (o < G) {
+            const uint32_t s0 = (N * (uint32_t)c) >> lc, s1 = (N * (uint32_t)(c + 1)) >> lc;
+            uint32_t s = s0;
+            for (; s + 1 < s1; s += 2) {
+              const int2 r = sr[s], r2 = sr[s + 1];
+              if (r.x == o) acc += (double)__int_as_float(r.y);
+              if (r2.x == o) acc2 += (double)__int_as_float(r2.y);
+            }
+            if (s < s1) {
+              const int2 r = sr[s];
+              if (r.x == o) acc += (double)__int_as_float(r.y);
+            }
+            acc += acc2;
           }
-          for (int st = 1; st < C; st <<= 1) {
-            const double other = __shfl_down_sync(kFull, acc, st * G);
-            if (c < C && (c & (2 * st - 1)) == 0 && c + st < C) acc += other;
+          for (int st = 1; st < (1 << lc); st <<= 1) {
+            const double other = __shfl_down_sync(kFull, acc, st << lg);
+            if ((c & (2 * st - 1)) == 0) acc += other;
           }
           if (lane < G) agg[lane] = acc;
         } else {
           for (int o = lane; o <= maxoff; o += 32) {
             double acc = 0.0;
-            for (uint32_t s = 0; s < N; ++s)
-              if (off[s] == o) acc += (double)amp[s];
+            for (uint32_t s = 0; s < N; ++s) {
+              const int2 r = sr[s];
+              if (r.x == o) acc += (double)__int_as_float(r.y);
+            }
             agg[o] = acc;
           }
         }
         __syncwarp();
+        // W[k] = sum_o A_o p[k - o], two fp64 chains per bin (even / odd
+        // offsets), the lane's running maximum on the way
         for (uint32_t k = lane; k < S; k += 32) {
           const int olo = max(0, (int)k - (int)taps + 1), ohi = min(maxoff, (int)k);
-          double w = 0.0;
-          for (int o = olo; o <= ohi; ++o) w = fma(agg[o], ker[k - o], w);
+          double w = 0.0, w2 = 0.0;
+          int o = olo;
+          for (; o + 1 <= ohi; o += 2) {
+            w = fma(agg[o], ker[k - o], w);
+            w2 = fma(agg[o + 1], ker[k - o - 1], w2);
+          }
+          if (o <= ohi) w = fma(agg[o], ker[k - o], w);
+          w += w2;
           W[k] = w;
+          Mlane = fmax(Mlane, w);
         }
       } else {
         // wide footprint (offsets spread over >= kAggCap bins, e.g. a crown and
@@ -347,14 +378,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         int G = 0;
         for (uint32_t c0 = 0; c0 < N; c0 += 32) {
           const uint32_t s = c0 + lane;
-          const int o = s < N ? off[s] : -1;
+          const int o = s < N ? sr[s].x : -1;
           const unsigned peers = __match_any_sync(kFull, o);
           const bool lead = o >= 0 && (int)(__ffs(peers) - 1) == lane;
           const unsigned leads = __ballot_sync(kFull, lead);
           const int idx = G + __popc(leads & ((1u << lane) - 1u));
           if (lead && idx < kGroupCap) {
             double acc = 0.0;
-            for (unsigned b = peers; b; b &= b - 1u) acc += (double)amp[c0 + __ffs(b) - 1];
+            for (unsigned b = peers; b; b &= b - 1u)
+              acc += (double)__int_as_float(sr[c0 + __ffs(b) - 1].y);
             gsum[idx] = acc;
             goff[idx] = o;
           }
@@ -374,9 +406,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           }
         } else {
           for (uint32_t s = 0; s < N; ++s) {
-            const int o = off[s];
+            const int2 r = sr[s];
+            const int o = r.x;
             if (o < 0) continue;
-            const double A = (double)amp[s];
+            const double A = (double)__int_as_float(r.y);
             for (uint32_t j = lane; j < taps; j += 32) {
               const uint32_t k = (uint32_t)o + j;
               if (k < S) W[k] = fma(A, ker[j], W[k]);
@@ -387,9 +420,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
       __syncwarp();
       // maximum (all W >= 0)
-      double M = 0.0;
-      for (uint32_t k = lane; k < S; k += 32) M = fmax(M, W[k]);
-      M = warp_max_nonneg(M);
+      if (!have_max)
+        for (uint32_t k = lane; k < S; k += 32) Mlane = fmax(Mlane, W[k]);
+      const double M = warp_max_nonneg(Mlane);
       const double thr = (double)a.thr * M;
       // local maxima in time order (ballot over 32 consecutive bins)
       for (uint32_t b0 = 0; b0 < S && nret < a.max_returns; b0 += 32) {
@@ -408,10 +441,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           double bc = 0.0;
           uint32_t bs = 0xFFFFFFFFu;
           for (uint32_t s = lane; s < N; s += 32) {
-            const int o = off[s];
+            const int2 r = sr[s];
+            const int o = r.x;
             const int j = (int)kk - o;
             if (o < 0 || j < 0 || j >= (int)taps) continue;
-            const double c = (double)amp[s] * ker[j];
+            const double c = (double)__int_as_float(r.y) * ker[j];
             if (bs == 0xFFFFFFFFu || c > bc) {
               bc = c;
               bs = s;
@@ -438,11 +472,18 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
               a.fit_jobs[job] = fj;
             }
           }
-          if (lane == 0) {
+          const double range = 0.5 * kC *
+              ((double)((long long)k0 + (long long)kk - (long long)a.jstar) + 0.5) * a.delta_ns * 1e-9;
+          if (reg_ret) {
+            if (lane == nret) {
+              rr_range = range;
+              rr_int = (float)W[kk];
+              rr_prim = a.prim[p * N + bs];
+            }
+          } else if (lane == 0) {
             helios_return r;
-            r.range_m = 0.5 * kC * ((double)((long long)k0 + (long long)kk - (long long)a.jstar) + 0.5) *
-                        a.delta_ns * 1e-9;
-            r.gps_time_s = a.time_s ? a.time_s[p] : 0.0;
+            r.range_m = range;
+            r.gps_time_s = tsec;
             r.intensity = (float)W[kk];
             r.prim_id = a.prim[p * N + bs];
             r.return_number = (uint8_t)(nret + 1);
@@ -456,14 +497,30 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
     }
     __syncwarp();
-    // return slots: patch the count, zero the unused ones
-    for (uint32_t r = lane; r < a.max_returns; r += 32) {
-      if (r < nret) {
-        slots[r].n_returns = (uint8_t)nret;
-      } else {
-        double2* q = reinterpret_cast<double2*>(slots + r);
-        q[0] = make_double2(0.0, 0.0);
-        q[1] = make_double2(0.0, 0.0);
+    // return slots: the used ones with their count, the unused ones zeroed
+    if (reg_ret) {
+      const double t_ret = __shfl_sync(kFull, tsec, 0);
+      if (lane < a.max_returns) {
+        uint4 w0 = make_uint4(0u, 0u, 0u, 0u), w1 = w0;
+        if (lane < nret) {
+          // {range_m, gps_time_s} {intensity, prim_id, (number, count, 0, 0), echo width NaN}
+          w0 = make_uint4((uint32_t)__double2loint(rr_range), (uint32_t)__double2hiint(rr_range),
+                          (uint32_t)__double2loint(t_ret), (uint32_t)__double2hiint(t_ret));
+          w1 = make_uint4(__float_as_uint(rr_int), rr_prim, (lane + 1u) | (nret << 8), 0x7fc00000u);
+        }
+        uint4* q = reinterpret_cast<uint4*>(slots + lane);
+        q[0] = w0;
+        q[1] = w1;
+      }
+    } else {
+      for (uint32_t r = lane; r < a.max_returns; r += 32) {
+        if (r < nret) {
+          slots[r].n_returns = (uint8_t)nret;
+        } else {
+          double2* q = reinterpret_cast<double2*>(slots + r);
+          q[0] = make_double2(0.0, 0.0);
+          q[1] = make_double2(0.0, 0.0);
+        }
       }
     }
     if (lane == 0) {
@@ -472,7 +529,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
     }
     if (a.counters) {
       unsigned h = 0;
-      for (uint32_t s = lane; s < N; s += 32) h += (off[s] != -1);
+      for (uint32_t s = lane; s < N; s += 32) h += (sr[s].x != -1);
       h = __reduce_add_sync(kFull, h);
       if (lane == 0) {
         atomicAdd(a.counters + 0, (unsigned long long)h);
@@ -507,7 +564,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         __stcs(body + q, v);
       }
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint32_t q = qs + lane; q < nvec; q += 32) __stcs(body + q, z4);
+      uint32_t q = qs + lane;
+      for (; q + 96 < nvec; q += 128) {
+        __stcs(body + q, z4);
+        __stcs(body + q + 32, z4);
+        __stcs(body + q + 64, z4);
+        __stcs(body + q + 96, z4);
+      }
+      for (; q < nvec; q += 32) __stcs(body + q, z4);
       const uint32_t t0 = head + 4 * nvec;
       if (t0 + lane < nb) row[t0 + lane] = t0 + lane < S ? (float)W[t0 + lane] : 0.0f;
     }
@@ -546,7 +610,15 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
     return pl;
   }
   pl.grid = (uint32_t)(sms * per_sm);
-  pl.scratch_bytes = sizeof(double) * (size_t)pl.grid * warps * n_bins;
+  // wide pulses (support > kWCap bins) keep their row in a per-warp global
+  // scratch row of n_bins doubles; for very long windows the persistent grid
+  // is reduced so that scratch stays within kScratchCap (K7 stays correct,
+  // only its parallelism shrinks)
+  constexpr size_t kScratchCap = 512ull << 20;
+  const size_t per_block = sizeof(double) * (size_t)warps * n_bins;
+  if ((size_t)pl.grid * per_block > kScratchCap)
+    pl.grid = (uint32_t)std::max<size_t>(1, kScratchCap / per_block);
+  pl.scratch_bytes = per_block * pl.grid;
   return pl;
 }
 

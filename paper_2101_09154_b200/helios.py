@@ -33,7 +33,8 @@ EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helio
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
             "helios_pulse_taps", "helios_simulate", "helios_simulate_batches",
             "helios_simulate_survey", "helios_get_tuning", "helios_set_tuning",
-            "helios_util_sort_pairs_u64", "helios_util_scan_u64")
+            "helios_util_sort_pairs_u64", "helios_util_scan_u64",
+            "helios_util_fp64_fma_tflops")
 
 
 class HeliosError(RuntimeError):
@@ -96,7 +97,9 @@ class helios_stats(ctypes.Structure):
                                      "returns", "nodes_visited", "tris_tested", "voxel_steps",
                                      "fp64_tests")] +
                 [("trace_ms", _d), ("waveform_ms", _d), ("beam_nodes", _u64), ("beam_ms", _d),
-                 ("batches", _u32), ("chunks", _u32)])
+                 ("batches", _u32), ("chunks", _u32), ("warp_entries", _u64),
+                 ("warp_entries_walked", _u64), ("warp_steps", _u64), ("warp_leaf_tris", _u64),
+                 ("warp_fp64_in_walk", _u64), ("second_definite_hits", _u64)])
 
 
 class helios_tuning(ctypes.Structure):
@@ -164,6 +167,8 @@ def lib() -> ctypes.CDLL:
         L.helios_set_tuning.argtypes = [ctypes.POINTER(helios_tuning)]
         L.helios_util_sort_pairs_u64.restype = ctypes.c_int
         L.helios_util_sort_pairs_u64.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp]
+        L.helios_util_fp64_fma_tflops.restype = ctypes.c_int
+        L.helios_util_fp64_fma_tflops.argtypes = [ctypes.POINTER(_d), _vp]
         L.helios_util_scan_u64.restype = ctypes.c_int
         L.helios_util_scan_u64.argtypes = [_vp, _vp, _u64, ctypes.c_int, _vp]
         _lib = L
@@ -294,6 +299,15 @@ def util_scan_u64(src, dst, inclusive: bool = True, stream=None) -> None:
     if rc:
         raise HeliosError(HELIOS_ERR_CUDA if rc == 3 else HELIOS_ERR_INVALID_ARGUMENT,
                           f"helios_util_scan_u64 returned {rc}")
+
+
+def util_fp64_fma_tflops(stream=None) -> float:
+    """Measured device fp64 FMA throughput (TFLOP/s)."""
+    v = _d()
+    rc = lib().helios_util_fp64_fma_tflops(ctypes.byref(v), _stream(stream))
+    if rc:
+        raise HeliosError(HELIOS_ERR_CUDA, f"helios_util_fp64_fma_tflops returned {rc}")
+    return v.value
 
 
 def helios_simulate_survey(scene: int, params: helios_scanner_params, survey: helios_survey,
@@ -524,7 +538,15 @@ def simulate_batches(scene: Scene, params, batches, outputs, stream=None, stats:
     st = helios_stats() if (stats or counters) else None
     if st is not None:
         st.collect_counters = 1 if counters else 0
-    helios_simulate_batches(scene.handle, hp, ps, os_, stream, st)
+    try:
+        helios_simulate_batches(scene.handle, hp, ps, os_, stream, st)
+    except HeliosError as err:
+        if err.status != HELIOS_ERR_CAPACITY:
+            raise
+        # grow every batch's packed buffer that was too small, run again
+        for out, o in zip(outputs, os_):
+            _grow_packed(out, o)
+        helios_simulate_batches(scene.handle, hp, ps, os_, stream, st)
     del keep
     return st
 
@@ -580,24 +602,30 @@ def _run_with_capacity_retry(call, outputs, o):
     except HeliosError as err:
         if err.status != HELIOS_ERR_CAPACITY:
             raise
-        import torch
-        pin = lambda t: bool(getattr(t, "is_pinned", lambda: False)())
-        if outputs.wf_compact is not None and int(outputs.wf_offset[-1]) > o.wf_compact_capacity:
-            need = int(outputs.wf_offset[-1])
-            old = outputs.wf_compact
-            outputs.wf_compact = torch.empty(need, dtype=torch.float32, device=old.device,
-                                             pin_memory=pin(old))
-            o.p_wf_compact = _ptr(outputs.wf_compact)
-            o.wf_compact_capacity = need
-        if (outputs.returns_packed is not None and
-                int(outputs.return_offset[-1]) > o.returns_capacity):
-            need = int(outputs.return_offset[-1])
-            old = outputs.returns_packed
-            outputs.returns_packed = torch.empty((need, 32), dtype=torch.uint8, device=old.device,
-                                                 pin_memory=pin(old))
-            o.p_returns_packed = _ptr(outputs.returns_packed)
-            o.returns_capacity = need
+        _grow_packed(outputs, o)
         call()
+
+
+def _grow_packed(outputs, o):
+    """Grow the packed buffers of `outputs` whose offsets report more than
+    their capacity (after a HELIOS_ERR_CAPACITY call)."""
+    import torch
+    pin = lambda t: bool(getattr(t, "is_pinned", lambda: False)())
+    if outputs.wf_compact is not None and int(outputs.wf_offset[-1]) > o.wf_compact_capacity:
+        need = int(outputs.wf_offset[-1])
+        old = outputs.wf_compact
+        outputs.wf_compact = torch.empty(need, dtype=torch.float32, device=old.device,
+                                         pin_memory=pin(old))
+        o.p_wf_compact = _ptr(outputs.wf_compact)
+        o.wf_compact_capacity = need
+    if (outputs.returns_packed is not None and
+            int(outputs.return_offset[-1]) > o.returns_capacity):
+        need = int(outputs.return_offset[-1])
+        old = outputs.returns_packed
+        outputs.returns_packed = torch.empty((need, 32), dtype=torch.uint8, device=old.device,
+                                             pin_memory=pin(old))
+        o.p_returns_packed = _ptr(outputs.returns_packed)
+        o.returns_capacity = need
 
 
 def _marshal_outputs(outputs: Outputs) -> helios_outputs:

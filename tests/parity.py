@@ -284,9 +284,10 @@ def gpu_invariants(gpu: dict, max_returns: int, thr: float, params=None) -> list
     raw = ret.view(np.uint8).reshape(ret.shape[0], R, 32) if ret.dtype.itemsize == 32 else None
     if raw is not None and np.any(raw[~used].any(axis=-1)):
         errs.append("unused return slot not zeroed")
-    if wf is not None and params is not None:
-        # each return's bin (from its range, R12) is a local maximum >= thr * max
-        # of the stored fp32 row (>=: fp32 rounding may equalise neighbours)
+    if wf is not None and params is not None and not getattr(params, "range_noise_sd_m", 0.0):
+        # each return's bin (from its range, R12; without ranging noise) is a
+        # local maximum >= thr * max of the stored fp32 row (>=: fp32 rounding
+        # may equalise neighbours)
         js = jstar_of(params)
         half = 0.5 * C * params.bin_width_ns * 1e-9
         p_idx, r_idx = np.nonzero(used)

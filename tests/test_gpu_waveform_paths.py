@@ -112,8 +112,9 @@ def test_wide_support_in_global_scratch():
                     [-500, -500, -150.0], [500, 500, -150.0], [-500, 500, -150.0]])
     tris = np.concatenate([near[None], far.reshape(2, 3, 3)]).astype(np.float32)
     scene = Scene(tri_xyz=tris, tri_reflectance=np.float32([0.3, 0.6, 0.6]))
+    # the far echo is (150/10)^4 = 5e4 times weaker (Eq. 7, R^-4): a low threshold
     p = ScannerParams(subray_count=19, divergence_rad=0.05, max_returns=7,
-                      detection_threshold=0.001)
+                      detection_threshold=1e-6)
     g, r = _run(scene, p, o, d, 128)
     off = _offsets(g)
     assert off.max() + 46 > 512
