@@ -40,7 +40,8 @@ def main(rep, cfg, source, pulses=None):
     per = {}
     for r in rows[2:]:
         name = r[kn]
-        key = ("k_beam" if "k_beam<0>" in name else "k_trace" if name.startswith("k_trace<0,") or "k_trace<false" in name
+        key = ("k_beam" if ("k_beam<0>" in name or "k_beam<false>" in name)
+               else "k_trace" if ("k_trace<0," in name or "k_trace<false" in name)
                else "k_waveform" if "k_waveform" in name else None)
         if key is None or key in per:
             continue
