@@ -236,7 +236,10 @@ def run_ours(args):
         batches.append((to(o), to(d), to(t), start))
     dense = args.waveform == "dense"
     out_bytes = B * (4 * n_bins * dense + 32 * p.max_returns + 9)
-    M = max(1, min(args.steps, int(DENSE_OUT_BUDGET // max(1, out_bytes))))
+    # output sets the timed steps rotate through (one per batch of a call):
+    # --out-sets (default 2: a batch's outputs are overwritten two steps later,
+    # D-4 "outputs are overwritten per batch"), capped by the device budget
+    M = max(1, min(args.steps, args.out_sets, int(DENSE_OUT_BUDGET // max(1, out_bytes))))
     outs = [h.alloc_outputs(B, hp, device=dev, waveform=dense,
                             compact=args.waveform == "compact",
                             compact_capacity=B * n_bins if args.waveform == "compact" else None)
@@ -532,6 +535,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--waveform", default="dense", choices=["dense", "compact", "none"],
                     help="waveform output of the device-resident steps")
+    ap.add_argument("--out-sets", type=int, default=2,
+                    help="device output sets the timed steps rotate through (batches per call)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-packed", action="store_true",
                     help="skip the device-resident packed-output measurement")

@@ -457,6 +457,7 @@ void free_scene(helios_scene sc, cudaStream_t s) {
   cudaFreeAsync(sc->d_lut, s);
   cudaFreeAsync(sc->d_bricks, s);
   cudaFreeAsync(sc->bvh.tris, s);
+  cudaFreeAsync(sc->bvh.filt, s);
   cudaFreeAsync(sc->bvh.nodes, s);
   cudaStreamSynchronize(s);
 }
@@ -618,7 +619,7 @@ helios_status helios_scene_get_info(helios_scene sc, helios_scene_info* out) {
   out->max_depth = sc->bvh.max_depth;
   out->leaf_max = kLeafMax;
   out->node_bytes = (uint64_t)sc->bvh.n_nodes * sizeof(Node);
-  out->tri_bytes = (uint64_t)sc->n_tris * sizeof(TriRecord);
+  out->tri_bytes = 2ull * sc->n_tris * sizeof(TriRecord);  // exact + filter records
   out->grid_bytes = (uint64_t)sc->nx * sc->ny * sc->nz * sizeof(float);
   out->build_ms = sc->bvh.ms;
   return HELIOS_OK;
@@ -942,6 +943,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
 
   TraceArgs ta{};
   ta.tris = sc->bvh.tris;
+  ta.filt = sc->bvh.filt;
   ta.nodes = sc->bvh.nodes;
   ta.root = sc->bvh.root;
   ta.n_tris = sc->n_tris;

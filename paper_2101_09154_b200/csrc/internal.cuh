@@ -3,6 +3,9 @@
 // Layout in HBM (DESIGN.md s.6):
 //   triangles  : TriRecord[n_tris] in LBVH leaf order, 48 B = 3 x float4
 //                { v0.xyz, bits(original id) } { v1.xyz, reflectance } { v2.xyz, 0 }
+//   filter recs: TriRecord[n_tris], same order, 48 B: { v0.xyz, A B } { e1.xyz, A }
+//                { e2.xyz, B } (fp32 edges, A = |e1|_1, B = |e2|_1): the fp32
+//                Moller-Trumbore filter reads only these, the fp64 test the above
 //   nodes      : Node[n_tris - 1] child-pair nodes, 64 B = 4 x float4
 //                { c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y }
 //                { c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y }
@@ -100,6 +103,7 @@ static_assert(sizeof(SubrayConst) == 64, "SubrayConst layout");
 // Everything a trace launch needs, passed by value (kernel parameter space).
 struct TraceArgs {
   const TriRecord* tris;
+  const TriRecord* filt;   // filter records (BuildResult::filt)
   const Node* nodes;
   int32_t root;          // root node ref (internal index or leaf ref)
   uint32_t n_tris;
@@ -246,6 +250,10 @@ cudaError_t sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t n, int bits,
 // LBVH build (lbvh.cu)
 struct BuildResult {
   TriRecord* tris;   // device, leaf order
+  TriRecord* filt;   // device, leaf order: K6's fp32 filter record of each triangle
+                     // {v0.xyz, |e1|_1 |e2|_1} {e1.xyz, |e1|_1} {e2.xyz, |e2|_1},
+                     // e1 = v1 - v0, e2 = v2 - v0 rounded to fp32 (the values the
+                     // filter used to recompute per test, bit for bit)
   Node* nodes;       // device
   uint32_t n_nodes;
   int32_t root;

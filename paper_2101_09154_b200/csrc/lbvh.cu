@@ -252,7 +252,7 @@ __global__ void k_depth(int n, const int* __restrict__ range, const int* __restr
 
 __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict__ refl,
                           const uint32_t* __restrict__ sorted_idx, uint32_t n,
-                          TriRecord* __restrict__ out) {
+                          TriRecord* __restrict__ out, TriRecord* __restrict__ filt) {
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   uint32_t src = sorted_idx[k];
@@ -263,6 +263,18 @@ __global__ void k_permute(const float* __restrict__ xyz, const float* __restrict
   rec.b = make_float4(t[3], t[4], t[5], r);
   rec.c = make_float4(t[6], t[7], t[8], 0.0f);
   out[k] = rec;
+  // K6's filter record: the fp32 edges (correctly rounded differences, the
+  // same values the filter computed per test) and their 1-norms, summed in
+  // the filter's order
+  const float e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
+  const float e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
+  const float A = __fadd_rn(__fadd_rn(fabsf(e1x), fabsf(e1y)), fabsf(e1z));
+  const float B = __fadd_rn(__fadd_rn(fabsf(e2x), fabsf(e2y)), fabsf(e2z));
+  TriRecord f;
+  f.a = make_float4(t[0], t[1], t[2], __fmul_rn(A, B));
+  f.b = make_float4(e1x, e1y, e1z, A);
+  f.c = make_float4(e2x, e2y, e2z, B);
+  filt[k] = f;
 }
 
 // ---- PLOC (parallel locally-ordered clustering, Meister & Bittner 2018) ----
@@ -450,6 +462,7 @@ cudaError_t dalloc(T** p, size_t count, cudaStream_t s) {
 cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int builder,
                        cudaStream_t s, BuildResult* out, char* err, size_t err_len) {
   out->tris = nullptr;
+  out->filt = nullptr;
   out->nodes = nullptr;
   out->n_nodes = 0;
   out->root = kEmptyRef;
@@ -501,6 +514,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
   CK(dalloc(&codes, n, s));
   CK(dalloc(&idx, n, s));
   CK(dalloc(&out->tris, n, s));
+  CK(dalloc(&out->filt, n, s));
   k_centroid_bounds<<<min(nb, 148u * 8u), T, 0, s>>>(xyz, n, bounds);
   CK(cudaGetLastError());
   k_morton<<<nb, T, 0, s>>>(xyz, n, bounds, codes, idx, bits, isotropic);
@@ -614,7 +628,8 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
     out->n_nodes = n - 1;
     out->root = 0;
   }
-  k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s_final ? idx_s_final : idx_s, n, out->tris);
+  k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s_final ? idx_s_final : idx_s, n, out->tris,
+                              out->filt);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
@@ -658,8 +673,10 @@ done:
   if (e1) cudaEventDestroy(e1);
   if (e != cudaSuccess) {
     cudaFreeAsync(out->tris, s);
+    cudaFreeAsync(out->filt, s);
     cudaFreeAsync(out->nodes, s);
     out->tris = nullptr;
+    out->filt = nullptr;
     out->nodes = nullptr;
   }
   cudaStreamSynchronize(s);

@@ -116,6 +116,22 @@ __device__ __forceinline__ double mt64(const D3& o, const D3& d, const TriRecord
   return t > 0.0 ? t : -1.0;
 }
 
+// t of a hit the fp32 filter certified (mt32_classify == 2: |det|, u, v,
+// 1 - u - v and t each beyond its forward-error bound, so the oracle's fp64
+// test accepts it: its degeneracy cut |det| <= 1e-12 |e1||e2| lies far below
+// the filter's det bound 32u |d|_1 |e1|_1 |e2|_1, and u, v keep their signs),
+// by the oracle's own operations for t: det = e1.(d x e2), q = s x e1,
+// t = (e2.q) / det -- bitwise mt64's t, without the tests it cannot fail.
+__device__ __forceinline__ double mt64_t(const D3& o, const D3& d, const TriRecord& tr) {
+  const D3 v0 = d3(tr.a.x, tr.a.y, tr.a.z);
+  const D3 e1 = sub(d3(tr.b.x, tr.b.y, tr.b.z), v0);
+  const D3 e2 = sub(d3(tr.c.x, tr.c.y, tr.c.z), v0);
+  const double det = dot(e1, cross(d, e2));
+  const double inv = __drcp_rn(det);
+  const D3 q = cross(sub(o, v0), e1);
+  return mul(dot(e2, q), inv);
+}
+
 // fp32 prefilter.  Returns true only when the triangle is DEFINITELY not a
 // candidate (a miss of the fp64 test, or a hit farther than t_hi); otherwise
 // the fp64 test above decides.  Forward-error argument: e1, e2, s are
@@ -140,7 +156,7 @@ __device__ __forceinline__ float l1(F3 a) { return fabsf(a.x) + fabsf(a.y) + fab
 // A definite hit's fp64 evaluation can wait: its interval already bounds the
 // ray's nearest hit from above (packet traversal, deferred decision).
 __device__ __forceinline__ int mt32_classify(const F3& o, const F3& d, float dl1,
-                                             const TriRecord& tr, float t_hi, float& tlo,
+                                             const TriRecord& fr, float t_hi, float& tlo,
                                              float& tup) {
   // the bounds of mt32_definite_miss, factored as (kU |d|_1)(|e1|_1 |e2|_1)
   // etc., and tested as soon as each value exists (the coherent lanes of a
@@ -150,12 +166,15 @@ __device__ __forceinline__ int mt32_classify(const F3& o, const F3& d, float dl1
 #define HELIOS_FILTER_U 32.0f
 #endif
   constexpr float kU = HELIOS_FILTER_U * 5.9604645e-8f;
-  const F3 v0 = {tr.a.x, tr.a.y, tr.a.z};
-  const F3 e1 = fsub({tr.b.x, tr.b.y, tr.b.z}, v0);
-  const F3 e2 = fsub({tr.c.x, tr.c.y, tr.c.z}, v0);
+  // the filter record (lbvh.cu k_permute): v0, the fp32 edges e1 = v1 - v0,
+  // e2 = v2 - v0 (correctly rounded differences), A = |e1|_1, B = |e2|_1, A B
+  // -- the values this filter used to compute per test, bit for bit
+  const F3 v0 = {fr.a.x, fr.a.y, fr.a.z};
+  const F3 e1 = {fr.b.x, fr.b.y, fr.b.z};
+  const F3 e2 = {fr.c.x, fr.c.y, fr.c.z};
   const F3 sv = fsub(o, v0);
-  const float A = l1(e1), B = l1(e2), S = l1(sv);
-  const float kd = kU * dl1, AB = A * B;
+  const float A = fr.b.w, B = fr.c.w, S = l1(sv);
+  const float kd = kU * dl1, AB = fr.a.w;
   const F3 p = fcross(d, e2);
   const float det = fdot(e1, p);
   const float err_det = kd * AB;
@@ -351,10 +370,10 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
       if (mine) {
         const uint32_t first = leaf_first(ref), cnt = leaf_count(ref);
         for (uint32_t k = first; k < first + cnt; ++k) {
-          const TriRecord tr = load_tri(a.tris, k);
+          const TriRecord fr = load_tri(a.filt, k);
           if (INSTR) ++c_tris;
           float tlo, tup;
-          const int cls = mt32_classify(O32, D32, dl1, tr, hs.bound, tlo, tup);
+          const int cls = mt32_classify(O32, D32, dl1, fr, hs.bound, tlo, tup);
           if (cls == 0) continue;
           // a definite hit is deferred when it is the first, or surely nearer
           // than the deferred one (which then cannot be the nearest)
@@ -370,6 +389,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
             if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) ++wc[4];
             wc[5] += cls == 2;  // a second definite hit, not surely nearer
           }
+          const TriRecord tr = load_tri(a.tris, k);  // the exact vertices and id
           const double t = mt64(O, D, tr);
           if (t > 0.0) {
             take_hit(hs, t, __float_as_uint(tr.a.w), k);
@@ -753,7 +773,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
           if (hs.def_k != kNoTri) {
             const TriRecord tr = load_tri(a.tris, hs.def_k);
             if (INSTR) ++c_f64;
-            const double t = mt64(O, D, tr);
+            const double t = mt64_t(O, D, tr);
             if (t > 0.0) take_hit(hs, t, __float_as_uint(tr.a.w), hs.def_k);
           }
           t_best = hs.t_best;
