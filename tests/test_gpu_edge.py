@@ -331,3 +331,30 @@ def test_lane_order_and_padding_are_bitwise_invariant(name, scale, start, count)
                     continue
                 for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
                     assert np.array_equal(ref[k].view(np.uint8), g[k].view(np.uint8)), (k, beam, order, pad)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,scale", [("C2", 1.0), ("C3", 1.0), ("C5", 1.0), ("C4", 1.0)])
+def test_karras_and_ploc_trees_give_bitwise_identical_results(cfg, scale):
+    """The nearest hit is the minimum over every triangle, exact ties
+    -> lower id (R22), so the result cannot depend on the hierarchy: the Karras
+    LBVH (helios_tuning.builder = 1) and PLOC trees of the FULL BASELINE
+    scenes (0.5 M / 4.2 M / 49.8 M triangles) must give bitwise equal outputs
+    on a stretch of each config's own pulses."""
+    import paper_2101_09154_b200 as h
+    torch = torch_cuda()
+    w = workload(cfg, scale)
+    n = min(50_000, w.n_pulses)
+    start = w.n_pulses // 2
+    o, d, t = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in w.pulses(start, n))
+    res, depth = [], []
+    for builder in (1, 0):
+        with h.tuning(builder=builder):
+            sc = h.Scene.from_workload_scene(w.scene)
+        depth.append(sc.info().max_depth)
+        out, _ = h.simulate(sc, w.params, o, d, t, pulse_index_base=start, subray_hits=True)
+        res.append(out.numpy())
+        sc.destroy()
+    for k in ("n_returns", "wf_first_bin", "waveform", "returns", "subray_hits"):
+        assert np.array_equal(np.ascontiguousarray(res[0][k]).view(np.uint8),
+                              np.ascontiguousarray(res[1][k]).view(np.uint8)), (k, depth)
