@@ -383,7 +383,10 @@ def run_ours(args):
                     hout = houts[k]
                     d2h[0] += B * (1 + 8) + 16 * (B + 1) + 32 * int(hout.return_offset[-1]) + \
                         4 * int(hout.wf_offset[-1])
-        h.simulate_batches(scene, hp, hb_in[:1], houts[:1])
+        # untimed warm-up over every host batch and output set: the first DMA
+        # to / from a freshly pinned buffer costs a one-time mapping (C3: 11.8
+        # vs 5.5 ms per step, tools/e2e_repro.py), and packed capacities grow
+        run_e2e()
         ems, _ = timed(run_e2e)
         e2e = {"value": subrays / (ems / 1e3) / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": B * (12 + 12 + 8), "d2h_bytes_per_step": d2h[0] // args.steps,
