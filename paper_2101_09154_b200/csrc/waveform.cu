@@ -34,12 +34,18 @@
 namespace helios {
 namespace {
 
-constexpr int kMaxWarps = 8;
+#ifndef HELIOS_WAVE_WARPS
+#define HELIOS_WAVE_WARPS 8
+#endif
+#ifndef HELIOS_K7_PREFETCH
+#define HELIOS_K7_PREFETCH 1  // next pulse's records loaded while this pulse is binned
+#endif
+constexpr int kMaxWarps = HELIOS_WAVE_WARPS;
 #ifndef HELIOS_WAVE_WCAP
 #define HELIOS_WAVE_WCAP 512
 #endif
 #ifndef HELIOS_WAVE_MIN_BLOCKS
-#define HELIOS_WAVE_MIN_BLOCKS 5
+#define HELIOS_WAVE_MIN_BLOCKS 4
 #endif
 constexpr int kWCap = HELIOS_WAVE_WCAP;  // fp64 bins per warp in shared memory
 constexpr int kAggCap = 64;   // offset groups handled by the grouped path
@@ -264,17 +270,41 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
   __syncthreads();
 
-  for (uint64_t p = (uint64_t)blockIdx.x * nw + warp; p < a.n_pulses;
-       p += (uint64_t)gridDim.x * nw) {
+  // software pipelining (N <= 96, every configured beam but C5's 93/96-lane
+  // variants fit): the records of the warp's next pulse are loaded into
+  // registers while this pulse is binned, so their DRAM latency is hidden
+  const uint64_t stride = (uint64_t)gridDim.x * nw;
+  const bool pf = HELIOS_K7_PREFETCH && N <= 96;
+  int2 nx0 = make_int2(-1, 0), nx1 = nx0, nx2 = nx0;
+  auto fetch = [&](uint64_t q) {
+    const int2* rq = reinterpret_cast<const int2*>(a.rec + q * N);
+    nx0 = (uint32_t)lane < N ? __ldcs(rq + lane) : make_int2(-1, 0);
+    nx1 = (uint32_t)lane + 32 < N ? __ldcs(rq + lane + 32) : make_int2(-1, 0);
+    nx2 = (uint32_t)lane + 64 < N ? __ldcs(rq + lane + 64) : make_int2(-1, 0);
+  };
+  const uint64_t p_first = (uint64_t)blockIdx.x * nw + warp;
+  if (pf && p_first < a.n_pulses) fetch(p_first);
+  for (uint64_t p = p_first; p < a.n_pulses; p += stride) {
     const int2* rec = reinterpret_cast<const int2*>(a.rec + p * N);
     // the pulse's time is needed only by its returns: load it early
     const double tsec = (a.time_s && lane == 0) ? a.time_s[p] : 0.0;
     // pass 1: records -> shared memory (read once, streaming), k0 = min k_s
     int kmin = INT_MAX;
-    for (uint32_t s = lane; s < N; s += 32) {
-      const int2 r = __ldcs(rec + s);
-      sr[s] = r;
-      if (r.x >= 0) kmin = min(kmin, r.x);
+    if (pf) {
+      const int2 c0 = nx0, c1 = nx1, c2 = nx2;
+      if (p + stride < a.n_pulses) fetch(p + stride);
+      if ((uint32_t)lane < N) sr[lane] = c0;
+      if ((uint32_t)lane + 32 < N) sr[lane + 32] = c1;
+      if ((uint32_t)lane + 64 < N) sr[lane + 64] = c2;
+      if (c0.x >= 0) kmin = c0.x;
+      if (c1.x >= 0) kmin = min(kmin, c1.x);
+      if (c2.x >= 0) kmin = min(kmin, c2.x);
+    } else {
+      for (uint32_t s = lane; s < N; s += 32) {
+        const int2 r = __ldcs(rec + s);
+        sr[s] = r;
+        if (r.x >= 0) kmin = min(kmin, r.x);
+      }
     }
     const int k0 = __reduce_min_sync(kFull, kmin);
     helios_return* slots = a.returns + p * a.max_returns;
