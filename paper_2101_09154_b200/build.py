@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhelios.so")
+DEBUG_LIB = os.path.join(HERE, "libhelios_debug.so")  # -DHELIOS_DEBUG: device invariant checks
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -31,6 +32,18 @@ def up_to_date() -> bool:
         return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(p) <= t for p in _deps())
+
+
+def build_debug(force: bool = False) -> str:
+    """libhelios_debug.so: the same sources with HELIOS_DEBUG (device-side
+    HELIOS_DASSERT checks of the kernels' invariants: traversal stack depth,
+    beam entry list bound, subray table index, waveform window, attribution);
+    load it with HELIOS_LIB to run any test or tool under the checks."""
+    if not force and os.path.exists(DEBUG_LIB):
+        t = os.path.getmtime(DEBUG_LIB)
+        if all(os.path.getmtime(p) <= t for p in _deps()):
+            return DEBUG_LIB
+    return build(force=True, defines=("HELIOS_DEBUG",), out=DEBUG_LIB)
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
@@ -68,5 +81,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
-                out=outs[0] if outs else None))
+    if "--debug" in sys.argv:
+        print(build_debug(force="--force" in sys.argv))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                    out=outs[0] if outs else None))

@@ -472,6 +472,7 @@ const char* helios_version(void) { return "helios-b200 0.2 sm_100a"; }
 
 helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream stream,
                                   helios_scene* out) {
+  helios::NvtxRange nvtx_("helios_scene_create");
   g_err.clear();
   if (!desc || !out) return fail(HELIOS_ERR_INVALID_ARGUMENT, "desc/out is NULL");
   *out = nullptr;
@@ -585,6 +586,7 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
 }
 
 helios_status helios_build_accel(helios_scene sc, helios_stream stream) {
+  helios::NvtxRange nvtx_("helios_build_accel");
   g_err.clear();
   if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
   if (sc->built) return HELIOS_OK;
@@ -697,6 +699,7 @@ enum Arr { A_ORIGIN = 0, A_DIR, A_TIME, A_NRET, A_RET, A_K0, A_WF, A_HITS, A_COU
 helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params,
                             const Job* jobs, uint32_t n_jobs, const helios_survey* survey,
                             uint64_t first_pulse, helios_stream stream, helios_stats* stats) {
+  NvtxRange nvtx_(survey ? "helios_simulate_survey" : (n_jobs > 1 ? "helios_simulate_batches" : "helios_simulate"));
   g_err.clear();
   if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
   if (!jobs || n_jobs == 0) return fail(HELIOS_ERR_INVALID_ARGUMENT, "no pulse batch given");
@@ -809,7 +812,11 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (beam || sc->d_pad != nullptr) {
       constexpr uint64_t kBeamChunkSubrays = 64ull << 20;
       uint64_t k = std::max<uint64_t>(2, (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
-      if (job_staged[j]) k = std::max<uint64_t>(k, 4);
+      // host staging: >= 4 chunks per batch so copies overlap compute within a
+      // single batch; a multi-batch call overlaps them across batches, and 2
+      // chunks per batch measured faster there (C5 e2e 12.67 -> 12.46 ms per
+      // 1 M pulses, tools/e2e_repro.py)
+      if (job_staged[j]) k = std::max<uint64_t>(k, n_jobs > 1 ? 2 : 4);
       chunk = std::max(chunk, (n + k - 1) / k);
     }
     if (tu.chunk_pulses >= 1024) chunk = std::min<uint64_t>(n, tu.chunk_pulses);
@@ -1160,6 +1167,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(ts, w_done[slot], 0);
     // K6 / K0 overwrite staged slot buffers chunk c-K copies out: wait for that
     if (e == cudaSuccess && any_staged && reuse) e = cudaStreamWaitEvent(ts, out_done[slot], 0);
+    NvtxRange nvtx_chunk("chunk: K0/K6a/K6 -> K7");
     if (e == cudaSuccess && gen) {
       e = launch_generate(sa, first_pulse + b, m, (float*)dev_ptr(A_ORIGIN, slot, ch),
                           (float*)dev_ptr(A_DIR, slot, ch), (double*)dev_ptr(A_TIME, slot, ch), ts);

@@ -15,13 +15,34 @@
 //   voxel grid : PAD float[nz][ny][nx] (x fastest).
 //   subray rec : helios_subray_hit[n_pulses][N] (16 B), K6 -> K7.
 #pragma once
+#include <assert.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include "../../include/helios.h"
 #include "../../include/helios_util.h"
 
 namespace helios {
+
+// NVTX ranges (header-only NVTX3: no cost unless a profiler is attached) around
+// the ABI calls, the build phases and each chunk's kernel launches, so a timeline shows K6a / K6 /
+// K7 / copies per chunk under the call that issued them
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// Device-side invariant checks of the debug build (build.py --debug ->
+// libhelios_debug.so, -DHELIOS_DEBUG): a failed check traps the kernel
+// (cudaErrorAssert); compiled out of the release library.
+#ifdef HELIOS_DEBUG
+#define HELIOS_DASSERT(x) assert(x)
+#else
+#define HELIOS_DASSERT(x) ((void)0)
+#endif
 
 // stream-ordered allocation from the library's private pool (api.cu)
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s);

@@ -515,12 +515,14 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
   CK(dalloc(&idx, n, s));
   CK(dalloc(&out->tris, n, s));
   CK(dalloc(&out->filt, n, s));
+  nvtxMarkA("build K1: centroid bounds + Morton codes");
   k_centroid_bounds<<<min(nb, 148u * 8u), T, 0, s>>>(xyz, n, bounds);
   CK(cudaGetLastError());
   k_morton<<<nb, T, 0, s>>>(xyz, n, bounds, codes, idx, bits, isotropic);
   CK(cudaGetLastError());
   temp_bytes = sort_temp_bytes(n);
   CK(dev_alloc(&temp, temp_bytes, s));
+  nvtxMarkA("build K2: radix sort");
   CK(sort_pairs_u64(codes, idx, n, 3 * bits, temp, temp_bytes, s));
   codes_s = codes;  // sorted in place
   idx_s = idx;
@@ -550,6 +552,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
     CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned), s));
     ptemp_bytes = scan_temp_bytes(n, sizeof(unsigned long long));
     CK(dev_alloc(&ptemp, ptemp_bytes, s));
+    nvtxMarkA("build K3: PLOC clustering");
     k_ploc_init<<<nb, T, 0, s>>>(xyz, idx_s, n, pcid, pbox, psize);
     CK(cudaGetLastError());
     {
@@ -615,6 +618,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
     CK(cudaMemsetAsync(flags, 0, sizeof(unsigned) * (n - 1), s));
     CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned), s));
     CK(dalloc(&out->nodes, n - 1, s));
+    nvtxMarkA("build K3: Karras hierarchy + refit");
     k_karras<<<ni, T, 0, s>>>(codes_s, (int)n, child, parent_int, parent_leaf, range);
     CK(cudaGetLastError());
     k_refit<<<nb, T, 0, s>>>(xyz, idx_s, (int)n, child, parent_int, parent_leaf, leafbox, nodebox,
@@ -628,6 +632,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
     out->n_nodes = n - 1;
     out->root = 0;
   }
+  nvtxMarkA("build K5: triangle records");
   k_permute<<<nb, T, 0, s>>>(xyz, refl, idx_s_final ? idx_s_final : idx_s, n, out->tris,
                               out->filt);
   CK(cudaGetLastError());

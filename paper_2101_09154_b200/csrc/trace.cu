@@ -433,6 +433,7 @@ __device__ __forceinline__ void traverse_packet(const TraceArgs& a, unsigned m, 
         }
       }
       ++sp;
+      HELIOS_DASSERT(sp <= kStackSize);  // the build checked depth <= kStackSize
       ref = near0 ? r0 : r1;
       m = near0 ? m0 : m1;
     } else if (m0) {
@@ -580,6 +581,7 @@ __global__ void __launch_bounds__(128) k_beam(const TraceArgs a) {
     const int32_t ref = stk[sp];
     // listed: final entries, leaves, and nodes whose children would not fit
     if (((emit >> sp) & 1u) || ref_is_leaf(ref) || cnt + sp + 2 > cap) {
+      HELIOS_DASSERT(cnt < kEntryMax);
       row[1 + cnt++] = make_int2(ref, __float_as_int(stt[sp]));
       continue;
     }
@@ -644,7 +646,7 @@ __device__ __forceinline__ void store_event(const TraceArgs& a, uint64_t slot, d
 #define HELIOS_TRACE_T 128  // K6 threads per block
 #endif
 #ifndef HELIOS_TRACE_MIN_BLOCKS
-#define HELIOS_TRACE_MIN_BLOCKS 8  // 64 registers: measured best (profiles/r01_regs_ab.txt)
+#define HELIOS_TRACE_MIN_BLOCKS 9  // 56 registers: measured best (profiles/r02_k6_regs_ab.txt; r01: 64 > 80)
 #endif
 // GRID: 0 no voxel grid, 1 transmissive voxels, 2 opaque / scaled cubes --
 // the A4 march is compiled in only where needed, so each scene kind keeps
@@ -665,7 +667,9 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
   // lane position j of the pulse -> subray s (the table is in K6's lane order,
   // each entry carries its index; the record goes to slot s)
   const uint32_t j = g32 - (uint32_t)p * NL;
+  HELIOS_DASSERT(j < NL);
   const SubrayConst sc = a.sub[j];
+  HELIOS_DASSERT(!in_range || sc.index < a.N);
   const uint32_t s = sc.index;
   const uint64_t slot = p * a.N + s;  // [pulse][subray] (R4 order) in every output
   unsigned long long c_nodes = 0, c_tris = 0, c_vox = 0, c_voxret = 0, c_f64 = 0;

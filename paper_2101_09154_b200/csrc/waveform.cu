@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       maxoff = __reduce_max_sync(kFull, maxoff);
       S = min(nb, (uint32_t)maxoff + taps);
       W = (S <= (uint32_t)kWCap) ? Ws : gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
+      HELIOS_DASSERT(maxoff >= 0 && maxoff < (int)nb && S >= 1 && S <= nb);
       __syncwarp();
       double Mlane = 0.0;  // this lane's maximum of W (grouped path: while computing W)
       bool have_max = false;
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         unsigned m = __ballot_sync(kFull, pk);
         while (m && nret < a.max_returns) {
           const uint32_t kk = b0 + (__ffs(m) - 1);
+        HELIOS_DASSERT(kk >= 1 && kk + 1 < nb && kk < S);
           m &= m - 1;
           // attribution (R13): largest contribution A_s p[kk - o_s], ties ->
           // lowest s: exact max over the warp, then the lowest s holding it
@@ -483,6 +485,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           }
           const double cmax = warp_max_nonneg(bs == 0xFFFFFFFFu ? 0.0 : bc);
           bs = __reduce_min_sync(kFull, (bs != 0xFFFFFFFFu && bc == cmax) ? bs : 0xFFFFFFFFu);
+        HELIOS_DASSERT(bs < N);  // a peak bin always has a contributor
           if (a.fit) {
             // echo-width job (R28): the echo's window, fitted later by k_fit
             int lo, hi;
