@@ -526,7 +526,10 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
   // radius 32 (default) or Karras (builder = 1)
   const int bits = kMortonBits, isotropic = 1;
   const bool use_ploc = builder != 1;
-  constexpr int ploc_r = 32;
+#ifndef HELIOS_PLOC_R
+#define HELIOS_PLOC_R 32
+#endif
+  constexpr int ploc_r = HELIOS_PLOC_R;
   int *pcid = nullptr, *pcid2 = nullptr, *pnn = nullptr, *pparent = nullptr;
   float *pbox = nullptr, *pbox2 = nullptr;
   uint32_t *psize = nullptr, *poff = nullptr, *pdepth = nullptr, *porder = nullptr;
