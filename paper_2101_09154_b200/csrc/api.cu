@@ -997,7 +997,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     for (const SubrayConst& t : tab) smax = std::max(smax, t.sin_t);
     ta.cone_sin = smax * (1.0 + 1e-9) + 1e-12;  // widened: covers the fp64 subray directions
 #ifndef HELIOS_BEAM_K
-#define HELIOS_BEAM_K 8.0
+#define HELIOS_BEAM_K 6.0
 #endif
     ta.beam_k = HELIOS_BEAM_K;  // measured (profiles/r01s3_beam_ab.txt, r02_beam_k_ab.txt)
   }
