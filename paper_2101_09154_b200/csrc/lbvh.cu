@@ -297,7 +297,7 @@ __device__ __forceinline__ float merged_area(const float* a, const float* b) {
 
 __global__ void k_ploc_init(const float* __restrict__ xyz, const uint32_t* __restrict__ sorted_idx,
                             uint32_t n, int* __restrict__ cid, float* __restrict__ cbox,
-                            uint32_t* __restrict__ size) {
+                            uint32_t* __restrict__ size, float* __restrict__ leafbox) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const Box b = tri_box(xyz, sorted_idx[k]);
@@ -307,6 +307,7 @@ __global__ void k_ploc_init(const float* __restrict__ xyz, const uint32_t* __res
     cbox[6ull * k + a] = b.lo[a];
     cbox[6ull * k + 3 + a] = b.hi[a];
   }
+  store_box(leafbox + 6ull * k, b);  // cluster k's triangle box (the collapse costs)
   size[k] = 1;
 }
 
@@ -392,10 +393,13 @@ __global__ void k_ploc_merge(const int* __restrict__ nn, uint32_t m,
 
 // top-down leaf offsets for the nodes created in one PLOC iteration (their
 // parents were created later, so are already placed); depth of kept nodes
+// node flags of the leaf collapse: the node is a leaf itself / lies inside one
+constexpr uint8_t kCollapsed = 1, kInside = 2;
+
 __global__ void k_ploc_offsets(uint32_t u0, uint32_t cnt, uint32_t n,
                                const int* __restrict__ child, const uint32_t* __restrict__ size,
                                uint32_t* __restrict__ off, uint32_t* __restrict__ depth,
-                               unsigned* __restrict__ max_depth) {
+                               uint8_t* __restrict__ nflag, unsigned* __restrict__ max_depth) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= cnt) return;
   const uint32_t u = u0 + t, v = n + u;
@@ -403,71 +407,78 @@ __global__ void k_ploc_offsets(uint32_t u0, uint32_t cnt, uint32_t n,
   const uint32_t o = off[v], d = depth[v];
   off[a] = o;
   off[b] = o + size[a];
-  depth[a] = d + 1;
-  depth[b] = d + 1;
-  // a kept pair is one more level (counted conservatively: every pair)
-  if (size[v] > 1u) atomicMax(max_depth, d);
+  const uint8_t f = nflag[u];
+  const bool emitted = !(f & (kCollapsed | kInside));
+  // depth = emitted internal nodes on the path (the traversal stack bound)
+  depth[a] = d + (emitted ? 1u : 0u);
+  depth[b] = d + (emitted ? 1u : 0u);
+  if (f & (kCollapsed | kInside)) {
+    if ((uint32_t)a >= n) nflag[a - n] |= kInside;
+    if ((uint32_t)b >= n) nflag[b - n] |= kInside;
+  }
+  if (emitted) atomicMax(max_depth, d);
 }
 
-__global__ void k_ploc_order(const uint32_t* __restrict__ sorted_idx, uint32_t n,
-                             const uint32_t* __restrict__ off, uint32_t* __restrict__ order,
-                             float* __restrict__ leafbox, const float* __restrict__ xyz) {
-  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  order[off[k]] = sorted_idx[k];
-  const Box b = tri_box(xyz, sorted_idx[k]);
-  store_box(leafbox + 6ull * k, b);
-}
-
-// Leaf collapse (surface-area heuristic on the two-triangle case): a cluster
-// of <= kLeafMax triangles becomes one leaf, except a pair whose boxes barely
-// overlap -- there a node step that culls one of the two beats testing both.
-// With a node step costing r C (C = one triangle test), splitting costs
-// C (r + (A0 + A1) / A) against 2 C for the leaf: collapse iff A0 + A1 >=
-// lambda A with lambda = 2 - r (surface areas).  lambda = 1.5 (r = 0.5)
-// measured best (C5 +3.6 %, C3 +7 % over always collapsing; 1.0 / 2.0 / 3.0
-// slower, profiles/r02_leaf_ab.txt).  Terrain and facade pairs (sharing an
-// edge) collapse, scattered leaves of a crown stay apart.
-#ifndef HELIOS_COLLAPSE_LAMBDA
-#define HELIOS_COLLAPSE_LAMBDA 1.5f
+// Leaf collapse by the surface-area heuristic, bottom-up (one launch per PLOC
+// iteration, in creation order, so the children's costs exist): with a
+// triangle test costing 1 and a node step r = HELIOS_SAH_NODE_COST,
+//   split(v) = r + (A0 cost(c0) + A1 cost(c1)) / A,   leaf(v) = size(v),
+// a cluster of <= kLeafMax triangles becomes one leaf iff leaf <= split, and
+// cost(v) = min of the two (a triangle costs 1).  For a pair this reads
+// A0 + A1 >= (2 - r) A: terrain and facade pairs (sharing an edge) share a
+// leaf, scattered crown leaves keep a node step each (profiles/r02_leaf_ab.txt).
+#ifndef HELIOS_SAH_NODE_COST
+#define HELIOS_SAH_NODE_COST 0.5f
 #endif
 __device__ __forceinline__ float half_area(const float* __restrict__ b) {
   const float dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
   return dx * dy + dy * dz + dz * dx;
 }
-__device__ __forceinline__ bool ploc_collapsed(int c, uint32_t n, const int* __restrict__ child,
-                                               const uint32_t* __restrict__ size,
-                                               const float* __restrict__ leafbox,
-                                               const float* __restrict__ nodebox) {
-  const uint32_t sz = size[c];
-  if (sz > (uint32_t)kLeafMax) return false;
-  if (sz != 2 || (uint32_t)c < n) return true;
-  const uint32_t u = (uint32_t)c - n;
-  const int a = child[2 * u], b = child[2 * u + 1];  // two triangles
-  return half_area(leafbox + 6ull * a) + half_area(leafbox + 6ull * b) >=
-         HELIOS_COLLAPSE_LAMBDA * half_area(nodebox + 6ull * u);
+__global__ void k_ploc_cost(uint32_t u0, uint32_t cnt, uint32_t n, const int* __restrict__ child,
+                            const uint32_t* __restrict__ size, const float* __restrict__ leafbox,
+                            const float* __restrict__ nodebox, float* __restrict__ cost,
+                            uint8_t* __restrict__ nflag) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const uint32_t u = u0 + t;
+  const int c[2] = {child[2 * u], child[2 * u + 1]};
+  float acc = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool tri = (uint32_t)c[i] < n;
+    const float a = half_area(tri ? leafbox + 6ull * c[i] : nodebox + 6ull * (c[i] - n));
+    acc += a * (tri ? 1.0f : cost[c[i] - n]);
+  }
+  const float A = half_area(nodebox + 6ull * u);
+  const float split = A > 0.0f ? HELIOS_SAH_NODE_COST + acc / A : INFINITY;
+  const uint32_t sz = size[n + u];
+  const bool leaf = sz <= (uint32_t)kLeafMax && (float)sz <= split;
+  cost[u] = leaf ? (float)sz : split;
+  nflag[u] = leaf ? kCollapsed : 0;
 }
 
-__device__ __forceinline__ int32_t ploc_ref(int c, uint32_t n, const int* __restrict__ child,
-                                            const uint32_t* __restrict__ size,
+__global__ void k_ploc_order(const uint32_t* __restrict__ sorted_idx, uint32_t n,
+                             const uint32_t* __restrict__ off, uint32_t* __restrict__ order) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  order[off[k]] = sorted_idx[k];
+}
+
+__device__ __forceinline__ int32_t ploc_ref(int c, uint32_t n, const uint32_t* __restrict__ size,
                                             const uint32_t* __restrict__ off,
-                                            const float* __restrict__ leafbox,
-                                            const float* __restrict__ nodebox) {
-  if (ploc_collapsed(c, n, child, size, leafbox, nodebox)) return leaf_ref(off[c], size[c]);
+                                            const uint8_t* __restrict__ nflag) {
+  if ((uint32_t)c < n) return leaf_ref(off[c], 1u);
+  if (nflag[c - n] & kCollapsed) return leaf_ref(off[c], size[c]);
   return (int32_t)((uint32_t)c - n);
 }
 
 __global__ void k_ploc_layout(uint32_t n, const int* __restrict__ child,
                               const uint32_t* __restrict__ size, const uint32_t* __restrict__ off,
                               const float* __restrict__ leafbox, const float* __restrict__ nodebox,
-                              Node* __restrict__ nodes) {
+                              const uint8_t* __restrict__ nflag, Node* __restrict__ nodes) {
   const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n - 1) return;
-  // inside a leaf: a collapsed cluster, or below one (every cluster of <=
-  // kLeafMax triangles under a collapsed one is itself collapsed or a pair)
-  if (size[n + u] <= (uint32_t)kLeafMax &&
-      (ploc_collapsed((int)(n + u), n, child, size, leafbox, nodebox) || size[n + u] != 2))
-    return;
+  if (nflag[u] & (kCollapsed | kInside)) return;  // a leaf, or inside one
   const int c0 = child[2 * u], c1 = child[2 * u + 1];
   const float* q0 = c0 < (int)n ? leafbox + 6ull * c0 : nodebox + 6ull * (c0 - n);
   const float* q1 = c1 < (int)n ? leafbox + 6ull * c1 : nodebox + 6ull * (c1 - n);
@@ -483,9 +494,8 @@ __global__ void k_ploc_layout(uint32_t n, const int* __restrict__ child,
   nd.xy0 = make_float4(b0[0], b0[3], b0[1], b0[4]);
   nd.xy1 = make_float4(b1[0], b1[3], b1[1], b1[4]);
   nd.z01 = make_float4(b0[2], b0[5], b1[2], b1[5]);
-  nd.ref = make_float4(__int_as_float(ploc_ref(c0, n, child, size, off, leafbox, nodebox)),
-                       __int_as_float(ploc_ref(c1, n, child, size, off, leafbox, nodebox)),
-                       0.0f, 0.0f);
+  nd.ref = make_float4(__int_as_float(ploc_ref(c0, n, size, off, nflag)),
+                       __int_as_float(ploc_ref(c1, n, size, off, nflag)), 0.0f, 0.0f);
   nodes[u] = nd;
 }
 
@@ -533,6 +543,8 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
   int *pcid = nullptr, *pcid2 = nullptr, *pnn = nullptr, *pparent = nullptr;
   float *pbox = nullptr, *pbox2 = nullptr;
   uint32_t *psize = nullptr, *poff = nullptr, *pdepth = nullptr, *porder = nullptr;
+  float* pcost = nullptr;
+  uint8_t* pnflag = nullptr;
   unsigned long long *pflags = nullptr, *pincl = nullptr;
   void* ptemp = nullptr;
   size_t ptemp_bytes = 0;
@@ -584,6 +596,8 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
     CK(dalloc(&poff, 2ull * n - 1, s));
     CK(dalloc(&pdepth, 2ull * n - 1, s));
     CK(dalloc(&porder, n, s));
+    CK(dalloc(&pcost, n - 1, s));
+    CK(dalloc(&pnflag, n - 1, s));
     CK(dalloc(&child, 2ull * (n - 1), s));
     CK(dalloc(&leafbox, 6ull * n, s));
     CK(dalloc(&nodebox, 6ull * (n - 1), s));
@@ -593,7 +607,7 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
     ptemp_bytes = scan_temp_bytes(n, sizeof(unsigned long long));
     CK(dev_alloc(&ptemp, ptemp_bytes, s));
     nvtxMarkA("build K3: PLOC clustering");
-    k_ploc_init<<<nb, T, 0, s>>>(xyz, idx_s, n, pcid, pbox, psize);
+    k_ploc_init<<<nb, T, 0, s>>>(xyz, idx_s, n, pcid, pbox, psize, leafbox);
     CK(cudaGetLastError());
     {
       uint32_t m = n, base = 0;
@@ -627,6 +641,12 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
         std::swap(pcid, pcid2);
         std::swap(pbox, pbox2);
       }
+      // leaf collapse costs, bottom-up: iterations in creation order
+      for (size_t t = 0; t < it_base.size(); ++t) {
+        k_ploc_cost<<<(it_cnt[t] + T - 1) / T, T, 0, s>>>(it_base[t], it_cnt[t], n, child,
+                                                         psize, leafbox, nodebox, pcost, pnflag);
+        CK(cudaGetLastError());
+      }
       // depth-first leaf offsets, top-down: iterations in reverse creation order
       const uint32_t root_v = n + (n - 2);
       const uint32_t one = 1, zero = 0;
@@ -634,13 +654,13 @@ cudaError_t build_lbvh(const float* xyz, const float* refl, uint32_t n, int buil
       CK(cudaMemcpyAsync(pdepth + root_v, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
       for (size_t t = it_base.size(); t-- > 0;) {
         k_ploc_offsets<<<(it_cnt[t] + T - 1) / T, T, 0, s>>>(it_base[t], it_cnt[t], n, child,
-                                                            psize, poff, pdepth, dmax);
+                                                            psize, poff, pdepth, pnflag, dmax);
         CK(cudaGetLastError());
       }
     }
-    k_ploc_order<<<nb, T, 0, s>>>(idx_s, n, poff, porder, leafbox, xyz);
+    k_ploc_order<<<nb, T, 0, s>>>(idx_s, n, poff, porder);
     CK(cudaGetLastError());
-    k_ploc_layout<<<ni, T, 0, s>>>(n, child, psize, poff, leafbox, nodebox, out->nodes);
+    k_ploc_layout<<<ni, T, 0, s>>>(n, child, psize, poff, leafbox, nodebox, pnflag, out->nodes);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&hdepth, dmax, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     out->n_nodes = n - 1;
@@ -713,6 +733,8 @@ done:
   cudaFreeAsync(poff, s);
   cudaFreeAsync(pdepth, s);
   cudaFreeAsync(porder, s);
+  cudaFreeAsync(pcost, s);
+  cudaFreeAsync(pnflag, s);
   cudaFreeAsync(ptemp, s);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
