@@ -850,6 +850,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   const size_t o_err = carve(sizeof(unsigned));
   const size_t o_cnt = carve(sizeof(unsigned long long) * 16);
   const size_t o_ws = carve(plan.scratch_bytes);
+  const size_t o_wlist = carve(sizeof(uint32_t) * chunk_max);  // K7 wide-pass list (one stream)
+  const size_t o_wcnt = carve(sizeof(unsigned));
   size_t o_wrec[kSlots], o_prim[kSlots], o_arr[A_COUNT][kSlots] = {}, o_ent[kSlots],
       o_frm[kSlots], o_fjob[kSlots], o_fy[kSlots], o_cst[kSlots], o_rst[kSlots];
   for (int k = 0; k < kSlots; ++k) {
@@ -1020,6 +1022,8 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
   wa.fit_stride = fit_stride;
   wa.err_flag = d_err;
   wa.seed = params->seed;
+  wa.wide_list = reinterpret_cast<uint32_t*>(buf + o_wlist);
+  wa.wide_count = reinterpret_cast<unsigned*>(buf + o_wcnt);
 
   // per-kernel device time (CUDA events on each kernel's stream)
   std::vector<cudaEvent_t> ev_b, ev_t, ev_w;
@@ -1252,7 +1256,7 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       ++launches;
     }
     mark(ev_w, ws);
-    ++launches;
+    launches += 2;  // K7 main + wide pass
     cudaStream_t post = ws;  // the stream that completes the chunk's returns
     if (e == cudaSuccess && fit) {
       // echo-width fits on their own stream (their tail overlaps later chunks)

@@ -205,6 +205,8 @@ struct WaveArgs {
   double noise_sd;               // ranging error sigma (R29), 0 = none
   uint64_t seed;                 // Philox key
   uint64_t pulse_base;           // global id of pulse 0 of this launch
+  uint32_t* wide_list;           // [n_pulses] pulses deferred to the wide pass (support > kWCap)
+  unsigned* wide_count;          // their count (zeroed by launch_waveform)
 };
 
 // On-device pulse generation (survey.cu; NEXT f2, R30).  Plain values copied
@@ -232,7 +234,8 @@ struct WavePlan {
   int warps;            // warps per block (0 = does not fit)
   size_t smem;          // dynamic shared memory per block
   uint32_t grid;        // persistent grid (SMs x occupancy)
-  size_t scratch_bytes; // per-warp global rows for wide pulses
+  size_t scratch_bytes; // per-warp global rows of the wide pass
+  uint32_t wide_grid;   // blocks of the wide pass
   uint32_t grid_cap;    // 0 = full persistent grid; else max blocks (overlap with K6)
 };
 WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);

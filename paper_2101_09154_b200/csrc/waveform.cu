@@ -18,12 +18,13 @@
 // into few distinct bin offsets o_s = k_s - k0 (coherent footprint), so the
 // amplitudes are first summed per offset group (each group in subray order),
 // then each lane computes its bins W[k] = sum_o A_o p[k - o] directly.  Pulses
-// whose offsets spread over >= kAggCap bins use match_any groups (or, past
-// kGroupCap groups, the per-subray accumulation).
+// whose offsets spread over >= kAggCap bins form match_any groups per 32-subray
+// chunk and add each group's shifted kernel into W, group after group.
 // The waveform window lives in a small per-warp shared-memory buffer; a pulse
-// whose support exceeds it (rare: a footprint spanning > kWCap - L_p bins)
-// uses a per-warp global scratch row.  Rows are stored as fp32 with 16-byte
-// vector stores (zeros outside the support).
+// whose support exceeds it (rare: a footprint spanning > kWCap - L_p bins) is
+// deferred to a second pass that keeps its row in a per-warp global scratch
+// row.  Rows are stored as fp32 with 16-byte vector stores (zeros outside the
+// support).
 #include <math.h>
 
 #include <algorithm>
@@ -49,7 +50,6 @@ constexpr int kMaxWarps = HELIOS_WAVE_WARPS;
 #endif
 constexpr int kWCap = HELIOS_WAVE_WCAP;  // fp64 bins per warp in shared memory
 constexpr int kAggCap = 64;   // offset groups handled by the grouped path
-constexpr int kGroupCap = kAggCap * 2 / 3;  // sparse groups (8 + 4 B) in the same space
 constexpr size_t kSmemCap = 200 * 1024;
 
 // Echo width ("Optionally, a Gaussian may be fitted to the resulting
@@ -249,101 +249,126 @@ __device__ __forceinline__ double warp_max_nonneg(double v) {
   return __hiloint2double((int)hmax, (int)lmax);
 }
 
+// offset of a record relative to the window anchor k0: -1 no event, -2
+// beyond maxFullwaveRange (discarded), else o_s = k_s - k0 < n_bins
+__device__ __forceinline__ int rec_offset(int k, unsigned k0u, uint32_t nb) {
+  const unsigned o = (unsigned)k - k0u;
+  return k < 0 ? -1 : (o < nb ? (int)o : -2);
+}
+
 // K7: one warp per pulse, persistent grid-stride loop.  Reads the pulse's
 // 8-B records (k_s, A_s) once, k0 = min k_s (one warp reduction), the
 // per-offset amplitude sums A_o (deterministic order), the support
-// W[k] = sum_o A_o p[k - o] (k < S = maxoff + L_p) in fp64 shared memory,
-// maximum, local maxima and returns, then the output row.
-__global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_waveform(const WaveArgs a,
-                                                             double* __restrict__ gscratch) {
+// W[k] = sum_o A_o p[k - o] (k < S = maxoff + L_p) in fp64, maximum, local
+// maxima and returns, then the output row.
+//
+// Two passes share this body.  The main pass (WIDE = false) keeps W in the
+// warp's shared-memory window of kWCap bins; a pulse whose support exceeds
+// it (C5: 0.8 % of pulses, roof edges over the ground) is appended to a list
+// and left untouched.  The wide pass (WIDE = true, launched right after on
+// the same stream) runs those pulses with W in a per-warp global scratch row.
+// Keeping the two apart lets the compiler address W as shared memory in the
+// main pass (LDS/STS, not generic loads).  R = ceil(N / 32) <= 3: records of
+// the next pulse prefetched into registers (R = 0: read in the loop, any N).  FIT: the echo-width jobs (R28) are
+// compiled in only where asked for (a smaller loop body for the usual case).
+template <bool WIDE, bool FIT, int R>
+__global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
+    k_waveform(const WaveArgs a, double* __restrict__ gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t N = a.N, nb = a.n_bins, taps = a.taps;
   const Layout L = layout_for(N, taps);
   double* ker = reinterpret_cast<double*>(smem_raw);
   double* base = ker + L.ker_d + (size_t)warp * L.per_warp_d;
-  double* Ws = base + L.w_off;
   double* agg = base + L.agg_off;
-  int2* sr = reinterpret_cast<int2*>(base + L.rec_off);  // {o_s (or k_s), bits of A_s}
+  int2* sr = reinterpret_cast<int2*>(base + L.rec_off);  // {o_s, bits of A_s}
   const unsigned kFull = 0xffffffffu;
 
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
   __syncthreads();
 
-  // software pipelining (N <= 96, every configured beam but C5's 93/96-lane
-  // variants fit): the records of the warp's next pulse are loaded into
-  // registers while this pulse is binned, so their DRAM latency is hidden
-  const uint64_t stride = (uint64_t)gridDim.x * nw;
-  const bool pf = HELIOS_K7_PREFETCH && N <= 96;
-  int2 nx0 = make_int2(-1, 0), nx1 = nx0, nx2 = nx0;
-  auto fetch = [&](uint64_t q) {
-    const int2* rq = reinterpret_cast<const int2*>(a.rec + q * N);
-    nx0 = (uint32_t)lane < N ? __ldcs(rq + lane) : make_int2(-1, 0);
-    nx1 = (uint32_t)lane + 32 < N ? __ldcs(rq + lane + 32) : make_int2(-1, 0);
-    nx2 = (uint32_t)lane + 64 < N ? __ldcs(rq + lane + 64) : make_int2(-1, 0);
+  const uint32_t gw = blockIdx.x * (uint32_t)nw + (uint32_t)warp;
+  const uint32_t stride = gridDim.x * (uint32_t)nw;
+  double* W = WIDE ? gscratch + (size_t)gw * nb : base + L.w_off;
+  const uint32_t count = WIDE ? *a.wide_count : (uint32_t)a.n_pulses;
+
+  // software pipelining (N <= 96: R = ceil(N / 32) records per lane): the
+  // records of the warp's next pulse are loaded into registers while this
+  // pulse is binned, so their DRAM latency is hidden (measured faster on C5
+  // than a cp.async double buffer in shared memory, profiles/r02_k7_rework_ab.txt)
+  constexpr int RR = R > 0 ? R : 1;
+  int2 nx[RR];
+  auto fetch = [&](uint32_t q) {
+    const int2* rq = reinterpret_cast<const int2*>(a.rec) + (size_t)q * N;
+#pragma unroll
+    for (int i = 0; i < RR; ++i)
+      nx[i] = (uint32_t)(lane + 32 * i) < N ? __ldcs(rq + lane + 32 * i) : make_int2(-1, 0);
   };
-  const uint64_t p_first = (uint64_t)blockIdx.x * nw + warp;
-  if (pf && p_first < a.n_pulses) fetch(p_first);
-  for (uint64_t p = p_first; p < a.n_pulses; p += stride) {
-    const int2* rec = reinterpret_cast<const int2*>(a.rec + p * N);
+  if (R > 0 && gw < count) fetch(gw);
+
+  for (uint32_t it = gw; it < count; it += stride) {  // @region prologue
+    const uint32_t p = WIDE ? a.wide_list[it] : it;
     // the pulse's time is needed only by its returns: load it early
     const double tsec = (a.time_s && lane == 0) ? a.time_s[p] : 0.0;
-    // pass 1: records -> shared memory (read once, streaming), k0 = min k_s
-    int kmin = INT_MAX;
-    if (pf) {
-      const int2 c0 = nx0, c1 = nx1, c2 = nx2;
-      if (p + stride < a.n_pulses) fetch(p + stride);
-      if ((uint32_t)lane < N) sr[lane] = c0;
-      if ((uint32_t)lane + 32 < N) sr[lane + 32] = c1;
-      if ((uint32_t)lane + 64 < N) sr[lane + 64] = c2;
-      if (c0.x >= 0) kmin = c0.x;
-      if (c1.x >= 0) kmin = min(kmin, c1.x);
-      if (c2.x >= 0) kmin = min(kmin, c2.x);
+    // records: k0 = min k_s over the events (a miss, k_s = -1, is the
+    // largest unsigned value), then o_s = k_s - k0 into shared memory
+    unsigned kmin = 0xFFFFFFFFu;  // @region records
+    int2 c[RR];
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) c[i] = nx[i];
+      if (it + stride < count) fetch(it + stride);
+#pragma unroll
+      for (int i = 0; i < R; ++i) kmin = min(kmin, (unsigned)c[i].x);
     } else {
+      const int2* rq = reinterpret_cast<const int2*>(a.rec) + (size_t)p * N;
       for (uint32_t s = lane; s < N; s += 32) {
-        const int2 r = __ldcs(rec + s);
+        const int2 r = __ldcs(rq + s);
         sr[s] = r;
-        if (r.x >= 0) kmin = min(kmin, r.x);
+        kmin = min(kmin, (unsigned)r.x);
       }
     }
-    const int k0 = __reduce_min_sync(kFull, kmin);
-    helios_return* slots = a.returns + p * a.max_returns;
-    float* row = a.waveform ? a.waveform + p * (uint64_t)nb : nullptr;
+    const unsigned k0u = __reduce_min_sync(kFull, kmin);
+    const bool any = k0u != 0xFFFFFFFFu;
+    int maxoff = 0;
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int o = rec_offset(c[i].x, k0u, nb);
+        maxoff = max(maxoff, o);
+        if ((uint32_t)(lane + 32 * i) < N) sr[lane + 32 * i] = make_int2(o, c[i].y);
+      }
+    } else {
+      for (uint32_t s = lane; s < N; s += 32) {
+        const int o = rec_offset(sr[s].x, k0u, nb);
+        maxoff = max(maxoff, o);
+        sr[s].x = o;
+      }
+    }
+    maxoff = __reduce_max_sync(kFull, maxoff);
+    const uint32_t S = any ? min(nb, (uint32_t)maxoff + taps) : 0u;
+    __syncwarp();
+    if (!WIDE && S > (uint32_t)kWCap) {
+      // the wide pass bins this pulse (and writes all its outputs)
+      if (lane == 0) a.wide_list[atomicAdd(a.wide_count, 1u)] = p;
+      continue;
+    }
+    helios_return* slots = a.returns + (size_t)p * a.max_returns;
+    float* row = a.waveform ? a.waveform + (size_t)p * nb : nullptr;
     // returns 0..31 are assembled in the registers of lane r and stored once
     // their count is known (one 32-B record per lane)
     const bool reg_ret = a.max_returns <= 32;
     double rr_range = 0.0;
     float rr_int = 0.0f;
     uint32_t rr_prim = 0;
-    uint32_t S = 0;
-    double* W = Ws;
     uint32_t nret = 0;
-    if (k0 != INT_MAX) {
-      // offsets within the window; beyond maxFullwaveRange -> discarded
-      int maxoff = 0;
-      for (uint32_t s = lane; s < N; s += 32) {
-        int o = sr[s].x;
-        if (o >= 0) {
-          o -= k0;
-          if (o >= (int)nb) o = -2;
-          else maxoff = max(maxoff, o);
-          sr[s].x = o;
-        }
-      }
-      maxoff = __reduce_max_sync(kFull, maxoff);
-      S = min(nb, (uint32_t)maxoff + taps);
-      W = (S <= (uint32_t)kWCap) ? Ws : gscratch + ((size_t)blockIdx.x * nw + warp) * nb;
+    if (any) {
       HELIOS_DASSERT(maxoff >= 0 && maxoff < (int)nb && S >= 1 && S <= nb);
-      __syncwarp();
       double Mlane = 0.0;  // this lane's maximum of W (grouped path: while computing W)
       bool have_max = false;
       if (maxoff < kAggCap) {
         have_max = true;
-        // amplitude per offset group.  Few groups (G <= 16, the usual case):
-        // lane (o, c) sums group o over subray chunk c of C = 32 / G chunks,
-        // then a fixed binary tree over the chunks combines the partials; else
-        // one lane per group over all subrays.  Either way a fixed order:
-        // deterministic.
+        // amplitude per offset group, in a fixed order (deterministic)  @region group_sums
         const int G = maxoff + 1;
         if (G <= 16) {
           // groups rounded up to G' = 2^lg <= 16 lanes: lane (o, c) = (lane mod
@@ -372,17 +397,26 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           }
           if (lane < G) agg[lane] = acc;
         } else {
-          for (int o = lane; o <= maxoff; o += 32) {
-            double acc = 0.0;
-            for (uint32_t s = 0; s < N; ++s) {
-              const int2 r = sr[s];
-              if (r.x == o) acc += (double)__int_as_float(r.y);
+          // 17..64 offsets: within each 32-subray chunk the lanes of equal
+          // offset (match_any); the lowest sums its members in subray order
+          // and adds the partial to its group's sum, chunk after chunk
+          for (int o = lane; o < G; o += 32) agg[o] = 0.0;
+          __syncwarp();
+          for (uint32_t c0 = 0; c0 < N; c0 += 32) {
+            const uint32_t s = c0 + lane;
+            const int2 r = s < N ? sr[s] : make_int2(-1, 0);
+            const unsigned peers = __match_any_sync(kFull, r.x);
+            if (r.x >= 0 && (peers & ((1u << lane) - 1u)) == 0u) {
+              double acc = (double)__int_as_float(r.y);
+              for (unsigned b = peers & (peers - 1u); b; b &= b - 1u)
+                acc += (double)__int_as_float(sr[c0 + __ffs(b) - 1].y);
+              agg[r.x] += acc;
             }
-            agg[o] = acc;
+            __syncwarp();
           }
         }
         __syncwarp();
-        // W[k] = sum_o A_o p[k - o], two fp64 chains per bin (even / odd
+        // W[k] = sum_o A_o p[k - o], two fp64 chains per bin (even / odd  @region W_grouped
         // offsets), the lane's running maximum on the way
         for (uint32_t k = lane; k < S; k += 32) {
           const int olo = max(0, (int)k - (int)taps + 1), ohi = min(maxoff, (int)k);
@@ -398,64 +432,53 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
           Mlane = fmax(Mlane, w);
         }
       } else {
-        // wide footprint (offsets spread over >= kAggCap bins, e.g. a crown and
+        // wide footprint (offsets spread over >= kAggCap bins, e.g. a crown and  @region wide
         // the ground below it).  Groups: within each 32-subray chunk the lanes
         // with equal offsets (match_any); the lowest lane sums its members in
-        // subray order.  Groups are kept in (chunk, lane) order and added one
-        // after the other: deterministic.  More than kGroupCap groups (or
-        // none fitting) -> per-subray accumulation in subray order.
-        double* gsum = agg;
-        int* goff = reinterpret_cast<int*>(agg + kGroupCap);
-        int G = 0;
+        // subray order; the chunk's groups are then added into W one after the
+        // other in lane order (broadcast by shuffles), chunk after chunk:
+        // deterministic, any number of groups.
+        for (uint32_t k = lane; k < S; k += 32) W[k] = 0.0;
+        // the lane's kernel taps j = lane, lane + 32 in registers (L_p <= 64)
+        const bool short_ker = taps <= 64;
+        const double kr0 = (uint32_t)lane < taps ? ker[lane] : 0.0;
+        const double kr1 = (uint32_t)lane + 32 < taps ? ker[lane + 32] : 0.0;
+        __syncwarp();
         for (uint32_t c0 = 0; c0 < N; c0 += 32) {
           const uint32_t s = c0 + lane;
           const int o = s < N ? sr[s].x : -1;
           const unsigned peers = __match_any_sync(kFull, o);
-          const bool lead = o >= 0 && (int)(__ffs(peers) - 1) == lane;
-          const unsigned leads = __ballot_sync(kFull, lead);
-          const int idx = G + __popc(leads & ((1u << lane) - 1u));
-          if (lead && idx < kGroupCap) {
-            double acc = 0.0;
+          const bool lead = o >= 0 && (peers & ((1u << lane) - 1u)) == 0u;
+          double acc = 0.0;
+          if (lead)
             for (unsigned b = peers; b; b &= b - 1u)
               acc += (double)__int_as_float(sr[c0 + __ffs(b) - 1].y);
-            gsum[idx] = acc;
-            goff[idx] = o;
-          }
-          G += __popc(leads);
-        }
-        for (uint32_t k = lane; k < S; k += 32) W[k] = 0.0;
-        __syncwarp();
-        if (G <= kGroupCap) {
-          for (int g = 0; g < G; ++g) {
-            const uint32_t o = (uint32_t)goff[g];
-            const double A = gsum[g];
-            for (uint32_t j = lane; j < taps; j += 32) {
-              const uint32_t k = o + j;
-              if (k < S) W[k] = fma(A, ker[j], W[k]);
-            }
-            __syncwarp();
-          }
-        } else {
-          for (uint32_t s = 0; s < N; ++s) {
-            const int2 r = sr[s];
-            const int o = r.x;
-            if (o < 0) continue;
-            const double A = (double)__int_as_float(r.y);
-            for (uint32_t j = lane; j < taps; j += 32) {
-              const uint32_t k = (uint32_t)o + j;
-              if (k < S) W[k] = fma(A, ker[j], W[k]);
+          for (unsigned leads = __ballot_sync(kFull, lead); leads; leads &= leads - 1u) {
+            const int src = __ffs(leads) - 1;
+            const double A = __shfl_sync(kFull, acc, src);
+            const uint32_t og = (uint32_t)__shfl_sync(kFull, o, src);
+            if (short_ker) {
+              const uint32_t k = og + lane;
+              if ((uint32_t)lane < taps && k < S) W[k] = fma(A, kr0, W[k]);
+              if ((uint32_t)lane + 32 < taps && k + 32 < S) W[k + 32] = fma(A, kr1, W[k + 32]);
+            } else {
+              for (uint32_t j = lane; j < taps; j += 32) {
+                const uint32_t k = og + j;
+                if (k < S) W[k] = fma(A, ker[j], W[k]);
+              }
             }
             __syncwarp();
           }
         }
       }
       __syncwarp();
-      // maximum (all W >= 0)
+      // maximum (all W >= 0)  @region max
       if (!have_max)
         for (uint32_t k = lane; k < S; k += 32) Mlane = fmax(Mlane, W[k]);
       const double M = warp_max_nonneg(Mlane);
       const double thr = (double)a.thr * M;
-      // local maxima in time order (ballot over 32 consecutive bins)
+      const int k0 = (int)k0u;
+      // local maxima in time order (ballot over 32 consecutive bins)  @region peaks_attr
       for (uint32_t b0 = 0; b0 < S && nret < a.max_returns; b0 += 32) {
         const uint32_t k = b0 + lane;
         bool pk = false;
@@ -466,7 +489,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
         unsigned m = __ballot_sync(kFull, pk);
         while (m && nret < a.max_returns) {
           const uint32_t kk = b0 + (__ffs(m) - 1);
-        HELIOS_DASSERT(kk >= 1 && kk + 1 < nb && kk < S);
+          HELIOS_DASSERT(kk >= 1 && kk + 1 < nb && kk < S);
           m &= m - 1;
           // attribution (R13): largest contribution A_s p[kk - o_s], ties ->
           // lowest s: exact max over the warp, then the lowest s holding it
@@ -477,16 +500,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
             const int o = r.x;
             const int j = (int)kk - o;
             if (o < 0 || j < 0 || j >= (int)taps) continue;
-            const double c = (double)__int_as_float(r.y) * ker[j];
-            if (bs == 0xFFFFFFFFu || c > bc) {
-              bc = c;
+            const double cc = (double)__int_as_float(r.y) * ker[j];
+            if (bs == 0xFFFFFFFFu || cc > bc) {
+              bc = cc;
               bs = s;
             }
           }
           const double cmax = warp_max_nonneg(bs == 0xFFFFFFFFu ? 0.0 : bc);
           bs = __reduce_min_sync(kFull, (bs != 0xFFFFFFFFu && bc == cmax) ? bs : 0xFFFFFFFFu);
-        HELIOS_DASSERT(bs < N);  // a peak bin always has a contributor
-          if (a.fit) {
+          HELIOS_DASSERT(bs < N);  // a peak bin always has a contributor
+          if (FIT) {
             // echo-width job (R28): the echo's window, fitted later by k_fit
             int lo, hi;
             echo_window(W, S, nb, (int)kk, a.fit_half, lo, hi);
@@ -498,7 +521,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
               y[i] = (uint32_t)(lo + i) < S ? W[lo + i] : 0.0;
             if (lane == 0) {
               FitJob fj;
-              fj.slot = (uint32_t)(p * a.max_returns + nret);
+              fj.slot = (uint32_t)((size_t)p * a.max_returns + nret);
               fj.lo = (int16_t)(lo - (int)kk);
               fj.n = (uint16_t)(hi - lo + 1);
               fj.peak = W[kk];
@@ -511,14 +534,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
             if (lane == nret) {
               rr_range = range;
               rr_int = (float)W[kk];
-              rr_prim = a.prim[p * N + bs];
+              rr_prim = a.prim[(size_t)p * N + bs];
             }
           } else if (lane == 0) {
             helios_return r;
             r.range_m = range;
             r.gps_time_s = tsec;
             r.intensity = (float)W[kk];
-            r.prim_id = a.prim[p * N + bs];
+            r.prim_id = a.prim[(size_t)p * N + bs];
             r.return_number = (uint8_t)(nret + 1);
             r.n_returns = 0;  // patched below once the count is known
             r.pad[0] = r.pad[1] = 0;
@@ -530,12 +553,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
     }
     __syncwarp();
-    // return slots: the used ones with their count, the unused ones zeroed
+    // return slots: the used ones with their count, the unused ones zeroed  @region returns
     if (reg_ret) {
       const double t_ret = __shfl_sync(kFull, tsec, 0);
-      if (lane < a.max_returns) {
+      if ((uint32_t)lane < a.max_returns) {
         uint4 w0 = make_uint4(0u, 0u, 0u, 0u), w1 = w0;
-        if (lane < nret) {
+        if ((uint32_t)lane < nret) {
           // {range_m, gps_time_s} {intensity, prim_id, (number, count, 0, 0), echo width NaN}
           w0 = make_uint4((uint32_t)__double2loint(rr_range), (uint32_t)__double2hiint(rr_range),
                           (uint32_t)__double2loint(t_ret), (uint32_t)__double2hiint(t_ret));
@@ -557,10 +580,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
     }
     if (lane == 0) {
-      a.first_bin[p] = (k0 == INT_MAX) ? -1 : (int64_t)k0;
+      a.first_bin[p] = any ? (int64_t)k0u : -1;
       a.n_returns[p] = (uint8_t)nret;
     }
-    if (a.counters) {
+    if (a.counters) {  // @region counters_compact
       unsigned h = 0;
       for (uint32_t s = lane; s < N; s += 32) h += (sr[s].x != -1);
       h = __reduce_add_sync(kFull, h);
@@ -579,11 +602,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS) k_wave
       }
     }
     if (row) {
-      // dense fp32 row: scalar head/tail, 16-byte streaming stores for the
+      // dense fp32 row: scalar head/tail, 16-byte streaming stores for the  @region row
       // aligned body (the support converted from W, then zeros)
       const uint32_t mis = (uint32_t)(((uintptr_t)row >> 2) & 3u);
       const uint32_t head = min(nb, (4u - mis) & 3u);
-      if (lane < head) row[lane] = lane < S ? (float)W[lane] : 0.0f;
+      if ((uint32_t)lane < head) row[lane] = (uint32_t)lane < S ? (float)W[lane] : 0.0f;
       const uint32_t nvec = (nb - head) >> 2;
       float4* body = reinterpret_cast<float4*>(row + head);
       const uint32_t qs = S > head ? min(nvec, (S - head + 3u) >> 2) : 0u;
@@ -633,9 +656,21 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaFuncSetAttribute(k_waveform, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)pl.smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waveform, warps * 32, pl.smem) !=
+  const void* kernels[] = {
+      (const void*)k_waveform<false, false, 0>, (const void*)k_waveform<false, false, 1>,
+      (const void*)k_waveform<false, false, 2>, (const void*)k_waveform<false, false, 3>,
+      (const void*)k_waveform<false, true, 0>,  (const void*)k_waveform<false, true, 1>,
+      (const void*)k_waveform<false, true, 2>,  (const void*)k_waveform<false, true, 3>,
+      (const void*)k_waveform<true, false, 0>,  (const void*)k_waveform<true, true, 0>};
+  for (const void* k : kernels)
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      pl.warps = 0;
+      return pl;
+    }
+  const int R = N <= 96 ? (int)((N + 31) / 32) : 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernels[R], warps * 32, pl.smem) !=
           cudaSuccess ||
       per_sm < 1) {
     cudaGetLastError();
@@ -643,15 +678,16 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
     return pl;
   }
   pl.grid = (uint32_t)(sms * per_sm);
-  // wide pulses (support > kWCap bins) keep their row in a per-warp global
-  // scratch row of n_bins doubles; for very long windows the persistent grid
-  // is reduced so that scratch stays within kScratchCap (K7 stays correct,
-  // only its parallelism shrinks)
+  // the wide pass (pulses whose support exceeds kWCap bins) keeps each
+  // warp's row in a global scratch row of n_bins doubles: one block per SM,
+  // fewer for very long windows so that scratch stays within kScratchCap
+  // (the pass stays correct, only its parallelism shrinks)
   constexpr size_t kScratchCap = 512ull << 20;
   const size_t per_block = sizeof(double) * (size_t)warps * n_bins;
-  if ((size_t)pl.grid * per_block > kScratchCap)
-    pl.grid = (uint32_t)std::max<size_t>(1, kScratchCap / per_block);
-  pl.scratch_bytes = per_block * pl.grid;
+  pl.wide_grid = (uint32_t)sms;
+  if ((size_t)pl.wide_grid * per_block > kScratchCap)
+    pl.wide_grid = (uint32_t)std::max<size_t>(1, kScratchCap / per_block);
+  pl.scratch_bytes = per_block * pl.wide_grid;
   return pl;
 }
 
@@ -722,12 +758,33 @@ cudaError_t launch_pack_returns(const helios_return* slots, const uint8_t* nr, u
 cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scratch,
                             cudaStream_t s) {
   if (a.n_pulses == 0) return cudaSuccess;
-  if (pl.warps == 0) return cudaErrorInvalidValue;
+  if (pl.warps == 0 || !a.wide_list || !a.wide_count) return cudaErrorInvalidValue;
   uint64_t want = (a.n_pulses + pl.warps - 1) / pl.warps;
   uint64_t grid = pl.grid;
   if (pl.grid_cap && pl.grid_cap < grid) grid = pl.grid_cap;
   if (want < grid) grid = want;
-  k_waveform<<<(unsigned)grid, pl.warps * 32, pl.smem, s>>>(a, scratch);
+  cudaError_t e = cudaMemsetAsync(a.wide_count, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  const unsigned g = (unsigned)grid, t = (unsigned)pl.warps * 32;
+  const int R = a.N <= 96 ? (int)((a.N + 31) / 32) : 0;
+  switch (R + (a.fit ? 4 : 0)) {
+    case 1: k_waveform<false, false, 1><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 2: k_waveform<false, false, 2><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 3: k_waveform<false, false, 3><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 4: k_waveform<false, true, 0><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 5: k_waveform<false, true, 1><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 6: k_waveform<false, true, 2><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 7: k_waveform<false, true, 3><<<g, t, pl.smem, s>>>(a, scratch); break;
+    default: k_waveform<false, false, 0><<<g, t, pl.smem, s>>>(a, scratch); break;
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // the pulses the main pass deferred (support > kWCap bins), same stream
+  const unsigned gw = (unsigned)std::min<uint64_t>(pl.wide_grid, want);
+  if (a.fit)
+    k_waveform<true, true, 0><<<gw, t, pl.smem, s>>>(a, scratch);
+  else
+    k_waveform<true, false, 0><<<gw, t, pl.smem, s>>>(a, scratch);
   return cudaGetLastError();
 }
 
