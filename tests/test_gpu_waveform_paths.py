@@ -2,10 +2,11 @@
 checked against the oracle (DESIGN.md s.7, waveform.cu):
 
   * offsets within 64 bins, <= 16 groups   -> chunked group sums (every config)
-  * offsets within 64 bins, > 16 groups    -> one lane per offset group
-  * offsets spread over >= 64 bins, <= 42 groups -> match_any groups
-  * > 42 groups                            -> per-subray accumulation
-  * support S > 512 bins                   -> the waveform row in global scratch
+  * offsets within 64 bins, > 16 groups    -> match_any group sums per 32-subray chunk
+  * offsets spread over >= 64 bins         -> match_any groups added into W one by one
+  * many such groups (61)                  -> the same path, no group cap
+  * support S > 512 bins                   -> deferred to the wide pass (global scratch row),
+                                              alone and mixed with ordinary pulses
 
 A "staircase" puts one tiny triangle on each subray's own direction at its
 own distance (placed with the oracle's subray_direction, pinned against the
@@ -81,7 +82,7 @@ def _offsets(g):
     return np.unique(k - k.min()).astype(int)
 
 
-def test_many_groups_within_64_bins_one_lane_per_group():
+def test_many_groups_within_64_bins_match_any_sums():
     # 37 subrays, distinct offsets 0..36 bins (0.15 m apart): G = 37 > 16, maxoff < 64
     g, _ = _staircase(37, 0.05, lambda s: 10.0 + 0.15 * s + 0.05)
     off = _offsets(g)
@@ -95,8 +96,8 @@ def test_spread_offsets_match_any_groups():
     assert 16 < len(off) <= 42 and off.max() >= 64
 
 
-def test_more_groups_than_the_group_cap_per_subray_accumulation():
-    # 61 distinct offsets (0.3 m apart): G = 61 > 42 groups
+def test_many_spread_groups_no_cap():
+    # 61 distinct offsets (0.3 m apart): G = 61 (the old kernel capped groups at 42)
     g, _ = _staircase(61, 0.05, lambda s: 10.0 + 0.3 * s)
     off = _offsets(g)
     assert len(off) > 42 and off.max() >= 64
@@ -119,3 +120,37 @@ def test_wide_support_in_global_scratch():
     off = _offsets(g)
     assert off.max() + 46 > 512
     assert (g["n_returns"] == 2).all()  # the near and the far echo
+
+
+def test_wide_pass_mixed_with_ordinary_pulses():
+    # alternate pulses see the near triangle over the far plane (support > 512
+    # bins: deferred to the wide pass) or the far plane alone (main pass): the
+    # deferral list must leave every other pulse to the main pass untouched
+    import paper_2101_09154_b200 as h
+    torch = torch_cuda()
+    near = np.array([[0.0, -5.0, -10.0], [5.0, -5.0, -10.0], [0.0, 5.0, -10.0]])
+    far = np.array([[-500, -500, -150.0], [500, -500, -150.0], [500, 500, -150.0],
+                    [-500, -500, -150.0], [500, 500, -150.0], [-500, 500, -150.0]])
+    tris = np.concatenate([near[None], far.reshape(2, 3, 3)]).astype(np.float32)
+    scene = Scene(tri_xyz=tris, tri_reflectance=np.float32([0.3, 0.6, 0.6]))
+    p = ScannerParams(subray_count=19, divergence_rad=0.05, max_returns=7,
+                      detection_threshold=1e-6)
+    n = 257
+    orig = np.zeros((n, 3), np.float32)
+    orig[1::2, 0] = 200.0  # odd pulses: beside the near triangle
+    orig[:, 2] = np.float32(1e-3) * np.arange(n, dtype=np.float32) / n
+    dirs = np.tile(np.float32([0.0, 0.0, -1.0]), (n, 1))
+    tim = np.arange(n) * 1e-6
+    sc = h.Scene.from_workload_scene(scene)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    out, _ = h.simulate(sc, p, dev(orig), dev(dirs), dev(tim), pulse_index_base=0,
+                        subray_hits=True)
+    torch.cuda.synchronize()
+    g = out.numpy()
+    sc.destroy()
+    r = oracle.simulate(scene, p, orig, dirs, tim, np.arange(n, dtype=np.uint64))
+    errs = gpu_invariants(g, p.max_returns, p.detection_threshold, p)
+    assert not errs, errs
+    rep = compare(g, r, scene.n_tris, p.bin_width_ns)
+    assert rep.ok(), rep.summary()
+    assert (g["n_returns"][0::2] == 2).all() and (g["n_returns"][1::2] == 1).all()

@@ -1,20 +1,19 @@
 #!/bin/bash
-# A/B of environment switches on configs (one gpurun call):
-#   VARIANTS="k7:HELIOS_FUSE=0 fused:HELIOS_FUSE=1" CFGS="C5 C3" bash tools/env_ab.sh
-# Prints Mrays/s of the pipelined steps and the exclusive per-kernel times.
-for cfg in ${CFGS:-C5 C3 C2}; do
-  for v in $VARIANTS; do
-    name=${v%%:*}; envs=${v#*:}
-    env ${envs//,/ } timeout 900 python bench.py --config $cfg --steps ${STEPS:-10} --warmup 3 \
-      --no-e2e --no-cpu-baseline --no-survey --no-packed --full-config 0 > gpurun_out/ab.json 2>gpurun_out/ab.err || tail -3 gpurun_out/ab.err
-    python - "$cfg" "$name" <<'PY'
+# A/B of tuning environments on bench.py (device value, blocking calls, packed, e2e):
+#   VARS="taper1:HELIOS_TAPER=1 taper0:HELIOS_TAPER=0" CFGS="C5 C3" bash tools/env_ab.sh
+for cfg in ${CFGS:-C5}; do
+  for v in ${VARS}; do
+    label=${v%%:*}; envs=${v#*:}
+    env $envs timeout 900 python bench.py --config $cfg --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline \
+      --no-survey --full-config 0 > gpurun_out/envab.json 2>gpurun_out/envab.err || tail -3 gpurun_out/envab.err
+    python - "$cfg" "$label" <<'PY'
 import json, sys
-d = json.load(open("gpurun_out/ab.json"))
-r = d["roofline"]
-k = r["kernels_exclusive_ms_per_step"]
-print(f"{sys.argv[1]} {sys.argv[2]:10s} {d['value']:8.1f} Mrays/s  {d['ms_per_step']:.3f} ms/step  "
-      f"K6a {k['k_beam (K6a)']:.3f} K6 {k['k_trace (K6)']:.3f} K7 {k['k_waveform (K7)']:.3f} "
-      f"serial {k['serialized_step']:.3f}  blocking {d['blocking_calls']['value']:.1f}", flush=True)
+d = json.load(open("gpurun_out/envab.json"))
+e = d.get("e2e") or {}
+b = d.get("blocking_calls") or {}
+pk = d.get("packed_outputs") or {}
+print(f"{sys.argv[1]} {sys.argv[2]:8s} value {d['value']:8.1f}  blocking {b.get('value', 0):8.1f}  "
+      f"packed {pk.get('value', 0):8.1f}  e2e {e.get('value', 0):8.1f} Mrays/s", flush=True)
 PY
   done
 done
