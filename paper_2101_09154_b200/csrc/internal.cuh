@@ -234,8 +234,10 @@ struct WavePlan {
   int warps;            // warps per block (0 = does not fit)
   size_t smem;          // dynamic shared memory per block
   uint32_t grid;        // persistent grid (SMs x occupancy)
-  size_t scratch_bytes; // per-warp global rows of the wide pass
+  size_t scratch_bytes; // per-warp global rows of the wide pass (0: rows in shared memory)
   uint32_t wide_grid;   // blocks of the wide pass
+  int wide_warps;       // warps per block of the wide pass
+  size_t wide_smem;     // its dynamic shared memory per block
   uint32_t grid_cap;    // 0 = full persistent grid; else max blocks (overlap with K6)
 };
 WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps);

@@ -38,9 +38,6 @@ namespace {
 #ifndef HELIOS_WAVE_WARPS
 #define HELIOS_WAVE_WARPS 8
 #endif
-#ifndef HELIOS_K7_PREFETCH
-#define HELIOS_K7_PREFETCH 1  // next pulse's records loaded while this pulse is binned
-#endif
 constexpr int kMaxWarps = HELIOS_WAVE_WARPS;
 #ifndef HELIOS_WAVE_WCAP
 #define HELIOS_WAVE_WCAP 512
@@ -50,6 +47,13 @@ constexpr int kMaxWarps = HELIOS_WAVE_WARPS;
 #endif
 constexpr int kWCap = HELIOS_WAVE_WCAP;  // fp64 bins per warp in shared memory
 constexpr int kAggCap = 64;   // offset groups handled by the grouped path
+// ceil(2^32 / d): floor(x / d) = umulhi(x, c_inv[d]) for x <= 3168, 2 <= d <= 32
+__constant__ uint32_t c_inv[33] = {
+    0u, 0u, 2147483648u, 1431655766u, 1073741824u, 858993460u, 715827883u, 613566757u,
+    536870912u, 477218589u, 429496730u, 390451573u, 357913942u, 330382100u, 306783379u,
+    286331154u, 268435456u, 252645136u, 238609295u, 226050911u, 214748365u, 204522253u,
+    195225787u, 186737709u, 178956971u, 171798692u, 165191050u, 159072863u, 153391690u,
+    148102321u, 143165577u, 138547333u, 134217728u};
 constexpr size_t kSmemCap = 200 * 1024;
 
 // Echo width ("Optionally, a Gaussian may be fitted to the resulting
@@ -227,15 +231,18 @@ __global__ void k_range_noise(helios_return* __restrict__ ret, const uint8_t* __
 }
 
 struct Layout {
-  size_t ker_d, per_warp_d, w_off, agg_off, rec_off;
+  size_t ker_d, kr_d, per_warp_d, w_off, agg_off, rec_off;
 };
-__host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps) {
+// wcap: bins of the per-warp W window in shared memory (main pass kWCap; the
+// wide pass n_bins rounded to even, or 0 when its rows live in global memory)
+__host__ __device__ inline Layout layout_for(uint32_t N, uint32_t taps, uint32_t wcap) {
   Layout L;
   L.ker_d = (taps + 1) & ~1u;
+  L.kr_d = (taps + 4) & ~1u;                   // one reversed, zero-padded copy (x2)
   L.w_off = 0;
-  L.agg_off = kWCap;
-  L.rec_off = kWCap + kAggCap;                 // int2[N] {offset o_s, bits of A_s}
-  L.per_warp_d = L.rec_off + N;
+  L.agg_off = wcap;
+  L.rec_off = wcap + kAggCap + 2;              // int2[N] {offset o_s, bits of A_s}
+  L.per_warp_d = (L.rec_off + N + 1) & ~(size_t)1;  // even: 16-B aligned per warp
   return L;
 }
 
@@ -262,35 +269,44 @@ __device__ __forceinline__ int rec_offset(int k, unsigned k0u, uint32_t nb) {
 // W[k] = sum_o A_o p[k - o] (k < S = maxoff + L_p) in fp64, maximum, local
 // maxima and returns, then the output row.
 //
-// Two passes share this body.  The main pass (WIDE = false) keeps W in the
-// warp's shared-memory window of kWCap bins; a pulse whose support exceeds
-// it (C5: 0.8 % of pulses, roof edges over the ground) is appended to a list
-// and left untouched.  The wide pass (WIDE = true, launched right after on
-// the same stream) runs those pulses with W in a per-warp global scratch row.
-// Keeping the two apart lets the compiler address W as shared memory in the
-// main pass (LDS/STS, not generic loads).  R = ceil(N / 32) <= 3: records of
+// Two passes share this body.  The main pass (MODE 0) keeps W in the warp's
+// shared-memory window of kWCap bins; a pulse whose support exceeds it (C5:
+// 0.8 % of pulses, roof edges over the ground) is appended to a list and left
+// untouched.  The wide pass (launched right after on the same stream) runs
+// those pulses with a whole n_bins row per warp in shared memory (MODE 1,
+// fewer warps per block), or, when even one such row does not fit, in a
+// per-warp global scratch row (MODE 2).  Keeping the modes apart lets the
+// compiler address W as shared memory (LDS/STS, not generic loads).  R = ceil(N / 32) <= 3: records of
 // the next pulse prefetched into registers (R = 0: read in the loop, any N).  FIT: the echo-width jobs (R28) are
 // compiled in only where asked for (a smaller loop body for the usual case).
-template <bool WIDE, bool FIT, int R>
+template <int MODE, bool FIT, int R>
 __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
     k_waveform(const WaveArgs a, double* __restrict__ gscratch) {
+  constexpr bool WIDE = MODE != 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t N = a.N, nb = a.n_bins, taps = a.taps;
-  const Layout L = layout_for(N, taps);
+  const uint32_t count = WIDE ? *a.wide_count : (uint32_t)a.n_pulses;
+  if (WIDE && count == 0) return;  // the usual case: nothing deferred
+  const Layout L = layout_for(N, taps, MODE == 0 ? kWCap : MODE == 1 ? (nb + 1) & ~1u : 0u);
   double* ker = reinterpret_cast<double*>(smem_raw);
-  double* base = ker + L.ker_d + (size_t)warp * L.per_warp_d;
+  double* krev = ker + L.ker_d;  // two copies of kr[m] = ker[taps - 1 - m], zero-padded
+  double* base = krev + 2 * L.kr_d + (size_t)warp * L.per_warp_d;
   double* agg = base + L.agg_off;
   int2* sr = reinterpret_cast<int2*>(base + L.rec_off);  // {o_s, bits of A_s}
   const unsigned kFull = 0xffffffffu;
 
   for (uint32_t j = threadIdx.x; j < taps; j += blockDim.x) ker[j] = a.kernel[j];
+  for (uint32_t j = threadIdx.x; j < 2 * L.kr_d; j += blockDim.x) {
+    const uint32_t q = j >= L.kr_d, i = j - q * (uint32_t)L.kr_d;  // copy q holds kr[m] at 2 - q + m
+    const int m = (int)i - 2 + (int)q;
+    krev[j] = (m >= 0 && m < (int)taps) ? a.kernel[taps - 1 - m] : 0.0;
+  }
   __syncthreads();
 
   const uint32_t gw = blockIdx.x * (uint32_t)nw + (uint32_t)warp;
   const uint32_t stride = gridDim.x * (uint32_t)nw;
-  double* W = WIDE ? gscratch + (size_t)gw * nb : base + L.w_off;
-  const uint32_t count = WIDE ? *a.wide_count : (uint32_t)a.n_pulses;
+  double* W = MODE == 2 ? gscratch + (size_t)gw * nb : base + L.w_off;
 
   // software pipelining (N <= 96: R = ceil(N / 32) records per lane): the
   // records of the warp's next pulse are loaded into registers while this
@@ -371,14 +387,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
         // amplitude per offset group, in a fixed order (deterministic)  @region group_sums
         const int G = maxoff + 1;
         if (G <= 16) {
-          // groups rounded up to G' = 2^lg <= 16 lanes: lane (o, c) = (lane mod
-          // G', lane / G') sums group o over subray chunk c of C = 32 / G'
-          // (shifts, no divisions), then a fixed binary tree over the chunks
-          const int lg = G <= 1 ? 0 : 32 - __clz(G - 1);
-          const int o = lane & ((1 << lg) - 1), c = lane >> lg, lc = 5 - lg;
+          // lane (o, c) = (lane mod G, lane / G) sums group o over subray
+          // chunk c of C = floor(32 / G) (lanes >= C G idle; divisions as
+          // exact reciprocal multiplies), then a fixed binary tree over the chunks
+          const uint32_t C = 32u / (uint32_t)G;  // warp-uniform
+          const uint32_t c = G == 1 ? (uint32_t)lane : __umulhi((uint32_t)lane, c_inv[G]);
+          const int o = lane - (int)c * G;
           double acc = 0.0, acc2 = 0.0;  // two chains (subrays of even / odd rank)
-          if (o < G) {
-            const uint32_t s0 = (N * (uint32_t)c) >> lc, s1 = (N * (uint32_t)(c + 1)) >> lc;
+          if (c < C) {
+            const uint32_t s0 = __umulhi(N * c, c_inv[C]), s1 = __umulhi(N * (c + 1), c_inv[C]);
             uint32_t s = s0;
             for (; s + 1 < s1; s += 2) {
               const int2 r = sr[s], r2 = sr[s + 1];
@@ -391,9 +408,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
             }
             acc += acc2;
           }
-          for (int st = 1; st < (1 << lc); st <<= 1) {
-            const double other = __shfl_down_sync(kFull, acc, st << lg);
-            if ((c & (2 * st - 1)) == 0) acc += other;
+          for (uint32_t st = 1; st < C; st <<= 1) {
+            const double other = __shfl_down_sync(kFull, acc, st * (uint32_t)G);
+            if ((c & (2 * st - 1)) == 0 && c + st < C) acc += other;
           }
           if (lane < G) agg[lane] = acc;
         } else {
@@ -418,18 +435,32 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
         __syncwarp();
         // W[k] = sum_o A_o p[k - o], two fp64 chains per bin (even / odd  @region W_grouped
         // offsets), the lane's running maximum on the way
-        for (uint32_t k = lane; k < S; k += 32) {
-          const int olo = max(0, (int)k - (int)taps + 1), ohi = min(maxoff, (int)k);
-          double w = 0.0, w2 = 0.0;
-          int o = olo;
-          for (; o + 1 <= ohi; o += 2) {
-            w = fma(agg[o], ker[k - o], w);
-            w2 = fma(agg[o + 1], ker[k - o - 1], w2);
+        {
+          // pairs of terms by 16-B loads: agg[o], agg[o + 1] and the reversed
+          // kernel kr[m], kr[m + 1] (ker[k - o] = kr[taps - 1 - k + o]); the
+          // copy of kr (shifted by one) that aligns the pair with agg's is
+          // taken per bin; an odd first or last term meets a zero pad
+          if (lane < 2) agg[G + lane] = 0.0;
+          __syncwarp();
+          for (uint32_t k = lane; k < S; k += 32) {
+            const int olo = max(0, (int)k - (int)taps + 1), ohi = min(maxoff, (int)k);
+            const int o0 = olo & ~1;                  // even start (agg[-1] never read)
+            const int m0 = (int)taps - 1 - (int)k + o0;  // kr index of the first term (>= -1)
+            // copy q = m0 mod 2 holds kr[m] at index 2 - q + m: the pairs
+            // {m0 + 2t, m0 + 2t + 1} start at even indices (16-B aligned)
+            const int q = m0 & 1;
+            const double2* kp = reinterpret_cast<const double2*>(krev + q * L.kr_d + 2 - q + m0);
+            const double2* ap = reinterpret_cast<const double2*>(agg + o0);
+            double w = 0.0, w2 = 0.0;
+            for (int t = 0; o0 + 2 * t <= ohi; ++t) {
+              const double2 av = ap[t], kv = kp[t];
+              w = fma(av.x, kv.x, w);
+              w2 = fma(av.y, kv.y, w2);
+            }
+            w += w2;
+            W[k] = w;
+            Mlane = fmax(Mlane, w);
           }
-          if (o <= ohi) w = fma(agg[o], ker[k - o], w);
-          w += w2;
-          W[k] = w;
-          Mlane = fmax(Mlane, w);
         }
       } else {
         // wide footprint (offsets spread over >= kAggCap bins, e.g. a crown and  @region wide
@@ -635,9 +666,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
   }
 }
 
-size_t smem_for(uint32_t N, uint32_t taps, int warps) {
-  const Layout L = layout_for(N, taps);
-  return 8 * (L.ker_d + (size_t)warps * L.per_warp_d);
+size_t smem_for(uint32_t N, uint32_t taps, int warps, uint32_t wcap = kWCap) {
+  const Layout L = layout_for(N, taps, wcap);
+  return 8 * (L.ker_d + 2 * L.kr_d + (size_t)warps * L.per_warp_d);
 }
 
 }  // namespace
@@ -657,11 +688,10 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const void* kernels[] = {
-      (const void*)k_waveform<false, false, 0>, (const void*)k_waveform<false, false, 1>,
-      (const void*)k_waveform<false, false, 2>, (const void*)k_waveform<false, false, 3>,
-      (const void*)k_waveform<false, true, 0>,  (const void*)k_waveform<false, true, 1>,
-      (const void*)k_waveform<false, true, 2>,  (const void*)k_waveform<false, true, 3>,
-      (const void*)k_waveform<true, false, 0>,  (const void*)k_waveform<true, true, 0>};
+      (const void*)k_waveform<0, false, 0>, (const void*)k_waveform<0, false, 1>,
+      (const void*)k_waveform<0, false, 2>, (const void*)k_waveform<0, false, 3>,
+      (const void*)k_waveform<0, true, 0>,  (const void*)k_waveform<0, true, 1>,
+      (const void*)k_waveform<0, true, 2>,  (const void*)k_waveform<0, true, 3>};
   for (const void* k : kernels)
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem) !=
         cudaSuccess) {
@@ -678,16 +708,40 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
     return pl;
   }
   pl.grid = (uint32_t)(sms * per_sm);
-  // the wide pass (pulses whose support exceeds kWCap bins) keeps each
-  // warp's row in a global scratch row of n_bins doubles: one block per SM,
-  // fewer for very long windows so that scratch stays within kScratchCap
-  // (the pass stays correct, only its parallelism shrinks)
-  constexpr size_t kScratchCap = 512ull << 20;
-  const size_t per_block = sizeof(double) * (size_t)warps * n_bins;
+  // the wide pass (pulses whose support exceeds kWCap bins): a whole n_bins
+  // row per warp in shared memory with as many warps per block as fit (C5:
+  // 8 warps x 10.7 KB), one block per SM; else (very long windows) each warp's
+  // row in a global scratch row, fewer blocks so that scratch stays within
+  // kScratchCap (the pass stays correct, only its parallelism shrinks)
+  const uint32_t wrow = (n_bins + 1) & ~1u;
+  pl.wide_warps = 0;
+  for (int w = kMaxWarps; w >= 1; --w)
+    if (smem_for(N, taps, w, wrow) <= kSmemCap) {
+      pl.wide_warps = w;
+      break;
+    }
+  const void* wide[] = {(const void*)k_waveform<1, false, 0>, (const void*)k_waveform<1, true, 0>,
+                        (const void*)k_waveform<2, false, 0>, (const void*)k_waveform<2, true, 0>};
   pl.wide_grid = (uint32_t)sms;
-  if ((size_t)pl.wide_grid * per_block > kScratchCap)
-    pl.wide_grid = (uint32_t)std::max<size_t>(1, kScratchCap / per_block);
-  pl.scratch_bytes = per_block * pl.wide_grid;
+  if (pl.wide_warps > 0) {
+    pl.wide_smem = smem_for(N, taps, pl.wide_warps, wrow);
+    pl.scratch_bytes = 0;
+  } else {
+    pl.wide_warps = warps;
+    pl.wide_smem = smem_for(N, taps, warps, 0);
+    constexpr size_t kScratchCap = 512ull << 20;
+    const size_t per_block = sizeof(double) * (size_t)warps * n_bins;
+    if ((size_t)pl.wide_grid * per_block > kScratchCap)
+      pl.wide_grid = (uint32_t)std::max<size_t>(1, kScratchCap / per_block);
+    pl.scratch_bytes = per_block * pl.wide_grid;
+  }
+  for (const void* k : wide)
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.wide_smem) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      pl.warps = 0;
+      return pl;
+    }
   return pl;
 }
 
@@ -768,23 +822,31 @@ cudaError_t launch_waveform(const WaveArgs& a, const WavePlan& pl, double* scrat
   const unsigned g = (unsigned)grid, t = (unsigned)pl.warps * 32;
   const int R = a.N <= 96 ? (int)((a.N + 31) / 32) : 0;
   switch (R + (a.fit ? 4 : 0)) {
-    case 1: k_waveform<false, false, 1><<<g, t, pl.smem, s>>>(a, scratch); break;
-    case 2: k_waveform<false, false, 2><<<g, t, pl.smem, s>>>(a, scratch); break;
-    case 3: k_waveform<false, false, 3><<<g, t, pl.smem, s>>>(a, scratch); break;
-    case 4: k_waveform<false, true, 0><<<g, t, pl.smem, s>>>(a, scratch); break;
-    case 5: k_waveform<false, true, 1><<<g, t, pl.smem, s>>>(a, scratch); break;
-    case 6: k_waveform<false, true, 2><<<g, t, pl.smem, s>>>(a, scratch); break;
-    case 7: k_waveform<false, true, 3><<<g, t, pl.smem, s>>>(a, scratch); break;
-    default: k_waveform<false, false, 0><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 1: k_waveform<0, false, 1><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 2: k_waveform<0, false, 2><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 3: k_waveform<0, false, 3><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 4: k_waveform<0, true, 0><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 5: k_waveform<0, true, 1><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 6: k_waveform<0, true, 2><<<g, t, pl.smem, s>>>(a, scratch); break;
+    case 7: k_waveform<0, true, 3><<<g, t, pl.smem, s>>>(a, scratch); break;
+    default: k_waveform<0, false, 0><<<g, t, pl.smem, s>>>(a, scratch); break;
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // the pulses the main pass deferred (support > kWCap bins), same stream
   const unsigned gw = (unsigned)std::min<uint64_t>(pl.wide_grid, want);
-  if (a.fit)
-    k_waveform<true, true, 0><<<gw, t, pl.smem, s>>>(a, scratch);
-  else
-    k_waveform<true, false, 0><<<gw, t, pl.smem, s>>>(a, scratch);
+  const unsigned tw = (unsigned)pl.wide_warps * 32;
+  if (pl.scratch_bytes == 0) {
+    if (a.fit)
+      k_waveform<1, true, 0><<<gw, tw, pl.wide_smem, s>>>(a, scratch);
+    else
+      k_waveform<1, false, 0><<<gw, tw, pl.wide_smem, s>>>(a, scratch);
+  } else {
+    if (a.fit)
+      k_waveform<2, true, 0><<<gw, tw, pl.wide_smem, s>>>(a, scratch);
+    else
+      k_waveform<2, false, 0><<<gw, tw, pl.wide_smem, s>>>(a, scratch);
+  }
   return cudaGetLastError();
 }
 

@@ -122,10 +122,13 @@ def test_wide_support_in_global_scratch():
     assert (g["n_returns"] == 2).all()  # the near and the far echo
 
 
-def test_wide_pass_mixed_with_ordinary_pulses():
+@pytest.mark.parametrize("bin_ns,n", [(1.0, 257), (0.05, 33)])
+def test_wide_pass_mixed_with_ordinary_pulses(bin_ns, n):
     # alternate pulses see the near triangle over the far plane (support > 512
     # bins: deferred to the wide pass) or the far plane alone (main pass): the
-    # deferral list must leave every other pulse to the main pass untouched
+    # deferral list must leave every other pulse to the main pass untouched.
+    # 1 ns bins: 1335-bin rows, the wide pass keeps them in shared memory;
+    # 0.05 ns bins over 2000 ns: 40000-bin rows (320 KB) -> global scratch rows
     import paper_2101_09154_b200 as h
     torch = torch_cuda()
     near = np.array([[0.0, -5.0, -10.0], [5.0, -5.0, -10.0], [0.0, 5.0, -10.0]])
@@ -134,8 +137,8 @@ def test_wide_pass_mixed_with_ordinary_pulses():
     tris = np.concatenate([near[None], far.reshape(2, 3, 3)]).astype(np.float32)
     scene = Scene(tri_xyz=tris, tri_reflectance=np.float32([0.3, 0.6, 0.6]))
     p = ScannerParams(subray_count=19, divergence_rad=0.05, max_returns=7,
-                      detection_threshold=1e-6)
-    n = 257
+                      detection_threshold=1e-6, bin_width_ns=bin_ns,
+                      **({} if bin_ns == 1.0 else {"max_fullwave_range_ns": 2000.0}))
     orig = np.zeros((n, 3), np.float32)
     orig[1::2, 0] = 200.0  # odd pulses: beside the near triangle
     orig[:, 2] = np.float32(1e-3) * np.arange(n, dtype=np.float32) / n

@@ -13,6 +13,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -40,9 +41,11 @@ def main(rep, cfg, source, pulses=None):
     per = {}
     for r in rows[2:]:
         name = r[kn]
+        wave_main = re.search(r"k_waveform<(\(bool\))?(0|false)", name)
         key = ("k_beam" if ("k_beam<0>" in name or "k_beam<false>" in name)
                else "k_trace" if ("k_trace<0," in name or "k_trace<false" in name)
-               else "k_waveform" if "k_waveform" in name else None)
+               else "k_waveform" if wave_main
+               else "k_waveform_wide" if "k_waveform" in name else None)
         if key is None or key in per:
             continue
         per[key] = {c: scale(units[idx[c]], r[idx[c]]) for c in COLS}
@@ -51,7 +54,14 @@ def main(rep, cfg, source, pulses=None):
     subrays = chunk * N
     t = per["k_trace"]
     b = per.get("k_beam", {c: 0.0 for c in COLS})
-    w = per["k_waveform"]
+    # K7 = the main pass + the wide pass (pulses whose support exceeds the
+    # shared-memory window) of the same chunk
+    w = dict(per["k_waveform"])
+    ww = per.get("k_waveform_wide")
+    if ww:
+        for c in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                  "smsp__inst_executed.sum"):
+            w[c] += ww[c]
     rec = {
         "source": source,
         "k_trace": {
@@ -74,6 +84,8 @@ def main(rep, cfg, source, pulses=None):
             "units": chunk, "unit": "pulse",
             "issue_slots_busy": w["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100,
             "duration_us": w["gpu__time_duration.sum"],
+            "wide_pass_duration_us": ww["gpu__time_duration.sum"] if ww else 0.0,
+            "wide_pass_warp_inst": ww["smsp__inst_executed.sum"] if ww else 0.0,
         },
     }
     path = os.path.join(ROOT, "profiles", "traffic.json")
