@@ -742,6 +742,15 @@ WavePlan plan_waveform(uint32_t n_bins, uint32_t N, uint32_t taps) {
       pl.warps = 0;
       return pl;
     }
+  // shared-memory rows: as many blocks as fit per SM (the pass is as long as
+  // its slowest warp's share of the deferred pulses)
+  int per_sm_w = 1;
+  if (pl.scratch_bytes == 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, wide[0], pl.wide_warps * 32,
+                                                    pl.wide_smem) == cudaSuccess &&
+      per_sm_w > 1)
+    pl.wide_grid = (uint32_t)(sms * per_sm_w);
+  cudaGetLastError();
   return pl;
 }
 
