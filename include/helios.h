@@ -317,6 +317,32 @@ helios_status helios_simulate_batches(helios_scene scene, const helios_scanner_p
                                       uint32_t n_batches, helios_stream stream,
                                       helios_stats* stats);
 
+/* Non-blocking helios_simulate_batches ("a non-blocking variant
+ * is NEXT").  Checks its own arguments, copies the parameter struct and the
+ * pulses / outputs descriptors (not the arrays they point to) and returns at
+ * once; a library worker thread runs the call (on the scene's device, on
+ * `stream`), so the caller's thread is free and calls on distinct streams
+ * overlap on the device (one call's pipeline head and tail under another's
+ * kernels; pulses are independent).  Results are bitwise those of
+ * helios_simulate_batches.  Every array the descriptors point to must stay
+ * valid and untouched until helios_call_wait returns; `stats` (may be NULL)
+ * is read when the call is submitted (collect_counters) and written by the
+ * wait.  Errors: INVALID_ARGUMENT (NULL call, scene or descriptors), or
+ * OUT_OF_MEMORY / CUDA if the worker cannot be started; everything else
+ * (including argument checks of the call itself) is returned by the wait. */
+typedef struct helios_call_s* helios_call;
+helios_status helios_simulate_batches_async(helios_scene scene,
+                                            const helios_scanner_params* params,
+                                            const helios_pulses* pulses,
+                                            const helios_outputs* outputs, uint32_t n_batches,
+                                            helios_stream stream, const helios_stats* stats,
+                                            helios_call* call);
+/* Wait for an async call to finish (its stream is then synchronised); returns
+ * the call's status -- its message, if any, through helios_last_error on this
+ * thread -- copies its statistics into `stats` (may be NULL) and frees the
+ * handle.  Each handle must be waited for exactly once. */
+helios_status helios_call_wait(helios_call call, helios_stats* stats);
+
 /* ------------------------------------------------------------------------
  * Process-wide tuning / test switches.  Not needed for correct use: every
  * value only changes how the same results are computed (the tests check the

@@ -14,6 +14,7 @@
 #include <limits>
 #include <list>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -1442,6 +1443,71 @@ helios_status helios_simulate_batches(helios_scene sc, const helios_scanner_para
   std::vector<Job> jobs(n_batches);
   for (uint32_t i = 0; i < n_batches; ++i) jobs[i] = Job{pulses + i, outputs + i};
   return simulate_impl(sc, params, jobs.data(), n_batches, nullptr, 0, stream, stats);
+}
+
+// Non-blocking calls: a worker thread per call runs the blocking pipeline on
+// the scene's device (the scratch cache is per caller stream and locked, so
+// calls on distinct streams run concurrently).
+struct helios_call_s {
+  std::thread worker;
+  helios_scanner_params params{};
+  std::vector<helios_pulses> pulses;
+  std::vector<helios_outputs> outputs;
+  helios_stats stats{};
+  bool has_stats = false;
+  helios_status status = HELIOS_OK;
+  std::string err;
+};
+
+helios_status helios_simulate_batches_async(helios_scene sc, const helios_scanner_params* params,
+                                            const helios_pulses* pulses,
+                                            const helios_outputs* outputs, uint32_t n_batches,
+                                            helios_stream stream, const helios_stats* stats,
+                                            helios_call* call) {
+  g_err.clear();
+  if (!call) return fail(HELIOS_ERR_INVALID_ARGUMENT, "call is NULL");
+  *call = nullptr;
+  if (!sc) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (!params) return fail(HELIOS_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (n_batches && (!pulses || !outputs))
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "pulses/outputs is NULL");
+  helios_call_s* c = new (std::nothrow) helios_call_s;
+  if (!c) return fail(HELIOS_ERR_OUT_OF_MEMORY, "helios_simulate_batches_async: no memory");
+  c->params = *params;
+  c->pulses.assign(pulses, pulses + n_batches);
+  c->outputs.assign(outputs, outputs + n_batches);
+  c->has_stats = stats != nullptr;
+  if (stats) c->stats = *stats;
+  const int dev = sc->device;
+  try {
+    c->worker = std::thread([c, sc, stream, dev]() {
+      cudaSetDevice(dev);
+      const uint32_t n = (uint32_t)c->pulses.size();
+      std::vector<Job> jobs(n);
+      for (uint32_t i = 0; i < n; ++i) jobs[i] = Job{&c->pulses[i], &c->outputs[i]};
+      g_err.clear();
+      c->status = n ? simulate_impl(sc, &c->params, jobs.data(), n, nullptr, 0, stream,
+                                    c->has_stats ? &c->stats : nullptr)
+                    : HELIOS_OK;
+      c->err = g_err;
+    });
+  } catch (...) {
+    delete c;
+    return fail(HELIOS_ERR_OUT_OF_MEMORY, "helios_simulate_batches_async: cannot start a worker");
+  }
+  *call = c;
+  return HELIOS_OK;
+}
+
+helios_status helios_call_wait(helios_call c, helios_stats* stats) {
+  g_err.clear();
+  if (!c) return fail(HELIOS_ERR_INVALID_ARGUMENT, "call is NULL");
+  c->worker.join();
+  const helios_status st = c->status;
+  if (stats) *stats = c->stats;
+  if (st != HELIOS_OK) g_err = c->err;
+  delete c;
+  return st;
 }
 
 helios_status helios_simulate_survey(helios_scene sc, const helios_scanner_params* params,

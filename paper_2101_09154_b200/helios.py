@@ -32,7 +32,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OUT_OF_MEMORY", 3: "CUDA", 4: "NO
 EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helios_build_accel",
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
             "helios_pulse_taps", "helios_simulate", "helios_simulate_batches",
-            "helios_simulate_survey", "helios_get_tuning", "helios_set_tuning",
+            "helios_simulate_batches_async", "helios_call_wait", "helios_simulate_survey", "helios_get_tuning", "helios_set_tuning",
             "helios_util_sort_pairs_u64", "helios_util_scan_u64",
             "helios_util_fp64_fma_tflops")
 
@@ -161,6 +161,14 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(helios_pulses),
                                               ctypes.POINTER(helios_outputs), _u32, _vp,
                                               ctypes.POINTER(helios_stats)]
+        L.helios_simulate_batches_async.restype = ctypes.c_int
+        L.helios_simulate_batches_async.argtypes = [_vp, ctypes.POINTER(helios_scanner_params),
+                                                    ctypes.POINTER(helios_pulses),
+                                                    ctypes.POINTER(helios_outputs), _u32, _vp,
+                                                    ctypes.POINTER(helios_stats),
+                                                    ctypes.POINTER(_vp)]
+        L.helios_call_wait.restype = ctypes.c_int
+        L.helios_call_wait.argtypes = [_vp, ctypes.POINTER(helios_stats)]
         L.helios_get_tuning.restype = ctypes.c_int
         L.helios_get_tuning.argtypes = [ctypes.POINTER(helios_tuning)]
         L.helios_set_tuning.restype = ctypes.c_int
@@ -251,6 +259,26 @@ def helios_simulate_batches(scene: int, params: helios_scanner_params, pulses, o
     O = (helios_outputs * n)(*outputs)
     _check(lib().helios_simulate_batches(scene, ctypes.byref(params), P, O, n, _stream(stream),
                                          None if stats is None else ctypes.byref(stats)))
+
+
+def helios_simulate_batches_async(scene: int, params: helios_scanner_params, pulses, outputs,
+                                  stream=None, stats: helios_stats | None = None) -> int:
+    """Submit; returns the helios_call handle (an int).  The descriptor arrays
+    are copied by the library; the arrays they point to must outlive the wait."""
+    n = len(pulses)
+    assert len(outputs) == n
+    P = (helios_pulses * n)(*pulses)
+    O = (helios_outputs * n)(*outputs)
+    h = _vp()
+    _check(lib().helios_simulate_batches_async(scene, ctypes.byref(params), P, O, n,
+                                               _stream(stream),
+                                               None if stats is None else ctypes.byref(stats),
+                                               ctypes.byref(h)))
+    return h.value
+
+
+def helios_call_wait(call: int, stats: helios_stats | None = None) -> None:
+    _check(lib().helios_call_wait(call, None if stats is None else ctypes.byref(stats)))
 
 
 def helios_get_tuning() -> helios_tuning:
@@ -549,6 +577,45 @@ def simulate_batches(scene: Scene, params, batches, outputs, stream=None, stats:
         helios_simulate_batches(scene.handle, hp, ps, os_, stream, st)
     del keep
     return st
+
+
+class Call:
+    """A submitted helios_simulate_batches_async call; wait() returns its
+    helios_stats (or None) and raises HeliosError on failure.  Keeps the pulse
+    and output arrays alive until the wait."""
+
+    def __init__(self, handle, keep, stats):
+        self._h, self._keep, self._stats = handle, keep, stats
+
+    def wait(self):
+        if self._h is None:
+            raise RuntimeError("helios call already waited for")
+        h, self._h = self._h, None
+        try:
+            helios_call_wait(h, self._stats)
+        finally:
+            self._keep = None
+        return self._stats
+
+
+def simulate_batches_async(scene: Scene, params, batches, outputs, stream=None,
+                           stats: bool = False, counters: bool = False) -> Call:
+    """helios_simulate_batches_async: the same arguments as simulate_batches;
+    returns at once with a Call (wait() for the results; no capacity retry)."""
+    hp = params if isinstance(params, helios_scanner_params) else make_params(params)
+    ps, keep = [], [hp, batches, outputs]
+    for (o, d, t, base) in batches:
+        p = helios_pulses()
+        p.p_origin, p.p_direction, p.p_time_s = _ptr(o), _ptr(d), _ptr(t)
+        p.n_pulses = int(o.shape[0])
+        p.pulse_index_base = int(base)
+        ps.append(p)
+    os_ = [_marshal_outputs(x) for x in outputs]
+    st = helios_stats() if (stats or counters) else None
+    if st is not None:
+        st.collect_counters = 1 if counters else 0
+    h = helios_simulate_batches_async(scene.handle, hp, ps, os_, stream, st)
+    return Call(h, keep, st)
 
 
 def make_survey(sv) -> tuple:

@@ -119,3 +119,17 @@ def test_struct_layouts_match_the_header(tmp_path):
         assert int(got[name]) == dt.itemsize, name
         for f in dt.names:
             assert int(got[f"{name}.{f}"]) == dt.fields[f][1], (name, f)
+
+
+def test_async_call_argument_checks_without_gpu(libpath):
+    """helios_simulate_batches_async / helios_call_wait reject NULL handles
+    and arguments on the host, before any device work."""
+    import paper_2101_09154_b200 as h
+    L = h.lib()
+    handle = ctypes.c_void_p(123)
+    assert L.helios_simulate_batches_async(None, None, None, None, 0, None, None, None) == 1
+    assert L.helios_simulate_batches_async(None, None, None, None, 0, None, None,
+                                           ctypes.byref(handle)) == 1
+    assert handle.value is None  # cleared on failure
+    assert "scene" in str(h.helios_last_error())
+    assert L.helios_call_wait(None, None) == 1

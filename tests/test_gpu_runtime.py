@@ -152,3 +152,54 @@ def test_tuning_switches_are_validated():
         h.helios_set_tuning(bad)
     after = h.helios_get_tuning()
     assert bytes(after) == bytes(t)
+
+
+def test_async_calls_equal_blocking_calls():
+    """helios_simulate_batches_async: two calls in flight on two caller streams
+    (device and pinned-host outputs) while the host thread is free, each
+    bitwise equal to the blocking call; stats come back through the wait."""
+    torch = torch_cuda()
+    h = _h()
+    w = workload("C5", 0.03)
+    sc = scene_for(w)
+    hp = h.make_params(w.params)
+    specs = [((300, 2500), (9000, 3001)), ((20000, 4099), (40000, 700))]
+    calls, outs_all = [], []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for ci, spans in enumerate(specs):
+        batches, outs = [], []
+        for start, cnt in spans:
+            o, d, t = w.pulses(start, cnt)
+            dev = ci == 0
+            conv = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()) if dev else \
+                (lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory())
+            batches.append((conv(o), conv(d), conv(t), start))
+            outs.append(h.alloc_outputs(cnt, hp, device="cuda" if dev else "cpu",
+                                        pin_memory=not dev, subray_hits=True))
+        torch.cuda.synchronize()  # inputs in place before a worker thread reads them
+        calls.append(h.simulate_batches_async(sc, hp, batches, outs, stream=streams[ci],
+                                              stats=True))
+        outs_all.append((spans, outs))
+    for c, (spans, outs) in zip(calls, outs_all):
+        st = c.wait()
+        assert st.batches == len(spans) and st.pulses == sum(n for _, n in spans)
+        with pytest.raises(RuntimeError):
+            c.wait()  # a handle is waited for once
+        for (start, cnt), out in zip(spans, outs):
+            _outputs_equal(out.numpy(), gpu_run(w, start, cnt))
+    torch.cuda.synchronize()
+
+
+def test_async_call_reports_errors_at_the_wait():
+    torch = torch_cuda()
+    h = _h()
+    w = workload("C2", 0.125)
+    sc = scene_for(w)
+    hp = h.make_params(w.params)
+    hp.subray_count = 20  # in neither pattern sequence (R1)
+    o, d, t = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in w.pulses(0, 100))
+    out = h.alloc_outputs(100, h.make_params(w.params), device="cuda")
+    c = h.simulate_batches_async(sc, hp, [(o, d, t, 0)], [out])
+    with pytest.raises(h.HeliosError) as e:
+        c.wait()
+    assert e.value.status == 1 and "subray_count" in str(e.value)
