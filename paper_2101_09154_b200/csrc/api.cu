@@ -811,8 +811,15 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
     if (n == 0) continue;
     uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(1024, (48ull << 20) / (12ull * N)));
     if (beam || sc->d_pad != nullptr) {
-      constexpr uint64_t kBeamChunkSubrays = 64ull << 20;
-      uint64_t k = std::max<uint64_t>(2, (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
+      // a batch of a multi-batch call with device outputs may be one chunk
+      // of <= 128 Mi subrays: the batches themselves overlap in the pipeline,
+      // and fewer, longer launches lose less to launch tails (C5 +1.2 %, C3
+      // +2.6 %, profiles/r02s3_chunk_ab.txt); alone, or with host outputs,
+      // >= 2 chunks of <= 64 Mi so that K6a / copies overlap within the batch
+      const bool one_ok = n_jobs > 1 && !job_staged[j];
+      const uint64_t kBeamChunkSubrays = one_ok ? (128ull << 20) : (64ull << 20);
+      uint64_t k = std::max<uint64_t>(one_ok ? 1 : 2,
+                                      (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
       // host staging: >= 4 chunks per batch so copies overlap compute within a
       // single batch; a multi-batch call overlaps them across batches, and 2
       // chunks per batch measured faster there (C5 e2e 12.67 -> 12.46 ms per
