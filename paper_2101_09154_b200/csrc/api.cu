@@ -816,7 +816,10 @@ helios_status simulate_impl(helios_scene sc, const helios_scanner_params* params
       // and fewer, longer launches lose less to launch tails (C5 +1.2 %, C3
       // +2.6 %, profiles/r02s3_chunk_ab.txt); alone, or with host outputs,
       // >= 2 chunks of <= 64 Mi so that K6a / copies overlap within the batch
-      const bool one_ok = n_jobs > 1 && !job_staged[j];
+      // (a single batch too when its pulses have >= 64 subrays: K6a's
+      // per-pulse walk is then small next to K6, so overlapping it with a
+      // previous chunk buys less than one launch tail costs)
+      const bool one_ok = !job_staged[j] && (n_jobs > 1 || N >= 64);
       const uint64_t kBeamChunkSubrays = one_ok ? (128ull << 20) : (64ull << 20);
       uint64_t k = std::max<uint64_t>(one_ok ? 1 : 2,
                                       (n * N + kBeamChunkSubrays - 1) / kBeamChunkSubrays);
