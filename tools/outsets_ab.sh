@@ -1,5 +1,4 @@
 #!/bin/bash
-#!/bin/bash
 # bench.py value with 2 vs 5 output sets (= device batches per helios_simulate_batches call), C5.
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for os in 2 5 2 5; do
