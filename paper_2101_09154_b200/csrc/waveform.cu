@@ -513,8 +513,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, HELIOS_WAVE_MIN_BLOCKS)
       for (uint32_t b0 = 0; b0 < S && nret < a.max_returns; b0 += 32) {
         const uint32_t k = b0 + lane;
         bool pk = false;
-        if (k >= 1 && k + 1 < nb && k < S) {
-          const double w = W[k], wl = W[k - 1], wr = (k + 1 < S) ? W[k + 1] : 0.0;
+        // a block with no bin at or above the threshold holds no peak: one
+        // load and one vote instead of three loads and the comparisons
+        const bool inb = k >= 1 && k + 1 < nb && k < S;
+        const double w = inb ? W[k] : 0.0;
+        if (!__any_sync(kFull, inb && w >= thr)) continue;
+        if (inb) {
+          const double wl = W[k - 1], wr = (k + 1 < S) ? W[k + 1] : 0.0;
           pk = w > wl && w > wr && w >= thr;
         }
         unsigned m = __ballot_sync(kFull, pk);
