@@ -679,6 +679,13 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
 
 
   // ---- A2: subray fan-out (R2, R4), fp64
+  // the pulse's entry row (K6a) is read only after the fan-out and a vote:
+  // start bringing it into L1 now (no register, no scoreboard; C3 K6 -1.1 %)
+  if (a.entries != nullptr) {
+    const char* er = reinterpret_cast<const char*>(a.entries + p * kEntryStride);
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(er));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(er + 128));
+  }
   const float ox = __ldg(a.origin + 3 * p), oy = __ldg(a.origin + 3 * p + 1),
               oz = __ldg(a.origin + 3 * p + 2);
   D3 Dp, U, V;
