@@ -129,6 +129,26 @@ helios_status helios_scene_create(const helios_scene_desc* desc, helios_stream s
  * deeper than the 64-entry traversal stack). */
 helios_status helios_build_accel(helios_scene scene, helios_stream stream);
 
+/* Saving and loading a built acceleration structure ("Saving and
+ * loading already built scenes is relying on boost serialisation"): the
+ * tree and both triangle record arrays of a built scene as one
+ * self-describing blob, so a later process skips helios_build_accel.
+ *   helios_accel_export: buffer == NULL -> *bytes = the blob's size; else
+ *     writes the blob (host or device memory, *bytes >= that size) and sets
+ *     *bytes to it.  Synchronises the stream.
+ *   helios_accel_import: installs a blob into a scene created from the SAME
+ *     triangle soup and reflectances (checked by a 64-bit fingerprint of both
+ *     arrays stored in the blob) in place of helios_build_accel; the scene is
+ *     then built (results bitwise those of the exporting scene).  Replaces an
+ *     existing tree.  Synchronises the stream.
+ * Errors: INVALID_ARGUMENT (NULL scene / bytes, buffer too small, a blob that
+ * is not one -- bad magic, version, record sizes, lengths -- or was exported
+ * from other triangles), NOT_BUILT (export before a build), OUT_OF_MEMORY, CUDA. */
+helios_status helios_accel_export(helios_scene scene, void* buffer, uint64_t* bytes,
+                                  helios_stream stream);
+helios_status helios_accel_import(helios_scene scene, const void* buffer, uint64_t bytes,
+                                  helios_stream stream);
+
 /* Free everything the scene owns.  NULL is a no-op.  Must not race with a
  * helios_simulate on the same scene. */
 helios_status helios_scene_destroy(helios_scene scene);

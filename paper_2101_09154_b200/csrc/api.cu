@@ -450,6 +450,80 @@ cudaError_t copy_in(T** dst, const T* src, size_t count, cudaStream_t s) {
   return e;
 }
 
+// ---- serialised acceleration structure (helios_accel_export / _import)
+constexpr uint64_t kAccelMagic = 0x31304343414C5848ull;  // "HXLACC01" little-endian
+constexpr uint32_t kAccelVersion = 1;
+struct AccelHeader {
+  uint64_t magic;
+  uint32_t version, header_bytes;
+  uint32_t n_tris, n_nodes;
+  int32_t root;
+  uint32_t max_depth;
+  uint64_t scene_hash;    // fingerprint of the triangle soup + reflectances
+  uint64_t tri_bytes;     // each of the two triangle record arrays
+  uint64_t node_bytes;
+  uint32_t record_sizes;  // sizeof(TriRecord) | sizeof(Node) << 16
+  uint32_t leaf_max;
+  uint64_t reserved[8];
+};
+static_assert(sizeof(AccelHeader) % 16 == 0, "keeps the record arrays 16-B aligned");
+
+// order-sensitive 64-bit fingerprint: the sum mod 2^64 of a mixed hash of
+// (word index, word) over every word (deterministic in any summation order)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_fingerprint(const uint32_t* __restrict__ w, uint64_t n, uint64_t salt,
+                              unsigned long long* __restrict__ acc) {
+  uint64_t sum = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    sum += mix64((i + salt) * 0x9E3779B97F4A7C15ull ^ (uint64_t)w[i]);
+  for (int d = 16; d; d >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, d);
+  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(acc, (unsigned long long)sum);
+}
+
+cudaError_t scene_fingerprint(helios_scene sc, cudaStream_t s, uint64_t* out) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = helios::dev_alloc((void**)&d, sizeof(*d), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d, 0, sizeof(*d), s);
+  const uint64_t n9 = 9ull * sc->n_tris, n1 = sc->n_tris;
+  auto run = [&](const void* p, uint64_t n, uint64_t salt) {
+    if (e != cudaSuccess || !p || !n) return;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+    k_fingerprint<<<blocks, 256, 0, s>>>(static_cast<const uint32_t*>(p), n, salt, d);
+    e = cudaGetLastError();
+  };
+  run(sc->d_xyz, n9, 0x51ull);
+  run(sc->d_refl, n1, 0xA7ull << 40);
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(d, s);
+  *out = (uint64_t)h ^ ((uint64_t)sc->n_tris << 1);
+  return e;
+}
+
+cudaError_t accel_header(helios_scene sc, cudaStream_t s, AccelHeader* h, bool tree = true) {
+  *h = AccelHeader{};
+  h->magic = kAccelMagic;
+  h->version = kAccelVersion;
+  h->header_bytes = sizeof(AccelHeader);
+  h->n_tris = sc->n_tris;
+  h->record_sizes = (uint32_t)sizeof(TriRecord) | ((uint32_t)sizeof(Node) << 16);
+  h->leaf_max = kLeafMax;
+  if (tree) {
+    h->n_nodes = sc->bvh.n_nodes;
+    h->root = sc->bvh.root;
+    h->max_depth = sc->bvh.max_depth;
+    h->tri_bytes = (uint64_t)sc->n_tris * sizeof(TriRecord);
+    h->node_bytes = (uint64_t)sc->bvh.n_nodes * sizeof(Node);
+  }
+  return scene_fingerprint(sc, s, &h->scene_hash);
+}
+
 void free_scene(helios_scene sc, cudaStream_t s) {
   sc->free_slots();
   cudaFreeAsync(sc->d_xyz, s);
@@ -602,6 +676,104 @@ helios_status helios_build_accel(helios_scene sc, helios_stream stream) {
       return fail(HELIOS_ERR_OUT_OF_MEMORY, "helios_build_accel: %s", err);
     return fail(HELIOS_ERR_CUDA, "helios_build_accel: %s", err);
   }
+  sc->built = true;
+  return HELIOS_OK;
+}
+
+helios_status helios_accel_export(helios_scene sc, void* buffer, uint64_t* bytes,
+                                  helios_stream stream) {
+  helios::NvtxRange nvtx_("helios_accel_export");
+  g_err.clear();
+  if (!sc || !bytes) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene/bytes is NULL");
+  if (!sc->built) return fail(HELIOS_ERR_NOT_BUILT, "helios_accel_export: scene not built");
+  const cudaStream_t s = (cudaStream_t)stream;
+  AccelHeader h{};
+  cudaError_t e = accel_header(sc, s, &h);
+  if (e != cudaSuccess) return cuda_fail(e, "helios_accel_export");
+  const uint64_t total = h.header_bytes + 2 * h.tri_bytes + h.node_bytes;
+  if (!buffer) {
+    *bytes = total;
+    return HELIOS_OK;
+  }
+  if (*bytes < total)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "helios_accel_export: buffer of %llu bytes < %llu",
+                (unsigned long long)*bytes, (unsigned long long)total);
+  char* out = static_cast<char*>(buffer);
+  e = cudaMemcpyAsync(out, &h, sizeof(h), cudaMemcpyDefault, s);
+  uint64_t at = h.header_bytes;
+  if (e == cudaSuccess && h.tri_bytes)
+    e = cudaMemcpyAsync(out + at, sc->bvh.tris, h.tri_bytes, cudaMemcpyDefault, s);
+  at += h.tri_bytes;
+  if (e == cudaSuccess && h.tri_bytes)
+    e = cudaMemcpyAsync(out + at, sc->bvh.filt, h.tri_bytes, cudaMemcpyDefault, s);
+  at += h.tri_bytes;
+  if (e == cudaSuccess && h.node_bytes)
+    e = cudaMemcpyAsync(out + at, sc->bvh.nodes, h.node_bytes, cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "helios_accel_export");
+  *bytes = total;
+  return HELIOS_OK;
+}
+
+helios_status helios_accel_import(helios_scene sc, const void* buffer, uint64_t bytes,
+                                  helios_stream stream) {
+  helios::NvtxRange nvtx_("helios_accel_import");
+  g_err.clear();
+  if (!sc || !buffer) return fail(HELIOS_ERR_INVALID_ARGUMENT, "scene/buffer is NULL");
+  const cudaStream_t s = (cudaStream_t)stream;
+  AccelHeader h{};
+  if (bytes < sizeof(h)) return fail(HELIOS_ERR_INVALID_ARGUMENT, "helios_accel_import: not an accel blob");
+  cudaError_t e = cudaMemcpyAsync(&h, buffer, sizeof(h), cudaMemcpyDefault, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "helios_accel_import");
+  AccelHeader mine{};
+  e = accel_header(sc, s, &mine, /*tree=*/false);
+  if (e != cudaSuccess) return cuda_fail(e, "helios_accel_import");
+  const uint64_t n = h.n_tris;
+  if (h.magic != kAccelMagic || h.version != kAccelVersion || h.header_bytes != sizeof(h) ||
+      h.record_sizes != mine.record_sizes || h.leaf_max != mine.leaf_max ||
+      h.tri_bytes != n * sizeof(TriRecord) || h.node_bytes != (uint64_t)h.n_nodes * sizeof(Node) ||
+      bytes < h.header_bytes + 2 * h.tri_bytes + h.node_bytes)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT, "helios_accel_import: not a valid accel blob");
+  if (h.n_tris != sc->n_tris || h.scene_hash != mine.scene_hash)
+    return fail(HELIOS_ERR_INVALID_ARGUMENT,
+                "helios_accel_import: the blob was exported from other triangles");
+  helios::BuildResult r{};
+  r.n_nodes = h.n_nodes;
+  r.root = h.root;
+  r.max_depth = h.max_depth;
+  r.ms = 0.f;
+  const char* in = static_cast<const char*>(buffer);
+  if (n) {
+    e = helios::dev_alloc((void**)&r.tris, h.tri_bytes, s);
+    if (e == cudaSuccess) e = helios::dev_alloc((void**)&r.filt, h.tri_bytes, s);
+    if (e == cudaSuccess && h.n_nodes) e = helios::dev_alloc((void**)&r.nodes, h.node_bytes, s);
+    uint64_t at = h.header_bytes;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(r.tris, in + at, h.tri_bytes, cudaMemcpyDefault, s);
+    at += h.tri_bytes;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(r.filt, in + at, h.tri_bytes, cudaMemcpyDefault, s);
+    at += h.tri_bytes;
+    if (e == cudaSuccess && h.n_nodes)
+      e = cudaMemcpyAsync(r.nodes, in + at, h.node_bytes, cudaMemcpyDefault, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(r.tris, s);
+      cudaFreeAsync(r.filt, s);
+      cudaFreeAsync(r.nodes, s);
+      cudaStreamSynchronize(s);
+      cudaGetLastError();
+      return e == cudaErrorMemoryAllocation
+                 ? fail(HELIOS_ERR_OUT_OF_MEMORY, "helios_accel_import: out of device memory")
+                 : cuda_fail(e, "helios_accel_import");
+    }
+  }
+  // replace the previous tree (no call may be running on this scene)
+  sc->free_slots();
+  cudaFreeAsync(sc->bvh.tris, s);
+  cudaFreeAsync(sc->bvh.filt, s);
+  cudaFreeAsync(sc->bvh.nodes, s);
+  cudaStreamSynchronize(s);
+  sc->bvh = r;
   sc->built = true;
   return HELIOS_OK;
 }

@@ -31,6 +31,7 @@ _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "OUT_OF_MEMORY", 3: "CUDA", 4: "NO
 
 EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helios_build_accel",
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
+            "helios_accel_export", "helios_accel_import",
             "helios_pulse_taps", "helios_simulate", "helios_simulate_batches",
             "helios_simulate_batches_async", "helios_call_wait", "helios_simulate_survey", "helios_get_tuning", "helios_set_tuning",
             "helios_util_sort_pairs_u64", "helios_util_scan_u64",
@@ -138,6 +139,10 @@ def lib() -> ctypes.CDLL:
                                           ctypes.POINTER(_vp)]
         L.helios_build_accel.restype = ctypes.c_int
         L.helios_build_accel.argtypes = [_vp, _vp]
+        L.helios_accel_export.restype = ctypes.c_int
+        L.helios_accel_export.argtypes = [_vp, _vp, ctypes.POINTER(_u64), _vp]
+        L.helios_accel_import.restype = ctypes.c_int
+        L.helios_accel_import.argtypes = [_vp, _vp, _u64, _vp]
         L.helios_scene_destroy.restype = ctypes.c_int
         L.helios_scene_destroy.argtypes = [_vp]
         L.helios_scene_get_info.restype = ctypes.c_int
@@ -223,6 +228,19 @@ def helios_scene_create(desc: helios_scene_desc, stream=None) -> int:
 
 def helios_build_accel(scene: int, stream=None) -> None:
     _check(lib().helios_build_accel(scene, _stream(stream)))
+
+
+def helios_accel_export(scene: int, stream=None) -> bytes:
+    """The built tree and triangle records as one blob."""
+    n = _u64(0)
+    _check(lib().helios_accel_export(scene, None, ctypes.byref(n), _stream(stream)))
+    buf = ctypes.create_string_buffer(n.value)
+    _check(lib().helios_accel_export(scene, buf, ctypes.byref(n), _stream(stream)))
+    return buf.raw[:n.value]
+
+
+def helios_accel_import(scene: int, blob: bytes, stream=None) -> None:
+    _check(lib().helios_accel_import(scene, blob, len(blob), _stream(stream)))
 
 
 def helios_scene_destroy(scene: int) -> None:
@@ -415,6 +433,14 @@ class Scene:
 
     def info(self) -> helios_scene_info:
         return helios_scene_get_info(self.handle)
+
+    def export_accel(self, stream=None) -> bytes:
+        """helios_accel_export: the built tree (save it; skip the build later)."""
+        return helios_accel_export(self.handle, stream)
+
+    def import_accel(self, blob: bytes, stream=None) -> None:
+        """helios_accel_import: install a saved tree (scene created with build=False)."""
+        helios_accel_import(self.handle, blob, stream)
 
     def destroy(self):
         if getattr(self, "handle", None):

@@ -133,3 +133,15 @@ def test_async_call_argument_checks_without_gpu(libpath):
     assert handle.value is None  # cleared on failure
     assert "scene" in str(h.helios_last_error())
     assert L.helios_call_wait(None, None) == 1
+
+
+def test_accel_io_argument_checks_without_gpu(libpath):
+    """helios_accel_export / helios_accel_import reject NULL scenes, sizes and
+    buffers on the host."""
+    import paper_2101_09154_b200 as h
+    L = h.lib()
+    n = ctypes.c_uint64(0)
+    assert L.helios_accel_export(None, None, ctypes.byref(n), None) == 1
+    assert L.helios_accel_export(None, None, None, None) == 1
+    assert L.helios_accel_import(None, None, 0, None) == 1
+    assert L.helios_accel_import(None, b"x" * 16, 16, None) == 1
