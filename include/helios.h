@@ -369,7 +369,8 @@ helios_status helios_call_wait(helios_call call, helios_stats* stats);
  * outputs bitwise invariant to them).  Read by a call when it starts.  At the
  * first use they are seeded once from the environment (HELIOS_BEAM,
  * HELIOS_BUILDER=lbvh|ploc, HELIOS_LANE_ORDER, HELIOS_PAD_LANES,
- * HELIOS_SERIALIZE, HELIOS_TRACE_SPANS, HELIOS_CHUNK_PULSES).
+ * HELIOS_SERIALIZE, HELIOS_TRACE_SPANS, HELIOS_CHUNK_PULSES; the fault injection
+ * fault_alloc_bytes is never seeded).
  * ---------------------------------------------------------------------- */
 typedef struct {
   int32_t beam_prepass; /* K6a: -1 or 1 on wherever it applies (trees with internal nodes,
@@ -381,6 +382,8 @@ typedef struct {
                            per-kernel device times in helios_stats); 0 default             */
   int32_t trace_spans;  /* 1: print per-stream device spans of every call to stderr         */
   uint64_t chunk_pulses;/* 0 auto, else pulses per pipeline chunk (>= 1024)                 */
+  uint64_t fault_alloc_bytes; /* fault injection (SURVEY s.5): 0 off, else every library
+                                 device allocation larger than this fails as out of memory  */
 } helios_tuning;
 helios_status helios_get_tuning(helios_tuning* out);
 helios_status helios_set_tuning(const helios_tuning* tuning); /* INVALID_ARGUMENT if out of range */

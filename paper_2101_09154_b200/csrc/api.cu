@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -32,7 +33,13 @@ cudaMemPool_t g_pool[64] = {};
 }  // namespace
 
 namespace helios {
+std::atomic<uint64_t> g_fault_alloc{0};  // helios_tuning.fault_alloc_bytes (0 = off)
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t s) {
+  const uint64_t lim = g_fault_alloc.load(std::memory_order_relaxed);
+  if (lim && bytes > lim) {
+    *p = nullptr;
+    return cudaErrorMemoryAllocation;  // injected (tests of the out-of-memory paths)
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -73,6 +80,7 @@ helios_tuning tuning_defaults() {
   t.serialize = 0;
   t.trace_spans = 0;
   t.chunk_pulses = 0;
+  t.fault_alloc_bytes = 0;
   return t;
 }
 
@@ -1725,6 +1733,7 @@ helios_status helios_set_tuning(const helios_tuning* t) {
   tuning_snapshot();  // seed from the environment first, then override
   std::lock_guard<std::mutex> g(g_tune_mu);
   g_tune = *t;
+  helios::g_fault_alloc.store(t->fault_alloc_bytes, std::memory_order_relaxed);
   return HELIOS_OK;
 }
 

@@ -33,7 +33,8 @@ EXPORTED = ("helios_last_error", "helios_version", "helios_scene_create", "helio
             "helios_scene_destroy", "helios_scene_get_info", "helios_waveform_bins",
             "helios_accel_export", "helios_accel_import",
             "helios_pulse_taps", "helios_simulate", "helios_simulate_batches",
-            "helios_simulate_batches_async", "helios_call_wait", "helios_simulate_survey", "helios_get_tuning", "helios_set_tuning",
+            "helios_simulate_batches_async", "helios_call_wait", "helios_simulate_survey",
+            "helios_get_tuning", "helios_set_tuning",
             "helios_util_sort_pairs_u64", "helios_util_scan_u64",
             "helios_util_fp64_fma_tflops")
 
@@ -107,7 +108,7 @@ class helios_tuning(ctypes.Structure):
     _fields_ = [("beam_prepass", ctypes.c_int32), ("builder", ctypes.c_int32),
                 ("lane_order", ctypes.c_int32), ("pad_lanes", ctypes.c_int32),
                 ("serialize", ctypes.c_int32), ("trace_spans", ctypes.c_int32),
-                ("chunk_pulses", _u64)]
+                ("chunk_pulses", _u64), ("fault_alloc_bytes", _u64)]
 
 
 class helios_scene_info(ctypes.Structure):
