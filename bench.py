@@ -269,6 +269,33 @@ def run_ours(args):
         torch.cuda.synchronize()
         return max_over_ranks(e0.elapsed_time(e1), world, dev), r
 
+    # non-blocking calls (helios_simulate_batches_async): one batch per call,
+    # two calls in flight on two streams, each with its own output set, so a
+    # call's tail (its last K7) overlaps the next call's head (K6a, K6).  The
+    # streams wait for the timing event first; every call is waited for before
+    # the end event is recorded.
+    astreams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+
+    def run_steps_async(idx, st=False):
+        tot = {}
+        pending = []
+        for s_ in astreams:
+            s_.wait_stream(stream)
+        for j, i in enumerate(idx):
+            if len(pending) == 2:
+                r = pending.pop(0).wait()
+                if r is not None:
+                    for f, _ in r._fields_:
+                        tot[f] = tot.get(f, 0) + getattr(r, f)
+            pending.append(h.simulate_batches_async(scene, hp, [batches[i]], [outs[j % M]],
+                                                    stream=astreams[j % 2], stats=st))
+        for c in pending:
+            r = c.wait()
+            if r is not None:
+                for f, _ in r._fields_:
+                    tot[f] = tot.get(f, 0) + getattr(r, f)
+        return tot
+
     run_steps(range(args.warmup))
     torch.cuda.synchronize()
     timed_idx = range(args.warmup, steps_total)
@@ -278,7 +305,13 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    ms_max, st_main = timed(lambda: run_steps(timed_idx, st=True))
+    use_async = args.value_api == "async" and M >= 2
+    if use_async:
+        run_steps_async(range(args.warmup))  # warm the two streams' scratch
+        torch.cuda.synchronize()
+        ms_max, st_main = timed(lambda: run_steps_async(timed_idx, st=True))
+    else:
+        ms_max, st_main = timed(lambda: run_steps(timed_idx, st=True))
     clk = clocks.stop()
     launches = int(st_main.get("kernel_launches", 0))
     subrays = B * N * args.steps * world
@@ -482,8 +515,11 @@ def run_ours(args):
             "config": {"workload": args.config, "pulses_per_step_per_gpu": B,
                        "subrays_per_pulse": N, "n_tris": w.scene.n_tris,
                        "n_bins": n_bins, "l2": "inputs larger than L2 (scene + outputs)",
-                       "api": f"helios_simulate_batches, {M} batches (steps) per call, "
-                              "distinct batches and output sets",
+                       "api": ("helios_simulate_batches_async, one batch (step) per call, two "
+                               "calls in flight on two streams, distinct batches and output sets"
+                               if use_async else
+                               f"helios_simulate_batches, {M} batches (steps) per call, "
+                               "distinct batches and output sets"),
                        "bvh_nodes": info.n_nodes, "bvh_depth": info.max_depth,
                        "build_ms": round(info.build_ms, 2), "gen_s": round(t_gen, 1),
                        "fit_echo_width": int(args.fit_echo_width),
@@ -538,6 +574,10 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--waveform", default="dense", choices=["dense", "compact", "none"],
                     help="waveform output of the device-resident steps")
+    ap.add_argument("--value-api", default="batches", choices=["batches", "async"],
+                    help="timed steps through helios_simulate_batches (<= out-sets batches per "
+                         "call) or helios_simulate_batches_async (one batch per call, two in "
+                         "flight)")
     ap.add_argument("--out-sets", type=int, default=2,
                     help="device output sets the timed steps rotate through (batches per call)")
     ap.add_argument("--no-e2e", action="store_true")
