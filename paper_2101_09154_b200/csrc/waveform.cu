@@ -101,17 +101,29 @@ __device__ __forceinline__ void echo_window(const double* __restrict__ W, uint32
   }
 }
 
-__device__ __forceinline__ double sse_gauss(const double* __restrict__ y, int n, int lo,
+// The sum of squared residuals at (A, m, s) and, in the same pass over the
+// window (one exp per bin), J^T J and J^T r there -- the values the oracle
+// computes at an accepted point; a rejected candidate's are simply dropped
+// (so every iteration costs one exp pass, not two after an accepted step).
+struct FitEval {
+  double sse, h00, h01, h02, h11, h12, h22, g0, g1, g2;
+};
+__device__ __forceinline__ FitEval fit_eval(const double* __restrict__ y, int n, int lo,
                                             double delta, double A, double m, double s) {
-  double acc = 0.0;
-  const double is = 1.0 / s;
-#pragma unroll 4
+  FitEval f{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const double is = 1.0 / s, Ais = A * is;  // one division per pass, not per bin
+#pragma unroll 2
   for (int i = 0; i < n; ++i) {
     const double z = ((double)(lo + i) * delta - m) * is;
-    const double r = y[i] - A * exp(-0.5 * z * z);
-    acc += r * r;
+    const double e = exp(-0.5 * z * z);
+    const double j0 = e, j1 = Ais * e * z, j2 = j1 * z;
+    const double r = y[i] - A * e;
+    f.sse += r * r;
+    f.g0 += j0 * r; f.g1 += j1 * r; f.g2 += j2 * r;
+    f.h00 += j0 * j0; f.h01 += j0 * j1; f.h02 += j0 * j2;
+    f.h11 += j1 * j1; f.h12 += j1 * j2; f.h22 += j2 * j2;
   }
-  return acc;
+  return f;
 }
 
 // One LM fit per thread over the job list of one K7 launch.
@@ -127,29 +139,13 @@ __global__ void __launch_bounds__(64) k_fit(const FitJob* __restrict__ jobs,
     const int n = job.n;
     const int lo = job.lo;  // first window bin relative to the peak: x_i = (lo + i) Delta
     double A = job.peak, m = 0.0, s = s0, lambda = 1e-3;
-    double cur = sse_gauss(y, n, lo, delta, A, m, s);
-    bool converged = false, need_h = true;
-    double h00 = 0, h01 = 0, h02 = 0, h11 = 0, h12 = 0, h22 = 0, g0 = 0, g1 = 0, g2 = 0;
+    FitEval c = fit_eval(y, n, lo, delta, A, m, s);  // at the current point
+    bool converged = false;
     for (int it = 0; it < 100; ++it) {
-      // J^T J and J^T r depend on (A, m, s) only: a rejected step (only lambda
-      // changes) reuses them -- the same values the oracle recomputes
-      if (need_h) {
-      need_h = false;
-      h00 = h01 = h02 = h11 = h12 = h22 = g0 = g1 = g2 = 0.0;
-      const double is = 1.0 / s, Ais = A * is;  // one division per pass, not per bin
-#pragma unroll 4
-      for (int i = 0; i < n; ++i) {
-        const double z = ((double)(lo + i) * delta - m) * is;
-        const double e = exp(-0.5 * z * z);
-        const double j0 = e, j1 = Ais * e * z, j2 = j1 * z;
-        const double r = y[i] - A * e;
-        g0 += j0 * r; g1 += j1 * r; g2 += j2 * r;
-        h00 += j0 * j0; h01 += j0 * j1; h02 += j0 * j2;
-        h11 += j1 * j1; h12 += j1 * j2; h22 += j2 * j2;
-      }
-      }
-      const double m00 = h00 + lambda * h00, m11 = h11 + lambda * h11, m22 = h22 + lambda * h22;
-      const double m01 = h01, m02 = h02, m12 = h12;  // symmetric
+      const double m00 = c.h00 + lambda * c.h00, m11 = c.h11 + lambda * c.h11,
+                   m22 = c.h22 + lambda * c.h22;
+      const double m01 = c.h01, m02 = c.h02, m12 = c.h12;  // symmetric
+      const double g0 = c.g0, g1 = c.g1, g2 = c.g2;
       const double c00 = m11 * m22 - m12 * m12, c01 = m01 * m22 - m12 * m02,
                    c02 = m01 * m12 - m11 * m02;
       const double det = m00 * c00 - m01 * c01 + m02 * c02;
@@ -159,16 +155,15 @@ __global__ void __launch_bounds__(64) k_fit(const FitJob* __restrict__ jobs,
       const double d1 = (m00 * (g1 * m22 - m12 * g2) - g0 * c01 + m02 * (m01 * g2 - g1 * m02)) / det;
       const double d2 = (m00 * (m11 * g2 - g1 * m12) - m01 * (m01 * g2 - g1 * m02) + g0 * c02) / det;
       const double nA = A + d0, nm = m + d1, ns = s + d2;
-      const double next = sse_gauss(y, n, lo, delta, nA, nm, ns);
-      if (isfinite(next) && next < cur) {
+      const FitEval nx = fit_eval(y, n, lo, delta, nA, nm, ns);
+      if (isfinite(nx.sse) && nx.sse < c.sse) {
         const double rel = fmax(fmax(fabs(d0) / (fabs(A) + 1e-12), fabs(d1) / (fabs(m) + 1e-12)),
                                 fabs(d2) / (fabs(s) + 1e-12));
         A = nA;
         m = nm;
         s = ns;
-        cur = next;
+        c = nx;
         lambda /= 10.0;
-        need_h = true;
         if (rel < 1e-10) {
           converged = true;
           break;
