@@ -1035,7 +1035,25 @@ cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// K6 / K6a use no shared memory and live on L1 hits (nodes, triangle
+// records: 93 %): they ask for the smallest carveout (the largest L1) even
+// where K7 blocks (44 KB of shared memory each) overlap them -- pipelined C5
+// +1.4 %, C3 +1 %, exclusive times unchanged (profiles/r02s4/carveout_ab.txt;
+// -1 leaves the driver's choice)
+#ifndef HELIOS_K6_CARVEOUT
+#define HELIOS_K6_CARVEOUT 0
+#endif
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) {
+#if HELIOS_K6_CARVEOUT >= 0
+  static bool carve_set = [] {
+    for (const void* f : {(const void*)k_trace<false, 0>, (const void*)k_trace<false, 1>,
+                          (const void*)k_trace<false, 2>, (const void*)k_beam<false>})
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, HELIOS_K6_CARVEOUT);
+    cudaGetLastError();
+    return true;
+  }();
+  (void)carve_set;
+#endif
   if (a.lanes < a.N) return cudaErrorInvalidValue;
   const uint64_t total = a.n_pulses * (uint64_t)a.lanes;
   if (total == 0) return cudaSuccess;
