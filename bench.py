@@ -350,7 +350,7 @@ def run_ours(args):
     ach_k6 = b_k6 / (k6_ms / 1e3) / 1e9
     ach_k7 = b_k7 / (k7_ms / 1e3) / 1e9
     r1 = (b_ray + b_pulse) / (ms_max / 1e3) / 1e9 / peak
-    traffic, issue = None, None
+    traffic, issue, alu = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f).get(args.config)
@@ -370,6 +370,21 @@ def run_ours(args):
                      "k6_issue_slots_busy": kt.get("issue_slots_busy"),
                      "k7_issue_slots_busy": kw.get("issue_slots_busy"),
                      "source": tj["source"]}
+            if "fp64_pipe_busy" in kt:
+                # K6's fp64 pipe against the FMA rate measured live by the library's
+                # own microbenchmark (util_fp64_fma_tflops): the share of that peak
+                # K6 uses while it runs, from the ncu capture's pipe-active fraction.
+                # Every decision of the path is fp64, so this is the ALU
+                # bound that matters on C4, whose DDA is fp64 throughout.
+                alu = {"bound": "alu", "pipe": "fp64", "kernel": "k_trace (K6)",
+                       "peak": fp64_tflops, "unit": "TFLOP/s (fp64 FMA, measured)",
+                       "frac": kt["fp64_pipe_busy"],
+                       "achieved": kt["fp64_pipe_busy"] * fp64_tflops if fp64_tflops else None,
+                       "k6_pipe_busy": {"fp64": kt["fp64_pipe_busy"], "alu": kt.get("alu_pipe_busy"),
+                                        "fma": kt.get("fma_pipe_busy")},
+                       "k7_pipe_busy": {"fp64": kw.get("fp64_pipe_busy"), "alu": kw.get("alu_pipe_busy"),
+                                        "fma": kw.get("fma_pipe_busy")},
+                       "source": "sm__inst_executed_pipe_*.avg.pct_of_peak_sustained_active, " + tj["source"]}
     except Exception:
         pass
 
@@ -539,6 +554,7 @@ def run_ours(args):
                          "k_waveform": {"bound": "hbm", "achieved": ach_k7, "frac": ach_k7 / peak,
                                         "bytes_per_pulse": b_k7 / pul_rank},
                          "issue_roofline": issue,
+                         "alu_roofline": alu,
                          "fp64_fma_tflops_measured": fp64_tflops,
                          "nodes_per_ray": nodes / sub_rank,
                          "beam_nodes_per_pulse": beam_nodes / pul_rank,

@@ -651,7 +651,13 @@ __device__ __forceinline__ void store_event(const TraceArgs& a, uint64_t slot, d
 // GRID: 0 no voxel grid, 1 transmissive voxels, 2 opaque / scaled cubes --
 // the A4 march is compiled in only where needed, so each scene kind keeps
 // the traversal's register budget
-template <bool INSTR, int GRID>
+// ENT: the launch knows that K6a's entry lists exist (every triangle scene
+// unless the pre-pass is switched off), so the walk from the root -- a second
+// inlined copy of the traversal -- is compiled out: 2024 -> 1560 instructions,
+// spills 168 -> 108 B, K6 -0.6 % (C5) ... -1.1 % (C2, C6).  A further variant
+// for warps that hold one pulse only (C5's 96 lanes: no second-pulse state)
+// spilled less still but ran 3.5 % slower on C5 (profiles/r02s5_ent_ab.txt).
+template <bool INSTR, int GRID, bool ENT = false>
 __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 / HELIOS_TRACE_T) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // a pulse occupies a.lanes (>= N) consecutive threads: N, or N padded to
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
           const int lane = threadIdx.x & 31;
           unsigned rem = m, skip = 0;
           while (rem) {
-            if (a.entries == nullptr) {
+            if (!ENT && a.entries == nullptr) {
               traverse_packet<INSTR>(a, rem, a.root, O, D, O32, D32, dl1, ix, iy, iz, hs,
                                      c_nodes, c_tris, c_f64, wc);
               break;
@@ -1046,8 +1052,9 @@ cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) {
 #if HELIOS_K6_CARVEOUT >= 0
   static bool carve_set = [] {
-    for (const void* f : {(const void*)k_trace<false, 0>, (const void*)k_trace<false, 1>,
-                          (const void*)k_trace<false, 2>, (const void*)k_beam<false>})
+    for (const void* f : {(const void*)k_trace<false, 0>, (const void*)k_trace<false, 0, true>,
+                          (const void*)k_trace<false, 1>, (const void*)k_trace<false, 2>,
+                          (const void*)k_beam<false>})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, HELIOS_K6_CARVEOUT);
     cudaGetLastError();
     return true;
@@ -1062,13 +1069,16 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) 
   if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
   const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
+  const bool ent = grid == 0 && a.entries != nullptr;
   if (instrumented) {
     if (grid == 1) k_trace<true, 1><<<g, T, 0, s>>>(a);
     else if (grid == 2) k_trace<true, 2><<<g, T, 0, s>>>(a);
+    else if (ent) k_trace<true, 0, true><<<g, T, 0, s>>>(a);
     else k_trace<true, 0><<<g, T, 0, s>>>(a);
   } else {
     if (grid == 1) k_trace<false, 1><<<g, T, 0, s>>>(a);
     else if (grid == 2) k_trace<false, 2><<<g, T, 0, s>>>(a);
+    else if (ent) k_trace<false, 0, true><<<g, T, 0, s>>>(a);
     else k_trace<false, 0><<<g, T, 0, s>>>(a);
   }
   return cudaGetLastError();

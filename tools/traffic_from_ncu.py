@@ -22,7 +22,11 @@ N_OF = {"C1": 19, "C2": 19, "C3": 37, "C4": 19, "C5": 91, "C6": 37}
 COLS = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
-        "sm__warps_active.avg.pct_of_peak_sustained_active")
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active")
+PIPES = {"fp64_pipe_busy": COLS[8], "alu_pipe_busy": COLS[9], "fma_pipe_busy": COLS[10]}
 
 
 def scale(unit, v):
@@ -77,6 +81,7 @@ def main(rep, cfg, source, pulses=None):
             "k_beam_duration_us": b["gpu__time_duration.sum"],
             "k_beam_warp_inst": b["smsp__inst_executed.sum"],
             "k_beam_occupancy": b["sm__warps_active.avg.pct_of_peak_sustained_active"] / 100,
+            **{k: t[c] / 100 for k, c in PIPES.items()},
         },
         "k_waveform": {
             "dram_bytes": w["dram__bytes_read.sum"] + w["dram__bytes_write.sum"],
@@ -86,6 +91,7 @@ def main(rep, cfg, source, pulses=None):
             "duration_us": w["gpu__time_duration.sum"],
             "wide_pass_duration_us": ww["gpu__time_duration.sum"] if ww else 0.0,
             "wide_pass_warp_inst": ww["smsp__inst_executed.sum"] if ww else 0.0,
+            **{k: per["k_waveform"][c] / 100 for k, c in PIPES.items()},
         },
     }
     path = os.path.join(ROOT, "profiles", "traffic.json")
