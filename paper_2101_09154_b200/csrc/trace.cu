@@ -651,12 +651,13 @@ __device__ __forceinline__ void store_event(const TraceArgs& a, uint64_t slot, d
 // GRID: 0 no voxel grid, 1 transmissive voxels, 2 opaque / scaled cubes --
 // the A4 march is compiled in only where needed, so each scene kind keeps
 // the traversal's register budget
-// ENT: the launch knows that K6a's entry lists exist (every triangle scene
-// unless the pre-pass is switched off), so the walk from the root -- a second
-// inlined copy of the traversal -- is compiled out: 2024 -> 1560 instructions,
-// spills 168 -> 108 B, K6 -0.6 % (C5) ... -1.1 % (C2, C6).  A further variant
-// for warps that hold one pulse only (C5's 96 lanes: no second-pulse state)
-// spilled less still but ran 3.5 % slower on C5 (profiles/r02s5_ent_ab.txt).
+// ENT: the launch knows that K6a's entry lists and pulse frames exist (every
+// triangle scene unless the pre-pass is switched off), so the walk from the
+// root -- a second inlined copy of the traversal -- and the in-kernel pulse
+// frame are compiled out: 2024 -> 1376 instructions, spills 168 -> 100 B,
+// K6 -1.2 % (C5), -2.4 % (C2, C3), -2.9 % (C6).  A further variant for warps
+// that hold one pulse only (C5's 96 lanes: no second-pulse state) spilled
+// less still but ran 3.5 % slower on C5 (profiles/r02s5_ent_ab.txt).
 template <bool INSTR, int GRID, bool ENT = false>
 __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 / HELIOS_TRACE_T) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
               oz = __ldg(a.origin + 3 * p + 2);
   D3 Dp, U, V;
   bool valid = in_range;
-  if (a.frames != nullptr) {  // the pulse frame K6a computed (bitwise the same values)
+  if (ENT || a.frames != nullptr) {  // the pulse frame K6a computed (bitwise the same values)
     const double2* f = reinterpret_cast<const double2*>(a.frames) + p * 5;
     const double2 f0 = __ldg(f), f1 = __ldg(f + 1), f2 = __ldg(f + 2), f3 = __ldg(f + 3),
                   f4 = __ldg(f + 4);
@@ -1069,7 +1070,7 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) 
   if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
   const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
-  const bool ent = grid == 0 && a.entries != nullptr;
+  const bool ent = grid == 0 && a.entries != nullptr && a.frames != nullptr;
   if (instrumented) {
     if (grid == 1) k_trace<true, 1><<<g, T, 0, s>>>(a);
     else if (grid == 2) k_trace<true, 2><<<g, T, 0, s>>>(a);
