@@ -23,6 +23,7 @@
 //     (no accumulated increments), chord lengths, exp(-sigma L), -ln(u)/sigma
 //     in fp64 (R17-R20);
 //   * range, Eq. 1/2 intensity and Eq. 7 amplitude in fp64 (R5, R14, R16).
+#include <type_traits>
 #include <math.h>
 
 #include "internal.cuh"
@@ -658,7 +659,7 @@ __device__ __forceinline__ void store_event(const TraceArgs& a, uint64_t slot, d
 // K6 -1.2 % (C5), -2.4 % (C2, C3), -2.9 % (C6).  A further variant for warps
 // that hold one pulse only (C5's 96 lanes: no second-pulse state) spilled
 // less still but ran 3.5 % slower on C5 (profiles/r02s5_ent_ab.txt).
-template <bool INSTR, int GRID, bool ENT = false>
+template <bool INSTR, int GRID, bool ENT>
 __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 / HELIOS_TRACE_T) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // a pulse occupies a.lanes (>= N) consecutive threads: N, or N padded to
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
               oz = __ldg(a.origin + 3 * p + 2);
   D3 Dp, U, V;
   bool valid = in_range;
-  if (ENT || a.frames != nullptr) {  // the pulse frame K6a computed (bitwise the same values)
+  if (ENT) {  // the pulse frame K6a computed (bitwise the same values)
     const double2* f = reinterpret_cast<const double2*>(a.frames) + p * 5;
     const double2 f0 = __ldg(f), f1 = __ldg(f + 1), f2 = __ldg(f + 2), f3 = __ldg(f + 3),
                   f4 = __ldg(f + 4);
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 
           const int lane = threadIdx.x & 31;
           unsigned rem = m, skip = 0;
           while (rem) {
-            if (!ENT && a.entries == nullptr) {
+            if (!ENT) {
               traverse_packet<INSTR>(a, rem, a.root, O, D, O32, D32, dl1, ix, iy, iz, hs,
                                      c_nodes, c_tris, c_f64, wc);
               break;
@@ -1053,8 +1054,9 @@ cudaError_t launch_beam(const TraceArgs& a, bool instrumented, cudaStream_t s) {
 cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) {
 #if HELIOS_K6_CARVEOUT >= 0
   static bool carve_set = [] {
-    for (const void* f : {(const void*)k_trace<false, 0>, (const void*)k_trace<false, 0, true>,
-                          (const void*)k_trace<false, 1>, (const void*)k_trace<false, 2>,
+    for (const void* f : {(const void*)k_trace<false, 0, false>, (const void*)k_trace<false, 0, true>,
+                          (const void*)k_trace<false, 1, false>, (const void*)k_trace<false, 1, true>,
+                          (const void*)k_trace<false, 2, false>, (const void*)k_trace<false, 2, true>,
                           (const void*)k_beam<false>})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, HELIOS_K6_CARVEOUT);
     cudaGetLastError();
@@ -1070,18 +1072,18 @@ cudaError_t launch_trace(const TraceArgs& a, bool instrumented, cudaStream_t s) 
   if (blocks > 0x7FFFFFFFull || total >= (1ull << 32)) return cudaErrorInvalidValue;
   const unsigned g = (unsigned)blocks;
   const int grid = a.pad == nullptr ? 0 : (a.voxel_mode == HELIOS_VOXEL_TRANSMISSIVE ? 1 : 2);
-  const bool ent = grid == 0 && a.entries != nullptr && a.frames != nullptr;
-  if (instrumented) {
-    if (grid == 1) k_trace<true, 1><<<g, T, 0, s>>>(a);
-    else if (grid == 2) k_trace<true, 2><<<g, T, 0, s>>>(a);
-    else if (ent) k_trace<true, 0, true><<<g, T, 0, s>>>(a);
-    else k_trace<true, 0><<<g, T, 0, s>>>(a);
-  } else {
-    if (grid == 1) k_trace<false, 1><<<g, T, 0, s>>>(a);
-    else if (grid == 2) k_trace<false, 2><<<g, T, 0, s>>>(a);
-    else if (ent) k_trace<false, 0, true><<<g, T, 0, s>>>(a);
-    else k_trace<false, 0><<<g, T, 0, s>>>(a);
-  }
+  const bool ent = a.entries != nullptr && a.frames != nullptr;
+  auto go = [&](auto instr, auto gr) {
+    if (ent) k_trace<decltype(instr)::value, decltype(gr)::value, true><<<g, T, 0, s>>>(a);
+    else k_trace<decltype(instr)::value, decltype(gr)::value, false><<<g, T, 0, s>>>(a);
+  };
+  auto by_grid = [&](auto instr) {
+    if (grid == 1) go(instr, std::integral_constant<int, 1>{});
+    else if (grid == 2) go(instr, std::integral_constant<int, 2>{});
+    else go(instr, std::integral_constant<int, 0>{});
+  };
+  if (instrumented) by_grid(std::true_type{});
+  else by_grid(std::false_type{});
   return cudaGetLastError();
 }
 
