@@ -652,13 +652,16 @@ __device__ __forceinline__ void store_event(const TraceArgs& a, uint64_t slot, d
 // GRID: 0 no voxel grid, 1 transmissive voxels, 2 opaque / scaled cubes --
 // the A4 march is compiled in only where needed, so each scene kind keeps
 // the traversal's register budget
-// ENT: the launch knows that K6a's entry lists and pulse frames exist (every
-// triangle scene unless the pre-pass is switched off), so the walk from the
-// root -- a second inlined copy of the traversal -- and the in-kernel pulse
-// frame are compiled out: 2024 -> 1376 instructions, spills 168 -> 100 B,
-// K6 -1.2 % (C5), -2.4 % (C2, C3), -2.9 % (C6).  A further variant for warps
-// that hold one pulse only (C5's 96 lanes: no second-pulse state) spilled
-// less still but ran 3.5 % slower on C5 (profiles/r02s5_ent_ab.txt).
+// ENT: whether K6a's entry lists and pulse frames exist (every scene with
+// an inner tree node unless the pre-pass is switched off) is known when the
+// kernel is launched, so each kernel holds one copy of the inlined traversal:
+// ENT walks the lists with the stored frames, !ENT walks from the root with
+// the frame computed here.  Triangle scenes: 2024 -> 1376 instructions,
+// spills 168 -> 100 B, K6 -1.2 % (C5), -2.4 % (C2, C3), -2.9 % (C6); the
+// voxel kernel without lists (C4): spills 264 -> 188 B, K6 -1.2 %.  A further
+// variant for warps that hold one pulse only (C5's 96 lanes: no second-pulse
+// state) spilled less still but ran 3.5 % slower on C5
+// (profiles/r02s5_ent_ab.txt).
 template <bool INSTR, int GRID, bool ENT>
 __global__ void __launch_bounds__(HELIOS_TRACE_T, HELIOS_TRACE_MIN_BLOCKS * 128 / HELIOS_TRACE_T) k_trace(const TraceArgs a) {
   const uint64_t gid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
